@@ -1,0 +1,137 @@
+/*
+ * exitlab_b200.h -- C ABI of the B200-native batched early-exit decode engine.
+ *
+ * Drop-in boundary for the reference's engine and exit-criterion API
+ * (/root/reference/proj, "exitlab"). Plain pointers and sizes only; every
+ * function returns an EL_* status code (mapped 1:1 onto the reference's
+ * exception classes) and leaves a message in
+ * el_last_error().  Host buffers are always caller-owned.
+ *
+ * Reference interface each entry point replaces (paths under proj/):
+ *   el_engine_create        Engine::Engine(EngineConfig[, ModelWeights])   include/exitlab/engine.hpp:135-136
+ *                           (+ ModelWeights::seeded, model.hpp:46; EngineConfig::validate engine.cpp:31-45)
+ *   el_engine_destroy       Engine::~Engine
+ *   el_engine_run           Transcript Engine::run(const Workload&) const  include/exitlab/engine.hpp:141
+ *   el_transcript_*         Transcript / IterationRecord / SequenceRecord  include/exitlab/engine.hpp:67-123
+ *   el_session_begin        admission of a fixed batch (engine.cpp:183-206) with a seeded KV prefix in place of
+ *                           prefill (engine.cpp:166-181)
+ *   el_decode_iteration     the decode_iteration body (engine.cpp:208-310): layer_forward (model.hpp:64-66),
+ *                           decide + *_confidence + threshold_at (exit_policy.hpp:46-70),
+ *                           ExitStatusVector::observe_layer (engine.hpp:53), fill_skipped (kv_cache.hpp:112-115),
+ *                           KvStore::commit (kv_cache.hpp:62), lm_head_logits + greedy_token (model.hpp:73-76)
+ *   el_decode_run           the same, n iterations back to back on the device (no host round trip)
+ *   el_set_fixed_confidences  test harness: ExitEvidence replaced by injected confidences (decide's "> lambda")
+ *   el_session_kv           KvStore::view(seq, layer, upto).key/value (kv_cache.hpp:56, 24-36)
+ *   el_session_block_table  KvStore block_table (kv_cache.hpp:83), read back from the device
+ *   el_kv_block_trace       KvStore::allocate / release LIFO order (kv_cache.cpp:53-55, 78-106, 182-194)
+ *   el_model_tensor         ModelWeights tensors (model.hpp:38-55), bf16 on the device
+ */
+#ifndef EXITLAB_B200_H
+#define EXITLAB_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes: reference exception class in brackets */
+#define EL_OK 0
+#define EL_INVALID_ARGUMENT 1 /* std::invalid_argument */
+#define EL_RUNTIME_ERROR 2    /* std::runtime_error (invariant violations) */
+#define EL_KV_OUT_OF_MEMORY 3 /* exitlab::KvOutOfMemory */
+#define EL_LOGIC_ERROR 4      /* std::logic_error (empty batch) */
+#define EL_CUDA_ERROR 6       /* device / driver failure (no reference counterpart) */
+
+/* ExitTechnique kinds (exit_policy.hpp:14-31) + the injected-confidence harness */
+#define EL_TECH_SOFTMAX 0
+#define EL_TECH_STATE 1
+#define EL_TECH_CLASSIFIER 2
+#define EL_TECH_NEVER 3
+#define EL_TECH_ALWAYS_AT 4
+#define EL_TECH_FIXED 5
+
+/* EngineConfig (engine.hpp:30-42) + ModelConfig (model.hpp:18-25) +
+ * ThresholdSchedule (exit_policy.hpp:36-42) + CostModel (engine.hpp:18-28). */
+typedef struct {
+    int n_layers, d_model, vocab_size;
+    uint64_t model_seed;
+    int technique, exit_layer;
+    double lambda0, gamma, lambda_min;
+    double c_layer_fixed, c_layer_per_seq, c_fill_per_seq_layer;
+    double c_check_softmax, c_check_classifier, c_check_state;
+    int max_batch, pool_blocks, block_capacity, eos_token;
+    int capture_kv;
+    int round_bf16;            /* weights are always bf16 on the device; kept for layout parity */
+    int64_t synthetic_kv_seed; /* <0: real prefill; >=0: prompts' KV prefix is seeded (bench workload) */
+} el_engine_config;
+
+typedef struct el_engine el_engine;
+typedef struct el_transcript el_transcript;
+
+const char* el_last_error(void);
+int el_version(void);
+
+int el_engine_create(const el_engine_config* cfg, el_engine** out);
+int el_engine_destroy(el_engine* e);
+/* options: "graph" (1: CUDA graph with a device-side WHILE over layers, 0: eager),
+ *          "rec_cap" (iterations kept in the device record ring) */
+int el_engine_set_option(el_engine* e, const char* key, int64_t value);
+
+/* Engine::run: requests as flat arrays (arrival[n], prompt_off[n+1], prompt[], max_new[n]) */
+int el_engine_run(el_engine* e, int n, const double* arrival, const int32_t* prompt_off,
+                  const int32_t* prompt, const int32_t* max_new, el_transcript** out);
+
+/* flat transcript fields (same names as the oracle / reference wrappers):
+ * i32: pf_seq pf_positions it_output_layer it_batch_off ps_seq ps_accept ps_token sq_id
+ *      sq_max_new sq_prompt_off sq_prompt sq_tok_off sq_tokens sq_exit_layers sq_iter_out
+ * f64: pf_clock pf_charge it_clock it_charge sq_arrival sq_first sq_finish meta it_conf */
+int64_t el_transcript_len(const el_transcript* t, const char* field);
+int el_transcript_get_i32(const el_transcript* t, const char* field, int32_t* out);
+int el_transcript_get_f64(const el_transcript* t, const char* field, double* out);
+int el_transcript_kv(const el_transcript* t, int seq_id, int layer, double* k, double* v, int64_t cap);
+int el_transcript_exit_states(const el_transcript* t, int seq_id, double* out, int64_t cap);
+void el_transcript_free(el_transcript* t);
+
+/* fixed batch of B sequences (ids seq_ids[b]) whose KV holds prefix_len seeded
+ * positions at every layer; first decode inputs first_tokens[b]; capacity in tokens */
+int el_session_begin(el_engine* e, int batch, const int32_t* first_tokens, int prefix_len, int capacity,
+                     uint64_t kv_seed, const int32_t* seq_ids);
+int el_session_end(el_engine* e);
+/* one iteration with host buffers (tokens_in may be NULL: keep the device-side
+ * next inputs); outputs tokens[B], accept[B], conf[L][B] (NULL to skip), output layer */
+int el_decode_iteration(el_engine* e, const int32_t* tokens_in, int32_t* tokens_out, int32_t* accept_out,
+                        float* conf_out, int32_t* output_layer);
+int el_decode_run(el_engine* e, int n_iters);
+/* records of iterations [first, first+n) of this session (ring of rec_cap) */
+int el_decode_records(el_engine* e, int first, int n, int32_t* tokens, int32_t* accept, int32_t* out_layer,
+                      float* conf);
+int el_decode_iterations_done(el_engine* e);
+int el_set_fixed_confidences(el_engine* e, const float* conf /* [L][B] */);
+int el_session_kv(el_engine* e, int row, int layer, int pos, float* k, float* v);
+int el_session_hidden(el_engine* e, int parity, float* out /* [B][d] */);
+int el_session_block_table(el_engine* e, int row, int32_t* out /* [L][bpl] */, int bpl_cap);
+
+/* timing on the engine's stream with CUDA events (synchronised on both sides) */
+int el_time_decode(el_engine* e, int n_iters, float* ms);
+/* standalone kernel timing on the current session state: kind 0 attention,
+ * 1 qkv gemm, 2 wo, 3 up, 4 down, 5 lm head; layer fixed; reps launches */
+int el_time_kernel(el_engine* e, int kind, int layer, int reps, float* ms);
+int el_sync(el_engine* e);
+/* kernels launched per iteration with the given output layer (for gpu_launches) */
+int el_launches_per_iteration(el_engine* e, int output_layer);
+/* plan details: attention chunking, GEMM splits (for DESIGN / bench reporting) */
+int el_plan_info(el_engine* e, int64_t* out, int cap);
+
+/* LIFO allocator on the host mirror (same arithmetic the device kernels run) */
+int el_kv_block_trace(int n_layers, int pool_blocks, int block_capacity, int n_ops, const int32_t* ops,
+                      const int32_t* caps, int n_ids, int bpl_max, int32_t* tables);
+/* model tensors as stored on the device (bf16 bits, unpadded):
+ * which 0 embedding, 1 lm_head, 2 probe_w (fp32 bits of bf16 values), 3 probe_b,
+ * 4..9 layer q,k,v,o,up,down */
+int el_model_tensor(el_engine* e, int which, int layer, uint16_t* out, int64_t cap);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

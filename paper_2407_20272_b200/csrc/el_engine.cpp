@@ -1,0 +1,1289 @@
+// el_engine.cpp -- host side of the B200 early-exit decode engine and the C ABI
+// declared in include/exitlab_b200.h.
+//
+// The host mirrors the reference engine's control plane exactly (Engine::run,
+// engine.cpp:110-330: FIFO admission with head-of-line deferral, eviction at
+// the start of the next pass, simulated-clock charges, transcript records),
+// while every per-token computation runs in the sm_100a kernels of
+// el_kernels.cu.  The KV block tables live on the device; the host keeps only
+// the free-block count and per-sequence bookkeeping needed for the reference's
+// invariant checks (write-once/contiguity/commit completeness).
+#include <cudaTypedefs.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/exitlab_b200.h"
+#include "el_common.cuh"
+#include "el_kernels.h"
+
+namespace {
+
+thread_local std::string g_err;
+
+struct ElError {
+    int code;
+    std::string msg;
+};
+[[noreturn]] void fail(int code, const char* fmt, ...) {
+    char buf[1024];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    throw ElError{code, buf};
+}
+#define CK(x)                                                                                        \
+    do {                                                                                             \
+        cudaError_t e_ = (x);                                                                        \
+        if (e_ != cudaSuccess) fail(EL_CUDA_ERROR, "%s failed: %s (%s:%d)", #x, cudaGetErrorString(e_), \
+                                    __FILE__, __LINE__);                                             \
+    } while (0)
+
+template <class T>
+struct DevBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    ~DevBuf() { release(); }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    void alloc(size_t count, bool zero = true) {
+        release();
+        if (count == 0) count = 1;
+        CK(cudaMalloc(&p, count * sizeof(T)));
+        n = count;
+        if (zero) CK(cudaMemset(p, 0, count * sizeof(T)));
+    }
+    void ensure(size_t count) {
+        if (count > n) alloc(count);
+    }
+};
+
+int round_up(int x, int m) { return (x + m - 1) / m * m; }
+int ceil_div(int a, int b) { return (a + b - 1) / b; }
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+        if (!p || q != cudaDriverEntryPointSuccess) fail(EL_CUDA_ERROR, "cuTensorMapEncodeTiled unavailable");
+        fn = (PFN_cuTensorMapEncodeTiled_v12000)p;
+    }
+    return fn;
+}
+
+// bf16 [rows][k] row-major, box [box_rows][64], 128-byte swizzle
+CUtensorMap make_map(const void* base, int rows, int k, int box_rows) {
+    CUtensorMap m;
+    cuuint64_t dims[2] = {(cuuint64_t)k, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)k * 2};
+    cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
+    cuuint32_t es[2] = {1, 1};
+    CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box,
+                             es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) fail(EL_CUDA_ERROR, "cuTensorMapEncodeTiled failed (%d) rows=%d k=%d box=%d", (int)r, rows, k, box_rows);
+    return m;
+}
+
+double threshold_at(double l0, double g, double lmin, int layer) {  // exit_policy.cpp:50-55
+    return std::max(lmin, l0 * std::pow(g, layer - 1));
+}
+
+// ----- flat transcript (same layout as the oracle / reference wrappers) -----
+struct Capture {
+    int committed = 0;
+    std::vector<double> k, v;  // [L][committed][d]
+    std::vector<double> exit_states;
+    bool have_kv = false;
+};
+}  // namespace
+
+struct el_transcript {
+    std::vector<int32_t> pf_seq, pf_positions, it_output_layer, it_batch_off, ps_seq, ps_accept, ps_token, sq_id,
+        sq_max_new, sq_prompt_off, sq_prompt, sq_tok_off, sq_tokens, sq_exit_layers, sq_iter_out;
+    std::vector<double> pf_clock, pf_charge, it_clock, it_charge, sq_arrival, sq_first, sq_finish, meta, it_conf;
+    std::map<int, Capture> caps;
+    int d = 0, L = 0;
+    std::vector<int32_t>* i32(const char* f) {
+#define F(n) if (!std::strcmp(f, #n)) return &n;
+        F(pf_seq) F(pf_positions) F(it_output_layer) F(it_batch_off) F(ps_seq) F(ps_accept) F(ps_token) F(sq_id)
+        F(sq_max_new) F(sq_prompt_off) F(sq_prompt) F(sq_tok_off) F(sq_tokens) F(sq_exit_layers) F(sq_iter_out)
+#undef F
+        return nullptr;
+    }
+    std::vector<double>* f64(const char* f) {
+#define F(n) if (!std::strcmp(f, #n)) return &n;
+        F(pf_clock) F(pf_charge) F(it_clock) F(it_charge) F(sq_arrival) F(sq_first) F(sq_finish) F(meta) F(it_conf)
+#undef F
+        return nullptr;
+    }
+};
+
+struct el_engine {
+    el_engine_config cfg{};
+    el::Dims dm{};
+    cudaStream_t stream = nullptr;
+    int device = 0;
+    bool use_graph = true;
+    int rec_cap = 4096;
+
+    // weights
+    DevBuf<uint16_t> wqkv, wo, wup, wdown, emb, lm;
+    DevBuf<float> probe_w;
+    float probe_b = 0.f;
+    // kv pool + device allocator
+    DevBuf<uint16_t> kpool, vpool;
+    DevBuf<int> stack, tables;
+    int top = 0;  // free blocks (device stack height)
+    int peak = 0;
+    // rows
+    DevBuf<int> row_slot, row_pos, row_tok, pf_slot, pf_pos, pf_tok, seq_ids_dev;
+    // activations / workspaces
+    DevBuf<float> h32, q32, mid32, attn_o, attn_ml, gemm_ws, conf, rec_conf;
+    DevBuf<uint16_t> hb, att_b, mid_b, up_b;
+    DevBuf<int> attn_cnt, gemm_cnt, layer, out_layer, status, first_accept, accept, exit_cnt, iter_counter,
+        cur_iter, rec_tok, rec_acc, rec_out;
+    DevBuf<float4> lm_part;
+    DevBuf<double> lambdas;
+    DevBuf<float> fixed_conf;
+    int* cont_host = nullptr;
+    int* cont_dev = nullptr;
+
+    // plans
+    CUtensorMap mapA_qkv{}, mapA_wo{}, mapA_up{}, mapA_down{}, mapA_lm{};
+    struct Plans {
+        el::GemmPlan qkv, wo, up, down, lm, fill;
+        int n_pad = 0;
+    };
+    std::map<int, Plans> plans;  // by n_pad
+    int attn_cb = 1, attn_stages = 2, attn_max_chunks = 1;
+
+    // graphs by batch size
+    struct Graph {
+        cudaGraph_t g = nullptr;
+        cudaGraphExec_t x = nullptr;
+    };
+    std::map<int, Graph> graphs;
+
+    // session state
+    bool in_session = false;
+    int sess_B = 0;
+    int sess_iters = 0;
+    std::vector<int> sess_ids;
+    std::vector<int> slot_bpl;  // per slot blocks per layer (0 = free)
+
+    ~el_engine() {
+        for (auto& kv : graphs) {
+            if (kv.second.x) cudaGraphExecDestroy(kv.second.x);
+            if (kv.second.g) cudaGraphDestroy(kv.second.g);
+        }
+        if (cont_host) cudaFreeHost(cont_host);
+        if (stream) cudaStreamDestroy(stream);
+    }
+
+    // ------------------------------------------------------------------
+    void validate() const {  // EngineConfig::validate (engine.cpp:31-45)
+        const el_engine_config& c = cfg;
+        if (c.n_layers < 2) fail(EL_INVALID_ARGUMENT, "ModelConfig: n_layers must be >= 2");
+        if (c.d_model < 2) fail(EL_INVALID_ARGUMENT, "ModelConfig: d_model must be >= 2");
+        if (c.vocab_size < 2) fail(EL_INVALID_ARGUMENT, "ModelConfig: vocab_size must be >= 2");
+        if (!(c.gamma > 0.0 && c.gamma <= 1.0)) fail(EL_INVALID_ARGUMENT, "ThresholdSchedule: gamma must be in (0, 1]");
+        if (c.lambda_min < 0.0) fail(EL_INVALID_ARGUMENT, "ThresholdSchedule: lambda_min must be >= 0");
+        if (c.lambda_min > c.lambda0) fail(EL_INVALID_ARGUMENT, "ThresholdSchedule: lambda_min must be <= lambda0");
+        for (double x : {c.c_layer_fixed, c.c_layer_per_seq, c.c_fill_per_seq_layer, c.c_check_softmax,
+                         c.c_check_classifier, c.c_check_state})
+            if (x < 0.0) fail(EL_INVALID_ARGUMENT, "CostModel: charges must be nonnegative");
+        if (c.max_batch < 1) fail(EL_INVALID_ARGUMENT, "EngineConfig: max_batch must be >= 1");
+        if (c.max_batch > 256) fail(EL_INVALID_ARGUMENT, "EngineConfig: max_batch > 256 unsupported on this engine");
+        if (c.pool_blocks < 1) fail(EL_INVALID_ARGUMENT, "EngineConfig: pool_blocks must be >= 1");
+        if (c.block_capacity < 1) fail(EL_INVALID_ARGUMENT, "EngineConfig: block_capacity must be >= 1");
+        if (c.block_capacity > 64) fail(EL_INVALID_ARGUMENT, "EngineConfig: block_capacity > 64 unsupported");
+        if (c.eos_token >= c.vocab_size) fail(EL_INVALID_ARGUMENT, "EngineConfig: eos_token outside vocab");
+        if (c.technique < 0 || c.technique > EL_TECH_FIXED) fail(EL_INVALID_ARGUMENT, "EngineConfig: unknown technique");
+        if (c.technique == EL_TECH_ALWAYS_AT && (c.exit_layer < 1 || c.exit_layer > c.n_layers))
+            fail(EL_INVALID_ARGUMENT, "EngineConfig: always_at layer outside [1, n_layers]");
+        if (c.d_model > 1024) fail(EL_INVALID_ARGUMENT, "d_model > 1024 unsupported on this engine");
+    }
+
+    double check_cost() const {
+        switch (cfg.technique) {
+            case EL_TECH_SOFTMAX: return cfg.c_check_softmax;
+            case EL_TECH_STATE: return cfg.c_check_state;
+            case EL_TECH_CLASSIFIER: return cfg.c_check_classifier;
+            default: return 0.0;
+        }
+    }
+
+    void create() {
+        validate();
+        CK(cudaGetDevice(&device));
+        CK(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+        const int L = cfg.n_layers, d = cfg.d_model, V = cfg.vocab_size;
+        dm.L = L;
+        dm.d = d;
+        dm.dp = round_up(d, 128);
+        dm.fp = round_up(4 * d, 128);
+        dm.V = V;
+        dm.Vp = round_up(V, 128);
+        dm.bc = cfg.block_capacity;
+        dm.Bmax = cfg.max_batch;
+        dm.slots = cfg.max_batch;
+        dm.bpl_max = 0;
+        const int dp = dm.dp, fp = dm.fp;
+
+        // ---- seeded weights (model.cpp:37-59), generated on the device, bf16 RNE ----
+        auto tseed = [&](uint64_t tag) { return el::splitmix64_at(cfg.model_seed, tag); };
+        wqkv.alloc((size_t)L * 3 * dp * dp, false);
+        wo.alloc((size_t)L * dp * dp, false);
+        wup.alloc((size_t)L * fp * dp, false);
+        wdown.alloc((size_t)L * dp * fp, false);
+        emb.alloc((size_t)dm.Vp * dp, false);
+        lm.alloc((size_t)dm.Vp * dp, false);
+        const double sd = 1.0 / std::sqrt((double)d), s4d = 1.0 / std::sqrt((double)(4 * d));
+        el::launch_weightgen(emb.p, V, d, dm.Vp, dp, tseed(0), sd, stream);
+        el::launch_weightgen(lm.p, V, d, dm.Vp, dp, tseed(1), sd, stream);
+        for (int i = 0; i < L; ++i) {
+            const uint64_t base = 4 + (uint64_t)i * 6;
+            uint16_t* q = wqkv.p + (size_t)i * 3 * dp * dp;
+            el::launch_weightgen(q, d, d, dp, dp, tseed(base + 0), sd, stream);
+            el::launch_weightgen(q + (size_t)dp * dp, d, d, dp, dp, tseed(base + 1), sd, stream);
+            el::launch_weightgen(q + (size_t)2 * dp * dp, d, d, dp, dp, tseed(base + 2), sd, stream);
+            el::launch_weightgen(wo.p + (size_t)i * dp * dp, d, d, dp, dp, tseed(base + 3), sd, stream);
+            el::launch_weightgen(wup.p + (size_t)i * fp * dp, 4 * d, d, fp, dp, tseed(base + 4), sd, stream);
+            el::launch_weightgen(wdown.p + (size_t)i * dp * fp, d, 4 * d, dp, fp, tseed(base + 5), s4d, stream);
+        }
+        // probe (tiny: host) -- seeded_vector(d) and b = 2u - 1, both bf16-rounded
+        {
+            std::vector<float> pw((size_t)dp, 0.f);
+            const uint64_t sw = tseed(2);
+            for (int i = 0; i < d; ++i) {
+                const double u = (double)(el::splitmix64_at(sw, (uint64_t)i) >> 11) * 0x1.0p-53;
+                const uint16_t bits = el::bf16_bits_rne((2.0 * u - 1.0) * sd);
+                uint32_t f = (uint32_t)bits << 16;
+                std::memcpy(&pw[(size_t)i], &f, 4);
+            }
+            probe_w.alloc((size_t)dp);
+            CK(cudaMemcpy(probe_w.p, pw.data(), sizeof(float) * dp, cudaMemcpyHostToDevice));
+            const double u = (double)(el::splitmix64_at(tseed(3), 0) >> 11) * 0x1.0p-53;
+            const uint16_t bits = el::bf16_bits_rne(2.0 * u - 1.0);
+            uint32_t f = (uint32_t)bits << 16;
+            std::memcpy(&probe_b, &f, 4);
+        }
+
+        // ---- KV pool + allocator ----
+        const size_t pool_elems = (size_t)cfg.pool_blocks * dm.bc * dp;
+        kpool.alloc(pool_elems);
+        vpool.alloc(pool_elems);
+        stack.alloc((size_t)cfg.pool_blocks);
+        reset_allocator();
+
+        // ---- rows / activations ----
+        const int Bm = dm.Bmax;
+        for (DevBuf<int>* b : {&row_slot, &row_pos, &row_tok, &pf_slot, &pf_pos, &pf_tok, &seq_ids_dev})
+            b->alloc((size_t)Bm);
+        h32.alloc((size_t)2 * Bm * dp);
+        hb.alloc((size_t)2 * Bm * dp);
+        q32.alloc((size_t)Bm * dp);
+        att_b.alloc((size_t)Bm * dp);
+        mid32.alloc((size_t)Bm * dp);
+        mid_b.alloc((size_t)Bm * dp);
+        up_b.alloc((size_t)Bm * fp);
+        attn_cnt.alloc((size_t)Bm);
+        lm_part.alloc((size_t)(dm.Vp / 128) * Bm);
+        for (DevBuf<int>* b : {&layer, &out_layer, &exit_cnt, &iter_counter, &cur_iter}) b->alloc(4);
+        status.alloc((size_t)Bm);
+        first_accept.alloc((size_t)Bm);
+        accept.alloc((size_t)Bm);
+        conf.alloc((size_t)L * Bm);
+        fixed_conf.alloc((size_t)L * Bm);
+        rec_tok.alloc((size_t)rec_cap * Bm);
+        rec_acc.alloc((size_t)rec_cap * Bm);
+        rec_out.alloc((size_t)rec_cap);
+        rec_conf.alloc((size_t)rec_cap * L * Bm);
+        {
+            std::vector<double> lam((size_t)L);
+            for (int l = 1; l <= L; ++l) lam[(size_t)l - 1] = threshold_at(cfg.lambda0, cfg.gamma, cfg.lambda_min, l);
+            lambdas.alloc((size_t)L);
+            CK(cudaMemcpy(lambdas.p, lam.data(), sizeof(double) * L, cudaMemcpyHostToDevice));
+        }
+        CK(cudaHostAlloc(&cont_host, sizeof(int) * 4, cudaHostAllocMapped));
+        CK(cudaHostGetDevicePointer((void**)&cont_dev, cont_host, 0));
+
+        mapA_qkv = make_map(wqkv.p, L * 3 * dp, dp, 128);
+        mapA_wo = make_map(wo.p, L * dp, dp, 128);
+        mapA_up = make_map(wup.p, L * fp, dp, 128);
+        mapA_down = make_map(wdown.p, L * dp, fp, 128);
+        mapA_lm = make_map(lm.p, dm.Vp, dp, 128);
+        el::init_kernel_attributes();
+        slot_bpl.assign((size_t)dm.slots, 0);
+        ensure_bpl(1);
+        CK(cudaStreamSynchronize(stream));
+        slot_bpl.assign((size_t)dm.slots, 0);
+    }
+
+    void reset_allocator() {
+        std::vector<int> st((size_t)cfg.pool_blocks);
+        for (int i = 0; i < cfg.pool_blocks; ++i) st[(size_t)i] = cfg.pool_blocks - 1 - i;  // pops 0 first
+        CK(cudaMemcpyAsync(stack.p, st.data(), sizeof(int) * st.size(), cudaMemcpyHostToDevice, stream));
+        CK(cudaStreamSynchronize(stream));
+        top = cfg.pool_blocks;
+        peak = 0;
+        slot_bpl.assign((size_t)dm.slots, 0);
+    }
+
+    // tables / attention workspace sized for bpl blocks per (seq, layer)
+    void ensure_bpl(int bpl) {
+        if (bpl <= dm.bpl_max) return;
+        for (int b : slot_bpl)
+            if (b) fail(EL_LOGIC_ERROR, "block tables cannot grow while sequences are live");
+        dm.bpl_max = bpl;
+        tables.alloc((size_t)dm.slots * dm.L * bpl);
+        const int B = dm.Bmax;
+        const int target_chunks = std::max(1, ceil_div(148 * 4, B));
+        attn_cb = std::max(1, ceil_div(bpl, target_chunks));
+        attn_max_chunks = ceil_div(bpl, attn_cb);
+        const int stage_bytes = 2 * dm.bc * dm.dp * 2;
+        attn_stages = std::min(std::max(2, (200 * 1024) / stage_bytes), 4);
+        attn_stages = std::min(attn_stages, std::max(1, attn_cb));
+        while (attn_stages > 1 && el::attn_smem_bytes(dm, attn_stages) > 227 * 1024) --attn_stages;
+        attn_o.alloc((size_t)B * attn_max_chunks * dm.dp, false);
+        attn_ml.alloc((size_t)B * attn_max_chunks * 2, false);
+        invalidate_graphs();
+    }
+
+    void invalidate_graphs() {
+        for (auto& kv : graphs) {
+            if (kv.second.x) cudaGraphExecDestroy(kv.second.x);
+            if (kv.second.g) cudaGraphDestroy(kv.second.g);
+        }
+        graphs.clear();
+    }
+
+    // ---- GEMM plans ----
+    static int pick_splits(int m_tiles, int kb_total) {
+        int best = 1;
+        for (int s = 1; s <= std::min(kb_total, 16); ++s) {
+            if (kb_total % s) continue;
+            best = s;
+            if (m_tiles * s >= 148) break;
+        }
+        return best;
+    }
+    el::GemmPlan make_plan(const CUtensorMap& A, const CUtensorMap& Bm, int m_tiles, int k, int n_pad, bool tile,
+                           int forced_splits = 0) {
+        el::GemmPlan p;
+        p.tmA = A;
+        p.tmB = Bm;
+        p.m_tiles = m_tiles;
+        const int kb = k / 64;
+        p.splits = forced_splits ? forced_splits : pick_splits(m_tiles, kb);
+        p.kb_per_split = kb / p.splits;
+        p.n_pad = n_pad;
+        const int stage = 128 * 64 * 2 + n_pad * 64 * 2;
+        p.stages = std::max(1, std::min(p.kb_per_split, (200 * 1024) / stage));
+        p.smem_bytes = el::gemm_smem_bytes(n_pad, p.stages, tile);
+        while (p.smem_bytes > 227 * 1024 && p.stages > 1) p.smem_bytes = el::gemm_smem_bytes(n_pad, --p.stages, tile);
+        int cols = 32;
+        while (cols < n_pad) cols <<= 1;
+        p.tmem_cols = cols;
+        if (!tile && p.splits > 1) {
+            gemm_ws.ensure((size_t)p.splits * m_tiles * n_pad * 128);
+            gemm_cnt.ensure((size_t)m_tiles);
+        }
+        return p;
+    }
+    Plans& plans_for(int B) {
+        const int n_pad = std::max(16, round_up(B, 16));
+        auto it = plans.find(n_pad);
+        if (it != plans.end()) return it->second;
+        const int dp = dm.dp, fp = dm.fp, Bm = dm.Bmax, L = dm.L;
+        Plans P;
+        P.n_pad = n_pad;
+        const CUtensorMap mh = make_map(hb.p, 2 * Bm, dp, n_pad);
+        const CUtensorMap ma = make_map(att_b.p, Bm, dp, n_pad);
+        const CUtensorMap mm = make_map(mid_b.p, Bm, dp, n_pad);
+        const CUtensorMap mu = make_map(up_b.p, Bm, fp, n_pad);
+        P.qkv = make_plan(mapA_qkv, mh, 3 * dp / 128, dp, n_pad, false);
+        P.wo = make_plan(mapA_wo, ma, dp / 128, dp, n_pad, false);
+        P.up = make_plan(mapA_up, mm, fp / 128, dp, n_pad, false);
+        P.down = make_plan(mapA_down, mu, dp / 128, fp, n_pad, false);
+        P.lm = make_plan(mapA_lm, mh, dm.Vp / 128, dp, n_pad, true, 1);
+        P.fill = make_plan(mapA_qkv, mh, (L - 1) * (2 * dp / 128), dp, n_pad, false);
+        invalidate_graphs();  // workspace may have moved
+        return plans.emplace(n_pad, P).first->second;
+    }
+
+    el::DevState state(bool prefill, int B) {
+        el::DevState s{};
+        s.dm = dm;
+        s.wqkv = wqkv.p; s.wo = wo.p; s.wup = wup.p; s.wdown = wdown.p; s.emb = emb.p; s.lm = lm.p;
+        s.probe_w = probe_w.p; s.probe_b = probe_b;
+        s.kpool = kpool.p; s.vpool = vpool.p; s.tables = tables.p;
+        if (prefill) s.rows = el::Rows{pf_slot.p, pf_pos.p, pf_tok.p, B};
+        else s.rows = el::Rows{row_slot.p, row_pos.p, row_tok.p, B};
+        s.h32 = h32.p; s.hb = hb.p; s.q32 = q32.p; s.att_b = att_b.p; s.mid32 = mid32.p; s.mid_b = mid_b.p;
+        s.up_b = up_b.p;
+        s.attn_o = attn_o.p; s.attn_ml = attn_ml.p; s.attn_cnt = attn_cnt.p;
+        s.attn_max_chunks = attn_max_chunks; s.attn_cb = attn_cb; s.attn_stages = attn_stages;
+        s.attn_scale = (float)(1.0 / std::sqrt((double)dm.d));
+        s.gemm_ws = gemm_ws.p; s.gemm_cnt = gemm_cnt.p;
+        s.lm_part = lm_part.p;
+        s.layer = layer.p; s.out_layer = out_layer.p; s.status = status.p; s.first_accept = first_accept.p;
+        s.accept = accept.p; s.conf = conf.p; s.exit_cnt = exit_cnt.p; s.cont_host = cont_dev;
+        s.lambdas = lambdas.p; s.fixed_conf = fixed_conf.p;
+        s.technique = prefill ? el::kNever : cfg.technique;
+        s.exit_layer = cfg.exit_layer;
+        s.use_cond = 0;
+        s.iter_counter = prefill ? cur_iter.p + 1 : iter_counter.p;  // prefill: scratch counter
+        s.cur_iter = prefill ? cur_iter.p + 2 : cur_iter.p;
+        s.rec_tok = rec_tok.p; s.rec_acc = rec_acc.p; s.rec_out = rec_out.p; s.rec_conf = rec_conf.p;
+        s.rec_cap = rec_cap;
+        return s;
+    }
+
+    // one layer's kernels (the WHILE body)
+    void launch_layer(const el::DevState& s, Plans& P) {
+        el::launch_gemm(el::kGemmQkv, P.qkv, s, stream);
+        el::launch_attention(s, stream);
+        el::launch_gemm(el::kGemmWo, P.wo, s, stream);
+        el::launch_gemm(el::kGemmUp, P.up, s, stream);
+        el::launch_gemm(el::kGemmDown, P.down, s, stream);
+        if (s.technique == el::kSoftmax) el::launch_gemm(el::kGemmLmCheck, P.lm, s, stream);
+        el::launch_exit(s, stream);
+    }
+    void launch_tail(const el::DevState& s, Plans& P) {
+        if (s.technique != el::kNever) el::launch_gemm(el::kGemmFill, P.fill, s, stream);
+        if (s.technique != el::kSoftmax) el::launch_gemm(el::kGemmLmFinal, P.lm, s, stream);
+        el::launch_finish(s, stream);
+    }
+    int launches_per_iteration(int e) const {
+        const int per_layer = 6 + (cfg.technique == EL_TECH_SOFTMAX ? 1 : 0);
+        return 1 + e * per_layer + (cfg.technique != EL_TECH_NEVER ? 1 : 0) + (cfg.technique != EL_TECH_SOFTMAX ? 1 : 0) + 1;
+    }
+
+    // eager iteration: host reads the device continue flag after each layer
+    void iteration_eager(int B) {
+        Plans& P = plans_for(B);
+        el::DevState s = state(false, B);
+        el::launch_embed(s, stream);
+        for (int l = 1; l <= dm.L; ++l) {
+            launch_layer(s, P);
+            CK(cudaStreamSynchronize(stream));
+            if (*(volatile int*)cont_host == 0) break;
+        }
+        launch_tail(s, P);
+    }
+
+    Graph& graph_for(int B) {
+        auto it = graphs.find(B);
+        if (it != graphs.end()) return it->second;
+        Plans& P = plans_for(B);
+        Graph G;
+        CK(cudaGraphCreate(&G.g, 0));
+        cudaGraphConditionalHandle h;
+        CK(cudaGraphConditionalHandleCreate(&h, G.g, 1, cudaGraphCondAssignDefault));
+        el::DevState s = state(false, B);
+        s.use_cond = 1;
+        s.cond = h;
+        s.cont_host = nullptr;
+        const cudaStreamCaptureMode mode = cudaStreamCaptureModeRelaxed;
+        // segment 1: embed
+        CK(cudaStreamBeginCaptureToGraph(stream, G.g, nullptr, nullptr, 0, mode));
+        el::launch_embed(s, stream);
+        cudaStreamCaptureStatus cs;
+        const cudaGraphNode_t* deps = nullptr;
+        size_t ndeps = 0;
+        CK(cudaStreamGetCaptureInfo(stream, &cs, nullptr, nullptr, &deps, &ndeps));
+        std::vector<cudaGraphNode_t> dv(deps, deps + ndeps);
+        CK(cudaStreamEndCapture(stream, &G.g));
+        // WHILE(layer loop)
+        cudaGraphNodeParams cp{};
+        cp.type = cudaGraphNodeTypeConditional;
+        cp.conditional.handle = h;
+        cp.conditional.type = cudaGraphCondTypeWhile;
+        cp.conditional.size = 1;
+        cudaGraphNode_t wnode;
+        CK(cudaGraphAddNode(&wnode, G.g, dv.data(), dv.size(), &cp));
+        cudaGraph_t body = cp.conditional.phGraph_out[0];
+        CK(cudaStreamBeginCaptureToGraph(stream, body, nullptr, nullptr, 0, mode));
+        launch_layer(s, P);
+        CK(cudaStreamEndCapture(stream, &body));
+        // tail: fill, lm head, finish
+        CK(cudaStreamBeginCaptureToGraph(stream, G.g, &wnode, nullptr, 1, mode));
+        launch_tail(s, P);
+        CK(cudaStreamEndCapture(stream, &G.g));
+        CK(cudaGraphInstantiate(&G.x, G.g, 0));
+        return graphs.emplace(B, G).first->second;
+    }
+
+    void iteration(int B) {
+        if (use_graph) {
+            Graph& G = graph_for(B);
+            CK(cudaGraphLaunch(G.x, stream));
+        } else {
+            iteration_eager(B);
+        }
+    }
+
+    // ---- allocator (kv_cache.cpp:78-106, 182-194) ----
+    int bpl_for(int capacity_tokens) const { return ceil_div(capacity_tokens, dm.bc); }
+    bool can_allocate(int capacity_tokens) const { return (long)bpl_for(capacity_tokens) * dm.L <= top; }
+    int free_slot() const {
+        for (int s = 0; s < dm.slots; ++s)
+            if (slot_bpl[(size_t)s] == 0) return s;
+        fail(EL_RUNTIME_ERROR, "no free sequence slot");
+    }
+    int allocate(int capacity_tokens) {
+        const int bpl = bpl_for(capacity_tokens);
+        if ((long)bpl * dm.L > top)
+            fail(EL_KV_OUT_OF_MEMORY, "allocate: need %ld blocks, %d free", (long)bpl * dm.L, top);
+        if (bpl > dm.bpl_max) fail(EL_RUNTIME_ERROR, "allocate: %d blocks per layer exceed the table width %d", bpl, dm.bpl_max);
+        const int slot = free_slot();
+        el::launch_kv_alloc(stack.p, top, tables.p, dm, slot, bpl, stream);
+        top -= bpl * dm.L;
+        peak = std::max(peak, cfg.pool_blocks - top);
+        slot_bpl[(size_t)slot] = bpl;
+        return slot;
+    }
+    void release(int slot) {
+        const int bpl = slot_bpl[(size_t)slot];
+        el::launch_kv_release(stack.p, top, tables.p, dm, slot, bpl, stream);
+        top += bpl * dm.L;
+        slot_bpl[(size_t)slot] = 0;
+    }
+
+    // ---- prefill of newly admitted sequences (engine.cpp:166-181), batched
+    //      across sequences (attention is per sequence, so this is exact) ----
+    struct PfSeq {
+        int slot;
+        std::vector<int> toks;  // prompt[0 .. P-2]
+    };
+    void prefill(const std::vector<PfSeq>& seqs) {
+        int maxn = 0;
+        for (const auto& q : seqs) maxn = std::max(maxn, (int)q.toks.size());
+        std::vector<int> hs, hp, ht;
+        for (int j = 0; j < maxn; ++j) {
+            hs.clear(); hp.clear(); ht.clear();
+            for (const auto& q : seqs)
+                if ((int)q.toks.size() > j) {
+                    hs.push_back(q.slot);
+                    hp.push_back(j);
+                    ht.push_back(q.toks[(size_t)j]);
+                }
+            const int B = (int)hs.size();
+            CK(cudaMemcpyAsync(pf_slot.p, hs.data(), sizeof(int) * B, cudaMemcpyHostToDevice, stream));
+            CK(cudaMemcpyAsync(pf_pos.p, hp.data(), sizeof(int) * B, cudaMemcpyHostToDevice, stream));
+            CK(cudaMemcpyAsync(pf_tok.p, ht.data(), sizeof(int) * B, cudaMemcpyHostToDevice, stream));
+            Plans& P = plans_for(B);
+            el::DevState s = state(true, B);
+            s.cont_host = nullptr;
+            el::launch_embed(s, stream);
+            for (int l = 1; l <= dm.L; ++l) {
+                el::launch_gemm(el::kGemmQkv, P.qkv, s, stream);
+                el::launch_attention(s, stream);
+                el::launch_gemm(el::kGemmWo, P.wo, s, stream);
+                el::launch_gemm(el::kGemmUp, P.up, s, stream);
+                el::launch_gemm(el::kGemmDown, P.down, s, stream);
+                el::launch_exit(s, stream);
+            }
+            el::launch_advance(s, stream);
+            CK(cudaStreamSynchronize(stream));  // host vectors are reused next step
+        }
+    }
+
+    // ---- records ----
+    struct IterOut {
+        int out_layer;
+        std::vector<int> tok, acc;
+        std::vector<float> conf;  // [L][B]
+    };
+    IterOut read_iteration(int iter_index, int B) {
+        IterOut o;
+        const int cur = iter_index % rec_cap, Bm = dm.Bmax, L = dm.L;
+        o.tok.resize((size_t)B);
+        o.acc.resize((size_t)B);
+        std::vector<float> cf((size_t)L * Bm);
+        CK(cudaMemcpyAsync(o.tok.data(), rec_tok.p + (size_t)cur * Bm, sizeof(int) * B, cudaMemcpyDeviceToHost, stream));
+        CK(cudaMemcpyAsync(o.acc.data(), rec_acc.p + (size_t)cur * Bm, sizeof(int) * B, cudaMemcpyDeviceToHost, stream));
+        CK(cudaMemcpyAsync(&o.out_layer, rec_out.p + cur, sizeof(int), cudaMemcpyDeviceToHost, stream));
+        CK(cudaMemcpyAsync(cf.data(), rec_conf.p + (size_t)cur * L * Bm, sizeof(float) * L * Bm, cudaMemcpyDeviceToHost, stream));
+        CK(cudaStreamSynchronize(stream));
+        o.conf.resize((size_t)L * B);
+        for (int l = 0; l < L; ++l)
+            for (int b = 0; b < B; ++b) o.conf[(size_t)l * B + b] = cf[(size_t)l * Bm + b];
+        return o;
+    }
+    int device_iter_counter() {
+        int c = 0;
+        CK(cudaMemcpy(&c, iter_counter.p, sizeof(int), cudaMemcpyDeviceToHost));
+        return c;
+    }
+
+    std::vector<float> read_kv(int slot, int layer_, int pos, int which) {
+        const int dp = dm.dp;
+        int blk = 0;
+        CK(cudaMemcpy(&blk, tables.p + ((size_t)slot * dm.L + (layer_ - 1)) * dm.bpl_max + pos / dm.bc, sizeof(int),
+                      cudaMemcpyDeviceToHost));
+        std::vector<uint16_t> raw((size_t)dp);
+        const uint16_t* src = (which == 0 ? kpool.p : vpool.p) + ((size_t)blk * dm.bc + pos % dm.bc) * dp;
+        CK(cudaMemcpy(raw.data(), src, sizeof(uint16_t) * dp, cudaMemcpyDeviceToHost));
+        std::vector<float> out((size_t)dm.d);
+        for (int i = 0; i < dm.d; ++i) {
+            uint32_t f = (uint32_t)raw[(size_t)i] << 16;
+            std::memcpy(&out[(size_t)i], &f, 4);
+        }
+        return out;
+    }
+
+    // ------------------------------------------------------------------
+    // Engine::run (engine.cpp:110-330)
+    // ------------------------------------------------------------------
+    struct Live {
+        int id, slot, max_new, next_input, committed;
+        bool finished = false;
+        double arrival, first_token = -1.0, finish = -1.0;
+        std::vector<int> prompt, tokens, exit_layers, iter_out;
+    };
+
+    el_transcript* run(int n, const double* arrival, const int32_t* off, const int32_t* prompt, const int32_t* max_new) {
+        if (in_session) fail(EL_LOGIC_ERROR, "run: a decode session is active");
+        const int L = dm.L, d = dm.d;
+        // Workload::validate_and_sort (workload.cpp:15-38)
+        std::vector<int> order((size_t)n);
+        for (int i = 0; i < n; ++i) order[(size_t)i] = i;
+        std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return arrival[a] < arrival[b]; });
+        int max_cap = 1;
+        for (int i = 0; i < n; ++i) {
+            const int r = order[(size_t)i];
+            const int plen = off[r + 1] - off[r];
+            if (arrival[r] < 0.0) fail(EL_INVALID_ARGUMENT, "workload: negative arrival_time at request %d", i);
+            if (plen < 1) fail(EL_INVALID_ARGUMENT, "workload: empty prompt at request %d", i);
+            if (max_new[r] < 1) fail(EL_INVALID_ARGUMENT, "workload: max_new_tokens must be >= 1 at request %d", i);
+            for (int j = off[r]; j < off[r + 1]; ++j)
+                if (prompt[j] < 0 || prompt[j] >= cfg.vocab_size)
+                    fail(EL_INVALID_ARGUMENT, "workload: token id %d outside vocab at request %d", prompt[j], i);
+            max_cap = std::max(max_cap, plen + max_new[r]);
+        }
+        reset_allocator();
+        ensure_bpl(std::min(bpl_for(max_cap), std::max(1, cfg.pool_blocks / L)));
+        CK(cudaMemsetAsync(iter_counter.p, 0, sizeof(int), stream));
+
+        auto t = std::make_unique<el_transcript>();
+        t->d = d;
+        t->L = L;
+        t->it_batch_off.push_back(0);
+        t->sq_prompt_off.push_back(0);
+        t->sq_tok_off.push_back(0);
+        double clock = 0.0, total_idle = 0.0;
+        int next_pending = 0, iteration_no = 0;
+        std::vector<Live> running;
+        std::vector<int> hs, hp, ht;
+
+        for (;;) {
+            // evict_finished (engine.cpp:130-164)
+            for (auto it = running.begin(); it != running.end();) {
+                if (!it->finished) { ++it; continue; }
+                if (cfg.capture_kv) {
+                    Capture& c = t->caps[it->id];
+                    c.committed = it->committed;
+                    c.k.assign((size_t)L * it->committed * d, 0.0);
+                    c.v.assign((size_t)L * it->committed * d, 0.0);
+                    for (int l = 1; l <= L; ++l)
+                        for (int p = 0; p < it->committed; ++p) {
+                            const auto kk = read_kv(it->slot, l, p, 0), vv = read_kv(it->slot, l, p, 1);
+                            for (int i = 0; i < d; ++i) {
+                                c.k[((size_t)(l - 1) * it->committed + p) * d + i] = kk[(size_t)i];
+                                c.v[((size_t)(l - 1) * it->committed + p) * d + i] = vv[(size_t)i];
+                            }
+                        }
+                    c.have_kv = true;
+                }
+                release(it->slot);
+                t->sq_id.push_back(it->id);
+                t->sq_arrival.push_back(it->arrival);
+                t->sq_first.push_back(it->first_token);
+                t->sq_finish.push_back(it->finish);
+                t->sq_max_new.push_back(it->max_new);
+                for (int x : it->prompt) t->sq_prompt.push_back(x);
+                t->sq_prompt_off.push_back((int32_t)t->sq_prompt.size());
+                for (size_t i = 0; i < it->tokens.size(); ++i) {
+                    t->sq_tokens.push_back(it->tokens[i]);
+                    t->sq_exit_layers.push_back(it->exit_layers[i]);
+                    t->sq_iter_out.push_back(it->iter_out[i]);
+                }
+                t->sq_tok_off.push_back((int32_t)t->sq_tokens.size());
+                it = running.erase(it);
+            }
+            // admit (engine.cpp:183-206) -- prefill charges advance the clock in
+            // admission order; the prefill math itself is batched afterwards
+            std::vector<PfSeq> pf;
+            while (next_pending < n) {
+                const int r = order[(size_t)next_pending];
+                if (arrival[r] > clock) break;
+                if ((int)running.size() >= cfg.max_batch) break;
+                const int plen = off[r + 1] - off[r];
+                const int need = plen + max_new[r];
+                if (!can_allocate(need)) break;  // strict FIFO: a deferred head blocks later arrivals
+                Live q;
+                q.id = next_pending;
+                q.slot = allocate(need);
+                q.arrival = arrival[r];
+                q.max_new = max_new[r];
+                q.prompt.assign(prompt + off[r], prompt + off[r + 1]);
+                q.next_input = q.prompt.back();
+                const int positions = plen - 1;
+                q.committed = positions;
+                PfSeq ps;
+                ps.slot = q.slot;
+                ps.toks.assign(q.prompt.begin(), q.prompt.end() - 1);
+                if (positions > 0) pf.push_back(std::move(ps));
+                const double charge = (double)positions * L * (cfg.c_layer_fixed + cfg.c_layer_per_seq);
+                clock += charge;
+                t->pf_clock.push_back(clock);
+                t->pf_charge.push_back(charge);
+                t->pf_seq.push_back(q.id);
+                t->pf_positions.push_back(positions);
+                running.push_back(std::move(q));
+                ++next_pending;
+            }
+            if (!pf.empty()) {
+                if (cfg.synthetic_kv_seed >= 0) {
+                    std::vector<int> ids, slots;
+                    int P = 0;
+                    for (size_t i = running.size() - pf.size(); i < running.size(); ++i) {
+                        ids.push_back(running[i].id);
+                        slots.push_back(running[i].slot);
+                        P = std::max(P, running[i].committed);
+                    }
+                    // seeded prefix for sequences admitted together must share the prefix length
+                    for (size_t i = running.size() - pf.size(); i < running.size(); ++i)
+                        if (running[i].committed != P)
+                            fail(EL_INVALID_ARGUMENT, "synthetic KV prefix needs equal prompt lengths per admission");
+                    seed_prefix(slots, ids, P, (uint64_t)cfg.synthetic_kv_seed);
+                } else {
+                    prefill(pf);
+                }
+            }
+            if (running.empty()) {
+                if (next_pending >= n) break;
+                {
+                    const int r = order[(size_t)next_pending];
+                    if (arrival[r] <= clock && !can_allocate(off[r + 1] - off[r] + max_new[r]))
+                        fail(EL_KV_OUT_OF_MEMORY, "allocate: request %d can never fit the pool", next_pending);
+                }
+                const double na = arrival[order[(size_t)next_pending]];
+                if (na > clock) {
+                    total_idle += na - clock;
+                    clock = na;
+                }
+                continue;
+            }
+
+            // decode_iteration (engine.cpp:208-310)
+            const int B = (int)running.size();
+            hs.assign((size_t)B, 0); hp.assign((size_t)B, 0); ht.assign((size_t)B, 0);
+            for (int b = 0; b < B; ++b) {
+                hs[(size_t)b] = running[(size_t)b].slot;
+                hp[(size_t)b] = running[(size_t)b].committed;
+                ht[(size_t)b] = running[(size_t)b].next_input;
+            }
+            CK(cudaMemcpyAsync(row_slot.p, hs.data(), sizeof(int) * B, cudaMemcpyHostToDevice, stream));
+            CK(cudaMemcpyAsync(row_pos.p, hp.data(), sizeof(int) * B, cudaMemcpyHostToDevice, stream));
+            CK(cudaMemcpyAsync(row_tok.p, ht.data(), sizeof(int) * B, cudaMemcpyHostToDevice, stream));
+            iteration(B);
+            const IterOut o = read_iteration(iteration_no, B);
+            ++iteration_no;
+            const int e = o.out_layer;
+            if (e < 1 || e > L) fail(EL_RUNTIME_ERROR, "decode_iteration: bad output layer %d", e);
+            for (auto& q : running) q.committed += 1;  // commit (engine.cpp:262-264)
+
+            const double charge = e * (cfg.c_layer_fixed + cfg.c_layer_per_seq * B) + e * B * check_cost() +
+                                  (double)(L - e) * B * cfg.c_fill_per_seq_layer;
+            clock += charge;
+            t->it_clock.push_back(clock);
+            t->it_charge.push_back(charge);
+            t->it_output_layer.push_back(e);
+            for (int l = 0; l < L; ++l)
+                for (int b = 0; b < B; ++b) t->it_conf.push_back((double)o.conf[(size_t)l * B + b]);
+            std::vector<float> hexit;
+            if (cfg.capture_kv) {
+                hexit.resize((size_t)B * dm.dp);
+                CK(cudaMemcpy(hexit.data(), h32.p + (size_t)(e & 1) * dm.Bmax * dm.dp, sizeof(float) * B * dm.dp,
+                              cudaMemcpyDeviceToHost));
+            }
+            int max_accept = 0;
+            for (int b = 0; b < B; ++b) {
+                Live& q = running[(size_t)b];
+                const int token = o.tok[(size_t)b];
+                const int acc = o.acc[(size_t)b];
+                max_accept = std::max(max_accept, acc);
+                t->ps_seq.push_back(q.id);
+                t->ps_accept.push_back(acc);
+                t->ps_token.push_back(token);
+                q.tokens.push_back(token);
+                q.exit_layers.push_back(acc);
+                q.iter_out.push_back(e);
+                if (cfg.capture_kv)
+                    for (int i = 0; i < d; ++i) t->caps[q.id].exit_states.push_back(hexit[(size_t)b * dm.dp + i]);
+                if (q.tokens.size() == 1) q.first_token = clock;
+                const bool hit_eos = cfg.eos_token >= 0 && token == cfg.eos_token;
+                if (hit_eos || (int)q.tokens.size() >= q.max_new) {
+                    q.finished = true;
+                    q.finish = clock;
+                } else {
+                    q.next_input = token;
+                }
+            }
+            if (max_accept != e) fail(EL_RUNTIME_ERROR, "decode_iteration: output_layer %d != max accept %d", e, max_accept);
+            t->it_batch_off.push_back((int32_t)t->ps_seq.size());
+        }
+        t->meta = {clock, total_idle, (double)cfg.pool_blocks, (double)top, (double)peak};
+        return t.release();
+    }
+
+    // seeded KV prefix for the sequences in `slots` (rows of the prefill row set)
+    void seed_prefix(const std::vector<int>& slots, const std::vector<int>& ids, int P, uint64_t kv_seed) {
+        const int B = (int)slots.size();
+        CK(cudaMemcpyAsync(pf_slot.p, slots.data(), sizeof(int) * B, cudaMemcpyHostToDevice, stream));
+        CK(cudaMemcpyAsync(seq_ids_dev.p, ids.data(), sizeof(int) * B, cudaMemcpyHostToDevice, stream));
+        el::DevState s = state(true, B);
+        el::launch_kv_prefix(s, seq_ids_dev.p, P, kv_seed, 1, stream);
+        CK(cudaStreamSynchronize(stream));
+    }
+
+    // ------------------------------------------------------------------
+    // decode session: fixed batch over a seeded KV prefix (bench workload)
+    // ------------------------------------------------------------------
+    void session_begin(int B, const int32_t* first, int prefix_len, int capacity, uint64_t kv_seed, const int32_t* ids) {
+        if (in_session) session_end();
+        if (B < 1) fail(EL_LOGIC_ERROR, "decode_iteration: empty batch");
+        if (B > dm.Bmax) fail(EL_INVALID_ARGUMENT, "session: batch %d > max_batch %d", B, dm.Bmax);
+        if (prefix_len < 0 || capacity < prefix_len + 1) fail(EL_INVALID_ARGUMENT, "session: capacity must exceed prefix");
+        for (int b = 0; b < B; ++b)
+            if (first[b] < 0 || first[b] >= cfg.vocab_size) fail(EL_INVALID_ARGUMENT, "session: token outside vocab");
+        reset_allocator();
+        ensure_bpl(bpl_for(capacity));
+        std::vector<int> slots, idv, pos((size_t)B, prefix_len), tok(first, first + B);
+        for (int b = 0; b < B; ++b) {
+            slots.push_back(allocate(capacity));
+            idv.push_back(ids ? ids[b] : b);
+        }
+        seed_prefix(slots, idv, prefix_len, kv_seed);
+        CK(cudaMemcpyAsync(row_slot.p, slots.data(), sizeof(int) * B, cudaMemcpyHostToDevice, stream));
+        CK(cudaMemcpyAsync(row_pos.p, pos.data(), sizeof(int) * B, cudaMemcpyHostToDevice, stream));
+        CK(cudaMemcpyAsync(row_tok.p, tok.data(), sizeof(int) * B, cudaMemcpyHostToDevice, stream));
+        CK(cudaMemsetAsync(iter_counter.p, 0, sizeof(int), stream));
+        CK(cudaStreamSynchronize(stream));
+        in_session = true;
+        sess_B = B;
+        sess_iters = 0;
+        sess_ids = idv;
+        sess_capacity = capacity;
+        sess_prefix = prefix_len;
+    }
+    int sess_capacity = 0, sess_prefix = 0;
+    void session_end() {
+        in_session = false;
+        reset_allocator();
+    }
+    void need_session() const {
+        if (!in_session) fail(EL_LOGIC_ERROR, "no active decode session");
+    }
+    void check_capacity(int n_more) const {
+        if (sess_prefix + sess_iters + n_more > sess_capacity)
+            fail(EL_KV_OUT_OF_MEMORY, "append: position exceeds reserved capacity %d", sess_capacity);
+    }
+};
+
+// ============================================================================
+// C ABI
+// ============================================================================
+#define API_BEGIN try {
+#define API_END                                   \
+    }                                             \
+    catch (const ElError& e) {                    \
+        g_err = e.msg;                            \
+        return e.code;                            \
+    }                                             \
+    catch (const std::exception& e) {             \
+        g_err = e.what();                         \
+        return EL_RUNTIME_ERROR;                  \
+    }                                             \
+    return EL_OK;
+
+extern "C" {
+
+const char* el_last_error(void) { return g_err.c_str(); }
+int el_version(void) { return 1; }
+
+int el_engine_create(const el_engine_config* cfg, el_engine** out) {
+    API_BEGIN
+    if (!cfg || !out) fail(EL_INVALID_ARGUMENT, "null argument");
+    *out = nullptr;
+    auto e = std::make_unique<el_engine>();
+    e->cfg = *cfg;
+    e->create();
+    *out = e.release();
+    API_END
+}
+
+int el_engine_destroy(el_engine* e) {
+    API_BEGIN
+    if (e) {
+        cudaStreamSynchronize(e->stream);
+        delete e;
+    }
+    API_END
+}
+
+int el_engine_set_option(el_engine* e, const char* key, int64_t v) {
+    API_BEGIN
+    if (!std::strcmp(key, "graph")) e->use_graph = v != 0;
+    else if (!std::strcmp(key, "rec_cap")) {
+        if (v < 1) fail(EL_INVALID_ARGUMENT, "rec_cap must be >= 1");
+        e->rec_cap = (int)v;
+        e->rec_tok.alloc((size_t)v * e->dm.Bmax);
+        e->rec_acc.alloc((size_t)v * e->dm.Bmax);
+        e->rec_out.alloc((size_t)v);
+        e->rec_conf.alloc((size_t)v * e->dm.L * e->dm.Bmax);
+        e->invalidate_graphs();
+    } else fail(EL_INVALID_ARGUMENT, "unknown option %s", key);
+    API_END
+}
+
+int el_engine_run(el_engine* e, int n, const double* arrival, const int32_t* off, const int32_t* prompt,
+                  const int32_t* max_new, el_transcript** out) {
+    API_BEGIN
+    *out = e->run(n, arrival, off, prompt, max_new);
+    API_END
+}
+
+int64_t el_transcript_len(const el_transcript* t, const char* f) {
+    auto* tt = const_cast<el_transcript*>(t);
+    if (auto* a = tt->i32(f)) return (int64_t)a->size();
+    if (auto* b = tt->f64(f)) return (int64_t)b->size();
+    return -1;
+}
+int el_transcript_get_i32(const el_transcript* t, const char* f, int32_t* out) {
+    auto* a = const_cast<el_transcript*>(t)->i32(f);
+    if (!a) { g_err = std::string("unknown field ") + f; return EL_INVALID_ARGUMENT; }
+    if (!a->empty()) std::memcpy(out, a->data(), sizeof(int32_t) * a->size());
+    return EL_OK;
+}
+int el_transcript_get_f64(const el_transcript* t, const char* f, double* out) {
+    auto* a = const_cast<el_transcript*>(t)->f64(f);
+    if (!a) { g_err = std::string("unknown field ") + f; return EL_INVALID_ARGUMENT; }
+    if (!a->empty()) std::memcpy(out, a->data(), sizeof(double) * a->size());
+    return EL_OK;
+}
+int el_transcript_kv(const el_transcript* t, int seq, int layer, double* k, double* v, int64_t cap) {
+    auto it = t->caps.find(seq);
+    if (it == t->caps.end() || !it->second.have_kv) { g_err = "no kv capture for seq"; return -EL_INVALID_ARGUMENT; }
+    const Capture& c = it->second;
+    const size_t n = (size_t)c.committed * t->d;
+    if ((int64_t)n > cap || layer < 1 || layer > t->L) { g_err = "bad kv request"; return -EL_INVALID_ARGUMENT; }
+    std::memcpy(k, c.k.data() + (size_t)(layer - 1) * n, sizeof(double) * n);
+    std::memcpy(v, c.v.data() + (size_t)(layer - 1) * n, sizeof(double) * n);
+    return c.committed;
+}
+int el_transcript_exit_states(const el_transcript* t, int seq, double* out, int64_t cap) {
+    auto it = t->caps.find(seq);
+    if (it == t->caps.end()) { g_err = "no capture for seq"; return -EL_INVALID_ARGUMENT; }
+    const auto& x = it->second.exit_states;
+    if ((int64_t)x.size() > cap) { g_err = "buffer too small"; return -EL_INVALID_ARGUMENT; }
+    std::memcpy(out, x.data(), sizeof(double) * x.size());
+    return (int)(x.size() / (size_t)t->d);
+}
+void el_transcript_free(el_transcript* t) { delete t; }
+
+int el_session_begin(el_engine* e, int B, const int32_t* first, int prefix_len, int capacity, uint64_t kv_seed,
+                     const int32_t* ids) {
+    API_BEGIN
+    e->session_begin(B, first, prefix_len, capacity, kv_seed, ids);
+    API_END
+}
+int el_session_end(el_engine* e) {
+    API_BEGIN
+    e->session_end();
+    API_END
+}
+
+int el_decode_iteration(el_engine* e, const int32_t* tokens_in, int32_t* tokens_out, int32_t* accept_out,
+                        float* conf_out, int32_t* output_layer) {
+    API_BEGIN
+    e->need_session();
+    e->check_capacity(1);
+    const int B = e->sess_B;
+    if (tokens_in) CK(cudaMemcpyAsync(e->row_tok.p, tokens_in, sizeof(int) * B, cudaMemcpyHostToDevice, e->stream));
+    e->iteration(B);
+    const auto o = e->read_iteration(e->sess_iters, B);
+    e->sess_iters++;
+    if (tokens_out) std::memcpy(tokens_out, o.tok.data(), sizeof(int) * B);
+    if (accept_out) std::memcpy(accept_out, o.acc.data(), sizeof(int) * B);
+    if (conf_out) std::memcpy(conf_out, o.conf.data(), sizeof(float) * o.conf.size());
+    if (output_layer) *output_layer = o.out_layer;
+    API_END
+}
+
+int el_decode_run(el_engine* e, int n) {
+    API_BEGIN
+    e->need_session();
+    e->check_capacity(n);
+    for (int i = 0; i < n; ++i) e->iteration(e->sess_B);
+    e->sess_iters += n;
+    API_END
+}
+
+int el_decode_records(el_engine* e, int first, int n, int32_t* tokens, int32_t* accept, int32_t* out_layer,
+                      float* conf) {
+    API_BEGIN
+    e->need_session();
+    if (first < 0 || first + n > e->sess_iters || n > e->rec_cap || first < e->sess_iters - e->rec_cap)
+        fail(EL_INVALID_ARGUMENT, "records [%d, %d) not available", first, first + n);
+    CK(cudaStreamSynchronize(e->stream));
+    const int B = e->sess_B, L = e->dm.L;
+    for (int i = 0; i < n; ++i) {
+        const auto o = e->read_iteration(first + i, B);
+        if (tokens) std::memcpy(tokens + (size_t)i * B, o.tok.data(), sizeof(int) * B);
+        if (accept) std::memcpy(accept + (size_t)i * B, o.acc.data(), sizeof(int) * B);
+        if (out_layer) out_layer[i] = o.out_layer;
+        if (conf) std::memcpy(conf + (size_t)i * L * B, o.conf.data(), sizeof(float) * L * B);
+    }
+    API_END
+}
+
+int el_decode_iterations_done(el_engine* e) { return e->sess_iters; }
+
+int el_set_fixed_confidences(el_engine* e, const float* conf) {
+    API_BEGIN
+    e->need_session();
+    const int B = e->sess_B, L = e->dm.L, Bm = e->dm.Bmax;
+    std::vector<float> buf((size_t)L * Bm, 0.f);
+    for (int l = 0; l < L; ++l)
+        for (int b = 0; b < B; ++b) buf[(size_t)l * Bm + b] = conf[(size_t)l * B + b];
+    CK(cudaMemcpyAsync(e->fixed_conf.p, buf.data(), sizeof(float) * buf.size(), cudaMemcpyHostToDevice, e->stream));
+    CK(cudaStreamSynchronize(e->stream));
+    API_END
+}
+
+int el_session_kv(el_engine* e, int row, int layer, int pos, float* k, float* v) {
+    API_BEGIN
+    e->need_session();
+    if (row < 0 || row >= e->sess_B || layer < 1 || layer > e->dm.L || pos < 0 || pos >= e->sess_prefix + e->sess_iters)
+        fail(EL_RUNTIME_ERROR, "view: entries missing at (row %d, layer %d, position %d)", row, layer, pos);
+    CK(cudaStreamSynchronize(e->stream));
+    int slot = 0;
+    CK(cudaMemcpy(&slot, e->row_slot.p + row, sizeof(int), cudaMemcpyDeviceToHost));
+    const auto kk = e->read_kv(slot, layer, pos, 0), vv = e->read_kv(slot, layer, pos, 1);
+    std::memcpy(k, kk.data(), sizeof(float) * kk.size());
+    std::memcpy(v, vv.data(), sizeof(float) * vv.size());
+    API_END
+}
+
+int el_session_hidden(el_engine* e, int parity, float* out) {
+    API_BEGIN
+    e->need_session();
+    CK(cudaStreamSynchronize(e->stream));
+    const int B = e->sess_B, dp = e->dm.dp, d = e->dm.d;
+    std::vector<float> buf((size_t)B * dp);
+    CK(cudaMemcpy(buf.data(), e->h32.p + (size_t)(parity & 1) * e->dm.Bmax * dp, sizeof(float) * buf.size(),
+                  cudaMemcpyDeviceToHost));
+    for (int b = 0; b < B; ++b) std::memcpy(out + (size_t)b * d, buf.data() + (size_t)b * dp, sizeof(float) * d);
+    API_END
+}
+
+int el_session_block_table(el_engine* e, int row, int32_t* out, int bpl_cap) {
+    API_BEGIN
+    e->need_session();
+    CK(cudaStreamSynchronize(e->stream));
+    int slot = 0;
+    CK(cudaMemcpy(&slot, e->row_slot.p + row, sizeof(int), cudaMemcpyDeviceToHost));
+    const int bpl = e->slot_bpl[(size_t)slot];
+    if (bpl > bpl_cap) fail(EL_INVALID_ARGUMENT, "bpl_cap too small");
+    for (int l = 0; l < e->dm.L; ++l)
+        CK(cudaMemcpy(out + (size_t)l * bpl, e->tables.p + ((size_t)slot * e->dm.L + l) * e->dm.bpl_max,
+                      sizeof(int) * bpl, cudaMemcpyDeviceToHost));
+    return bpl;
+    API_END
+}
+
+int el_time_decode(el_engine* e, int n, float* ms) {
+    API_BEGIN
+    e->need_session();
+    e->check_capacity(n);
+    cudaEvent_t a, b;
+    CK(cudaEventCreate(&a));
+    CK(cudaEventCreate(&b));
+    CK(cudaStreamSynchronize(e->stream));
+    CK(cudaEventRecord(a, e->stream));
+    for (int i = 0; i < n; ++i) e->iteration(e->sess_B);
+    CK(cudaEventRecord(b, e->stream));
+    CK(cudaEventSynchronize(b));
+    CK(cudaEventElapsedTime(ms, a, b));
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    e->sess_iters += n;
+    API_END
+}
+
+int el_time_kernel(el_engine* e, int kind, int layer, int reps, float* ms) {
+    API_BEGIN
+    e->need_session();
+    if (layer < 1 || layer > e->dm.L) fail(EL_INVALID_ARGUMENT, "layer out of range");
+    const int B = e->sess_B;
+    auto& P = e->plans_for(B);
+    el::DevState s = e->state(false, B);
+    s.cont_host = nullptr;
+    CK(cudaMemcpyAsync(e->layer.p, &layer, sizeof(int), cudaMemcpyHostToDevice, e->stream));
+    cudaEvent_t a, b;
+    CK(cudaEventCreate(&a));
+    CK(cudaEventCreate(&b));
+    auto one = [&]() {
+        switch (kind) {
+            case 0: el::launch_attention(s, e->stream); break;
+            case 1: el::launch_gemm(el::kGemmQkv, P.qkv, s, e->stream); break;
+            case 2: el::launch_gemm(el::kGemmWo, P.wo, s, e->stream); break;
+            case 3: el::launch_gemm(el::kGemmUp, P.up, s, e->stream); break;
+            case 4: el::launch_gemm(el::kGemmDown, P.down, s, e->stream); break;
+            case 5: el::launch_gemm(el::kGemmLmCheck, P.lm, s, e->stream); break;
+            default: fail(EL_INVALID_ARGUMENT, "unknown kernel kind %d", kind);
+        }
+    };
+    // note: kind 1 rewrites K/V at the current position of `layer` with the same
+    // values the iteration would write (idempotent for timing purposes)
+    one();
+    CK(cudaStreamSynchronize(e->stream));
+    CK(cudaEventRecord(a, e->stream));
+    for (int i = 0; i < reps; ++i) one();
+    CK(cudaEventRecord(b, e->stream));
+    CK(cudaEventSynchronize(b));
+    CK(cudaEventElapsedTime(ms, a, b));
+    *ms /= (float)reps;
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    API_END
+}
+
+int el_sync(el_engine* e) {
+    API_BEGIN
+    CK(cudaStreamSynchronize(e->stream));
+    API_END
+}
+
+int el_launches_per_iteration(el_engine* e, int output_layer) { return e->launches_per_iteration(output_layer); }
+
+int el_plan_info(el_engine* e, int64_t* out, int cap) {
+    API_BEGIN
+    auto& P = e->plans_for(e->in_session ? e->sess_B : e->dm.Bmax);
+    const int64_t v[] = {e->attn_cb,    e->attn_stages,   e->attn_max_chunks, P.n_pad,       P.qkv.splits,
+                         P.wo.splits,   P.up.splits,      P.down.splits,      P.fill.splits, P.qkv.stages,
+                         P.lm.m_tiles,  e->dm.dp,         e->dm.fp,           e->dm.Vp,      e->dm.bpl_max};
+    const int n = (int)(sizeof v / sizeof v[0]);
+    for (int i = 0; i < std::min(n, cap); ++i) out[i] = v[i];
+    return n;
+    API_END
+}
+
+int el_kv_block_trace(int L, int pool, int cap, int n_ops, const int32_t* ops, const int32_t* caps, int n_ids,
+                      int bpl_max, int32_t* tables) {
+    try {
+        if (L <= 0 || pool <= 0 || cap <= 0) fail(EL_INVALID_ARGUMENT, "KvStore: all constructor parameters must be positive");
+        std::vector<int> stack((size_t)pool);
+        for (int i = 0; i < pool; ++i) stack[(size_t)i] = pool - 1 - i;
+        int top = pool;
+        std::vector<std::vector<int>> tab((size_t)n_ids);
+        for (int64_t i = 0; i < (int64_t)n_ids * L * bpl_max; ++i) tables[i] = -1;
+        for (int i = 0; i < n_ops; ++i) {
+            if (ops[i] > 0) {
+                const int id = ops[i] - 1;
+                if (id >= n_ids) fail(EL_INVALID_ARGUMENT, "allocate: id out of range");
+                if (!tab[(size_t)id].empty()) fail(EL_INVALID_ARGUMENT, "allocate: seq_id %d already allocated", id);
+                const int bpl = ceil_div(caps[i], cap);
+                if ((long)bpl * L > top) continue;  // KvOutOfMemory: admission defers
+                std::vector<int> flat((size_t)bpl * L);
+                el::kv_pop_host(stack.data(), top, flat.data(), bpl * L);
+                top -= bpl * L;
+                for (int l = 0; l < L; ++l)
+                    for (int b = 0; b < bpl && b < bpl_max; ++b)
+                        tables[((size_t)id * L + l) * bpl_max + b] = flat[(size_t)l * bpl + b];
+                tab[(size_t)id] = flat;
+                if (flat.empty()) tab[(size_t)id].push_back(-1);
+            } else if (ops[i] < 0) {
+                const int id = -ops[i] - 1;
+                if (id >= n_ids || tab[(size_t)id].empty())
+                    fail(EL_INVALID_ARGUMENT, "release: unknown or already released seq_id %d", id);
+                auto& flat = tab[(size_t)id];
+                if (!(flat.size() == 1 && flat[0] == -1)) {
+                    el::kv_push_host(stack.data(), top, flat.data(), (int)flat.size());
+                    top += (int)flat.size();
+                }
+                flat.clear();
+            }
+        }
+        return top;
+    } catch (const ElError& e) {
+        g_err = e.msg;
+        return -e.code;
+    }
+}
+
+int el_model_tensor(el_engine* e, int which, int layer, uint16_t* out, int64_t cap) {
+    API_BEGIN
+    const int d = e->dm.d, dp = e->dm.dp, fp = e->dm.fp, V = e->dm.V, L = e->dm.L;
+    const uint16_t* base = nullptr;
+    int rows = 0, cols = 0, ld = 0;
+    if (which == 0 || which == 1) {
+        base = which == 0 ? e->emb.p : e->lm.p;
+        rows = V; cols = d; ld = dp;
+    } else if (which == 2 || which == 3) {
+        // probe as fp32 bit patterns split into two uint16 halves: return bf16 bits
+        if (which == 2) {
+            if (cap < d) fail(EL_INVALID_ARGUMENT, "buffer too small");
+            std::vector<float> pw((size_t)dp);
+            CK(cudaMemcpy(pw.data(), e->probe_w.p, sizeof(float) * dp, cudaMemcpyDeviceToHost));
+            for (int i = 0; i < d; ++i) {
+                uint32_t u;
+                std::memcpy(&u, &pw[(size_t)i], 4);
+                out[i] = (uint16_t)(u >> 16);
+            }
+        } else {
+            uint32_t u;
+            std::memcpy(&u, &e->probe_b, 4);
+            out[0] = (uint16_t)(u >> 16);
+        }
+        return EL_OK;
+    } else if (which >= 4 && which <= 9) {
+        if (layer < 1 || layer > L) fail(EL_INVALID_ARGUMENT, "layer out of range");
+        const int k = which - 4, i = layer - 1;
+        switch (k) {
+            case 0: case 1: case 2:
+                base = e->wqkv.p + (size_t)i * 3 * dp * dp + (size_t)k * dp * dp; rows = d; cols = d; ld = dp; break;
+            case 3: base = e->wo.p + (size_t)i * dp * dp; rows = d; cols = d; ld = dp; break;
+            case 4: base = e->wup.p + (size_t)i * fp * dp; rows = 4 * d; cols = d; ld = dp; break;
+            case 5: base = e->wdown.p + (size_t)i * dp * fp; rows = d; cols = 4 * d; ld = fp; break;
+        }
+    } else fail(EL_INVALID_ARGUMENT, "bad tensor id");
+    if (cap < (int64_t)rows * cols) fail(EL_INVALID_ARGUMENT, "buffer too small");
+    CK(cudaMemcpy2D(out, sizeof(uint16_t) * cols, base, sizeof(uint16_t) * ld, sizeof(uint16_t) * cols, rows,
+                    cudaMemcpyDeviceToHost));
+    API_END
+}
+
+}  // extern "C"

@@ -1,0 +1,135 @@
+// el_kernels.h -- host-visible launch interface of the exitlab-b200 kernels.
+//
+// One decode iteration (engine.cpp:208-310) on the device is:
+//   embed -> WHILE(layer loop) { qkv_gemm -> attention -> wo_gemm -> up_gemm ->
+//            down_gemm -> [lm_gemm (softmax check)] -> exit } -> fill_gemm ->
+//   [lm_gemm (greedy)] -> finish
+// Every kernel reads the current layer / output layer from device memory, so the
+// same launches serve the eager path and the CUDA-graph path (WHILE conditional
+// node set from the exit kernel).
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace el {
+
+enum Technique : int { kSoftmax = 0, kState = 1, kClassifier = 2, kNever = 3, kAlwaysAt = 4, kFixed = 5 };
+
+// Model/cache dimensions.  dp = d rounded up to 128 (GEMM M-tile), fp = 4d
+// rounded up to 128, Vp = V rounded up to 128; padding rows/cols are zero.
+struct Dims {
+    int L, d, dp, fp, V, Vp;
+    int bc;       // KV block capacity (positions per block)
+    int bpl_max;  // max blocks per (seq, layer) in the device block tables
+    int Bmax;     // max rows (max_batch)
+    int slots;    // sequence slots in the device block tables
+};
+
+// Rows of the current iteration (decode batch or prefill batch).
+struct Rows {
+    const int* slot;  // [Bmax] sequence slot of each row
+    int* pos;         // [Bmax] committed length = position written this iteration
+    int* tok;         // [Bmax] input token of this iteration
+    int B;
+};
+
+// All device pointers of one engine.  POD, passed by value to every kernel.
+struct DevState {
+    Dims dm;
+    // weights (bf16 bit patterns), packed per layer
+    const uint16_t* wqkv;   // [L][3dp][dp]  rows q | k | v
+    const uint16_t* wo;     // [L][dp][dp]
+    const uint16_t* wup;    // [L][fp][dp]
+    const uint16_t* wdown;  // [L][dp][fp]
+    const uint16_t* emb;    // [Vp][dp]
+    const uint16_t* lm;     // [Vp][dp]
+    const float* probe_w;   // [dp]
+    float probe_b;
+    // paged KV pool
+    uint16_t* kpool;        // [pool][bc][dp]
+    uint16_t* vpool;
+    const int* tables;      // [slots][L][bpl_max]
+    Rows rows;
+    // activations
+    float* h32;       // [2][Bmax][dp]  residual stream, parity = layer & 1
+    uint16_t* hb;     // [2][Bmax][dp]  bf16 copy (GEMM B operand)
+    float* q32;       // [Bmax][dp]
+    uint16_t* att_b;  // [Bmax][dp]
+    float* mid32;     // [Bmax][dp]
+    uint16_t* mid_b;  // [Bmax][dp]
+    uint16_t* up_b;   // [Bmax][fp]
+    // attention split-context workspace
+    float* attn_o;    // [Bmax][attn_max_chunks][dp]
+    float* attn_ml;   // [Bmax][attn_max_chunks][2]
+    int* attn_cnt;    // [Bmax]
+    int attn_max_chunks;
+    int attn_cb;      // blocks per chunk
+    int attn_stages;
+    float attn_scale; // 1/sqrt(d)
+    // split-K GEMM workspace
+    float* gemm_ws;
+    int* gemm_cnt;
+    // LM-head per-tile partials [Vp/128][Bmax] {max1, max2, sumexp(rel max1), argmax}
+    float4* lm_part;
+    // exit status (Algorithm 1 "Status")
+    int* layer;              // current layer (1-based), advanced by the exit kernel
+    int* out_layer;          // output_layer of the iteration
+    int* status;             // [Bmax] OR-latched accept
+    int* first_accept;       // [Bmax] 0 = never
+    int* accept;             // [Bmax] this layer's decision
+    float* conf;             // [L][Bmax] this iteration's confidences
+    int* exit_cnt;
+    int* cont_host;          // mapped host flag (eager path reads it)
+    const double* lambdas;   // [L] threshold_at(schedule, layer)
+    const float* fixed_conf; // [L][Bmax] injected confidences (technique kFixed)
+    int technique, exit_layer;
+    cudaGraphConditionalHandle cond;
+    int use_cond;
+    // per-iteration records (ring)
+    int* iter_counter;
+    int* cur_iter;
+    int* rec_tok;     // [rec_cap][Bmax]
+    int* rec_acc;     // [rec_cap][Bmax]
+    int* rec_out;     // [rec_cap]
+    float* rec_conf;  // [rec_cap][L][Bmax]
+    int rec_cap;
+};
+
+// one split-K weight-streaming GEMM launch: D[M x N] = W[M x K] . X[N x K]^T
+struct GemmPlan {
+    CUtensorMap tmA;  // weights, box [128 rows][64 k]
+    CUtensorMap tmB;  // activations, box [n_pad rows][64 k]
+    int m_tiles, splits, kb_per_split, n_pad, stages, smem_bytes, tmem_cols;
+};
+
+enum GemmKind : int { kGemmQkv = 0, kGemmWo, kGemmUp, kGemmDown, kGemmLmCheck, kGemmLmFinal, kGemmFill };
+
+int gemm_smem_bytes(int n_pad, int stages, bool tile_reduce);
+void init_kernel_attributes();
+void launch_gemm(GemmKind kind, const GemmPlan& p, const DevState& st, cudaStream_t s);
+
+void launch_weightgen(uint16_t* out, int rows, int cols, int rows_p, int cols_p, uint64_t seed, double scale,
+                      cudaStream_t s);
+void launch_kv_prefix(const DevState& st, const int* row_seq_ids, int prefix_len, uint64_t kv_seed, int round_bf16,
+                      cudaStream_t s);
+void launch_embed(const DevState& st, cudaStream_t s);
+int attn_smem_bytes(const Dims& dm, int stages);
+void launch_attention(const DevState& st, cudaStream_t s);
+void launch_exit(const DevState& st, cudaStream_t s);
+void launch_finish(const DevState& st, cudaStream_t s);
+void launch_advance(const DevState& st, cudaStream_t s);  // prefill commit: pos += 1
+// LIFO block allocator on the device (kv_cache.cpp:78-106, 182-194)
+void launch_kv_alloc(int* stack, int top, int* tables, const Dims& dm, int slot, int bpl, cudaStream_t s);
+void launch_kv_release(int* stack, int top, const int* tables, const Dims& dm, int slot, int bpl, cudaStream_t s);
+
+// host+device mirror of the allocator arithmetic (used by el_kv_block_trace)
+inline void kv_pop_host(const int* stack, int top, int* table_flat, int n) {
+    for (int i = 0; i < n; ++i) table_flat[i] = stack[top - 1 - i];
+}
+inline void kv_push_host(int* stack, int top, const int* table_flat, int n) {
+    for (int i = 0; i < n; ++i) stack[top + i] = table_flat[i];
+}
+
+}  // namespace el

@@ -1,0 +1,475 @@
+"""Python mirror of the reference's engine / exit-policy API over the C ABI.
+
+Names, argument meaning and error behaviour follow the reference
+(/root/reference/proj/include/exitlab):
+
+* ``ModelConfig``, ``ThresholdSchedule``, ``CostModel``, ``EngineConfig``  (model.hpp:18-25,
+  exit_policy.hpp:36-42, engine.hpp:18-42)
+* ``ExitTechnique.softmax_response() / state_similarity() / classifier() / never() /
+  always_at(k)`` and ``technique_from_name`` (exit_policy.hpp:14-31)
+* ``Engine(config).run(workload) -> Transcript``  (engine.hpp:131-147)
+* errors: ``ValueError`` = std::invalid_argument, ``KvOutOfMemory`` (a RuntimeError) =
+  exitlab::KvOutOfMemory, ``RuntimeError`` = std::runtime_error, ``LogicError`` = std::logic_error
+
+Every compute call goes to libexitlab_b200.so on the GPU; nothing here computes.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from .build import LIB
+
+EL_OK, EL_INVALID_ARGUMENT, EL_RUNTIME_ERROR, EL_KV_OUT_OF_MEMORY, EL_LOGIC_ERROR, EL_CUDA_ERROR = 0, 1, 2, 3, 4, 6
+TECH = {"softmax": 0, "state": 1, "classifier": 2, "never": 3, "always_at": 4, "fixed": 5}
+
+
+class KvOutOfMemory(RuntimeError):
+    """exitlab::KvOutOfMemory (kv_cache.hpp:101-103)."""
+
+
+class LogicError(RuntimeError):
+    """std::logic_error (e.g. decode_iteration on an empty batch)."""
+
+
+class CudaError(RuntimeError):
+    """Device failure (no reference counterpart)."""
+
+
+_lib = None
+
+
+def lib():
+    """Load the in-tree library; raise (never fall back) when it is missing."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB):
+            raise ImportError(f"exitlab-b200 CUDA library not built: {LIB} (run __graft_entry__.build())")
+        L = C.CDLL(LIB)
+        L.el_last_error.restype = C.c_char_p
+        L.el_engine_create.argtypes = [C.c_void_p, C.POINTER(C.c_void_p)]
+        L.el_engine_destroy.argtypes = [C.c_void_p]
+        L.el_engine_set_option.argtypes = [C.c_void_p, C.c_char_p, C.c_int64]
+        L.el_engine_run.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                    C.POINTER(C.c_void_p)]
+        L.el_transcript_len.restype = C.c_int64
+        L.el_transcript_len.argtypes = [C.c_void_p, C.c_char_p]
+        L.el_transcript_get_i32.argtypes = [C.c_void_p, C.c_char_p, C.c_void_p]
+        L.el_transcript_get_f64.argtypes = [C.c_void_p, C.c_char_p, C.c_void_p]
+        L.el_transcript_kv.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_int64]
+        L.el_transcript_exit_states.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_int64]
+        L.el_transcript_free.argtypes = [C.c_void_p]
+        L.el_transcript_free.restype = None
+        L.el_session_begin.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_int, C.c_uint64, C.c_void_p]
+        L.el_session_end.argtypes = [C.c_void_p]
+        L.el_decode_iteration.argtypes = [C.c_void_p] + [C.c_void_p] * 5
+        L.el_decode_run.argtypes = [C.c_void_p, C.c_int]
+        L.el_decode_records.argtypes = [C.c_void_p, C.c_int, C.c_int] + [C.c_void_p] * 4
+        L.el_decode_iterations_done.argtypes = [C.c_void_p]
+        L.el_set_fixed_confidences.argtypes = [C.c_void_p, C.c_void_p]
+        L.el_session_kv.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p]
+        L.el_session_hidden.argtypes = [C.c_void_p, C.c_int, C.c_void_p]
+        L.el_session_block_table.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_int]
+        L.el_time_decode.argtypes = [C.c_void_p, C.c_int, C.POINTER(C.c_float)]
+        L.el_time_kernel.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_float)]
+        L.el_sync.argtypes = [C.c_void_p]
+        L.el_launches_per_iteration.argtypes = [C.c_void_p, C.c_int]
+        L.el_plan_info.argtypes = [C.c_void_p, C.c_void_p, C.c_int]
+        L.el_kv_block_trace.argtypes = [C.c_int] * 4 + [C.c_void_p] * 2 + [C.c_int, C.c_int, C.c_void_p]
+        L.el_model_tensor.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_int64]
+        _lib = L
+    return _lib
+
+
+def _check(rc: int):
+    if rc == EL_OK:
+        return
+    msg = lib().el_last_error().decode()
+    if rc == EL_INVALID_ARGUMENT:
+        raise ValueError(msg)
+    if rc == EL_KV_OUT_OF_MEMORY:
+        raise KvOutOfMemory(msg)
+    if rc == EL_LOGIC_ERROR:
+        raise LogicError(msg)
+    if rc == EL_CUDA_ERROR:
+        raise CudaError(msg)
+    raise RuntimeError(msg)
+
+
+def _ptr(a):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+# ---------------------------------------------------------------- config types
+@dataclass
+class ModelConfig:  # model.hpp:18-25
+    n_layers: int = 8
+    d_model: int = 64
+    vocab_size: int = 256
+    seed: int = 0
+
+
+@dataclass
+class ExitTechnique:  # exit_policy.hpp:14-31
+    kind: str = "never"
+    exit_layer: int = 1
+
+    @staticmethod
+    def softmax_response():
+        return ExitTechnique("softmax")
+
+    @staticmethod
+    def state_similarity():
+        return ExitTechnique("state")
+
+    @staticmethod
+    def classifier():
+        return ExitTechnique("classifier")
+
+    @staticmethod
+    def never():
+        return ExitTechnique("never")
+
+    @staticmethod
+    def always_at(layer: int):
+        return ExitTechnique("always_at", layer)
+
+    @staticmethod
+    def fixed():
+        """test harness: injected confidences (el_set_fixed_confidences)."""
+        return ExitTechnique("fixed")
+
+    @property
+    def name(self) -> str:  # technique_name (exit_policy.cpp:8-18)
+        return f"always-at={self.exit_layer}" if self.kind == "always_at" else self.kind
+
+
+def technique_from_name(name: str) -> ExitTechnique:  # exit_policy.cpp:20-36
+    if name in ("softmax", "state", "classifier", "never"):
+        return ExitTechnique(name)
+    if name.startswith("always-at="):
+        arg = name[len("always-at="):]
+        if not arg.isdigit():
+            raise ValueError(f"technique: bad layer in '{name}'")
+        if int(arg) < 1:
+            raise ValueError("technique: always-at layer must be >= 1")
+        return ExitTechnique.always_at(int(arg))
+    raise ValueError(f"technique: unknown name '{name}' (expected softmax|state|classifier|never|always-at=K)")
+
+
+@dataclass
+class ThresholdSchedule:  # exit_policy.hpp:36-42
+    lambda0: float = 0.85
+    gamma: float = 1.0
+    lambda_min: float = 0.0
+
+
+@dataclass
+class CostModel:  # engine.hpp:18-28
+    c_layer_fixed: float = 1e-3
+    c_layer_per_seq: float = 1e-4
+    c_fill_per_seq_layer: float = 2e-5
+    c_check_softmax: float = 5e-5
+    c_check_classifier: float = 5e-5
+    c_check_state: float = 1e-5
+
+
+@dataclass
+class EngineConfig:  # engine.hpp:30-42
+    model: ModelConfig = field(default_factory=ModelConfig)
+    technique: ExitTechnique = field(default_factory=ExitTechnique.never)
+    schedule: ThresholdSchedule = field(default_factory=ThresholdSchedule)
+    costs: CostModel = field(default_factory=CostModel)
+    max_batch: int = 8
+    pool_blocks: int = 4096
+    block_capacity: int = 16
+    eos_token: int = 0
+    capture_kv: bool = False
+    synthetic_kv_seed: int = -1
+
+
+class _CConfig(C.Structure):
+    """el_engine_config (include/exitlab_b200.h); same layout as the oracle's."""
+    _fields_ = [("n_layers", C.c_int), ("d_model", C.c_int), ("vocab_size", C.c_int),
+                ("model_seed", C.c_uint64), ("technique", C.c_int), ("exit_layer", C.c_int),
+                ("lambda0", C.c_double), ("gamma", C.c_double), ("lambda_min", C.c_double),
+                ("c_layer_fixed", C.c_double), ("c_layer_per_seq", C.c_double),
+                ("c_fill_per_seq_layer", C.c_double), ("c_check_softmax", C.c_double),
+                ("c_check_classifier", C.c_double), ("c_check_state", C.c_double),
+                ("max_batch", C.c_int), ("pool_blocks", C.c_int), ("block_capacity", C.c_int),
+                ("eos_token", C.c_int), ("capture_kv", C.c_int), ("round_bf16", C.c_int),
+                ("synthetic_kv_seed", C.c_int64)]
+
+
+def to_c_config(cfg: EngineConfig) -> _CConfig:
+    c = _CConfig()
+    c.n_layers, c.d_model, c.vocab_size = cfg.model.n_layers, cfg.model.d_model, cfg.model.vocab_size
+    c.model_seed = cfg.model.seed
+    c.technique = TECH[cfg.technique.kind]
+    c.exit_layer = cfg.technique.exit_layer
+    c.lambda0, c.gamma, c.lambda_min = cfg.schedule.lambda0, cfg.schedule.gamma, cfg.schedule.lambda_min
+    for k in ("c_layer_fixed", "c_layer_per_seq", "c_fill_per_seq_layer", "c_check_softmax",
+              "c_check_classifier", "c_check_state"):
+        setattr(c, k, getattr(cfg.costs, k))
+    c.max_batch, c.pool_blocks, c.block_capacity, c.eos_token = (cfg.max_batch, cfg.pool_blocks,
+                                                                  cfg.block_capacity, cfg.eos_token)
+    c.capture_kv = int(cfg.capture_kv)
+    c.round_bf16 = 1
+    c.synthetic_kv_seed = cfg.synthetic_kv_seed
+    return c
+
+
+# ---------------------------------------------------------------- workload
+@dataclass
+class Request:  # workload.hpp:10-14
+    arrival_time: float
+    prompt: list
+    max_new_tokens: int = 1
+
+
+@dataclass
+class Workload:
+    requests: list = field(default_factory=list)
+
+    def flat(self):
+        n = len(self.requests)
+        arrival = np.array([r.arrival_time for r in self.requests], dtype=np.float64)
+        off = np.zeros(n + 1, dtype=np.int32)
+        toks = []
+        for i, r in enumerate(self.requests):
+            toks.extend(int(t) for t in r.prompt)
+            off[i + 1] = len(toks)
+        return (arrival, off, np.array(toks, dtype=np.int32),
+                np.array([r.max_new_tokens for r in self.requests], dtype=np.int32))
+
+    @staticmethod
+    def from_flat(arrival, off, prompt, max_new):
+        return Workload([Request(float(arrival[i]), prompt[off[i]:off[i + 1]].tolist(), int(max_new[i]))
+                         for i in range(len(arrival))])
+
+
+# ---------------------------------------------------------------- transcript
+I32_FIELDS = ["pf_seq", "pf_positions", "it_output_layer", "it_batch_off", "ps_seq", "ps_accept",
+              "ps_token", "sq_id", "sq_max_new", "sq_prompt_off", "sq_prompt", "sq_tok_off",
+              "sq_tokens", "sq_exit_layers", "sq_iter_out"]
+F64_FIELDS = ["pf_clock", "pf_charge", "it_clock", "it_charge", "sq_arrival", "sq_first",
+              "sq_finish", "meta", "it_conf"]
+
+
+class Transcript:
+    """Flat transcript (engine.hpp:67-123), fields identical to the oracle's."""
+
+    def __init__(self, handle, d, L):
+        L_ = lib()
+        self.f = {}
+        for name in I32_FIELDS:
+            n = L_.el_transcript_len(handle, name.encode())
+            a = np.zeros(max(n, 0), dtype=np.int32)
+            if n > 0:
+                _check(L_.el_transcript_get_i32(handle, name.encode(), _ptr(a)))
+            self.f[name] = a
+        for name in F64_FIELDS:
+            n = L_.el_transcript_len(handle, name.encode())
+            a = np.zeros(max(n, 0), dtype=np.float64)
+            if n > 0:
+                _check(L_.el_transcript_get_f64(handle, name.encode(), _ptr(a)))
+            self.f[name] = a
+        self._h = handle
+        self.d, self.L = d, L
+
+    def __del__(self):
+        try:
+            if self._h:
+                lib().el_transcript_free(self._h)
+        except Exception:
+            pass
+
+    def __getitem__(self, k):
+        return self.f[k]
+
+    @property
+    def final_clock(self):
+        return float(self.f["meta"][0])
+
+    @property
+    def iterations(self):
+        off = self.f["it_batch_off"]
+        return [dict(clock=self.f["it_clock"][i], charge=self.f["it_charge"][i],
+                     output_layer=int(self.f["it_output_layer"][i]),
+                     batch_ids=self.f["ps_seq"][off[i]:off[i + 1]].tolist(),
+                     accept=self.f["ps_accept"][off[i]:off[i + 1]].tolist(),
+                     tokens=self.f["ps_token"][off[i]:off[i + 1]].tolist())
+                for i in range(len(self.f["it_output_layer"]))]
+
+    @property
+    def sequences(self):
+        po, to = self.f["sq_prompt_off"], self.f["sq_tok_off"]
+        return [dict(id=int(self.f["sq_id"][i]), arrival=self.f["sq_arrival"][i],
+                     first_token=self.f["sq_first"][i], finish=self.f["sq_finish"][i],
+                     max_new=int(self.f["sq_max_new"][i]),
+                     prompt=self.f["sq_prompt"][po[i]:po[i + 1]].tolist(),
+                     tokens=self.f["sq_tokens"][to[i]:to[i + 1]].tolist(),
+                     exit_layers=self.f["sq_exit_layers"][to[i]:to[i + 1]].tolist(),
+                     iter_output_layers=self.f["sq_iter_out"][to[i]:to[i + 1]].tolist())
+                for i in range(len(self.f["sq_id"]))]
+
+    def kv(self, seq_id, layer):
+        n = 1 << 22
+        k = np.zeros(n)
+        v = np.zeros(n)
+        c = lib().el_transcript_kv(self._h, seq_id, layer, _ptr(k), _ptr(v), n)
+        if c < 0:
+            _check(-c)
+        return k[: c * self.d].reshape(c, self.d), v[: c * self.d].reshape(c, self.d)
+
+    def exit_states(self, seq_id):
+        n = 1 << 22
+        o = np.zeros(n)
+        c = lib().el_transcript_exit_states(self._h, seq_id, _ptr(o), n)
+        if c < 0:
+            _check(-c)
+        return o[: c * self.d].reshape(c, self.d)
+
+
+# ---------------------------------------------------------------- engine
+class Engine:
+    """exitlab::Engine on one B200 (engine.hpp:131-147). Weights are seeded from
+    config.model (ModelWeights::seeded, model.cpp:37-59) and stored as bf16."""
+
+    def __init__(self, config: EngineConfig, graph: bool = True):
+        self.config = config
+        self._c = to_c_config(config)
+        h = C.c_void_p()
+        _check(lib().el_engine_create(C.byref(self._c), C.byref(h)))
+        self._h = h
+        self.L, self.d, self.V = config.model.n_layers, config.model.d_model, config.model.vocab_size
+        self.B = 0
+        self.set_option("graph", int(graph))
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().el_engine_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_option(self, key: str, value: int):
+        _check(lib().el_engine_set_option(self._h, key.encode(), int(value)))
+
+    def run(self, workload: Workload) -> Transcript:  # Engine::run (engine.cpp:110-330)
+        arrival, off, prompt, max_new = workload.flat()
+        t = C.c_void_p()
+        _check(lib().el_engine_run(self._h, len(arrival), _ptr(arrival), _ptr(off), _ptr(prompt),
+                                   _ptr(max_new), C.byref(t)))
+        return Transcript(t, self.d, self.L)
+
+    # ---- fixed-batch decode session over a seeded KV prefix ----
+    def session_begin(self, first_tokens, prefix_len, capacity, kv_seed, seq_ids=None):
+        ft = np.ascontiguousarray(first_tokens, dtype=np.int32)
+        ids = None if seq_ids is None else np.ascontiguousarray(seq_ids, dtype=np.int32)
+        _check(lib().el_session_begin(self._h, len(ft), _ptr(ft), prefix_len, capacity, kv_seed, _ptr(ids)))
+        self.B = len(ft)
+
+    def session_end(self):
+        _check(lib().el_session_end(self._h))
+
+    def decode_iteration(self, tokens_in=None):
+        """decode_iteration (engine.cpp:208-310) with host buffers in and out."""
+        B, L = self.B, self.L
+        tin = None if tokens_in is None else np.ascontiguousarray(tokens_in, dtype=np.int32)
+        tok = np.zeros(B, np.int32)
+        acc = np.zeros(B, np.int32)
+        conf = np.zeros((L, B), np.float32)
+        e = np.zeros(1, np.int32)
+        _check(lib().el_decode_iteration(self._h, _ptr(tin), _ptr(tok), _ptr(acc), _ptr(conf), _ptr(e)))
+        return dict(output_layer=int(e[0]), tokens=tok, accept=acc, conf=conf)
+
+    def decode_run(self, n):
+        _check(lib().el_decode_run(self._h, n))
+
+    def records(self, first, n):
+        B, L = self.B, self.L
+        tok = np.zeros((n, B), np.int32)
+        acc = np.zeros((n, B), np.int32)
+        out = np.zeros(n, np.int32)
+        conf = np.zeros((n, L, B), np.float32)
+        _check(lib().el_decode_records(self._h, first, n, _ptr(tok), _ptr(acc), _ptr(out), _ptr(conf)))
+        return dict(tokens=tok, accept=acc, output_layer=out, conf=conf)
+
+    def set_fixed_confidences(self, conf):
+        c = np.ascontiguousarray(conf, dtype=np.float32)
+        _check(lib().el_set_fixed_confidences(self._h, _ptr(c)))
+
+    def kv(self, row, layer, pos):
+        k = np.zeros(self.d, np.float32)
+        v = np.zeros(self.d, np.float32)
+        _check(lib().el_session_kv(self._h, row, layer, pos, _ptr(k), _ptr(v)))
+        return k, v
+
+    def hidden(self, parity):
+        out = np.zeros((self.B, self.d), np.float32)
+        _check(lib().el_session_hidden(self._h, parity, _ptr(out)))
+        return out
+
+    def block_table(self, row, bpl_cap=4096):
+        out = np.zeros(self.L * bpl_cap, np.int32)
+        n = lib().el_session_block_table(self._h, row, _ptr(out), bpl_cap)
+        if n < 0:
+            _check(-n)
+        return out[: self.L * n].reshape(self.L, n)
+
+    def time_decode(self, n):
+        ms = C.c_float()
+        _check(lib().el_time_decode(self._h, n, C.byref(ms)))
+        return ms.value
+
+    def time_kernel(self, kind, layer, reps):
+        ms = C.c_float()
+        _check(lib().el_time_kernel(self._h, kind, layer, reps, C.byref(ms)))
+        return ms.value
+
+    def sync(self):
+        _check(lib().el_sync(self._h))
+
+    def launches_per_iteration(self, output_layer):
+        return lib().el_launches_per_iteration(self._h, output_layer)
+
+    def plan_info(self):
+        out = np.zeros(32, np.int64)
+        n = lib().el_plan_info(self._h, _ptr(out), 32)
+        names = ["attn_cb", "attn_stages", "attn_max_chunks", "n_pad", "qkv_splits", "wo_splits", "up_splits",
+                 "down_splits", "fill_splits", "qkv_stages", "lm_tiles", "dp", "fp", "Vp", "bpl_max"]
+        return dict(zip(names, out[:n].tolist()))
+
+    def model_tensor(self, which, layer=0):
+        names = {"embedding": 0, "lm_head": 1, "probe_w": 2, "probe_b": 3, "w_q": 4, "w_k": 5, "w_v": 6,
+                 "w_o": 7, "w_up": 8, "w_down": 9}
+        w = names[which] if isinstance(which, str) else which
+        d, V = self.d, self.V
+        shape = {0: (V, d), 1: (V, d), 2: (d,), 3: (1,), 4: (d, d), 5: (d, d), 6: (d, d), 7: (d, d),
+                 8: (4 * d, d), 9: (d, 4 * d)}[w]
+        out = np.zeros(int(np.prod(shape)), np.uint16)
+        _check(lib().el_model_tensor(self._h, w, layer, _ptr(out), out.size))
+        return out.reshape(shape)
+
+
+def bf16_to_f64(bits: np.ndarray) -> np.ndarray:
+    return (bits.astype(np.uint32) << 16).view(np.float32).astype(np.float64)
+
+
+def kv_block_trace(n_layers, pool, cap, ops, caps, n_ids, bpl_max):
+    """KvStore LIFO allocation order on the host mirror (kv_cache.cpp:53-55, 78-106, 182-194)."""
+    ops = np.ascontiguousarray(ops, dtype=np.int32)
+    caps = np.ascontiguousarray(caps, dtype=np.int32)
+    tab = np.zeros((n_ids, n_layers, bpl_max), np.int32)
+    nf = lib().el_kv_block_trace(n_layers, pool, cap, len(ops), _ptr(ops), _ptr(caps), n_ids, bpl_max, _ptr(tab))
+    if nf < 0:
+        _check(-nf)
+    return tab, nf
