@@ -118,6 +118,8 @@ int el_time_decode(el_engine* e, int n_iters, float* ms);
  * 1 qkv gemm, 2 wo, 3 up, 4 down, 5 lm head; layer fixed; reps launches */
 int el_time_kernel(el_engine* e, int kind, int layer, int reps, float* ms);
 int el_sync(el_engine* e);
+/* experiment support: per-CTA phase timestamps (option "dbg" bit 8) */
+int el_debug_timestamps(el_engine* e, uint64_t* out, int n);
 /* kernels launched per iteration with the given output layer (for gpu_launches) */
 int el_launches_per_iteration(el_engine* e, int output_layer);
 /* plan details: attention chunking, GEMM splits (for DESIGN / bench reporting) */

@@ -386,17 +386,22 @@ class Session:
         except Exception:
             pass
 
-    def step(self, forced=0, fixed_conf=None):
+    def step(self, forced=0, fixed_conf=None, tokens_in=None):
+        """One decode iteration. forced>0 replays a recorded output layer;
+        tokens_in overrides the inputs (teacher forcing from another engine)."""
         B, L, d = self.B, self.m.L, self.m.d
         toks = np.zeros(B, np.int32); acc = np.zeros(B, np.int32)
         conf = np.zeros((L, B)); hx = np.zeros((B, d))
+        tin = np.ascontiguousarray(tokens_in, dtype=np.int32) if tokens_in is not None else None
         lib = self.m.lib
         if lib.prefix == "eo_":
             fc = np.ascontiguousarray(fixed_conf, dtype=np.float64) if fixed_conf is not None else None
-            e = lib.fn("session_step")(self.h, forced, _p(fc, C.c_double), _p(toks, C.c_int32), _p(acc, C.c_int32),
-                                       _p(conf, C.c_double), _p(hx, C.c_double))
+            e = lib.fn("session_step")(self.h, forced, _p(fc, C.c_double), _p(tin, C.c_int32), _p(toks, C.c_int32),
+                                       _p(acc, C.c_int32), _p(conf, C.c_double), _p(hx, C.c_double))
         else:
-            e = lib.fn("session_step")(self.h, forced, _p(toks, C.c_int32), _p(acc, C.c_int32),
+            if fixed_conf is not None:
+                raise ValueError("the reference session has no injected-confidence mode")
+            e = lib.fn("session_step")(self.h, forced, _p(tin, C.c_int32), _p(toks, C.c_int32), _p(acc, C.c_int32),
                                        _p(conf, C.c_double), _p(hx, C.c_double))
         if e < 0:
             raise RuntimeError(lib.err())
@@ -423,7 +428,8 @@ class Port(_Lib):
                                     C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.POINTER(C.c_int32),
                                     C.POINTER(C.c_double), C.c_int, C.POINTER(C.c_void_p)]
         L.eo_session_step.argtypes = [C.c_void_p, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_int32),
-                                      C.POINTER(C.c_int32), C.POINTER(C.c_double), C.POINTER(C.c_double)]
+                                      C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.POINTER(C.c_double),
+                                      C.POINTER(C.c_double)]
         L.eo_round_bf16.restype = C.c_double
         L.eo_round_bf16.argtypes = [C.c_double]
         L.eo_splitmix64_at.restype = C.c_uint64
@@ -463,7 +469,7 @@ class Ref(_Lib):
                                      C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.POINTER(C.c_int32),
                                      C.POINTER(C.c_void_p)]
         L.ref_session_step.argtypes = [C.c_void_p, C.c_int, C.POINTER(C.c_int32), C.POINTER(C.c_int32),
-                                       C.POINTER(C.c_double), C.POINTER(C.c_double)]
+                                       C.POINTER(C.c_int32), C.POINTER(C.c_double), C.POINTER(C.c_double)]
         L.ref_greedy_token.argtypes = [C.POINTER(C.c_double), C.c_int]
 
     def engine_run(self, model, cfg, wl: Workload, fixed_conf=None) -> Transcript:

@@ -1025,11 +1025,12 @@ void eo_session_free(eo_session* s) {
     free(s);
 }
 
-int eo_session_step(eo_session* s, int forced, const double* fixed_conf, int32_t* tokens, int32_t* accept,
-                    double* conf, double* h_exit) {
+int eo_session_step(eo_session* s, int forced, const double* fixed_conf, const int32_t* tokens_in,
+                    int32_t* tokens, int32_t* accept, double* conf, double* h_exit) {
     const eo_model* m = s->m;
     const eo_engine_config* c = &s->cfg;
     const int L = c->n_layers, d = c->d_model, B = s->B;
+    if (tokens_in) for (int b = 0; b < B; ++b) s->next_input[b] = tokens_in[b];
     for (int b = 0; b < B; ++b)
         memcpy(s->states + (size_t)b * d, m->emb + (size_t)s->next_input[b] * d, sizeof(double) * (size_t)d);
     unsigned char* status = (unsigned char*)calloc((size_t)B, 1);

@@ -151,10 +151,12 @@ eo_session* eo_session_create(const eo_model* m, const eo_engine_config* cfg, in
                               uint64_t kv_seed, const int32_t* seq_ids);
 void eo_session_free(eo_session* s);
 /* one iteration; forced_output_layer>0 overrides the exit decision (replay).
+ * tokens_in (may be null) overrides the inputs (teacher forcing).
  * outputs: tokens[B], accept[B], conf[L][B] (NaN when not computed), h_exit[B][d];
  * returns the output layer (<0 on error). */
 int eo_session_step(eo_session* s, int forced_output_layer, const double* fixed_conf,
-                    int32_t* tokens, int32_t* accept, double* conf, double* h_exit);
+                    const int32_t* tokens_in, int32_t* tokens, int32_t* accept, double* conf,
+                    double* h_exit);
 /* copy K/V at (row, layer, position) */
 int eo_session_kv(const eo_session* s, int row, int layer, int position, double* k, double* v);
 

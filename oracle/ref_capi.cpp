@@ -489,10 +489,12 @@ void ref_session_free(void* s) { delete static_cast<Session*>(s); }
 // decode_iteration (engine.cpp:208-310) restated over the reference's public
 // functions; forced>0 ends the layer loop at that layer (replay of a recorded
 // output layer), otherwise the status vector decides.
-int ref_session_step(void* sp, int forced, int32_t* tokens, int32_t* accept, double* conf,
-                     double* h_exit) {
+int ref_session_step(void* sp, int forced, const int32_t* tokens_in, int32_t* tokens, int32_t* accept,
+                     double* conf, double* h_exit) {
     try {
         auto* s = static_cast<Session*>(sp);
+        if (tokens_in)
+            for (size_t b = 0; b < s->ids.size(); ++b) s->next_input[b] = tokens_in[b];
         const ModelWeights& w = *s->w;
         const int L = s->cfg.n_layers, d = s->cfg.d_model, B = (int)s->ids.size();
         const ExitTechnique& technique = s->ec.technique;

@@ -142,6 +142,8 @@ struct el_engine {
     cudaStream_t stream = nullptr;
     int device = 0;
     bool use_graph = true;
+    bool pdl = true;
+    int dbg = 0;
     int rec_cap = 4096;
 
     // weights
@@ -156,12 +158,13 @@ struct el_engine {
     // rows
     DevBuf<int> row_slot, row_pos, row_tok, pf_slot, pf_pos, pf_tok, seq_ids_dev;
     // activations / workspaces
-    DevBuf<float> h32, q32, mid32, attn_o, attn_ml, gemm_ws, conf, rec_conf;
+    DevBuf<float> h32, q32, mid32, attn_o, attn_ml, conf, rec_conf;
     DevBuf<uint16_t> hb, att_b, mid_b, up_b;
-    DevBuf<int> attn_cnt, gemm_cnt, layer, out_layer, status, first_accept, accept, exit_cnt, iter_counter,
+    DevBuf<int> attn_cnt, attn_queue, layer, out_layer, status, first_accept, accept, exit_cnt, iter_counter,
         cur_iter, rec_tok, rec_acc, rec_out;
     DevBuf<float4> lm_part;
     DevBuf<double> lambdas;
+    DevBuf<unsigned long long> dbg_ts;
     DevBuf<float> fixed_conf;
     int* cont_host = nullptr;
     int* cont_dev = nullptr;
@@ -173,7 +176,7 @@ struct el_engine {
         int n_pad = 0;
     };
     std::map<int, Plans> plans;  // by n_pad
-    int attn_cb = 1, attn_stages = 2, attn_max_chunks = 1;
+    int attn_cb = 1, attn_stages = 2, attn_max_chunks = 1, attn_grid = 148;
 
     // graphs by batch size
     struct Graph {
@@ -306,7 +309,9 @@ struct el_engine {
         mid_b.alloc((size_t)Bm * dp);
         up_b.alloc((size_t)Bm * fp);
         attn_cnt.alloc((size_t)Bm);
+        attn_queue.alloc(4);
         lm_part.alloc((size_t)(dm.Vp / 128) * Bm);
+        dbg_ts.alloc(65536);
         for (DevBuf<int>* b : {&layer, &out_layer, &exit_cnt, &iter_counter, &cur_iter}) b->alloc(4);
         status.alloc((size_t)Bm);
         first_accept.alloc((size_t)Bm);
@@ -355,14 +360,28 @@ struct el_engine {
             if (b) fail(EL_LOGIC_ERROR, "block tables cannot grow while sequences are live");
         dm.bpl_max = bpl;
         tables.alloc((size_t)dm.slots * dm.L * bpl);
+        plan_attention();
+        invalidate_graphs();
+    }
+
+    // attention split: ~4 CTAs per SM worth of (sequence, chunk) work items; a
+    // ring of stages sized so two CTAs fit per SM when the block pair allows it
+    int opt_attn_cb = 0, opt_attn_stages = 0, opt_splits_cap = 8;
+    void plan_attention() {
+        const int bpl = std::max(1, dm.bpl_max);
         const int B = dm.Bmax;
-        const int target_chunks = std::max(1, ceil_div(148 * 4, B));
-        attn_cb = std::max(1, ceil_div(bpl, target_chunks));
+        // items of ~4 blocks keep the queue balanced; the persistent producer
+        // streams across item boundaries, so short items cost no pipeline drain
+        attn_cb = opt_attn_cb ? opt_attn_cb : std::max(1, std::min(16, ceil_div(bpl * B, 148 * 2)));
+        attn_cb = std::min(std::max(attn_cb, ceil_div(bpl, 128)), 32);
         attn_max_chunks = ceil_div(bpl, attn_cb);
-        const int stage_bytes = 2 * dm.bc * dm.dp * 2;
-        attn_stages = std::min(std::max(2, (200 * 1024) / stage_bytes), 4);
-        attn_stages = std::min(attn_stages, std::max(1, attn_cb));
+        const int stage_bytes = el::attn_stage_bytes(dm);
+        // one persistent CTA per SM with as many block stages as shared memory holds
+        attn_stages = opt_attn_stages ? opt_attn_stages : std::min(8, std::max(2, (224 * 1024) / stage_bytes));
         while (attn_stages > 1 && el::attn_smem_bytes(dm, attn_stages) > 227 * 1024) --attn_stages;
+        int sms = 148;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+        attn_grid = sms * el::attn_ctas_per_sm(dm, attn_stages);
         attn_o.alloc((size_t)B * attn_max_chunks * dm.dp, false);
         attn_ml.alloc((size_t)B * attn_max_chunks * 2, false);
         invalidate_graphs();
@@ -377,14 +396,10 @@ struct el_engine {
     }
 
     // ---- GEMM plans ----
-    static int pick_splits(int m_tiles, int kb_total) {
-        int best = 1;
-        for (int s = 1; s <= std::min(kb_total, 16); ++s) {
-            if (kb_total % s) continue;
-            best = s;
-            if (m_tiles * s >= 148) break;
-        }
-        return best;
+    // split-K cluster size: aim at ~one CTA per SM, at most 8 (portable clusters)
+    int pick_splits(int m_tiles, int kb_total) const {
+        int s = (148 + m_tiles / 2) / m_tiles;
+        return std::max(1, std::min({s, opt_splits_cap, kb_total}));
     }
     el::GemmPlan make_plan(const CUtensorMap& A, const CUtensorMap& Bm, int m_tiles, int k, int n_pad, bool tile,
                            int forced_splits = 0) {
@@ -392,21 +407,17 @@ struct el_engine {
         p.tmA = A;
         p.tmB = Bm;
         p.m_tiles = m_tiles;
-        const int kb = k / 64;
-        p.splits = forced_splits ? forced_splits : pick_splits(m_tiles, kb);
-        p.kb_per_split = kb / p.splits;
+        p.kb_total = k / 64;
+        p.splits = forced_splits ? forced_splits : pick_splits(m_tiles, p.kb_total);
+        const int kb_max = ceil_div(p.kb_total, p.splits);
         p.n_pad = n_pad;
         const int stage = 128 * 64 * 2 + n_pad * 64 * 2;
-        p.stages = std::max(1, std::min(p.kb_per_split, (200 * 1024) / stage));
+        p.stages = std::max(1, std::min(kb_max, (200 * 1024) / stage));
         p.smem_bytes = el::gemm_smem_bytes(n_pad, p.stages, tile);
         while (p.smem_bytes > 227 * 1024 && p.stages > 1) p.smem_bytes = el::gemm_smem_bytes(n_pad, --p.stages, tile);
         int cols = 32;
         while (cols < n_pad) cols <<= 1;
         p.tmem_cols = cols;
-        if (!tile && p.splits > 1) {
-            gemm_ws.ensure((size_t)p.splits * m_tiles * n_pad * 128);
-            gemm_cnt.ensure((size_t)m_tiles);
-        }
         return p;
     }
     Plans& plans_for(int B) {
@@ -442,8 +453,10 @@ struct el_engine {
         s.up_b = up_b.p;
         s.attn_o = attn_o.p; s.attn_ml = attn_ml.p; s.attn_cnt = attn_cnt.p;
         s.attn_max_chunks = attn_max_chunks; s.attn_cb = attn_cb; s.attn_stages = attn_stages;
+        s.dbg = dbg;
+        s.dbg_ts = dbg_ts.p;
+        s.attn_grid = attn_grid; s.attn_queue = attn_queue.p; s.attn_done = attn_queue.p + 1;
         s.attn_scale = (float)(1.0 / std::sqrt((double)dm.d));
-        s.gemm_ws = gemm_ws.p; s.gemm_cnt = gemm_cnt.p;
         s.lm_part = lm_part.p;
         s.layer = layer.p; s.out_layer = out_layer.p; s.status = status.p; s.first_accept = first_accept.p;
         s.accept = accept.p; s.conf = conf.p; s.exit_cnt = exit_cnt.p; s.cont_host = cont_dev;
@@ -458,24 +471,34 @@ struct el_engine {
         return s;
     }
 
-    // one layer's kernels (the WHILE body)
+    // one layer's kernels (the WHILE body). PDL: every kernel after the first
+    // may launch while its predecessor drains (weights / old KV blocks are
+    // prefetched before griddepcontrol.wait).
     void launch_layer(const el::DevState& s, Plans& P) {
-        el::launch_gemm(el::kGemmQkv, P.qkv, s, stream);
-        el::launch_attention(s, stream);
-        el::launch_gemm(el::kGemmWo, P.wo, s, stream);
-        el::launch_gemm(el::kGemmUp, P.up, s, stream);
-        el::launch_gemm(el::kGemmDown, P.down, s, stream);
-        if (s.technique == el::kSoftmax) el::launch_gemm(el::kGemmLmCheck, P.lm, s, stream);
-        el::launch_exit(s, stream);
+        el::launch_gemm(el::kGemmQkv, P.qkv, s, stream, false);
+        el::launch_attention(s, stream, pdl);
+        el::launch_gemm(el::kGemmWo, P.wo, s, stream, pdl);
+        el::launch_gemm(el::kGemmUp, P.up, s, stream, pdl);
+        el::launch_gemm(el::kGemmDown, P.down, s, stream, pdl);
+        if (s.technique == el::kSoftmax) el::launch_gemm(el::kGemmLmCheck, P.lm, s, stream, pdl);
+        el::launch_exit(s, stream, pdl);
     }
     void launch_tail(const el::DevState& s, Plans& P) {
-        if (s.technique != el::kNever) el::launch_gemm(el::kGemmFill, P.fill, s, stream);
-        if (s.technique != el::kSoftmax) el::launch_gemm(el::kGemmLmFinal, P.lm, s, stream);
-        el::launch_finish(s, stream);
+        bool first = true;  // first kernel after the conditional node: plain dependency
+        if (s.technique != el::kNever) {
+            el::launch_gemm(el::kGemmFill, P.fill, s, stream, false);
+            first = false;
+        }
+        if (s.technique != el::kSoftmax) {
+            el::launch_gemm(el::kGemmLmFinal, P.lm, s, stream, pdl && !first);
+            first = false;
+        }
+        el::launch_finish(s, stream, pdl && !first);
     }
     int launches_per_iteration(int e) const {
         const int per_layer = 6 + (cfg.technique == EL_TECH_SOFTMAX ? 1 : 0);
-        return 1 + e * per_layer + (cfg.technique != EL_TECH_NEVER ? 1 : 0) + (cfg.technique != EL_TECH_SOFTMAX ? 1 : 0) + 1;
+        return 1 + e * per_layer + (cfg.technique != EL_TECH_NEVER ? 1 : 0) +
+               (cfg.technique != EL_TECH_SOFTMAX ? 1 : 0) + 1;
     }
 
     // eager iteration: host reads the device continue flag after each layer
@@ -596,12 +619,12 @@ struct el_engine {
             s.cont_host = nullptr;
             el::launch_embed(s, stream);
             for (int l = 1; l <= dm.L; ++l) {
-                el::launch_gemm(el::kGemmQkv, P.qkv, s, stream);
-                el::launch_attention(s, stream);
-                el::launch_gemm(el::kGemmWo, P.wo, s, stream);
-                el::launch_gemm(el::kGemmUp, P.up, s, stream);
-                el::launch_gemm(el::kGemmDown, P.down, s, stream);
-                el::launch_exit(s, stream);
+                el::launch_gemm(el::kGemmQkv, P.qkv, s, stream, false);
+                el::launch_attention(s, stream, pdl);
+                el::launch_gemm(el::kGemmWo, P.wo, s, stream, pdl);
+                el::launch_gemm(el::kGemmUp, P.up, s, stream, pdl);
+                el::launch_gemm(el::kGemmDown, P.down, s, stream, pdl);
+                el::launch_exit(s, stream, pdl);
             }
             el::launch_advance(s, stream);
             CK(cudaStreamSynchronize(stream));  // host vectors are reused next step
@@ -956,6 +979,23 @@ int el_engine_destroy(el_engine* e) {
 int el_engine_set_option(el_engine* e, const char* key, int64_t v) {
     API_BEGIN
     if (!std::strcmp(key, "graph")) e->use_graph = v != 0;
+    else if (!std::strcmp(key, "dbg")) {
+        e->dbg = (int)v;
+        e->invalidate_graphs();
+    }
+    else if (!std::strcmp(key, "attn_cb") || !std::strcmp(key, "attn_stages")) {
+        (key[5] == 'c' ? e->opt_attn_cb : e->opt_attn_stages) = (int)v;
+        e->plan_attention();
+    } else if (!std::strcmp(key, "splits_cap")) {
+        if (v < 1 || v > 8) fail(EL_INVALID_ARGUMENT, "splits_cap must be in [1, 8]");
+        e->opt_splits_cap = (int)v;
+        e->plans.clear();
+        e->invalidate_graphs();
+    }
+    else if (!std::strcmp(key, "pdl")) {
+        e->pdl = v != 0;
+        e->invalidate_graphs();
+    }
     else if (!std::strcmp(key, "rec_cap")) {
         if (v < 1) fail(EL_INVALID_ARGUMENT, "rec_cap must be >= 1");
         e->rec_cap = (int)v;
@@ -1157,12 +1197,12 @@ int el_time_kernel(el_engine* e, int kind, int layer, int reps, float* ms) {
     CK(cudaEventCreate(&b));
     auto one = [&]() {
         switch (kind) {
-            case 0: el::launch_attention(s, e->stream); break;
-            case 1: el::launch_gemm(el::kGemmQkv, P.qkv, s, e->stream); break;
-            case 2: el::launch_gemm(el::kGemmWo, P.wo, s, e->stream); break;
-            case 3: el::launch_gemm(el::kGemmUp, P.up, s, e->stream); break;
-            case 4: el::launch_gemm(el::kGemmDown, P.down, s, e->stream); break;
-            case 5: el::launch_gemm(el::kGemmLmCheck, P.lm, s, e->stream); break;
+            case 0: el::launch_attention(s, e->stream, false); break;
+            case 1: el::launch_gemm(el::kGemmQkv, P.qkv, s, e->stream, false); break;
+            case 2: el::launch_gemm(el::kGemmWo, P.wo, s, e->stream, false); break;
+            case 3: el::launch_gemm(el::kGemmUp, P.up, s, e->stream, false); break;
+            case 4: el::launch_gemm(el::kGemmDown, P.down, s, e->stream, false); break;
+            case 5: el::launch_gemm(el::kGemmLmCheck, P.lm, s, e->stream, false); break;
             default: fail(EL_INVALID_ARGUMENT, "unknown kernel kind %d", kind);
         }
     };
@@ -1181,6 +1221,13 @@ int el_time_kernel(el_engine* e, int kind, int layer, int reps, float* ms) {
     API_END
 }
 
+int el_debug_timestamps(el_engine* e, uint64_t* out, int n) {
+    API_BEGIN
+    CK(cudaStreamSynchronize(e->stream));
+    CK(cudaMemcpy(out, e->dbg_ts.p, sizeof(uint64_t) * std::min<size_t>((size_t)n, e->dbg_ts.n), cudaMemcpyDeviceToHost));
+    API_END
+}
+
 int el_sync(el_engine* e) {
     API_BEGIN
     CK(cudaStreamSynchronize(e->stream));
@@ -1193,7 +1240,7 @@ int el_plan_info(el_engine* e, int64_t* out, int cap) {
     API_BEGIN
     auto& P = e->plans_for(e->in_session ? e->sess_B : e->dm.Bmax);
     const int64_t v[] = {e->attn_cb,    e->attn_stages,   e->attn_max_chunks, P.n_pad,       P.qkv.splits,
-                         P.wo.splits,   P.up.splits,      P.down.splits,      P.fill.splits, P.qkv.stages,
+                         P.wo.splits,   P.up.splits,      P.down.splits,      P.fill.splits, P.down.stages,
                          P.lm.m_tiles,  e->dm.dp,         e->dm.fp,           e->dm.Vp,      e->dm.bpl_max};
     const int n = (int)(sizeof v / sizeof v[0]);
     for (int i = 0; i < std::min(n, cap); ++i) out[i] = v[i];

@@ -11,6 +11,7 @@
 #include <cuda_runtime_api.h>
 
 #include <cstdio>
+#include <utility>
 
 #include "el_common.cuh"
 #include "el_kernels.h"
@@ -25,6 +26,27 @@ namespace el {
                     __FILE__, __LINE__);                                                    \
         }                                                                                   \
     } while (0)
+
+// launch with optional programmatic dependent launch (PDL)
+template <typename... KArgs, typename... Args>
+static void launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, int smem, cudaStream_t s, bool pdl,
+                     Args&&... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = (size_t)smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl ? 1 : 0;
+    cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+    EL_CUDA_LAUNCH_CHECK();
+}
+
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 // ===========================================================================
 // 1. Weight-streaming GEMM on tcgen05:  D[M x N] = W[M x K] . X[N x K]^T
@@ -213,9 +235,20 @@ template <>
 struct Epi<kGemmLmFinal> : EpiLm<kGemmLmFinal> {};
 
 struct GemmArgs {
-    int m_tiles, splits, kb_per_split, n_pad, stages, tmem_cols;
+    int m_tiles, splits, kb_total, n_pad, stages, tmem_cols, pdl;
 };
 
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+// Split-K runs as a thread-block cluster along K (grid.y = cluster.y = splits):
+// every CTA parks its fp32 partial tile in its own shared memory, then each CTA
+// reduces a disjoint set of output columns by reading the partials of all
+// cluster peers over DSMEM in fixed rank order (deterministic, no global
+// workspace, no atomics).  With PDL the weight (A) tiles are requested before
+// griddepcontrol.wait: weights never depend on the previous kernel, so their
+// HBM latency overlaps the producer kernel's tail.
 template <GemmKind K>
 __global__ void __launch_bounds__(128, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, GemmArgs g,
@@ -230,15 +263,32 @@ __global__ void __launch_bounds__(128, 1)
     uint8_t* sA = smem;
     uint8_t* sB = smem + (size_t)g.stages * kAStage;
     size_t region = (size_t)g.stages * (kAStage + b_stage);
-    if (E::kTile && region < (size_t)g.n_pad * 129 * 4) region = (size_t)g.n_pad * 129 * 4;
+    const size_t part_bytes = (size_t)g.n_pad * kBM * 4;
+    if ((E::kTile || g.splits > 1) && region < part_bytes) region = part_bytes;
     uint64_t* full = (uint64_t*)(smem + region);
     uint64_t* empty = full + g.stages;
     uint64_t* accf = empty + g.stages;
     uint32_t* tmem_slot = (uint32_t*)(accf + 1);
     EpiSmem& es = *(EpiSmem*)(((uintptr_t)(tmem_slot + 4) + 15) & ~(uintptr_t)15);
 
+    auto stamp = [&](int i) {
+        if ((st.dbg & 8) && tid == 0) {
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+            st.dbg_ts[(blockIdx.y * gridDim.x + blockIdx.x) * 8 + i] = t;
+        }
+    };
+    stamp(0);
     int a_row = 0, b_row = 0;
-    if (!E::setup(st, tile, es, a_row, b_row)) return;  // uniform across the CTA
+    // setup() only reads layer / output-layer counters written before this
+    // kernel's predecessor started (see el_kernels.h), so it may run pre-wait.
+    if (!E::setup(st, tile, es, a_row, b_row)) {  // uniform across the CTA and its cluster
+        if (g.pdl) pdl_trigger();
+        return;
+    }
+    const int kb0 = (int)((long)split * g.kb_total / g.splits);
+    const int kb1 = (int)((long)(split + 1) * g.kb_total / g.splits);
+    const int nkb = kb1 - kb0;
 
     if (tid == 0) {
         for (int s = 0; s < g.stages; ++s) {
@@ -253,15 +303,23 @@ __global__ void __launch_bounds__(128, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
-    const int kb0 = split * g.kb_per_split;
+    stamp(1);
 
     if (warp == 0 && lane == 0) {
         // ---- TMA producer ----
         tma_prefetch_desc(&tmA);
         tma_prefetch_desc(&tmB);
-        for (int kb = 0; kb < g.kb_per_split; ++kb) {
+        const int pre = min(nkb, g.stages);
+        for (int kb = 0; kb < pre; ++kb) {  // weights first: independent of the previous kernel
+            mbar_arrive_expect_tx(&full[kb], kAStage + b_stage);
+            tma_load_2d(sA + (size_t)kb * kAStage, &tmA, &full[kb], (kb0 + kb) * kBK, a_row);
+        }
+        if (g.pdl) pdl_wait();
+        for (int kb = 0; kb < pre; ++kb)
+            tma_load_2d(sB + (size_t)kb * b_stage, &tmB, &full[kb], (kb0 + kb) * kBK, b_row);
+        for (int kb = pre; kb < nkb; ++kb) {
             const int s = kb % g.stages;
-            if (kb >= g.stages) mbar_wait(&empty[s], ((kb / g.stages) - 1) & 1);
+            mbar_wait(&empty[s], ((kb / g.stages) - 1) & 1);
             mbar_arrive_expect_tx(&full[s], kAStage + b_stage);
             tma_load_2d(sA + (size_t)s * kAStage, &tmA, &full[s], (kb0 + kb) * kBK, a_row);
             tma_load_2d(sB + (size_t)s * b_stage, &tmB, &full[s], (kb0 + kb) * kBK, b_row);
@@ -269,7 +327,7 @@ __global__ void __launch_bounds__(128, 1)
     } else if (warp == 1 && lane == 0) {
         // ---- MMA issuer (single thread) ----
         const uint32_t idesc = idesc_bf16_m128((uint32_t)g.n_pad);
-        for (int kb = 0; kb < g.kb_per_split; ++kb) {
+        for (int kb = 0; kb < nkb; ++kb) {
             const int s = kb % g.stages;
             mbar_wait(&full[s], (kb / g.stages) & 1);
             tc_fence_after();
@@ -283,12 +341,16 @@ __global__ void __launch_bounds__(128, 1)
         tc_commit(accf);
     }
     __syncwarp();
+    if (g.pdl) pdl_wait();  // epilogue reads activations of earlier kernels
+    if (g.pdl) pdl_trigger();
 
     // ---- epilogue: all four warps, thread t <-> TMEM lane t <-> output row t ----
     E::prologue(st, es);
+    stamp(2);
     mbar_wait(accf, 0);
     tc_fence_after();
     __syncthreads();
+    stamp(3);
     const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
     const int nval = st.rows.B;
     const int row = tid;
@@ -314,56 +376,95 @@ __global__ void __launch_bounds__(128, 1)
                 if (c0 + j < nval) E::apply(st, es, row, c0 + j, v[j]);
         }
     } else {
-        float* my = st.gemm_ws + ((size_t)(split * g.m_tiles + tile) * g.n_pad) * kBM;
+        float* part = (float*)smem;  // [n][128], stage buffers are free now
         for (int c0 = 0; c0 < nval; c0 += 16) {
             float v[16];
             tmem_ld16(trow + (uint32_t)c0, v);
 #pragma unroll
             for (int j = 0; j < 16; ++j)
-                if (c0 + j < nval) my[(size_t)(c0 + j) * kBM + row] = v[j];
+                if (c0 + j < nval) part[(c0 + j) * kBM + row] = v[j];
         }
-        __threadfence();
-        __syncthreads();
-        if (tid == 0) es.last = (atomicAdd(&st.gemm_cnt[tile], 1) == g.splits - 1);
-        __syncthreads();
-        if (es.last) {
-            __threadfence();
-            for (int c = 0; c < nval; ++c) {
+        cluster_sync_all();
+        stamp(4);
+        // this CTA owns columns [c0, c1); all remote loads of a column group are
+        // issued before the (fixed-order) sums so DSMEM latency overlaps
+        const int per = (nval + g.splits - 1) / g.splits;
+        const int c0 = split * per, c1 = min(nval, c0 + per);
+        const float* peer[8];
+#pragma unroll
+        for (int s = 0; s < 8; ++s)
+            peer[s] = (const float*)__cluster_map_shared_rank((void*)part, s < g.splits ? s : 0);
+        for (int c = c0; c < c1; c += 4) {
+            float v[4][8];
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+#pragma unroll
+                for (int s = 0; s < 8; ++s)
+                    v[j][s] = (s < g.splits && c + j < c1) ? peer[s][(c + j) * kBM + row] : 0.f;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                if (c + j >= c1) break;
                 float acc = 0.f;
-                for (int s = 0; s < g.splits; ++s)
-                    acc += __ldcg(st.gemm_ws + ((size_t)(s * g.m_tiles + tile) * g.n_pad + c) * kBM + row);
-                E::apply(st, es, row, c, acc);
+#pragma unroll
+                for (int s = 0; s < 8; ++s)
+                    if (s < g.splits) acc += v[j][s];
+                E::apply(st, es, row, c + j, acc);
             }
-            if (tid == 0) st.gemm_cnt[tile] = 0;
         }
+        stamp(5);
+        cluster_sync_all();  // peers keep their smem alive until everyone has read it
     }
+    stamp(6);
     tc_fence_before();
     __syncthreads();
     if (warp == 1) tmem_dealloc(tmem, (uint32_t)g.tmem_cols);
+    stamp(7);
 }
 
 int gemm_smem_bytes(int n_pad, int stages, bool tile_reduce) {
     int main = stages * (kAStage + n_pad * kBK * 2);
-    if (tile_reduce) main = main > n_pad * 129 * 4 ? main : n_pad * 129 * 4;
+    const int part = tile_reduce ? n_pad * 129 * 4 : n_pad * kBM * 4;  // split-K partial or LM tile
+    main = main > part ? main : part;
     return 1024 + main + (2 * stages + 1) * 8 + 16 + (int)sizeof(EpiSmem) + 64;
 }
 
 template <GemmKind K>
-static void launch_gemm_t(const GemmPlan& p, const DevState& st, cudaStream_t s) {
-    GemmArgs g{p.m_tiles, p.splits, p.kb_per_split, p.n_pad, p.stages, p.tmem_cols};
-    gemm_kernel<K><<<dim3(p.m_tiles, p.splits), 128, p.smem_bytes, s>>>(p.tmA, p.tmB, g, st);
+static void launch_gemm_t(const GemmPlan& p, const DevState& st, cudaStream_t s, bool pdl) {
+    GemmArgs g{p.m_tiles, p.splits, p.kb_total, p.n_pad, p.stages, p.tmem_cols, pdl ? 1 : 0};
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(p.m_tiles, p.splits);
+    cfg.blockDim = dim3(128);
+    cfg.dynamicSmemBytes = p.smem_bytes;
+    cfg.stream = s;
+    cudaLaunchAttribute at[2];
+    int na = 0;
+    if (p.splits > 1) {
+        at[na].id = cudaLaunchAttributeClusterDimension;
+        at[na].val.clusterDim.x = 1;
+        at[na].val.clusterDim.y = p.splits;
+        at[na].val.clusterDim.z = 1;
+        ++na;
+    }
+    if (pdl) {
+        at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[na].val.programmaticStreamSerializationAllowed = 1;
+        ++na;
+    }
+    cfg.attrs = at;
+    cfg.numAttrs = na;
+    cudaLaunchKernelEx(&cfg, gemm_kernel<K>, p.tmA, p.tmB, g, st);
     EL_CUDA_LAUNCH_CHECK();
 }
 
-void launch_gemm(GemmKind kind, const GemmPlan& p, const DevState& st, cudaStream_t s) {
+void launch_gemm(GemmKind kind, const GemmPlan& p, const DevState& st, cudaStream_t s, bool pdl) {
     switch (kind) {
-        case kGemmQkv: launch_gemm_t<kGemmQkv>(p, st, s); break;
-        case kGemmWo: launch_gemm_t<kGemmWo>(p, st, s); break;
-        case kGemmUp: launch_gemm_t<kGemmUp>(p, st, s); break;
-        case kGemmDown: launch_gemm_t<kGemmDown>(p, st, s); break;
-        case kGemmLmCheck: launch_gemm_t<kGemmLmCheck>(p, st, s); break;
-        case kGemmLmFinal: launch_gemm_t<kGemmLmFinal>(p, st, s); break;
-        case kGemmFill: launch_gemm_t<kGemmFill>(p, st, s); break;
+        case kGemmQkv: launch_gemm_t<kGemmQkv>(p, st, s, pdl); break;
+        case kGemmWo: launch_gemm_t<kGemmWo>(p, st, s, pdl); break;
+        case kGemmUp: launch_gemm_t<kGemmUp>(p, st, s, pdl); break;
+        case kGemmDown: launch_gemm_t<kGemmDown>(p, st, s, pdl); break;
+        case kGemmLmCheck: launch_gemm_t<kGemmLmCheck>(p, st, s, pdl); break;
+        case kGemmLmFinal: launch_gemm_t<kGemmLmFinal>(p, st, s, pdl); break;
+        case kGemmFill: launch_gemm_t<kGemmFill>(p, st, s, pdl); break;
     }
 }
 
@@ -377,200 +478,346 @@ void launch_gemm(GemmKind kind, const GemmPlan& p, const DevState& st, cudaStrea
 //    sequence combines the partials in chunk order (flash-decoding) and emits
 //    the bf16 attention output for the W_o GEMM.
 // ===========================================================================
+// Work item = (sequence b, chunk c of attn_cb KV blocks).  The kernel is
+// persistent (one CTA per SM); a producer warp pulls items from an atomic
+// queue and streams their K/V blocks (plus the sequence's q on an item's first
+// block) through a ring of shared-memory stages with 1-D bulk TMA, running
+// ahead across item boundaries so HBM never idles.  Eight consumer warps own
+// two rows of every block each (processed together for ILP) and keep their
+// own online-softmax state (m, l, o); a stage is released by 8 warp arrivals
+// on its "empty" mbarrier, so the main loop has no CTA-wide barrier.  At the
+// end of an item the warps merge in fixed order inside the just-consumed
+// stage buffer; the last chunk of a sequence to finish combines the partials
+// in chunk order (flash-decoding) into the bf16 attention output.
+constexpr int kAttnWarps = 8;
+constexpr int kAttnThreads = (kAttnWarps + 1) * 32;
+
+struct AttnDesc {
+    int b, c, rows, first, last, pad[3];
+};
 struct AttnSmem {
     uint64_t full[8];
-    float sc[64];
-    int last;
+    uint64_t empty[8];
+    AttnDesc desc[8];
+    float wm[kAttnWarps], wl[kAttnWarps];
+    float cw[128];
+    float cl[128];
+    int last_flag;
+    int pad[3];
 };
 
-__device__ __forceinline__ float dot8(uint4 k, const float* q) {
+__device__ __forceinline__ float dot8p(uint4 k, const float* q) {
     const uint32_t w[4] = {k.x, k.y, k.z, k.w};
-    float a = 0.f;
+    float a0 = 0.f, a1 = 0.f;
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-        a = fmaf(__uint_as_float(w[i] << 16), q[2 * i], a);
-        a = fmaf(__uint_as_float(w[i] & 0xFFFF0000u), q[2 * i + 1], a);
+        a0 = fmaf(__uint_as_float(w[i] << 16), q[2 * i], a0);
+        a1 = fmaf(__uint_as_float(w[i] & 0xFFFF0000u), q[2 * i + 1], a1);
     }
-    return a;
+    return a0 + a1;
+}
+__device__ __forceinline__ void axpy8(float p, uint4 v, float* o) {
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        o[2 * e] = fmaf(p, __uint_as_float(w[e] << 16), o[2 * e]);
+        o[2 * e + 1] = fmaf(p, __uint_as_float(w[e] & 0xFFFF0000u), o[2 * e + 1]);
+    }
+}
+__device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+__device__ __forceinline__ int atom_add_acq_rel(int* p, int v) {
+    int old;
+    asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+    return old;
 }
 
 template <int NJ>
-__global__ void __launch_bounds__(128) attn_kernel(DevState st) {
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 127) & ~(uintptr_t)127);
+__global__ void __launch_bounds__(kAttnThreads) attn_kernel(DevState st) {
+    extern __shared__ __align__(128) uint8_t smem_raw[];
     const Dims& dm = st.dm;
-    const int b = blockIdx.y, c = blockIdx.x;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int layer = *st.layer;
-    const int ctx = st.rows.pos[b] + 1;
-    const int nblk = (ctx + dm.bc - 1) / dm.bc;
-    const int nch = (nblk + st.attn_cb - 1) / st.attn_cb;
-    if (c >= nch) return;
-    const int blk0 = c * st.attn_cb;
-    const int n = min(nblk, blk0 + st.attn_cb) - blk0;
     const int dp = dm.dp, nchunk = dp / 8;
-    const int* table = st.tables + ((size_t)st.rows.slot[b] * dm.L + (layer - 1)) * dm.bpl_max;
-    const uint32_t blk_bytes = (uint32_t)dm.bc * dp * 2;
-
-    AttnSmem& a = *(AttnSmem*)smem;
-    uint8_t* stages = smem + ((sizeof(AttnSmem) + 127) & ~(size_t)127);
     const int S = st.attn_stages;
-
-    auto issue = [&](int i) {
-        const int s = i % S;
-        const int blk = blk0 + i;
-        const int rows = min(dm.bc, ctx - blk * dm.bc);
-        const uint32_t bytes = (uint32_t)rows * dp * 2;
-        const int id = table[blk];
-        mbar_arrive_expect_tx(&a.full[s], 2 * bytes);
-        bulk_load(stages + (size_t)s * 2 * blk_bytes, st.kpool + (size_t)id * dm.bc * dp, bytes, &a.full[s]);
-        bulk_load(stages + (size_t)s * 2 * blk_bytes + blk_bytes, st.vpool + (size_t)id * dm.bc * dp, bytes,
-                  &a.full[s]);
-    };
+    const uint32_t blk_bytes = (uint32_t)dm.bc * dp * 2;
+    const uint32_t stage_bytes = (uint32_t)attn_stage_bytes(dm);  // K | V | q (>= merge buffer)
+    AttnSmem& a = *reinterpret_cast<AttnSmem*>(smem_raw);
+    uint8_t* stages = smem_raw + ((sizeof(AttnSmem) + 127) & ~(size_t)127);
+    const int layer = *st.layer;
+    const int n_items = st.rows.B * st.attn_max_chunks;
 
     if (tid == 0) {
-        for (int s = 0; s < S; ++s) mbar_init(&a.full[s], 1);
+        for (int s = 0; s < S; ++s) {
+            mbar_init(&a.full[s], 1);
+            mbar_init(&a.empty[s], kAttnWarps);
+        }
         fence_barrier_init();
-        for (int i = 0; i < min(S, n); ++i) issue(i);
-    }
-    // q (pre-scaled) for the chunks this lane owns in the K pass
-    float qv[NJ][8];
-    const float* q = st.q32 + (size_t)b * dp;
-#pragma unroll
-    for (int t = 0; t < NJ; ++t) {
-        const int j = lane + 32 * t;
-#pragma unroll
-        for (int i = 0; i < 8; ++i) qv[t][i] = (j < nchunk) ? q[j * 8 + i] * st.attn_scale : 0.f;
     }
     __syncthreads();
 
-    float m_run = -INFINITY, l_run = 0.f;
-    float o[2][8];
-#pragma unroll
-    for (int u = 0; u < 2; ++u)
-#pragma unroll
-        for (int i = 0; i < 8; ++i) o[u][i] = 0.f;
-
-    for (int i = 0; i < n; ++i) {
-        const int s = i % S;
-        const int rows = min(dm.bc, ctx - (blk0 + i) * dm.bc);
-        mbar_wait(&a.full[s], (i / S) & 1);
-        const uint4* sk = (const uint4*)(stages + (size_t)s * 2 * blk_bytes);
-        const uint4* sv = (const uint4*)(stages + (size_t)s * 2 * blk_bytes + blk_bytes);
-        for (int r = warp; r < rows; r += 4) {
-            float acc = 0.f;
-#pragma unroll
-            for (int t = 0; t < NJ; ++t) {
-                const int j = lane + 32 * t;
-                if (j < nchunk) acc += dot8(sk[r * nchunk + j], qv[t]);
+    if (warp == kAttnWarps) {
+        // ---------------- producer warp ----------------
+        // lane 0 drives the ring; the whole warp fetches an item's block ids
+        // in parallel (one global latency per item instead of one per block)
+        pdl_wait();  // this layer's K/V at `pos` and q come from the QKV kernel
+        int seq = 0;
+        for (;;) {
+            int item = 0;
+            if (lane == 0) item = atomicAdd(st.attn_queue, 1);
+            item = __shfl_sync(0xffffffffu, item, 0);
+            if (item >= n_items) break;
+            const int b = item / st.attn_max_chunks, c = item % st.attn_max_chunks;
+            const int ctx = st.rows.pos[b] + 1;
+            const int nblk = (ctx + dm.bc - 1) / dm.bc;
+            const int blk0 = c * st.attn_cb;
+            if (blk0 >= nblk) continue;
+            const int blk1 = min(nblk, blk0 + st.attn_cb);
+            const int* table = st.tables + ((size_t)st.rows.slot[b] * dm.L + (layer - 1)) * dm.bpl_max;
+            const int my_id = (blk0 + lane < blk1) ? table[blk0 + lane] : 0;  // attn_cb <= 32
+            for (int blk = blk0; blk < blk1; ++blk, ++seq) {
+                const int id = __shfl_sync(0xffffffffu, my_id, blk - blk0);
+                if (lane == 0) {
+                    const int s = seq % S;
+                    if (seq >= S) mbar_wait(&a.empty[s], ((seq / S) - 1) & 1);
+                    const int rows = min(dm.bc, ctx - blk * dm.bc);
+                    const uint32_t bytes = (uint32_t)rows * dp * 2;
+                    const bool first = blk == blk0;
+                    a.desc[s] = AttnDesc{b, c, rows, first, blk == blk1 - 1, {0, 0, 0}};
+                    uint8_t* sb = stages + (size_t)s * stage_bytes;
+                    mbar_arrive_expect_tx(&a.full[s], 2 * bytes + (first ? (uint32_t)dp * 4 : 0u));
+                    if (first) bulk_load(sb + 2 * blk_bytes, st.q32 + (size_t)b * dp, (uint32_t)dp * 4, &a.full[s]);
+                    bulk_load(sb, st.kpool + (size_t)id * dm.bc * dp, bytes, &a.full[s]);
+                    bulk_load(sb + blk_bytes, st.vpool + (size_t)id * dm.bc * dp, bytes, &a.full[s]);
+                }
+                __syncwarp();
             }
-#pragma unroll
-            for (int off = 16; off; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
-            if (lane == 0) a.sc[r] = acc;
         }
-        __syncthreads();
-        float mloc = -INFINITY;
-        for (int r = 0; r < rows; ++r) mloc = fmaxf(mloc, a.sc[r]);
-        const float m_new = fmaxf(m_run, mloc);
-        const float alpha = __expf(m_run - m_new);
-        float psum = 0.f;
+        if (lane == 0) {
+            const int s = seq % S;  // terminal descriptor
+            if (seq >= S) mbar_wait(&a.empty[s], ((seq / S) - 1) & 1);
+            a.desc[s].b = -1;
+            mbar_arrive(&a.full[s]);
+        }
+    } else {
+        // ---------------- consumer warps ----------------
+        float q[NJ][8], o[NJ][8];
+        float m = -INFINITY, l = 0.f;
+        const int r0 = warp, r1 = warp + kAttnWarps;
+        for (int seq = 0;; ++seq) {
+            const int s = seq % S;
+            mbar_wait(&a.full[s], (seq / S) & 1);
+            const AttnDesc d = a.desc[s];
+            if (d.b < 0) break;
+            uint8_t* sb = stages + (size_t)s * stage_bytes;
+            const uint4* sk = reinterpret_cast<const uint4*>(sb);
+            const uint4* sv = reinterpret_cast<const uint4*>(sb + blk_bytes);
+            if (d.first) {
+                const float* qs = reinterpret_cast<const float*>(sb + 2 * blk_bytes);
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
-            const int j = tid + 128 * u;
-            if (j < nchunk) {
+                for (int t = 0; t < NJ; ++t) {
+                    const int j = lane + 32 * t;
 #pragma unroll
-                for (int e = 0; e < 8; ++e) o[u][e] *= alpha;
+                    for (int i = 0; i < 8; ++i) {
+                        q[t][i] = (j < nchunk) ? qs[j * 8 + i] * st.attn_scale : 0.f;
+                        o[t][i] = 0.f;
+                    }
+                }
+                m = -INFINITY;
+                l = 0.f;
             }
-        }
-        for (int r = 0; r < rows; ++r) {
-            const float p = __expf(a.sc[r] - m_new);
-            psum += p;
+            for (int rb = 0; rb < ((st.dbg & 1) ? 0 : d.rows); rb += 2 * kAttnWarps) {
+                const int ra = rb + r0, rc = rb + r1;
+                const bool va = ra < d.rows, vc = rc < d.rows;
+                float sa = 0.f, sc = 0.f;
 #pragma unroll
-            for (int u = 0; u < 2; ++u) {
-                const int j = tid + 128 * u;
-                if (j < nchunk) {
-                    const uint4 vv = sv[r * nchunk + j];
-                    const uint32_t w[4] = {vv.x, vv.y, vv.z, vv.w};
+                for (int t = 0; t < NJ; ++t) {
+                    const int j = lane + 32 * t;
+                    if (j < nchunk) {
+                        if (va) sa += dot8p(sk[ra * nchunk + j], q[t]);
+                        if (vc) sc += dot8p(sk[rc * nchunk + j], q[t]);
+                    }
+                }
 #pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        o[u][2 * e] = fmaf(p, __uint_as_float(w[e] << 16), o[u][2 * e]);
-                        o[u][2 * e + 1] = fmaf(p, __uint_as_float(w[e] & 0xFFFF0000u), o[u][2 * e + 1]);
+                for (int off = 16; off; off >>= 1) {
+                    sa += __shfl_xor_sync(0xffffffffu, sa, off);
+                    sc += __shfl_xor_sync(0xffffffffu, sc, off);
+                }
+                if (!va) sa = -INFINITY;
+                if (!vc) sc = -INFINITY;
+                const float m_new = fmaxf(m, fmaxf(sa, sc));
+                if (m_new == -INFINITY) continue;  // this warp has no rows here
+                const float pa = __expf(sa - m_new), pc = __expf(sc - m_new);
+                if (m_new != m) {
+                    const float alpha = __expf(m - m_new);
+                    l *= alpha;
+#pragma unroll
+                    for (int t = 0; t < NJ; ++t)
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) o[t][i] *= alpha;
+                    m = m_new;
+                }
+                l += pa + pc;
+#pragma unroll
+                for (int t = 0; t < NJ; ++t) {
+                    const int j = lane + 32 * t;
+                    if (j < nchunk) {
+                        if (va) axpy8(pa, sv[ra * nchunk + j], o[t]);
+                        if (vc) axpy8(pc, sv[rc * nchunk + j], o[t]);
                     }
                 }
             }
-        }
-        l_run = l_run * alpha + psum;
-        m_run = m_new;
-        __syncthreads();  // stage s consumed
-        if (tid == 0 && i + S < n) issue(i + S);
-    }
+            if (!d.last || (st.dbg & 4)) {
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&a.empty[s]);
+                continue;
+            }
 
-    // ---- partial write + last-CTA combine (chunk order => deterministic) ----
-    const size_t pbase = (size_t)b * st.attn_max_chunks;
+            // ---- end of item: merge the 8 warps in fixed order inside this
+            //      (fully consumed, not yet released) stage buffer ----
+            named_bar(1, kAttnWarps * 32);
+            float* merge = reinterpret_cast<float*>(sb);  // [8][dp] fp32 <= 2 * blk_bytes
+            if (lane == 0) {
+                a.wm[warp] = m;
+                a.wl[warp] = l;
+            }
 #pragma unroll
-    for (int u = 0; u < 2; ++u) {
-        const int j = tid + 128 * u;
-        if (j < nchunk) {
-            float4* dst = (float4*)(st.attn_o + (pbase + c) * dp + j * 8);
-            dst[0] = make_float4(o[u][0], o[u][1], o[u][2], o[u][3]);
-            dst[1] = make_float4(o[u][4], o[u][5], o[u][6], o[u][7]);
+            for (int t = 0; t < NJ; ++t) {
+                const int j = lane + 32 * t;
+                if (j < nchunk) {
+                    float4* dst = reinterpret_cast<float4*>(merge + (size_t)warp * dp + j * 8);
+                    dst[0] = make_float4(o[t][0], o[t][1], o[t][2], o[t][3]);
+                    dst[1] = make_float4(o[t][4], o[t][5], o[t][6], o[t][7]);
+                }
+            }
+            named_bar(1, kAttnWarps * 32);
+            float M = -INFINITY;
+#pragma unroll
+            for (int w = 0; w < kAttnWarps; ++w) M = fmaxf(M, a.wm[w]);
+            float scw[kAttnWarps], Lsum = 0.f;
+#pragma unroll
+            for (int w = 0; w < kAttnWarps; ++w) {
+                scw[w] = (a.wm[w] == -INFINITY) ? 0.f : __expf(a.wm[w] - M);
+                Lsum += scw[w] * a.wl[w];
+            }
+            const size_t pidx = (size_t)d.b * st.attn_max_chunks + d.c;
+            for (int i = tid; i < dp; i += kAttnWarps * 32) {
+                float acc = 0.f;
+#pragma unroll
+                for (int w = 0; w < kAttnWarps; ++w) acc += scw[w] * merge[(size_t)w * dp + i];
+                st.attn_o[pidx * dp + i] = acc;
+            }
+            if (tid == 0) {
+                st.attn_ml[pidx * 2 + 0] = M;
+                st.attn_ml[pidx * 2 + 1] = Lsum;
+            }
+            named_bar(1, kAttnWarps * 32);  // all partial stores issued (ordered by the release below)
+            if (lane == 0) mbar_arrive(&a.empty[s]);
+            const int ctx = st.rows.pos[d.b] + 1;
+            const int nch = ((ctx + dm.bc - 1) / dm.bc + st.attn_cb - 1) / st.attn_cb;
+            if (tid == 0) {
+                asm volatile("fence.acq_rel.gpu;" ::: "memory");  // publish the CTA's partial (bar.sync-ordered)
+                a.last_flag = (atom_add_acq_rel(&st.attn_cnt[d.b], 1) == nch - 1);
+            }
+            named_bar(1, kAttnWarps * 32);
+            if (a.last_flag) {
+                const size_t pbase = (size_t)d.b * st.attn_max_chunks;
+                float* cw = a.cw;  // per-chunk weights exp(m_c - M) / L, computed once
+                if (warp == 0) {  // nch <= 128 (host guarantees)
+                    float mc[4], lc[4];
+                    float Mg = -INFINITY;
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int cc = lane + 32 * u;
+                        mc[u] = -INFINITY;
+                        lc[u] = 0.f;
+                        if (cc < nch) {
+                            const float2 ml = __ldcg(reinterpret_cast<const float2*>(st.attn_ml) + pbase + cc);
+                            mc[u] = ml.x;
+                            lc[u] = ml.y;
+                        }
+                        Mg = fmaxf(Mg, mc[u]);
+                    }
+#pragma unroll
+                    for (int off = 16; off; off >>= 1) Mg = fmaxf(Mg, __shfl_xor_sync(0xffffffffu, Mg, off));
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int cc = lane + 32 * u;
+                        if (cc < nch) {
+                            cw[cc] = __expf(mc[u] - Mg);
+                            a.cl[cc] = cw[cc] * lc[u];
+                        }
+                    }
+                    __syncwarp();
+                    float Lg = 0.f;  // fixed chunk order: deterministic
+                    for (int cc = 0; cc < nch; ++cc) Lg += a.cl[cc];
+                    const float inv = 1.f / Lg;
+                    __syncwarp();
+#pragma unroll
+                    for (int u = 0; u < 4; ++u)
+                        if (lane + 32 * u < nch) cw[lane + 32 * u] *= inv;
+                }
+                named_bar(1, kAttnWarps * 32);
+                for (int j = tid; j < nchunk; j += kAttnWarps * 32) {
+                    float acc[8];
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) acc[e] = 0.f;
+                    for (int cc = 0; cc < nch; ++cc) {
+                        const float w = cw[cc];
+                        const float4* src = reinterpret_cast<const float4*>(st.attn_o + (pbase + cc) * dp + j * 8);
+                        const float4 x0 = __ldcg(src), x1 = __ldcg(src + 1);
+                        acc[0] = fmaf(w, x0.x, acc[0]); acc[1] = fmaf(w, x0.y, acc[1]);
+                        acc[2] = fmaf(w, x0.z, acc[2]); acc[3] = fmaf(w, x0.w, acc[3]);
+                        acc[4] = fmaf(w, x1.x, acc[4]); acc[5] = fmaf(w, x1.y, acc[5]);
+                        acc[6] = fmaf(w, x1.z, acc[6]); acc[7] = fmaf(w, x1.w, acc[7]);
+                    }
+                    uint32_t pk[4];
+#pragma unroll
+                    for (int e = 0; e < 4; ++e)
+                        pk[e] = (uint32_t)f32_to_bf16(acc[2 * e]) | ((uint32_t)f32_to_bf16(acc[2 * e + 1]) << 16);
+                    *reinterpret_cast<uint4*>(st.att_b + (size_t)d.b * dp + j * 8) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+                }
+                if (tid == 0) st.attn_cnt[d.b] = 0;
+            }
         }
+        pdl_trigger();
     }
+    // last CTA out resets the work queue for the next launch
+    __syncthreads();
     if (tid == 0) {
-        st.attn_ml[(pbase + c) * 2 + 0] = m_run;
-        st.attn_ml[(pbase + c) * 2 + 1] = l_run;
-    }
-    __threadfence();
-    __syncthreads();
-    if (tid == 0) a.last = (atomicAdd(&st.attn_cnt[b], 1) == nch - 1);
-    __syncthreads();
-    if (!a.last) return;
-    __threadfence();
-    float M = -INFINITY;
-    for (int cc = 0; cc < nch; ++cc) M = fmaxf(M, __ldcg(&st.attn_ml[(pbase + cc) * 2]));
-    float Ls = 0.f;
-    for (int cc = 0; cc < nch; ++cc) Ls += __expf(__ldcg(&st.attn_ml[(pbase + cc) * 2]) - M) * __ldcg(&st.attn_ml[(pbase + cc) * 2 + 1]);
-    const float inv = 1.f / Ls;
-#pragma unroll
-    for (int u = 0; u < 2; ++u) {
-        const int j = tid + 128 * u;
-        if (j >= nchunk) continue;
-        float acc[8];
-#pragma unroll
-        for (int e = 0; e < 8; ++e) acc[e] = 0.f;
-        for (int cc = 0; cc < nch; ++cc) {
-            const float w = __expf(__ldcg(&st.attn_ml[(pbase + cc) * 2]) - M);
-            const float4* src = (const float4*)(st.attn_o + (pbase + cc) * dp + j * 8);
-            const float4 x0 = __ldcg(src), x1 = __ldcg(src + 1);
-            acc[0] = fmaf(w, x0.x, acc[0]); acc[1] = fmaf(w, x0.y, acc[1]);
-            acc[2] = fmaf(w, x0.z, acc[2]); acc[3] = fmaf(w, x0.w, acc[3]);
-            acc[4] = fmaf(w, x1.x, acc[4]); acc[5] = fmaf(w, x1.y, acc[5]);
-            acc[6] = fmaf(w, x1.z, acc[6]); acc[7] = fmaf(w, x1.w, acc[7]);
+        if (atom_add_acq_rel(st.attn_done, 1) == (int)gridDim.x - 1) {
+            *st.attn_queue = 0;
+            *st.attn_done = 0;
         }
-        uint32_t pk[4];
-#pragma unroll
-        for (int e = 0; e < 4; ++e)
-            pk[e] = (uint32_t)f32_to_bf16(acc[2 * e] * inv) | ((uint32_t)f32_to_bf16(acc[2 * e + 1] * inv) << 16);
-        *(uint4*)(st.att_b + (size_t)b * dp + j * 8) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
     }
-    if (tid == 0) st.attn_cnt[b] = 0;
 }
 
 int attn_smem_bytes(const Dims& dm, int stages) {
-    return 256 + (int)((sizeof(AttnSmem) + 127) & ~(size_t)127) + stages * 2 * dm.bc * dm.dp * 2;
+    return (int)((sizeof(AttnSmem) + 127) & ~(size_t)127) + stages * attn_stage_bytes(dm);
 }
 
-void launch_attention(const DevState& st, cudaStream_t s) {
+int attn_threads() { return kAttnThreads; }
+
+void launch_attention(const DevState& st, cudaStream_t s, bool pdl) {
     const int smem = attn_smem_bytes(st.dm, st.attn_stages);
     const int nj = (st.dm.dp / 8 + 31) / 32;
-    dim3 grid(st.attn_max_chunks, st.rows.B);
-#define EL_ATTN(NJV) attn_kernel<NJV><<<grid, 128, smem, s>>>(st)
+    dim3 grid(st.attn_grid);
+#define EL_ATTN(NJV) launch_k(attn_kernel<NJV>, grid, dim3(kAttnThreads), smem, s, pdl, st)
     if (nj <= 1) EL_ATTN(1);
     else if (nj == 2) EL_ATTN(2);
     else if (nj == 3) EL_ATTN(3);
     else EL_ATTN(4);
 #undef EL_ATTN
-    EL_CUDA_LAUNCH_CHECK();
+}
+
+int attn_ctas_per_sm(const Dims& dm, int stages) {
+    int n = 0;
+    const int smem = attn_smem_bytes(dm, stages);
+    const int nj = (dm.dp / 8 + 31) / 32;
+    cudaError_t e;
+    if (nj <= 1) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, attn_kernel<1>, kAttnThreads, smem);
+    else if (nj == 2) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, attn_kernel<2>, kAttnThreads, smem);
+    else if (nj == 3) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, attn_kernel<3>, kAttnThreads, smem);
+    else e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, attn_kernel<4>, kAttnThreads, smem);
+    return (e == cudaSuccess && n > 0) ? n : 1;
 }
 
 // ===========================================================================
@@ -640,6 +887,7 @@ __device__ double block_sum_d(double v) {
 __global__ void __launch_bounds__(256) exit_kernel(DevState st) {
     __shared__ int s_last;
     const int b = blockIdx.x, tid = threadIdx.x;
+    pdl_wait();
     const int layer = *st.layer;
     const int L = st.dm.L, dp = st.dm.dp, Bm = st.dm.Bmax;
     float conf = __int_as_float(0x7fc00000);  // NaN: not computed
@@ -717,9 +965,8 @@ __global__ void __launch_bounds__(256) exit_kernel(DevState st) {
     }
 }
 
-void launch_exit(const DevState& st, cudaStream_t s) {
-    exit_kernel<<<st.rows.B, 256, 0, s>>>(st);
-    EL_CUDA_LAUNCH_CHECK();
+void launch_exit(const DevState& st, cudaStream_t s, bool pdl) {
+    launch_k(exit_kernel, dim3(st.rows.B), dim3(256), 0, s, pdl, st);
 }
 
 // ===========================================================================
@@ -758,6 +1005,7 @@ void launch_embed(const DevState& st, cudaStream_t s) {
 
 __global__ void __launch_bounds__(256) finish_kernel(DevState st) {
     const int b = blockIdx.x, tid = threadIdx.x;
+    pdl_wait();
     const int L = st.dm.L, Bm = st.dm.Bmax;
     const LmRed r = lm_reduce_col(st, b);
     const int cur = *st.cur_iter % st.rec_cap;
@@ -772,9 +1020,8 @@ __global__ void __launch_bounds__(256) finish_kernel(DevState st) {
         st.rows.pos[b] += 1;     // KvStore::commit (engine.cpp:262-264)
     }
 }
-void launch_finish(const DevState& st, cudaStream_t s) {
-    finish_kernel<<<st.rows.B, 256, 0, s>>>(st);
-    EL_CUDA_LAUNCH_CHECK();
+void launch_finish(const DevState& st, cudaStream_t s, bool pdl) {
+    launch_k(finish_kernel, dim3(st.rows.B), dim3(256), 0, s, pdl, st);
 }
 
 __global__ void advance_kernel(DevState st) {
@@ -862,6 +1109,11 @@ void launch_kv_release(int* stack, int top, const int* tables, const Dims& dm, i
 void init_kernel_attributes() {
     const int m = 227 * 1024;
     cudaFuncSetAttribute(gemm_kernel<kGemmQkv>, cudaFuncAttributeMaxDynamicSharedMemorySize, m);
+    cudaFuncSetAttribute(gemm_kernel<kGemmQkv>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaFuncSetAttribute(gemm_kernel<kGemmWo>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaFuncSetAttribute(gemm_kernel<kGemmUp>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaFuncSetAttribute(gemm_kernel<kGemmDown>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaFuncSetAttribute(gemm_kernel<kGemmFill>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     cudaFuncSetAttribute(gemm_kernel<kGemmWo>, cudaFuncAttributeMaxDynamicSharedMemorySize, m);
     cudaFuncSetAttribute(gemm_kernel<kGemmUp>, cudaFuncAttributeMaxDynamicSharedMemorySize, m);
     cudaFuncSetAttribute(gemm_kernel<kGemmDown>, cudaFuncAttributeMaxDynamicSharedMemorySize, m);

@@ -67,10 +67,13 @@ struct DevState {
     int attn_max_chunks;
     int attn_cb;      // blocks per chunk
     int attn_stages;
+    int attn_grid;    // persistent CTAs
+    int* attn_queue;  // work-item counter (reset by the last CTA)
+    int* attn_done;
+    int dbg;          // experiment knob (0 = normal)
+    unsigned long long* dbg_ts;
     float attn_scale; // 1/sqrt(d)
     // split-K GEMM workspace
-    float* gemm_ws;
-    int* gemm_cnt;
     // LM-head per-tile partials [Vp/128][Bmax] {max1, max2, sumexp(rel max1), argmax}
     float4* lm_part;
     // exit status (Algorithm 1 "Status")
@@ -101,24 +104,32 @@ struct DevState {
 struct GemmPlan {
     CUtensorMap tmA;  // weights, box [128 rows][64 k]
     CUtensorMap tmB;  // activations, box [n_pad rows][64 k]
-    int m_tiles, splits, kb_per_split, n_pad, stages, smem_bytes, tmem_cols;
+    int m_tiles, splits, kb_total, n_pad, stages, smem_bytes, tmem_cols;
 };
 
 enum GemmKind : int { kGemmQkv = 0, kGemmWo, kGemmUp, kGemmDown, kGemmLmCheck, kGemmLmFinal, kGemmFill };
 
 int gemm_smem_bytes(int n_pad, int stages, bool tile_reduce);
 void init_kernel_attributes();
-void launch_gemm(GemmKind kind, const GemmPlan& p, const DevState& st, cudaStream_t s);
+void launch_gemm(GemmKind kind, const GemmPlan& p, const DevState& st, cudaStream_t s, bool pdl);
 
 void launch_weightgen(uint16_t* out, int rows, int cols, int rows_p, int cols_p, uint64_t seed, double scale,
                       cudaStream_t s);
 void launch_kv_prefix(const DevState& st, const int* row_seq_ids, int prefix_len, uint64_t kv_seed, int round_bf16,
                       cudaStream_t s);
 void launch_embed(const DevState& st, cudaStream_t s);
+// one attention stage: K block | V block | q (fp32); also hosts the 8-warp merge
+__host__ __device__ inline int attn_stage_bytes(const Dims& dm) {
+    const int kvq = 2 * dm.bc * dm.dp * 2 + dm.dp * 4;
+    const int merge = 8 * dm.dp * 4;
+    return ((kvq > merge ? kvq : merge) + 127) / 128 * 128;
+}
 int attn_smem_bytes(const Dims& dm, int stages);
-void launch_attention(const DevState& st, cudaStream_t s);
-void launch_exit(const DevState& st, cudaStream_t s);
-void launch_finish(const DevState& st, cudaStream_t s);
+int attn_ctas_per_sm(const Dims& dm, int stages);
+int attn_threads();
+void launch_attention(const DevState& st, cudaStream_t s, bool pdl);
+void launch_exit(const DevState& st, cudaStream_t s, bool pdl);
+void launch_finish(const DevState& st, cudaStream_t s, bool pdl);
 void launch_advance(const DevState& st, cudaStream_t s);  // prefill commit: pos += 1
 // LIFO block allocator on the device (kv_cache.cpp:78-106, 182-194)
 void launch_kv_alloc(int* stack, int top, int* tables, const Dims& dm, int slot, int bpl, cudaStream_t s);
