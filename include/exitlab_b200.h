@@ -71,6 +71,9 @@ typedef struct el_transcript el_transcript;
 
 const char* el_last_error(void);
 int el_version(void);
+/* select the CUDA device for engines created by this thread (one process per GPU) */
+int el_set_device(int device);
+int el_device_count(int* n);
 
 int el_engine_create(const el_engine_config* cfg, el_engine** out);
 int el_engine_destroy(el_engine* e);

@@ -956,6 +956,18 @@ extern "C" {
 const char* el_last_error(void) { return g_err.c_str(); }
 int el_version(void) { return 1; }
 
+int el_set_device(int device) {
+    API_BEGIN
+    CK(cudaSetDevice(device));
+    API_END
+}
+
+int el_device_count(int* n) {
+    API_BEGIN
+    CK(cudaGetDeviceCount(n));
+    API_END
+}
+
 int el_engine_create(const el_engine_config* cfg, el_engine** out) {
     API_BEGIN
     if (!cfg || !out) fail(EL_INVALID_ARGUMENT, "null argument");

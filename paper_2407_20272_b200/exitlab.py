@@ -80,6 +80,8 @@ def lib():
         L.el_plan_info.argtypes = [C.c_void_p, C.c_void_p, C.c_int]
         L.el_kv_block_trace.argtypes = [C.c_int] * 4 + [C.c_void_p] * 2 + [C.c_int, C.c_int, C.c_void_p]
         L.el_model_tensor.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_int64]
+        L.el_set_device.argtypes = [C.c_int]
+        L.el_device_count.argtypes = [C.c_void_p]
         _lib = L
     return _lib
 
@@ -458,6 +460,17 @@ class Engine:
         out = np.zeros(int(np.prod(shape)), np.uint16)
         _check(lib().el_model_tensor(self._h, w, layer, _ptr(out), out.size))
         return out.reshape(shape)
+
+
+def set_device(device: int):
+    """Device for engines created afterwards in this thread (one process per GPU)."""
+    _check(lib().el_set_device(int(device)))
+
+
+def device_count() -> int:
+    n = C.c_int(0)
+    _check(lib().el_device_count(C.byref(n)))
+    return n.value
 
 
 def bf16_to_f64(bits: np.ndarray) -> np.ndarray:
