@@ -123,6 +123,7 @@ int el_time_kernel(el_engine* e, int kind, int layer, int reps, float* ms);
 int el_sync(el_engine* e);
 /* experiment support: per-CTA phase timestamps (option "dbg" bit 8) */
 int el_debug_timestamps(el_engine* e, uint64_t* out, int n);
+int el_debug_timeline_reset(el_engine* e);
 /* kernels launched per iteration with the given output layer (for gpu_launches) */
 int el_launches_per_iteration(el_engine* e, int output_layer);
 /* plan details: attention chunking, GEMM splits (for DESIGN / bench reporting) */

@@ -170,13 +170,13 @@ struct el_engine {
     int* cont_dev = nullptr;
 
     // plans
-    CUtensorMap mapA_qkv{}, mapA_wo{}, mapA_up{}, mapA_down{}, mapA_lm{};
     struct Plans {
         el::GemmPlan qkv, wo, up, down, lm, fill;
         int n_pad = 0;
     };
     std::map<int, Plans> plans;  // by n_pad
     int attn_cb = 1, attn_stages = 2, attn_max_chunks = 1, attn_grid = 148;
+    int NR = 16;
 
     // graphs by batch size
     struct Graph {
@@ -260,17 +260,19 @@ struct el_engine {
         emb.alloc((size_t)dm.Vp * dp, false);
         lm.alloc((size_t)dm.Vp * dp, false);
         const double sd = 1.0 / std::sqrt((double)d), s4d = 1.0 / std::sqrt((double)(4 * d));
-        el::launch_weightgen(emb.p, V, d, dm.Vp, dp, tseed(0), sd, stream);
-        el::launch_weightgen(lm.p, V, d, dm.Vp, dp, tseed(1), sd, stream);
+        // embedding stays row-major (row gather); every GEMM operand is tiled + pre-swizzled.
+        // Row blocks of 128 are whole tiles, so a tensor at row offset R starts at tile R/128.
+        el::launch_weightgen(emb.p, V, d, dm.Vp, dp, tseed(0), sd, 0, stream);
+        el::launch_weightgen(lm.p, V, d, dm.Vp, dp, tseed(1), sd, 1, stream);
         for (int i = 0; i < L; ++i) {
             const uint64_t base = 4 + (uint64_t)i * 6;
             uint16_t* q = wqkv.p + (size_t)i * 3 * dp * dp;
-            el::launch_weightgen(q, d, d, dp, dp, tseed(base + 0), sd, stream);
-            el::launch_weightgen(q + (size_t)dp * dp, d, d, dp, dp, tseed(base + 1), sd, stream);
-            el::launch_weightgen(q + (size_t)2 * dp * dp, d, d, dp, dp, tseed(base + 2), sd, stream);
-            el::launch_weightgen(wo.p + (size_t)i * dp * dp, d, d, dp, dp, tseed(base + 3), sd, stream);
-            el::launch_weightgen(wup.p + (size_t)i * fp * dp, 4 * d, d, fp, dp, tseed(base + 4), sd, stream);
-            el::launch_weightgen(wdown.p + (size_t)i * dp * fp, d, 4 * d, dp, fp, tseed(base + 5), s4d, stream);
+            el::launch_weightgen(q, d, d, dp, dp, tseed(base + 0), sd, 1, stream);
+            el::launch_weightgen(q + (size_t)dp * dp, d, d, dp, dp, tseed(base + 1), sd, 1, stream);
+            el::launch_weightgen(q + (size_t)2 * dp * dp, d, d, dp, dp, tseed(base + 2), sd, 1, stream);
+            el::launch_weightgen(wo.p + (size_t)i * dp * dp, d, d, dp, dp, tseed(base + 3), sd, 1, stream);
+            el::launch_weightgen(wup.p + (size_t)i * fp * dp, 4 * d, d, fp, dp, tseed(base + 4), sd, 1, stream);
+            el::launch_weightgen(wdown.p + (size_t)i * dp * fp, d, 4 * d, dp, fp, tseed(base + 5), s4d, 1, stream);
         }
         // probe (tiny: host) -- seeded_vector(d) and b = 2u - 1, both bf16-rounded
         {
@@ -301,13 +303,14 @@ struct el_engine {
         const int Bm = dm.Bmax;
         for (DevBuf<int>* b : {&row_slot, &row_pos, &row_tok, &pf_slot, &pf_pos, &pf_tok, &seq_ids_dev})
             b->alloc((size_t)Bm);
+        NR = std::max(16, round_up(Bm, 16));
         h32.alloc((size_t)2 * Bm * dp);
-        hb.alloc((size_t)2 * Bm * dp);
+        hb.alloc((size_t)2 * NR * dp);
         q32.alloc((size_t)Bm * dp);
-        att_b.alloc((size_t)Bm * dp);
+        att_b.alloc((size_t)NR * dp);
         mid32.alloc((size_t)Bm * dp);
-        mid_b.alloc((size_t)Bm * dp);
-        up_b.alloc((size_t)Bm * fp);
+        mid_b.alloc((size_t)NR * dp);
+        up_b.alloc((size_t)NR * fp);
         attn_cnt.alloc((size_t)Bm);
         attn_queue.alloc(4);
         lm_part.alloc((size_t)(dm.Vp / 128) * Bm);
@@ -331,11 +334,6 @@ struct el_engine {
         CK(cudaHostAlloc(&cont_host, sizeof(int) * 4, cudaHostAllocMapped));
         CK(cudaHostGetDevicePointer((void**)&cont_dev, cont_host, 0));
 
-        mapA_qkv = make_map(wqkv.p, L * 3 * dp, dp, 128);
-        mapA_wo = make_map(wo.p, L * dp, dp, 128);
-        mapA_up = make_map(wup.p, L * fp, dp, 128);
-        mapA_down = make_map(wdown.p, L * dp, fp, 128);
-        mapA_lm = make_map(lm.p, dm.Vp, dp, 128);
         el::init_kernel_attributes();
         slot_bpl.assign((size_t)dm.slots, 0);
         ensure_bpl(1);
@@ -372,12 +370,17 @@ struct el_engine {
         const int B = dm.Bmax;
         // items of ~4 blocks keep the queue balanced; the persistent producer
         // streams across item boundaries, so short items cost no pipeline drain
-        attn_cb = opt_attn_cb ? opt_attn_cb : std::max(1, std::min(16, ceil_div(bpl * B, 148 * 2)));
-        attn_cb = std::min(std::max(attn_cb, ceil_div(bpl, 128)), 32);
-        attn_max_chunks = ceil_div(bpl, attn_cb);
+        // partial slots per sequence: one per CTA segment (<= blocks of the sequence)
+        attn_cb = 1;
+        attn_max_chunks = std::min(bpl, 128);
+        if (bpl > 128) fail(EL_INVALID_ARGUMENT, "attention: more than 128 KV blocks per sequence unsupported");
+        if (B > 256) fail(EL_INVALID_ARGUMENT, "attention: batch > 256 unsupported");
+        (void)opt_attn_cb;
         const int stage_bytes = el::attn_stage_bytes(dm);
         // one persistent CTA per SM with as many block stages as shared memory holds
-        attn_stages = opt_attn_stages ? opt_attn_stages : std::min(8, std::max(2, (224 * 1024) / stage_bytes));
+        // ~3 stages (<= 160 KB): leaves room for a co-resident GEMM CTA, so with
+        // PDL the next/previous kernel's prologue overlaps this one
+        attn_stages = opt_attn_stages ? opt_attn_stages : std::min(8, std::max(2, (160 * 1024) / stage_bytes));
         while (attn_stages > 1 && el::attn_smem_bytes(dm, attn_stages) > 227 * 1024) --attn_stages;
         int sms = 148;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
@@ -401,18 +404,20 @@ struct el_engine {
         int s = (148 + m_tiles / 2) / m_tiles;
         return std::max(1, std::min({s, opt_splits_cap, kb_total}));
     }
-    el::GemmPlan make_plan(const CUtensorMap& A, const CUtensorMap& Bm, int m_tiles, int k, int n_pad, bool tile,
-                           int forced_splits = 0) {
+    el::GemmPlan make_plan(const uint16_t* A, const uint16_t* Bp, size_t b_par_stride, int m_tiles, int k, int n_pad,
+                           bool tile, int forced_splits = 0) {
         el::GemmPlan p;
-        p.tmA = A;
-        p.tmB = Bm;
+        p.A = A;
+        p.Bp = Bp;
+        p.b_par_stride = b_par_stride;
         p.m_tiles = m_tiles;
         p.kb_total = k / 64;
         p.splits = forced_splits ? forced_splits : pick_splits(m_tiles, p.kb_total);
         const int kb_max = ceil_div(p.kb_total, p.splits);
         p.n_pad = n_pad;
         const int stage = 128 * 64 * 2 + n_pad * 64 * 2;
-        p.stages = std::max(1, std::min(kb_max, (200 * 1024) / stage));
+        // LM head: <= ~100 KB so two CTAs share an SM (251 tiles in one wave)
+        p.stages = std::max(1, std::min(kb_max, (tile ? 100 * 1024 : 200 * 1024) / stage));
         p.smem_bytes = el::gemm_smem_bytes(n_pad, p.stages, tile);
         while (p.smem_bytes > 227 * 1024 && p.stages > 1) p.smem_bytes = el::gemm_smem_bytes(n_pad, --p.stages, tile);
         int cols = 32;
@@ -427,16 +432,14 @@ struct el_engine {
         const int dp = dm.dp, fp = dm.fp, Bm = dm.Bmax, L = dm.L;
         Plans P;
         P.n_pad = n_pad;
-        const CUtensorMap mh = make_map(hb.p, 2 * Bm, dp, n_pad);
-        const CUtensorMap ma = make_map(att_b.p, Bm, dp, n_pad);
-        const CUtensorMap mm = make_map(mid_b.p, Bm, dp, n_pad);
-        const CUtensorMap mu = make_map(up_b.p, Bm, fp, n_pad);
-        P.qkv = make_plan(mapA_qkv, mh, 3 * dp / 128, dp, n_pad, false);
-        P.wo = make_plan(mapA_wo, ma, dp / 128, dp, n_pad, false);
-        P.up = make_plan(mapA_up, mm, fp / 128, dp, n_pad, false);
-        P.down = make_plan(mapA_down, mu, dp / 128, fp, n_pad, false);
-        P.lm = make_plan(mapA_lm, mh, dm.Vp / 128, dp, n_pad, true, 1);
-        P.fill = make_plan(mapA_qkv, mh, (L - 1) * (2 * dp / 128), dp, n_pad, false);
+        (void)Bm;
+        const size_t hpar = (size_t)NR * dp;  // hidden-state parity stride
+        P.qkv = make_plan(wqkv.p, hb.p, hpar, 3 * dp / 128, dp, n_pad, false);
+        P.wo = make_plan(wo.p, att_b.p, 0, dp / 128, dp, n_pad, false);
+        P.up = make_plan(wup.p, mid_b.p, 0, fp / 128, dp, n_pad, false);
+        P.down = make_plan(wdown.p, up_b.p, 0, dp / 128, fp, n_pad, false);
+        P.lm = make_plan(lm.p, hb.p, hpar, dm.Vp / 128, dp, n_pad, true, 1);
+        P.fill = make_plan(wqkv.p, hb.p, hpar, (L - 1) * (2 * dp / 128), dp, n_pad, false);
         invalidate_graphs();  // workspace may have moved
         return plans.emplace(n_pad, P).first->second;
     }
@@ -449,6 +452,7 @@ struct el_engine {
         s.kpool = kpool.p; s.vpool = vpool.p; s.tables = tables.p;
         if (prefill) s.rows = el::Rows{pf_slot.p, pf_pos.p, pf_tok.p, B};
         else s.rows = el::Rows{row_slot.p, row_pos.p, row_tok.p, B};
+        s.NR = NR;
         s.h32 = h32.p; s.hb = hb.p; s.q32 = q32.p; s.att_b = att_b.p; s.mid32 = mid32.p; s.mid_b = mid_b.p;
         s.up_b = up_b.p;
         s.attn_o = attn_o.p; s.attn_ml = attn_ml.p; s.attn_cnt = attn_cnt.p;
@@ -1233,6 +1237,19 @@ int el_time_kernel(el_engine* e, int kind, int layer, int reps, float* ms) {
     API_END
 }
 
+int el_debug_timeline_reset(el_engine* e) {
+    API_BEGIN
+    std::vector<unsigned long long> v(2 * 32 * 16);
+    for (size_t i = 0; i < v.size(); i += 2) {
+        v[i] = ~0ull;
+        v[i + 1] = 0;
+    }
+    CK(cudaMemcpyAsync(e->dbg_ts.p + 16384, v.data(), sizeof(unsigned long long) * v.size(), cudaMemcpyHostToDevice,
+                       e->stream));
+    CK(cudaStreamSynchronize(e->stream));
+    API_END
+}
+
 int el_debug_timestamps(el_engine* e, uint64_t* out, int n) {
     API_BEGIN
     CK(cudaStreamSynchronize(e->stream));
@@ -1340,8 +1357,16 @@ int el_model_tensor(el_engine* e, int which, int layer, uint16_t* out, int64_t c
         }
     } else fail(EL_INVALID_ARGUMENT, "bad tensor id");
     if (cap < (int64_t)rows * cols) fail(EL_INVALID_ARGUMENT, "buffer too small");
-    CK(cudaMemcpy2D(out, sizeof(uint16_t) * cols, base, sizeof(uint16_t) * ld, sizeof(uint16_t) * cols, rows,
-                    cudaMemcpyDeviceToHost));
+    if (which == 0) {
+        CK(cudaMemcpy2D(out, sizeof(uint16_t) * cols, base, sizeof(uint16_t) * ld, sizeof(uint16_t) * cols, rows,
+                        cudaMemcpyDeviceToHost));
+    } else {  // tiled + swizzled GEMM operand: copy the padded block and untile on the host
+        const int rows_p = round_up(rows, 128);
+        std::vector<uint16_t> buf((size_t)rows_p * ld);
+        CK(cudaMemcpy(buf.data(), base, sizeof(uint16_t) * buf.size(), cudaMemcpyDeviceToHost));
+        for (int r = 0; r < rows; ++r)
+            for (int c = 0; c < cols; ++c) out[(size_t)r * cols + c] = buf[el::tiled_offset(r, c, ld)];
+    }
     API_END
 }
 

@@ -46,6 +46,17 @@ static void launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, int smem, cu
 }
 
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// device-side kernel timeline (option dbg bit 64): slot = kind * 32 + layer,
+// [2 * slot] = earliest CTA start, [2 * slot + 1] = latest CTA end
+__device__ __forceinline__ void tl_mark(const DevState& st, int kind, int layer, int end) {
+    if ((st.dbg & 64) && threadIdx.x == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+        unsigned long long* slot = st.dbg_ts + 16384 + 2 * (kind * 32 + layer) + end;
+        if (end) atomicMax(slot, t);
+        else atomicMin(slot, t);
+    }
+}
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 // ===========================================================================
@@ -71,6 +82,24 @@ constexpr int kAStage = kBM * kBK * 2;  // 16 KB
 template <GemmKind K>
 struct Epi;
 
+// LM-head partial over a vocab range: max, second max (with duplicates),
+// sum exp(l - max), argmax (lowest index on ties)
+struct LmPart {
+    float m1, m2, s;
+    int idx;
+};
+__device__ __forceinline__ LmPart lm_part_merge(LmPart a, LmPart b) {
+    const bool take_b = b.m1 > a.m1 || (b.m1 == a.m1 && b.idx < a.idx);
+    const LmPart& hi = take_b ? b : a;
+    const LmPart& lo = take_b ? a : b;
+    LmPart r;
+    r.m1 = hi.m1;
+    r.idx = hi.idx;
+    r.m2 = fmaxf(lo.m1, hi.m2);
+    r.s = hi.s + (lo.m1 == -INFINITY ? 0.f : lo.s * __expf(lo.m1 - hi.m1));
+    return r;
+}
+
 // --- q | k | v projection; K,V scattered into the paged pool at (slot, layer, pos)
 //     (model.cpp:218-226: matvec_batch w_q/w_k/w_v + KvStore::append)
 template <>
@@ -81,7 +110,7 @@ struct Epi<kGemmQkv> {
         e.layer = layer;
         e.row0 = tile * kBM;
         a_row = (layer - 1) * 3 * st.dm.dp + tile * kBM;
-        b_row = ((layer - 1) & 1) * st.dm.Bmax;
+        b_row = (layer - 1) & 1;
         return true;
     }
     __device__ static void prologue(const DevState& st, EpiSmem& e) {
@@ -115,7 +144,7 @@ struct Epi<kGemmFill> {
         e.layer = j;
         e.row0 = (tile % t2) * kBM;
         a_row = (j - 1) * 3 * st.dm.dp + st.dm.dp + e.row0;
-        b_row = (eo & 1) * st.dm.Bmax;
+        b_row = eo & 1;
         return true;
     }
     __device__ static void prologue(const DevState& st, EpiSmem& e) { Epi<kGemmQkv>::prologue(st, e); }
@@ -147,7 +176,7 @@ struct Epi<kGemmWo> {
         const float h = st.h32[(size_t)e.par_in * st.dm.Bmax * dp + i];
         const float o = h + v;
         st.mid32[i] = o;
-        st.mid_b[i] = f32_to_bf16(o);
+        st.mid_b[act_offset(col, e.row0 + row, st.NR)] = f32_to_bf16(o);
     }
 };
 
@@ -165,7 +194,7 @@ struct Epi<kGemmUp> {
     }
     __device__ static void prologue(const DevState&, EpiSmem&) {}
     __device__ static void apply(const DevState& st, const EpiSmem& e, int row, int col, float v) {
-        st.up_b[(size_t)col * st.dm.fp + e.row0 + row] = f32_to_bf16(v > 0.f ? v : 0.f);
+        st.up_b[act_offset(col, e.row0 + row, st.NR)] = f32_to_bf16(v > 0.f ? v : 0.f);
     }
 };
 
@@ -187,9 +216,8 @@ struct Epi<kGemmDown> {
         const int dp = st.dm.dp;
         const size_t i = (size_t)col * dp + e.row0 + row;
         const float o = st.mid32[i] + v;
-        const size_t j = (size_t)e.par_out * st.dm.Bmax * dp + i;
-        st.h32[j] = o;
-        st.hb[j] = f32_to_bf16(o);
+        st.h32[(size_t)e.par_out * st.dm.Bmax * dp + i] = o;
+        st.hb[(size_t)e.par_out * (size_t)st.NR * dp + act_offset(col, e.row0 + row, st.NR)] = f32_to_bf16(o);
     }
 };
 
@@ -199,34 +227,58 @@ struct Epi<kGemmDown> {
 template <GemmKind K>
 struct EpiLm {
     static constexpr bool kTile = true;
+    static constexpr bool kFull = (K == kGemmLmCheck);  // softmax check needs max2 + sum exp; greedy only argmax
     __device__ static bool setup(const DevState& st, int tile, EpiSmem& e, int& a_row, int& b_row) {
         const int par = (K == kGemmLmCheck) ? (*st.layer & 1) : (*st.out_layer & 1);
         e.row0 = tile * kBM;
         a_row = tile * kBM;
-        b_row = par * st.dm.Bmax;
+        b_row = par;
         return true;
     }
     __device__ static void prologue(const DevState&, EpiSmem&) {}
-    // sm: [n][129] logits of this tile (column n = batch row)
+    // sm: [n][129] logits of this tile (column n = batch row). R threads per
+    // column scan disjoint row ranges in index order, then merge in a fixed
+    // shuffle tree (lowest index wins ties).
     __device__ static void tile_reduce(const DevState& st, const EpiSmem& e, int tile, const float* sm) {
-        const int n = threadIdx.x;
-        if (n >= st.rows.B) return;
+        const int nb = st.rows.B;
         const int rows = min(kBM, st.dm.V - e.row0);
-        float m1 = -INFINITY, m2 = -INFINITY, s = 0.f;
-        int idx = 0;
-        for (int r = 0; r < rows; ++r) {
-            const float x = sm[n * 129 + r];
-            if (x > m1) {
-                m2 = m1;
-                s = (m1 == -INFINITY) ? 1.f : s * __expf(m1 - x) + 1.f;
-                m1 = x;
-                idx = e.row0 + r;
-            } else {
-                if (x > m2) m2 = x;
-                s += __expf(x - m1);
+        int R = 1;
+        while (R < 32 && R * 2 * nb <= kBM) R *= 2;
+        const int tid = threadIdx.x;
+        for (int cbase = 0; cbase < nb; cbase += kBM / R) {
+            const int n = cbase + tid / R, part = tid % R;
+            const int r0 = part * (kBM / R), r1 = min(rows, r0 + kBM / R);
+            float m1 = -INFINITY, m2 = -INFINITY, s = 0.f;
+            int idx = 0x7fffffff;
+            if (n < nb) {
+                const float* col = sm + n * 129;
+                for (int r = r0; r < r1; ++r) {
+                    const float x = col[r];
+                    if (x > m1) {
+                        if (kFull) {
+                            m2 = m1;
+                            s = s * __expf(m1 - x) + 1.f;
+                        }
+                        m1 = x;
+                        idx = e.row0 + r;
+                    } else if (kFull) {
+                        m2 = fmaxf(m2, x);
+                        s += __expf(x - m1);
+                    }
+                }
             }
+            LmPart p{m1, m2, s, idx};
+            for (int off = 1; off < R; off <<= 1) {  // lanes of one column are consecutive
+                LmPart q;
+                q.m1 = __shfl_xor_sync(0xffffffffu, p.m1, off);
+                q.m2 = __shfl_xor_sync(0xffffffffu, p.m2, off);
+                q.s = __shfl_xor_sync(0xffffffffu, p.s, off);
+                q.idx = __shfl_xor_sync(0xffffffffu, p.idx, off);
+                p = (part & off) ? lm_part_merge(q, p) : lm_part_merge(p, q);
+            }
+            if (part == 0 && n < nb)
+                st.lm_part[(size_t)tile * st.dm.Bmax + n] = make_float4(p.m1, p.m2, p.s, __int_as_float(p.idx));
         }
-        st.lm_part[(size_t)tile * st.dm.Bmax + n] = make_float4(m1, m2, s, __int_as_float(idx));
     }
 };
 template <>
@@ -235,6 +287,10 @@ template <>
 struct Epi<kGemmLmFinal> : EpiLm<kGemmLmFinal> {};
 
 struct GemmArgs {
+    const uint16_t* A;   // weights in tiled, pre-swizzled layout (tiled_offset)
+    const uint16_t* Bp;  // activations in act_offset layout
+    size_t b_par_stride;
+    int NR;
     int m_tiles, splits, kb_total, n_pad, stages, tmem_cols, pdl;
 };
 
@@ -251,11 +307,11 @@ __device__ __forceinline__ void cluster_sync_all() {
 // HBM latency overlaps the producer kernel's tail.
 template <GemmKind K>
 __global__ void __launch_bounds__(128, 1)
-    gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, GemmArgs g,
-                DevState st) {
+    gemm_kernel(GemmArgs g, DevState st) {
     using E = Epi<K>;
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    // 1024-byte alignment by pointer offset (keeps the shared address space visible to the compiler)
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     const int tile = blockIdx.x, split = blockIdx.y;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
@@ -263,14 +319,18 @@ __global__ void __launch_bounds__(128, 1)
     uint8_t* sA = smem;
     uint8_t* sB = smem + (size_t)g.stages * kAStage;
     size_t region = (size_t)g.stages * (kAStage + b_stage);
-    const size_t part_bytes = (size_t)g.n_pad * kBM * 4;
+    const size_t part_bytes = E::kTile ? (size_t)g.n_pad * 129 * 4 : (size_t)g.n_pad * kBM * 4;
     if ((E::kTile || g.splits > 1) && region < part_bytes) region = part_bytes;
-    uint64_t* full = (uint64_t*)(smem + region);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + region);
     uint64_t* empty = full + g.stages;
     uint64_t* accf = empty + g.stages;
-    uint32_t* tmem_slot = (uint32_t*)(accf + 1);
-    EpiSmem& es = *(EpiSmem*)(((uintptr_t)(tmem_slot + 4) + 15) & ~(uintptr_t)15);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accf + 1);
+    EpiSmem& es = *reinterpret_cast<EpiSmem*>(smem + region + (2 * g.stages + 1) * 8 + 16);
 
+    constexpr int tl_kind = K == kGemmQkv ? 1 : K == kGemmWo ? 3 : K == kGemmUp ? 4 : K == kGemmDown ? 5
+                          : K == kGemmLmCheck ? 10 : K == kGemmLmFinal ? 8 : 7;
+    const int tl_layer = (K == kGemmLmFinal || K == kGemmFill) ? 0 : *st.layer;
+    tl_mark(st, tl_kind, tl_layer, 0);
     auto stamp = [&](int i) {
         if ((st.dbg & 8) && tid == 0) {
             unsigned long long t;
@@ -282,10 +342,8 @@ __global__ void __launch_bounds__(128, 1)
     int a_row = 0, b_row = 0;
     // setup() only reads layer / output-layer counters written before this
     // kernel's predecessor started (see el_kernels.h), so it may run pre-wait.
-    if (!E::setup(st, tile, es, a_row, b_row)) {  // uniform across the CTA and its cluster
-        if (g.pdl) pdl_trigger();
-        return;
-    }
+    pdl_trigger();  // single-wave grid: let the next kernel's prologue start now (no-op without a dependent)
+    if (!E::setup(st, tile, es, a_row, b_row)) return;  // uniform across the CTA and its cluster
     const int kb0 = (int)((long)split * g.kb_total / g.splits);
     const int kb1 = (int)((long)(split + 1) * g.kb_total / g.splits);
     const int nkb = kb1 - kb0;
@@ -307,22 +365,30 @@ __global__ void __launch_bounds__(128, 1)
 
     if (warp == 0 && lane == 0) {
         // ---- TMA producer ----
-        tma_prefetch_desc(&tmA);
-        tma_prefetch_desc(&tmB);
         const int pre = min(nkb, g.stages);
+        // weights: one contiguous 16 KB bulk copy per 128x64 tile (stored pre-swizzled)
+        const uint16_t* a_tiles = g.A + (size_t)(a_row / kBM) * g.kb_total * (kBM * kBK);
         for (int kb = 0; kb < pre; ++kb) {  // weights first: independent of the previous kernel
             mbar_arrive_expect_tx(&full[kb], kAStage + b_stage);
-            tma_load_2d(sA + (size_t)kb * kAStage, &tmA, &full[kb], (kb0 + kb) * kBK, a_row);
+            bulk_load(sA + (size_t)kb * kAStage, a_tiles + (size_t)(kb0 + kb) * (kBM * kBK), kAStage, &full[kb]);
         }
-        if (g.pdl) pdl_wait();
+        // activations: the first n_pad rows of a k-block tile are contiguous
+        const uint16_t* b_tiles = g.Bp + (size_t)b_row * g.b_par_stride;
+        const size_t b_kstride = (size_t)g.NR * kBK;
+        pdl_wait();  // no-op unless launched as a PDL secondary
         for (int kb = 0; kb < pre; ++kb)
-            tma_load_2d(sB + (size_t)kb * b_stage, &tmB, &full[kb], (kb0 + kb) * kBK, b_row);
+            bulk_load(sB + (size_t)kb * b_stage, b_tiles + (size_t)(kb0 + kb) * b_kstride, b_stage, &full[kb]);
         for (int kb = pre; kb < nkb; ++kb) {
             const int s = kb % g.stages;
             mbar_wait(&empty[s], ((kb / g.stages) - 1) & 1);
+            if ((st.dbg & 16) && blockIdx.x == 0 && blockIdx.y == 0 && kb < 64) {
+                unsigned long long t;
+                asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+                st.dbg_ts[4096 + 64 + kb] = t;
+            }
             mbar_arrive_expect_tx(&full[s], kAStage + b_stage);
-            tma_load_2d(sA + (size_t)s * kAStage, &tmA, &full[s], (kb0 + kb) * kBK, a_row);
-            tma_load_2d(sB + (size_t)s * b_stage, &tmB, &full[s], (kb0 + kb) * kBK, b_row);
+            bulk_load(sA + (size_t)s * kAStage, a_tiles + (size_t)(kb0 + kb) * (kBM * kBK), kAStage, &full[s]);
+            bulk_load(sB + (size_t)s * b_stage, b_tiles + (size_t)(kb0 + kb) * b_kstride, b_stage, &full[s]);
         }
     } else if (warp == 1 && lane == 0) {
         // ---- MMA issuer (single thread) ----
@@ -330,6 +396,11 @@ __global__ void __launch_bounds__(128, 1)
         for (int kb = 0; kb < nkb; ++kb) {
             const int s = kb % g.stages;
             mbar_wait(&full[s], (kb / g.stages) & 1);
+            if ((st.dbg & 16) && blockIdx.x == 0 && blockIdx.y == 0 && kb < 64) {
+                unsigned long long t;
+                asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+                st.dbg_ts[4096 + kb] = t;
+            }
             tc_fence_after();
             const uint64_t ad = sdesc_k_sw128(smem_u32(sA + (size_t)s * kAStage));
             const uint64_t bd = sdesc_k_sw128(smem_u32(sB + (size_t)s * b_stage));
@@ -341,8 +412,7 @@ __global__ void __launch_bounds__(128, 1)
         tc_commit(accf);
     }
     __syncwarp();
-    if (g.pdl) pdl_wait();  // epilogue reads activations of earlier kernels
-    if (g.pdl) pdl_trigger();
+    pdl_wait();  // epilogue reads activations of earlier kernels
 
     // ---- epilogue: all four warps, thread t <-> TMEM lane t <-> output row t ----
     E::prologue(st, es);
@@ -357,7 +427,7 @@ __global__ void __launch_bounds__(128, 1)
 
     if constexpr (E::kTile) {
         // splits == 1: transpose the tile through smem (stage buffers are free now)
-        float* sm = (float*)smem;
+        float* sm = reinterpret_cast<float*>(smem);
         for (int c0 = 0; c0 < nval; c0 += 16) {
             float v[16];
             tmem_ld16(trow + (uint32_t)c0, v);
@@ -376,18 +446,18 @@ __global__ void __launch_bounds__(128, 1)
                 if (c0 + j < nval) E::apply(st, es, row, c0 + j, v[j]);
         }
     } else {
-        float* part = (float*)smem;  // [n][128], stage buffers are free now
+        // partial tile [n][128] fp32: a warp's DSMEM loads below are 128 contiguous bytes
+        float* part = reinterpret_cast<float*>(smem);
         for (int c0 = 0; c0 < nval; c0 += 16) {
             float v[16];
             tmem_ld16(trow + (uint32_t)c0, v);
 #pragma unroll
-            for (int j = 0; j < 16; ++j)
-                if (c0 + j < nval) part[(c0 + j) * kBM + row] = v[j];
+            for (int j = 0; j < 16; ++j) part[(c0 + j) * kBM + row] = v[j];
         }
         cluster_sync_all();
         stamp(4);
-        // this CTA owns columns [c0, c1); all remote loads of a column group are
-        // issued before the (fixed-order) sums so DSMEM latency overlaps
+        // this CTA owns columns [c0, c1); all DSMEM loads of a column group are
+        // issued before the (fixed rank order) sums so the latency overlaps
         const int per = (nval + g.splits - 1) / g.splits;
         const int c0 = split * per, c1 = min(nval, c0 + per);
         const float* peer[8];
@@ -419,6 +489,7 @@ __global__ void __launch_bounds__(128, 1)
     __syncthreads();
     if (warp == 1) tmem_dealloc(tmem, (uint32_t)g.tmem_cols);
     stamp(7);
+    tl_mark(st, tl_kind, tl_layer, 1);
 }
 
 int gemm_smem_bytes(int n_pad, int stages, bool tile_reduce) {
@@ -430,7 +501,8 @@ int gemm_smem_bytes(int n_pad, int stages, bool tile_reduce) {
 
 template <GemmKind K>
 static void launch_gemm_t(const GemmPlan& p, const DevState& st, cudaStream_t s, bool pdl) {
-    GemmArgs g{p.m_tiles, p.splits, p.kb_total, p.n_pad, p.stages, p.tmem_cols, pdl ? 1 : 0};
+    GemmArgs g{p.A, p.Bp, p.b_par_stride, st.NR, p.m_tiles, p.splits, p.kb_total, p.n_pad, p.stages, p.tmem_cols,
+               pdl ? 1 : 0};
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(p.m_tiles, p.splits);
     cfg.blockDim = dim3(128);
@@ -452,7 +524,7 @@ static void launch_gemm_t(const GemmPlan& p, const DevState& st, cudaStream_t s,
     }
     cfg.attrs = at;
     cfg.numAttrs = na;
-    cudaLaunchKernelEx(&cfg, gemm_kernel<K>, p.tmA, p.tmB, g, st);
+    cudaLaunchKernelEx(&cfg, gemm_kernel<K>, g, st);
     EL_CUDA_LAUNCH_CHECK();
 }
 
@@ -493,7 +565,7 @@ constexpr int kAttnWarps = 8;
 constexpr int kAttnThreads = (kAttnWarps + 1) * 32;
 
 struct AttnDesc {
-    int b, c, rows, first, last, pad[3];
+    int b, c, rows, first, last, nseg, pad[2];  // c = partial slot of this CTA's segment of sequence b
 };
 struct AttnSmem {
     uint64_t full[8];
@@ -502,8 +574,9 @@ struct AttnSmem {
     float wm[kAttnWarps], wl[kAttnWarps];
     float cw[128];
     float cl[128];
+    int pref[257];  // block prefix sum over the batch rows
     int last_flag;
-    int pad[3];
+    int pad[2];
 };
 
 __device__ __forceinline__ float dot8p(uint4 k, const float* q) {
@@ -543,7 +616,13 @@ __global__ void __launch_bounds__(kAttnThreads) attn_kernel(DevState st) {
     AttnSmem& a = *reinterpret_cast<AttnSmem*>(smem_raw);
     uint8_t* stages = smem_raw + ((sizeof(AttnSmem) + 127) & ~(size_t)127);
     const int layer = *st.layer;
-    const int n_items = st.rows.B * st.attn_max_chunks;
+    tl_mark(st, 2, layer, 0);
+    if ((st.dbg & 32) && tid == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+        if (blockIdx.x < 4) st.dbg_ts[8192 + 4 * 128 + blockIdx.x] = t;
+        st.dbg_ts[24576 + 4 * blockIdx.x] = t;
+    }
 
     if (tid == 0) {
         for (int s = 0; s < S; ++s) {
@@ -556,41 +635,112 @@ __global__ void __launch_bounds__(kAttnThreads) attn_kernel(DevState st) {
 
     if (warp == kAttnWarps) {
         // ---------------- producer warp ----------------
-        // lane 0 drives the ring; the whole warp fetches an item's block ids
-        // in parallel (one global latency per item instead of one per block)
-        pdl_wait();  // this layer's K/V at `pos` and q come from the QKV kernel
+        // Static balanced split: the batch's KV blocks are flattened in (row,
+        // block) order and CTA i streams [i*T/G, (i+1)*T/G) -- equal work per SM,
+        // no queue, at most a few sequence segments per CTA.  Lane 0 drives the
+        // ring; the warp fetches block ids in parallel.  Before
+        // griddepcontrol.wait only K/V written by earlier iterations is
+        // streamed; q and the block holding `pos` (written by this layer's QKV
+        // kernel) are requested after it (one pending stage).
+        const int B = st.rows.B;
+        {  // warp-parallel prefix sum of blocks per row
+            int base = 0;
+            for (int r0 = 0; r0 < B; r0 += 32) {
+                const int r = r0 + lane;
+                int v = (r < B) ? (st.rows.pos[r] + dm.bc) / dm.bc : 0;
+#pragma unroll
+                for (int off = 1; off < 32; off <<= 1) {
+                    const int t = __shfl_up_sync(0xffffffffu, v, off);
+                    if (lane >= off) v += t;
+                }
+                if (r < B) a.pref[r + 1] = base + v;
+                base += __shfl_sync(0xffffffffu, v, 31);
+            }
+            if (lane == 0) a.pref[0] = 0;
+            __syncwarp();
+        }
+        // with fewer blocks than CTAs only the first T CTAs work (every range non-empty,
+        // so each CTA between a sequence's first and last owner contributes a partial)
+        const long long T = a.pref[B], G = min((long long)gridDim.x, T);
+        auto cta_of = [&](long long g) { return (int)(((g + 1) * G + T - 1) / T - 1); };
+        const bool active = (long long)blockIdx.x < G;
+        const long long g0 = active ? (long long)blockIdx.x * T / G : 0, g1 = active ? (long long)(blockIdx.x + 1) * T / G : 0;
+        bool waited = false;
+        int dq = -1, ds = -1, did = 0;
+        uint32_t dbytes = 0;
+        auto flush = [&]() {
+            if (!waited) {
+                pdl_wait();
+                waited = true;
+            }
+            if (ds >= 0) {
+                uint8_t* sb = stages + (size_t)ds * stage_bytes;
+                if (dq >= 0) bulk_load(sb + 2 * blk_bytes, st.q32 + (size_t)dq * dp, (uint32_t)dp * 4, &a.full[ds]);
+                if (dbytes) {
+                    bulk_load(sb, st.kpool + (size_t)did * dm.bc * dp, dbytes, &a.full[ds]);
+                    bulk_load(sb + blk_bytes, st.vpool + (size_t)did * dm.bc * dp, dbytes, &a.full[ds]);
+                }
+                ds = -1;
+                dq = -1;
+                dbytes = 0;
+            }
+        };
         int seq = 0;
-        for (;;) {
-            int item = 0;
-            if (lane == 0) item = atomicAdd(st.attn_queue, 1);
-            item = __shfl_sync(0xffffffffu, item, 0);
-            if (item >= n_items) break;
-            const int b = item / st.attn_max_chunks, c = item % st.attn_max_chunks;
+        int b = 0;
+        while (b < B && a.pref[b + 1] <= g0) ++b;
+        for (long long g = g0; g < g1 && b < B;) {
+            // one segment: blocks [g, seg_end) of row b
+            const long long sb0 = a.pref[b], sb1 = a.pref[b + 1];
+            const long long seg_end = min(g1, sb1);
+            const int nblk = (int)(sb1 - sb0);
             const int ctx = st.rows.pos[b] + 1;
-            const int nblk = (ctx + dm.bc - 1) / dm.bc;
-            const int blk0 = c * st.attn_cb;
-            if (blk0 >= nblk) continue;
-            const int blk1 = min(nblk, blk0 + st.attn_cb);
+            const int cfirst = cta_of(sb0);
+            const int slot = (int)blockIdx.x - cfirst, nseg = cta_of(sb1 - 1) - cfirst + 1;
             const int* table = st.tables + ((size_t)st.rows.slot[b] * dm.L + (layer - 1)) * dm.bpl_max;
-            const int my_id = (blk0 + lane < blk1) ? table[blk0 + lane] : 0;  // attn_cb <= 32
-            for (int blk = blk0; blk < blk1; ++blk, ++seq) {
-                const int id = __shfl_sync(0xffffffffu, my_id, blk - blk0);
-                if (lane == 0) {
-                    const int s = seq % S;
-                    if (seq >= S) mbar_wait(&a.empty[s], ((seq / S) - 1) & 1);
-                    const int rows = min(dm.bc, ctx - blk * dm.bc);
-                    const uint32_t bytes = (uint32_t)rows * dp * 2;
-                    const bool first = blk == blk0;
-                    a.desc[s] = AttnDesc{b, c, rows, first, blk == blk1 - 1, {0, 0, 0}};
-                    uint8_t* sb = stages + (size_t)s * stage_bytes;
-                    mbar_arrive_expect_tx(&a.full[s], 2 * bytes + (first ? (uint32_t)dp * 4 : 0u));
-                    if (first) bulk_load(sb + 2 * blk_bytes, st.q32 + (size_t)b * dp, (uint32_t)dp * 4, &a.full[s]);
-                    bulk_load(sb, st.kpool + (size_t)id * dm.bc * dp, bytes, &a.full[s]);
-                    bulk_load(sb + blk_bytes, st.vpool + (size_t)id * dm.bc * dp, bytes, &a.full[s]);
+            for (long long gb = g; gb < seg_end; gb += 32) {
+                const int blk_base = (int)(gb - sb0);
+                const int nb = (int)min(32LL, seg_end - gb);
+                const int my_id = (lane < nb) ? table[blk_base + lane] : 0;
+                for (int u = 0; u < nb; ++u, ++seq) {
+                    const int id = __shfl_sync(0xffffffffu, my_id, u);
+                    const int blk = blk_base + u;
+                    if (lane == 0) {
+                        const int s = seq % S;
+                        if (seq >= S) {
+                            if (!waited) flush();  // the ring is full: release the deferred stage first
+                            mbar_wait(&a.empty[s], ((seq / S) - 1) & 1);
+                        }
+                        const int rows = min(dm.bc, ctx - blk * dm.bc);
+                        const uint32_t bytes = (uint32_t)rows * dp * 2;
+                        const bool first = (gb + u) == g, newest = blk == nblk - 1;
+                        a.desc[s] = AttnDesc{b, slot, rows, first, (gb + u) == seg_end - 1, nseg, {0, 0}};
+                        uint8_t* sbuf = stages + (size_t)s * stage_bytes;
+                        mbar_arrive_expect_tx(&a.full[s], 2 * bytes + (first ? (uint32_t)dp * 4 : 0u));
+                        if (!waited && (first || newest) && ds >= 0) flush();  // one pending stage at most
+                        if (!waited && (first || newest)) {
+                            ds = s;
+                            dq = first ? b : -1;
+                            if (newest) {
+                                did = id;
+                                dbytes = bytes;
+                            } else {
+                                bulk_load(sbuf, st.kpool + (size_t)id * dm.bc * dp, bytes, &a.full[s]);
+                                bulk_load(sbuf + blk_bytes, st.vpool + (size_t)id * dm.bc * dp, bytes, &a.full[s]);
+                            }
+                        } else {
+                            if (first)
+                                bulk_load(sbuf + 2 * blk_bytes, st.q32 + (size_t)b * dp, (uint32_t)dp * 4, &a.full[s]);
+                            bulk_load(sbuf, st.kpool + (size_t)id * dm.bc * dp, bytes, &a.full[s]);
+                            bulk_load(sbuf + blk_bytes, st.vpool + (size_t)id * dm.bc * dp, bytes, &a.full[s]);
+                        }
+                    }
                 }
                 __syncwarp();
             }
+            g = seg_end;
+            ++b;
         }
+        if (lane == 0) flush();  // short run: anything still deferred
         if (lane == 0) {
             const int s = seq % S;  // terminal descriptor
             if (seq >= S) mbar_wait(&a.empty[s], ((seq / S) - 1) & 1);
@@ -606,6 +756,13 @@ __global__ void __launch_bounds__(kAttnThreads) attn_kernel(DevState st) {
             const int s = seq % S;
             mbar_wait(&a.full[s], (seq / S) & 1);
             const AttnDesc d = a.desc[s];
+            if ((st.dbg & 32) && tid == 0) {
+                unsigned long long t;
+                asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+                if (blockIdx.x < 4 && seq < 60) st.dbg_ts[8192 + blockIdx.x * 128 + seq] = t;
+                if (seq == 0) st.dbg_ts[24576 + 4 * blockIdx.x + 1] = t;
+                st.dbg_ts[24576 + 4 * blockIdx.x + 2] = t;
+            }
             if (d.b < 0) break;
             uint8_t* sb = stages + (size_t)s * stage_bytes;
             const uint4* sk = reinterpret_cast<const uint4*>(sb);
@@ -711,8 +868,7 @@ __global__ void __launch_bounds__(kAttnThreads) attn_kernel(DevState st) {
             }
             named_bar(1, kAttnWarps * 32);  // all partial stores issued (ordered by the release below)
             if (lane == 0) mbar_arrive(&a.empty[s]);
-            const int ctx = st.rows.pos[d.b] + 1;
-            const int nch = ((ctx + dm.bc - 1) / dm.bc + st.attn_cb - 1) / st.attn_cb;
+            const int nch = d.nseg;
             if (tid == 0) {
                 asm volatile("fence.acq_rel.gpu;" ::: "memory");  // publish the CTA's partial (bar.sync-ordered)
                 a.last_flag = (atom_add_acq_rel(&st.attn_cnt[d.b], 1) == nch - 1);
@@ -773,21 +929,19 @@ __global__ void __launch_bounds__(kAttnThreads) attn_kernel(DevState st) {
 #pragma unroll
                     for (int e = 0; e < 4; ++e)
                         pk[e] = (uint32_t)f32_to_bf16(acc[2 * e]) | ((uint32_t)f32_to_bf16(acc[2 * e + 1]) << 16);
-                    *reinterpret_cast<uint4*>(st.att_b + (size_t)d.b * dp + j * 8) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+                    *reinterpret_cast<uint4*>(st.att_b + act_offset(d.b, j * 8, st.NR)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
                 }
                 if (tid == 0) st.attn_cnt[d.b] = 0;
             }
         }
         pdl_trigger();
     }
-    // last CTA out resets the work queue for the next launch
-    __syncthreads();
-    if (tid == 0) {
-        if (atom_add_acq_rel(st.attn_done, 1) == (int)gridDim.x - 1) {
-            *st.attn_queue = 0;
-            *st.attn_done = 0;
-        }
+    if ((st.dbg & 32) && tid == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+        st.dbg_ts[24576 + 4 * blockIdx.x + 3] = t;
     }
+    tl_mark(st, 2, layer, 1);
 }
 
 int attn_smem_bytes(const Dims& dm, int stages) {
@@ -888,7 +1042,9 @@ __global__ void __launch_bounds__(256) exit_kernel(DevState st) {
     __shared__ int s_last;
     const int b = blockIdx.x, tid = threadIdx.x;
     pdl_wait();
+    pdl_trigger();
     const int layer = *st.layer;
+    tl_mark(st, 6, layer, 0);
     const int L = st.dm.L, dp = st.dm.dp, Bm = st.dm.Bmax;
     float conf = __int_as_float(0x7fc00000);  // NaN: not computed
     int acc = 0;
@@ -941,6 +1097,7 @@ __global__ void __launch_bounds__(256) exit_kernel(DevState st) {
     __syncthreads();
     if (tid == 0) s_last = (atomicAdd(st.exit_cnt, 1) == st.rows.B - 1);
     __syncthreads();
+    tl_mark(st, 6, layer, 1);
     if (!s_last) return;
     __threadfence();
     int all = 1;
@@ -975,16 +1132,17 @@ void launch_exit(const DevState& st, cudaStream_t s, bool pdl) {
 // ===========================================================================
 __global__ void embed_kernel(DevState st) {
     const int b = blockIdx.x;
+    tl_mark(st, 0, 0, 0);
     const int dp = st.dm.dp;
     const int tok = st.rows.tok[b];
     const uint16_t* e = st.emb + (size_t)tok * dp;
     float* h = st.h32 + (size_t)b * dp;
-    uint16_t* hb = st.hb + (size_t)b * dp;
     for (int i = threadIdx.x; i < dp; i += blockDim.x) {
         const uint16_t x = e[i];
-        hb[i] = x;
+        st.hb[act_offset(b, i, st.NR)] = x;
         h[i] = bf16_to_f32(x);
     }
+    tl_mark(st, 0, 0, 1);
     if (b == 0) {
         for (int r = threadIdx.x; r < st.dm.Bmax; r += blockDim.x) {
             st.status[r] = 0;
@@ -1006,6 +1164,7 @@ void launch_embed(const DevState& st, cudaStream_t s) {
 __global__ void __launch_bounds__(256) finish_kernel(DevState st) {
     const int b = blockIdx.x, tid = threadIdx.x;
     pdl_wait();
+    tl_mark(st, 9, 0, 0);
     const int L = st.dm.L, Bm = st.dm.Bmax;
     const LmRed r = lm_reduce_col(st, b);
     const int cur = *st.cur_iter % st.rec_cap;
@@ -1019,6 +1178,7 @@ __global__ void __launch_bounds__(256) finish_kernel(DevState st) {
         st.rows.tok[b] = r.idx;  // next input (engine.cpp:304)
         st.rows.pos[b] += 1;     // KvStore::commit (engine.cpp:262-264)
     }
+    tl_mark(st, 9, 0, 1);
 }
 void launch_finish(const DevState& st, cudaStream_t s, bool pdl) {
     launch_k(finish_kernel, dim3(st.rows.B), dim3(256), 0, s, pdl, st);
@@ -1037,18 +1197,18 @@ void launch_advance(const DevState& st, cudaStream_t s) {
 // 5. setup kernels: seeded weights (model.cpp:37-59) and the seeded KV prefix
 // ===========================================================================
 __global__ void weightgen_kernel(uint16_t* out, int rows, int cols, int rows_p, int cols_p, uint64_t seed,
-                                 double scale) {
+                                 double scale, int tiled) {
     const size_t n = (size_t)rows_p * cols_p;
     for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
         const int r = (int)(i / cols_p), c = (int)(i % cols_p);
         uint16_t v = 0;
         if (r < rows && c < cols) v = bf16_bits_rne(seeded_value(seed, (uint64_t)r * cols + c, scale));
-        out[i] = v;
+        out[tiled ? tiled_offset(r, c, cols_p) : i] = v;
     }
 }
 void launch_weightgen(uint16_t* out, int rows, int cols, int rows_p, int cols_p, uint64_t seed, double scale,
-                      cudaStream_t s) {
-    weightgen_kernel<<<148 * 8, 256, 0, s>>>(out, rows, cols, rows_p, cols_p, seed, scale);
+                      int tiled, cudaStream_t s) {
+    weightgen_kernel<<<148 * 8, 256, 0, s>>>(out, rows, cols, rows_p, cols_p, seed, scale, tiled);
     EL_CUDA_LAUNCH_CHECK();
 }
 

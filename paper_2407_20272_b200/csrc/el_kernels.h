@@ -52,7 +52,8 @@ struct DevState {
     uint16_t* vpool;
     const int* tables;      // [slots][L][bpl_max]
     Rows rows;
-    // activations
+    int NR;           // activation tile height (act_offset)
+    // activations (bf16 copies in act_offset layout)
     float* h32;       // [2][Bmax][dp]  residual stream, parity = layer & 1
     uint16_t* hb;     // [2][Bmax][dp]  bf16 copy (GEMM B operand)
     float* q32;       // [Bmax][dp]
@@ -100,10 +101,30 @@ struct DevState {
     int rec_cap;
 };
 
+// Weight (GEMM A operand) layout in HBM: 128x64 bf16 tiles, tile-major
+// [row/128][col/64], each tile stored exactly as TMA SWIZZLE_128B would place
+// it in shared memory (16-byte chunk c of row r at chunk c ^ (r & 7)), so one
+// contiguous 16 KB bulk copy lands a ready-to-use UMMA operand.
+__host__ __device__ inline size_t tiled_offset(int r, int c, int cols_p) {
+    const int kb_total = cols_p / 64;
+    const size_t tile = (size_t)(r >> 7) * kb_total + (c >> 6);
+    const int rr = r & 127, cc = c & 63;
+    return tile * 8192 + (size_t)rr * 64 + (size_t)((((cc >> 3) ^ (rr & 7)) << 3) | (cc & 7));
+}
+
+// Activation (GEMM B operand) layout: [col/64][NR rows][64 cols] with the same
+// 128-byte swizzle; NR = Bmax rounded up to 16. A k-block of the first n rows
+// is one contiguous n*128-byte bulk copy.
+__host__ __device__ inline size_t act_offset(int row, int col, int NR) {
+    const int cc = col & 63;
+    return ((size_t)(col >> 6) * NR + row) * 64 + (size_t)((((cc >> 3) ^ (row & 7)) << 3) | (cc & 7));
+}
+
 // one split-K weight-streaming GEMM launch: D[M x N] = W[M x K] . X[N x K]^T
 struct GemmPlan {
-    CUtensorMap tmA;  // weights, box [128 rows][64 k]
-    CUtensorMap tmB;  // activations, box [n_pad rows][64 k]
+    const uint16_t* A;  // weights, tiled layout (tiled_offset)
+    const uint16_t* Bp; // activations, act_offset layout (parity 0)
+    size_t b_par_stride; // elements between the two hidden-state parities
     int m_tiles, splits, kb_total, n_pad, stages, smem_bytes, tmem_cols;
 };
 
@@ -114,7 +135,7 @@ void init_kernel_attributes();
 void launch_gemm(GemmKind kind, const GemmPlan& p, const DevState& st, cudaStream_t s, bool pdl);
 
 void launch_weightgen(uint16_t* out, int rows, int cols, int rows_p, int cols_p, uint64_t seed, double scale,
-                      cudaStream_t s);
+                      int tiled, cudaStream_t s);
 void launch_kv_prefix(const DevState& st, const int* row_seq_ids, int prefix_len, uint64_t kv_seed, int round_bf16,
                       cudaStream_t s);
 void launch_embed(const DevState& st, cudaStream_t s);

@@ -16,7 +16,7 @@ for rep in range(2):
     ts = np.zeros(65536, np.uint64)
     lib.el_debug_timestamps(e._h, ts.ctypes.data_as(C.c_void_p), 65536)
 info = e.plan_info()
-n = {1: info["qkv_splits"] * 18, 2: info["wo_splits"] * 6, 3: info["up_splits"] * 24, 4: info["down_splits"] * 6}[kind]
+n = {1: info["qkv_splits"] * 18, 2: info["wo_splits"] * 6, 3: info["up_splits"] * 24, 4: info["down_splits"] * 6, 5: 251}[kind]
 t = ts[: n * 8].reshape(n, 8).astype(np.int64)
 t0 = t[:, 0].min()
 names = ["start", "tmem+bar", "prologue", "accf", "csync1", "reduce", "done", "dealloc"]
