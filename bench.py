@@ -81,14 +81,19 @@ def workload(n, seed=1):
 
 
 class ClockSampler:
-    """SM clocks + throttle reasons polled through NVML (1 ms) during the timed region."""
+    """SM clocks + throttle reasons polled through NVML during the timed region.
+
+    Polling starts before the region (NVML init is slow); summary() uses the
+    samples taken between mark_start() and mark_end(), or -- when the region is
+    shorter than the NVML sampling interval -- the samples closest to it."""
 
     NAMES = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20, "sw_power_cap": 0x4}
 
     def __init__(self, gpu: int):
         self.gpu, self.rows, self.stop, self.h = gpu, [], False, None
+        self.t_start = self.t_end = None
 
-    def __enter__(self):
+    def start(self):
         try:
             import pynvml
             pynvml.nvmlInit()
@@ -107,12 +112,19 @@ class ClockSampler:
             try:
                 sm = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
                 rs = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
-                self.rows.append((sm, rs))
+                self.rows.append((time.perf_counter(), sm, rs))
             except Exception:
                 pass
-            time.sleep(0.001)
+            time.sleep(0.0005)
 
-    def __exit__(self, *a):
+    def mark_start(self):
+        self.t_start = time.perf_counter()
+
+    def mark_end(self):
+        self.t_end = time.perf_counter()
+
+    def finish(self):
+        time.sleep(0.02)
         self.stop = True
         if self.h is not None:
             self.t.join(timeout=2)
@@ -120,10 +132,16 @@ class ClockSampler:
     def summary(self):
         if not self.rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
-        sm = [r[0] for r in self.rows]
-        reasons = sorted({n for _, rs in self.rows for n, bit in self.NAMES.items() if rs & bit})
+        inside = [r for r in self.rows if self.t_start <= r[0] <= self.t_end]
+        note = "nvml samples inside the timed region"
+        if len(inside) < 3:
+            mid = 0.5 * (self.t_start + self.t_end)
+            inside = sorted(self.rows, key=lambda r: abs(r[0] - mid))[:5]
+            note = "timed region shorter than the nvml sampling period: 5 samples nearest to it"
+        sm = [r[1] for r in inside]
+        reasons = sorted({n for _, _, rs in inside for n, bit in self.NAMES.items() if rs & bit})
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": self.maxc, "reasons": reasons,
-                "samples": len(self.rows), "source": "nvml, 1 ms polling during the timed region"}
+                "samples": len(inside), "source": note}
 
 
 def attn_bytes(d, ctx_list, B):
@@ -139,6 +157,21 @@ def iteration_bytes(L, d, e, ctx_sum, B, tech):
     return e * (24 * d * d + 4 * d * ctx_sum + 4 * B * d) + (L - e) * (4 * d * d + 4 * B * d) + e * chk + lm_final + 2 * B * d
 
 
+def shard(rank, world, B):
+    """request ids of this rank: contiguous ranges of B per GPU (request-sharded replicas)."""
+    return list(range(rank * B, (rank + 1) * B))
+
+
+def reduce_max(x, dist, device=None):
+    """max over ranks of a float (NCCL tensor on the GPU, or gloo on the CPU)."""
+    if dist is None:
+        return x
+    import torch
+    t = torch.tensor([x], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 # ---------------------------------------------------------------- our arm
 def run_ours(args, rank, world, local_rank, dist):
     from paper_2407_20272_b200 import exitlab as X
@@ -146,7 +179,7 @@ def run_ours(args, rank, world, local_rank, dist):
     c = CONFIGS[args.config]
     L, d, B = c["L"], c["d"], c["B"]
     prompts = workload(B * world)
-    mine = list(range(rank * B, (rank + 1) * B))
+    mine = shard(rank, world, B)
     first = np.array([prompts[i][-1] for i in mine], np.int32)
     ids = np.array(mine, np.int32)
     cap = PROMPT + OUT_LEN
@@ -165,21 +198,19 @@ def run_ours(args, rank, world, local_rank, dist):
             dist.barrier()
 
     def max_over_ranks(x):
-        if dist is None:
-            return x
-        import torch
-        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local_rank}")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
+        return reduce_max(x, dist, f"cuda:{local_rank}")
 
     # 1. early-exit engine, device-resident timed region
     ee = engine(c["tech"])
     ee.session_begin(first, PROMPT - 1, cap, 1, ids)
+    clk = ClockSampler(local_rank).start()
     ee.decode_run(args.warmup)
     ee.sync()
     barrier()
-    with ClockSampler(local_rank) as clk:
-        ms = ee.time_decode(args.steps)  # CUDA events on the engine stream, synced both sides
+    clk.mark_start()
+    ms = ee.time_decode(args.steps)  # CUDA events on the engine stream, synced both sides
+    clk.mark_end()
+    clk.finish()
     barrier()
     ms = max_over_ranks(ms)
     rec = ee.records(args.warmup, args.steps)
