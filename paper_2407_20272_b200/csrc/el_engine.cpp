@@ -143,6 +143,9 @@ struct el_engine {
     int device = 0;
     bool use_graph = true;
     bool pdl = true;
+    bool body_head = false;
+    bool fuse_exit = true;
+    bool fuse_exit_all = false;
     int dbg = 0;
     int rec_cap = 4096;
 
@@ -163,7 +166,7 @@ struct el_engine {
     DevBuf<int> attn_cnt, attn_queue, layer, out_layer, status, first_accept, accept, exit_cnt, iter_counter,
         cur_iter, rec_tok, rec_acc, rec_out;
     DevBuf<float4> lm_part;
-    DevBuf<double> lambdas;
+    DevBuf<double> lambdas, exit_part;
     DevBuf<unsigned long long> dbg_ts;
     DevBuf<float> fixed_conf;
     int* cont_host = nullptr;
@@ -315,6 +318,7 @@ struct el_engine {
         attn_queue.alloc(4);
         lm_part.alloc((size_t)(dm.Vp / 128) * Bm);
         dbg_ts.alloc(65536);
+        exit_part.alloc((size_t)(dp / 128 + 1) * Bm * 3);
         for (DevBuf<int>* b : {&layer, &out_layer, &exit_cnt, &iter_counter, &cur_iter}) b->alloc(4);
         status.alloc((size_t)Bm);
         first_accept.alloc((size_t)Bm);
@@ -364,7 +368,7 @@ struct el_engine {
 
     // attention split: ~4 CTAs per SM worth of (sequence, chunk) work items; a
     // ring of stages sized so two CTAs fit per SM when the block pair allows it
-    int opt_attn_cb = 0, opt_attn_stages = 0, opt_splits_cap = 8;
+    int opt_attn_cb = 0, opt_attn_stages = 0, opt_splits_cap = 8, opt_fill_splits = 4;
     void plan_attention() {
         const int bpl = std::max(1, dm.bpl_max);
         const int B = dm.Bmax;
@@ -439,7 +443,8 @@ struct el_engine {
         P.up = make_plan(wup.p, mid_b.p, 0, fp / 128, dp, n_pad, false);
         P.down = make_plan(wdown.p, up_b.p, 0, dp / 128, fp, n_pad, false);
         P.lm = make_plan(lm.p, hb.p, hpar, dm.Vp / 128, dp, n_pad, true, 1);
-        P.fill = make_plan(wqkv.p, hb.p, hpar, (L - 1) * (2 * dp / 128), dp, n_pad, false);
+        P.fill = make_plan(wqkv.p, hb.p, hpar, (L - 1) * (2 * dp / 128), dp, n_pad, false,
+                           std::min(opt_fill_splits, dp / 64));
         invalidate_graphs();  // workspace may have moved
         return plans.emplace(n_pad, P).first->second;
     }
@@ -464,6 +469,8 @@ struct el_engine {
         s.lm_part = lm_part.p;
         s.layer = layer.p; s.out_layer = out_layer.p; s.status = status.p; s.first_accept = first_accept.p;
         s.accept = accept.p; s.conf = conf.p; s.exit_cnt = exit_cnt.p; s.cont_host = cont_dev;
+        s.exit_part = exit_part.p;
+        s.fuse_exit = (!prefill && fuse_exit_active()) ? 1 : 0;
         s.lambdas = lambdas.p; s.fixed_conf = fixed_conf.p;
         s.technique = prefill ? el::kNever : cfg.technique;
         s.exit_layer = cfg.exit_layer;
@@ -479,13 +486,14 @@ struct el_engine {
     // may launch while its predecessor drains (weights / old KV blocks are
     // prefetched before griddepcontrol.wait).
     void launch_layer(const el::DevState& s, Plans& P) {
-        el::launch_gemm(el::kGemmQkv, P.qkv, s, stream, false);
+        if (body_head) el::launch_layer_head(s, stream);
+        el::launch_gemm(el::kGemmQkv, P.qkv, s, stream, body_head && pdl);
         el::launch_attention(s, stream, pdl);
         el::launch_gemm(el::kGemmWo, P.wo, s, stream, pdl);
         el::launch_gemm(el::kGemmUp, P.up, s, stream, pdl);
         el::launch_gemm(el::kGemmDown, P.down, s, stream, pdl);
         if (s.technique == el::kSoftmax) el::launch_gemm(el::kGemmLmCheck, P.lm, s, stream, pdl);
-        el::launch_exit(s, stream, pdl);
+        if (!s.fuse_exit) el::launch_exit(s, stream, pdl);
     }
     void launch_tail(const el::DevState& s, Plans& P) {
         bool first = true;  // first kernel after the conditional node: plain dependency
@@ -499,8 +507,17 @@ struct el_engine {
         }
         el::launch_finish(s, stream, pdl && !first);
     }
+    // The exit check runs inside the down-projection epilogue when it needs no
+    // confidence reduction (never / always_at / injected); for state and classifier
+    // the separate exit kernel measured faster (its B CTAs read whole rows in parallel)
+    bool fuse_exit_active() const {
+        if (!fuse_exit) return false;
+        if (fuse_exit_all) return cfg.technique != EL_TECH_SOFTMAX;
+        return cfg.technique == EL_TECH_NEVER || cfg.technique == EL_TECH_ALWAYS_AT || cfg.technique == EL_TECH_FIXED;
+    }
     int launches_per_iteration(int e) const {
-        const int per_layer = 6 + (cfg.technique == EL_TECH_SOFTMAX ? 1 : 0);
+        const bool fused = fuse_exit_active();
+        const int per_layer = (fused ? 5 : 6) + (cfg.technique == EL_TECH_SOFTMAX ? 1 : 0) + (body_head ? 1 : 0);
         return 1 + e * per_layer + (cfg.technique != EL_TECH_NEVER ? 1 : 0) +
                (cfg.technique != EL_TECH_SOFTMAX ? 1 : 0) + 1;
     }
@@ -995,13 +1012,25 @@ int el_engine_destroy(el_engine* e) {
 int el_engine_set_option(el_engine* e, const char* key, int64_t v) {
     API_BEGIN
     if (!std::strcmp(key, "graph")) e->use_graph = v != 0;
-    else if (!std::strcmp(key, "dbg")) {
+    else if (!std::strcmp(key, "fuse_exit")) {
+        e->fuse_exit = v != 0;
+        e->fuse_exit_all = v == 2;
+        e->invalidate_graphs();
+    } else if (!std::strcmp(key, "body_head")) {
+        e->body_head = v != 0;
+        e->invalidate_graphs();
+    } else if (!std::strcmp(key, "dbg")) {
         e->dbg = (int)v;
         e->invalidate_graphs();
     }
     else if (!std::strcmp(key, "attn_cb") || !std::strcmp(key, "attn_stages")) {
         (key[5] == 'c' ? e->opt_attn_cb : e->opt_attn_stages) = (int)v;
         e->plan_attention();
+    } else if (!std::strcmp(key, "fill_splits")) {
+        if (v < 1 || v > 8) fail(EL_INVALID_ARGUMENT, "fill_splits must be in [1, 8]");
+        e->opt_fill_splits = (int)v;
+        e->plans.clear();
+        e->invalidate_graphs();
     } else if (!std::strcmp(key, "splits_cap")) {
         if (v < 1 || v > 8) fail(EL_INVALID_ARGUMENT, "splits_cap must be in [1, 8]");
         e->opt_splits_cap = (int)v;

@@ -286,6 +286,38 @@ struct Epi<kGemmLmCheck> : EpiLm<kGemmLmCheck> {};
 template <>
 struct Epi<kGemmLmFinal> : EpiLm<kGemmLmFinal> {};
 
+// ExitStatusVector::observe_layer (engine.cpp:55-66) for this layer, run by one
+// whole CTA once every row's decision is in st.accept: OR-latch, first accept,
+// all-set; ends the layer loop on the device when all rows are set or layer == L.
+__device__ void exit_latch(const DevState& st, int layer) {
+    int all = 1;
+    for (int r = threadIdx.x; r < st.rows.B; r += blockDim.x) {
+        const int a = __ldcg(&st.accept[r]);
+        int s = st.status[r];
+        if (!s && a) {
+            s = 1;
+            st.status[r] = 1;
+            st.first_accept[r] = layer;
+        }
+        all &= s;
+    }
+    all = __syncthreads_and(all);
+    if (threadIdx.x == 0) {
+        const int done = all || layer >= st.dm.L;
+        if (done) *st.out_layer = layer;
+        *st.layer = layer + 1;
+        *st.exit_cnt = 0;
+        if (st.use_cond) cudaGraphSetConditional(st.cond, done ? 0u : 1u);
+        if (st.cont_host) *(volatile int*)st.cont_host = done ? 0 : 1;
+    }
+}
+
+__device__ __forceinline__ double warp_sum_d(double v) {
+#pragma unroll
+    for (int off = 16; off; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+    return v;
+}
+
 struct GemmArgs {
     const uint16_t* A;   // weights in tiled, pre-swizzled layout (tiled_offset)
     const uint16_t* Bp;  // activations in act_offset layout
@@ -483,6 +515,82 @@ __global__ void __launch_bounds__(128, 1)
         }
         stamp(5);
         cluster_sync_all();  // peers keep their smem alive until everyone has read it
+    }
+    if constexpr (K == kGemmDown) {
+        if (st.fuse_exit) {
+            // exit check fused into the down projection: per-tile partial dots of the
+            // columns this CTA owns (fixed shuffle order), then the grid's last CTA
+            // decides every row and latches the status vector
+            const int layer = es.layer, Bm = st.dm.Bmax, dp = st.dm.dp;
+            const int per = (nval + g.splits - 1) / g.splits;
+            const int c0 = (g.splits > 1) ? split * per : 0;
+            const int c1 = (g.splits > 1) ? min(nval, c0 + per) : nval;
+            __syncthreads();  // this CTA's h32 writes are visible inside the CTA
+            if (st.technique == kState || st.technique == kClassifier) {
+                const float* ho = st.h32 + (size_t)(layer & 1) * Bm * dp;
+                const float* hi = st.h32 + (size_t)((layer - 1) & 1) * Bm * dp;
+                for (int c = c0 + warp; c < c1; c += 4) {
+                    double x0 = 0.0, x1 = 0.0, x2 = 0.0;
+                    for (int m = lane; m < kBM; m += 32) {
+                        const int f = es.row0 + m;
+                        const double y = ho[(size_t)c * dp + f];
+                        if (st.technique == kState) {
+                            const double x = hi[(size_t)c * dp + f];
+                            x0 += x * y;
+                            x1 += x * x;
+                            x2 += y * y;
+                        } else {
+                            x0 += (double)st.probe_w[f] * y;
+                        }
+                    }
+                    x0 = warp_sum_d(x0);
+                    x1 = warp_sum_d(x1);
+                    x2 = warp_sum_d(x2);
+                    if (lane == 0) {
+                        double* p = st.exit_part + ((size_t)tile * Bm + c) * 3;
+                        p[0] = x0;
+                        p[1] = x1;
+                        p[2] = x2;
+                    }
+                }
+            }
+            __syncthreads();
+            if (tid == 0) {
+                asm volatile("fence.acq_rel.gpu;" ::: "memory");
+                es.last = atomicAdd(st.exit_cnt, 1) == (int)(gridDim.x * gridDim.y) - 1;
+            }
+            __syncthreads();
+            if (es.last) {
+                asm volatile("fence.acq_rel.gpu;" ::: "memory");
+                for (int r = tid; r < nval; r += blockDim.x) {
+                    float conf = __int_as_float(0x7fc00000);
+                    int acc = 0;
+                    if (st.technique == kState || st.technique == kClassifier) {
+                        double x0 = 0.0, x1 = 0.0, x2 = 0.0;
+                        for (int t = 0; t < (int)gridDim.x; ++t) {  // fixed tile order
+                            const double* p = st.exit_part + ((size_t)t * Bm + r) * 3;
+                            x0 += __ldcg(p);
+                            x1 += __ldcg(p + 1);
+                            x2 += __ldcg(p + 2);
+                        }
+                        double cd;
+                        if (st.technique == kState) cd = x0 / (sqrt(x1) * sqrt(x2));  // NaN on a zero-norm state
+                        else cd = 1.0 / (1.0 + exp(-(x0 + (double)st.probe_b)));
+                        conf = (float)cd;
+                        acc = cd > st.lambdas[layer - 1];
+                    } else if (st.technique == kFixed) {
+                        conf = st.fixed_conf[(size_t)(layer - 1) * Bm + r];
+                        acc = (double)conf > st.lambdas[layer - 1];
+                    } else if (st.technique == kAlwaysAt) {
+                        acc = layer >= st.exit_layer;
+                    }
+                    st.accept[r] = acc;
+                    st.conf[(size_t)(layer - 1) * Bm + r] = conf;
+                }
+                __syncthreads();
+                exit_latch(st, layer);
+            }
+        }
     }
     stamp(6);
     tc_fence_before();
@@ -1100,26 +1208,7 @@ __global__ void __launch_bounds__(256) exit_kernel(DevState st) {
     tl_mark(st, 6, layer, 1);
     if (!s_last) return;
     __threadfence();
-    int all = 1;
-    for (int r = tid; r < st.rows.B; r += blockDim.x) {
-        const int a = __ldcg(&st.accept[r]);
-        int s = st.status[r];
-        if (!s && a) {
-            s = 1;
-            st.status[r] = 1;
-            st.first_accept[r] = layer;
-        }
-        all &= s;
-    }
-    all = __syncthreads_and(all);
-    if (tid == 0) {
-        const int done = all || layer >= L;
-        if (done) *st.out_layer = layer;
-        *st.layer = layer + 1;
-        *st.exit_cnt = 0;
-        if (st.use_cond) cudaGraphSetConditional(st.cond, done ? 0u : 1u);
-        if (st.cont_host) *(volatile int*)st.cont_host = done ? 0 : 1;
-    }
+    exit_latch(st, layer);
 }
 
 void launch_exit(const DevState& st, cudaStream_t s, bool pdl) {
@@ -1183,6 +1272,15 @@ __global__ void __launch_bounds__(256) finish_kernel(DevState st) {
 void launch_finish(const DevState& st, cudaStream_t s, bool pdl) {
     launch_k(finish_kernel, dim3(st.rows.B), dim3(256), 0, s, pdl, st);
 }
+
+// first node of the layer body: a plain (non-cluster) kernel so the cluster GEMM
+// that follows can be launched early through PDL
+__global__ void layer_head_kernel(DevState st) {
+    pdl_trigger();
+    tl_mark(st, 11, *st.layer, 0);
+    tl_mark(st, 11, *st.layer, 1);
+}
+void launch_layer_head(const DevState& st, cudaStream_t s) { launch_k(layer_head_kernel, dim3(1), dim3(32), 0, s, false, st); }
 
 __global__ void advance_kernel(DevState st) {
     const int b = threadIdx.x + blockIdx.x * blockDim.x;

@@ -85,6 +85,8 @@ struct DevState {
     int* accept;             // [Bmax] this layer's decision
     float* conf;             // [L][Bmax] this iteration's confidences
     int* exit_cnt;
+    double* exit_part;       // [Vp/128 tiles][Bmax][3] per-tile partial dots (fused exit)
+    int fuse_exit;           // exit check runs in the down-projection epilogue
     int* cont_host;          // mapped host flag (eager path reads it)
     const double* lambdas;   // [L] threshold_at(schedule, layer)
     const float* fixed_conf; // [L][Bmax] injected confidences (technique kFixed)
@@ -151,7 +153,8 @@ int attn_threads();
 void launch_attention(const DevState& st, cudaStream_t s, bool pdl);
 void launch_exit(const DevState& st, cudaStream_t s, bool pdl);
 void launch_finish(const DevState& st, cudaStream_t s, bool pdl);
-void launch_advance(const DevState& st, cudaStream_t s);  // prefill commit: pos += 1
+void launch_advance(const DevState& st, cudaStream_t s);
+void launch_layer_head(const DevState& st, cudaStream_t s);  // prefill commit: pos += 1
 // LIFO block allocator on the device (kv_cache.cpp:78-106, 182-194)
 void launch_kv_alloc(int* stack, int top, int* tables, const Dims& dm, int slot, int bpl, cudaStream_t s);
 void launch_kv_release(int* stack, int top, const int* tables, const Dims& dm, int slot, int bpl, cudaStream_t s);

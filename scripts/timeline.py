@@ -19,7 +19,7 @@ lib.el_debug_timeline_reset(e._h)
 e.decode_run(1); e.sync()
 ts = np.zeros(65536, np.uint64); lib.el_debug_timestamps(e._h, ts.ctypes.data_as(C.c_void_p), 65536)
 t = ts[16384:16384 + 2 * 32 * 16].reshape(16, 32, 2).astype(np.float64)
-names = {0: "embed", 1: "qkv", 2: "attn", 3: "wo", 4: "up", 5: "down", 10: "lmchk", 6: "exit", 7: "fill", 8: "lm", 9: "finish"}
+names = {11: "head", 0: "embed", 1: "qkv", 2: "attn", 3: "wo", 4: "up", 5: "down", 10: "lmchk", 6: "exit", 7: "fill", 8: "lm", 9: "finish"}
 valid = t[:, :, 0] < 1.8e19
 t0 = t[:, :, 0][valid].min()
 ev = []
