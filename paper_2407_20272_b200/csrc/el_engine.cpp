@@ -368,7 +368,7 @@ struct el_engine {
 
     // attention split: ~4 CTAs per SM worth of (sequence, chunk) work items; a
     // ring of stages sized so two CTAs fit per SM when the block pair allows it
-    int opt_attn_cb = 0, opt_attn_stages = 0, opt_splits_cap = 8, opt_fill_splits = 4;
+    int opt_attn_cb = 0, opt_attn_stages = 0, opt_splits_cap = 8, opt_fill_splits = 4, opt_nsplit = 2, opt_cta_target = 148;
     void plan_attention() {
         const int bpl = std::max(1, dm.bpl_max);
         const int B = dm.Bmax;
@@ -405,9 +405,11 @@ struct el_engine {
     // ---- GEMM plans ----
     // split-K cluster size: aim at ~one CTA per SM, at most 8 (portable clusters)
     int pick_splits(int m_tiles, int kb_total) const {
-        int s = (148 + m_tiles / 2) / m_tiles;
+        int s = (opt_cta_target + m_tiles / 2) / m_tiles;
         return std::max(1, std::min({s, opt_splits_cap, kb_total}));
     }
+    // n_pad: padded batch; the plan splits it into ns column groups of nc (MMA N)
+    // so each CTA's split-K partial (and its DSMEM reduction) stays small
     el::GemmPlan make_plan(const uint16_t* A, const uint16_t* Bp, size_t b_par_stride, int m_tiles, int k, int n_pad,
                            bool tile, int forced_splits = 0) {
         el::GemmPlan p;
@@ -416,7 +418,11 @@ struct el_engine {
         p.b_par_stride = b_par_stride;
         p.m_tiles = m_tiles;
         p.kb_total = k / 64;
-        p.splits = forced_splits ? forced_splits : pick_splits(m_tiles, p.kb_total);
+        int nc = n_pad;
+        if (!tile && opt_nsplit > 1) nc = std::max(16, round_up(ceil_div(n_pad, opt_nsplit), 16));
+        const int ns = ceil_div(n_pad, nc);
+        n_pad = nc;
+        p.splits = forced_splits ? forced_splits : pick_splits(m_tiles * ns, p.kb_total);
         const int kb_max = ceil_div(p.kb_total, p.splits);
         p.n_pad = n_pad;
         const int stage = 128 * 64 * 2 + n_pad * 64 * 2;
@@ -1026,6 +1032,11 @@ int el_engine_set_option(el_engine* e, const char* key, int64_t v) {
     else if (!std::strcmp(key, "attn_cb") || !std::strcmp(key, "attn_stages")) {
         (key[5] == 'c' ? e->opt_attn_cb : e->opt_attn_stages) = (int)v;
         e->plan_attention();
+    } else if (!std::strcmp(key, "nsplit") || !std::strcmp(key, "cta_target")) {
+        if (v < 1) fail(EL_INVALID_ARGUMENT, "value must be >= 1");
+        (key[0] == 'n' ? e->opt_nsplit : e->opt_cta_target) = (int)v;
+        e->plans.clear();
+        e->invalidate_graphs();
     } else if (!std::strcmp(key, "fill_splits")) {
         if (v < 1 || v > 8) fail(EL_INVALID_ARGUMENT, "fill_splits must be in [1, 8]");
         e->opt_fill_splits = (int)v;

@@ -323,7 +323,7 @@ struct GemmArgs {
     const uint16_t* Bp;  // activations in act_offset layout
     size_t b_par_stride;
     int NR;
-    int m_tiles, splits, kb_total, n_pad, stages, tmem_cols, pdl;
+    int m_tiles, splits, kb_total, n_pad, stages, tmem_cols, pdl;  // n_pad = columns per CTA (MMA N)
 };
 
 __device__ __forceinline__ void cluster_sync_all() {
@@ -345,6 +345,7 @@ __global__ void __launch_bounds__(128, 1)
     // 1024-byte alignment by pointer offset (keeps the shared address space visible to the compiler)
     uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     const int tile = blockIdx.x, split = blockIdx.y;
+    const int n0 = blockIdx.z * g.n_pad;  // N split: this CTA's first batch column
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
     const uint32_t b_stage = (uint32_t)g.n_pad * kBK * 2;
@@ -409,7 +410,8 @@ __global__ void __launch_bounds__(128, 1)
         const size_t b_kstride = (size_t)g.NR * kBK;
         pdl_wait();  // no-op unless launched as a PDL secondary
         for (int kb = 0; kb < pre; ++kb)
-            bulk_load(sB + (size_t)kb * b_stage, b_tiles + (size_t)(kb0 + kb) * b_kstride, b_stage, &full[kb]);
+            bulk_load(sB + (size_t)kb * b_stage, b_tiles + (size_t)(kb0 + kb) * b_kstride + (size_t)n0 * kBK, b_stage,
+                      &full[kb]);
         for (int kb = pre; kb < nkb; ++kb) {
             const int s = kb % g.stages;
             mbar_wait(&empty[s], ((kb / g.stages) - 1) & 1);
@@ -420,7 +422,8 @@ __global__ void __launch_bounds__(128, 1)
             }
             mbar_arrive_expect_tx(&full[s], kAStage + b_stage);
             bulk_load(sA + (size_t)s * kAStage, a_tiles + (size_t)(kb0 + kb) * (kBM * kBK), kAStage, &full[s]);
-            bulk_load(sB + (size_t)s * b_stage, b_tiles + (size_t)(kb0 + kb) * b_kstride, b_stage, &full[s]);
+            bulk_load(sB + (size_t)s * b_stage, b_tiles + (size_t)(kb0 + kb) * b_kstride + (size_t)n0 * kBK, b_stage,
+                      &full[s]);
         }
     } else if (warp == 1 && lane == 0) {
         // ---- MMA issuer (single thread) ----
@@ -454,7 +457,7 @@ __global__ void __launch_bounds__(128, 1)
     __syncthreads();
     stamp(3);
     const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
-    const int nval = st.rows.B;
+    const int nval = min(st.rows.B - n0, g.n_pad);  // valid columns of this CTA (>= 1 by construction)
     const int row = tid;
 
     if constexpr (E::kTile) {
@@ -475,7 +478,7 @@ __global__ void __launch_bounds__(128, 1)
             tmem_ld16(trow + (uint32_t)c0, v);
 #pragma unroll
             for (int j = 0; j < 16; ++j)
-                if (c0 + j < nval) E::apply(st, es, row, c0 + j, v[j]);
+                if (c0 + j < nval) E::apply(st, es, row, n0 + c0 + j, v[j]);
         }
     } else {
         // partial tile [n][128] fp32: a warp's DSMEM loads below are 128 contiguous bytes
@@ -510,7 +513,7 @@ __global__ void __launch_bounds__(128, 1)
 #pragma unroll
                 for (int s = 0; s < 8; ++s)
                     if (s < g.splits) acc += v[j][s];
-                E::apply(st, es, row, c + j, acc);
+                E::apply(st, es, row, n0 + c + j, acc);
             }
         }
         stamp(5);
@@ -529,7 +532,8 @@ __global__ void __launch_bounds__(128, 1)
             if (st.technique == kState || st.technique == kClassifier) {
                 const float* ho = st.h32 + (size_t)(layer & 1) * Bm * dp;
                 const float* hi = st.h32 + (size_t)((layer - 1) & 1) * Bm * dp;
-                for (int c = c0 + warp; c < c1; c += 4) {
+                for (int cl = c0 + warp; cl < c1; cl += 4) {
+                    const int c = n0 + cl;
                     double x0 = 0.0, x1 = 0.0, x2 = 0.0;
                     for (int m = lane; m < kBM; m += 32) {
                         const int f = es.row0 + m;
@@ -557,12 +561,12 @@ __global__ void __launch_bounds__(128, 1)
             __syncthreads();
             if (tid == 0) {
                 asm volatile("fence.acq_rel.gpu;" ::: "memory");
-                es.last = atomicAdd(st.exit_cnt, 1) == (int)(gridDim.x * gridDim.y) - 1;
+                es.last = atomicAdd(st.exit_cnt, 1) == (int)(gridDim.x * gridDim.y * gridDim.z) - 1;
             }
             __syncthreads();
             if (es.last) {
                 asm volatile("fence.acq_rel.gpu;" ::: "memory");
-                for (int r = tid; r < nval; r += blockDim.x) {
+                for (int r = tid; r < st.rows.B; r += blockDim.x) {
                     float conf = __int_as_float(0x7fc00000);
                     int acc = 0;
                     if (st.technique == kState || st.technique == kClassifier) {
@@ -611,8 +615,9 @@ template <GemmKind K>
 static void launch_gemm_t(const GemmPlan& p, const DevState& st, cudaStream_t s, bool pdl) {
     GemmArgs g{p.A, p.Bp, p.b_par_stride, st.NR, p.m_tiles, p.splits, p.kb_total, p.n_pad, p.stages, p.tmem_cols,
                pdl ? 1 : 0};
+    const int ns = (st.rows.B + p.n_pad - 1) / p.n_pad;  // N splits actually needed for this batch
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(p.m_tiles, p.splits);
+    cfg.gridDim = dim3(p.m_tiles, p.splits, ns);
     cfg.blockDim = dim3(128);
     cfg.dynamicSmemBytes = p.smem_bytes;
     cfg.stream = s;
