@@ -39,9 +39,9 @@ CONFIGS = {
                name="configs[0]: CALM-T5-small dims (L=6, d=512), softmax-response exit, batch 8"),
     "c2": dict(L=12, d=768, B=64, tech="state", lam=0.981, gamma=0.997,
                name="configs[1]: CALM-T5-base dims (L=12, d=768), hidden-state-similarity exit, batch 64, paged KV"),
-    "c3": dict(L=24, d=1024, B=128, tech="classifier", lam=0.41, gamma=0.998,
+    "c3": dict(L=24, d=1024, B=128, tech="classifier", lam=0.41, gamma=0.997,
                name="configs[2]: CALM-T5-large dims (L=24, d=1024), exit classifier, batch 128, skipped-layer KV fill"),
-    "c5": dict(L=24, d=1024, B=256, tech="classifier", lam=0.41, gamma=0.998,
+    "c5": dict(L=24, d=1024, B=256, tech="classifier", lam=0.41, gamma=0.997,
                name="configs[4]: CALM-T5-large dims, request-sharded batch 256/GPU"),
 }
 METRIC = "decode tokens/sec/GPU (early-exit vs full-layer), avg exit layer, %roofline"

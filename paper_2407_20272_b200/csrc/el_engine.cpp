@@ -139,7 +139,8 @@ struct el_transcript {
 struct el_engine {
     el_engine_config cfg{};
     el::Dims dm{};
-    cudaStream_t stream = nullptr;
+    cudaStream_t stream = nullptr, stream2 = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     int device = 0;
     bool use_graph = true;
     bool pdl = true;
@@ -201,6 +202,9 @@ struct el_engine {
             if (kv.second.g) cudaGraphDestroy(kv.second.g);
         }
         if (cont_host) cudaFreeHost(cont_host);
+        if (ev_fork) cudaEventDestroy(ev_fork);
+        if (ev_join) cudaEventDestroy(ev_join);
+        if (stream2) cudaStreamDestroy(stream2);
         if (stream) cudaStreamDestroy(stream);
     }
 
@@ -241,6 +245,9 @@ struct el_engine {
         validate();
         CK(cudaGetDevice(&device));
         CK(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+        CK(cudaStreamCreateWithFlags(&stream2, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
         const int L = cfg.n_layers, d = cfg.d_model, V = cfg.vocab_size;
         dm.L = L;
         dm.d = d;
@@ -501,17 +508,23 @@ struct el_engine {
         if (s.technique == el::kSoftmax) el::launch_gemm(el::kGemmLmCheck, P.lm, s, stream, pdl);
         if (!s.fuse_exit) el::launch_exit(s, stream, pdl);
     }
+    // tail: the skipped-layer fill and the greedy LM head both only read h_e, so
+    // they run as two graph branches (fork/join through a second stream)
     void launch_tail(const el::DevState& s, Plans& P) {
-        bool first = true;  // first kernel after the conditional node: plain dependency
-        if (s.technique != el::kNever) {
-            el::launch_gemm(el::kGemmFill, P.fill, s, stream, false);
-            first = false;
+        const bool fill = s.technique != el::kNever, lmf = s.technique != el::kSoftmax;
+        if (fill && lmf) {
+            CK(cudaEventRecord(ev_fork, stream));
+            CK(cudaStreamWaitEvent(stream2, ev_fork, 0));
+            el::launch_gemm(el::kGemmFill, P.fill, s, stream2, false);
+            CK(cudaEventRecord(ev_join, stream2));
+            el::launch_gemm(el::kGemmLmFinal, P.lm, s, stream, false);
+            CK(cudaStreamWaitEvent(stream, ev_join, 0));
+            el::launch_finish(s, stream, false);
+            return;
         }
-        if (s.technique != el::kSoftmax) {
-            el::launch_gemm(el::kGemmLmFinal, P.lm, s, stream, pdl && !first);
-            first = false;
-        }
-        el::launch_finish(s, stream, pdl && !first);
+        if (fill) el::launch_gemm(el::kGemmFill, P.fill, s, stream, false);
+        if (lmf) el::launch_gemm(el::kGemmLmFinal, P.lm, s, stream, false);
+        el::launch_finish(s, stream, pdl);
     }
     // The exit check runs inside the down-projection epilogue when it needs no
     // confidence reduction (never / always_at / injected); for state and classifier

@@ -689,7 +689,8 @@ struct AttnSmem {
     float cl[128];
     int pref[257];  // block prefix sum over the batch rows
     int last_flag;
-    int pad[2];
+    int seq_next;   // ring sequence base for the next pass
+    int pad;
 };
 
 __device__ __forceinline__ float dot8p(uint4 k, const float* q) {
@@ -717,35 +718,18 @@ __device__ __forceinline__ int atom_add_acq_rel(int* p, int v) {
     return old;
 }
 
+// One attention pass over layer `layer` (see the comment above). Shared by the
+// standalone kernel and the persistent iteration kernel; `seq0` continues the
+// mbarrier ring's sequence (phase parity) across calls; on return a.seq_next
+// holds the next base.
 template <int NJ>
-__global__ void __launch_bounds__(kAttnThreads) attn_kernel(DevState st) {
-    extern __shared__ __align__(128) uint8_t smem_raw[];
+__device__ void attn_body(const DevState& st, AttnSmem& a, uint8_t* stages, int layer, int seq0) {
     const Dims& dm = st.dm;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int dp = dm.dp, nchunk = dp / 8;
     const int S = st.attn_stages;
     const uint32_t blk_bytes = (uint32_t)dm.bc * dp * 2;
     const uint32_t stage_bytes = (uint32_t)attn_stage_bytes(dm);  // K | V | q (>= merge buffer)
-    AttnSmem& a = *reinterpret_cast<AttnSmem*>(smem_raw);
-    uint8_t* stages = smem_raw + ((sizeof(AttnSmem) + 127) & ~(size_t)127);
-    const int layer = *st.layer;
-    tl_mark(st, 2, layer, 0);
-    if ((st.dbg & 32) && tid == 0) {
-        unsigned long long t;
-        asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-        if (blockIdx.x < 4) st.dbg_ts[8192 + 4 * 128 + blockIdx.x] = t;
-        st.dbg_ts[24576 + 4 * blockIdx.x] = t;
-    }
-
-    if (tid == 0) {
-        for (int s = 0; s < S; ++s) {
-            mbar_init(&a.full[s], 1);
-            mbar_init(&a.empty[s], kAttnWarps);
-        }
-        fence_barrier_init();
-    }
-    __syncthreads();
-
     if (warp == kAttnWarps) {
         // ---------------- producer warp ----------------
         // Static balanced split: the batch's KV blocks are flattened in (row,
@@ -798,7 +782,7 @@ __global__ void __launch_bounds__(kAttnThreads) attn_kernel(DevState st) {
                 dbytes = 0;
             }
         };
-        int seq = 0;
+        int seq = seq0;
         int b = 0;
         while (b < B && a.pref[b + 1] <= g0) ++b;
         for (long long g = g0; g < g1 && b < B;) {
@@ -865,10 +849,15 @@ __global__ void __launch_bounds__(kAttnThreads) attn_kernel(DevState st) {
         float q[NJ][8], o[NJ][8];
         float m = -INFINITY, l = 0.f;
         const int r0 = warp, r1 = warp + kAttnWarps;
-        for (int seq = 0;; ++seq) {
+        for (int seq = seq0;; ++seq) {
             const int s = seq % S;
             mbar_wait(&a.full[s], (seq / S) & 1);
             const AttnDesc d = a.desc[s];
+            if (d.b < 0) {  // terminal descriptor: release its slot too (the ring persists across passes)
+                if (tid == 0) a.seq_next = seq + 1;
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&a.empty[s]);
+            }
             if ((st.dbg & 32) && tid == 0) {
                 unsigned long long t;
                 asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -1049,6 +1038,31 @@ __global__ void __launch_bounds__(kAttnThreads) attn_kernel(DevState st) {
         }
         pdl_trigger();
     }
+}
+
+template <int NJ>
+__global__ void __launch_bounds__(kAttnThreads) attn_kernel(DevState st) {
+    extern __shared__ __align__(128) uint8_t smem_raw[];
+    const int tid = threadIdx.x;
+    AttnSmem& a = *reinterpret_cast<AttnSmem*>(smem_raw);
+    uint8_t* stages = smem_raw + ((sizeof(AttnSmem) + 127) & ~(size_t)127);
+    const int layer = *st.layer;
+    tl_mark(st, 2, layer, 0);
+    if ((st.dbg & 32) && tid == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+        if (blockIdx.x < 4) st.dbg_ts[8192 + 4 * 128 + blockIdx.x] = t;
+        st.dbg_ts[24576 + 4 * blockIdx.x] = t;
+    }
+    if (tid == 0) {
+        for (int s = 0; s < st.attn_stages; ++s) {
+            mbar_init(&a.full[s], 1);
+            mbar_init(&a.empty[s], kAttnWarps);
+        }
+        fence_barrier_init();
+    }
+    __syncthreads();
+    attn_body<NJ>(st, a, stages, layer, 0);
     if ((st.dbg & 32) && tid == 0) {
         unsigned long long t;
         asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
