@@ -190,7 +190,7 @@ def run_ours(args, rank, world, local_rank, dist):
         cfg = X.EngineConfig(model=X.ModelConfig(L, d, V, 0), technique=X.ExitTechnique(tech),
                              schedule=X.ThresholdSchedule(c["lam"], c["gamma"], 0.0), max_batch=B,
                              pool_blocks=B * L * (-(-cap // 16)), eos_token=-1)
-        return X.Engine(cfg, graph=not args.eager)
+        return X.Engine(cfg, graph=not args.eager, mega=not args.no_mega)
 
     def barrier():
         if dist is not None:
@@ -376,6 +376,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--eager", action="store_true", help="host-driven layer loop (for ncu, which cannot "
                     "profile kernels inside conditional graphs)")
+    ap.add_argument("--no-mega", action="store_true", help="per-phase kernels instead of the persistent "
+                    "decode-iteration kernel (A/B comparison)")
     args = ap.parse_args()
     if args.warmup < 3:
         raise SystemExit("warmup must be >= 3")

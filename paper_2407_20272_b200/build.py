@@ -14,7 +14,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libexitlab_b200.so")
 SOURCES = ["el_kernels.cu", "el_engine.cpp"]
-HEADERS = ["el_common.cuh", "el_kernels.h"]
+HEADERS = ["el_common.cuh", "el_kernels.h", "el_iter.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-O2", "--expt-relaxed-constexpr", "-cudart", "static",

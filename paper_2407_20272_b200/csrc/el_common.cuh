@@ -111,6 +111,22 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     }
 }
 
+__device__ __forceinline__ void mbar_wait_addr(uint32_t a, uint32_t parity) {
+    if (mbar_try_wait(a, parity)) return;
+    const long long t0 = clock64();
+    while (!mbar_try_wait(a, parity)) {
+        if (clock64() - t0 > EL_SPIN_LIMIT) __trap();
+    }
+}
+
+// warp-collective wait: lane 0 polls, the other lanes sleep at __syncwarp and
+// then observe the completed phase once (keeps 32 pollers off the mbarrier)
+__device__ __forceinline__ void mbar_wait_warp(uint64_t* bar, uint32_t parity) {
+    if ((threadIdx.x & 31) == 0) mbar_wait(bar, parity);
+    __syncwarp();
+    mbar_wait(bar, parity);
+}
+
 // ---------------------------------------------------------------------------
 // TMA
 // ---------------------------------------------------------------------------

@@ -147,6 +147,7 @@ struct el_engine {
     bool body_head = false;
     bool fuse_exit = true;
     bool fuse_exit_all = false;
+    bool use_mega = true;  // persistent decode-iteration kernel (el_iter.cuh)
     int dbg = 0;
     int rec_cap = 4096;
 
@@ -179,6 +180,12 @@ struct el_engine {
         int n_pad = 0;
     };
     std::map<int, Plans> plans;  // by n_pad
+    std::map<int, el::IterPlan> mplans;  // persistent-kernel plans by n_pad
+    DevBuf<float> mpart;                 // split-K partial workspace of the persistent kernel
+    DevBuf<unsigned> mbar;               // its grid barrier (arrivals, generation)
+    int mega_grid = 0, mega_att_stages = 2, sms = 148;
+    int opt_mega_fill_splits = 0, opt_mega_att_stages = 0, opt_mega_pf = 0, opt_mega_kv_pf_mb = 0,
+        opt_mega_bm_max = 128;
     int attn_cb = 1, attn_stages = 2, attn_max_chunks = 1, attn_grid = 148;
     int NR = 16;
 
@@ -324,7 +331,7 @@ struct el_engine {
         attn_cnt.alloc((size_t)Bm);
         attn_queue.alloc(4);
         lm_part.alloc((size_t)(dm.Vp / 128) * Bm);
-        dbg_ts.alloc(65536);
+        dbg_ts.alloc(65536 + 256 * 1024);
         exit_part.alloc((size_t)(dp / 128 + 1) * Bm * 3);
         for (DevBuf<int>* b : {&layer, &out_layer, &exit_cnt, &iter_counter, &cur_iter}) b->alloc(4);
         status.alloc((size_t)Bm);
@@ -346,6 +353,9 @@ struct el_engine {
         CK(cudaHostGetDevicePointer((void**)&cont_dev, cont_host, 0));
 
         el::init_kernel_attributes();
+        el::init_iter_attributes();
+        mbar.alloc(2048 + 32 * 1024);
+        CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
         slot_bpl.assign((size_t)dm.slots, 0);
         ensure_bpl(1);
         CK(cudaStreamSynchronize(stream));
@@ -462,6 +472,99 @@ struct el_engine {
         return plans.emplace(n_pad, P).first->second;
     }
 
+    // ---- persistent decode-iteration kernel plan ----
+    // split-K: aim at one unit per CTA (units = m_tiles * splits <= grid), >= 2 splits
+    int mega_splits(int m_tiles, int kb_total) const {
+        int s = std::max(1, mega_grid / m_tiles);
+        s = std::min(s, kb_total);
+        return std::max(s, std::min(2, kb_total));
+    }
+    el::IterPlan& mplan_for(int B) {
+        const int n_pad = std::max(16, round_up(B, 16));
+        auto it = mplans.find(n_pad);
+        if (it != mplans.end()) return it->second;
+        const int dp = dm.dp, fp = dm.fp, L = dm.L;
+        const int cap = 227 * 1024 - el::iter_smem_fixed();
+        // attention ring: as many K|V|q stages as shared memory holds (<= 8)
+        const int att_stage = el::attn_stage_bytes(dm);
+        mega_att_stages = std::min(8, cap / att_stage);
+        if (opt_mega_att_stages) mega_att_stages = std::min(mega_att_stages, opt_mega_att_stages);
+        if (mega_att_stages < 2) fail(EL_INVALID_ARGUMENT, "persistent kernel: attention ring does not fit");
+        mega_grid = sms;
+        el::IterPlan P{};
+        auto g = [&](const uint16_t* A, int m_tiles, int kb_total, int layer_rows, int row_off, int splits) {
+            el::IterGemm x;
+            x.A = A;
+            x.m_tiles = m_tiles;
+            x.kb_total = kb_total;
+            x.splits = splits;
+            x.layer_rows = layer_rows;
+            x.row_off = row_off;
+            x.mode = 0;
+            x.nt = 0;
+            return x;
+        };
+        P.g[el::kIQkv] = g(wqkv.p, 3 * dp / 128, dp / 64, 3 * dp / 128, 0, mega_splits(3 * dp / 128, dp / 64));
+        P.g[el::kIWo] = g(wo.p, dp / 128, dp / 64, dp / 128, 0, mega_splits(dp / 128, dp / 64));
+        P.g[el::kIUp] = g(wup.p, fp / 128, dp / 64, fp / 128, 0, mega_splits(fp / 128, dp / 64));
+        P.g[el::kIDown] = g(wdown.p, dp / 128, fp / 64, dp / 128, 0, mega_splits(dp / 128, fp / 64));
+        // fill: full-K units (direct epilogue) at large N, where split-K partials would outweigh the weights
+        int fs = opt_mega_fill_splits ? opt_mega_fill_splits : (n_pad >= 128 ? 1 : std::min(4, dp / 64));
+        fs = std::min(fs, dp / 64);
+        P.g[el::kIFill] = g(wqkv.p, 2 * dp / 128, dp / 64, 3 * dp / 128, dp / 128, fs);
+        P.n_pad = n_pad;
+        // batch-M full-K GEMMs (no split-K reduce phase) for QKV / W_o / up at small batch
+        int nt_max = 16;
+        if (n_pad <= opt_mega_bm_max) {
+            for (int k : {el::kIQkv, el::kIWo, el::kIUp}) {
+                el::IterGemm& x = P.g[k];
+                const int F = x.m_tiles * 128;
+                int nt = 16;
+                while (nt < 128 && F / nt > mega_grid) nt *= 2;
+                x.mode = 1;
+                x.nt = nt;
+                nt_max = std::max(nt_max, nt);
+            }
+        }
+        const int stage = 128 * 64 * 2 + n_pad * 128;
+        P.stage_bytes = stage;
+        // batch-M ring: n_pad activation rows + nt weight rows per k-block (1 KB aligned regions)
+        P.stage2_boff = round_up(n_pad * 128, 1024);
+        P.stage2_bytes = P.stage2_boff + round_up(nt_max * 128, 1024);
+        // the MMA reads a full 16 KB A tile from each stage start: keep that inside the ring region
+        P.stages2 = std::min(16, (cap - el::kIterTbufBytes - 16384) / P.stage2_bytes);
+        const int ring_att = mega_att_stages * att_stage;
+        P.stages = std::min(8, (cap - el::kIterTbufBytes) / stage);
+        if (P.stages < 2) fail(EL_INVALID_ARGUMENT, "persistent kernel: GEMM ring does not fit");
+        P.gemm_ring = P.stages * stage;
+        P.ring_bytes = round_up(std::max({ring_att, P.gemm_ring + el::kIterTbufBytes,
+                                          P.stages2 * P.stage2_bytes + 16384}), 1024);
+        P.lm_tiles = dm.Vp / 128;
+        if (el::iter_max_ctas_per_sm(dm, P.ring_bytes) < 1)
+            fail(EL_CUDA_ERROR, "persistent kernel does not fit on an SM (%d bytes)", el::iter_smem_bytes(P.ring_bytes));
+        size_t units = 0;
+        for (int k = 0; k < el::kIFill; ++k) units = std::max(units, (size_t)P.g[k].m_tiles * P.g[k].splits);
+        if (fs > 1) units = std::max(units, (size_t)(L - 1) * (2 * dp / 128) * fs);
+        const size_t need = units * n_pad * 128;
+        if (mpart.n < need) {
+            mpart.alloc(need, false);
+            for (auto& kv : mplans) kv.second.part = mpart.p;
+        }
+        P.part = mpart.p;
+        P.bar = mbar.p;
+        P.pf_flags = opt_mega_pf & 1;
+        // next-layer K/V into L2: a budget of opt_mega_kv_pf_mb MB spread over the grid
+        const long long blk2 = 2LL * dm.bc * dp * 2;
+        P.kv_pf_blocks = (int)std::min<long long>(1 << 20, (long long)opt_mega_kv_pf_mb * (1 << 20) / (blk2 * mega_grid));
+        return mplans.emplace(n_pad, P).first->second;
+    }
+    void launch_mega(int B) {
+        el::IterPlan& P = mplan_for(B);
+        el::DevState s = state(false, B);
+        s.attn_stages = mega_att_stages;
+        el::launch_iter(s, P, mega_grid, stream);
+    }
+
     el::DevState state(bool prefill, int B) {
         el::DevState s{};
         s.dm = dm;
@@ -535,6 +638,7 @@ struct el_engine {
         return cfg.technique == EL_TECH_NEVER || cfg.technique == EL_TECH_ALWAYS_AT || cfg.technique == EL_TECH_FIXED;
     }
     int launches_per_iteration(int e) const {
+        if (use_mega) return 1;
         const bool fused = fuse_exit_active();
         const int per_layer = (fused ? 5 : 6) + (cfg.technique == EL_TECH_SOFTMAX ? 1 : 0) + (body_head ? 1 : 0);
         return 1 + e * per_layer + (cfg.technique != EL_TECH_NEVER ? 1 : 0) +
@@ -597,7 +701,9 @@ struct el_engine {
     }
 
     void iteration(int B) {
-        if (use_graph) {
+        if (use_mega) {
+            launch_mega(B);
+        } else if (use_graph) {
             Graph& G = graph_for(B);
             CK(cudaGraphLaunch(G.x, stream));
         } else {
@@ -1031,6 +1137,20 @@ int el_engine_destroy(el_engine* e) {
 int el_engine_set_option(el_engine* e, const char* key, int64_t v) {
     API_BEGIN
     if (!std::strcmp(key, "graph")) e->use_graph = v != 0;
+    else if (!std::strcmp(key, "mega")) e->use_mega = v != 0;
+    else if (!std::strcmp(key, "mega_bm_max")) {
+        e->opt_mega_bm_max = (int)v;
+        e->mplans.clear();
+    } else if (!std::strcmp(key, "mega_pf") || !std::strcmp(key, "mega_kv_pf_mb")) {
+        if (v < 0 || v > 4096) fail(EL_INVALID_ARGUMENT, "value out of range");
+        (key[5] == 'k' ? e->opt_mega_kv_pf_mb : e->opt_mega_pf) = (int)v;
+        e->mplans.clear();
+    }
+    else if (!std::strcmp(key, "mega_fill_splits") || !std::strcmp(key, "mega_att_stages")) {
+        if (v < 0 || v > 16) fail(EL_INVALID_ARGUMENT, "value out of range");
+        (key[5] == 'f' ? e->opt_mega_fill_splits : e->opt_mega_att_stages) = (int)v;
+        e->mplans.clear();
+    }
     else if (!std::strcmp(key, "fuse_exit")) {
         e->fuse_exit = v != 0;
         e->fuse_exit_all = v == 2;
@@ -1321,9 +1441,15 @@ int el_launches_per_iteration(el_engine* e, int output_layer) { return e->launch
 int el_plan_info(el_engine* e, int64_t* out, int cap) {
     API_BEGIN
     auto& P = e->plans_for(e->in_session ? e->sess_B : e->dm.Bmax);
+    auto& M = e->mplan_for(e->in_session ? e->sess_B : e->dm.Bmax);
     const int64_t v[] = {e->attn_cb,    e->attn_stages,   e->attn_max_chunks, P.n_pad,       P.qkv.splits,
                          P.wo.splits,   P.up.splits,      P.down.splits,      P.fill.splits, P.down.stages,
-                         P.lm.m_tiles,  e->dm.dp,         e->dm.fp,           e->dm.Vp,      e->dm.bpl_max};
+                         P.lm.m_tiles,  e->dm.dp,         e->dm.fp,           e->dm.Vp,      e->dm.bpl_max,
+                         // persistent kernel: modes (1 = batch-M), splits, N per unit, ring depths
+                         M.g[el::kIQkv].mode, M.g[el::kIWo].mode, M.g[el::kIUp].mode,
+                         M.g[el::kIQkv].splits, M.g[el::kIWo].splits, M.g[el::kIUp].splits, M.g[el::kIDown].splits,
+                         M.g[el::kIFill].splits, M.g[el::kIQkv].nt, M.g[el::kIWo].nt, M.g[el::kIUp].nt,
+                         M.stages, M.stages2, e->mega_att_stages, e->use_mega ? 1 : 0};
     const int n = (int)(sizeof v / sizeof v[0]);
     for (int i = 0; i < std::min(n, cap); ++i) out[i] = v[i];
     return n;

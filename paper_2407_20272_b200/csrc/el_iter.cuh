@@ -1,0 +1,990 @@
+// el_iter.cuh -- the persistent decode-iteration kernel: ONE launch per decode
+// iteration (engine.cpp:208-310, Algorithm 1).  Included by el_kernels.cu
+// inside namespace el (reuses the tcgen05 / bulk-copy primitives and the paged
+// attention body).
+//
+// One CTA per SM (cooperative launch, co-residency guaranteed), 9 warps:
+// warps 0-7 compute (epilogues, attention consumers, reductions), warp 8 is the
+// bulk-copy producer.  TMEM (512 columns) is allocated once per launch.  The
+// layer loop runs on the device; phases are separated by a grid barrier:
+//
+//   embed | { QKV-partial | QKV-reduce(+paged K/V append) | attention |
+//             Wo-partial | Wo-reduce(+residual) | Up-partial | Up-reduce(+ReLU) |
+//             Down-partial | Down-reduce(+residual, exit dot partials) |
+//             [LM-check | softmax decide] | exit latch }*  |
+//   LM-final + skipped-layer fill partials | fill-reduce(+paged K/V) + greedy finish
+//
+// GEMMs are weight-streaming split-K (swap-AB: weights are the M=128 operand,
+// the batch is N): unit (m-tile, k-split) accumulates in TMEM, its fp32
+// partial goes to an L2-resident workspace, and the reduce phase sums the
+// splits in fixed order (deterministic, no atomics) and runs the fused
+// epilogue, spread over every warp of the grid.  The exit decision is computed
+// redundantly (and identically) by every CTA from the per-tile partial dots, so
+// the "all rows exited" test needs no extra barrier and no host round trip.
+
+constexpr int kIterWarps = 9;
+constexpr int kIterThreads = kIterWarps * 32;
+constexpr int kProducerWarp = 8;
+
+
+struct IterSmem {
+    AttnSmem att;  // attention ring barriers/descriptors (persist across layers)
+    uint64_t full[8], empty[8], acc;
+    uint64_t full2[16], empty2[16];  // batch-M GEMM ring (small stages, deeper)
+    unsigned long long tdbg[4];
+    uint32_t tmem;
+    int pad0;
+    int pos[256], slot[256], status[256], first[256];
+};
+
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned atom_add_acq_rel_u32(unsigned* p, unsigned v) {
+    unsigned old;
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+    return old;
+}
+__device__ __forceinline__ void fence_proxy_async_global() {
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+__device__ __forceinline__ void l2_prefetch(const void* src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+
+// L2 prefetch of the weight tiles of this CTA's units of a GEMM phase (issued by
+// one warp one phase ahead: the GEMM then streams its A operand from L2)
+__device__ __forceinline__ void l2_prefetch_gemm(const IterGemm& g, int layer) {
+    const int lane = threadIdx.x & 31;
+    const int U = g.m_tiles * g.splits;
+    for (int u = blockIdx.x; u < U; u += gridDim.x) {
+        const int m = u / g.splits, s = u % g.splits;
+        const int kb0 = s * g.kb_total / g.splits, kb1 = (s + 1) * g.kb_total / g.splits;
+        const uint16_t* a = g.A + (size_t)((layer - 1) * g.layer_rows + g.row_off + m) * g.kb_total * (kBM * kBK);
+        for (int kb = kb0 + lane; kb < kb1; kb += 32) l2_prefetch(a + (size_t)kb * (kBM * kBK), kAStage);
+    }
+}
+
+// L2 prefetch of the first `nblk` KV blocks of this CTA's attention range of
+// `layer` (same static split as attn_body; a.pref holds the block prefix sum
+// of the last attention pass).  Old positions only change when written, so the
+// next layer's blocks can stream into the 126 MB L2 while HBM would otherwise
+// idle (GEMM / reduce / barrier phases).
+__device__ __forceinline__ void l2_prefetch_kv(const DevState& st, const AttnSmem& a, int layer, int nblk) {
+    const int lane = threadIdx.x & 31;
+    const Dims& dm = st.dm;
+    const int B = st.rows.B;
+    const long long T = a.pref[B], G = min((long long)gridDim.x, T);
+    if ((long long)blockIdx.x >= G) return;
+    const long long g0 = (long long)blockIdx.x * T / G, g1 = (long long)(blockIdx.x + 1) * T / G;
+    const long long ge = min(g1, g0 + nblk);
+    const uint32_t bytes = (uint32_t)dm.bc * dm.dp * 2;
+    int b = 0;
+    for (long long g = g0 + lane; g < ge; g += 32) {
+        while (b < B && a.pref[b + 1] <= g) ++b;
+        const int blk = (int)(g - a.pref[b]);
+        const int id = st.tables[((size_t)st.rows.slot[b] * dm.L + (layer - 1)) * dm.bpl_max + blk];
+        l2_prefetch(st.kpool + (size_t)id * dm.bc * dm.dp, bytes);
+        l2_prefetch(st.vpool + (size_t)id * dm.bc * dm.dp, bytes);
+    }
+}
+
+__device__ __forceinline__ unsigned ld_relaxed_u32(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+__device__ __forceinline__ void red_release_add_u32(unsigned* p, unsigned v) {
+    asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Grid barrier over co-resident CTAs.  Generic global writes before it are
+// visible (and ordered for the async proxy: bulk copies read them) to every
+// CTA after it.  bar layout (unsigned): [0] arrivals, [1024] generation,
+// [2048 + cta*32] per-CTA flags (variant C).  Variants (probe, dbg bits):
+//   D (default): red.release arrivals, CTA 0 polls the count and releases the generation
+//   A (2048): atomic arrive with return, last arriver resets the count and releases the generation
+//   C (4096): per-CTA epoch flags, every CTA polls all flags (no atomics)
+//   E (16384): D with relaxed polling + one acquire fence;  F (32768): C with relaxed polling
+// Measured on B200 (scripts/bar_probe.py): D ~2.0 us, A ~2.9 us, C ~2.8 us, E ~2.7 us.
+__device__ __noinline__ void grid_sync(const IterPlan& p, const DevState& st, int& nbar, unsigned g0) {
+    if (threadIdx.x == 0 && (st.dbg & 128) && nbar < 1024) {  // per-CTA arrival (work done) time
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+        st.dbg_ts[65536 + (size_t)blockIdx.x * 1024 + nbar] = t;
+    }
+    if (!(st.dbg & 512)) fence_proxy_async_global();
+    __syncthreads();
+    const unsigned k = (unsigned)nbar + 1u;  // barrier index within this launch (1-based)
+    unsigned* cnt = p.bar;
+    unsigned* gen = p.bar + 1024;
+    const int G = (int)gridDim.x;
+    if (st.dbg & 16384) {  // E: D with relaxed polling and one acquire fence after
+        if (threadIdx.x == 0) {
+            red_release_add_u32(cnt, 1u);
+            const long long t0 = clock64();
+            if (blockIdx.x == 0) {
+                while (ld_relaxed_u32(cnt) < (unsigned)G * k)
+                    if (clock64() - t0 > EL_SPIN_LIMIT) __trap();
+                fence_acq_rel_gpu();
+                st_release_u32(gen, g0 + k);
+            } else {
+                while ((int)(ld_relaxed_u32(gen) - (g0 + k)) < 0)
+                    if (clock64() - t0 > EL_SPIN_LIMIT) __trap();
+            }
+            fence_acq_rel_gpu();
+        }
+    } else if (st.dbg & 32768) {  // F: C with relaxed polling
+        if (threadIdx.x < 32) {
+            unsigned* flags = p.bar + 2048;
+            if (threadIdx.x == 0) st_release_u32(flags + blockIdx.x * 32, g0 + k);
+            const long long t0 = clock64();
+            for (;;) {
+                bool ok = true;
+                for (int c = (int)threadIdx.x; c < G; c += 32) ok &= (int)(ld_relaxed_u32(flags + c * 32) - (g0 + k)) >= 0;
+                if (__all_sync(0xffffffffu, ok)) break;
+                if (clock64() - t0 > EL_SPIN_LIMIT) __trap();
+            }
+            fence_acq_rel_gpu();
+        }
+    } else if (st.dbg & 4096) {
+        if (threadIdx.x < 32) {
+            unsigned* flags = p.bar + 2048;
+            if (threadIdx.x == 0) st_release_u32(flags + blockIdx.x * 32, g0 + k);
+            const long long t0 = clock64();
+            for (;;) {
+                bool ok = true;
+                for (int c = (int)threadIdx.x; c < G; c += 32) ok &= (int)(ld_acquire_u32(flags + c * 32) - (g0 + k)) >= 0;
+                if (__all_sync(0xffffffffu, ok)) break;
+                if (clock64() - t0 > EL_SPIN_LIMIT) __trap();
+            }
+        }
+    } else if ((st.dbg & 2048) && threadIdx.x == 0) {
+        const unsigned g = ld_acquire_u32(gen);
+        if (!(st.dbg & 1024)) __threadfence();
+        if (atom_add_acq_rel_u32(cnt, 1u) == (unsigned)G - 1) {
+            *(volatile unsigned*)cnt = 0u;
+            st_release_u32(gen, g + 1u);
+        } else {
+            const long long t0 = clock64();
+            while (ld_acquire_u32(gen) == g) {
+                if (clock64() - t0 > EL_SPIN_LIMIT) __trap();
+            }
+        }
+        if (!(st.dbg & 1024)) __threadfence();
+    } else if (!(st.dbg & 2048)) {  // D (default)
+        if (threadIdx.x == 0) {
+            red_release_add_u32(cnt, 1u);
+            const long long t0 = clock64();
+            if (blockIdx.x == 0) {
+                while (ld_acquire_u32(cnt) < (unsigned)G * k)
+                    if (clock64() - t0 > EL_SPIN_LIMIT) __trap();
+                st_release_u32(gen, g0 + k);
+            } else {
+                while ((int)(ld_acquire_u32(gen) - (g0 + k)) < 0)
+                    if (clock64() - t0 > EL_SPIN_LIMIT) __trap();
+            }
+        }
+    }
+    if (threadIdx.x == 0 && (st.dbg & 128) && blockIdx.x == 0 && nbar < 1024) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+        st.dbg_ts[20480 + nbar] = t;
+    }
+    ++nbar;
+    __syncthreads();
+    if (!(st.dbg & 512)) fence_proxy_async_global();
+}
+
+// ---------------------------------------------------------------------------
+// GEMM unit: TMEM[0, n_pad) = sum_{kb in [kb0, kb0+nkb)} W_tile(kb) . X_tile(kb)^T
+// producer = warp 8 lane 0, MMA issuer = warp 0 lane 0.  On return the
+// accumulator is complete and visible to warps 0-7.
+// ---------------------------------------------------------------------------
+struct RingDesc {
+    uint64_t* full;
+    uint64_t* empty;
+    uint32_t stages, stride, b_off;  // stage count, stage stride, offset of the B region in a stage
+};
+
+__device__ __forceinline__ void unit_mainloop(IterSmem& sm, uint8_t* ring, const RingDesc& r, uint32_t& kseq,
+                                              const uint16_t* a_src, uint32_t a_bytes, size_t a_kstride,
+                                              const uint16_t* b_src, uint32_t b_bytes, size_t b_kstride, int kb0,
+                                              int nkb, uint32_t n_mma, uint32_t useq, int dbg = 0) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // single-thread issue loops: stage index / phase / addresses are strength-reduced (no div/mod per
+    // k-block -- a lone thread cannot hide the latency of that arithmetic)
+    if (warp == kProducerWarp) {
+        if (lane == 0) {
+            uint32_t s = kseq % r.stages, ph = (kseq / r.stages) & 1;
+            bool wrapped = kseq >= r.stages;
+            const uint32_t ring0 = smem_u32(ring), full0 = smem_u32(r.full), empty0 = smem_u32(r.empty);
+            const uint8_t* ap = reinterpret_cast<const uint8_t*>(a_src + (size_t)kb0 * a_kstride);
+            const uint8_t* bp = reinterpret_cast<const uint8_t*>(b_src + (size_t)kb0 * b_kstride);
+            const size_t ast = a_kstride * 2, bst = b_kstride * 2;
+            const uint32_t tx = a_bytes + b_bytes;
+#pragma unroll 1
+            for (int i = 0; i < nkb; ++i) {
+                if (wrapped) mbar_wait_addr(empty0 + 8 * s, ph ^ 1);
+                const uint32_t fb = full0 + 8 * s, sb = ring0 + s * r.stride;
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(fb), "r"(tx) : "memory");
+                asm volatile(
+                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(sb),
+                    "l"(ap), "r"(a_bytes), "r"(fb)
+                    : "memory");
+                asm volatile(
+                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                        sb + r.b_off),
+                    "l"(bp), "r"(b_bytes), "r"(fb)
+                    : "memory");
+                ap += ast;
+                bp += bst;
+                if (++s == r.stages) {
+                    s = 0;
+                    ph ^= 1;
+                    wrapped = true;
+                }
+            }
+            kseq += (uint32_t)nkb;
+        }
+    } else if (warp == 0) {
+        if (lane == 0) {
+            const uint32_t idesc = idesc_bf16_m128(n_mma);
+            uint32_t s = kseq % r.stages, ph = (kseq / r.stages) & 1;
+            const uint32_t full0 = smem_u32(r.full), ring0 = smem_u32(ring);
+#pragma unroll 1
+            for (int i = 0; i < nkb; ++i) {
+                mbar_wait_addr(full0 + 8 * s, ph);
+                tc_fence_after();
+                // (descriptors rebuilt per stage: the 14-bit address field wraps modulo 256 KB)
+                const uint32_t sa = ring0 + s * r.stride;
+                const uint64_t ad = sdesc_k_sw128(sa), bd = sdesc_k_sw128(sa + r.b_off);
+                if (!(dbg & (1 << 18)))
+#pragma unroll
+                    for (int k = 0; k < kBK / 16; ++k)
+                        tc_mma_bf16(sm.tmem, ad + (uint64_t)(2 * k), bd + (uint64_t)(2 * k), idesc, (i | k) != 0);
+                tc_commit(&r.empty[s]);
+                if (++s == r.stages) {
+                    s = 0;
+                    ph ^= 1;
+                }
+            }
+            kseq += (uint32_t)nkb;
+            tc_commit(&sm.acc);
+        }
+    }
+    __syncwarp();
+    if (warp < 8) {
+        mbar_wait(&sm.acc, useq & 1);
+        tc_fence_after();
+    }
+}
+// weight-streaming unit (swap-AB): weights = A (16 KB tile per k-block), activations = B (n_pad rows)
+__device__ __forceinline__ void unit_ws(IterSmem& sm, uint8_t* ring, const IterPlan& p, uint32_t& kseq,
+                                        const uint16_t* a_row, const uint16_t* b_src, size_t b_kstride, int kb0,
+                                        int nkb, uint32_t useq) {
+    const RingDesc r{sm.full, sm.empty, (uint32_t)p.stages, (uint32_t)p.stage_bytes, (uint32_t)kAStage};
+    unit_mainloop(sm, ring, r, kseq, a_row, kAStage, (size_t)(kBM * kBK), b_src, (uint32_t)p.n_pad * 128u, b_kstride,
+                  kb0, nkb, (uint32_t)p.n_pad, useq);
+}
+
+// split-K partial: part[u][c][row] for the nval valid columns
+__device__ __forceinline__ void epi_partial(const IterSmem& sm, const IterPlan& p, int u, int nval) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int row = 32 * (warp & 3) + lane;
+    const uint32_t trow = sm.tmem + ((uint32_t)(32 * (warp & 3)) << 16);
+    float* dst = p.part + (size_t)u * p.n_pad * kBM + row;
+    for (int c0 = 16 * (warp >> 2); c0 < nval; c0 += 32) {
+        float v[16];
+        tmem_ld16(trow + (uint32_t)c0, v);
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+            if (c0 + j < nval) __stcg(dst + (size_t)(c0 + j) * kBM, v[j]);
+    }
+}
+
+// LM-head tile epilogue: per column (sequence) the tile's (max1, max2, sum exp
+// rel. max1, argmax lowest index) -> lm_part[tile][col]; logits stay on chip.
+template <bool kFull>
+__device__ void epi_lm(const DevState& st, const IterSmem& sm, float* tbuf, int tile, int nval) {
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int row0 = tile * kBM;
+    const int rows = min(kBM, st.dm.V - row0);
+    const uint32_t trow = sm.tmem + ((uint32_t)(32 * (warp & 3)) << 16);
+    for (int c0 = 0; c0 < nval; c0 += 32) {
+        const int cc = c0 + 16 * (warp >> 2);
+        if (cc < nval) {
+            float v[16];
+            tmem_ld16(trow + (uint32_t)cc, v);
+#pragma unroll
+            for (int j = 0; j < 16; ++j) tbuf[(16 * (warp >> 2) + j) * 129 + 32 * (warp & 3) + lane] = v[j];
+        }
+        named_bar(2, 256);
+        const int n = tid >> 3, part = tid & 7;  // 8 threads per column, 16 rows each
+        const int col = c0 + n;
+        float m1 = -INFINITY, m2 = -INFINITY, s = 0.f;
+        int idx = 0x7fffffff;
+        if (col < nval) {
+            const float* cl = tbuf + n * 129;
+            const int r1 = min(rows, part * 16 + 16);
+            for (int r = part * 16; r < r1; ++r) {
+                const float x = cl[r];
+                if (x > m1) {
+                    if (kFull) {
+                        m2 = m1;
+                        s = s * __expf(m1 - x) + 1.f;
+                    }
+                    m1 = x;
+                    idx = row0 + r;
+                } else if (kFull) {
+                    m2 = fmaxf(m2, x);
+                    s += __expf(x - m1);
+                }
+            }
+        }
+        LmPart q{m1, m2, s, idx};
+#pragma unroll
+        for (int off = 1; off < 8; off <<= 1) {
+            LmPart o;
+            o.m1 = __shfl_xor_sync(0xffffffffu, q.m1, off);
+            o.m2 = __shfl_xor_sync(0xffffffffu, q.m2, off);
+            o.s = __shfl_xor_sync(0xffffffffu, q.s, off);
+            o.idx = __shfl_xor_sync(0xffffffffu, q.idx, off);
+            q = (part & off) ? lm_part_merge(o, q) : lm_part_merge(q, o);
+        }
+        if (part == 0 && col < nval)
+            st.lm_part[(size_t)tile * st.dm.Bmax + col] = make_float4(q.m1, q.m2, q.s, __int_as_float(q.idx));
+        named_bar(2, 256);
+    }
+}
+
+// one LM-head column reduced over all vocab tiles by one warp (fixed tree)
+__device__ __forceinline__ LmPart lm_col_warp(const DevState& st, int b) {
+    const int lane = threadIdx.x & 31, tiles = st.dm.Vp / kBM;
+    LmPart acc{-INFINITY, -INFINITY, 0.f, 0x7fffffff};
+    for (int t = lane; t < tiles; t += 32) {
+        const float4 q = __ldcg(&st.lm_part[(size_t)t * st.dm.Bmax + b]);
+        acc = lm_part_merge(acc, LmPart{q.x, q.y, q.z, __float_as_int(q.w)});
+    }
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        LmPart o;
+        o.m1 = __shfl_xor_sync(0xffffffffu, acc.m1, off);
+        o.m2 = __shfl_xor_sync(0xffffffffu, acc.m2, off);
+        o.s = __shfl_xor_sync(0xffffffffu, acc.s, off);
+        o.idx = __shfl_xor_sync(0xffffffffu, acc.idx, off);
+        acc = (lane & off) ? lm_part_merge(o, acc) : lm_part_merge(acc, o);
+    }
+    return acc;
+}
+
+// ---------------------------------------------------------------------------
+// epilogues applied to a finished output element (m-tile m, column c, row r)
+// ---------------------------------------------------------------------------
+struct IterCtx {
+    int layer;  // layer of the weights (fill: the skipped layer j)
+    int pin, pout;
+};
+
+// K/V element offset of (column c, layer) at the column's current position
+__device__ __forceinline__ long long kv_dst(const DevState& st, const IterSmem& sm, int c, int layer) {
+    const Dims& dm = st.dm;
+    const int pos = sm.pos[c];
+    const int blk = __ldg(&st.tables[((size_t)sm.slot[c] * dm.L + (layer - 1)) * dm.bpl_max + pos / dm.bc]);
+    return ((long long)blk * dm.bc + pos % dm.bc) * dm.dp;
+}
+
+// 4 consecutive rows r0..r0+3 (r0 % 4 == 0) of output tile m, column c
+template <int K>
+__device__ __forceinline__ void apply4(const DevState& st, const IterSmem& sm, const IterCtx& x, int m, int c, int r0,
+                                       float4 v) {
+    const int dp = st.dm.dp, NR = st.NR, Bm = st.dm.Bmax;
+    const int R = m * kBM + r0;
+    if constexpr (K == kIQkv || K == kIFill) {
+        const int kind = (K == kIQkv) ? R / dp : 1 + R / dp;  // 0 q, 1 k, 2 v
+        if (kind == 0) {
+            *reinterpret_cast<float4*>(st.q32 + (size_t)c * dp + R) = v;
+        } else {
+            const int f = R - (K == kIQkv ? kind : kind - 1) * dp;
+            uint16_t* dst = (kind == 1 ? st.kpool : st.vpool) + kv_dst(st, sm, c, x.layer) + f;
+            const uint2 pk = make_uint2((uint32_t)f32_to_bf16(v.x) | ((uint32_t)f32_to_bf16(v.y) << 16),
+                                        (uint32_t)f32_to_bf16(v.z) | ((uint32_t)f32_to_bf16(v.w) << 16));
+            *reinterpret_cast<uint2*>(dst) = pk;
+        }
+    } else if constexpr (K == kIWo) {
+        const size_t i = (size_t)c * dp + R;
+        const float4 h = __ldcg(reinterpret_cast<const float4*>(st.h32 + (size_t)x.pin * Bm * dp + i));
+        const float4 o = make_float4(h.x + v.x, h.y + v.y, h.z + v.z, h.w + v.w);
+        *reinterpret_cast<float4*>(st.mid32 + i) = o;
+        *reinterpret_cast<uint2*>(st.mid_b + act_offset(c, R, NR)) =
+            make_uint2((uint32_t)f32_to_bf16(o.x) | ((uint32_t)f32_to_bf16(o.y) << 16),
+                       (uint32_t)f32_to_bf16(o.z) | ((uint32_t)f32_to_bf16(o.w) << 16));
+    } else if constexpr (K == kIUp) {
+        const float4 o = make_float4(fmaxf(v.x, 0.f), fmaxf(v.y, 0.f), fmaxf(v.z, 0.f), fmaxf(v.w, 0.f));
+        *reinterpret_cast<uint2*>(st.up_b + act_offset(c, R, NR)) =
+            make_uint2((uint32_t)f32_to_bf16(o.x) | ((uint32_t)f32_to_bf16(o.y) << 16),
+                       (uint32_t)f32_to_bf16(o.z) | ((uint32_t)f32_to_bf16(o.w) << 16));
+    }
+}
+
+// the fill epilogue for a full-K unit straight from TMEM (one row per thread)
+__device__ __forceinline__ void epi_fill_direct(const DevState& st, const IterSmem& sm, int layer, int m, int nval) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, dp = st.dm.dp;
+    const int row = 32 * (warp & 3) + lane;
+    const int R = m * kBM + row;
+    const int kind = R / dp;  // 0 k, 1 v
+    const int f = R - kind * dp;
+    uint16_t* pool = kind == 0 ? st.kpool : st.vpool;
+    const uint32_t trow = sm.tmem + ((uint32_t)(32 * (warp & 3)) << 16);
+    for (int c0 = 16 * (warp >> 2); c0 < nval; c0 += 32) {
+        float v[16];
+        tmem_ld16(trow + (uint32_t)c0, v);
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+            if (c0 + j < nval) pool[kv_dst(st, sm, c0 + j, layer) + f] = f32_to_bf16(v[j]);
+    }
+}
+
+// Reduce phase: piece (m, c) = 128 rows of one output column, one warp per
+// piece (4 rows per lane), two pieces in flight per warp; the K splits are
+// summed in split order (deterministic).  K == kIDown also produces the exit
+// check's per-tile partial dots (fp64, fixed shuffle tree).
+template <int K>
+__device__ void reduce_phase(const DevState& st, const IterSmem& sm, const IterPlan& p, const IterGemm& g,
+                             const IterCtx& x, int nval, int unit_base, int m_total) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (warp >= 8) return;
+    const int S = g.splits;
+    const int P = m_total * nval;
+    const int GW = (int)gridDim.x * 8, gw = (int)blockIdx.x * 8 + warp;
+    const int dp = st.dm.dp, Bm = st.dm.Bmax;
+    for (int p0 = gw; p0 < P; p0 += 2 * GW) {
+        int mm[2], cc[2];
+        bool ok[2];
+        float4 acc[2];
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            const int pp = p0 + j * GW;
+            ok[j] = pp < P;
+            mm[j] = ok[j] ? pp / nval : 0;
+            cc[j] = ok[j] ? pp % nval : 0;
+            acc[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        for (int s0 = 0; s0 < S; s0 += 8) {
+            float4 v[2][8];
+#pragma unroll
+            for (int j = 0; j < 2; ++j)
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    v[j][k] = make_float4(0.f, 0.f, 0.f, 0.f);
+                    if (ok[j] && s0 + k < S) {
+                        // unit index of (tile m, split s): fill units are (jj, m2, s) with m = jj*m2 + m2 == tile index
+                        const size_t u = (size_t)unit_base + (size_t)mm[j] * S + s0 + k;
+                        v[j][k] = __ldcg(reinterpret_cast<const float4*>(p.part + (u * p.n_pad + cc[j]) * kBM) + lane);
+                    }
+                }
+#pragma unroll
+            for (int j = 0; j < 2; ++j)
+#pragma unroll
+                for (int k = 0; k < 8; ++k)
+                    if (s0 + k < S) {
+                        acc[j].x += v[j][k].x;
+                        acc[j].y += v[j][k].y;
+                        acc[j].z += v[j][k].z;
+                        acc[j].w += v[j][k].w;
+                    }
+        }
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            if (!ok[j]) continue;  // warp-uniform
+            const int m = mm[j], c = cc[j], r0 = 4 * lane;
+            if constexpr (K == kIFill) {
+                const int m2 = 2 * dp / kBM;
+                IterCtx y = x;
+                y.layer = x.layer + m / m2;  // x.layer = first skipped layer
+                apply4<K>(st, sm, y, m % m2, c, r0, acc[j]);
+            } else if constexpr (K == kIDown) {
+                const int R = m * kBM + r0;
+                const size_t i = (size_t)c * dp + R;
+                const float4 mid = __ldcg(reinterpret_cast<const float4*>(st.mid32 + i));
+                const float4 o = make_float4(mid.x + acc[j].x, mid.y + acc[j].y, mid.z + acc[j].z, mid.w + acc[j].w);
+                *reinterpret_cast<float4*>(st.h32 + (size_t)x.pout * Bm * dp + i) = o;
+                *reinterpret_cast<uint2*>(st.hb + (size_t)x.pout * st.NR * dp + act_offset(c, R, st.NR)) =
+                    make_uint2((uint32_t)f32_to_bf16(o.x) | ((uint32_t)f32_to_bf16(o.y) << 16),
+                               (uint32_t)f32_to_bf16(o.z) | ((uint32_t)f32_to_bf16(o.w) << 16));
+                if (st.technique == kState || st.technique == kClassifier) {
+                    double x0 = 0.0, x1 = 0.0, x2 = 0.0;
+                    const float ov[4] = {o.x, o.y, o.z, o.w};
+                    if (st.technique == kState) {
+                        const float4 h = __ldcg(reinterpret_cast<const float4*>(st.h32 + (size_t)x.pin * Bm * dp + i));
+                        const float hv[4] = {h.x, h.y, h.z, h.w};
+#pragma unroll
+                        for (int t = 0; t < 4; ++t) {
+                            const double a = hv[t], b = ov[t];
+                            x0 += a * b;
+                            x1 += a * a;
+                            x2 += b * b;
+                        }
+                    } else {
+#pragma unroll
+                        for (int t = 0; t < 4; ++t) x0 += (double)__ldg(&st.probe_w[R + t]) * (double)ov[t];
+                    }
+                    x0 = warp_sum_d(x0);
+                    x1 = warp_sum_d(x1);
+                    x2 = warp_sum_d(x2);
+                    if (lane == 0) {
+                        double* q = st.exit_part + ((size_t)m * Bm + c) * 3;
+                        q[0] = x0;
+                        q[1] = x1;
+                        q[2] = x2;
+                    }
+                }
+            } else {
+                apply4<K>(st, sm, x, m, c, r0, acc[j]);
+            }
+        }
+    }
+}
+
+// exit decision of `layer` for every row, computed identically by every CTA
+// (exit_policy.cpp:89-115, engine.cpp:55-66); returns "stop here".
+__device__ bool exit_decide(const DevState& st, IterSmem& sm, int layer, int B) {
+    const int tid = threadIdx.x, Bm = st.dm.Bmax, mt = st.dm.dp / kBM;
+    int all = 1;
+    if (tid < B) {
+        const int b = tid;
+        float conf = __int_as_float(0x7fc00000);
+        int acc = 0;
+        const double lam = st.lambdas[layer - 1];
+        switch (st.technique) {
+            case kState:
+            case kClassifier: {
+                double x0 = 0.0, x1 = 0.0, x2 = 0.0;
+                for (int m = 0; m < mt; ++m) {  // fixed tile order
+                    const double* q = st.exit_part + ((size_t)m * Bm + b) * 3;
+                    x0 += __ldcg(q);
+                    x1 += __ldcg(q + 1);
+                    x2 += __ldcg(q + 2);
+                }
+                double cd;
+                if (st.technique == kState) cd = x0 / (sqrt(x1) * sqrt(x2));  // NaN on a zero-norm state
+                else cd = 1.0 / (1.0 + exp(-(x0 + (double)st.probe_b)));
+                conf = (float)cd;
+                acc = cd > lam;
+                break;
+            }
+            case kSoftmax:
+                conf = __ldcg(&st.conf[(size_t)(layer - 1) * Bm + b]);
+                acc = __ldcg(&st.accept[b]);
+                break;
+            case kFixed:
+                conf = st.fixed_conf[(size_t)(layer - 1) * Bm + b];
+                acc = (double)conf > lam;
+                break;
+            case kAlwaysAt: acc = layer >= st.exit_layer; break;
+            default: acc = 0; break;
+        }
+        int s = sm.status[b];
+        if (!s && acc) {
+            s = 1;
+            sm.status[b] = 1;
+            sm.first[b] = layer;
+        }
+        all = s;
+        if (blockIdx.x == 0) {
+            if (st.technique != kSoftmax) {  // softmax: written by the distributed decide phase
+                st.conf[(size_t)(layer - 1) * Bm + b] = conf;
+                st.accept[b] = acc;
+            }
+            st.status[b] = s;
+            st.first_accept[b] = sm.first[b];
+        }
+    }
+    all = __syncthreads_and(all);
+    return all || layer >= st.dm.L;
+}
+
+// ---------------------------------------------------------------------------
+// batch-M GEMM (small batch): the batch rows are the M=128 operand (only the
+// n_pad valid rows are loaded; the rest of the tile is ignored), a block of nt
+// output features is N, and each unit runs the FULL reduction dimension, so the
+// epilogue applies directly from TMEM -- no split-K partials, no reduce phase,
+// one grid barrier per GEMM.  Costs an L2 read of the whole activation matrix
+// per CTA (B x K bf16), cheap for B <= 128.
+// ---------------------------------------------------------------------------
+template <int K>
+__device__ __forceinline__ void apply16_t(const DevState& st, const IterSmem& sm, const IterCtx& x, int b, int f,
+                                          const float* v) {
+    const int dp = st.dm.dp, NR = st.NR, Bm = st.dm.Bmax;
+    auto pack = [](const float* w) {
+        return make_uint4((uint32_t)f32_to_bf16(w[0]) | ((uint32_t)f32_to_bf16(w[1]) << 16),
+                          (uint32_t)f32_to_bf16(w[2]) | ((uint32_t)f32_to_bf16(w[3]) << 16),
+                          (uint32_t)f32_to_bf16(w[4]) | ((uint32_t)f32_to_bf16(w[5]) << 16),
+                          (uint32_t)f32_to_bf16(w[6]) | ((uint32_t)f32_to_bf16(w[7]) << 16));
+    };
+    if constexpr (K == kIQkv) {
+        const int kind = f / dp;
+        if (kind == 0) {
+            float4* q = reinterpret_cast<float4*>(st.q32 + (size_t)b * dp + f);
+#pragma unroll
+            for (int t = 0; t < 4; ++t) q[t] = make_float4(v[4 * t], v[4 * t + 1], v[4 * t + 2], v[4 * t + 3]);
+        } else {
+            uint16_t* dst = (kind == 1 ? st.kpool : st.vpool) + kv_dst(st, sm, b, x.layer) + (f - kind * dp);
+            reinterpret_cast<uint4*>(dst)[0] = pack(v);
+            reinterpret_cast<uint4*>(dst)[1] = pack(v + 8);
+        }
+    } else if constexpr (K == kIWo) {
+        const size_t i = (size_t)b * dp + f;
+        const float4* h = reinterpret_cast<const float4*>(st.h32 + (size_t)x.pin * Bm * dp + i);
+        float o[16];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            const float4 hv = __ldcg(h + t);
+            o[4 * t] = hv.x + v[4 * t];
+            o[4 * t + 1] = hv.y + v[4 * t + 1];
+            o[4 * t + 2] = hv.z + v[4 * t + 2];
+            o[4 * t + 3] = hv.w + v[4 * t + 3];
+        }
+        float4* m = reinterpret_cast<float4*>(st.mid32 + i);
+#pragma unroll
+        for (int t = 0; t < 4; ++t) m[t] = make_float4(o[4 * t], o[4 * t + 1], o[4 * t + 2], o[4 * t + 3]);
+        *reinterpret_cast<uint4*>(st.mid_b + act_offset(b, f, NR)) = pack(o);
+        *reinterpret_cast<uint4*>(st.mid_b + act_offset(b, f + 8, NR)) = pack(o + 8);
+    } else if constexpr (K == kIUp) {
+        float o[16];
+#pragma unroll
+        for (int t = 0; t < 16; ++t) o[t] = fmaxf(v[t], 0.f);
+        *reinterpret_cast<uint4*>(st.up_b + act_offset(b, f, NR)) = pack(o);
+        *reinterpret_cast<uint4*>(st.up_b + act_offset(b, f + 8, NR)) = pack(o + 8);
+    }
+}
+
+template <int K>
+__device__ __forceinline__ void gemm_phase_t(const DevState& st, IterSmem& sm, uint8_t* ring, const IterPlan& p,
+                                             const IterGemm& g, const IterCtx& x, const uint16_t* act,
+                                             uint32_t& kseq2, uint32_t& useq, int B) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int U = g.m_tiles * kBM / g.nt;
+    auto stamp = [&](int k) {  // dbg 64: per-CTA unit timeline of layer 1's batch-M GEMMs
+        if ((st.dbg & 64) && x.layer == 1 && (threadIdx.x & 31) == 0) {
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+            st.dbg_ts[300000 + (size_t)blockIdx.x * 32 + K * 8 + k] = t;
+        }
+    };
+    if (threadIdx.x == 0) stamp(0);
+    for (int u = blockIdx.x; u < U; u += gridDim.x) {
+        const int f0 = u * g.nt;
+        // weight rows [f0, f0 + nt) of every k-block: nt x 128 B inside the pre-swizzled 128-row tile
+        const uint16_t* w = g.A + (size_t)((x.layer - 1) * g.layer_rows + g.row_off + f0 / kBM) * g.kb_total *
+                                      (kBM * kBK) + (size_t)(f0 % kBM) * kBK;
+        // small stages: the A (batch) region holds only n_pad rows; the MMA's reads of rows >= n_pad run into
+        // the next stage (ignored output rows), so up to 16 k-blocks are in flight at once
+        const RingDesc r{sm.full2, sm.empty2, (uint32_t)p.stages2, (uint32_t)p.stage2_bytes, (uint32_t)p.stage2_boff};
+        // timing probes (wrong results): dbg 1<<16 reads weights from one fixed tile, 1<<17 activations from one k-block
+        const size_t wks = (st.dbg & (1 << 16)) ? 0 : (size_t)(kBM * kBK);
+        const size_t aks = (st.dbg & (1 << 17)) ? 0 : (size_t)st.NR * kBK;
+        unit_mainloop(sm, ring, r, kseq2, act, (uint32_t)p.n_pad * 128u, aks, w, (uint32_t)g.nt * 128u, wks, 0,
+                      g.kb_total, (uint32_t)g.nt, useq, st.dbg);
+        if (threadIdx.x == 0) {
+            stamp(2);
+            if ((st.dbg & 64) && x.layer == 1) {
+                st.dbg_ts[300000 + (size_t)blockIdx.x * 32 + K * 8 + 4] = sm.tdbg[0];
+                st.dbg_ts[300000 + (size_t)blockIdx.x * 32 + K * 8 + 5] = sm.tdbg[1];
+                st.dbg_ts[300000 + (size_t)blockIdx.x * 32 + K * 8 + 6] = sm.tdbg[2];
+                st.dbg_ts[300000 + (size_t)blockIdx.x * 32 + K * 8 + 7] = sm.tdbg[3];
+            }
+        }
+        if (warp < 8) {
+            const int b = 32 * (warp & 3) + lane;
+            const uint32_t trow = sm.tmem + ((uint32_t)(32 * (warp & 3)) << 16);
+            for (int c0 = 16 * (warp >> 2); c0 < g.nt; c0 += 32) {
+                float v[16];
+                tmem_ld16(trow + (uint32_t)c0, v);
+                if (b < B) apply16_t<K>(st, sm, x, b, f0 + c0, v);
+            }
+        }
+        if (threadIdx.x == 0) stamp(3);
+        ++useq;
+        tc_fence_before();
+        __syncthreads();
+    }
+}
+
+// weight-streaming GEMM phase: this CTA's units (u = cta, cta + G, ...)
+__device__ __forceinline__ void gemm_phase(const DevState& st, IterSmem& sm, uint8_t* ring, const IterPlan& p,
+                                           const IterGemm& g, int layer, const uint16_t* bsrc, uint32_t& kseq,
+                                           uint32_t& useq, int nval) {
+    const int U = g.m_tiles * g.splits;
+    const size_t bks = (size_t)st.NR * kBK;
+    for (int u = blockIdx.x; u < U; u += gridDim.x) {
+        const int m = u / g.splits, s = u % g.splits;
+        const int kb0 = s * g.kb_total / g.splits, kb1 = (s + 1) * g.kb_total / g.splits;
+        const uint16_t* a = g.A + (size_t)((layer - 1) * g.layer_rows + g.row_off + m) * g.kb_total * (kBM * kBK);
+        unit_ws(sm, ring, p, kseq, a, bsrc, bks, kb0, kb1 - kb0, useq);
+        if ((threadIdx.x >> 5) < 8) epi_partial(sm, p, u, nval);
+        ++useq;
+        tc_fence_before();
+        __syncthreads();
+    }
+}
+
+template <int NJ>
+__global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(DevState st, IterPlan p) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* ring = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    IterSmem& sm = *reinterpret_cast<IterSmem*>(ring + p.ring_bytes);
+    float* tbuf = reinterpret_cast<float*>(ring + p.gemm_ring);
+    const int tid = threadIdx.x, warp = tid >> 5;
+    const int G = (int)gridDim.x, cta = (int)blockIdx.x;
+    const Dims& dm = st.dm;
+    const int B = st.rows.B, L = dm.L, dp = dm.dp, Bm = dm.Bmax, NR = st.NR;
+
+    if (tid == 0) {
+        for (int s = 0; s < 8; ++s) {
+            mbar_init(&sm.full[s], 1);
+            mbar_init(&sm.empty[s], 1);
+            mbar_init(&sm.att.full[s], 1);
+            mbar_init(&sm.att.empty[s], kAttnWarps);
+        }
+        for (int s = 0; s < 16; ++s) {
+            mbar_init(&sm.full2[s], 1);
+            mbar_init(&sm.empty2[s], 1);
+        }
+        mbar_init(&sm.acc, 1);
+        fence_barrier_init();
+    }
+    if (warp == 0) tmem_alloc(&sm.tmem, 512);
+    for (int b = tid; b < 256; b += blockDim.x) {
+        sm.pos[b] = b < B ? st.rows.pos[b] : 0;
+        sm.slot[b] = b < B ? st.rows.slot[b] : 0;
+        sm.status[b] = 0;
+        sm.first[b] = 0;
+    }
+    const int iter = *st.iter_counter;  // advanced by CTA 0 at the very end
+    // generation base of this launch: no barrier of this launch can complete before every CTA read it
+    const unsigned g0 = (st.dbg & (4096 | 32768)) ? *(volatile unsigned*)(p.bar + 1025) : *(volatile unsigned*)(p.bar + 1024);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+
+    uint32_t kseq = 0, kseq2 = 0, useq = 0;
+    int aseq = 0, nbar = 0;
+    if (st.dbg & 256)  // barrier cost probe: 32 back-to-back grid barriers
+        for (int i = 0; i < 32; ++i) grid_sync(p, st, nbar, g0);
+
+    // ---- embed (model.cpp:171-183): h_0 = embedding row of the input token ----
+    for (int b = cta; b < B; b += G) {
+        const uint16_t* e = st.emb + (size_t)st.rows.tok[b] * dp;
+        float* h = st.h32 + (size_t)b * dp;
+        for (int i = tid; i < dp; i += blockDim.x) {
+            const uint16_t v = e[i];
+            st.hb[act_offset(b, i, NR)] = v;
+            h[i] = bf16_to_f32(v);
+        }
+    }
+    grid_sync(p, st, nbar, g0);
+
+    int e_out = L;
+    for (int layer = 1; layer <= L; ++layer) {
+        const IterCtx x{layer, (layer - 1) & 1, layer & 1};
+        // q | k | v, K/V appended to the paged pool (model.cpp:218-226)
+        if (p.g[kIQkv].mode) {
+            gemm_phase_t<kIQkv>(st, sm, ring, p, p.g[kIQkv], x, st.hb + (size_t)x.pin * NR * dp, kseq2, useq, B);
+        } else {
+            gemm_phase(st, sm, ring, p, p.g[kIQkv], layer, st.hb + (size_t)x.pin * NR * dp, kseq, useq, B);
+            grid_sync(p, st, nbar, g0);
+            reduce_phase<kIQkv>(st, sm, p, p.g[kIQkv], x, B, 0, p.g[kIQkv].m_tiles);
+        }
+        grid_sync(p, st, nbar, g0);
+        // paged attention (model.cpp:223-243)
+        auto astamp = [&](int w) {
+            if ((st.dbg & 128) && tid == 0 && layer <= 24) {
+                unsigned long long t;
+                asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+                st.dbg_ts[40000 + (layer - 1) * 512 + cta * 2 + w] = t;
+            }
+        };
+        astamp(0);
+        if (warp == kProducerWarp && (p.pf_flags & 1)) {  // this layer's W_o / up / down tiles -> L2
+            l2_prefetch_gemm(p.g[kIWo], layer);
+            l2_prefetch_gemm(p.g[kIUp], layer);
+            l2_prefetch_gemm(p.g[kIDown], layer);
+        }
+        __syncwarp();
+        attn_body<NJ>(st, sm.att, ring, layer, aseq);
+        astamp(1);
+        grid_sync(p, st, nbar, g0);
+        aseq = sm.att.seq_next;
+        if (warp == kProducerWarp && layer < L && p.kv_pf_blocks > 0)  // next layer's K/V -> L2
+            l2_prefetch_kv(st, sm.att, layer + 1, p.kv_pf_blocks);
+        __syncwarp();
+        // W_o + residual (model.cpp:245-253)
+        if (p.g[kIWo].mode) {
+            gemm_phase_t<kIWo>(st, sm, ring, p, p.g[kIWo], x, st.att_b, kseq2, useq, B);
+        } else {
+            gemm_phase(st, sm, ring, p, p.g[kIWo], layer, st.att_b, kseq, useq, B);
+            grid_sync(p, st, nbar, g0);
+            reduce_phase<kIWo>(st, sm, p, p.g[kIWo], x, B, 0, p.g[kIWo].m_tiles);
+        }
+        grid_sync(p, st, nbar, g0);
+        // up + ReLU (model.cpp:255-260)
+        if (p.g[kIUp].mode) {
+            gemm_phase_t<kIUp>(st, sm, ring, p, p.g[kIUp], x, st.mid_b, kseq2, useq, B);
+        } else {
+            gemm_phase(st, sm, ring, p, p.g[kIUp], layer, st.mid_b, kseq, useq, B);
+            grid_sync(p, st, nbar, g0);
+            reduce_phase<kIUp>(st, sm, p, p.g[kIUp], x, B, 0, p.g[kIUp].m_tiles);
+        }
+        grid_sync(p, st, nbar, g0);
+        // down + residual (model.cpp:261-270) + exit-check partial dots
+        gemm_phase(st, sm, ring, p, p.g[kIDown], layer, st.up_b, kseq, useq, B);
+        grid_sync(p, st, nbar, g0);
+        if (warp == kProducerWarp && layer < L && (p.pf_flags & 1)) l2_prefetch_gemm(p.g[kIQkv], layer + 1);
+        reduce_phase<kIDown>(st, sm, p, p.g[kIDown], x, B, 0, p.g[kIDown].m_tiles);
+        grid_sync(p, st, nbar, g0);
+        if (st.technique == kSoftmax) {
+            // LM head over h_l with the fused (max1, max2, sum exp) reduction
+            const uint16_t* bsrc = st.hb + (size_t)x.pout * NR * dp;
+            for (int t = cta; t < p.lm_tiles; t += G) {
+                unit_ws(sm, ring, p, kseq, st.lm + (size_t)t * (dp / kBK) * (kBM * kBK), bsrc, (size_t)NR * kBK, 0,
+                        dp / kBK, useq);
+                if (warp < 8) epi_lm<true>(st, sm, tbuf, t, B);
+                ++useq;
+                tc_fence_before();
+                __syncthreads();
+            }
+            grid_sync(p, st, nbar, g0);
+            // softmax_response_confidence (exit_policy.cpp:57-72), rows spread over the grid
+            if (warp < 8)
+                for (int b = cta + G * warp; b < B; b += G * 8) {
+                    const LmPart r = lm_col_warp(st, b);
+                    if ((tid & 31) == 0) {
+                        const float gap = (r.m2 == -INFINITY) ? 1.f : -expm1f(r.m2 - r.m1);
+                        const float conf = gap / r.s;
+                        st.conf[(size_t)(layer - 1) * Bm + b] = conf;
+                        st.accept[b] = (double)conf > st.lambdas[layer - 1];
+                    }
+                }
+            grid_sync(p, st, nbar, g0);
+        }
+        if (exit_decide(st, sm, layer, B)) {
+            e_out = layer;
+            break;
+        }
+    }
+
+    // ---- tail: greedy LM head over h_e and the skipped-layer fill (kv_cache.cpp:222-234) ----
+    const int pe = e_out & 1;
+    const IterGemm& gf = p.g[kIFill];
+    const int n_lm = (st.technique == kSoftmax) ? 0 : p.lm_tiles;  // softmax: the last check's partials
+    const int m2 = 2 * dp / kBM;
+    const int fill_units = (L - e_out) * m2 * gf.splits;
+    {
+        const uint16_t* bsrc = st.hb + (size_t)pe * NR * dp;
+        for (int it = cta; it < n_lm + fill_units; it += G) {
+            if (it < n_lm) {
+                unit_ws(sm, ring, p, kseq, st.lm + (size_t)it * (dp / kBK) * (kBM * kBK), bsrc, (size_t)NR * kBK, 0,
+                        dp / kBK, useq);
+                if (warp < 8) epi_lm<false>(st, sm, tbuf, it, B);
+            } else {
+                const int u = it - n_lm;
+                const int mj = u / gf.splits, s = u % gf.splits;  // mj = (jj, m) flattened
+                const int j = e_out + 1 + mj / m2, m = mj % m2;
+                const int kb0 = s * gf.kb_total / gf.splits, kb1 = (s + 1) * gf.kb_total / gf.splits;
+                const uint16_t* a =
+                    gf.A + (size_t)((j - 1) * gf.layer_rows + gf.row_off + m) * gf.kb_total * (kBM * kBK);
+                unit_ws(sm, ring, p, kseq, a, bsrc, (size_t)NR * kBK, kb0, kb1 - kb0, useq);
+                if (warp < 8) {
+                    if (gf.splits == 1) epi_fill_direct(st, sm, j, m, B);
+                    else epi_partial(sm, p, u, B);
+                }
+            }
+            ++useq;
+            tc_fence_before();
+            __syncthreads();
+        }
+    }
+    grid_sync(p, st, nbar, g0);
+    if (fill_units > 0 && gf.splits > 1) {
+        const IterCtx x{e_out + 1, 0, 0};
+        reduce_phase<kIFill>(st, sm, p, gf, x, B, 0, (L - e_out) * m2);
+    }
+    // greedy_token (model.cpp:288-299) + commit + records (engine.cpp:280-306)
+    if (warp < 8) {
+        const int lane = tid & 31;
+        const int cur = iter % st.rec_cap;
+        for (int b = cta + G * warp; b < B; b += G * 8) {
+            const LmPart r = lm_col_warp(st, b);
+            for (int l = lane; l < L; l += 32)
+                st.rec_conf[((size_t)cur * L + l) * Bm + b] = __ldcg(&st.conf[(size_t)l * Bm + b]);
+            if (lane == 0) {
+                const int fa = sm.first[b];
+                st.rec_tok[(size_t)cur * Bm + b] = r.idx;
+                st.rec_acc[(size_t)cur * Bm + b] = fa ? fa : L;
+                st.rows.tok[b] = r.idx;       // next input (engine.cpp:304)
+                st.rows.pos[b] = sm.pos[b] + 1;  // KvStore::commit (engine.cpp:262-264)
+            }
+        }
+    }
+    if (cta == 0 && tid == 0) {
+        if (!(st.dbg & (2048 | 4096 | 32768))) *(volatile unsigned*)p.bar = 0u;  // arrivals of this launch are all in
+        if (st.dbg & (4096 | 32768)) *(volatile unsigned*)(p.bar + 1025) = g0 + (unsigned)nbar;  // flag epochs continue
+        st.rec_out[iter % st.rec_cap] = e_out;
+        *st.out_layer = e_out;
+        *st.layer = e_out + 1;
+        *st.cur_iter = iter;
+        *st.iter_counter = iter + 1;
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) tmem_dealloc(sm.tmem, 512);
+}
+
+int iter_smem_bytes(int ring_bytes) { return 1024 + ring_bytes + (int)sizeof(IterSmem); }
+
+void launch_iter(const DevState& st, const IterPlan& p, int grid, cudaStream_t s) {
+    const int nj = (st.dm.dp / 8 + 31) / 32;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kIterThreads);
+    cfg.dynamicSmemBytes = (size_t)iter_smem_bytes(p.ring_bytes);
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    if (nj <= 1) cudaLaunchKernelEx(&cfg, iter_kernel<1>, st, p);
+    else if (nj == 2) cudaLaunchKernelEx(&cfg, iter_kernel<2>, st, p);
+    else if (nj == 3) cudaLaunchKernelEx(&cfg, iter_kernel<3>, st, p);
+    else cudaLaunchKernelEx(&cfg, iter_kernel<4>, st, p);
+    EL_CUDA_LAUNCH_CHECK();
+}
+
+int iter_max_ctas_per_sm(const Dims& dm, int ring_bytes) {
+    const int nj = (dm.dp / 8 + 31) / 32;
+    const int smem = iter_smem_bytes(ring_bytes);
+    int n = 0;
+    cudaError_t e;
+    if (nj <= 1) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, iter_kernel<1>, kIterThreads, smem);
+    else if (nj == 2) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, iter_kernel<2>, kIterThreads, smem);
+    else if (nj == 3) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, iter_kernel<3>, kIterThreads, smem);
+    else e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, iter_kernel<4>, kIterThreads, smem);
+    return e == cudaSuccess ? n : 0;
+}
+
+void init_iter_attributes() {
+    const int m = 227 * 1024;
+    cudaFuncSetAttribute(iter_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, m);
+    cudaFuncSetAttribute(iter_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, m);
+    cudaFuncSetAttribute(iter_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, m);
+    cudaFuncSetAttribute(iter_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, m);
+}
+int iter_smem_fixed() { return 1024 + (int)sizeof(IterSmem); }

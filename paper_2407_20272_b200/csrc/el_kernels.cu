@@ -1403,4 +1403,6 @@ void init_kernel_attributes() {
     cudaFuncSetAttribute(attn_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, m);
 }
 
+#include "el_iter.cuh"
+
 }  // namespace el

@@ -159,6 +159,43 @@ void launch_layer_head(const DevState& st, cudaStream_t s);  // prefill commit: 
 void launch_kv_alloc(int* stack, int top, int* tables, const Dims& dm, int slot, int bpl, cudaStream_t s);
 void launch_kv_release(int* stack, int top, const int* tables, const Dims& dm, int slot, int bpl, cudaStream_t s);
 
+
+// ---- persistent decode-iteration kernel (el_iter.cuh) ----
+enum IterGemmId : int { kIQkv = 0, kIWo, kIUp, kIDown, kIFill, kINumGemm };
+
+struct IterGemm {
+    const uint16_t* A;  // tiled weights (tiled_offset), tile row 0 of layer 1
+    int m_tiles;        // 128-row output tiles (per layer)
+    int kb_total;       // 64-wide k-blocks of the reduction dimension
+    int splits;         // K splits per output tile (units = m_tiles * splits)
+    int layer_rows;     // tile rows per layer in A
+    int row_off;        // tile-row offset inside a layer (fill: the k|v rows)
+    int mode;           // 0 weight-streaming split-K + reduce phase; 1 batch-M full-K (direct epilogue)
+    int nt;             // mode 1: output features per unit (MMA N)
+};
+
+struct IterPlan {
+    IterGemm g[kINumGemm];
+    int n_pad;       // MMA N: batch rounded up to 16
+    int stages;      // GEMM ring depth
+    int stage_bytes; // GEMM ring stage stride (A region 16 KB | B region)
+    int stages2, stage2_bytes, stage2_boff;  // batch-M ring: depth, stride, offset of the weight region
+    int ring_bytes;  // shared ring region (attention stages / GEMM stages + LM transpose buffer)
+    int gemm_ring;   // bytes of the GEMM stages inside the ring region
+    int lm_tiles;    // Vp / 128
+    int kv_pf_blocks;  // per CTA: K/V blocks of the next layer prefetched into L2 after attention
+    int pf_flags;      // bit 0: L2 prefetch of GEMM weight tiles one phase ahead
+    float* part;     // split-K partials [unit][n_pad][128] fp32
+    unsigned* bar;   // grid barrier: [0] arrivals, [32] generation
+};
+
+int iter_smem_bytes(int ring_bytes);   // dynamic shared memory of the launch
+int iter_smem_fixed();                 // bytes outside the ring region (alignment slack + control block)
+int iter_max_ctas_per_sm(const Dims& dm, int ring_bytes);
+void init_iter_attributes();
+void launch_iter(const DevState& st, const IterPlan& p, int grid, cudaStream_t s);
+constexpr int kIterTbufBytes = 32 * 129 * 4;
+
 // host+device mirror of the allocator arithmetic (used by el_kv_block_trace)
 inline void kv_pop_host(const int* stack, int top, int* table_flat, int n) {
     for (int i = 0; i < n; ++i) table_flat[i] = stack[top - 1 - i];

@@ -341,7 +341,11 @@ class Engine:
     """exitlab::Engine on one B200 (engine.hpp:131-147). Weights are seeded from
     config.model (ModelWeights::seeded, model.cpp:37-59) and stored as bf16."""
 
-    def __init__(self, config: EngineConfig, graph: bool = True):
+    def __init__(self, config: EngineConfig, graph: bool = True, mega: bool = True):
+        """graph/mega select how a decode iteration is launched: mega (default) =
+        one persistent kernel per iteration (layer loop on the device); otherwise
+        per-phase kernels in a CUDA graph with a device-side WHILE (graph) or a
+        host-driven layer loop (eager)."""
         self.config = config
         self._c = to_c_config(config)
         h = C.c_void_p()
@@ -350,6 +354,7 @@ class Engine:
         self.L, self.d, self.V = config.model.n_layers, config.model.d_model, config.model.vocab_size
         self.B = 0
         self.set_option("graph", int(graph))
+        self.set_option("mega", int(mega))
 
     def close(self):
         if getattr(self, "_h", None):
@@ -444,10 +449,13 @@ class Engine:
         return lib().el_launches_per_iteration(self._h, output_layer)
 
     def plan_info(self):
-        out = np.zeros(32, np.int64)
-        n = lib().el_plan_info(self._h, _ptr(out), 32)
+        out = np.zeros(64, np.int64)
+        n = lib().el_plan_info(self._h, _ptr(out), 64)
         names = ["attn_cb", "attn_stages", "attn_max_chunks", "n_pad", "qkv_splits", "wo_splits", "up_splits",
-                 "down_splits", "fill_splits", "qkv_stages", "lm_tiles", "dp", "fp", "Vp", "bpl_max"]
+                 "down_splits", "fill_splits", "qkv_stages", "lm_tiles", "dp", "fp", "Vp", "bpl_max",
+                 "mega_qkv_mode", "mega_wo_mode", "mega_up_mode", "mega_qkv_splits", "mega_wo_splits",
+                 "mega_up_splits", "mega_down_splits", "mega_fill_splits", "mega_qkv_nt", "mega_wo_nt", "mega_up_nt",
+                 "mega_stages", "mega_stages2", "mega_att_stages", "mega"]
         return dict(zip(names, out[:n].tolist()))
 
     def model_tensor(self, which, layer=0):

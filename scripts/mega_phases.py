@@ -1,0 +1,102 @@
+"""Phase timeline of the persistent decode-iteration kernel (dbg bit 128: CTA 0
+stamps %globaltimer at every grid barrier).  Usage:
+    python scripts/mega_phases.py [config c2|c5|c1|c3] [technique] [json options]
+Prints per-phase durations of one iteration, averaged per layer."""
+import ctypes as C
+import json
+import sys
+
+import numpy as np
+
+sys.path.insert(0, "/root/repo")
+from paper_2407_20272_b200 import exitlab as X  # noqa: E402
+
+DIMS = {"c1": (6, 512, 8), "c2": (12, 768, 64), "c3": (24, 1024, 128), "c5": (24, 1024, 256)}
+cfgname = sys.argv[1] if len(sys.argv) > 1 else "c2"
+tech = sys.argv[2] if len(sys.argv) > 2 else "never"
+opts = json.loads(sys.argv[3]) if len(sys.argv) > 3 else {}
+L, d, B = DIMS[cfgname]
+cfg = X.EngineConfig(model=X.ModelConfig(L, d, 32128, 0), technique=X.ExitTechnique(tech, 4),
+                     schedule=X.ThresholdSchedule(0.981, 0.997, 0.0), max_batch=B, pool_blocks=B * L * 40,
+                     eos_token=-1)
+e = X.Engine(cfg)
+for kk, v in opts.items():
+    if kk != "xdbg":
+        e.set_option(kk, v)
+e.session_begin(np.arange(B) + 1, 511, 640, 1)
+lib = X.lib()
+lib.el_debug_timestamps.argtypes = [C.c_void_p, C.c_void_p, C.c_int]
+e.decode_run(3)
+e.sync()
+e.set_option("dbg", 128 | 64 | int(opts.get("xdbg", 0)))
+e.decode_run(1)
+e.sync()
+ts = np.zeros(65536 + 256 * 1024, np.uint64)
+lib.el_debug_timestamps(e._h, ts.ctypes.data_as(C.c_void_p), ts.size)
+t = ts[20480:20480 + 1024].astype(np.float64)
+n = int(np.argmax(t == 0)) if (t == 0).any() else 1024
+t = t[:n]
+dt = np.diff(t) / 1e3
+pi = e.plan_info()
+per_layer = []
+for nm in ("qkv", "attn", "wo", "up", "down"):
+    per_layer.append(nm)
+    if nm == "down" or (nm != "attn" and not pi[f"mega_{nm}_mode"]):
+        per_layer.append(nm + "_red")
+print({k: v for k, v in pi.items() if k.startswith("mega")})
+if tech == "softmax":
+    per_layer += ["lmchk", "sm_decide"]
+names = ["embed->first"]
+rec = e.records(3, 1)
+eo = int(rec["output_layer"][0])
+for layer in range(eo):
+    names += [f"{x}@{layer + 1}" for x in per_layer]
+names += ["tail(lm+fill)"]
+print(f"config {cfgname} tech {tech} e={eo} barriers={n} span {(t[-1] - t[0]) / 1e3:.2f} us")
+acc = {}
+arr = ts[65536:65536 + 148 * 1024].reshape(148, 1024)[:, :n].astype(np.float64)  # per-CTA arrival times
+wrk = {}
+for i, v in enumerate(dt):
+    nm = names[i + 1] if i + 1 < len(names) else f"?{i}"
+    key = nm.split("@")[0]
+    acc.setdefault(key, []).append(v)
+    # critical path of the phase: last CTA arrival - previous barrier exit (CTA 0)
+    wrk.setdefault(key, []).append((arr[:, i + 1].max() - t[i]) / 1e3)
+for k, v in acc.items():
+    print(f"{k:12s} n={len(v):3d} mean {np.mean(v):7.2f} us  (work crit path {np.mean(wrk[k]):6.2f}, barrier "
+          f"{np.mean(v) - np.mean(wrk[k]):5.2f})  total {np.sum(v):8.2f} us")
+e.set_option("dbg", 0)
+ms = e.time_decode(10)
+print(f"timed: {ms / 10 * 1e3:.1f} us/iteration")
+# per-CTA attention phase spans (dbg 128): start skew and duration spread
+A = ts[40000:40000 + 24 * 512].reshape(24, 256, 2).astype(np.float64)[:, :148]
+for layer in (0, eo - 1):
+    a = A[layer]
+    if a[:, 0].min() == 0:
+        continue
+    st0 = a[:, 0].min()
+    dur = (a[:, 1] - a[:, 0]) / 1e3
+    print(f"attn layer {layer + 1}: start skew {(a[:, 0].max() - st0) / 1e3:.2f} us, dur min {dur.min():.2f} "
+          f"p50 {np.median(dur):.2f} max {dur.max():.2f} us, last end {(a[:, 1].max() - st0) / 1e3:.2f} us")
+    order = np.argsort(dur)
+    print("   slowest CTAs:", order[-8:].tolist(), "fastest:", order[:8].tolist())
+
+# batch-M GEMM unit timeline of layer 1 (dbg 64): [start, -, acc ready, epilogue done] per CTA
+U = ts[300000:300000 + 148 * 32].reshape(148, 4, 8).astype(np.float64)
+for k, nm in ((0, "qkv"), (1, "wo"), (2, "up")):
+    u = U[:, k]
+    ok = (u[:, 0] > 0) & (u[:, 2] > 0)
+    if not ok.any():
+        continue
+    t0 = u[ok, 0].min()
+    acc = (u[ok, 2] - u[ok, 0]) / 1e3
+    epi = (u[ok, 3] - u[ok, 2]) / 1e3
+    f1 = (u[ok, 4] - u[ok, 0]) / 1e3
+    fl = (u[ok, 5] - u[ok, 0]) / 1e3
+    i0 = (u[ok, 6] - u[ok, 0]) / 1e3
+    i1 = (u[ok, 7] - u[ok, 0]) / 1e3
+    print(f"{nm}: producer issued first at p50 {np.median(i0):.2f} last at p50 {np.median(i1):.2f} max {i1.max():.2f}")
+    print(f"{nm}: first stage full p50 {np.median(f1):.2f} max {f1.max():.2f}; last stage full p50 {np.median(fl):.2f} "
+          f"max {fl.max():.2f}")
+    print(f"{nm}: start skew {(u[ok, 0].max() - t0) / 1e3:.2f} us; start->acc min {acc.min():.2f} p50 {np.median(acc):.2f} "
+          f"max {acc.max():.2f}; epilogue p50 {np.median(epi):.2f} max {epi.max():.2f}; last done {(u[ok, 3].max() - t0) / 1e3:.2f}")
