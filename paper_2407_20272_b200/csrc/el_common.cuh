@@ -149,6 +149,23 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
         : "memory");
 }
 
+// same with an L2 cache-eviction hint: streamed-once data (KV blocks, weights)
+// is loaded evict-first so it does not push the kernel's code, activations and
+// split-K partials out of L2
+constexpr uint64_t kL2EvictFirst = 0x12F0000000000000ull;
+constexpr uint64_t kL2EvictLast = 0x14F0000000000000ull;
+__device__ __forceinline__ void bulk_load_hint(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar,
+                                               uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+            dst),
+        "l"(src), "r"(bytes), "r"(bar), "l"(policy)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_load_ef(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    bulk_load_hint(smem_u32(dst), src, bytes, smem_u32(bar), kL2EvictFirst);
+}
+
 // ---------------------------------------------------------------------------
 // tcgen05 (5th-gen tensor cores, accumulators in TMEM)
 // ---------------------------------------------------------------------------

@@ -185,7 +185,7 @@ struct el_engine {
     DevBuf<unsigned> mbar;               // its grid barrier (arrivals, generation)
     int mega_grid = 0, mega_att_stages = 2, sms = 148;
     int opt_mega_fill_splits = 0, opt_mega_att_stages = 0, opt_mega_pf = 0, opt_mega_kv_pf_mb = 0,
-        opt_mega_bm_max = 128;
+        opt_mega_bm_max = 128, opt_attn_dyn_permille = 0, opt_attn_dyn_cb = 4;
     int attn_cb = 1, attn_stages = 2, attn_max_chunks = 1, attn_grid = 148;
     int NR = 16;
 
@@ -562,6 +562,8 @@ struct el_engine {
         el::IterPlan& P = mplan_for(B);
         el::DevState s = state(false, B);
         s.attn_stages = mega_att_stages;
+        s.attn_dyn_permille = opt_attn_dyn_permille;
+        s.attn_dyn_cb = opt_attn_dyn_cb;
         el::launch_iter(s, P, mega_grid, stream);
     }
 
@@ -1138,7 +1140,13 @@ int el_engine_set_option(el_engine* e, const char* key, int64_t v) {
     API_BEGIN
     if (!std::strcmp(key, "graph")) e->use_graph = v != 0;
     else if (!std::strcmp(key, "mega")) e->use_mega = v != 0;
-    else if (!std::strcmp(key, "mega_bm_max")) {
+    else if (!std::strcmp(key, "attn_dyn_permille")) {
+        if (v < 0 || v > 1000) fail(EL_INVALID_ARGUMENT, "attn_dyn_permille must be in [0, 1000]");
+        e->opt_attn_dyn_permille = (int)v;
+    } else if (!std::strcmp(key, "attn_dyn_cb")) {
+        if (v < 1 || v > 64) fail(EL_INVALID_ARGUMENT, "attn_dyn_cb must be in [1, 64]");
+        e->opt_attn_dyn_cb = (int)v;
+    } else if (!std::strcmp(key, "mega_bm_max")) {
         e->opt_mega_bm_max = (int)v;
         e->mplans.clear();
     } else if (!std::strcmp(key, "mega_pf") || !std::strcmp(key, "mega_kv_pf_mb")) {

@@ -216,7 +216,8 @@ struct RingDesc {
 __device__ __forceinline__ void unit_mainloop(IterSmem& sm, uint8_t* ring, const RingDesc& r, uint32_t& kseq,
                                               const uint16_t* a_src, uint32_t a_bytes, size_t a_kstride,
                                               const uint16_t* b_src, uint32_t b_bytes, size_t b_kstride, int kb0,
-                                              int nkb, uint32_t n_mma, uint32_t useq, int dbg = 0) {
+                                              int nkb, uint32_t n_mma, uint32_t useq, uint64_t a_policy,
+                                              uint64_t b_policy, int dbg = 0) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     // single-thread issue loops: stage index / phase / addresses are strength-reduced (no div/mod per
     // k-block -- a lone thread cannot hide the latency of that arithmetic)
@@ -234,15 +235,8 @@ __device__ __forceinline__ void unit_mainloop(IterSmem& sm, uint8_t* ring, const
                 if (wrapped) mbar_wait_addr(empty0 + 8 * s, ph ^ 1);
                 const uint32_t fb = full0 + 8 * s, sb = ring0 + s * r.stride;
                 asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(fb), "r"(tx) : "memory");
-                asm volatile(
-                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(sb),
-                    "l"(ap), "r"(a_bytes), "r"(fb)
-                    : "memory");
-                asm volatile(
-                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                        sb + r.b_off),
-                    "l"(bp), "r"(b_bytes), "r"(fb)
-                    : "memory");
+                bulk_load_hint(sb, ap, a_bytes, fb, a_policy);
+                bulk_load_hint(sb + r.b_off, bp, b_bytes, fb, b_policy);
                 ap += ast;
                 bp += bst;
                 if (++s == r.stages) {
@@ -252,6 +246,11 @@ __device__ __forceinline__ void unit_mainloop(IterSmem& sm, uint8_t* ring, const
                 }
             }
             kseq += (uint32_t)nkb;
+            if (dbg & 64) {
+                unsigned long long t;
+                asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+                sm.tdbg[3] = t;
+            }
         }
     } else if (warp == 0) {
         if (lane == 0) {
@@ -261,6 +260,11 @@ __device__ __forceinline__ void unit_mainloop(IterSmem& sm, uint8_t* ring, const
 #pragma unroll 1
             for (int i = 0; i < nkb; ++i) {
                 mbar_wait_addr(full0 + 8 * s, ph);
+                if ((dbg & 64) && (i == 0 || i == nkb - 1)) {
+                    unsigned long long t;
+                    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+                    sm.tdbg[i == 0 ? 0 : 1] = t;
+                }
                 tc_fence_after();
                 // (descriptors rebuilt per stage: the 14-bit address field wraps modulo 256 KB)
                 const uint32_t sa = ring0 + s * r.stride;
@@ -291,7 +295,7 @@ __device__ __forceinline__ void unit_ws(IterSmem& sm, uint8_t* ring, const IterP
                                         int nkb, uint32_t useq) {
     const RingDesc r{sm.full, sm.empty, (uint32_t)p.stages, (uint32_t)p.stage_bytes, (uint32_t)kAStage};
     unit_mainloop(sm, ring, r, kseq, a_row, kAStage, (size_t)(kBM * kBK), b_src, (uint32_t)p.n_pad * 128u, b_kstride,
-                  kb0, nkb, (uint32_t)p.n_pad, useq);
+                  kb0, nkb, (uint32_t)p.n_pad, useq, kL2EvictFirst, kL2EvictLast);
 }
 
 // split-K partial: part[u][c][row] for the nval valid columns
@@ -691,13 +695,14 @@ __device__ __forceinline__ void gemm_phase_t(const DevState& st, IterSmem& sm, u
         const size_t wks = (st.dbg & (1 << 16)) ? 0 : (size_t)(kBM * kBK);
         const size_t aks = (st.dbg & (1 << 17)) ? 0 : (size_t)st.NR * kBK;
         unit_mainloop(sm, ring, r, kseq2, act, (uint32_t)p.n_pad * 128u, aks, w, (uint32_t)g.nt * 128u, wks, 0,
-                      g.kb_total, (uint32_t)g.nt, useq, st.dbg);
+                      g.kb_total, (uint32_t)g.nt, useq, kL2EvictLast, kL2EvictFirst,
+                      x.layer == 1 ? st.dbg : (st.dbg & ~64));
         if (threadIdx.x == 0) {
             stamp(2);
             if ((st.dbg & 64) && x.layer == 1) {
                 st.dbg_ts[300000 + (size_t)blockIdx.x * 32 + K * 8 + 4] = sm.tdbg[0];
                 st.dbg_ts[300000 + (size_t)blockIdx.x * 32 + K * 8 + 5] = sm.tdbg[1];
-                st.dbg_ts[300000 + (size_t)blockIdx.x * 32 + K * 8 + 6] = sm.tdbg[2];
+                st.dbg_ts[300000 + (size_t)blockIdx.x * 32 + K * 8 + 6] = sm.tdbg[0];
                 st.dbg_ts[300000 + (size_t)blockIdx.x * 32 + K * 8 + 7] = sm.tdbg[3];
             }
         }
@@ -778,7 +783,15 @@ __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(DevState st, Iter
     int aseq = 0, nbar = 0;
     if (st.dbg & 256)  // barrier cost probe: 32 back-to-back grid barriers
         for (int i = 0; i < 32; ++i) grid_sync(p, st, nbar, g0);
+    if (st.dbg & (1 << 19)) {  // TMA probe: two QKV batch-M units back to back at kernel start
+        const IterCtx x0{1, 0, 1};
+        for (int rep = 0; rep < 2; ++rep) {
+            gemm_phase_t<kIQkv>(st, sm, ring, p, p.g[kIQkv], x0, st.hb, kseq2, useq, B);
+            grid_sync(p, st, nbar, g0);
+        }
+    }
 
+    if (warp == kProducerWarp) attn_prefix_sum(st, sm.att);  // KV blocks per row: fixed for the iteration
     // ---- embed (model.cpp:171-183): h_0 = embedding row of the input token ----
     for (int b = cta; b < B; b += G) {
         const uint16_t* e = st.emb + (size_t)st.rows.tok[b] * dp;
@@ -818,10 +831,12 @@ __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(DevState st, Iter
             l2_prefetch_gemm(p.g[kIDown], layer);
         }
         __syncwarp();
-        attn_body<NJ>(st, sm.att, ring, layer, aseq);
+        attn_body<NJ>(st, sm.att, ring, layer, aseq, true);
         astamp(1);
         grid_sync(p, st, nbar, g0);
         aseq = sm.att.seq_next;
+        // the next layer's dynamic-tail counter (this one's twin) is idle now: rearm it
+        if (cta == 0 && tid == 0 && st.attn_queue) st.attn_queue[(layer + 1) & 1] = 0;
         if (warp == kProducerWarp && layer < L && p.kv_pf_blocks > 0)  // next layer's K/V -> L2
             l2_prefetch_kv(st, sm.att, layer + 1, p.kv_pf_blocks);
         __syncwarp();
@@ -934,6 +949,7 @@ __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(DevState st, Iter
         }
     }
     if (cta == 0 && tid == 0) {
+        if (st.attn_queue) st.attn_queue[1] = 0;  // layer 1 of the next launch (layer 2's is rearmed in layer 1)
         if (!(st.dbg & (2048 | 4096 | 32768))) *(volatile unsigned*)p.bar = 0u;  // arrivals of this launch are all in
         if (st.dbg & (4096 | 32768)) *(volatile unsigned*)(p.bar + 1025) = g0 + (unsigned)nbar;  // flag epochs continue
         st.rec_out[iter % st.rec_cap] = e_out;

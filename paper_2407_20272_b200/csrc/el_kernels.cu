@@ -722,8 +722,32 @@ __device__ __forceinline__ int atom_add_acq_rel(int* p, int v) {
 // standalone kernel and the persistent iteration kernel; `seq0` continues the
 // mbarrier ring's sequence (phase parity) across calls; on return a.seq_next
 // holds the next base.
+// attn_prefix_sum: the warp-parallel prefix sum of KV blocks per row into a.pref
+// (rows.pos is constant for a whole decode iteration, so the persistent kernel
+// computes it once per launch and passes persistent = true).
+__device__ __forceinline__ void attn_prefix_sum(const DevState& st, AttnSmem& a) {
+    const int lane = threadIdx.x & 31, B = st.rows.B, bc = st.dm.bc;
+    int base = 0;
+    for (int r0 = 0; r0 < B; r0 += 32) {
+        const int r = r0 + lane;
+        int v = (r < B) ? (st.rows.pos[r] + bc) / bc : 0;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const int t = __shfl_up_sync(0xffffffffu, v, off);
+            if (lane >= off) v += t;
+        }
+        if (r < B) a.pref[r + 1] = base + v;
+        base += __shfl_sync(0xffffffffu, v, 31);
+    }
+    if (lane == 0) a.pref[0] = 0;
+    __syncwarp();
+}
+
+// persistent: called from the persistent kernel -- a.pref is already valid and
+// no programmatic-dependent-launch deferral is needed (every input is ready).
 template <int NJ>
-__device__ void attn_body(const DevState& st, AttnSmem& a, uint8_t* stages, int layer, int seq0) {
+__device__ void attn_body(const DevState& st, AttnSmem& a, uint8_t* stages, int layer, int seq0,
+                          bool persistent = false) {
     const Dims& dm = st.dm;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int dp = dm.dp, nchunk = dp / 8;
@@ -740,29 +764,36 @@ __device__ void attn_body(const DevState& st, AttnSmem& a, uint8_t* stages, int 
         // streamed; q and the block holding `pos` (written by this layer's QKV
         // kernel) are requested after it (one pending stage).
         const int B = st.rows.B;
-        {  // warp-parallel prefix sum of blocks per row
-            int base = 0;
-            for (int r0 = 0; r0 < B; r0 += 32) {
-                const int r = r0 + lane;
-                int v = (r < B) ? (st.rows.pos[r] + dm.bc) / dm.bc : 0;
-#pragma unroll
-                for (int off = 1; off < 32; off <<= 1) {
-                    const int t = __shfl_up_sync(0xffffffffu, v, off);
-                    if (lane >= off) v += t;
-                }
-                if (r < B) a.pref[r + 1] = base + v;
-                base += __shfl_sync(0xffffffffu, v, 31);
-            }
-            if (lane == 0) a.pref[0] = 0;
-            __syncwarp();
-        }
-        // with fewer blocks than CTAs only the first T CTAs work (every range non-empty,
-        // so each CTA between a sequence's first and last owner contributes a partial)
-        const long long T = a.pref[B], G = min((long long)gridDim.x, T);
-        auto cta_of = [&](long long g) { return (int)(((g + 1) * G + T - 1) / T - 1); };
-        const bool active = (long long)blockIdx.x < G;
-        const long long g0 = active ? (long long)blockIdx.x * T / G : 0, g1 = active ? (long long)(blockIdx.x + 1) * T / G : 0;
-        bool waited = false;
+        if (!persistent) attn_prefix_sum(st, a);
+        // Work split: the flattened (row, block) space [0, T) is cut into a static
+        // head [0, Ts) -- CTA i streams [i*Ts/G, (i+1)*Ts/G), with fewer blocks than
+        // CTAs only the first Ts CTAs work -- and a dynamic tail [Ts, T) of items
+        // of `cb` blocks that CTAs grab from an atomic counter when their static
+        // range is done, so SMs that HBM serves faster take more of the tail.
+        // Partial slots per row: static segments in CTA order, then tail items in
+        // item order -- the combine order never depends on which CTA ran what.
+        const long long T = a.pref[B];
+        const int cb = max(1, st.attn_dyn_cb);
+        const long long Td = (st.attn_dyn_permille > 0 && st.attn_queue)
+                                 ? min(T, (T * st.attn_dyn_permille / 1000 + cb - 1) / cb * cb) : 0;
+        const long long Ts = T - Td;
+        const long long n_items = (Td + cb - 1) / cb;
+        const long long G = min((long long)gridDim.x, Ts);
+        auto cta_of = [&](long long g) { return (int)(((g + 1) * G + Ts - 1) / Ts - 1); };
+        // segment bookkeeping of row r: static segments and the first tail item touching it
+        auto row_static = [&](int r, int& first_cta) {
+            const long long r0 = a.pref[r], r1 = min((long long)a.pref[r + 1], Ts);
+            if (r0 >= r1) return 0;
+            first_cta = cta_of(r0);
+            return cta_of(r1 - 1) - first_cta + 1;
+        };
+        auto row_items = [&](int r, long long& i0) {
+            const long long r0 = max((long long)a.pref[r], Ts), r1 = a.pref[r + 1];
+            if (r0 >= r1) return 0LL;
+            i0 = (r0 - Ts) / cb;
+            return (r1 - 1 - Ts) / cb - i0 + 1;
+        };
+        bool waited = persistent;  // PDL secondary: defer q / the newest block until griddepcontrol.wait
         int dq = -1, ds = -1, did = 0;
         uint32_t dbytes = 0;
         auto flush = [&]() {
@@ -774,8 +805,8 @@ __device__ void attn_body(const DevState& st, AttnSmem& a, uint8_t* stages, int 
                 uint8_t* sb = stages + (size_t)ds * stage_bytes;
                 if (dq >= 0) bulk_load(sb + 2 * blk_bytes, st.q32 + (size_t)dq * dp, (uint32_t)dp * 4, &a.full[ds]);
                 if (dbytes) {
-                    bulk_load(sb, st.kpool + (size_t)did * dm.bc * dp, dbytes, &a.full[ds]);
-                    bulk_load(sb + blk_bytes, st.vpool + (size_t)did * dm.bc * dp, dbytes, &a.full[ds]);
+                    bulk_load_ef(sb, st.kpool + (size_t)did * dm.bc * dp, dbytes, &a.full[ds]);
+                    bulk_load_ef(sb + blk_bytes, st.vpool + (size_t)did * dm.bc * dp, dbytes, &a.full[ds]);
                 }
                 ds = -1;
                 dq = -1;
@@ -783,16 +814,11 @@ __device__ void attn_body(const DevState& st, AttnSmem& a, uint8_t* stages, int 
             }
         };
         int seq = seq0;
-        int b = 0;
-        while (b < B && a.pref[b + 1] <= g0) ++b;
-        for (long long g = g0; g < g1 && b < B;) {
-            // one segment: blocks [g, seg_end) of row b
+        // stream blocks [g, seg_end) of row b as one segment (partial slot `slot` of `nseg`)
+        auto emit = [&](int b, long long g, long long seg_end, int slot, int nseg) {
             const long long sb0 = a.pref[b], sb1 = a.pref[b + 1];
-            const long long seg_end = min(g1, sb1);
             const int nblk = (int)(sb1 - sb0);
             const int ctx = st.rows.pos[b] + 1;
-            const int cfirst = cta_of(sb0);
-            const int slot = (int)blockIdx.x - cfirst, nseg = cta_of(sb1 - 1) - cfirst + 1;
             const int* table = st.tables + ((size_t)st.rows.slot[b] * dm.L + (layer - 1)) * dm.bpl_max;
             for (long long gb = g; gb < seg_end; gb += 32) {
                 const int blk_base = (int)(gb - sb0);
@@ -812,6 +838,11 @@ __device__ void attn_body(const DevState& st, AttnSmem& a, uint8_t* stages, int 
                         const bool first = (gb + u) == g, newest = blk == nblk - 1;
                         a.desc[s] = AttnDesc{b, slot, rows, first, (gb + u) == seg_end - 1, nseg, {0, 0}};
                         uint8_t* sbuf = stages + (size_t)s * stage_bytes;
+                        if ((st.dbg & 32) && blockIdx.x < 4 && seq < 60) {  // issue time of each block
+                            unsigned long long t;
+                            asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+                            st.dbg_ts[8192 + 1024 + blockIdx.x * 128 + seq] = t;
+                        }
                         mbar_arrive_expect_tx(&a.full[s], 2 * bytes + (first ? (uint32_t)dp * 4 : 0u));
                         if (!waited && (first || newest) && ds >= 0) flush();  // one pending stage at most
                         if (!waited && (first || newest)) {
@@ -821,21 +852,67 @@ __device__ void attn_body(const DevState& st, AttnSmem& a, uint8_t* stages, int 
                                 did = id;
                                 dbytes = bytes;
                             } else {
-                                bulk_load(sbuf, st.kpool + (size_t)id * dm.bc * dp, bytes, &a.full[s]);
-                                bulk_load(sbuf + blk_bytes, st.vpool + (size_t)id * dm.bc * dp, bytes, &a.full[s]);
+                                bulk_load_ef(sbuf, st.kpool + (size_t)id * dm.bc * dp, bytes, &a.full[s]);
+                                bulk_load_ef(sbuf + blk_bytes, st.vpool + (size_t)id * dm.bc * dp, bytes, &a.full[s]);
                             }
                         } else {
                             if (first)
                                 bulk_load(sbuf + 2 * blk_bytes, st.q32 + (size_t)b * dp, (uint32_t)dp * 4, &a.full[s]);
-                            bulk_load(sbuf, st.kpool + (size_t)id * dm.bc * dp, bytes, &a.full[s]);
-                            bulk_load(sbuf + blk_bytes, st.vpool + (size_t)id * dm.bc * dp, bytes, &a.full[s]);
+                            bulk_load_ef(sbuf, st.kpool + (size_t)id * dm.bc * dp, bytes, &a.full[s]);
+                            bulk_load_ef(sbuf + blk_bytes, st.vpool + (size_t)id * dm.bc * dp, bytes, &a.full[s]);
                         }
                     }
                 }
                 __syncwarp();
             }
-            g = seg_end;
-            ++b;
+        };
+        // ---- static head ----
+        if ((long long)blockIdx.x < G) {
+            const long long g0 = (long long)blockIdx.x * Ts / G, g1 = (long long)(blockIdx.x + 1) * Ts / G;
+            int b = 0;
+            while (b < B && a.pref[b + 1] <= g0) ++b;
+            for (long long g = g0; g < g1 && b < B;) {
+                const long long seg_end = min(g1, (long long)a.pref[b + 1]);
+                int fc = 0;
+                const int ns = row_static(b, fc);
+                long long i0 = 0;
+                const int nseg = ns + (int)row_items(b, i0);
+                emit(b, g, seg_end, (int)blockIdx.x - fc, nseg);
+                g = seg_end;
+                ++b;
+            }
+        }
+        // ---- dynamic tail: grab items until the counter runs past the end ----
+        if (n_items > 0) {
+            int it = 0;
+            if (lane == 0) it = atomicAdd(st.attn_queue + (layer & 1), 1);
+            it = __shfl_sync(0xffffffffu, it, 0);
+            while (it < n_items) {
+                int nxt = 0;
+                if (lane == 0) nxt = atomicAdd(st.attn_queue + (layer & 1), 1);  // latency overlaps this item
+                const long long gs = Ts + (long long)it * cb, ge = min(T, gs + cb);
+                int b = 0;
+                {  // row holding block gs (binary search on the prefix sums)
+                    int lo = 0, hi = B - 1;
+                    while (lo < hi) {
+                        const int mid = (lo + hi + 1) >> 1;
+                        if (a.pref[mid] <= gs) lo = mid;
+                        else hi = mid - 1;
+                    }
+                    b = lo;
+                }
+                for (long long g = gs; g < ge && b < B; ++b) {
+                    const long long seg_end = min(ge, (long long)a.pref[b + 1]);
+                    if (seg_end <= g) continue;
+                    int fc = 0;
+                    const int ns = row_static(b, fc);
+                    long long i0 = 0;
+                    const int nseg = ns + (int)row_items(b, i0);
+                    emit(b, g, seg_end, ns + (int)(it - i0), nseg);
+                    g = seg_end;
+                }
+                it = __shfl_sync(0xffffffffu, nxt, 0);
+            }
         }
         if (lane == 0) flush();  // short run: anything still deferred
         if (lane == 0) {
@@ -847,12 +924,28 @@ __device__ void attn_body(const DevState& st, AttnSmem& a, uint8_t* stages, int 
     } else {
         // ---------------- consumer warps ----------------
         float q[NJ][8], o[NJ][8];
+#pragma unroll
+        for (int t = 0; t < NJ; ++t)
+#pragma unroll
+            for (int i = 0; i < 8; ++i) q[t][i] = o[t][i] = 0.f;
         float m = -INFINITY, l = 0.f;
         const int r0 = warp, r1 = warp + kAttnWarps;
+        // Persistent kernel: the consumer path is cold in the instruction cache at
+        // the start of every pass (the other phases' code evicted it), so the
+        // first real block used to take ~4x a steady-state one.  Run the block
+        // math once on whatever the first stage holds while its data is still in
+        // flight (results are discarded: the first real descriptor of a pass is
+        // always a segment start, which resets q, o, m, l).
+        bool warm = persistent;
         for (int seq = seq0;; ++seq) {
             const int s = seq % S;
-            mbar_wait(&a.full[s], (seq / S) & 1);
-            const AttnDesc d = a.desc[s];
+            AttnDesc d;
+            if (warm) {
+                d = AttnDesc{0, 0, dm.bc, 0, 0, 1, {0, 0}};
+            } else {
+                mbar_wait(&a.full[s], (seq / S) & 1);
+                d = a.desc[s];
+            }
             if (d.b < 0) {  // terminal descriptor: release its slot too (the ring persists across passes)
                 if (tid == 0) a.seq_next = seq + 1;
                 __syncwarp();
@@ -923,6 +1016,16 @@ __device__ void attn_body(const DevState& st, AttnSmem& a, uint8_t* stages, int 
                         if (vc) axpy8(pc, sv[rc * nchunk + j], o[t]);
                     }
                 }
+            }
+            if ((st.dbg & 32) && tid == 0 && blockIdx.x < 4 && seq < 60) {  // block processed (before release)
+                unsigned long long t;
+                asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+                st.dbg_ts[8192 + 2048 + blockIdx.x * 128 + seq] = t;
+            }
+            if (warm) {  // dry run done: now the real first block of this stage
+                warm = false;
+                --seq;
+                continue;
             }
             if (!d.last || (st.dbg & 4)) {
                 __syncwarp();

@@ -69,8 +69,10 @@ struct DevState {
     int attn_cb;      // blocks per chunk
     int attn_stages;
     int attn_grid;    // persistent CTAs
-    int* attn_queue;  // work-item counter (reset by the last CTA)
+    int* attn_queue;  // [2] dynamic-tail item counters (by layer parity; persistent kernel only)
     int* attn_done;
+    int attn_dyn_permille;  // share of the KV blocks handed out dynamically (0 = static split only)
+    int attn_dyn_cb;        // blocks per dynamic item
     int dbg;          // experiment knob (0 = normal)
     unsigned long long* dbg_ts;
     float attn_scale; // 1/sqrt(d)

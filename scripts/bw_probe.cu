@@ -4,7 +4,8 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 __device__ __forceinline__ uint32_t su(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-__global__ void bulk_stream(const uint8_t* src, size_t chunk, int n_chunks, int S, unsigned long long* sink) {
+__global__ void bulk_stream(const uint8_t* src, size_t chunk, int n_chunks, int S, unsigned long long* sink,
+                            int scatter = 0, int contiguous = 0) {
   extern __shared__ __align__(128) uint8_t sm[];
   __shared__ uint64_t full[16];
   const int tid = threadIdx.x;
@@ -21,7 +22,9 @@ __global__ void bulk_stream(const uint8_t* src, size_t chunk, int n_chunks, int 
         acc += sm[(size_t)s * chunk];
       }
       if (i < mine) {
-        const int s = i % S; const size_t c = blockIdx.x + (size_t)i * gridDim.x;
+        const int s = i % S;
+        size_t c = contiguous ? (size_t)blockIdx.x * mine + i : blockIdx.x + (size_t)i * gridDim.x;
+        if (scatter) c = (c * 2654435761ull) % (size_t)n_chunks;  // scattered blocks (like a paged KV pool)
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(su(&full[s])), "r"((uint32_t)chunk) : "memory");
         asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" :: "r"(su(sm + (size_t)s * chunk)), "l"(src + c * chunk), "r"((uint32_t)chunk), "r"(su(&full[s])) : "memory");
       }
@@ -56,6 +59,18 @@ int main() {
     cudaEventRecord(b); cudaEventSynchronize(b);
     float ms; cudaEventElapsedTime(&ms, a, b);
     printf("bulk chunk=%6zu S=%d ctas/sm=%d : %.0f GB/s\n", chunk, S, per, 5.0 * bytes / (ms * 1e-3) / 1e9);
+  }
+  // short bursts over a C2-attention-sized working set (~108 MB): fill/tail effects, scattered blocks
+  for (int scat : {0, 1}) for (int contig : {0, 1}) for (int S : {3, 4}) {
+    const size_t chunk = 24576; const int n_chunks = (int)(108ull * 1000 * 1000 / chunk);
+    cudaFuncSetAttribute(bulk_stream, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024);
+    bulk_stream<<<sms, 32, chunk * S>>>(buf, chunk, n_chunks, S, sink, scat, contig);
+    cudaEventRecord(a);
+    for (int r = 0; r < 20; ++r) bulk_stream<<<sms, 32, chunk * S>>>(buf + (r % 4) * (256ull << 20), chunk, n_chunks, S, sink, scat, contig);
+    cudaEventRecord(b); cudaEventSynchronize(b);
+    float ms; cudaEventElapsedTime(&ms, a, b);
+    printf("short 108MB scatter=%d contiguous-per-cta=%d S=%d : %.1f us/launch, %.0f GB/s\n", scat, contig, S, ms * 1e3 / 20,
+           20.0 * n_chunks * chunk / (ms * 1e-3) / 1e9);
   }
   for (int tpb : {256, 512, 1024}) for (int bps : {1, 2, 4}) {
     const int grid = sms * bps;

@@ -163,11 +163,21 @@ int main() {
                first[sms / 2], all[sms / 2], all.back(), (t1 - t0) / 1e3, bytes / ((t1 - t0) / 1e3) / 1e3);
     }
     cudaFuncSetAttribute(probe2, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    for (int spin : {0, 1}) {
+    cudaFuncSetAttribute(probe2, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    for (int spin : {0, 1, 2, 3}) {
         for (int rep = 0; rep < 3; ++rep) {
             cudaMemset(buf + ((size_t)1 << 30), rep, (size_t)1 << 30);
             probe<<<sms, 128, 200 * 1024>>>(buf, 0, 0, 12, 8192, out);  // act chunk warm in L2
-            probe2<<<sms, 288, 200 * 1024>>>(buf, buf + (256 << 20) + ((size_t)rep << 22), 12, spin, out);
+            const uint8_t* a0 = buf;
+            const uint8_t* w0 = buf + (256 << 20) + ((size_t)rep << 22);
+            int nk = 12, sp = spin & 1;
+            unsigned long long* o = out;
+            if (spin >= 2) {  // cooperative launch, 220 KB smem, like the persistent kernel
+                void* args[] = {(void*)&a0, (void*)&w0, (void*)&nk, (void*)&sp, (void*)&o};
+                cudaLaunchCooperativeKernel((void*)probe2, sms, 288, args, 220 * 1024, 0);
+            } else {
+                probe2<<<sms, 288, 200 * 1024>>>(a0, w0, nk, sp, o);
+            }
             cudaDeviceSynchronize();
         }
         cudaMemcpy(h.data(), out, sms * 4 * 8, cudaMemcpyDeviceToHost);
@@ -178,7 +188,7 @@ int main() {
         }
         std::sort(first.begin(), first.end());
         std::sort(all.begin(), all.end());
-        printf("batch-M pattern 12x(8KB L2 + 2KB HBM) spin=%d: first p50 %.2f | all p50 %.2f max %.2f us\n", spin,
+        printf("batch-M pattern 12x(8KB L2 + 2KB HBM) spin=%d coop=%d: first p50 %.2f | all p50 %.2f max %.2f us\n", spin & 1, spin >> 1,
                first[sms / 2], all[sms / 2], all.back());
     }
     printf("%s\n", cudaGetErrorString(cudaGetLastError()));
