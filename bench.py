@@ -190,7 +190,7 @@ def run_ours(args, rank, world, local_rank, dist):
         cfg = X.EngineConfig(model=X.ModelConfig(L, d, V, 0), technique=X.ExitTechnique(tech),
                              schedule=X.ThresholdSchedule(c["lam"], c["gamma"], 0.0), max_batch=B,
                              pool_blocks=B * L * (-(-cap // 16)), eos_token=-1)
-        return X.Engine(cfg, graph=not args.eager, mega=not args.no_mega)
+        return X.Engine(cfg, graph=not args.eager, mega=False if args.no_mega else (True if args.mega else None))
 
     def barrier():
         if dist is not None:
@@ -264,7 +264,7 @@ def run_ours(args, rank, world, local_rank, dist):
             with open(tp) as f:
                 return json.load(f).get("dram_bytes_per_launch")
         return None
-    mega = not args.no_mega
+    mega = bool(plan.get("mega"))
     out = {
         "metric": METRIC, "value": round(value, 1), "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4), "higher_is_better": True,
@@ -389,8 +389,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--eager", action="store_true", help="host-driven layer loop (for ncu, which cannot "
                     "profile kernels inside conditional graphs)")
-    ap.add_argument("--no-mega", action="store_true", help="per-phase kernels instead of the persistent "
-                    "decode-iteration kernel (A/B comparison)")
+    ap.add_argument("--no-mega", action="store_true", help="force per-phase kernels (A/B comparison)")
+    ap.add_argument("--mega", action="store_true", help="force the persistent decode-iteration kernel (A/B "
+                    "comparison; default: the engine picks per batch size)")
     args = ap.parse_args()
     if args.warmup < 3:
         raise SystemExit("warmup must be >= 3")

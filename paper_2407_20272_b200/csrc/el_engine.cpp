@@ -147,7 +147,14 @@ struct el_engine {
     bool body_head = false;
     bool fuse_exit = true;
     bool fuse_exit_all = false;
-    bool use_mega = true;  // persistent decode-iteration kernel (el_iter.cuh)
+    // decode-iteration strategy: 0 per-phase kernels (graph / eager), 1 persistent kernel
+    // (el_iter.cuh), 2 auto: persistent at batch >= 128 (measured faster there: weight
+    // streaming and the exit check amortise its grid barriers), per-phase kernels below
+    int use_mega = 2;
+    bool mega_for(int B) const {
+        if (use_mega != 2) return use_mega == 1;
+        return B > 64 && cfg.technique != EL_TECH_SOFTMAX;
+    }
     int dbg = 0;
     int rec_cap = 4096;
 
@@ -640,7 +647,7 @@ struct el_engine {
         return cfg.technique == EL_TECH_NEVER || cfg.technique == EL_TECH_ALWAYS_AT || cfg.technique == EL_TECH_FIXED;
     }
     int launches_per_iteration(int e) const {
-        if (use_mega) return 1;
+        if (mega_for(in_session ? sess_B : dm.Bmax)) return 1;
         const bool fused = fuse_exit_active();
         const int per_layer = (fused ? 5 : 6) + (cfg.technique == EL_TECH_SOFTMAX ? 1 : 0) + (body_head ? 1 : 0);
         return 1 + e * per_layer + (cfg.technique != EL_TECH_NEVER ? 1 : 0) +
@@ -703,7 +710,7 @@ struct el_engine {
     }
 
     void iteration(int B) {
-        if (use_mega) {
+        if (mega_for(B)) {
             launch_mega(B);
         } else if (use_graph) {
             Graph& G = graph_for(B);
@@ -1139,7 +1146,10 @@ int el_engine_destroy(el_engine* e) {
 int el_engine_set_option(el_engine* e, const char* key, int64_t v) {
     API_BEGIN
     if (!std::strcmp(key, "graph")) e->use_graph = v != 0;
-    else if (!std::strcmp(key, "mega")) e->use_mega = v != 0;
+    else if (!std::strcmp(key, "mega")) {
+        if (v < 0 || v > 2) fail(EL_INVALID_ARGUMENT, "mega must be 0 (off), 1 (on) or 2 (auto)");
+        e->use_mega = (int)v;
+    }
     else if (!std::strcmp(key, "attn_dyn_permille")) {
         if (v < 0 || v > 1000) fail(EL_INVALID_ARGUMENT, "attn_dyn_permille must be in [0, 1000]");
         e->opt_attn_dyn_permille = (int)v;
@@ -1457,7 +1467,8 @@ int el_plan_info(el_engine* e, int64_t* out, int cap) {
                          M.g[el::kIQkv].mode, M.g[el::kIWo].mode, M.g[el::kIUp].mode,
                          M.g[el::kIQkv].splits, M.g[el::kIWo].splits, M.g[el::kIUp].splits, M.g[el::kIDown].splits,
                          M.g[el::kIFill].splits, M.g[el::kIQkv].nt, M.g[el::kIWo].nt, M.g[el::kIUp].nt,
-                         M.stages, M.stages2, e->mega_att_stages, e->use_mega ? 1 : 0};
+                         M.stages, M.stages2, e->mega_att_stages,
+                         e->mega_for(e->in_session ? e->sess_B : e->dm.Bmax) ? 1 : 0};
     const int n = (int)(sizeof v / sizeof v[0]);
     for (int i = 0; i < std::min(n, cap); ++i) out[i] = v[i];
     return n;

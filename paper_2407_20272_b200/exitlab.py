@@ -341,11 +341,12 @@ class Engine:
     """exitlab::Engine on one B200 (engine.hpp:131-147). Weights are seeded from
     config.model (ModelWeights::seeded, model.cpp:37-59) and stored as bf16."""
 
-    def __init__(self, config: EngineConfig, graph: bool = True, mega: bool = True):
-        """graph/mega select how a decode iteration is launched: mega (default) =
-        one persistent kernel per iteration (layer loop on the device); otherwise
+    def __init__(self, config: EngineConfig, graph: bool = True, mega=None):
+        """graph/mega select how a decode iteration is launched: mega=True = one
+        persistent kernel per iteration (layer loop on the device); mega=False =
         per-phase kernels in a CUDA graph with a device-side WHILE (graph) or a
-        host-driven layer loop (eager)."""
+        host-driven layer loop (eager); mega=None (default) picks per batch size
+        (persistent at batch >= 128, where it measured faster)."""
         self.config = config
         self._c = to_c_config(config)
         h = C.c_void_p()
@@ -354,7 +355,7 @@ class Engine:
         self.L, self.d, self.V = config.model.n_layers, config.model.d_model, config.model.vocab_size
         self.B = 0
         self.set_option("graph", int(graph))
-        self.set_option("mega", int(mega))
+        self.set_option("mega", 2 if mega is None else int(bool(mega)))
 
     def close(self):
         if getattr(self, "_h", None):

@@ -111,13 +111,13 @@ def test_block_tables_bit_exact(port):
     e.close()
 
 
-@pytest.mark.parametrize("graph", [True, False])
-def test_exit_masks_bit_exact_at_fixed_confidences(port, graph):
+@pytest.mark.parametrize("graph,mega", [(True, False), (False, False), (True, True)])
+def test_exit_masks_bit_exact_at_fixed_confidences(port, graph, mega):
     """ExitStatusVector on the device == reference semantics at injected
     confidences: OR-latch, first accept, output layer = max accept, strict '>'."""
     L, B = 6, 12
     g, o = cfg_pair(L, 128, 512, 3, "fixed", lam=0.6, gamma=0.97, B=B)
-    e = X.Engine(g, graph=graph)
+    e = X.Engine(g, graph=graph, mega=mega)
     e.session_begin(np.arange(B) + 5, 8, 8 + 40, 2)
     rng = np.random.default_rng(0)
     lam = np.array([OB.port().threshold_at(0.6, 0.97, 0.0, l) for l in range(1, L + 1)])
@@ -164,12 +164,14 @@ def _teacher_forced(e, s, n_iters, lm, V, d, check_conf=None):
     return stats
 
 
+@pytest.mark.parametrize("mega", [False, True])
 @pytest.mark.parametrize("tech,lam,gamma", [("state", 0.972, 0.998), ("classifier", 0.59, 1.0),
                                             ("softmax", 1e-4, 1.0), ("always_at", 0.5, 1.0), ("never", 0.5, 1.0)])
-def test_decode_parity_small_dims(port, tech, lam, gamma):
+def test_decode_parity_small_dims(port, tech, lam, gamma, mega):
+    """Both decode strategies (per-phase kernels; persistent kernel) against the oracle."""
     L, d, V, B = 4, 128, 512, 8
     g, o = cfg_pair(L, d, V, 5, tech, lam=lam, gamma=gamma, exit_layer=2, B=B)
-    e = X.Engine(g)
+    e = X.Engine(g, mega=mega)
     first = np.array([3, 9, 27, 81, 243, 100, 7, 500])
     e.session_begin(first, 30, 60, 1234)
     m = port.model(L, d, V, 5, True)
@@ -257,12 +259,13 @@ def test_engine_run_with_real_prefill_matches_oracle(port):
 
 
 @pytest.mark.slow
-def test_bench_config_c2_parity(port):
+@pytest.mark.parametrize("mega", [False, True])
+def test_bench_config_c2_parity(port, mega):
     """BASELINE configs[1] dims (L=12, d=768, V=32128), B=64, state exit: the
-    bench workload itself, two teacher-forced iterations."""
+    bench workload itself, two teacher-forced iterations, both decode strategies."""
     L, d, V, B = 12, 768, 32128, 64
     g, o = cfg_pair(L, d, V, 0, "state", lam=0.972, gamma=0.998, B=B)
-    e = X.Engine(g)
+    e = X.Engine(g, mega=mega)
     wl = port.gen_workload(n_requests=B, prompt_len_min=512, prompt_len_max=512, output_len_min=128,
                            output_len_max=128, seed=1, vocab_size=V)
     first = wl.prompt[wl.prompt_off[1:] - 1]
@@ -274,3 +277,27 @@ def test_bench_config_c2_parity(port):
         assert x["h"] <= HID_TOL and x["conf"] <= CONF_TOL
         assert np.all(x["agree"] | (x["gap"] < TIE_GAP))
     e.close()
+
+
+@pytest.mark.parametrize("B,tech", [(16, "classifier"), (136, "state")])
+def test_persistent_kernel_deterministic_and_matches_per_phase(B, tech):
+    """The persistent kernel is run-to-run bitwise deterministic (fixed split-K
+    and attention-partial reduction orders, no atomics on values) and agrees
+    with the per-phase kernels within the bf16 tolerance; B = 136 exercises the
+    split-K + reduce GEMM path (batch > 128), B = 16 the batch-M path."""
+    L, d, V = 5, 256, 1024
+    outs = []
+    for mega in (True, True, False):
+        g, _ = cfg_pair(L, d, V, 8, tech, lam=0.97 if tech == "state" else 0.5, gamma=0.995, B=B)
+        e = X.Engine(g, mega=mega)
+        e.session_begin(np.arange(B) * 3 + 1, 40, 80, 77)
+        rs = [e.decode_iteration() for _ in range(4)]
+        outs.append((rs, e.hidden(rs[-1]["output_layer"] & 1), e.kv(B - 1, L, 43)))
+        e.close()
+    (ra, ha, ka), (rb, hb, kb), (rc, hc, kc) = outs
+    for x, y in zip(ra, rb):
+        assert x["output_layer"] == y["output_layer"]
+        assert np.array_equal(x["tokens"], y["tokens"]) and np.array_equal(x["conf"], y["conf"])
+    assert np.array_equal(ha, hb) and np.array_equal(ka[0], kb[0]) and np.array_equal(ka[1], kb[1])
+    assert relerr(ha, hc) <= HID_TOL and relerr(ka[0], kc[0]) <= HID_TOL
+    assert np.mean([np.mean(x["tokens"] == y["tokens"]) for x, y in zip(ra, rc)]) >= 0.9
