@@ -64,6 +64,10 @@ typedef struct {
     int capture_kv;
     int round_bf16;            /* weights are always bf16 on the device; kept for layout parity */
     int64_t synthetic_kv_seed; /* <0: real prefill; >=0: prompts' KV prefix is seeded (bench workload) */
+    /* T5 mode (north_star (1), CALM-T5; NOT in the reference): > 0 adds a
+     * cross-attention sub-layer over this many synthetic encoder states per sequence
+     * (static cross K/V written once at admission; the skipped-layer fill is unchanged). */
+    int encoder_len;
 } el_engine_config;
 
 typedef struct el_engine el_engine;

@@ -231,11 +231,22 @@ class _Lib:
         return self.fn("last_error")().decode()
 
     # ---- model ----
-    def model(self, n_layers, d_model, vocab, seed, round_bf16=False):
-        h = self.fn("model_seeded")(n_layers, d_model, vocab, C.c_uint64(seed), int(round_bf16))
+    def model(self, n_layers, d_model, vocab, seed, round_bf16=False, encoder_len=0):
+        """encoder_len > 0: the T5-mode extension (cross-attention over synthetic
+        encoder states) -- the C restatement only; the compiled reference has no
+        encoder, so parity of that mode is not pinned by it."""
+        if encoder_len:
+            if self.prefix != "eo_":
+                raise ValueError("the reference has no encoder / cross-attention (SPEC.md:13, 184)")
+            h = self.fn("model_seeded_t5")(n_layers, d_model, vocab, C.c_uint64(seed), int(round_bf16),
+                                           int(encoder_len))
+        else:
+            h = self.fn("model_seeded")(n_layers, d_model, vocab, C.c_uint64(seed), int(round_bf16))
         if not h:
             raise ValueError(self.err())
-        return Model(self, h, n_layers, d_model, vocab, seed)
+        m = Model(self, h, n_layers, d_model, vocab, seed)
+        m.encoder_len = encoder_len
+        return m
 
     def gen_workload(self, n_requests=8, mean_interarrival=0.0, prompt_len_min=1, prompt_len_max=8,
                      output_len_min=1, output_len_max=16, seed=0, vocab_size=256, eos_token=0) -> Workload:
@@ -322,13 +333,18 @@ class Model:
         except Exception:
             pass
 
+    def encoder_state(self, seq_id, t):
+        out = np.zeros(self.d)
+        self.lib.fn("encoder_state")(self.h, seq_id, t, _p(out, C.c_double))
+        return out
+
     def tensor(self, which, layer=0):
         names = {"embedding": 0, "lm_head": 1, "probe_w": 2, "probe_b": 3, "w_q": 4, "w_k": 5, "w_v": 6,
-                 "w_o": 7, "w_up": 8, "w_down": 9}
+                 "w_o": 7, "w_up": 8, "w_down": 9, "w_qc": 10, "w_kc": 11, "w_vc": 12, "w_oc": 13}
         w = names[which] if isinstance(which, str) else which
         d, V = self.d, self.V
         shape = {0: (V, d), 1: (V, d), 2: (d,), 3: (1,), 4: (d, d), 5: (d, d), 6: (d, d), 7: (d, d),
-                 8: (4 * d, d), 9: (d, 4 * d)}[w]
+                 8: (4 * d, d), 9: (d, 4 * d), 10: (d, d), 11: (d, d), 12: (d, d), 13: (d, d)}[w]
         out = np.zeros(int(np.prod(shape)))
         rc = self.lib.fn("model_tensor")(self.h, w, layer, _p(out, C.c_double), out.size)
         if rc:
@@ -424,6 +440,10 @@ class Port(_Lib):
         L = self.lib
         L.eo_model_seeded.restype = C.c_void_p
         L.eo_model_seeded.argtypes = [C.c_int, C.c_int, C.c_int, C.c_uint64, C.c_int]
+        L.eo_model_seeded_t5.restype = C.c_void_p
+        L.eo_model_seeded_t5.argtypes = [C.c_int, C.c_int, C.c_int, C.c_uint64, C.c_int, C.c_int]
+        L.eo_encoder_state.restype = None
+        L.eo_encoder_state.argtypes = [C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_double)]
         L.eo_engine_run.argtypes = [C.c_void_p, C.POINTER(EngineConfig), C.c_int, C.POINTER(C.c_double),
                                     C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.POINTER(C.c_int32),
                                     C.POINTER(C.c_double), C.c_int, C.POINTER(C.c_void_p)]

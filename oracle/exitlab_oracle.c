@@ -78,6 +78,13 @@ struct eo_model {
     double* pw;    /* d */
     double pb;
     double** w;    /* per layer: q,k,v,o (d x d), up (4d x d), down (d x 4d) */
+    /* T5 mode (north_star (1); NOT in the reference): cross-attention
+       over synthetic encoder states, enc_len > 0.  Parity of this mode is pinned only
+       by this restatement (the compiled reference has no encoder/cross-attention). */
+    int enc_len;
+    int round_bf16;
+    uint64_t enc_seed;
+    double** wc;   /* per layer: q_c, k_c, v_c, o_c (d x d) */
 };
 static const int kLayerTensors = 6;
 
@@ -91,9 +98,35 @@ static void tensor_shape(const eo_model* m, int k, int* r, int* c) {
 static void round_all(double* p, size_t n) { for (size_t i = 0; i < n; ++i) p[i] = eo_round_bf16(p[i]); }
 
 eo_model* eo_model_seeded(int L, int d, int V, uint64_t seed, int round_bf16) {
+    return eo_model_seeded_t5(L, d, V, seed, round_bf16, 0);
+}
+
+/* T5 mode extension (no reference counterpart): cross weights seeded with tags
+   after the reference's last one (4 + 6L + 4i + k), encoder states per
+   (sequence id, position) from their own stream; bf16-rounded like the weights. */
+static const int kCrossTensors = 4;
+uint64_t eo_encoder_seed(uint64_t model_seed) { return eo_splitmix64_at(model_seed, 0x454E43u); }
+void eo_encoder_state(const eo_model* m, int seq_id, int t, double* out) {
+    eo_seeded_vector(m->d, eo_splitmix64_at(m->enc_seed, ((uint64_t)seq_id << 20) | (uint64_t)t), out);
+    if (m->round_bf16) round_all(out, (size_t)m->d);
+}
+
+eo_model* eo_model_seeded_t5(int L, int d, int V, uint64_t seed, int round_bf16, int enc_len) {
     if (L < 2 || d < 2 || V < 2) { set_err("ModelConfig: bad dims"); return NULL; }
+    if (enc_len < 0) { set_err("ModelConfig: encoder_len must be >= 0"); return NULL; }
     eo_model* m = (eo_model*)calloc(1, sizeof(eo_model));
     m->L = L; m->d = d; m->V = V; m->seed = seed;
+    m->enc_len = enc_len; m->round_bf16 = round_bf16; m->enc_seed = eo_encoder_seed(seed);
+    if (enc_len > 0) {
+        m->wc = (double**)calloc((size_t)L * kCrossTensors, sizeof(double*));
+        for (int i = 0; i < L; ++i)
+            for (int k = 0; k < kCrossTensors; ++k) {
+                double* t = (double*)malloc(sizeof(double) * (size_t)d * d);
+                eo_seeded_matrix(d, d, eo_splitmix64_at(seed, 4 + (uint64_t)L * 6 + (uint64_t)i * 4 + k), t);
+                if (round_bf16) round_all(t, (size_t)d * d);
+                m->wc[i * kCrossTensors + k] = t;
+            }
+    }
     m->emb = (double*)malloc(sizeof(double) * (size_t)V * d);
     m->lm = (double*)malloc(sizeof(double) * (size_t)V * d);
     m->pw = (double*)malloc(sizeof(double) * (size_t)d);
@@ -128,6 +161,10 @@ eo_model* eo_model_seeded(int L, int d, int V, uint64_t seed, int round_bf16) {
 
 void eo_model_free(eo_model* m) {
     if (!m) return;
+    if (m->wc) {
+        for (int i = 0; i < m->L * kCrossTensors; ++i) free(m->wc[i]);
+        free(m->wc);
+    }
     for (int i = 0; i < m->L * kLayerTensors; ++i) free(m->w[i]);
     free(m->w); free(m->emb); free(m->lm); free(m->pw); free(m);
 }
@@ -138,6 +175,10 @@ int eo_model_tensor(const eo_model* m, int which, int layer, double* out, int64_
     else if (which == 1) { src = m->lm; n = (int64_t)m->V * m->d; }
     else if (which == 2) { src = m->pw; n = m->d; }
     else if (which == 3) { src = &m->pb; n = 1; }
+    else if (which >= 10 && which < 10 + kCrossTensors) {  /* T5 mode: q_c, k_c, v_c, o_c */
+        if (!m->wc || layer < 1 || layer > m->L) { set_err("bad tensor"); return EO_INVALID_ARGUMENT; }
+        src = m->wc[(layer - 1) * kCrossTensors + (which - 10)]; n = (int64_t)m->d * m->d;
+    }
     else {
         if (layer < 1 || layer > m->L || which - 4 >= kLayerTensors) { set_err("bad tensor"); return EO_INVALID_ARGUMENT; }
         int r, c;
@@ -398,6 +439,40 @@ static int layer_forward(const eo_model* m, int layer, int B, const int* ids, co
     for (int b = 0; b < B; ++b) matvec(wo, d, d, w->att + (size_t)b * d, w->proj + (size_t)b * d);
     for (int b = 0; b < B; ++b)
         for (int i = 0; i < d; ++i) w->mid[(size_t)b * d + i] = h[(size_t)b * d + i] + w->proj[(size_t)b * d + i];
+    if (m->enc_len > 0) {
+        /* T5 mode: mid += W_oc . softmax(q_c K_c^T / sqrt(d)) V_c, q_c = W_qc . mid,
+           K_c[t] = W_kc . E[t], V_c[t] = W_vc . E[t] over the sequence's encoder states */
+        const int T = m->enc_len;
+        const double *wqc = m->wc[(layer - 1) * kCrossTensors + 0], *wkc = m->wc[(layer - 1) * kCrossTensors + 1];
+        const double *wvc = m->wc[(layer - 1) * kCrossTensors + 2], *woc = m->wc[(layer - 1) * kCrossTensors + 3];
+        double* e = (double*)malloc(sizeof(double) * (size_t)d);
+        double* kc = (double*)malloc(sizeof(double) * (size_t)T * d);
+        double* vc = (double*)malloc(sizeof(double) * (size_t)T * d);
+        scratch_scores(w, T);
+        for (int b = 0; b < B; ++b) {
+            for (int t = 0; t < T; ++t) {
+                eo_encoder_state(m, ids[b], t, e);
+                matvec(wkc, d, d, e, kc + (size_t)t * d);
+                matvec(wvc, d, d, e, vc + (size_t)t * d);
+            }
+            double* q = w->q + (size_t)b * d;
+            matvec(wqc, d, d, w->mid + (size_t)b * d, q);
+            for (int t = 0; t < T; ++t) {
+                double acc = 0.0;
+                for (int i = 0; i < d; ++i) acc += kc[(size_t)t * d + i] * q[i];
+                w->scores[t] = acc * scale;
+            }
+            int rc = softmax(w->scores, T, w->probs);
+            if (rc) { free(e); free(kc); free(vc); return rc; }
+            double* a = w->att + (size_t)b * d;
+            for (int i = 0; i < d; ++i) a[i] = 0.0;
+            for (int t = 0; t < T; ++t)
+                for (int i = 0; i < d; ++i) a[i] += w->probs[t] * vc[(size_t)t * d + i];
+            matvec(woc, d, d, a, w->proj + (size_t)b * d);
+            for (int i = 0; i < d; ++i) w->mid[(size_t)b * d + i] += w->proj[(size_t)b * d + i];
+        }
+        free(e); free(kc); free(vc);
+    }
     for (int b = 0; b < B; ++b) {
         double* u = w->up + (size_t)b * 4 * d;
         matvec(wup, 4 * d, d, w->mid + (size_t)b * d, u);

@@ -58,6 +58,13 @@ uint16_t eo_bf16_bits(double x);
 /* ---- model ---- */
 typedef struct eo_model eo_model;
 eo_model* eo_model_seeded(int n_layers, int d_model, int vocab, uint64_t seed, int round_bf16);
+/* T5-mode extension (north_star (1); no counterpart in the reference -- parity of this
+   mode is pinned only by this restatement): a cross-attention sub-layer over
+   `encoder_len` synthetic encoder states per sequence after the self-attention
+   residual.  encoder_len = 0 is exactly eo_model_seeded. */
+eo_model* eo_model_seeded_t5(int n_layers, int d_model, int vocab, uint64_t seed, int round_bf16, int encoder_len);
+uint64_t eo_encoder_seed(uint64_t model_seed);
+void eo_encoder_state(const eo_model* m, int seq_id, int t, double* out);
 void eo_model_free(eo_model* m);
 /* which: 0 embedding, 1 lm_head, 2 probe_w, 3 probe_b, 4+k: layer tensor k in
  * {q,k,v,o,up,down}; layer is 1-based (ignored for globals). Copies into out. */

@@ -152,6 +152,10 @@ struct el_engine {
     // streaming and the exit check amortise its grid barriers), per-phase kernels below
     int use_mega = 2;
     bool mega_for(int B) const {
+        if (cfg.encoder_len > 0) {  // T5 mode: the cross-attention sub-layer lives in the persistent kernel
+            if (use_mega == 0) fail(EL_INVALID_ARGUMENT, "T5 mode (encoder_len > 0) runs on the persistent kernel");
+            return true;
+        }
         if (use_mega != 2) return use_mega == 1;
         return B > 64 && cfg.technique != EL_TECH_SOFTMAX;
     }
@@ -160,6 +164,11 @@ struct el_engine {
 
     // weights
     DevBuf<uint16_t> wqkv, wo, wup, wdown, emb, lm;
+    // T5 mode (encoder_len > 0): cross weights, static encoder K/V pool + tables, encoder-state staging
+    DevBuf<uint16_t> wqc, wkvc, woc, ckpool, cvpool, enc_act;
+    DevBuf<int> ctables, xslot, xid;
+    int enc_blocks = 0;
+    uint64_t enc_seed = 0;
     DevBuf<float> probe_w;
     float probe_b = 0.f;
     // kv pool + device allocator
@@ -244,6 +253,8 @@ struct el_engine {
         if (c.technique == EL_TECH_ALWAYS_AT && (c.exit_layer < 1 || c.exit_layer > c.n_layers))
             fail(EL_INVALID_ARGUMENT, "EngineConfig: always_at layer outside [1, n_layers]");
         if (c.d_model > 1024) fail(EL_INVALID_ARGUMENT, "d_model > 1024 unsupported on this engine");
+        if (c.encoder_len < 0 || c.encoder_len > 2048)
+            fail(EL_INVALID_ARGUMENT, "ModelConfig: encoder_len must be in [0, 2048]");
     }
 
     double check_cost() const {
@@ -314,6 +325,35 @@ struct el_engine {
             const uint16_t bits = el::bf16_bits_rne(2.0 * u - 1.0);
             uint32_t f = (uint32_t)bits << 16;
             std::memcpy(&probe_b, &f, 4);
+        }
+
+        // ---- T5 mode: cross-attention weights (tags after the reference's last, 4 + 6L + 4i + k),
+        //      the static per-sequence encoder K/V blocks and their (identity) block tables ----
+        if (cfg.encoder_len > 0) {
+            const int T = cfg.encoder_len;
+            wqc.alloc((size_t)L * dp * dp, false);
+            wkvc.alloc((size_t)L * 2 * dp * dp, false);
+            woc.alloc((size_t)L * dp * dp, false);
+            for (int i = 0; i < L; ++i) {
+                const uint64_t base = 4 + (uint64_t)L * 6 + (uint64_t)i * 4;
+                el::launch_weightgen(wqc.p + (size_t)i * dp * dp, d, d, dp, dp, tseed(base + 0), sd, 1, stream);
+                uint16_t* kv = wkvc.p + (size_t)i * 2 * dp * dp;
+                el::launch_weightgen(kv, d, d, dp, dp, tseed(base + 1), sd, 1, stream);
+                el::launch_weightgen(kv + (size_t)dp * dp, d, d, dp, dp, tseed(base + 2), sd, 1, stream);
+                el::launch_weightgen(woc.p + (size_t)i * dp * dp, d, d, dp, dp, tseed(base + 3), sd, 1, stream);
+            }
+            enc_blocks = ceil_div(T, cfg.block_capacity);
+            const size_t nblk = (size_t)cfg.max_batch * L * enc_blocks;
+            ckpool.alloc(nblk * cfg.block_capacity * dp);
+            cvpool.alloc(nblk * cfg.block_capacity * dp);
+            std::vector<int> tab(nblk);
+            for (size_t i = 0; i < nblk; ++i) tab[i] = (int)i;
+            ctables.alloc(nblk);
+            CK(cudaMemcpy(ctables.p, tab.data(), sizeof(int) * nblk, cudaMemcpyHostToDevice));
+            xslot.alloc((size_t)cfg.max_batch);
+            xid.alloc((size_t)cfg.max_batch);
+            enc_act.alloc((size_t)round_up(cfg.max_batch * T, 256) * dp, false);
+            enc_seed = el::splitmix64_at(cfg.model_seed, 0x454E43u);  // oracle: eo_encoder_seed
         }
 
         // ---- KV pool + allocator ----
@@ -400,7 +440,8 @@ struct el_engine {
         // streams across item boundaries, so short items cost no pipeline drain
         // partial slots per sequence: one per CTA segment (<= blocks of the sequence)
         attn_cb = 1;
-        attn_max_chunks = std::min(bpl, 128);
+        attn_max_chunks = std::min(std::max(bpl, enc_blocks), 128);
+        if (enc_blocks > 128) fail(EL_INVALID_ARGUMENT, "cross-attention: more than 128 encoder blocks unsupported");
         if (bpl > 128) fail(EL_INVALID_ARGUMENT, "attention: more than 128 KV blocks per sequence unsupported");
         if (B > 256) fail(EL_INVALID_ARGUMENT, "attention: batch > 256 unsupported");
         (void)opt_attn_cb;
@@ -516,6 +557,8 @@ struct el_engine {
         P.g[el::kIUp] = g(wup.p, fp / 128, dp / 64, fp / 128, 0, mega_splits(fp / 128, dp / 64));
         P.g[el::kIDown] = g(wdown.p, dp / 128, fp / 64, dp / 128, 0, mega_splits(dp / 128, fp / 64));
         // fill: full-K units (direct epilogue) at large N, where split-K partials would outweigh the weights
+        P.g[el::kIQc] = g(wqc.p, dp / 128, dp / 64, dp / 128, 0, mega_splits(dp / 128, dp / 64));
+        P.g[el::kIWoc] = g(woc.p, dp / 128, dp / 64, dp / 128, 0, mega_splits(dp / 128, dp / 64));
         int fs = opt_mega_fill_splits ? opt_mega_fill_splits : (n_pad >= 128 ? 1 : std::min(4, dp / 64));
         fs = std::min(fs, dp / 64);
         P.g[el::kIFill] = g(wqkv.p, 2 * dp / 128, dp / 64, 3 * dp / 128, dp / 128, fs);
@@ -523,7 +566,7 @@ struct el_engine {
         // batch-M full-K GEMMs (no split-K reduce phase) for QKV / W_o / up at small batch
         int nt_max = 16;
         if (n_pad <= opt_mega_bm_max) {
-            for (int k : {el::kIQkv, el::kIWo, el::kIUp}) {
+            for (int k : {el::kIQkv, el::kIWo, el::kIUp, el::kIQc, el::kIWoc}) {
                 el::IterGemm& x = P.g[k];
                 const int F = x.m_tiles * 128;
                 int nt = 16;
@@ -550,7 +593,8 @@ struct el_engine {
         if (el::iter_max_ctas_per_sm(dm, P.ring_bytes) < 1)
             fail(EL_CUDA_ERROR, "persistent kernel does not fit on an SM (%d bytes)", el::iter_smem_bytes(P.ring_bytes));
         size_t units = 0;
-        for (int k = 0; k < el::kIFill; ++k) units = std::max(units, (size_t)P.g[k].m_tiles * P.g[k].splits);
+        for (int k = 0; k < el::kINumGemm; ++k)
+            if (k != el::kIFill) units = std::max(units, (size_t)P.g[k].m_tiles * P.g[k].splits);
         if (fs > 1) units = std::max(units, (size_t)(L - 1) * (2 * dp / 128) * fs);
         const size_t need = units * n_pad * 128;
         if (mpart.n < need) {
@@ -604,6 +648,10 @@ struct el_engine {
         s.cur_iter = prefill ? cur_iter.p + 2 : cur_iter.p;
         s.rec_tok = rec_tok.p; s.rec_acc = rec_acc.p; s.rec_out = rec_out.p; s.rec_conf = rec_conf.p;
         s.rec_cap = rec_cap;
+        s.enc_len = cfg.encoder_len;
+        s.enc_blocks = enc_blocks;
+        s.wqc = wqc.p; s.wkvc = wkvc.p; s.woc = woc.p;
+        s.ckpool = ckpool.p; s.cvpool = cvpool.p; s.ctables = ctables.p;
         return s;
     }
 
@@ -858,6 +906,9 @@ struct el_engine {
                 if (prompt[j] < 0 || prompt[j] >= cfg.vocab_size)
                     fail(EL_INVALID_ARGUMENT, "workload: token id %d outside vocab at request %d", prompt[j], i);
             max_cap = std::max(max_cap, plen + max_new[r]);
+            if (cfg.encoder_len > 0 && plen > 1 && cfg.synthetic_kv_seed < 0)
+                fail(EL_INVALID_ARGUMENT, "T5 mode: a decoder prompt is the single start token (the input goes to "
+                                          "the encoder); request %d has %d tokens", i, plen);
         }
         reset_allocator();
         ensure_bpl(std::min(bpl_for(max_cap), std::max(1, cfg.pool_blocks / L)));
@@ -912,6 +963,7 @@ struct el_engine {
             // admit (engine.cpp:183-206) -- prefill charges advance the clock in
             // admission order; the prefill math itself is batched afterwards
             std::vector<PfSeq> pf;
+            size_t admitted_now = 0;
             while (next_pending < n) {
                 const int r = order[(size_t)next_pending];
                 if (arrival[r] > clock) break;
@@ -939,7 +991,16 @@ struct el_engine {
                 t->pf_seq.push_back(q.id);
                 t->pf_positions.push_back(positions);
                 running.push_back(std::move(q));
+                ++admitted_now;
                 ++next_pending;
+            }
+            if (cfg.encoder_len > 0 && admitted_now > 0) {  // T5 mode: static cross K/V of the new sequences
+                std::vector<int> ids, slots;
+                for (size_t i = running.size() - admitted_now; i < running.size(); ++i) {
+                    ids.push_back(running[i].id);
+                    slots.push_back(running[i].slot);
+                }
+                cross_prefill(slots, ids);
             }
             if (!pf.empty()) {
                 if (cfg.synthetic_kv_seed >= 0) {
@@ -1036,6 +1097,28 @@ struct el_engine {
         return t.release();
     }
 
+    // T5 mode: the static cross K/V of newly admitted sequences -- encoder states generated
+    // on the device, then K_c | V_c = W_kvc^(l) E^T for every layer as a tensor-core GEMM
+    // (N = sequences x encoder_len) written straight into the sequences' cross blocks
+    void cross_prefill(const std::vector<int>& slots, const std::vector<int>& ids) {
+        if (cfg.encoder_len <= 0 || slots.empty()) return;
+        const int n = (int)slots.size(), T = cfg.encoder_len, dp = dm.dp;
+        CK(cudaMemcpyAsync(xslot.p, slots.data(), sizeof(int) * n, cudaMemcpyHostToDevice, stream));
+        CK(cudaMemcpyAsync(xid.p, ids.data(), sizeof(int) * n, cudaMemcpyHostToDevice, stream));
+        const int N = n * T, NRe = round_up(N, 256);
+        el::launch_encoder_states(enc_act.p, NRe, xid.p, n, T, cfg.d_model, dp, enc_seed, stream);
+        el::GemmPlan P = make_plan(wkvc.p, enc_act.p, 0, 2 * dp / 128, dp, 256, false, 1);
+        el::DevState s = state(true, N);
+        s.rows.slot = xslot.p;
+        s.rows.B = N;
+        s.NR = NRe;
+        for (int l = 1; l <= dm.L; ++l) {
+            CK(cudaMemcpyAsync(layer.p, &l, sizeof(int), cudaMemcpyHostToDevice, stream));
+            el::launch_gemm(el::kGemmCross, P, s, stream, false);
+        }
+        CK(cudaStreamSynchronize(stream));  // l is a host stack variable
+    }
+
     // seeded KV prefix for the sequences in `slots` (rows of the prefill row set)
     void seed_prefix(const std::vector<int>& slots, const std::vector<int>& ids, int P, uint64_t kv_seed) {
         const int B = (int)slots.size();
@@ -1064,6 +1147,7 @@ struct el_engine {
             idv.push_back(ids ? ids[b] : b);
         }
         seed_prefix(slots, idv, prefix_len, kv_seed);
+        cross_prefill(slots, idv);
         CK(cudaMemcpyAsync(row_slot.p, slots.data(), sizeof(int) * B, cudaMemcpyHostToDevice, stream));
         CK(cudaMemcpyAsync(row_pos.p, pos.data(), sizeof(int) * B, cudaMemcpyHostToDevice, stream));
         CK(cudaMemcpyAsync(row_tok.p, tok.data(), sizeof(int) * B, cudaMemcpyHostToDevice, stream));

@@ -421,6 +421,14 @@ __device__ __forceinline__ void apply4(const DevState& st, const IterSmem& sm, c
                                         (uint32_t)f32_to_bf16(v.z) | ((uint32_t)f32_to_bf16(v.w) << 16));
             *reinterpret_cast<uint2*>(dst) = pk;
         }
+    } else if constexpr (K == kIWoc) {  // T5 mode: mid += W_oc . cross
+        const size_t i = (size_t)c * dp + R;
+        const float4 h = __ldcg(reinterpret_cast<const float4*>(st.mid32 + i));
+        const float4 o = make_float4(h.x + v.x, h.y + v.y, h.z + v.z, h.w + v.w);
+        *reinterpret_cast<float4*>(st.mid32 + i) = o;
+        *reinterpret_cast<uint2*>(st.mid_b + act_offset(c, R, NR)) =
+            make_uint2((uint32_t)f32_to_bf16(o.x) | ((uint32_t)f32_to_bf16(o.y) << 16),
+                       (uint32_t)f32_to_bf16(o.z) | ((uint32_t)f32_to_bf16(o.w) << 16));
     } else if constexpr (K == kIWo) {
         const size_t i = (size_t)c * dp + R;
         const float4 h = __ldcg(reinterpret_cast<const float4*>(st.h32 + (size_t)x.pin * Bm * dp + i));
@@ -660,6 +668,22 @@ __device__ __forceinline__ void apply16_t(const DevState& st, const IterSmem& sm
         for (int t = 0; t < 4; ++t) m[t] = make_float4(o[4 * t], o[4 * t + 1], o[4 * t + 2], o[4 * t + 3]);
         *reinterpret_cast<uint4*>(st.mid_b + act_offset(b, f, NR)) = pack(o);
         *reinterpret_cast<uint4*>(st.mid_b + act_offset(b, f + 8, NR)) = pack(o + 8);
+    } else if constexpr (K == kIWoc) {  // T5 mode: cross-attention output projection + residual (in place)
+        const size_t i = (size_t)b * dp + f;
+        float4* m4 = reinterpret_cast<float4*>(st.mid32 + i);
+        float o[16];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            const float4 hv = __ldcg(m4 + t);
+            o[4 * t] = hv.x + v[4 * t];
+            o[4 * t + 1] = hv.y + v[4 * t + 1];
+            o[4 * t + 2] = hv.z + v[4 * t + 2];
+            o[4 * t + 3] = hv.w + v[4 * t + 3];
+        }
+#pragma unroll
+        for (int t = 0; t < 4; ++t) m4[t] = make_float4(o[4 * t], o[4 * t + 1], o[4 * t + 2], o[4 * t + 3]);
+        *reinterpret_cast<uint4*>(st.mid_b + act_offset(b, f, NR)) = pack(o);
+        *reinterpret_cast<uint4*>(st.mid_b + act_offset(b, f + 8, NR)) = pack(o + 8);
     } else if constexpr (K == kIUp) {
         float o[16];
 #pragma unroll
@@ -791,7 +815,14 @@ __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(DevState st, Iter
         }
     }
 
-    if (warp == kProducerWarp) attn_prefix_sum(st, sm.att);  // KV blocks per row: fixed for the iteration
+    if (warp == kProducerWarp) {
+        attn_prefix_sum(st, sm.att);  // KV blocks per row: fixed for the iteration
+        if (st.enc_len > 0)
+            for (int b = tid & 31; b <= B; b += 32) sm.att.pref_c[b] = b * st.enc_blocks;
+        __syncwarp();
+    }
+    const AttnSrc self_src{st.tables, dm.bpl_max, st.kpool, st.vpool, 0, sm.att.pref};
+    const AttnSrc cross_src{st.ctables, st.enc_blocks, st.ckpool, st.cvpool, st.enc_len, sm.att.pref_c};
     // ---- embed (model.cpp:171-183): h_0 = embedding row of the input token ----
     for (int b = cta; b < B; b += G) {
         const uint16_t* e = st.emb + (size_t)st.rows.tok[b] * dp;
@@ -831,7 +862,7 @@ __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(DevState st, Iter
             l2_prefetch_gemm(p.g[kIDown], layer);
         }
         __syncwarp();
-        attn_body<NJ>(st, sm.att, ring, layer, aseq, true);
+        attn_body<NJ>(st, sm.att, ring, layer, aseq, true, self_src);
         astamp(1);
         grid_sync(p, st, nbar, g0);
         aseq = sm.att.seq_next;
@@ -849,6 +880,28 @@ __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(DevState st, Iter
             reduce_phase<kIWo>(st, sm, p, p.g[kIWo], x, B, 0, p.g[kIWo].m_tiles);
         }
         grid_sync(p, st, nbar, g0);
+        if (st.enc_len > 0) {
+            // T5 mode: mid += W_oc . softmax(q_c K_c^T / sqrt(d)) V_c, q_c = W_qc . mid
+            if (p.g[kIQc].mode) {
+                gemm_phase_t<kIQkv>(st, sm, ring, p, p.g[kIQc], x, st.mid_b, kseq2, useq, B);  // q_c -> q32
+            } else {
+                gemm_phase(st, sm, ring, p, p.g[kIQc], layer, st.mid_b, kseq, useq, B);
+                grid_sync(p, st, nbar, g0);
+                reduce_phase<kIQkv>(st, sm, p, p.g[kIQc], x, B, 0, p.g[kIQc].m_tiles);
+            }
+            grid_sync(p, st, nbar, g0);
+            attn_body<NJ>(st, sm.att, ring, layer, aseq, true, cross_src);  // -> att_b
+            grid_sync(p, st, nbar, g0);
+            aseq = sm.att.seq_next;
+            if (p.g[kIWoc].mode) {
+                gemm_phase_t<kIWoc>(st, sm, ring, p, p.g[kIWoc], x, st.att_b, kseq2, useq, B);
+            } else {
+                gemm_phase(st, sm, ring, p, p.g[kIWoc], layer, st.att_b, kseq, useq, B);
+                grid_sync(p, st, nbar, g0);
+                reduce_phase<kIWoc>(st, sm, p, p.g[kIWoc], x, B, 0, p.g[kIWoc].m_tiles);
+            }
+            grid_sync(p, st, nbar, g0);
+        }
         // up + ReLU (model.cpp:255-260)
         if (p.g[kIUp].mode) {
             gemm_phase_t<kIUp>(st, sm, ring, p, p.g[kIUp], x, st.mid_b, kseq2, useq, B);

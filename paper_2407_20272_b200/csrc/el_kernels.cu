@@ -156,6 +156,30 @@ struct Epi<kGemmFill> {
     }
 };
 
+// --- T5 mode: static cross K/V of newly admitted sequences, K_c | V_c = W_kvc^(l) E^T
+//     over their encoder states (column = row j * T + t of the encoder batch; rows.slot[j]
+//     is sequence j's slot), written once into the sequence's cross blocks.
+template <>
+struct Epi<kGemmCross> {
+    static constexpr bool kTile = false;
+    __device__ static bool setup(const DevState& st, int tile, EpiSmem& e, int& a_row, int& b_row) {
+        const int layer = *st.layer;
+        e.layer = layer;
+        e.row0 = tile * kBM;
+        a_row = (layer - 1) * 2 * st.dm.dp + tile * kBM;
+        b_row = 0;
+        return true;
+    }
+    __device__ static void prologue(const DevState&, EpiSmem&) {}
+    __device__ static void apply(const DevState& st, const EpiSmem& e, int row, int col, float v) {
+        const Dims& dm = st.dm;
+        const int m = e.row0 + row, kind = m >= dm.dp, f = m - kind * dm.dp;
+        const int j = col / st.enc_len, t = col % st.enc_len;
+        const int blk = st.ctables[((size_t)st.rows.slot[j] * dm.L + (e.layer - 1)) * st.enc_blocks + t / dm.bc];
+        (kind ? st.cvpool : st.ckpool)[((size_t)blk * dm.bc + t % dm.bc) * dm.dp + f] = f32_to_bf16(v);
+    }
+};
+
 // --- attention output projection + residual (model.cpp:245-253)
 template <>
 struct Epi<kGemmWo> {
@@ -361,7 +385,7 @@ __global__ void __launch_bounds__(128, 1)
     EpiSmem& es = *reinterpret_cast<EpiSmem*>(smem + region + (2 * g.stages + 1) * 8 + 16);
 
     constexpr int tl_kind = K == kGemmQkv ? 1 : K == kGemmWo ? 3 : K == kGemmUp ? 4 : K == kGemmDown ? 5
-                          : K == kGemmLmCheck ? 10 : K == kGemmLmFinal ? 8 : 7;
+                          : K == kGemmLmCheck ? 10 : K == kGemmLmFinal ? 8 : K == kGemmCross ? 12 : 7;
     const int tl_layer = (K == kGemmLmFinal || K == kGemmFill) ? 0 : *st.layer;
     tl_mark(st, tl_kind, tl_layer, 0);
     auto stamp = [&](int i) {
@@ -650,6 +674,7 @@ void launch_gemm(GemmKind kind, const GemmPlan& p, const DevState& st, cudaStrea
         case kGemmLmCheck: launch_gemm_t<kGemmLmCheck>(p, st, s, pdl); break;
         case kGemmLmFinal: launch_gemm_t<kGemmLmFinal>(p, st, s, pdl); break;
         case kGemmFill: launch_gemm_t<kGemmFill>(p, st, s, pdl); break;
+        case kGemmCross: launch_gemm_t<kGemmCross>(p, st, s, pdl); break;
     }
 }
 
@@ -688,6 +713,7 @@ struct AttnSmem {
     float cw[128];
     float cl[128];
     int pref[257];  // block prefix sum over the batch rows
+    int pref_c[257];  // the same for the cross-attention (T5 mode) blocks: row b -> b * enc_blocks
     int last_flag;
     int seq_next;   // ring sequence base for the next pass
     int pad;
@@ -722,6 +748,18 @@ __device__ __forceinline__ int atom_add_acq_rel(int* p, int v) {
 // standalone kernel and the persistent iteration kernel; `seq0` continues the
 // mbarrier ring's sequence (phase parity) across calls; on return a.seq_next
 // holds the next base.
+// What one attention pass reads: the self-attention pass streams the paged
+// decoder KV (context pos + 1 per row); the T5-mode cross pass streams the
+// static per-sequence encoder K/V (context = encoder length for every row).
+struct AttnSrc {
+    const int* tables;  // [slots][L][tstride] block ids
+    int tstride;
+    const uint16_t* kpool;
+    const uint16_t* vpool;
+    int ctx_fixed;      // > 0: every row attends over this many positions (no position written this pass)
+    const int* pref;    // shared-memory block prefix sum over the rows
+};
+
 // attn_prefix_sum: the warp-parallel prefix sum of KV blocks per row into a.pref
 // (rows.pos is constant for a whole decode iteration, so the persistent kernel
 // computes it once per launch and passes persistent = true).
@@ -747,7 +785,7 @@ __device__ __forceinline__ void attn_prefix_sum(const DevState& st, AttnSmem& a)
 // no programmatic-dependent-launch deferral is needed (every input is ready).
 template <int NJ>
 __device__ void attn_body(const DevState& st, AttnSmem& a, uint8_t* stages, int layer, int seq0,
-                          bool persistent = false) {
+                          bool persistent, const AttnSrc& src) {
     const Dims& dm = st.dm;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int dp = dm.dp, nchunk = dp / 8;
@@ -764,7 +802,7 @@ __device__ void attn_body(const DevState& st, AttnSmem& a, uint8_t* stages, int 
         // streamed; q and the block holding `pos` (written by this layer's QKV
         // kernel) are requested after it (one pending stage).
         const int B = st.rows.B;
-        if (!persistent) attn_prefix_sum(st, a);
+        if (!persistent) attn_prefix_sum(st, a);  // (standalone kernel: src.pref == a.pref)
         // Work split: the flattened (row, block) space [0, T) is cut into a static
         // head [0, Ts) -- CTA i streams [i*Ts/G, (i+1)*Ts/G), with fewer blocks than
         // CTAs only the first Ts CTAs work -- and a dynamic tail [Ts, T) of items
@@ -772,7 +810,7 @@ __device__ void attn_body(const DevState& st, AttnSmem& a, uint8_t* stages, int 
         // range is done, so SMs that HBM serves faster take more of the tail.
         // Partial slots per row: static segments in CTA order, then tail items in
         // item order -- the combine order never depends on which CTA ran what.
-        const long long T = a.pref[B];
+        const long long T = src.pref[B];
         const int cb = max(1, st.attn_dyn_cb);
         const long long Td = (st.attn_dyn_permille > 0 && st.attn_queue)
                                  ? min(T, (T * st.attn_dyn_permille / 1000 + cb - 1) / cb * cb) : 0;
@@ -782,13 +820,13 @@ __device__ void attn_body(const DevState& st, AttnSmem& a, uint8_t* stages, int 
         auto cta_of = [&](long long g) { return (int)(((g + 1) * G + Ts - 1) / Ts - 1); };
         // segment bookkeeping of row r: static segments and the first tail item touching it
         auto row_static = [&](int r, int& first_cta) {
-            const long long r0 = a.pref[r], r1 = min((long long)a.pref[r + 1], Ts);
+            const long long r0 = src.pref[r], r1 = min((long long)src.pref[r + 1], Ts);
             if (r0 >= r1) return 0;
             first_cta = cta_of(r0);
             return cta_of(r1 - 1) - first_cta + 1;
         };
         auto row_items = [&](int r, long long& i0) {
-            const long long r0 = max((long long)a.pref[r], Ts), r1 = a.pref[r + 1];
+            const long long r0 = max((long long)src.pref[r], Ts), r1 = src.pref[r + 1];
             if (r0 >= r1) return 0LL;
             i0 = (r0 - Ts) / cb;
             return (r1 - 1 - Ts) / cb - i0 + 1;
@@ -805,8 +843,8 @@ __device__ void attn_body(const DevState& st, AttnSmem& a, uint8_t* stages, int 
                 uint8_t* sb = stages + (size_t)ds * stage_bytes;
                 if (dq >= 0) bulk_load(sb + 2 * blk_bytes, st.q32 + (size_t)dq * dp, (uint32_t)dp * 4, &a.full[ds]);
                 if (dbytes) {
-                    bulk_load_ef(sb, st.kpool + (size_t)did * dm.bc * dp, dbytes, &a.full[ds]);
-                    bulk_load_ef(sb + blk_bytes, st.vpool + (size_t)did * dm.bc * dp, dbytes, &a.full[ds]);
+                    bulk_load_ef(sb, src.kpool + (size_t)did * dm.bc * dp, dbytes, &a.full[ds]);
+                    bulk_load_ef(sb + blk_bytes, src.vpool + (size_t)did * dm.bc * dp, dbytes, &a.full[ds]);
                 }
                 ds = -1;
                 dq = -1;
@@ -816,10 +854,10 @@ __device__ void attn_body(const DevState& st, AttnSmem& a, uint8_t* stages, int 
         int seq = seq0;
         // stream blocks [g, seg_end) of row b as one segment (partial slot `slot` of `nseg`)
         auto emit = [&](int b, long long g, long long seg_end, int slot, int nseg) {
-            const long long sb0 = a.pref[b], sb1 = a.pref[b + 1];
+            const long long sb0 = src.pref[b], sb1 = src.pref[b + 1];
             const int nblk = (int)(sb1 - sb0);
-            const int ctx = st.rows.pos[b] + 1;
-            const int* table = st.tables + ((size_t)st.rows.slot[b] * dm.L + (layer - 1)) * dm.bpl_max;
+            const int ctx = src.ctx_fixed > 0 ? src.ctx_fixed : st.rows.pos[b] + 1;
+            const int* table = src.tables + ((size_t)st.rows.slot[b] * dm.L + (layer - 1)) * src.tstride;
             for (long long gb = g; gb < seg_end; gb += 32) {
                 const int blk_base = (int)(gb - sb0);
                 const int nb = (int)min(32LL, seg_end - gb);
@@ -852,14 +890,14 @@ __device__ void attn_body(const DevState& st, AttnSmem& a, uint8_t* stages, int 
                                 did = id;
                                 dbytes = bytes;
                             } else {
-                                bulk_load_ef(sbuf, st.kpool + (size_t)id * dm.bc * dp, bytes, &a.full[s]);
-                                bulk_load_ef(sbuf + blk_bytes, st.vpool + (size_t)id * dm.bc * dp, bytes, &a.full[s]);
+                                bulk_load_ef(sbuf, src.kpool + (size_t)id * dm.bc * dp, bytes, &a.full[s]);
+                                bulk_load_ef(sbuf + blk_bytes, src.vpool + (size_t)id * dm.bc * dp, bytes, &a.full[s]);
                             }
                         } else {
                             if (first)
                                 bulk_load(sbuf + 2 * blk_bytes, st.q32 + (size_t)b * dp, (uint32_t)dp * 4, &a.full[s]);
-                            bulk_load_ef(sbuf, st.kpool + (size_t)id * dm.bc * dp, bytes, &a.full[s]);
-                            bulk_load_ef(sbuf + blk_bytes, st.vpool + (size_t)id * dm.bc * dp, bytes, &a.full[s]);
+                            bulk_load_ef(sbuf, src.kpool + (size_t)id * dm.bc * dp, bytes, &a.full[s]);
+                            bulk_load_ef(sbuf + blk_bytes, src.vpool + (size_t)id * dm.bc * dp, bytes, &a.full[s]);
                         }
                     }
                 }
@@ -870,9 +908,9 @@ __device__ void attn_body(const DevState& st, AttnSmem& a, uint8_t* stages, int 
         if ((long long)blockIdx.x < G) {
             const long long g0 = (long long)blockIdx.x * Ts / G, g1 = (long long)(blockIdx.x + 1) * Ts / G;
             int b = 0;
-            while (b < B && a.pref[b + 1] <= g0) ++b;
+            while (b < B && src.pref[b + 1] <= g0) ++b;
             for (long long g = g0; g < g1 && b < B;) {
-                const long long seg_end = min(g1, (long long)a.pref[b + 1]);
+                const long long seg_end = min(g1, (long long)src.pref[b + 1]);
                 int fc = 0;
                 const int ns = row_static(b, fc);
                 long long i0 = 0;
@@ -896,13 +934,13 @@ __device__ void attn_body(const DevState& st, AttnSmem& a, uint8_t* stages, int 
                     int lo = 0, hi = B - 1;
                     while (lo < hi) {
                         const int mid = (lo + hi + 1) >> 1;
-                        if (a.pref[mid] <= gs) lo = mid;
+                        if (src.pref[mid] <= gs) lo = mid;
                         else hi = mid - 1;
                     }
                     b = lo;
                 }
                 for (long long g = gs; g < ge && b < B; ++b) {
-                    const long long seg_end = min(ge, (long long)a.pref[b + 1]);
+                    const long long seg_end = min(ge, (long long)src.pref[b + 1]);
                     if (seg_end <= g) continue;
                     int fc = 0;
                     const int ns = row_static(b, fc);
@@ -1165,7 +1203,8 @@ __global__ void __launch_bounds__(kAttnThreads) attn_kernel(DevState st) {
         fence_barrier_init();
     }
     __syncthreads();
-    attn_body<NJ>(st, a, stages, layer, 0);
+    const AttnSrc src{st.tables, st.dm.bpl_max, st.kpool, st.vpool, 0, a.pref};
+    attn_body<NJ>(st, a, stages, layer, 0, false, src);
     if ((st.dbg & 32) && tid == 0) {
         unsigned long long t;
         asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -1367,6 +1406,22 @@ __global__ void embed_kernel(DevState st) {
         }
     }
 }
+// T5 mode: encoder state (seq id, t) = seeded_vector(d, splitmix64_at(enc_seed, id << 20 | t)),
+// bf16-rounded (oracle/exitlab_oracle.c: eo_encoder_state), as GEMM B-operand rows j * T + t
+__global__ void encoder_state_kernel(uint16_t* act, int NR, const int* ids, int T, int d, int dp, uint64_t enc_seed) {
+    const int row = blockIdx.x, j = row / T, t = row % T;
+    const uint64_t vs = splitmix64_at(enc_seed, ((uint64_t)ids[j] << 20) | (uint64_t)t);
+    const double scale = 1.0 / sqrt((double)d);
+    for (int i = threadIdx.x; i < dp; i += blockDim.x)
+        act[act_offset(row, i, NR)] = (i < d) ? bf16_bits_rne(seeded_value(vs, (uint64_t)i, scale)) : (uint16_t)0;
+}
+void launch_encoder_states(uint16_t* act, int NR, const int* ids, int n, int T, int d, int dp, uint64_t enc_seed,
+                           cudaStream_t s) {
+    if (n * T <= 0) return;
+    encoder_state_kernel<<<n * T, 128, 0, s>>>(act, NR, ids, T, d, dp, enc_seed);
+    EL_CUDA_LAUNCH_CHECK();
+}
+
 void launch_embed(const DevState& st, cudaStream_t s) {
     embed_kernel<<<st.rows.B, 128, 0, s>>>(st);
     EL_CUDA_LAUNCH_CHECK();
@@ -1500,6 +1555,8 @@ void init_kernel_attributes() {
     cudaFuncSetAttribute(gemm_kernel<kGemmLmCheck>, cudaFuncAttributeMaxDynamicSharedMemorySize, m);
     cudaFuncSetAttribute(gemm_kernel<kGemmLmFinal>, cudaFuncAttributeMaxDynamicSharedMemorySize, m);
     cudaFuncSetAttribute(gemm_kernel<kGemmFill>, cudaFuncAttributeMaxDynamicSharedMemorySize, m);
+    cudaFuncSetAttribute(gemm_kernel<kGemmCross>, cudaFuncAttributeMaxDynamicSharedMemorySize, m);
+    cudaFuncSetAttribute(gemm_kernel<kGemmCross>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     cudaFuncSetAttribute(attn_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, m);
     cudaFuncSetAttribute(attn_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, m);
     cudaFuncSetAttribute(attn_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, m);

@@ -103,6 +103,14 @@ struct DevState {
     int* rec_out;     // [rec_cap]
     float* rec_conf;  // [rec_cap][L][Bmax]
     int rec_cap;
+    // T5 mode (encoder_len > 0): cross-attention weights and the static encoder K/V
+    int enc_len, enc_blocks;    // encoder states per sequence; KV blocks they occupy
+    const uint16_t* wqc;        // [L][dp][dp]   tiled
+    const uint16_t* wkvc;       // [L][2dp][dp]  tiled, rows k_c | v_c
+    const uint16_t* woc;        // [L][dp][dp]   tiled
+    uint16_t* ckpool;           // [slots * L * enc_blocks][bc][dp]
+    uint16_t* cvpool;
+    const int* ctables;         // [slots][L][enc_blocks] (static)
 };
 
 // Weight (GEMM A operand) layout in HBM: 128x64 bf16 tiles, tile-major
@@ -132,7 +140,7 @@ struct GemmPlan {
     int m_tiles, splits, kb_total, n_pad, stages, smem_bytes, tmem_cols;
 };
 
-enum GemmKind : int { kGemmQkv = 0, kGemmWo, kGemmUp, kGemmDown, kGemmLmCheck, kGemmLmFinal, kGemmFill };
+enum GemmKind : int { kGemmQkv = 0, kGemmWo, kGemmUp, kGemmDown, kGemmLmCheck, kGemmLmFinal, kGemmFill, kGemmCross };
 
 int gemm_smem_bytes(int n_pad, int stages, bool tile_reduce);
 void init_kernel_attributes();
@@ -143,6 +151,9 @@ void launch_weightgen(uint16_t* out, int rows, int cols, int rows_p, int cols_p,
 void launch_kv_prefix(const DevState& st, const int* row_seq_ids, int prefix_len, uint64_t kv_seed, int round_bf16,
                       cudaStream_t s);
 void launch_embed(const DevState& st, cudaStream_t s);
+// T5 mode: seeded encoder states of n sequences (ids) as bf16 GEMM B operand rows j*T + t (act layout, NR rows)
+void launch_encoder_states(uint16_t* act, int NR, const int* ids, int n, int T, int d, int dp, uint64_t enc_seed,
+                           cudaStream_t s);
 // one attention stage: K block | V block | q (fp32); also hosts the 8-warp merge
 __host__ __device__ inline int attn_stage_bytes(const Dims& dm) {
     const int kvq = 2 * dm.bc * dm.dp * 2 + dm.dp * 4;
@@ -163,7 +174,7 @@ void launch_kv_release(int* stack, int top, const int* tables, const Dims& dm, i
 
 
 // ---- persistent decode-iteration kernel (el_iter.cuh) ----
-enum IterGemmId : int { kIQkv = 0, kIWo, kIUp, kIDown, kIFill, kINumGemm };
+enum IterGemmId : int { kIQkv = 0, kIWo, kIUp, kIDown, kIFill, kIQc, kIWoc, kINumGemm };
 
 struct IterGemm {
     const uint16_t* A;  // tiled weights (tiled_offset), tile row 0 of layer 1

@@ -301,3 +301,55 @@ def test_persistent_kernel_deterministic_and_matches_per_phase(B, tech):
     assert np.array_equal(ha, hb) and np.array_equal(ka[0], kb[0]) and np.array_equal(ka[1], kb[1])
     assert relerr(ha, hc) <= HID_TOL and relerr(ka[0], kc[0]) <= HID_TOL
     assert np.mean([np.mean(x["tokens"] == y["tokens"]) for x, y in zip(ra, rc)]) >= 0.9
+
+
+@pytest.mark.parametrize("B", [8, 136])
+@pytest.mark.parametrize("tech,lam,gamma", [("state", 0.972, 0.998), ("classifier", 0.59, 1.0), ("never", 0.5, 1.0)])
+def test_t5_cross_attention_parity(port, tech, lam, gamma, B):
+    """T5 mode (north_star (1): cross-attention over encoder states; no reference
+    counterpart -- oracle = the C restatement, itself checked against an independent
+    numpy decoder in test_t5_oracle_cpu.py).  B = 8 runs the batch-M GEMM phases,
+    B = 136 the split-K + reduce phases of the persistent kernel."""
+    L, d, V, T = 4, 128, 512, 24
+    g = X.EngineConfig(model=X.ModelConfig(L, d, V, 5, encoder_len=T), technique=X.ExitTechnique(tech, 2),
+                       schedule=X.ThresholdSchedule(lam, gamma, 0.0), max_batch=B, pool_blocks=B * L * 8,
+                       eos_token=-1)
+    o = OB.engine_config(L, d, V, 5, tech, exit_layer=2, lambda0=lam, gamma=gamma, max_batch=B,
+                         pool_blocks=B * L * 8, eos_token=-1, round_bf16=True)
+    e = X.Engine(g)
+    first = (np.arange(B) * 37 + 3) % V
+    e.session_begin(first, 30, 60, 1234)
+    m = port.model(L, d, V, 5, True, encoder_len=T)
+    s = m.session(o, first, 30, 60, 1234)
+    st = _teacher_forced(e, s, 3, m.tensor("lm_head"), V, d)
+    for x in st:
+        assert x["h"] <= HID_TOL, x["h"]
+        assert x["conf"] <= CONF_TOL, x["conf"]
+        assert np.all(x["agree"] | (x["gap"] < TIE_GAP)), x["gap"][~x["agree"]]
+    assert np.mean([x["agree"].mean() for x in st]) >= 0.9
+    pos = 30 + len(st) - 1
+    for layer in range(1, L + 1):
+        kg, vg = e.kv(1, layer, pos)
+        ko, vo = s.kv(1, layer, pos)
+        assert relerr(kg, ko) <= HID_TOL and relerr(vg, vo) <= HID_TOL, layer
+    e.close()
+
+
+def test_t5_engine_run_matches_oracle(port):
+    """Engine::run in T5 mode (decoder prompt = start token, input in the encoder)."""
+    L, d, V, T = 3, 64, 256, 16
+    g = X.EngineConfig(model=X.ModelConfig(L, d, V, 9, encoder_len=T), technique=X.ExitTechnique("never"),
+                       max_batch=4, pool_blocks=512, eos_token=-1)
+    o = OB.engine_config(L, d, V, 9, "never", max_batch=4, pool_blocks=512, eos_token=-1, round_bf16=True)
+    reqs = [(0.0, [1], 6), (0.0, [5], 4), (0.0, [9], 7), (0.01, [2], 3), (0.02, [7], 5)]
+    e = X.Engine(g)
+    t = e.run(X.Workload([X.Request(*r) for r in reqs]))
+    tp = port.model(L, d, V, 9, True, encoder_len=T).run(o, OB.Workload.from_requests(reqs))
+    for f in ["it_output_layer", "it_batch_off", "ps_seq", "sq_id"]:
+        assert np.array_equal(t[f], tp[f]), f
+    gt = {s["id"]: s["tokens"] for s in t.sequences}
+    pt = {s["id"]: s["tokens"] for s in tp.sequences}
+    assert np.mean([a == b for k in pt for a, b in zip(gt[k], pt[k])]) >= 0.9
+    with pytest.raises(ValueError):  # decoder prompts are the start token in T5 mode
+        e.run(X.Workload([X.Request(0.0, [1, 2], 2)]))
+    e.close()
