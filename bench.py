@@ -43,6 +43,15 @@ CONFIGS = {
                name="configs[2]: CALM-T5-large dims (L=24, d=1024), exit classifier, batch 128, skipped-layer KV fill"),
     "c5": dict(L=24, d=1024, B=256, tech="classifier", lam=0.41, gamma=0.997,
                name="configs[4]: CALM-T5-large dims, request-sharded batch 256/GPU"),
+    # T5 mode (north_star (1); not in the reference): the 512-token input goes through cross-attention
+    # over 512 synthetic encoder states; the decoder self-attention holds the generated tokens
+    # (seeded prefix of 63 = mid-generation of the 128-token outputs)
+    "c2t5": dict(L=12, d=768, B=64, tech="state", lam=0.981, gamma=0.997, enc=512, prefix=63,
+                 name="configs[1] in T5 mode: CALM-T5-base dims, cross-attention over 512 encoder states, "
+                      "state exit, batch 64"),
+    "c5t5": dict(L=24, d=1024, B=256, tech="classifier", lam=0.41, gamma=0.997, enc=512, prefix=63,
+                 name="configs[4] in T5 mode: CALM-T5-large dims, cross-attention over 512 encoder states, "
+                      "classifier exit, batch 256/GPU"),
 }
 METRIC = "decode tokens/sec/GPU (early-exit vs full-layer), avg exit layer, %roofline"
 
@@ -150,11 +159,15 @@ def attn_bytes(d, ctx_list, B):
     return 4 * d * int(sum(ctx_list)) + B * d * 4 + B * d * 2
 
 
-def iteration_bytes(L, d, e, ctx_sum, B, tech):
-    """sum_{l<=e}[24d^2 + 4d*sum(c+1) + 4Bd] + sum_{l>e}[4d^2 + 4Bd] + e*C_chk + 2Vd + 2Bd."""
+def iteration_bytes(L, d, e, ctx_sum, B, tech, enc=0):
+    """sum_{l<=e}[24d^2 + 4d*sum(c+1) + 4Bd] + sum_{l>e}[4d^2 + 4Bd] + e*C_chk + 2Vd + 2Bd.
+    T5 mode adds per executed layer the cross weights W_qc, W_oc (4d^2) and the static encoder K/V
+    (4d * enc per row)."""
     chk = {"softmax": 2 * V * d, "classifier": 2 * d, "state": 0}.get(tech, 0)
     lm_final = 0 if tech == "softmax" else 2 * V * d  # softmax reuses the check's LM head (e == last check)
-    return e * (24 * d * d + 4 * d * ctx_sum + 4 * B * d) + (L - e) * (4 * d * d + 4 * B * d) + e * chk + lm_final + 2 * B * d
+    cross = (4 * d * d + 4 * d * enc * B) if enc else 0
+    return (e * (24 * d * d + 4 * d * ctx_sum + 4 * B * d + cross) + (L - e) * (4 * d * d + 4 * B * d) + e * chk
+            + lm_final + 2 * B * d)
 
 
 def shard(rank, world, B):
@@ -184,10 +197,12 @@ def run_ours(args, rank, world, local_rank, dist):
     ids = np.array(mine, np.int32)
     # one generation of the workload is 128 tokens; longer timed runs simply keep decoding
     # (contexts grow past 640), so any --steps/--warmup is valid
-    cap = PROMPT + max(OUT_LEN, args.warmup + args.steps + 1)
+    enc = c.get("enc", 0)
+    prefix = c.get("prefix", PROMPT - 1)
+    cap = prefix + 1 + max(OUT_LEN, args.warmup + args.steps + 1)
 
     def engine(tech):
-        cfg = X.EngineConfig(model=X.ModelConfig(L, d, V, 0), technique=X.ExitTechnique(tech),
+        cfg = X.EngineConfig(model=X.ModelConfig(L, d, V, 0, encoder_len=enc), technique=X.ExitTechnique(tech),
                              schedule=X.ThresholdSchedule(c["lam"], c["gamma"], 0.0), max_batch=B,
                              pool_blocks=B * L * (-(-cap // 16)), eos_token=-1)
         return X.Engine(cfg, graph=not args.eager, mega=False if args.no_mega else (True if args.mega else None))
@@ -201,7 +216,7 @@ def run_ours(args, rank, world, local_rank, dist):
 
     # 1. early-exit engine, device-resident timed region
     ee = engine(c["tech"])
-    ee.session_begin(first, PROMPT - 1, cap, 1, ids)
+    ee.session_begin(first, prefix, cap, 1, ids)
     clk = ClockSampler(local_rank).start()
     ee.decode_run(args.warmup)
     ee.sync()
@@ -217,10 +232,10 @@ def run_ours(args, rank, world, local_rank, dist):
     launches = int(sum(ee.launches_per_iteration(e) for e in exits))
     mean_e = float(np.mean(exits))
     # dominant kernel (paged attention) timed live on the same stream, same state
-    ctx = [PROMPT + args.warmup + args.steps] * B
+    ctx = [prefix + 1 + args.warmup + args.steps] * B
     attn_ms = ee.time_kernel(0, 1, 10)
     a_bytes = attn_bytes(d, ctx, B)
-    it_bytes = iteration_bytes(L, d, mean_e, float(np.mean(ctx)) * B, B, c["tech"])
+    it_bytes = iteration_bytes(L, d, mean_e, float(np.mean(ctx)) * B, B, c["tech"], enc)
     plan = ee.plan_info()
     ee.session_end()
 
@@ -228,7 +243,7 @@ def run_ours(args, rank, world, local_rank, dist):
     import torch
     pin = torch.empty(B, dtype=torch.int32, pin_memory=True).numpy()
     pin[:] = first
-    ee.session_begin(first, PROMPT - 1, cap, 1, ids)
+    ee.session_begin(first, prefix, cap, 1, ids)
     for _ in range(args.warmup):
         r = ee.decode_iteration(pin)
         pin[:] = r["tokens"]
@@ -243,7 +258,7 @@ def run_ours(args, rank, world, local_rank, dist):
 
     # 3. the same engine running full layers (exit disabled), same inputs
     fl = engine("never")
-    fl.session_begin(first, PROMPT - 1, cap, 1, ids)
+    fl.session_begin(first, prefix, cap, 1, ids)
     fl.decode_run(args.warmup)
     fl.sync()
     barrier()
@@ -273,7 +288,8 @@ def run_ours(args, rank, world, local_rank, dist):
                 "seeded random-init weights (ModelWeights::seeded, bf16-rounded)",
         "config": {"workload": c["name"], "model_dims": {"L": L, "d": d, "V": V}, "technique": c["tech"],
                    "schedule": {"lambda0": c["lam"], "gamma": c["gamma"]}, "batch_per_gpu": B,
-                   "global_batch": B * world, "seq_len": PROMPT, "ctx_range": [PROMPT, PROMPT + args.warmup + args.steps],
+                   "global_batch": B * world, "seq_len": PROMPT, "ctx_range": [prefix + 1, prefix + 1 + args.warmup + args.steps],
+                   "encoder_len": enc,
                    "parallelism": f"dp{world} (request-sharded replicas, no collective on the hot path)",
                    "l2": "inputs larger than L2 (>= %.0f MB read per step vs 126 MB L2)" % (it_bytes / 1e6)},
         "avg_exit_layer": round(mean_e, 3), "exit_layers": exits,
@@ -361,6 +377,9 @@ def run_reference(args, rank):
     if rank != 0:
         return None
     c = CONFIGS[args.config]
+    if c.get("enc"):
+        return {"impl": "reference", "unavailable": "the reference has no encoder / cross-attention "
+                "(T5 mode is the north_star extension; SPEC.md:13, 184)"}
     procs = os.cpu_count() or 1
     n = min(c["B"], procs * 4)
     r = cpu_arm(c, procs, args.steps, args.warmup, n)
@@ -414,7 +433,9 @@ def main():
         dist = tdist
     out = run_ours(args, rank, world, local_rank, dist)
     if out is not None:
-        if world == 1 and not args.no_cpu_baseline:
+        if CONFIGS[args.config].get("enc"):
+            out["cpu_baseline"] = None  # no reference implementation of T5 mode
+        elif world == 1 and not args.no_cpu_baseline:
             c = CONFIGS[args.config]
             procs = os.cpu_count() or 1
             n = min(c["B"], procs)
