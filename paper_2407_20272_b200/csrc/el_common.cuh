@@ -194,6 +194,28 @@ __device__ __forceinline__ void tc_mma_bf16(uint32_t tmem_d, uint64_t adesc, uin
         "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
         : "memory");
 }
+// Warp-collective forms: the whole (converged) warp executes them with identical
+// operands, one elected lane issues.  Keeping the issue loop warp-uniform lets the
+// compiler hold descriptors in uniform registers -- a lane-0-only loop pays an
+// elect / R2UR broadcast round per instruction (~100 cycles per MMA measured).
+__device__ __forceinline__ void tc_mma_bf16_warp(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                                 uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+__device__ __forceinline__ void tc_commit_warp(uint64_t* bar) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(smem_u32(bar))
+        : "memory");
+}
+
 // arrive on an mbarrier once all previously issued tcgen05.mma of this thread complete
 __device__ __forceinline__ void tc_commit(uint64_t* bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
@@ -226,9 +248,10 @@ __device__ __forceinline__ uint64_t sdesc_k_sw128(uint32_t saddr) {
     d |= (uint64_t)2u << 61;
     return d;
 }
-// instruction descriptor: D f32, A/B bf16, both K-major, M = 128, N = n
-__host__ __device__ __forceinline__ uint32_t idesc_bf16_m128(uint32_t n) {
-    return (1u << 4) | (1u << 7) | (1u << 10) | ((n >> 3) << 17) | ((128u >> 4) << 24);
+// instruction descriptor: D f32, A/B bf16, both K-major, M = m (64 or 128), N = n
+__host__ __device__ __forceinline__ uint32_t idesc_bf16(uint32_t m, uint32_t n) {
+    return (1u << 4) | (1u << 7) | (1u << 10) | ((n >> 3) << 17) | ((m >> 4) << 24);
 }
+__host__ __device__ __forceinline__ uint32_t idesc_bf16_m128(uint32_t n) { return idesc_bf16(128u, n); }
 
 }  // namespace el

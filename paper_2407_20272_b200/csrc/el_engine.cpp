@@ -102,6 +102,21 @@ CUtensorMap make_map(const void* base, int rows, int k, int box_rows) {
     return m;
 }
 
+// batch-M weight operand map: the tiled weight tensor viewed as [tiles][128 rows][64 cols] bf16
+// (no swizzle: the tiles are stored pre-swizzled), box = nt rows x kb_total consecutive tiles
+CUtensorMap make_bm_map(const void* base, size_t tiles, int nt, int kb_total) {
+    CUtensorMap m;
+    cuuint64_t dims[3] = {64, 128, (cuuint64_t)tiles};
+    cuuint64_t strides[2] = {128, 16384};
+    cuuint32_t box[3] = {64, (cuuint32_t)nt, (cuuint32_t)kb_total};
+    cuuint32_t es[3] = {1, 1, 1};
+    CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, es,
+                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) fail(EL_CUDA_ERROR, "cuTensorMapEncodeTiled (batch-M) failed (%d)", (int)r);
+    return m;
+}
+
 double threshold_at(double l0, double g, double lmin, int layer) {  // exit_policy.cpp:50-55
     return std::max(lmin, l0 * std::pow(g, layer - 1));
 }
@@ -157,7 +172,7 @@ struct el_engine {
             return true;
         }
         if (use_mega != 2) return use_mega == 1;
-        return B > 64 && cfg.technique != EL_TECH_SOFTMAX;
+        return B >= 64 && cfg.technique != EL_TECH_SOFTMAX;
     }
     int dbg = 0;
     int rec_cap = 4096;
@@ -197,11 +212,14 @@ struct el_engine {
     };
     std::map<int, Plans> plans;  // by n_pad
     std::map<int, el::IterPlan> mplans;  // persistent-kernel plans by n_pad
+    std::map<int, el::IterMaps> mmaps;   // their batch-M weight tensor maps
     DevBuf<float> mpart;                 // split-K partial workspace of the persistent kernel
     DevBuf<unsigned> mbar;               // its grid barrier (arrivals, generation)
     int mega_grid = 0, mega_att_stages = 2, sms = 148;
     int opt_mega_fill_splits = 0, opt_mega_att_stages = 0, opt_mega_pf = 0, opt_mega_kv_pf_mb = 0,
-        opt_mega_bm_max = 128, opt_attn_dyn_permille = 0, opt_attn_dyn_cb = 4;
+        opt_mega_bm_max = 128, opt_attn_dyn_permille = 0, opt_attn_dyn_cb = 4, opt_mega_bm_prefetch = 1,
+        opt_mega_bm_chunk_kb = 0, opt_mega_bm_act_policy = 0, opt_mega_bm_nt_min = 16,
+        opt_mega_bm_m128 = 0;
     int attn_cb = 1, attn_stages = 2, attn_max_chunks = 1, attn_grid = 148;
     int NR = 16;
 
@@ -533,10 +551,11 @@ struct el_engine {
         if (it != mplans.end()) return it->second;
         const int dp = dm.dp, fp = dm.fp, L = dm.L;
         const int cap = 227 * 1024 - el::iter_smem_fixed();
-        // attention ring: as many K|V|q stages as shared memory holds (<= 8)
+        // attention ring: 2 K|V|q stages (measured: 2 >= 3 >= 4 in the persistent kernel -- a
+        // smaller burst at phase start -- and it leaves room for the batch-M weight buffer)
         const int att_stage = el::attn_stage_bytes(dm);
         mega_att_stages = std::min(8, cap / att_stage);
-        if (opt_mega_att_stages) mega_att_stages = std::min(mega_att_stages, opt_mega_att_stages);
+        mega_att_stages = std::min(mega_att_stages, opt_mega_att_stages ? opt_mega_att_stages : 2);
         if (mega_att_stages < 2) fail(EL_INVALID_ARGUMENT, "persistent kernel: attention ring does not fit");
         mega_grid = sms;
         el::IterPlan P{};
@@ -569,7 +588,7 @@ struct el_engine {
             for (int k : {el::kIQkv, el::kIWo, el::kIUp, el::kIQc, el::kIWoc}) {
                 el::IterGemm& x = P.g[k];
                 const int F = x.m_tiles * 128;
-                int nt = 16;
+                int nt = opt_mega_bm_nt_min;
                 while (nt < 128 && F / nt > mega_grid) nt *= 2;
                 x.mode = 1;
                 x.nt = nt;
@@ -578,17 +597,30 @@ struct el_engine {
         }
         const int stage = 128 * 64 * 2 + n_pad * 128;
         P.stage_bytes = stage;
-        // batch-M ring: n_pad activation rows + nt weight rows per k-block (1 KB aligned regions)
-        P.stage2_boff = round_up(n_pad * 128, 1024);
-        P.stage2_bytes = P.stage2_boff + round_up(nt_max * 128, 1024);
-        // the MMA reads a full 16 KB A tile from each stage start: keep that inside the ring region
-        P.stages2 = std::min(16, (cap - el::kIterTbufBytes - 16384) / P.stage2_bytes);
+        // batch-M ring: stages of bm_kc activation k-blocks (NR rows each, ~32 KB per copy), then the
+        // unit's weights (nt_max rows x dp/64 k-blocks); 16 KB slack for the MMA's full-tile A reads
+        // The batch-M weight buffer sits at the end of the ring region (bm_woff), past the attention
+        // stages, the batch-M activation stages and the weight-streaming ring + LM transpose buffer,
+        // so a prefetch into it never collides with the phase in flight.
+        const bool bm = n_pad <= opt_mega_bm_max;
         const int ring_att = mega_att_stages * att_stage;
-        P.stages = std::min(8, (cap - el::kIterTbufBytes) / stage);
+        P.bm_rows = NR;
+        P.bm_kc = std::max(1, std::min(dp / 64, (opt_mega_bm_chunk_kb ? opt_mega_bm_chunk_kb * 1024 : 32768) / (NR * 128)));
+        P.bm_act_policy = opt_mega_bm_act_policy;
+        P.bm_m = (n_pad <= 64 && !opt_mega_bm_m128) ? 64 : 128;
+        P.bm_astage = P.bm_kc * NR * 128;
+        const int bm_w = bm ? (dp / 64) * nt_max * 128 : 0;
+        P.bm_woff = (cap - bm_w) / 1024 * 1024;
+        P.bm_stages = std::max(2, std::min(4, P.bm_woff / P.bm_astage));
+        if (bm && P.bm_stages * P.bm_astage > P.bm_woff)
+            fail(EL_INVALID_ARGUMENT, "persistent kernel: batch-M ring does not fit");
+        P.bm_prefetch = (bm && opt_mega_bm_prefetch && ring_att <= P.bm_woff) ? 1 : 0;
+        const int ws_cap = bm ? P.bm_woff : cap;  // weight-streaming ring + transpose buffer stay below it
+        P.stages = std::min(8, (ws_cap - el::kIterTbufBytes) / stage);
         if (P.stages < 2) fail(EL_INVALID_ARGUMENT, "persistent kernel: GEMM ring does not fit");
         P.gemm_ring = P.stages * stage;
         P.ring_bytes = round_up(std::max({ring_att, P.gemm_ring + el::kIterTbufBytes,
-                                          P.stages2 * P.stage2_bytes + 16384}), 1024);
+                                          P.bm_stages * P.bm_astage + 16384, bm ? P.bm_woff + bm_w : 0}), 1024);
         P.lm_tiles = dm.Vp / 128;
         if (el::iter_max_ctas_per_sm(dm, P.ring_bytes) < 1)
             fail(EL_CUDA_ERROR, "persistent kernel does not fit on an SM (%d bytes)", el::iter_smem_bytes(P.ring_bytes));
@@ -603,6 +635,13 @@ struct el_engine {
         }
         P.part = mpart.p;
         P.bar = mbar.p;
+        el::IterMaps MM{};
+        for (int k : {el::kIQkv, el::kIWo, el::kIUp, el::kIQc, el::kIWoc}) {
+            const el::IterGemm& x = P.g[k];
+            if (!x.mode || !x.A) continue;
+            MM.w[k] = make_bm_map(x.A, (size_t)L * x.layer_rows * x.kb_total, x.nt, x.kb_total);
+        }
+        mmaps[n_pad] = MM;
         P.pf_flags = opt_mega_pf & 1;
         // next-layer K/V into L2: a budget of opt_mega_kv_pf_mb MB spread over the grid
         const long long blk2 = 2LL * dm.bc * dp * 2;
@@ -615,7 +654,7 @@ struct el_engine {
         s.attn_stages = mega_att_stages;
         s.attn_dyn_permille = opt_attn_dyn_permille;
         s.attn_dyn_cb = opt_attn_dyn_cb;
-        el::launch_iter(s, P, mega_grid, stream);
+        el::launch_iter(s, P, mmaps[P.n_pad], mega_grid, stream);
     }
 
     el::DevState state(bool prefill, int B) {
@@ -1240,6 +1279,19 @@ int el_engine_set_option(el_engine* e, const char* key, int64_t v) {
     } else if (!std::strcmp(key, "attn_dyn_cb")) {
         if (v < 1 || v > 64) fail(EL_INVALID_ARGUMENT, "attn_dyn_cb must be in [1, 64]");
         e->opt_attn_dyn_cb = (int)v;
+    } else if (!std::strcmp(key, "mega_bm_chunk_kb") || !std::strcmp(key, "mega_bm_act_policy")) {
+        (key[8] == 'c' ? e->opt_mega_bm_chunk_kb : e->opt_mega_bm_act_policy) = (int)v;
+        e->mplans.clear();
+    } else if (!std::strcmp(key, "mega_bm_m128")) {
+        e->opt_mega_bm_m128 = v != 0;
+        e->mplans.clear();
+    } else if (!std::strcmp(key, "mega_bm_nt_min")) {
+        if (v != 16 && v != 32 && v != 64 && v != 128) fail(EL_INVALID_ARGUMENT, "mega_bm_nt_min: 16/32/64/128");
+        e->opt_mega_bm_nt_min = (int)v;
+        e->mplans.clear();
+    } else if (!std::strcmp(key, "mega_bm_prefetch")) {
+        e->opt_mega_bm_prefetch = v != 0;
+        e->mplans.clear();
     } else if (!std::strcmp(key, "mega_bm_max")) {
         e->opt_mega_bm_max = (int)v;
         e->mplans.clear();
@@ -1551,7 +1603,7 @@ int el_plan_info(el_engine* e, int64_t* out, int cap) {
                          M.g[el::kIQkv].mode, M.g[el::kIWo].mode, M.g[el::kIUp].mode,
                          M.g[el::kIQkv].splits, M.g[el::kIWo].splits, M.g[el::kIUp].splits, M.g[el::kIDown].splits,
                          M.g[el::kIFill].splits, M.g[el::kIQkv].nt, M.g[el::kIWo].nt, M.g[el::kIUp].nt,
-                         M.stages, M.stages2, e->mega_att_stages,
+                         M.stages, M.bm_stages, e->mega_att_stages,
                          e->mega_for(e->in_session ? e->sess_B : e->dm.Bmax) ? 1 : 0};
     const int n = (int)(sizeof v / sizeof v[0]);
     for (int i = 0; i < std::min(n, cap); ++i) out[i] = v[i];

@@ -30,7 +30,8 @@ constexpr int kProducerWarp = 8;
 struct IterSmem {
     AttnSmem att;  // attention ring barriers/descriptors (persist across layers)
     uint64_t full[8], empty[8], acc;
-    uint64_t full2[16], empty2[16];  // batch-M GEMM ring (small stages, deeper)
+    uint64_t full2[16], empty2[16];  // batch-M GEMM activation ring
+    uint64_t wfull;                  // batch-M unit weights (one tensor copy per unit)
     unsigned long long tdbg[4];
     uint32_t tmem;
     int pad0;
@@ -253,14 +254,14 @@ __device__ __forceinline__ void unit_mainloop(IterSmem& sm, uint8_t* ring, const
             }
         }
     } else if (warp == 0) {
-        if (lane == 0) {
+        {  // whole warp 0, one elected lane issues (uniform descriptors)
             const uint32_t idesc = idesc_bf16_m128(n_mma);
             uint32_t s = kseq % r.stages, ph = (kseq / r.stages) & 1;
             const uint32_t full0 = smem_u32(r.full), ring0 = smem_u32(ring);
 #pragma unroll 1
             for (int i = 0; i < nkb; ++i) {
                 mbar_wait_addr(full0 + 8 * s, ph);
-                if ((dbg & 64) && (i == 0 || i == nkb - 1)) {
+                if (lane == 0 && (dbg & 64) && (i == 0 || i == nkb - 1)) {
                     unsigned long long t;
                     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
                     sm.tdbg[i == 0 ? 0 : 1] = t;
@@ -272,15 +273,15 @@ __device__ __forceinline__ void unit_mainloop(IterSmem& sm, uint8_t* ring, const
                 if (!(dbg & (1 << 18)))
 #pragma unroll
                     for (int k = 0; k < kBK / 16; ++k)
-                        tc_mma_bf16(sm.tmem, ad + (uint64_t)(2 * k), bd + (uint64_t)(2 * k), idesc, (i | k) != 0);
-                tc_commit(&r.empty[s]);
+                        tc_mma_bf16_warp(sm.tmem, ad + (uint64_t)(2 * k), bd + (uint64_t)(2 * k), idesc, (i | k) != 0);
+                tc_commit_warp(&r.empty[s]);
                 if (++s == r.stages) {
                     s = 0;
                     ph ^= 1;
                 }
             }
             kseq += (uint32_t)nkb;
-            tc_commit(&sm.acc);
+            tc_commit_warp(&sm.acc);
         }
     }
     __syncwarp();
@@ -693,57 +694,178 @@ __device__ __forceinline__ void apply16_t(const DevState& st, const IterSmem& sm
     }
 }
 
+__device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map, uint32_t bar, int x, int y, int z,
+                                            uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(dst),
+        "l"(map), "r"(bar), "r"(x), "r"(y), "r"(z), "l"(policy)
+        : "memory");
+}
+
+// batch-M unit mainloop.  A unit's weights (nt rows x the whole reduction dim) arrive
+// with ONE 3-D tensor copy (rows f0..f0+nt of every k-block tile: the tiles are
+// pre-swizzled, so the raw bytes are ready UMMA operands); the activations (the
+// n_pad batch rows of all k-blocks, contiguous in the act layout) arrive in a few
+// large 1-D copies of bm_kc k-blocks each.  Few big copies instead of two per
+// k-block: a bulk copy costs ~60 ns of issue/processing on the SM's TMA unit
+// regardless of its size.
+__device__ __forceinline__ void unit_bm(IterSmem& sm, uint8_t* ring, const IterPlan& p, uint32_t& cseq,
+                                        uint32_t& wseq, const CUtensorMap* wmap, int wx, int wy, int wz,
+                                        const uint16_t* act, int kb_total, int nt, uint32_t useq, bool w_ready) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t NRb = (uint32_t)p.bm_rows * 128u;  // bytes of one activation k-block
+    const int nch = (kb_total + p.bm_kc - 1) / p.bm_kc;
+    const uint32_t ring0 = smem_u32(ring), wbase = ring0 + (uint32_t)p.bm_woff;
+    if (warp == kProducerWarp) {
+        if (lane == 0) {
+            if (!w_ready) {  // (else: prefetched into the weight buffer one phase ahead by bm_prefetch)
+                const uint32_t wf = smem_u32(&sm.wfull);
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(wf),
+                             "r"((uint32_t)(nt * 128 * kb_total))
+                             : "memory");
+                tma_load_3d(wbase, wmap, wf, wx, wy, wz, kL2EvictFirst);
+            }
+            uint32_t s = cseq % (uint32_t)p.bm_stages, ph = (cseq / (uint32_t)p.bm_stages) & 1;
+            bool wrapped = cseq >= (uint32_t)p.bm_stages;
+            const uint32_t full0 = smem_u32(sm.full2), empty0 = smem_u32(sm.empty2);
+#pragma unroll 1
+            for (int c = 0; c < nch; ++c) {
+                const int kc = min(p.bm_kc, kb_total - c * p.bm_kc);
+                if (wrapped) mbar_wait_addr(empty0 + 8 * s, ph ^ 1);
+                const uint32_t fb = full0 + 8 * s, bytes = (uint32_t)kc * NRb;
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(fb), "r"(bytes) : "memory");
+                bulk_load_hint(ring0 + s * (uint32_t)p.bm_astage, act + (size_t)c * p.bm_kc * p.bm_rows * kBK, bytes,
+                               fb, (p.bm_act_policy & 1) ? kL2EvictFirst : kL2EvictLast);
+                if (++s == (uint32_t)p.bm_stages) {
+                    s = 0;
+                    ph ^= 1;
+                    wrapped = true;
+                }
+            }
+            cseq += (uint32_t)nch;
+            ++wseq;
+        }
+    } else if (warp == 0) {
+        {  // whole warp 0, one elected lane issues (uniform descriptors)
+            // M = 64 when the batch fits (half the A-operand shared-memory reads of M = 128)
+            const uint32_t idesc = idesc_bf16((uint32_t)p.bm_m, (uint32_t)nt);
+            mbar_wait_addr(smem_u32(&sm.wfull), wseq & 1);
+            if (lane == 0) {
+                unsigned long long t;
+                asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+                sm.tdbg[3] = t;
+            }
+            uint32_t s = cseq % (uint32_t)p.bm_stages, ph = (cseq / (uint32_t)p.bm_stages) & 1;
+            const uint32_t full0 = smem_u32(sm.full2);
+            int kb = 0;
+#pragma unroll 1
+            for (int c = 0; c < nch; ++c) {
+                const int kc = min(p.bm_kc, kb_total - c * p.bm_kc);
+                mbar_wait_addr(full0 + 8 * s, ph);
+                if (lane == 0 && (c == 0 || c == nch - 1)) {
+                    unsigned long long t;
+                    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+                    sm.tdbg[c == 0 ? 1 : 2] = t;
+                }
+                tc_fence_after();
+#pragma unroll 1
+                for (int j = 0; j < kc; ++j, ++kb) {
+                    if (p.bm_act_policy & 2) continue;  // timing probe: no MMAs (wrong results)
+                    // rows >= n_pad of the A tile read the next k-block / stage / weights: ignored output rows
+                    const uint64_t ad = sdesc_k_sw128(ring0 + s * (uint32_t)p.bm_astage + (uint32_t)j * NRb);
+                    const uint64_t bd = sdesc_k_sw128(wbase + (uint32_t)(kb * nt * 128));
+#pragma unroll
+                    for (int k = 0; k < kBK / 16; ++k)
+                        tc_mma_bf16_warp(sm.tmem, ad + (uint64_t)(2 * k), bd + (uint64_t)(2 * k), idesc, (kb | k) != 0);
+                }
+                tc_commit_warp(&sm.empty2[s]);
+                if (++s == (uint32_t)p.bm_stages) {
+                    s = 0;
+                    ph ^= 1;
+                }
+            }
+            cseq += (uint32_t)nch;
+            ++wseq;
+            if (lane == 0) {
+                unsigned long long t;
+                asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+                sm.tdbg[0] = t;  // MMA issue finished
+            }
+            tc_commit_warp(&sm.acc);
+        }
+    }
+    __syncwarp();
+    if (warp < 8) {
+        mbar_wait(&sm.acc, useq & 1);
+        tc_fence_after();
+    }
+}
+
+// Weights of this CTA's first unit of batch-M GEMM `gid` at `layer`, issued one phase
+// ahead into the weight buffer (which lies outside the attention / GEMM rings) by the
+// producer lane; weights never depend on the previous phase, so their HBM latency
+// overlaps the phase in flight and the grid barrier.  Returns whether it issued.
+__device__ __forceinline__ bool bm_prefetch(IterSmem& sm, uint8_t* ring, const IterPlan& p, const IterMaps& maps,
+                                            int gid, int layer) {
+    const IterGemm& g = p.g[gid];
+    if (!g.mode || !p.bm_prefetch) return false;
+    if ((int)blockIdx.x >= g.m_tiles * kBM / g.nt) return false;
+    const int f0 = (int)blockIdx.x * g.nt;
+    const int row_block = (layer - 1) * g.layer_rows + g.row_off + f0 / kBM;
+    const uint32_t wf = smem_u32(&sm.wfull);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(wf),
+                 "r"((uint32_t)(g.nt * 128 * g.kb_total))
+                 : "memory");
+    tma_load_3d(smem_u32(ring) + (uint32_t)p.bm_woff, &maps.w[gid], wf, 0, f0 % kBM, row_block * g.kb_total,
+                kL2EvictFirst);
+    return true;
+}
+
 template <int K>
 __device__ __forceinline__ void gemm_phase_t(const DevState& st, IterSmem& sm, uint8_t* ring, const IterPlan& p,
-                                             const IterGemm& g, const IterCtx& x, const uint16_t* act,
-                                             uint32_t& kseq2, uint32_t& useq, int B) {
+                                             const IterMaps& maps, int gid, const IterCtx& x, const uint16_t* act,
+                                             uint32_t& cseq, uint32_t& wseq, uint32_t& useq, int B, bool& wpf,
+                                             int next_gid, int next_layer) {
+    const IterGemm& g = p.g[gid];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int U = g.m_tiles * kBM / g.nt;
     auto stamp = [&](int k) {  // dbg 64: per-CTA unit timeline of layer 1's batch-M GEMMs
-        if ((st.dbg & 64) && x.layer == 1 && (threadIdx.x & 31) == 0) {
+        if ((st.dbg & 64) && x.layer == 1 && threadIdx.x == 0) {
             unsigned long long t;
             asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
             st.dbg_ts[300000 + (size_t)blockIdx.x * 32 + K * 8 + k] = t;
         }
     };
-    if (threadIdx.x == 0) stamp(0);
+    stamp(0);
     for (int u = blockIdx.x; u < U; u += gridDim.x) {
         const int f0 = u * g.nt;
-        // weight rows [f0, f0 + nt) of every k-block: nt x 128 B inside the pre-swizzled 128-row tile
-        const uint16_t* w = g.A + (size_t)((x.layer - 1) * g.layer_rows + g.row_off + f0 / kBM) * g.kb_total *
-                                      (kBM * kBK) + (size_t)(f0 % kBM) * kBK;
-        // small stages: the A (batch) region holds only n_pad rows; the MMA's reads of rows >= n_pad run into
-        // the next stage (ignored output rows), so up to 16 k-blocks are in flight at once
-        const RingDesc r{sm.full2, sm.empty2, (uint32_t)p.stages2, (uint32_t)p.stage2_bytes, (uint32_t)p.stage2_boff};
-        // timing probes (wrong results): dbg 1<<16 reads weights from one fixed tile, 1<<17 activations from one k-block
-        const size_t wks = (st.dbg & (1 << 16)) ? 0 : (size_t)(kBM * kBK);
-        const size_t aks = (st.dbg & (1 << 17)) ? 0 : (size_t)st.NR * kBK;
-        unit_mainloop(sm, ring, r, kseq2, act, (uint32_t)p.n_pad * 128u, aks, w, (uint32_t)g.nt * 128u, wks, 0,
-                      g.kb_total, (uint32_t)g.nt, useq, kL2EvictLast, kL2EvictFirst,
-                      x.layer == 1 ? st.dbg : (st.dbg & ~64));
-        if (threadIdx.x == 0) {
-            stamp(2);
-            if ((st.dbg & 64) && x.layer == 1) {
-                st.dbg_ts[300000 + (size_t)blockIdx.x * 32 + K * 8 + 4] = sm.tdbg[0];
-                st.dbg_ts[300000 + (size_t)blockIdx.x * 32 + K * 8 + 5] = sm.tdbg[1];
-                st.dbg_ts[300000 + (size_t)blockIdx.x * 32 + K * 8 + 6] = sm.tdbg[0];
-                st.dbg_ts[300000 + (size_t)blockIdx.x * 32 + K * 8 + 7] = sm.tdbg[3];
-            }
-        }
+        const int row_block = (x.layer - 1) * g.layer_rows + g.row_off + f0 / kBM;
+        unit_bm(sm, ring, p, cseq, wseq, &maps.w[gid], 0, f0 % kBM, row_block * g.kb_total, act, g.kb_total, g.nt,
+                useq, wpf);
+        wpf = false;
+        stamp(2);
+        if ((st.dbg & 64) && x.layer == 1 && threadIdx.x == 0)
+            for (int k = 0; k < 4; ++k) st.dbg_ts[300000 + (size_t)blockIdx.x * 32 + K * 8 + 4 + k] = sm.tdbg[k];
         if (warp < 8) {
-            const int b = 32 * (warp & 3) + lane;
+            // M = 128: batch row b in TMEM lane b.  M = 64: rows 16q..16q+15 in lanes 32q..32q+15.
+            const bool m64 = p.bm_m == 64;
+            const int b = m64 ? 16 * (warp & 3) + lane : 32 * (warp & 3) + lane;
+            const bool valid = b < B && (!m64 || lane < 16);
             const uint32_t trow = sm.tmem + ((uint32_t)(32 * (warp & 3)) << 16);
             for (int c0 = 16 * (warp >> 2); c0 < g.nt; c0 += 32) {
                 float v[16];
                 tmem_ld16(trow + (uint32_t)c0, v);
-                if (b < B) apply16_t<K>(st, sm, x, b, f0 + c0, v);
+                if (valid) apply16_t<K>(st, sm, x, b, f0 + c0, v);
             }
         }
-        if (threadIdx.x == 0) stamp(3);
+        stamp(3);
         ++useq;
         tc_fence_before();
         __syncthreads();
     }
+    // this phase's MMAs are done: the weight buffer is free for the next batch-M GEMM's weights
+    if (next_gid >= 0 && threadIdx.x == kProducerWarp * 32) wpf = bm_prefetch(sm, ring, p, maps, next_gid, next_layer);
 }
 
 // weight-streaming GEMM phase: this CTA's units (u = cta, cta + G, ...)
@@ -765,7 +887,8 @@ __device__ __forceinline__ void gemm_phase(const DevState& st, IterSmem& sm, uin
 }
 
 template <int NJ>
-__global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(DevState st, IterPlan p) {
+__global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(DevState st, IterPlan p,
+                                                                const __grid_constant__ IterMaps maps) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* ring = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     IterSmem& sm = *reinterpret_cast<IterSmem*>(ring + p.ring_bytes);
@@ -786,6 +909,7 @@ __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(DevState st, Iter
             mbar_init(&sm.full2[s], 1);
             mbar_init(&sm.empty2[s], 1);
         }
+        mbar_init(&sm.wfull, 1);
         mbar_init(&sm.acc, 1);
         fence_barrier_init();
     }
@@ -803,14 +927,15 @@ __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(DevState st, Iter
     __syncthreads();
     tc_fence_after();
 
-    uint32_t kseq = 0, kseq2 = 0, useq = 0;
+    uint32_t kseq = 0, kseq2 = 0, wseq = 0, useq = 0;
+    bool wpf = false;  // producer lane: the next batch-M unit's weights were prefetched
     int aseq = 0, nbar = 0;
     if (st.dbg & 256)  // barrier cost probe: 32 back-to-back grid barriers
         for (int i = 0; i < 32; ++i) grid_sync(p, st, nbar, g0);
     if (st.dbg & (1 << 19)) {  // TMA probe: two QKV batch-M units back to back at kernel start
         const IterCtx x0{1, 0, 1};
         for (int rep = 0; rep < 2; ++rep) {
-            gemm_phase_t<kIQkv>(st, sm, ring, p, p.g[kIQkv], x0, st.hb, kseq2, useq, B);
+            gemm_phase_t<kIQkv>(st, sm, ring, p, maps, kIQkv, x0, st.hb, kseq2, wseq, useq, B, wpf, -1, 0);
             grid_sync(p, st, nbar, g0);
         }
     }
@@ -840,7 +965,8 @@ __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(DevState st, Iter
         const IterCtx x{layer, (layer - 1) & 1, layer & 1};
         // q | k | v, K/V appended to the paged pool (model.cpp:218-226)
         if (p.g[kIQkv].mode) {
-            gemm_phase_t<kIQkv>(st, sm, ring, p, p.g[kIQkv], x, st.hb + (size_t)x.pin * NR * dp, kseq2, useq, B);
+            gemm_phase_t<kIQkv>(st, sm, ring, p, maps, kIQkv, x, st.hb + (size_t)x.pin * NR * dp, kseq2, wseq, useq, B,
+                                wpf, -1, 0);
         } else {
             gemm_phase(st, sm, ring, p, p.g[kIQkv], layer, st.hb + (size_t)x.pin * NR * dp, kseq, useq, B);
             grid_sync(p, st, nbar, g0);
@@ -853,9 +979,13 @@ __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(DevState st, Iter
                 unsigned long long t;
                 asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
                 st.dbg_ts[40000 + (layer - 1) * 512 + cta * 2 + w] = t;
+                unsigned smid;
+                asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+                st.dbg_ts[40000 + 24 * 512 + cta] = smid;
             }
         };
         astamp(0);
+        if (tid == kProducerWarp * 32) wpf = bm_prefetch(sm, ring, p, maps, kIWo, layer);  // W_o under attention
         if (warp == kProducerWarp && (p.pf_flags & 1)) {  // this layer's W_o / up / down tiles -> L2
             l2_prefetch_gemm(p.g[kIWo], layer);
             l2_prefetch_gemm(p.g[kIUp], layer);
@@ -873,7 +1003,8 @@ __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(DevState st, Iter
         __syncwarp();
         // W_o + residual (model.cpp:245-253)
         if (p.g[kIWo].mode) {
-            gemm_phase_t<kIWo>(st, sm, ring, p, p.g[kIWo], x, st.att_b, kseq2, useq, B);
+            gemm_phase_t<kIWo>(st, sm, ring, p, maps, kIWo, x, st.att_b, kseq2, wseq, useq, B, wpf,
+                               st.enc_len > 0 ? (int)kIQc : (int)kIUp, layer);
         } else {
             gemm_phase(st, sm, ring, p, p.g[kIWo], layer, st.att_b, kseq, useq, B);
             grid_sync(p, st, nbar, g0);
@@ -883,18 +1014,21 @@ __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(DevState st, Iter
         if (st.enc_len > 0) {
             // T5 mode: mid += W_oc . softmax(q_c K_c^T / sqrt(d)) V_c, q_c = W_qc . mid
             if (p.g[kIQc].mode) {
-                gemm_phase_t<kIQkv>(st, sm, ring, p, p.g[kIQc], x, st.mid_b, kseq2, useq, B);  // q_c -> q32
+                gemm_phase_t<kIQkv>(st, sm, ring, p, maps, kIQc, x, st.mid_b, kseq2, wseq, useq, B, wpf, -1,
+                                    0);  // q_c -> q32
             } else {
                 gemm_phase(st, sm, ring, p, p.g[kIQc], layer, st.mid_b, kseq, useq, B);
                 grid_sync(p, st, nbar, g0);
                 reduce_phase<kIQkv>(st, sm, p, p.g[kIQc], x, B, 0, p.g[kIQc].m_tiles);
             }
             grid_sync(p, st, nbar, g0);
+            if (tid == kProducerWarp * 32) wpf = bm_prefetch(sm, ring, p, maps, kIWoc, layer);
             attn_body<NJ>(st, sm.att, ring, layer, aseq, true, cross_src);  // -> att_b
             grid_sync(p, st, nbar, g0);
             aseq = sm.att.seq_next;
             if (p.g[kIWoc].mode) {
-                gemm_phase_t<kIWoc>(st, sm, ring, p, p.g[kIWoc], x, st.att_b, kseq2, useq, B);
+                gemm_phase_t<kIWoc>(st, sm, ring, p, maps, kIWoc, x, st.att_b, kseq2, wseq, useq, B, wpf, kIUp,
+                                    layer);
             } else {
                 gemm_phase(st, sm, ring, p, p.g[kIWoc], layer, st.att_b, kseq, useq, B);
                 grid_sync(p, st, nbar, g0);
@@ -904,7 +1038,7 @@ __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(DevState st, Iter
         }
         // up + ReLU (model.cpp:255-260)
         if (p.g[kIUp].mode) {
-            gemm_phase_t<kIUp>(st, sm, ring, p, p.g[kIUp], x, st.mid_b, kseq2, useq, B);
+            gemm_phase_t<kIUp>(st, sm, ring, p, maps, kIUp, x, st.mid_b, kseq2, wseq, useq, B, wpf, -1, 0);
         } else {
             gemm_phase(st, sm, ring, p, p.g[kIUp], layer, st.mid_b, kseq, useq, B);
             grid_sync(p, st, nbar, g0);
@@ -915,6 +1049,7 @@ __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(DevState st, Iter
         gemm_phase(st, sm, ring, p, p.g[kIDown], layer, st.up_b, kseq, useq, B);
         grid_sync(p, st, nbar, g0);
         if (warp == kProducerWarp && layer < L && (p.pf_flags & 1)) l2_prefetch_gemm(p.g[kIQkv], layer + 1);
+        if (tid == kProducerWarp * 32 && layer < L) wpf = bm_prefetch(sm, ring, p, maps, kIQkv, layer + 1);
         reduce_phase<kIDown>(st, sm, p, p.g[kIDown], x, B, 0, p.g[kIDown].m_tiles);
         grid_sync(p, st, nbar, g0);
         if (st.technique == kSoftmax) {
@@ -944,6 +1079,18 @@ __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(DevState st, Iter
         }
         if (exit_decide(st, sm, layer, B)) {
             e_out = layer;
+            // the next layer's QKV weights were prefetched for nothing: retire that load
+            const IterGemm& gq = p.g[kIQkv];
+            if (layer < L && gq.mode && p.bm_prefetch && cta < gq.m_tiles * kBM / gq.nt) {
+                if (warp == 0) {  // the MMA warp retires it
+                    mbar_wait(&sm.wfull, wseq & 1);
+                    ++wseq;
+                }
+                if (tid == kProducerWarp * 32) {
+                    ++wseq;
+                    wpf = false;
+                }
+            }
             break;
         }
     }
@@ -1018,7 +1165,7 @@ __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(DevState st, Iter
 
 int iter_smem_bytes(int ring_bytes) { return 1024 + ring_bytes + (int)sizeof(IterSmem); }
 
-void launch_iter(const DevState& st, const IterPlan& p, int grid, cudaStream_t s) {
+void launch_iter(const DevState& st, const IterPlan& p, const IterMaps& maps, int grid, cudaStream_t s) {
     const int nj = (st.dm.dp / 8 + 31) / 32;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid);
@@ -1030,10 +1177,10 @@ void launch_iter(const DevState& st, const IterPlan& p, int grid, cudaStream_t s
     at[0].val.cooperative = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    if (nj <= 1) cudaLaunchKernelEx(&cfg, iter_kernel<1>, st, p);
-    else if (nj == 2) cudaLaunchKernelEx(&cfg, iter_kernel<2>, st, p);
-    else if (nj == 3) cudaLaunchKernelEx(&cfg, iter_kernel<3>, st, p);
-    else cudaLaunchKernelEx(&cfg, iter_kernel<4>, st, p);
+    if (nj <= 1) cudaLaunchKernelEx(&cfg, iter_kernel<1>, st, p, maps);
+    else if (nj == 2) cudaLaunchKernelEx(&cfg, iter_kernel<2>, st, p, maps);
+    else if (nj == 3) cudaLaunchKernelEx(&cfg, iter_kernel<3>, st, p, maps);
+    else cudaLaunchKernelEx(&cfg, iter_kernel<4>, st, p, maps);
     EL_CUDA_LAUNCH_CHECK();
 }
 

@@ -192,7 +192,12 @@ struct IterPlan {
     int n_pad;       // MMA N: batch rounded up to 16
     int stages;      // GEMM ring depth
     int stage_bytes; // GEMM ring stage stride (A region 16 KB | B region)
-    int stages2, stage2_bytes, stage2_boff;  // batch-M ring: depth, stride, offset of the weight region
+    // batch-M ring: bm_stages stages of bm_kc activation k-blocks (bm_astage bytes each, bm_rows
+    // batch rows per k-block), the unit's weights at bm_woff
+    int bm_rows, bm_kc, bm_astage, bm_stages, bm_woff;
+    int bm_prefetch;  // issue each batch-M unit's weights one phase ahead (weight buffer outside the rings)
+    int bm_act_policy;  // L2 hint of the activation copies: 0 evict-last, 1 evict-first (probe)
+    int bm_m;           // UMMA M of the batch-M GEMMs: 64 (batch <= 64) or 128
     int ring_bytes;  // shared ring region (attention stages / GEMM stages + LM transpose buffer)
     int gemm_ring;   // bytes of the GEMM stages inside the ring region
     int lm_tiles;    // Vp / 128
@@ -202,11 +207,16 @@ struct IterPlan {
     unsigned* bar;   // grid barrier: [0] arrivals, [32] generation
 };
 
+// 3-D (64 x 128 rows x tiles, no swizzle: the tiles are pre-swizzled) tensor maps over the
+// batch-M GEMMs' weights, box = nt rows x all k-blocks (one copy per unit)
+struct alignas(64) IterMaps {
+    CUtensorMap w[kINumGemm];
+};
 int iter_smem_bytes(int ring_bytes);   // dynamic shared memory of the launch
 int iter_smem_fixed();                 // bytes outside the ring region (alignment slack + control block)
 int iter_max_ctas_per_sm(const Dims& dm, int ring_bytes);
 void init_iter_attributes();
-void launch_iter(const DevState& st, const IterPlan& p, int grid, cudaStream_t s);
+void launch_iter(const DevState& st, const IterPlan& p, const IterMaps& maps, int grid, cudaStream_t s);
 constexpr int kIterTbufBytes = 32 * 129 * 4;
 
 // host+device mirror of the allocator arithmetic (used by el_kv_block_trace)

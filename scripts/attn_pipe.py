@@ -12,7 +12,7 @@ DIMS = {"c2": (12, 768, 64), "c5": (24, 1024, 256)}
 L, d, B = DIMS[sys.argv[1] if len(sys.argv) > 1 else "c2"]
 cfg = X.EngineConfig(model=X.ModelConfig(L, d, 32128, 0), technique=X.ExitTechnique("always_at", 1), max_batch=B,
                      pool_blocks=B * L * 42, eos_token=-1)
-e = X.Engine(cfg)
+e = X.Engine(cfg, mega=True)
 e.session_begin(np.arange(B) + 1, 511, 660, 1)
 lib = X.lib()
 lib.el_debug_timestamps.argtypes = [C.c_void_p, C.c_void_p, C.c_int]

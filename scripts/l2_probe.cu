@@ -109,6 +109,12 @@ __global__ void probe(const uint8_t* src, size_t stride, int mode, int nk, uint3
     }
 }
 
+// every CTA writes a slice of the buffer with generic stores (like an epilogue producing activations)
+__global__ void writer(uint8_t* buf, size_t bytes, int val) {
+    for (size_t i = (blockIdx.x * (size_t)blockDim.x + threadIdx.x) * 16; i < bytes; i += (size_t)gridDim.x * blockDim.x * 16)
+        *reinterpret_cast<uint4*>(buf + i) = make_uint4(val, val, val, val);
+}
+
 int main() {
     int sms;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
@@ -190,6 +196,17 @@ int main() {
         std::sort(all.begin(), all.end());
         printf("batch-M pattern 12x(8KB L2 + 2KB HBM) spin=%d coop=%d: first p50 %.2f | all p50 %.2f max %.2f us\n", spin & 1, spin >> 1,
                first[sms / 2], all[sms / 2], all.back());
+    }
+    // freshly written vs clean: 3 x 32 KB same-address copies per CTA
+    for (int fresh : {0, 1, 0, 1}) {
+        if (fresh) writer<<<sms, 256>>>(buf, 96 * 1024, 7);
+        probe<<<sms, 128, 200 * 1024>>>(buf, 0, 0, 3, 32768, out);
+        cudaDeviceSynchronize();
+        cudaMemcpy(h.data(), out, sms * 4 * 8, cudaMemcpyDeviceToHost);
+        std::vector<double> all;
+        for (int i = 0; i < sms; ++i) all.push_back((h[i * 4 + 2] - h[i * 4]) / 1e3);
+        std::sort(all.begin(), all.end());
+        printf("same 3x32KB (L2) %s: all p50 %.2f max %.2f us\n", fresh ? "FRESHLY WRITTEN" : "clean", all[sms / 2], all.back());
     }
     printf("%s\n", cudaGetErrorString(cudaGetLastError()));
     return 0;

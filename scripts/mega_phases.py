@@ -19,7 +19,7 @@ L, d, B = DIMS[cfgname]
 cfg = X.EngineConfig(model=X.ModelConfig(L, d, 32128, 0), technique=X.ExitTechnique(tech, 4),
                      schedule=X.ThresholdSchedule(0.981, 0.997, 0.0), max_batch=B, pool_blocks=B * L * 40,
                      eos_token=-1)
-e = X.Engine(cfg)
+e = X.Engine(cfg, mega=True)
 for kk, v in opts.items():
     if kk != "xdbg":
         e.set_option(kk, v)
@@ -83,20 +83,22 @@ for layer in (0, eo - 1):
 
 # batch-M GEMM unit timeline of layer 1 (dbg 64): [start, -, acc ready, epilogue done] per CTA
 U = ts[300000:300000 + 148 * 32].reshape(148, 4, 8).astype(np.float64)
+arrv = ts[65536:65536 + 148 * 1024].reshape(148, 1024).astype(np.float64)
 for k, nm in ((0, "qkv"), (1, "wo"), (2, "up")):
     u = U[:, k]
     ok = (u[:, 0] > 0) & (u[:, 2] > 0)
     if not ok.any():
         continue
     t0 = u[ok, 0].min()
+    st_ = (u[ok, 0] - t0) / 1e3
     acc = (u[ok, 2] - u[ok, 0]) / 1e3
     epi = (u[ok, 3] - u[ok, 2]) / 1e3
-    f1 = (u[ok, 4] - u[ok, 0]) / 1e3
-    fl = (u[ok, 5] - u[ok, 0]) / 1e3
-    i0 = (u[ok, 6] - u[ok, 0]) / 1e3
-    i1 = (u[ok, 7] - u[ok, 0]) / 1e3
-    print(f"{nm}: producer issued first at p50 {np.median(i0):.2f} last at p50 {np.median(i1):.2f} max {i1.max():.2f}")
-    print(f"{nm}: first stage full p50 {np.median(f1):.2f} max {f1.max():.2f}; last stage full p50 {np.median(fl):.2f} "
-          f"max {fl.max():.2f}")
-    print(f"{nm}: start skew {(u[ok, 0].max() - t0) / 1e3:.2f} us; start->acc min {acc.min():.2f} p50 {np.median(acc):.2f} "
-          f"max {acc.max():.2f}; epilogue p50 {np.median(epi):.2f} max {epi.max():.2f}; last done {(u[ok, 3].max() - t0) / 1e3:.2f}")
+    # this CTA's arrival at the next grid barrier (first arrival stamp after its epilogue)
+    arr = np.array([min([a for a in arrv[c] if a >= u[c, 3]] or [np.nan]) for c in np.where(ok)[0]])
+    tail = (arr - u[ok, 3]) / 1e3
+    rel = lambda j: (u[ok, j] - u[ok, 0]) / 1e3
+    print(f"{nm}: MMA issue done p50 {np.median(rel(4)):.2f} | weights ready p50 {np.median(rel(7)):.2f} | chunk0 full p50 "
+          f"{np.median(rel(5)):.2f} | last chunk full p50 {np.median(rel(6)):.2f} max {rel(6).max():.2f}")
+    print(f"{nm}: start skew p50 {np.median(st_):.2f} max {st_.max():.2f} | start->acc p50 {np.median(acc):.2f} max "
+          f"{acc.max():.2f} | epilogue p50 {np.median(epi):.2f} max {epi.max():.2f} | epi->arrive p50 "
+          f"{np.nanmedian(tail):.2f} max {np.nanmax(tail):.2f} | last arrival {(np.nanmax(arr) - t0) / 1e3:.2f} us")

@@ -17,7 +17,7 @@ for tech in techs:
     cfg = X.EngineConfig(model=X.ModelConfig(L, d, 32128, 0), technique=X.ExitTechnique(tech, 4),
                          schedule=X.ThresholdSchedule(0.981, 0.997, 0.0), max_batch=B, pool_blocks=B * L * 42,
                          eos_token=-1)
-    e = X.Engine(cfg)
+    e = X.Engine(cfg, mega=True)
     for v in variants:
         for k, x in v.items():
             e.set_option(k, x)
