@@ -219,7 +219,7 @@ struct el_engine {
     int opt_mega_fill_splits = 0, opt_mega_att_stages = 0, opt_mega_pf = 0, opt_mega_kv_pf_mb = 0,
         opt_mega_bm_max = 128, opt_attn_dyn_permille = 0, opt_attn_dyn_cb = 4, opt_mega_bm_prefetch = 1,
         opt_mega_bm_chunk_kb = 0, opt_mega_bm_act_policy = 0, opt_mega_bm_nt_min = 16,
-        opt_mega_bm_m128 = 0;
+        opt_mega_bm_m128 = 0, opt_mega_bm_down = 0;
     int attn_cb = 1, attn_stages = 2, attn_max_chunks = 1, attn_grid = 148;
     int NR = 16;
 
@@ -397,7 +397,7 @@ struct el_engine {
         attn_queue.alloc(4);
         lm_part.alloc((size_t)(dm.Vp / 128) * Bm);
         dbg_ts.alloc(65536 + 256 * 1024);
-        exit_part.alloc((size_t)(dp / 128 + 1) * Bm * 3);
+        exit_part.alloc((size_t)(dp / 16 + 1) * Bm * 3);  // per 128-row tile (split-K) or 16-feature slice (batch-M)
         for (DevBuf<int>* b : {&layer, &out_layer, &exit_cnt, &iter_counter, &cur_iter}) b->alloc(4);
         status.alloc((size_t)Bm);
         first_accept.alloc((size_t)Bm);
@@ -583,16 +583,18 @@ struct el_engine {
         P.g[el::kIFill] = g(wqkv.p, 2 * dp / 128, dp / 64, 3 * dp / 128, dp / 128, fs);
         P.n_pad = n_pad;
         // batch-M full-K GEMMs (no split-K reduce phase) for QKV / W_o / up at small batch
-        int nt_max = 16;
+        int nt_max = 16, bm_w = 0;  // bm_w: the largest unit weight slab (nt rows x K)
         if (n_pad <= opt_mega_bm_max) {
-            for (int k : {el::kIQkv, el::kIWo, el::kIUp, el::kIQc, el::kIWoc}) {
+            for (int k : {el::kIQkv, el::kIWo, el::kIUp, el::kIQc, el::kIWoc, el::kIDown}) {
+                // down (K = 4d): batch-M only at batch <= 64, where its 16-row weight slab fits
+                if (k == el::kIDown && (n_pad > 64 || !opt_mega_bm_down)) continue;
                 el::IterGemm& x = P.g[k];
                 const int F = x.m_tiles * 128;
-                int nt = opt_mega_bm_nt_min;
+                int nt = k == el::kIDown ? 16 : opt_mega_bm_nt_min;
                 while (nt < 128 && F / nt > mega_grid) nt *= 2;
                 x.mode = 1;
                 x.nt = nt;
-                nt_max = std::max(nt_max, nt);
+                bm_w = std::max(bm_w, x.kb_total * nt * 128);
             }
         }
         const int stage = 128 * 64 * 2 + n_pad * 128;
@@ -609,9 +611,9 @@ struct el_engine {
         P.bm_act_policy = opt_mega_bm_act_policy;
         P.bm_m = (n_pad <= 64 && !opt_mega_bm_m128) ? 64 : 128;
         P.bm_astage = P.bm_kc * NR * 128;
-        const int bm_w = bm ? (dp / 64) * nt_max * 128 : 0;
+        (void)nt_max;
         P.bm_woff = (cap - bm_w) / 1024 * 1024;
-        P.bm_stages = std::max(2, std::min(4, P.bm_woff / P.bm_astage));
+        P.bm_stages = std::max(2, std::min(4, (P.bm_woff - 16384) / P.bm_astage));
         if (bm && P.bm_stages * P.bm_astage > P.bm_woff)
             fail(EL_INVALID_ARGUMENT, "persistent kernel: batch-M ring does not fit");
         P.bm_prefetch = (bm && opt_mega_bm_prefetch && ring_att <= P.bm_woff) ? 1 : 0;
@@ -636,7 +638,7 @@ struct el_engine {
         P.part = mpart.p;
         P.bar = mbar.p;
         el::IterMaps MM{};
-        for (int k : {el::kIQkv, el::kIWo, el::kIUp, el::kIQc, el::kIWoc}) {
+        for (int k : {el::kIQkv, el::kIWo, el::kIUp, el::kIQc, el::kIWoc, el::kIDown}) {
             const el::IterGemm& x = P.g[k];
             if (!x.mode || !x.A) continue;
             MM.w[k] = make_bm_map(x.A, (size_t)L * x.layer_rows * x.kb_total, x.nt, x.kb_total);
@@ -1281,6 +1283,9 @@ int el_engine_set_option(el_engine* e, const char* key, int64_t v) {
         e->opt_attn_dyn_cb = (int)v;
     } else if (!std::strcmp(key, "mega_bm_chunk_kb") || !std::strcmp(key, "mega_bm_act_policy")) {
         (key[8] == 'c' ? e->opt_mega_bm_chunk_kb : e->opt_mega_bm_act_policy) = (int)v;
+        e->mplans.clear();
+    } else if (!std::strcmp(key, "mega_bm_down")) {
+        e->opt_mega_bm_down = v != 0;
         e->mplans.clear();
     } else if (!std::strcmp(key, "mega_bm_m128")) {
         e->opt_mega_bm_m128 = v != 0;

@@ -567,8 +567,8 @@ __device__ void reduce_phase(const DevState& st, const IterSmem& sm, const IterP
 
 // exit decision of `layer` for every row, computed identically by every CTA
 // (exit_policy.cpp:89-115, engine.cpp:55-66); returns "stop here".
-__device__ bool exit_decide(const DevState& st, IterSmem& sm, int layer, int B) {
-    const int tid = threadIdx.x, Bm = st.dm.Bmax, mt = st.dm.dp / kBM;
+__device__ bool exit_decide(const DevState& st, IterSmem& sm, int layer, int B, int mt) {
+    const int tid = threadIdx.x, Bm = st.dm.Bmax;
     int all = 1;
     if (tid < B) {
         const int b = tid;
@@ -685,6 +685,49 @@ __device__ __forceinline__ void apply16_t(const DevState& st, const IterSmem& sm
         for (int t = 0; t < 4; ++t) m4[t] = make_float4(o[4 * t], o[4 * t + 1], o[4 * t + 2], o[4 * t + 3]);
         *reinterpret_cast<uint4*>(st.mid_b + act_offset(b, f, NR)) = pack(o);
         *reinterpret_cast<uint4*>(st.mid_b + act_offset(b, f + 8, NR)) = pack(o + 8);
+    } else if constexpr (K == kIDown) {  // down + residual -> h_l; exit-check partial dots of these 16 features
+        const size_t i = (size_t)b * dp + f;
+        const float4* m4 = reinterpret_cast<const float4*>(st.mid32 + i);
+        float o[16];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            const float4 hv = __ldcg(m4 + t);
+            o[4 * t] = hv.x + v[4 * t];
+            o[4 * t + 1] = hv.y + v[4 * t + 1];
+            o[4 * t + 2] = hv.z + v[4 * t + 2];
+            o[4 * t + 3] = hv.w + v[4 * t + 3];
+        }
+        float4* h4 = reinterpret_cast<float4*>(st.h32 + (size_t)x.pout * Bm * dp + i);
+#pragma unroll
+        for (int t = 0; t < 4; ++t) h4[t] = make_float4(o[4 * t], o[4 * t + 1], o[4 * t + 2], o[4 * t + 3]);
+        uint16_t* hb = st.hb + (size_t)x.pout * NR * dp;
+        *reinterpret_cast<uint4*>(hb + act_offset(b, f, NR)) = pack(o);
+        *reinterpret_cast<uint4*>(hb + act_offset(b, f + 8, NR)) = pack(o + 8);
+        if (st.technique == kState || st.technique == kClassifier) {
+            double x0 = 0.0, x1 = 0.0, x2 = 0.0;
+            if (st.technique == kState) {
+                const float4* p4 = reinterpret_cast<const float4*>(st.h32 + (size_t)x.pin * Bm * dp + i);
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                    const float4 hv = __ldcg(p4 + t);
+                    const float hp[4] = {hv.x, hv.y, hv.z, hv.w};
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const double a = hp[q], c = o[4 * t + q];
+                        x0 += a * c;
+                        x1 += a * a;
+                        x2 += c * c;
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int t = 0; t < 16; ++t) x0 += (double)__ldg(&st.probe_w[f + t]) * (double)o[t];
+            }
+            double* q = st.exit_part + ((size_t)(f >> 4) * Bm + b) * 3;  // one partial per 16-feature slice
+            q[0] = x0;
+            q[1] = x1;
+            q[2] = x2;
+        }
     } else if constexpr (K == kIUp) {
         float o[16];
 #pragma unroll
@@ -1038,7 +1081,8 @@ __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(DevState st, Iter
         }
         // up + ReLU (model.cpp:255-260)
         if (p.g[kIUp].mode) {
-            gemm_phase_t<kIUp>(st, sm, ring, p, maps, kIUp, x, st.mid_b, kseq2, wseq, useq, B, wpf, -1, 0);
+            gemm_phase_t<kIUp>(st, sm, ring, p, maps, kIUp, x, st.mid_b, kseq2, wseq, useq, B, wpf,
+                               p.g[kIDown].mode ? (int)kIDown : -1, layer);
         } else {
             gemm_phase(st, sm, ring, p, p.g[kIUp], layer, st.mid_b, kseq, useq, B);
             grid_sync(p, st, nbar, g0);
@@ -1046,11 +1090,16 @@ __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(DevState st, Iter
         }
         grid_sync(p, st, nbar, g0);
         // down + residual (model.cpp:261-270) + exit-check partial dots
-        gemm_phase(st, sm, ring, p, p.g[kIDown], layer, st.up_b, kseq, useq, B);
-        grid_sync(p, st, nbar, g0);
-        if (warp == kProducerWarp && layer < L && (p.pf_flags & 1)) l2_prefetch_gemm(p.g[kIQkv], layer + 1);
-        if (tid == kProducerWarp * 32 && layer < L) wpf = bm_prefetch(sm, ring, p, maps, kIQkv, layer + 1);
-        reduce_phase<kIDown>(st, sm, p, p.g[kIDown], x, B, 0, p.g[kIDown].m_tiles);
+        if (p.g[kIDown].mode) {
+            gemm_phase_t<kIDown>(st, sm, ring, p, maps, kIDown, x, st.up_b, kseq2, wseq, useq, B, wpf,
+                                 layer < L ? (int)kIQkv : -1, layer + 1);
+        } else {
+            gemm_phase(st, sm, ring, p, p.g[kIDown], layer, st.up_b, kseq, useq, B);
+            grid_sync(p, st, nbar, g0);
+            if (warp == kProducerWarp && layer < L && (p.pf_flags & 1)) l2_prefetch_gemm(p.g[kIQkv], layer + 1);
+            if (tid == kProducerWarp * 32 && layer < L) wpf = bm_prefetch(sm, ring, p, maps, kIQkv, layer + 1);
+            reduce_phase<kIDown>(st, sm, p, p.g[kIDown], x, B, 0, p.g[kIDown].m_tiles);
+        }
         grid_sync(p, st, nbar, g0);
         if (st.technique == kSoftmax) {
             // LM head over h_l with the fused (max1, max2, sum exp) reduction
@@ -1077,7 +1126,7 @@ __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(DevState st, Iter
                 }
             grid_sync(p, st, nbar, g0);
         }
-        if (exit_decide(st, sm, layer, B)) {
+        if (exit_decide(st, sm, layer, B, p.g[kIDown].mode ? st.dm.dp / 16 : st.dm.dp / kBM)) {
             e_out = layer;
             // the next layer's QKV weights were prefetched for nothing: retire that load
             const IterGemm& gq = p.g[kIQkv];
