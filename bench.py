@@ -312,7 +312,9 @@ def run_ours(args, rank, world, local_rank, dist):
                                "launch_ms": round(attn_ms, 5),
                                "traffic": traffic_of(f"attn_traffic_{args.config}.json")},
         "e2e": {"value": round(B * world * args.steps / e2e_s, 1), "unit": "tokens/s",
-                "h2d_bytes_per_step": B * 4, "d2h_bytes_per_step": B * 4 * 2 + 4 + L * B * 4},
+                "h2d_bytes_per_step": B * 4,
+                # one packed record per step: tokens, accept, output layer, per-layer confidences
+                "d2h_bytes_per_step": 4 * (-(-(2 * B + 4 + L * B) // 32) * 32)},
         "gpu_launches": launches,
         "clocks": clk.summary(),
         "plan": plan,

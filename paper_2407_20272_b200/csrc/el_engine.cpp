@@ -194,10 +194,12 @@ struct el_engine {
     // rows
     DevBuf<int> row_slot, row_pos, row_tok, pf_slot, pf_pos, pf_tok, seq_ids_dev;
     // activations / workspaces
-    DevBuf<float> h32, q32, mid32, attn_o, attn_ml, conf, rec_conf;
+    DevBuf<float> h32, q32, mid32, attn_o, attn_ml, conf;
     DevBuf<uint16_t> hb, att_b, mid_b, up_b;
     DevBuf<int> attn_cnt, attn_queue, layer, out_layer, status, first_accept, accept, exit_cnt, iter_counter,
-        cur_iter, rec_tok, rec_acc, rec_out;
+        cur_iter, rec;
+    int rec_stride = 0;
+    int* rec_host = nullptr;  // pinned staging for one packed record
     DevBuf<float4> lm_part;
     DevBuf<double> lambdas, exit_part;
     DevBuf<unsigned long long> dbg_ts;
@@ -243,6 +245,7 @@ struct el_engine {
             if (kv.second.g) cudaGraphDestroy(kv.second.g);
         }
         if (cont_host) cudaFreeHost(cont_host);
+        if (rec_host) cudaFreeHost(rec_host);
         if (ev_fork) cudaEventDestroy(ev_fork);
         if (ev_join) cudaEventDestroy(ev_join);
         if (stream2) cudaStreamDestroy(stream2);
@@ -404,10 +407,9 @@ struct el_engine {
         accept.alloc((size_t)Bm);
         conf.alloc((size_t)L * Bm);
         fixed_conf.alloc((size_t)L * Bm);
-        rec_tok.alloc((size_t)rec_cap * Bm);
-        rec_acc.alloc((size_t)rec_cap * Bm);
-        rec_out.alloc((size_t)rec_cap);
-        rec_conf.alloc((size_t)rec_cap * L * Bm);
+        rec_stride = round_up(2 * Bm + 4 + L * Bm, 32);
+        rec.alloc((size_t)rec_cap * rec_stride);
+        CK(cudaHostAlloc(&rec_host, sizeof(int) * rec_stride, cudaHostAllocDefault));
         {
             std::vector<double> lam((size_t)L);
             for (int l = 1; l <= L; ++l) lam[(size_t)l - 1] = threshold_at(cfg.lambda0, cfg.gamma, cfg.lambda_min, l);
@@ -687,7 +689,7 @@ struct el_engine {
         s.use_cond = 0;
         s.iter_counter = prefill ? cur_iter.p + 1 : iter_counter.p;  // prefill: scratch counter
         s.cur_iter = prefill ? cur_iter.p + 2 : cur_iter.p;
-        s.rec_tok = rec_tok.p; s.rec_acc = rec_acc.p; s.rec_out = rec_out.p; s.rec_conf = rec_conf.p;
+        s.rec = rec.p; s.rec_stride = rec_stride;
         s.rec_cap = rec_cap;
         s.enc_len = cfg.encoder_len;
         s.enc_blocks = enc_blocks;
@@ -884,14 +886,14 @@ struct el_engine {
     IterOut read_iteration(int iter_index, int B) {
         IterOut o;
         const int cur = iter_index % rec_cap, Bm = dm.Bmax, L = dm.L;
-        o.tok.resize((size_t)B);
-        o.acc.resize((size_t)B);
-        std::vector<float> cf((size_t)L * Bm);
-        CK(cudaMemcpyAsync(o.tok.data(), rec_tok.p + (size_t)cur * Bm, sizeof(int) * B, cudaMemcpyDeviceToHost, stream));
-        CK(cudaMemcpyAsync(o.acc.data(), rec_acc.p + (size_t)cur * Bm, sizeof(int) * B, cudaMemcpyDeviceToHost, stream));
-        CK(cudaMemcpyAsync(&o.out_layer, rec_out.p + cur, sizeof(int), cudaMemcpyDeviceToHost, stream));
-        CK(cudaMemcpyAsync(cf.data(), rec_conf.p + (size_t)cur * L * Bm, sizeof(float) * L * Bm, cudaMemcpyDeviceToHost, stream));
+        // the whole packed record in one copy through pinned staging
+        CK(cudaMemcpyAsync(rec_host, rec.p + (size_t)cur * rec_stride, sizeof(int) * rec_stride, cudaMemcpyDeviceToHost,
+                           stream));
         CK(cudaStreamSynchronize(stream));
+        o.tok.assign(rec_host, rec_host + B);
+        o.acc.assign(rec_host + Bm, rec_host + Bm + B);
+        o.out_layer = rec_host[2 * Bm];
+        const float* cf = reinterpret_cast<const float*>(rec_host + 2 * Bm + 4);
         o.conf.resize((size_t)L * B);
         for (int l = 0; l < L; ++l)
             for (int b = 0; b < B; ++b) o.conf[(size_t)l * B + b] = cf[(size_t)l * Bm + b];
@@ -1347,10 +1349,7 @@ int el_engine_set_option(el_engine* e, const char* key, int64_t v) {
     else if (!std::strcmp(key, "rec_cap")) {
         if (v < 1) fail(EL_INVALID_ARGUMENT, "rec_cap must be >= 1");
         e->rec_cap = (int)v;
-        e->rec_tok.alloc((size_t)v * e->dm.Bmax);
-        e->rec_acc.alloc((size_t)v * e->dm.Bmax);
-        e->rec_out.alloc((size_t)v);
-        e->rec_conf.alloc((size_t)v * e->dm.L * e->dm.Bmax);
+        e->rec.alloc((size_t)v * e->rec_stride);
         e->invalidate_graphs();
     } else fail(EL_INVALID_ARGUMENT, "unknown option %s", key);
     API_END

@@ -1187,11 +1187,11 @@ __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(DevState st, Iter
         for (int b = cta + G * warp; b < B; b += G * 8) {
             const LmPart r = lm_col_warp(st, b);
             for (int l = lane; l < L; l += 32)
-                st.rec_conf[((size_t)cur * L + l) * Bm + b] = __ldcg(&st.conf[(size_t)l * Bm + b]);
+                rec_conf(st, cur)[(size_t)l * Bm + b] = __ldcg(&st.conf[(size_t)l * Bm + b]);
             if (lane == 0) {
                 const int fa = sm.first[b];
-                st.rec_tok[(size_t)cur * Bm + b] = r.idx;
-                st.rec_acc[(size_t)cur * Bm + b] = fa ? fa : L;
+                rec_rec(st, cur)[b] = r.idx;
+                rec_rec(st, cur)[Bm + b] = fa ? fa : L;
                 st.rows.tok[b] = r.idx;       // next input (engine.cpp:304)
                 st.rows.pos[b] = sm.pos[b] + 1;  // KvStore::commit (engine.cpp:262-264)
             }
@@ -1201,7 +1201,7 @@ __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(DevState st, Iter
         if (st.attn_queue) st.attn_queue[1] = 0;  // layer 1 of the next launch (layer 2's is rearmed in layer 1)
         if (!(st.dbg & (2048 | 4096 | 32768))) *(volatile unsigned*)p.bar = 0u;  // arrivals of this launch are all in
         if (st.dbg & (4096 | 32768)) *(volatile unsigned*)(p.bar + 1025) = g0 + (unsigned)nbar;  // flag epochs continue
-        st.rec_out[iter % st.rec_cap] = e_out;
+        rec_rec(st, iter % st.rec_cap)[2 * Bm] = e_out;
         *st.out_layer = e_out;
         *st.layer = e_out + 1;
         *st.cur_iter = iter;

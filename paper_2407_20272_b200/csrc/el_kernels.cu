@@ -1435,12 +1435,12 @@ __global__ void __launch_bounds__(256) finish_kernel(DevState st) {
     const LmRed r = lm_reduce_col(st, b);
     const int cur = *st.cur_iter % st.rec_cap;
     for (int l = tid; l < L; l += blockDim.x)
-        st.rec_conf[((size_t)cur * L + l) * Bm + b] = st.conf[(size_t)l * Bm + b];
+        rec_conf(st, cur)[(size_t)l * Bm + b] = st.conf[(size_t)l * Bm + b];
     if (tid == 0) {
         const int fa = st.first_accept[b];
-        st.rec_tok[(size_t)cur * Bm + b] = r.idx;
-        st.rec_acc[(size_t)cur * Bm + b] = fa ? fa : L;
-        if (b == 0) st.rec_out[cur] = *st.out_layer;
+        rec_rec(st, cur)[b] = r.idx;
+        rec_rec(st, cur)[Bm + b] = fa ? fa : L;
+        if (b == 0) rec_rec(st, cur)[2 * Bm] = *st.out_layer;
         st.rows.tok[b] = r.idx;  // next input (engine.cpp:304)
         st.rows.pos[b] += 1;     // KvStore::commit (engine.cpp:262-264)
     }

@@ -98,10 +98,10 @@ struct DevState {
     // per-iteration records (ring)
     int* iter_counter;
     int* cur_iter;
-    int* rec_tok;     // [rec_cap][Bmax]
-    int* rec_acc;     // [rec_cap][Bmax]
-    int* rec_out;     // [rec_cap]
-    float* rec_conf;  // [rec_cap][L][Bmax]
+    // packed record per iteration (one D2H copy): [tokens Bmax | accept Bmax | output layer, pad 3 |
+    // conf (float) L x Bmax], rec_stride ints apart
+    int* rec;
+    int rec_stride;
     int rec_cap;
     // T5 mode (encoder_len > 0): cross-attention weights and the static encoder K/V
     int enc_len, enc_blocks;    // encoder states per sequence; KV blocks they occupy
@@ -112,6 +112,11 @@ struct DevState {
     uint16_t* cvpool;
     const int* ctables;         // [slots][L][enc_blocks] (static)
 };
+
+__host__ __device__ inline int* rec_rec(const DevState& st, int cur) { return st.rec + (size_t)cur * st.rec_stride; }
+__host__ __device__ inline float* rec_conf(const DevState& st, int cur) {
+    return reinterpret_cast<float*>(rec_rec(st, cur) + 2 * st.dm.Bmax + 4);
+}
 
 // Weight (GEMM A operand) layout in HBM: 128x64 bf16 tiles, tile-major
 // [row/128][col/64], each tile stored exactly as TMA SWIZZLE_128B would place
