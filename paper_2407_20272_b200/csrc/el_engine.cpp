@@ -195,6 +195,9 @@ struct el_engine {
     DevBuf<int> row_slot, row_pos, row_tok, pf_slot, pf_pos, pf_tok, seq_ids_dev;
     // activations / workspaces
     DevBuf<float> h32, q32, mid32, attn_o, attn_ml, conf;
+    static constexpr int kPfRows = 256;  // rows of one batched-prefill launch
+    DevBuf<float> pf_h32, pf_q32, pf_mid32;
+    DevBuf<uint16_t> pf_hb, pf_att_b, pf_mid_b, pf_up_b;
     DevBuf<uint16_t> hb, att_b, mid_b, up_b;
     DevBuf<int> attn_cnt, attn_queue, layer, out_layer, status, first_accept, accept, exit_cnt, iter_counter,
         cur_iter, rec;
@@ -221,7 +224,7 @@ struct el_engine {
     int opt_mega_fill_splits = 0, opt_mega_att_stages = 0, opt_mega_pf = 0, opt_mega_kv_pf_mb = 0,
         opt_mega_bm_max = 128, opt_attn_dyn_permille = 0, opt_attn_dyn_cb = 4, opt_mega_bm_prefetch = 1,
         opt_mega_bm_chunk_kb = 0, opt_mega_bm_act_policy = 0, opt_mega_bm_nt_min = 16,
-        opt_mega_bm_m128 = 0, opt_mega_bm_down = 0;
+        opt_mega_bm_m128 = 0, opt_mega_bm_down = 0, opt_mega_att_l2 = 0;
     int attn_cb = 1, attn_stages = 2, attn_max_chunks = 1, attn_grid = 148;
     int NR = 16;
 
@@ -386,8 +389,16 @@ struct el_engine {
 
         // ---- rows / activations ----
         const int Bm = dm.Bmax;
-        for (DevBuf<int>* b : {&row_slot, &row_pos, &row_tok, &pf_slot, &pf_pos, &pf_tok, &seq_ids_dev})
-            b->alloc((size_t)Bm);
+        for (DevBuf<int>* b : {&row_slot, &row_pos, &row_tok, &seq_ids_dev}) b->alloc((size_t)Bm);
+        // prefill rows: up to kPfRows prompt positions per persistent-kernel launch (own activation set)
+        for (DevBuf<int>* b : {&pf_slot, &pf_pos, &pf_tok}) b->alloc((size_t)std::max(Bm, kPfRows));
+        pf_h32.alloc((size_t)2 * kPfRows * dp);
+        pf_hb.alloc((size_t)2 * kPfRows * dp);
+        pf_q32.alloc((size_t)kPfRows * dp);
+        pf_att_b.alloc((size_t)kPfRows * dp);
+        pf_mid32.alloc((size_t)kPfRows * dp);
+        pf_mid_b.alloc((size_t)kPfRows * dp);
+        pf_up_b.alloc((size_t)kPfRows * fp);
         NR = std::max(16, round_up(Bm, 16));
         h32.alloc((size_t)2 * Bm * dp);
         hb.alloc((size_t)2 * NR * dp);
@@ -396,7 +407,7 @@ struct el_engine {
         mid32.alloc((size_t)Bm * dp);
         mid_b.alloc((size_t)NR * dp);
         up_b.alloc((size_t)NR * fp);
-        attn_cnt.alloc((size_t)Bm);
+        attn_cnt.alloc((size_t)std::max(Bm, kPfRows));
         attn_queue.alloc(4);
         lm_part.alloc((size_t)(dm.Vp / 128) * Bm);
         dbg_ts.alloc(65536 + 256 * 1024);
@@ -474,8 +485,8 @@ struct el_engine {
         int sms = 148;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
         attn_grid = sms * el::attn_ctas_per_sm(dm, attn_stages);
-        attn_o.alloc((size_t)B * attn_max_chunks * dm.dp, false);
-        attn_ml.alloc((size_t)B * attn_max_chunks * 2, false);
+        attn_o.alloc((size_t)std::max(B, kPfRows) * attn_max_chunks * dm.dp, false);
+        attn_ml.alloc((size_t)std::max(B, kPfRows) * attn_max_chunks * 2, false);
         invalidate_graphs();
     }
 
@@ -547,9 +558,11 @@ struct el_engine {
         s = std::min(s, kb_total);
         return std::max(s, std::min(2, kb_total));
     }
-    el::IterPlan& mplan_for(int B) {
+    el::IterPlan& mplan_for(int B, int nr_override = 0) {
         const int n_pad = std::max(16, round_up(B, 16));
-        auto it = mplans.find(n_pad);
+        const int NR = nr_override ? nr_override : this->NR;  // activation rows of the operand layout
+        const int key = n_pad + (nr_override ? 100000 : 0);
+        auto it = mplans.find(key);
         if (it != mplans.end()) return it->second;
         const int dp = dm.dp, fp = dm.fp, L = dm.L;
         const int cap = 227 * 1024 - el::iter_smem_fixed();
@@ -612,6 +625,7 @@ struct el_engine {
         P.bm_kc = std::max(1, std::min(dp / 64, (opt_mega_bm_chunk_kb ? opt_mega_bm_chunk_kb * 1024 : 32768) / (NR * 128)));
         P.bm_act_policy = opt_mega_bm_act_policy;
         P.bm_m = (n_pad <= 64 && !opt_mega_bm_m128) ? 64 : 128;
+        P.att_l2_blocks = opt_mega_att_l2;
         P.bm_astage = P.bm_kc * NR * 128;
         (void)nt_max;
         P.bm_woff = (cap - bm_w) / 1024 * 1024;
@@ -645,12 +659,13 @@ struct el_engine {
             if (!x.mode || !x.A) continue;
             MM.w[k] = make_bm_map(x.A, (size_t)L * x.layer_rows * x.kb_total, x.nt, x.kb_total);
         }
-        mmaps[n_pad] = MM;
+        mmaps[key] = MM;
+        P.map_key = key;
         P.pf_flags = opt_mega_pf & 1;
         // next-layer K/V into L2: a budget of opt_mega_kv_pf_mb MB spread over the grid
         const long long blk2 = 2LL * dm.bc * dp * 2;
         P.kv_pf_blocks = (int)std::min<long long>(1 << 20, (long long)opt_mega_kv_pf_mb * (1 << 20) / (blk2 * mega_grid));
-        return mplans.emplace(n_pad, P).first->second;
+        return mplans.emplace(key, P).first->second;
     }
     void launch_mega(int B) {
         el::IterPlan& P = mplan_for(B);
@@ -658,7 +673,7 @@ struct el_engine {
         s.attn_stages = mega_att_stages;
         s.attn_dyn_permille = opt_attn_dyn_permille;
         s.attn_dyn_cb = opt_attn_dyn_cb;
-        el::launch_iter(s, P, mmaps[P.n_pad], mega_grid, stream);
+        el::launch_iter(s, P, mmaps[P.map_key], mega_grid, stream);
     }
 
     el::DevState state(bool prefill, int B) {
@@ -845,6 +860,10 @@ struct el_engine {
         std::vector<int> toks;  // prompt[0 .. P-2]
     };
     void prefill(const std::vector<PfSeq>& seqs) {
+        if (use_mega != 0) {
+            prefill_batched(seqs);
+            return;
+        }
         int maxn = 0;
         for (const auto& q : seqs) maxn = std::max(maxn, (int)q.toks.size());
         std::vector<int> hs, hp, ht;
@@ -875,6 +894,45 @@ struct el_engine {
             el::launch_advance(s, stream);
             CK(cudaStreamSynchronize(stream));  // host vectors are reused next step
         }
+    }
+
+    // Batched causal prefill on the persistent kernel: the rows of one launch are prompt
+    // positions (position-major across the admitted sequences, up to max_batch rows).  Each
+    // layer's QKV phase writes the K/V of every row before its attention phase, and earlier
+    // positions were written by earlier launches, so row (s, p) attends over exactly positions
+    // 0..p of sequence s -- the reference's token-by-token prefill, batched over positions.
+    void prefill_batched(const std::vector<PfSeq>& seqs) {
+        std::vector<int> hs, hp, ht;
+        int maxn = 0;
+        for (const auto& q : seqs) maxn = std::max(maxn, (int)q.toks.size());
+        auto flush = [&]() {
+            const int B = (int)hs.size();
+            if (!B) return;
+            CK(cudaMemcpyAsync(pf_slot.p, hs.data(), sizeof(int) * B, cudaMemcpyHostToDevice, stream));
+            CK(cudaMemcpyAsync(pf_pos.p, hp.data(), sizeof(int) * B, cudaMemcpyHostToDevice, stream));
+            CK(cudaMemcpyAsync(pf_tok.p, ht.data(), sizeof(int) * B, cudaMemcpyHostToDevice, stream));
+            el::IterPlan& P = mplan_for(B, kPfRows);
+            el::DevState s = state(true, B);
+            s.cont_host = nullptr;
+            s.prefill = 1;
+            // the prefill activation set: kPfRows rows (act layout stride kPfRows)
+            s.NR = kPfRows;
+            s.h32 = pf_h32.p; s.hb = pf_hb.p; s.q32 = pf_q32.p; s.att_b = pf_att_b.p;
+            s.mid32 = pf_mid32.p; s.mid_b = pf_mid_b.p; s.up_b = pf_up_b.p;
+            s.attn_stages = mega_att_stages;
+            el::launch_iter(s, P, mmaps[P.map_key], mega_grid, stream);
+            CK(cudaStreamSynchronize(stream));  // host vectors are reused
+            hs.clear(); hp.clear(); ht.clear();
+        };
+        for (int j = 0; j < maxn; ++j)
+            for (const auto& q : seqs)
+                if ((int)q.toks.size() > j) {
+                    if ((int)hs.size() == kPfRows) flush();
+                    hs.push_back(q.slot);
+                    hp.push_back(j);
+                    ht.push_back(q.toks[(size_t)j]);
+                }
+        flush();
     }
 
     // ---- records ----
@@ -1285,6 +1343,9 @@ int el_engine_set_option(el_engine* e, const char* key, int64_t v) {
         e->opt_attn_dyn_cb = (int)v;
     } else if (!std::strcmp(key, "mega_bm_chunk_kb") || !std::strcmp(key, "mega_bm_act_policy")) {
         (key[8] == 'c' ? e->opt_mega_bm_chunk_kb : e->opt_mega_bm_act_policy) = (int)v;
+        e->mplans.clear();
+    } else if (!std::strcmp(key, "mega_att_l2")) {
+        e->opt_mega_att_l2 = (int)v;
         e->mplans.clear();
     } else if (!std::strcmp(key, "mega_bm_down")) {
         e->opt_mega_bm_down = v != 0;

@@ -610,7 +610,7 @@ __device__ bool exit_decide(const DevState& st, IterSmem& sm, int layer, int B, 
             sm.first[b] = layer;
         }
         all = s;
-        if (blockIdx.x == 0) {
+        if (blockIdx.x == 0 && !st.prefill) {  // (prefill rows may exceed max_batch: no decode records)
             if (st.technique != kSoftmax) {  // softmax: written by the distributed decide phase
                 st.conf[(size_t)(layer - 1) * Bm + b] = conf;
                 st.accept[b] = acc;
@@ -1007,6 +1007,9 @@ __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(DevState st, Iter
     for (int layer = 1; layer <= L; ++layer) {
         const IterCtx x{layer, (layer - 1) & 1, layer & 1};
         // q | k | v, K/V appended to the paged pool (model.cpp:218-226)
+        // this layer's first attention blocks (old positions: not written by this layer) into L2
+        if (warp == kProducerWarp && p.att_l2_blocks > 0) l2_prefetch_kv(st, sm.att, layer, p.att_l2_blocks);
+        __syncwarp();
         if (p.g[kIQkv].mode) {
             gemm_phase_t<kIQkv>(st, sm, ring, p, maps, kIQkv, x, st.hb + (size_t)x.pin * NR * dp, kseq2, wseq, useq, B,
                                 wpf, -1, 0);
@@ -1144,6 +1147,19 @@ __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(DevState st, Iter
         }
     }
 
+    if (st.prefill) {
+        // batched causal prefill (engine.cpp:166-181): every layer's K/V of all rows is written;
+        // no exit, no tokens, no records -- only the launch bookkeeping below
+        if (cta == 0 && tid == 0) {
+            if (st.attn_queue) st.attn_queue[1] = 0;
+            if (!(st.dbg & (2048 | 4096 | 32768))) *(volatile unsigned*)p.bar = 0u;
+            if (st.dbg & (4096 | 32768)) *(volatile unsigned*)(p.bar + 1025) = g0 + (unsigned)nbar;
+        }
+        tc_fence_before();
+        __syncthreads();
+        if (warp == 0) tmem_dealloc(sm.tmem, 512);
+        return;
+    }
     // ---- tail: greedy LM head over h_e and the skipped-layer fill (kv_cache.cpp:222-234) ----
     const int pe = e_out & 1;
     const IterGemm& gf = p.g[kIFill];

@@ -103,6 +103,7 @@ struct DevState {
     int* rec;
     int rec_stride;
     int rec_cap;
+    int prefill;  // persistent kernel in batched-prefill mode (rows = prompt positions; K/V only)
     // T5 mode (encoder_len > 0): cross-attention weights and the static encoder K/V
     int enc_len, enc_blocks;    // encoder states per sequence; KV blocks they occupy
     const uint16_t* wqc;        // [L][dp][dp]   tiled
@@ -203,6 +204,8 @@ struct IterPlan {
     int bm_prefetch;  // issue each batch-M unit's weights one phase ahead (weight buffer outside the rings)
     int bm_act_policy;  // L2 hint of the activation copies: 0 evict-last, 1 evict-first (probe)
     int bm_m;           // UMMA M of the batch-M GEMMs: 64 (batch <= 64) or 128
+    int map_key;        // host-side key of this plan's tensor maps
+    int att_l2_blocks;  // per CTA: first attention K/V blocks of the layer prefetched into L2 during QKV
     int ring_bytes;  // shared ring region (attention stages / GEMM stages + LM transpose buffer)
     int gemm_ring;   // bytes of the GEMM stages inside the ring region
     int lm_tiles;    // Vp / 128

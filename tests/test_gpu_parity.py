@@ -353,3 +353,33 @@ def test_t5_engine_run_matches_oracle(port):
     with pytest.raises(ValueError):  # decoder prompts are the start token in T5 mode
         e.run(X.Workload([X.Request(0.0, [1, 2], 2)]))
     e.close()
+
+
+@pytest.mark.parametrize("mega", [False, True])
+def test_batched_prefill_kv_matches_oracle(port, mega):
+    """f1: the prompt's K/V of every layer after Engine::run's prefill (engine.cpp:166-181).
+    mega=True runs the batched causal prefill on the persistent kernel (rows = prompt
+    positions, several per sequence per launch, max_batch rows per launch); mega=False the
+    per-position per-phase path.  Both vs the oracle's token-by-token fp64 prefill."""
+    L, d, V, B = 3, 128, 512, 6
+    g = X.EngineConfig(model=X.ModelConfig(L, d, V, 21), technique=X.ExitTechnique("never"), max_batch=B,
+                       pool_blocks=4096, eos_token=-1, capture_kv=True)
+    o = OB.engine_config(L, d, V, 21, "never", max_batch=B, pool_blocks=4096, eos_token=-1, capture_kv=True,
+                         round_bf16=True)
+    rng = np.random.default_rng(5)
+    reqs = [(0.0, [int(x) for x in rng.integers(1, V, n)], 2) for n in (41, 7, 33, 1, 58, 20)]
+    e = X.Engine(g, mega=mega)
+    t = e.run(X.Workload([X.Request(*r) for r in reqs]))
+    tp = port.model(L, d, V, 21, True).run(o, OB.Workload.from_requests(reqs))
+    for sid in range(len(reqs)):
+        for layer in range(1, L + 1):
+            kg, vg = t.kv(sid, layer)
+            ko, vo = port.transcript_kv(tp, sid, layer, d)
+            n = len(reqs[sid][1]) - 1  # prefill positions
+            if n == 0:
+                continue
+            assert relerr(kg[:n], ko[:n]) <= HID_TOL and relerr(vg[:n], vo[:n]) <= HID_TOL, (sid, layer)
+    gt = {s["id"]: s["tokens"] for s in t.sequences}
+    pt = {s["id"]: s["tokens"] for s in tp.sequences}
+    assert np.mean([a == b for k in pt for a, b in zip(gt[k], pt[k])]) >= 0.9
+    e.close()
