@@ -283,6 +283,12 @@ class _Lib:
             raise ValueError(self.err())
         return o[: c * d].reshape(c, d)
 
+    def write_transcript_jsonl(self, t, path):
+        """the reference's own writer (oracle/_ref only)"""
+        rc = self.fn("transcript_write_jsonl")(t.handle, path.encode())
+        if rc:
+            raise RuntimeError(self.err())
+
     def free_transcript(self, t):
         if getattr(t, "handle", None):
             self.fn("transcript_free")(t.handle)

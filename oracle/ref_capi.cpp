@@ -284,6 +284,13 @@ int ref_engine_run(const void* mp, const eo_engine_config* c, int n, const doubl
 }
 
 void ref_transcript_free(void* t) { delete static_cast<FlatTranscript*>(t); }
+// the reference's own transcript persistence (engine.cpp:336-393), for byte comparisons
+int ref_transcript_write_jsonl(void* tp, const char* path) {
+    GUARD_BEGIN
+    write_transcript_jsonl(static_cast<FlatTranscript*>(tp)->t, path);
+    return EO_OK;
+    GUARD_END(ret_code)
+}
 int64_t ref_transcript_len(void* tp, const char* f) {
     auto* t = static_cast<FlatTranscript*>(tp);
     if (auto* a = t->i32(f)) return (int64_t)a->size();

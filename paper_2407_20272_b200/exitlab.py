@@ -320,6 +320,13 @@ class Transcript:
                      iter_output_layers=self.f["sq_iter_out"][to[i]:to[i + 1]].tolist())
                 for i in range(len(self.f["sq_id"]))]
 
+    # ---- persistence: the reference's JSON-lines format (engine.cpp:336-393) ----
+    def to_jsonl(self, path, model: "ModelConfig" = None, technique: "ExitTechnique" = None):
+        """write_transcript_jsonl: same records, key order and number formatting as the
+        reference (nlohmann ordered_json dump), so B200 transcripts are byte-comparable with
+        the reference's and readable by read_transcript_jsonl / compute_metrics."""
+        write_transcript_jsonl(self, path, model or self.model, technique or self.technique)
+
     def kv(self, seq_id, layer):
         n = 1 << 22
         k = np.zeros(n)
@@ -336,6 +343,87 @@ class Transcript:
         if c < 0:
             _check(-c)
         return o[: c * self.d].reshape(c, self.d)
+
+
+def _json_num(x):
+    if isinstance(x, (bool, np.bool_)):
+        return "true" if x else "false"
+    if isinstance(x, (int, np.integer)):
+        return str(int(x))
+    x = float(x)
+    if x != x or x in (float("inf"), float("-inf")):
+        return "null"  # nlohmann dumps non-finite numbers as null
+    r = repr(x)  # shortest round-trip, like nlohmann's dtoa
+    if "e" not in r and "." not in r:
+        r += ".0"
+    return r
+
+
+def _json_dump(v):
+    """nlohmann::ordered_json::dump() formatting: no spaces, insertion order."""
+    import json
+    if isinstance(v, dict):
+        return "{" + ",".join(json.dumps(k) + ":" + _json_dump(x) for k, x in v.items()) + "}"
+    if isinstance(v, (list, tuple)):
+        return "[" + ",".join(_json_dump(x) for x in v) + "]"
+    if isinstance(v, str):
+        return json.dumps(v, ensure_ascii=False)
+    return _json_num(v)
+
+
+def transcript_records(t, model, technique):
+    """The records of write_transcript_jsonl (engine.cpp:336-393) for a flat transcript."""
+    m = t["meta"]  # final_clock, total_idle, pool_blocks, free_blocks, peak_blocks
+    yield {"type": "meta", "n_layers": model.n_layers, "d_model": model.d_model, "vocab_size": model.vocab_size,
+           "model_seed": int(model.seed), "technique": technique.name, "final_clock": float(m[0]),
+           "total_idle": float(m[1]),
+           "cache": {"pool_blocks": int(m[2]), "free_blocks": int(m[3]), "peak_blocks": int(m[4])}}
+    for i in range(len(t["pf_seq"])):
+        yield {"type": "prefill", "clock": float(t["pf_clock"][i]), "charge": float(t["pf_charge"][i]),
+               "seq_id": int(t["pf_seq"][i]), "positions": int(t["pf_positions"][i])}
+    for it in t.iterations:
+        yield {"type": "iteration", "clock": float(it["clock"]), "charge": float(it["charge"]),
+               "batch_ids": [int(x) for x in it["batch_ids"]], "output_layer": it["output_layer"],
+               "per_seq": [{"seq_id": int(sid), "accept_layer": int(a), "token": int(tok)}
+                           for sid, a, tok in zip(it["batch_ids"], it["accept"], it["tokens"])]}
+    for sq in t.sequences:
+        yield {"type": "sequence", "seq_id": sq["id"], "arrival": float(sq["arrival"]),
+               "first_token": float(sq["first_token"]), "finish": float(sq["finish"]),
+               "max_new_tokens": sq["max_new"], "prompt": sq["prompt"], "tokens": sq["tokens"],
+               "exit_layers": sq["exit_layers"], "iter_output_layers": sq["iter_output_layers"]}
+
+
+def write_transcript_jsonl(t, path, model, technique):
+    """write_transcript_jsonl (engine.cpp:336-393) for any flat transcript (product, oracle port or
+    reference wrapper): byte-identical to the reference's writer."""
+    with open(path, "w") as f:
+        for rec in transcript_records(t, model, technique):
+            f.write(_json_dump(rec) + "\n")
+
+
+def read_transcript_jsonl(path):
+    """read_transcript_jsonl (engine.cpp:395-461): the records as dicts, validated like the
+    reference (unknown types and a missing meta record are errors)."""
+    import json
+    out = {"meta": None, "prefills": [], "iterations": [], "sequences": []}
+    with open(path) as f:
+        for no, line in enumerate(f, 1):
+            if not line.strip():
+                continue
+            try:
+                j = json.loads(line)
+            except json.JSONDecodeError as e:
+                raise RuntimeError(f"transcript: parse error at line {no}: {e}") from None
+            kind = j.get("type")
+            if kind == "meta":
+                out["meta"] = j
+            elif kind in ("prefill", "iteration", "sequence"):
+                out[kind + "s" if kind != "prefill" else "prefills"].append(j)
+            else:
+                raise RuntimeError(f"transcript: unknown record type '{kind}' at line {no}")
+    if out["meta"] is None:
+        raise RuntimeError(f"transcript: missing meta record in {path}")
+    return out
 
 
 # ---------------------------------------------------------------- engine
@@ -378,7 +466,9 @@ class Engine:
         t = C.c_void_p()
         _check(lib().el_engine_run(self._h, len(arrival), _ptr(arrival), _ptr(off), _ptr(prompt),
                                    _ptr(max_new), C.byref(t)))
-        return Transcript(t, self.d, self.L)
+        tr = Transcript(t, self.d, self.L)
+        tr.model, tr.technique = self.config.model, self.config.technique
+        return tr
 
     # ---- fixed-batch decode session over a seeded KV prefix ----
     def session_begin(self, first_tokens, prefix_len, capacity, kv_seed, seq_ids=None):

@@ -383,3 +383,20 @@ def test_batched_prefill_kv_matches_oracle(port, mega):
     pt = {s["id"]: s["tokens"] for s in tp.sequences}
     assert np.mean([a == b for k in pt for a, b in zip(gt[k], pt[k])]) >= 0.9
     e.close()
+
+
+def test_transcript_jsonl_byte_identical_on_device(port, tmp_path):
+    """f3: the B200 engine's transcript written in the reference's JSONL format is byte-identical
+    to the oracle's (and so to the reference's writer, tests/test_transcript_jsonl_cpu.py) when
+    the decisions are fixed (technique never / always_at, tiny model: tokens equal too)."""
+    for tech, kw in (("never", {}), ("always_at", dict(exit_layer=2))):
+        g, o = cfg_pair(3, 8, 16, 11, tech, B=4, pool=64, bc=4, eos=-1, **kw)
+        reqs = [(0.0, [1, 2, 3], 5), (0.0, [4, 5], 3), (0.01, [6], 4)]
+        e = X.Engine(g)
+        t = e.run(X.Workload([X.Request(*r) for r in reqs]))
+        tp = port.model(3, 8, 16, 11, True).run(o, OB.Workload.from_requests(reqs))
+        a, b = tmp_path / f"gpu_{tech}.jsonl", tmp_path / f"port_{tech}.jsonl"
+        t.to_jsonl(str(a))
+        X.write_transcript_jsonl(tp, str(b), g.model, g.technique)
+        assert a.read_bytes() == b.read_bytes(), tech
+        e.close()
