@@ -224,7 +224,8 @@ struct el_engine {
     int opt_mega_fill_splits = 0, opt_mega_att_stages = 0, opt_mega_pf = 0, opt_mega_kv_pf_mb = 0,
         opt_mega_bm_max = 128, opt_attn_dyn_permille = 0, opt_attn_dyn_cb = 4, opt_mega_bm_prefetch = 1,
         opt_mega_bm_chunk_kb = 0, opt_mega_bm_act_policy = 0, opt_mega_bm_nt_min = 16,
-        opt_mega_bm_m128 = 0, opt_mega_bm_down = 0, opt_mega_att_l2 = 0;
+        opt_mega_bm_m128 = 0, opt_mega_bm_down = 0, opt_mega_att_l2 = 0, opt_mega_down_splits = 0,
+        opt_mega_splits_cap = 8;
     int attn_cb = 1, attn_stages = 2, attn_max_chunks = 1, attn_grid = 148;
     int NR = 16;
 
@@ -555,7 +556,7 @@ struct el_engine {
     // split-K: aim at one unit per CTA (units = m_tiles * splits <= grid), >= 2 splits
     int mega_splits(int m_tiles, int kb_total) const {
         int s = std::max(1, mega_grid / m_tiles);
-        s = std::min(s, kb_total);
+        s = std::min({s, kb_total, opt_mega_splits_cap});  // fewer splits: less partial traffic to reduce
         return std::max(s, std::min(2, kb_total));
     }
     el::IterPlan& mplan_for(int B, int nr_override = 0) {
@@ -589,7 +590,9 @@ struct el_engine {
         P.g[el::kIQkv] = g(wqkv.p, 3 * dp / 128, dp / 64, 3 * dp / 128, 0, mega_splits(3 * dp / 128, dp / 64));
         P.g[el::kIWo] = g(wo.p, dp / 128, dp / 64, dp / 128, 0, mega_splits(dp / 128, dp / 64));
         P.g[el::kIUp] = g(wup.p, fp / 128, dp / 64, fp / 128, 0, mega_splits(fp / 128, dp / 64));
-        P.g[el::kIDown] = g(wdown.p, dp / 128, fp / 64, dp / 128, 0, mega_splits(dp / 128, fp / 64));
+        P.g[el::kIDown] = g(wdown.p, dp / 128, fp / 64, dp / 128, 0,
+                            opt_mega_down_splits ? std::min(opt_mega_down_splits, fp / 64)
+                                                 : mega_splits(dp / 128, fp / 64));
         // fill: full-K units (direct epilogue) at large N, where split-K partials would outweigh the weights
         P.g[el::kIQc] = g(wqc.p, dp / 128, dp / 64, dp / 128, 0, mega_splits(dp / 128, dp / 64));
         P.g[el::kIWoc] = g(woc.p, dp / 128, dp / 64, dp / 128, 0, mega_splits(dp / 128, dp / 64));
@@ -1343,6 +1346,13 @@ int el_engine_set_option(el_engine* e, const char* key, int64_t v) {
         e->opt_attn_dyn_cb = (int)v;
     } else if (!std::strcmp(key, "mega_bm_chunk_kb") || !std::strcmp(key, "mega_bm_act_policy")) {
         (key[8] == 'c' ? e->opt_mega_bm_chunk_kb : e->opt_mega_bm_act_policy) = (int)v;
+        e->mplans.clear();
+    } else if (!std::strcmp(key, "mega_splits_cap")) {
+        if (v < 1) fail(EL_INVALID_ARGUMENT, "mega_splits_cap must be >= 1");
+        e->opt_mega_splits_cap = (int)v;
+        e->mplans.clear();
+    } else if (!std::strcmp(key, "mega_down_splits")) {
+        e->opt_mega_down_splits = (int)v;
         e->mplans.clear();
     } else if (!std::strcmp(key, "mega_att_l2")) {
         e->opt_mega_att_l2 = (int)v;
