@@ -220,12 +220,13 @@ struct el_engine {
     std::map<int, el::IterMaps> mmaps;   // their batch-M weight tensor maps
     DevBuf<float> mpart;                 // split-K partial workspace of the persistent kernel
     DevBuf<unsigned> mbar;               // its grid barrier (arrivals, generation)
+    DevBuf<unsigned> mtcnt;              // its per-tile split-K arrival counters
     int mega_grid = 0, mega_att_stages = 2, sms = 148;
     int opt_mega_fill_splits = 0, opt_mega_att_stages = 0, opt_mega_pf = 0, opt_mega_kv_pf_mb = 0,
         opt_mega_bm_max = 128, opt_attn_dyn_permille = 0, opt_attn_dyn_cb = 4, opt_mega_bm_prefetch = 1,
         opt_mega_bm_chunk_kb = 0, opt_mega_bm_act_policy = 0, opt_mega_bm_nt_min = 16,
         opt_mega_bm_m128 = 0, opt_mega_bm_down = 0, opt_mega_att_l2 = 0, opt_mega_down_splits = 0,
-        opt_mega_splits_cap = 8;
+        opt_mega_splits_cap = 8, opt_mega_fused_reduce = 1;
     int attn_cb = 1, attn_stages = 2, attn_max_chunks = 1, attn_grid = 148;
     int NR = 16;
 
@@ -434,6 +435,7 @@ struct el_engine {
         el::init_kernel_attributes();
         el::init_iter_attributes();
         mbar.alloc(2048 + 32 * 1024);
+        mtcnt.alloc(el::kINumGemm * 64);
         CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
         slot_bpl.assign((size_t)dm.slots, 0);
         ensure_bpl(1);
@@ -629,6 +631,8 @@ struct el_engine {
         P.bm_act_policy = opt_mega_bm_act_policy;
         P.bm_m = (n_pad <= 64 && !opt_mega_bm_m128) ? 64 : 128;
         P.att_l2_blocks = opt_mega_att_l2;
+        P.fused_reduce = opt_mega_fused_reduce;
+        P.tcnt = mtcnt.p;
         P.bm_astage = P.bm_kc * NR * 128;
         (void)nt_max;
         P.bm_woff = (cap - bm_w) / 1024 * 1024;
@@ -1346,6 +1350,9 @@ int el_engine_set_option(el_engine* e, const char* key, int64_t v) {
         e->opt_attn_dyn_cb = (int)v;
     } else if (!std::strcmp(key, "mega_bm_chunk_kb") || !std::strcmp(key, "mega_bm_act_policy")) {
         (key[8] == 'c' ? e->opt_mega_bm_chunk_kb : e->opt_mega_bm_act_policy) = (int)v;
+        e->mplans.clear();
+    } else if (!std::strcmp(key, "mega_fused_reduce")) {
+        e->opt_mega_fused_reduce = v != 0;
         e->mplans.clear();
     } else if (!std::strcmp(key, "mega_splits_cap")) {
         if (v < 1) fail(EL_INVALID_ARGUMENT, "mega_splits_cap must be >= 1");

@@ -468,16 +468,14 @@ __device__ __forceinline__ void epi_fill_direct(const DevState& st, const IterSm
 // piece (4 rows per lane), two pieces in flight per warp; the K splits are
 // summed in split order (deterministic).  K == kIDown also produces the exit
 // check's per-tile partial dots (fp64, fixed shuffle tree).
+// pieces [P0, P) (piece = m * nval + c), this warp's first piece P0 + gw, stride GW
 template <int K>
-__device__ void reduce_phase(const DevState& st, const IterSmem& sm, const IterPlan& p, const IterGemm& g,
-                             const IterCtx& x, int nval, int unit_base, int m_total) {
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (warp >= 8) return;
+__device__ void reduce_range(const DevState& st, const IterSmem& sm, const IterPlan& p, const IterGemm& g,
+                             const IterCtx& x, int nval, int unit_base, int P0, int P, int gw, int GW) {
+    const int lane = threadIdx.x & 31;
     const int S = g.splits;
-    const int P = m_total * nval;
-    const int GW = (int)gridDim.x * 8, gw = (int)blockIdx.x * 8 + warp;
     const int dp = st.dm.dp, Bm = st.dm.Bmax;
-    for (int p0 = gw; p0 < P; p0 += 2 * GW) {
+    for (int p0 = P0 + gw; p0 < P; p0 += 2 * GW) {
         int mm[2], cc[2];
         bool ok[2];
         float4 acc[2];
@@ -563,6 +561,15 @@ __device__ void reduce_phase(const DevState& st, const IterSmem& sm, const IterP
             }
         }
     }
+}
+
+template <int K>
+__device__ void reduce_phase(const DevState& st, const IterSmem& sm, const IterPlan& p, const IterGemm& g,
+                             const IterCtx& x, int nval, int unit_base, int m_total) {
+    const int warp = threadIdx.x >> 5;
+    if (warp >= 8) return;
+    reduce_range<K>(st, sm, p, g, x, nval, unit_base, 0, m_total * nval, (int)blockIdx.x * 8 + warp,
+                    (int)gridDim.x * 8);
 }
 
 // exit decision of `layer` for every row, computed identically by every CTA
@@ -911,6 +918,53 @@ __device__ __forceinline__ void gemm_phase_t(const DevState& st, IterSmem& sm, u
     if (next_gid >= 0 && threadIdx.x == kProducerWarp * 32) wpf = bm_prefetch(sm, ring, p, maps, next_gid, next_layer);
 }
 
+// Split-K GEMM phase with the reduction fused per output tile: every unit's CTA
+// publishes its partial and bumps the tile's arrival counter (monotonic within the
+// launch, zeroed at its end); once all S splits of its tile are in, the S CTAs of
+// the tile each reduce their own 1/S of the columns (in split order: deterministic)
+// and apply the epilogue.  Replaces a grid barrier + a separate reduce phase by a
+// wait on the S - 1 peers of the tile.
+template <int K>
+__device__ void gemm_phase_fused(const DevState& st, IterSmem& sm, uint8_t* ring, const IterPlan& p, int gid,
+                                 const IterCtx& x, const uint16_t* bsrc, uint32_t& kseq, uint32_t& useq, int nval,
+                                 int use) {
+    const IterGemm& g = p.g[gid];
+    const int warp = threadIdx.x >> 5;
+    const int U = g.m_tiles * g.splits;
+    const size_t bks = (size_t)st.NR * kBK;
+    unsigned* cnt = p.tcnt + gid * 64;
+    for (int u = blockIdx.x; u < U; u += gridDim.x) {
+        const int m = u / g.splits, s = u % g.splits;
+        const int kb0 = s * g.kb_total / g.splits, kb1 = (s + 1) * g.kb_total / g.splits;
+        const uint16_t* a = g.A + (size_t)((x.layer - 1) * g.layer_rows + g.row_off + m) * g.kb_total * (kBM * kBK);
+        unit_ws(sm, ring, p, kseq, a, bsrc, bks, kb0, kb1 - kb0, useq);
+        if (warp < 8) epi_partial(sm, p, u, nval);
+        ++useq;
+        tc_fence_before();
+        fence_proxy_async_global();
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            red_release_add_u32(cnt + m, 1u);
+        }
+    }
+    for (int u = blockIdx.x; u < U; u += gridDim.x) {
+        const int m = u / g.splits, s = u % g.splits;
+        if (threadIdx.x == 0) {
+            const unsigned target = (unsigned)(g.splits * use);
+            const long long t0 = clock64();
+            while (ld_acquire_u32(cnt + m) < target)
+                if (clock64() - t0 > EL_SPIN_LIMIT) __trap();
+            __threadfence();
+        }
+        __syncthreads();
+        if (warp < 8) {
+            const int c0 = s * nval / g.splits, c1 = (s + 1) * nval / g.splits;
+            reduce_range<K>(st, sm, p, g, x, nval, 0, m * nval + c0, m * nval + c1, warp, 8);
+        }
+    }
+}
+
 // weight-streaming GEMM phase: this CTA's units (u = cta, cta + G, ...)
 __device__ __forceinline__ void gemm_phase(const DevState& st, IterSmem& sm, uint8_t* ring, const IterPlan& p,
                                            const IterGemm& g, int layer, const uint16_t* bsrc, uint32_t& kseq,
@@ -1013,6 +1067,8 @@ __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(DevState st, Iter
         if (p.g[kIQkv].mode) {
             gemm_phase_t<kIQkv>(st, sm, ring, p, maps, kIQkv, x, st.hb + (size_t)x.pin * NR * dp, kseq2, wseq, useq, B,
                                 wpf, -1, 0);
+        } else if (p.fused_reduce) {
+            gemm_phase_fused<kIQkv>(st, sm, ring, p, kIQkv, x, st.hb + (size_t)x.pin * NR * dp, kseq, useq, B, layer);
         } else {
             gemm_phase(st, sm, ring, p, p.g[kIQkv], layer, st.hb + (size_t)x.pin * NR * dp, kseq, useq, B);
             grid_sync(p, st, nbar, g0);
@@ -1051,6 +1107,8 @@ __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(DevState st, Iter
         if (p.g[kIWo].mode) {
             gemm_phase_t<kIWo>(st, sm, ring, p, maps, kIWo, x, st.att_b, kseq2, wseq, useq, B, wpf,
                                st.enc_len > 0 ? (int)kIQc : (int)kIUp, layer);
+        } else if (p.fused_reduce) {
+            gemm_phase_fused<kIWo>(st, sm, ring, p, kIWo, x, st.att_b, kseq, useq, B, layer);
         } else {
             gemm_phase(st, sm, ring, p, p.g[kIWo], layer, st.att_b, kseq, useq, B);
             grid_sync(p, st, nbar, g0);
@@ -1062,6 +1120,8 @@ __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(DevState st, Iter
             if (p.g[kIQc].mode) {
                 gemm_phase_t<kIQkv>(st, sm, ring, p, maps, kIQc, x, st.mid_b, kseq2, wseq, useq, B, wpf, -1,
                                     0);  // q_c -> q32
+            } else if (p.fused_reduce) {
+                gemm_phase_fused<kIQkv>(st, sm, ring, p, kIQc, x, st.mid_b, kseq, useq, B, layer);
             } else {
                 gemm_phase(st, sm, ring, p, p.g[kIQc], layer, st.mid_b, kseq, useq, B);
                 grid_sync(p, st, nbar, g0);
@@ -1075,6 +1135,8 @@ __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(DevState st, Iter
             if (p.g[kIWoc].mode) {
                 gemm_phase_t<kIWoc>(st, sm, ring, p, maps, kIWoc, x, st.att_b, kseq2, wseq, useq, B, wpf, kIUp,
                                     layer);
+            } else if (p.fused_reduce) {
+                gemm_phase_fused<kIWoc>(st, sm, ring, p, kIWoc, x, st.att_b, kseq, useq, B, layer);
             } else {
                 gemm_phase(st, sm, ring, p, p.g[kIWoc], layer, st.att_b, kseq, useq, B);
                 grid_sync(p, st, nbar, g0);
@@ -1086,6 +1148,8 @@ __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(DevState st, Iter
         if (p.g[kIUp].mode) {
             gemm_phase_t<kIUp>(st, sm, ring, p, maps, kIUp, x, st.mid_b, kseq2, wseq, useq, B, wpf,
                                p.g[kIDown].mode ? (int)kIDown : -1, layer);
+        } else if (p.fused_reduce) {
+            gemm_phase_fused<kIUp>(st, sm, ring, p, kIUp, x, st.mid_b, kseq, useq, B, layer);
         } else {
             gemm_phase(st, sm, ring, p, p.g[kIUp], layer, st.mid_b, kseq, useq, B);
             grid_sync(p, st, nbar, g0);
@@ -1096,6 +1160,9 @@ __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(DevState st, Iter
         if (p.g[kIDown].mode) {
             gemm_phase_t<kIDown>(st, sm, ring, p, maps, kIDown, x, st.up_b, kseq2, wseq, useq, B, wpf,
                                  layer < L ? (int)kIQkv : -1, layer + 1);
+        } else if (p.fused_reduce) {
+            if (tid == kProducerWarp * 32 && layer < L) wpf = bm_prefetch(sm, ring, p, maps, kIQkv, layer + 1);
+            gemm_phase_fused<kIDown>(st, sm, ring, p, kIDown, x, st.up_b, kseq, useq, B, layer);
         } else {
             gemm_phase(st, sm, ring, p, p.g[kIDown], layer, st.up_b, kseq, useq, B);
             grid_sync(p, st, nbar, g0);
@@ -1151,6 +1218,7 @@ __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(DevState st, Iter
         // batched causal prefill (engine.cpp:166-181): every layer's K/V of all rows is written;
         // no exit, no tokens, no records -- only the launch bookkeeping below
         if (cta == 0 && tid == 0) {
+            for (int i = 0; i < kINumGemm * 64; ++i) p.tcnt[i] = 0u;  // all tile waits are behind us
             if (st.attn_queue) st.attn_queue[1] = 0;
             if (!(st.dbg & (2048 | 4096 | 32768))) *(volatile unsigned*)p.bar = 0u;
             if (st.dbg & (4096 | 32768)) *(volatile unsigned*)(p.bar + 1025) = g0 + (unsigned)nbar;
@@ -1214,6 +1282,7 @@ __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(DevState st, Iter
         }
     }
     if (cta == 0 && tid == 0) {
+        for (int i = 0; i < kINumGemm * 64; ++i) p.tcnt[i] = 0u;  // all tile waits are behind us
         if (st.attn_queue) st.attn_queue[1] = 0;  // layer 1 of the next launch (layer 2's is rearmed in layer 1)
         if (!(st.dbg & (2048 | 4096 | 32768))) *(volatile unsigned*)p.bar = 0u;  // arrivals of this launch are all in
         if (st.dbg & (4096 | 32768)) *(volatile unsigned*)(p.bar + 1025) = g0 + (unsigned)nbar;  // flag epochs continue

@@ -205,6 +205,8 @@ struct IterPlan {
     int bm_act_policy;  // L2 hint of the activation copies: 0 evict-last, 1 evict-first (probe)
     int bm_m;           // UMMA M of the batch-M GEMMs: 64 (batch <= 64) or 128
     int map_key;        // host-side key of this plan's tensor maps
+    int fused_reduce;   // split-K: per-tile arrival counters + the tile's CTAs reduce (no grid barrier)
+    unsigned* tcnt;     // [kINumGemm][64] per-tile arrival counters (zeroed at the end of each launch)
     int att_l2_blocks;  // per CTA: first attention K/V blocks of the layer prefetched into L2 during QKV
     int ring_bytes;  // shared ring region (attention stages / GEMM stages + LM transpose buffer)
     int gemm_ring;   // bytes of the GEMM stages inside the ring region
