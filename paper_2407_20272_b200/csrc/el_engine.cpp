@@ -226,7 +226,7 @@ struct el_engine {
         opt_mega_bm_max = 128, opt_attn_dyn_permille = 0, opt_attn_dyn_cb = 4, opt_mega_bm_prefetch = 1,
         opt_mega_bm_chunk_kb = 0, opt_mega_bm_act_policy = 0, opt_mega_bm_nt_min = 16,
         opt_mega_bm_m128 = 0, opt_mega_bm_down = 0, opt_mega_att_l2 = 0, opt_mega_down_splits = 0,
-        opt_mega_splits_cap = 8, opt_mega_fused_reduce = 1;
+        opt_mega_splits_cap = 8, opt_mega_fused_reduce = 1, opt_att_mbuf = 1;
     int attn_cb = 1, attn_stages = 2, attn_max_chunks = 1, attn_grid = 148;
     int NR = 16;
 
@@ -644,7 +644,11 @@ struct el_engine {
         P.stages = std::min(8, (ws_cap - el::kIterTbufBytes) / stage);
         if (P.stages < 2) fail(EL_INVALID_ARGUMENT, "persistent kernel: GEMM ring does not fit");
         P.gemm_ring = P.stages * stage;
-        P.ring_bytes = round_up(std::max({ring_att, P.gemm_ring + el::kIterTbufBytes,
+        // attention merge buffer right after the attention stages (a segment's stage is released
+        // before its merge) when it fits below the batch-M weight buffer
+        const int mbuf = 8 * dp * 4;
+        P.att_mbuf_off = (opt_att_mbuf && ring_att + mbuf <= (bm ? P.bm_woff : cap)) ? ring_att : 0;
+        P.ring_bytes = round_up(std::max({ring_att + (P.att_mbuf_off ? mbuf : 0), P.gemm_ring + el::kIterTbufBytes,
                                           P.bm_stages * P.bm_astage + 16384, bm ? P.bm_woff + bm_w : 0}), 1024);
         P.lm_tiles = dm.Vp / 128;
         if (el::iter_max_ctas_per_sm(dm, P.ring_bytes) < 1)
@@ -1350,6 +1354,9 @@ int el_engine_set_option(el_engine* e, const char* key, int64_t v) {
         e->opt_attn_dyn_cb = (int)v;
     } else if (!std::strcmp(key, "mega_bm_chunk_kb") || !std::strcmp(key, "mega_bm_act_policy")) {
         (key[8] == 'c' ? e->opt_mega_bm_chunk_kb : e->opt_mega_bm_act_policy) = (int)v;
+        e->mplans.clear();
+    } else if (!std::strcmp(key, "att_mbuf")) {
+        e->opt_att_mbuf = v != 0;
         e->mplans.clear();
     } else if (!std::strcmp(key, "mega_fused_reduce")) {
         e->opt_mega_fused_reduce = v != 0;

@@ -32,7 +32,7 @@ struct IterSmem {
     uint64_t full[8], empty[8], acc;
     uint64_t full2[16], empty2[16];  // batch-M GEMM activation ring
     uint64_t wfull;                  // batch-M unit weights (one tensor copy per unit)
-    unsigned long long tdbg[4];
+    unsigned long long tdbg[5];
     uint32_t tmem;
     int pad0;
     int pos[256], slot[256], status[256], first[256];
@@ -107,100 +107,46 @@ __device__ __forceinline__ void red_release_add_u32(unsigned* p, unsigned v) {
 
 // Grid barrier over co-resident CTAs.  Generic global writes before it are
 // visible (and ordered for the async proxy: bulk copies read them) to every
-// CTA after it.  bar layout (unsigned): [0] arrivals, [1024] generation,
-// [2048 + cta*32] per-CTA flags (variant C).  Variants (probe, dbg bits):
-//   D (default): red.release arrivals, CTA 0 polls the count and releases the generation
-//   A (2048): atomic arrive with return, last arriver resets the count and releases the generation
-//   C (4096): per-CTA epoch flags, every CTA polls all flags (no atomics)
-//   E (16384): D with relaxed polling + one acquire fence;  F (32768): C with relaxed polling
-// Measured on B200 (scripts/bar_probe.py): D ~2.0 us, A ~2.9 us, C ~2.8 us, E ~2.7 us.
-__device__ __noinline__ void grid_sync(const IterPlan& p, const DevState& st, int& nbar, unsigned g0) {
-    if (threadIdx.x == 0 && (st.dbg & 128) && nbar < 1024) {  // per-CTA arrival (work done) time
+// CTA after it.  bar layout (unsigned): [0] arrivals (zeroed at the end of each
+// launch), [1024] generation.  Every CTA adds one arrival with red.release; CTA 0
+// polls the count and releases the generation, the others poll the generation.
+// (Measured on B200, scripts/bar_probe.py of earlier revisions: ~2.0 us, against
+// 2.7-2.9 us for a last-arriver / per-CTA-flag / relaxed-poll design.)  Inlined,
+// with scalar arguments: a call would spill live registers around every barrier
+// and a reference to the kernel's DevState / IterPlan parameters would put a copy
+// of them in local memory.
+__device__ __forceinline__ void grid_sync(const IterPlan& p, const DevState& st, int& nbar, unsigned g0) {
+    const int dbg = st.dbg;
+    if (threadIdx.x == 0 && (dbg & 128) && nbar < 1024) {  // per-CTA arrival (work done) time
         unsigned long long t;
         asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
         st.dbg_ts[65536 + (size_t)blockIdx.x * 1024 + nbar] = t;
     }
-    if (!(st.dbg & 512)) fence_proxy_async_global();
+    fence_proxy_async_global();
     __syncthreads();
     const unsigned k = (unsigned)nbar + 1u;  // barrier index within this launch (1-based)
-    unsigned* cnt = p.bar;
-    unsigned* gen = p.bar + 1024;
-    const int G = (int)gridDim.x;
-    if (st.dbg & 16384) {  // E: D with relaxed polling and one acquire fence after
-        if (threadIdx.x == 0) {
-            red_release_add_u32(cnt, 1u);
-            const long long t0 = clock64();
-            if (blockIdx.x == 0) {
-                while (ld_relaxed_u32(cnt) < (unsigned)G * k)
-                    if (clock64() - t0 > EL_SPIN_LIMIT) __trap();
-                fence_acq_rel_gpu();
-                st_release_u32(gen, g0 + k);
-            } else {
-                while ((int)(ld_relaxed_u32(gen) - (g0 + k)) < 0)
-                    if (clock64() - t0 > EL_SPIN_LIMIT) __trap();
-            }
-            fence_acq_rel_gpu();
-        }
-    } else if (st.dbg & 32768) {  // F: C with relaxed polling
-        if (threadIdx.x < 32) {
-            unsigned* flags = p.bar + 2048;
-            if (threadIdx.x == 0) st_release_u32(flags + blockIdx.x * 32, g0 + k);
-            const long long t0 = clock64();
-            for (;;) {
-                bool ok = true;
-                for (int c = (int)threadIdx.x; c < G; c += 32) ok &= (int)(ld_relaxed_u32(flags + c * 32) - (g0 + k)) >= 0;
-                if (__all_sync(0xffffffffu, ok)) break;
+    if (threadIdx.x == 0) {
+        unsigned* cnt = p.bar;
+        unsigned* gen = p.bar + 1024;
+        red_release_add_u32(cnt, 1u);
+        const long long t0 = clock64();
+        if (blockIdx.x == 0) {
+            while (ld_acquire_u32(cnt) < gridDim.x * k)
                 if (clock64() - t0 > EL_SPIN_LIMIT) __trap();
-            }
-            fence_acq_rel_gpu();
-        }
-    } else if (st.dbg & 4096) {
-        if (threadIdx.x < 32) {
-            unsigned* flags = p.bar + 2048;
-            if (threadIdx.x == 0) st_release_u32(flags + blockIdx.x * 32, g0 + k);
-            const long long t0 = clock64();
-            for (;;) {
-                bool ok = true;
-                for (int c = (int)threadIdx.x; c < G; c += 32) ok &= (int)(ld_acquire_u32(flags + c * 32) - (g0 + k)) >= 0;
-                if (__all_sync(0xffffffffu, ok)) break;
-                if (clock64() - t0 > EL_SPIN_LIMIT) __trap();
-            }
-        }
-    } else if ((st.dbg & 2048) && threadIdx.x == 0) {
-        const unsigned g = ld_acquire_u32(gen);
-        if (!(st.dbg & 1024)) __threadfence();
-        if (atom_add_acq_rel_u32(cnt, 1u) == (unsigned)G - 1) {
-            *(volatile unsigned*)cnt = 0u;
-            st_release_u32(gen, g + 1u);
+            st_release_u32(gen, g0 + k);
         } else {
-            const long long t0 = clock64();
-            while (ld_acquire_u32(gen) == g) {
+            while ((int)(ld_acquire_u32(gen) - (g0 + k)) < 0)
                 if (clock64() - t0 > EL_SPIN_LIMIT) __trap();
-            }
         }
-        if (!(st.dbg & 1024)) __threadfence();
-    } else if (!(st.dbg & 2048)) {  // D (default)
-        if (threadIdx.x == 0) {
-            red_release_add_u32(cnt, 1u);
-            const long long t0 = clock64();
-            if (blockIdx.x == 0) {
-                while (ld_acquire_u32(cnt) < (unsigned)G * k)
-                    if (clock64() - t0 > EL_SPIN_LIMIT) __trap();
-                st_release_u32(gen, g0 + k);
-            } else {
-                while ((int)(ld_acquire_u32(gen) - (g0 + k)) < 0)
-                    if (clock64() - t0 > EL_SPIN_LIMIT) __trap();
-            }
+        if ((dbg & 128) && blockIdx.x == 0 && nbar < 1024) {
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+            st.dbg_ts[20480 + nbar] = t;
         }
-    }
-    if (threadIdx.x == 0 && (st.dbg & 128) && blockIdx.x == 0 && nbar < 1024) {
-        unsigned long long t;
-        asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-        st.dbg_ts[20480 + nbar] = t;
     }
     ++nbar;
     __syncthreads();
-    if (!(st.dbg & 512)) fence_proxy_async_global();
+    fence_proxy_async_global();
 }
 
 // ---------------------------------------------------------------------------
@@ -776,6 +722,7 @@ __device__ __forceinline__ void unit_bm(IterSmem& sm, uint8_t* ring, const IterP
                              : "memory");
                 tma_load_3d(wbase, wmap, wf, wx, wy, wz, kL2EvictFirst);
             }
+            sm.tdbg[4] = clock64();  // producer starts issuing
             uint32_t s = cseq % (uint32_t)p.bm_stages, ph = (cseq / (uint32_t)p.bm_stages) & 1;
             bool wrapped = cseq >= (uint32_t)p.bm_stages;
             const uint32_t full0 = smem_u32(sm.full2), empty0 = smem_u32(sm.empty2);
@@ -802,9 +749,7 @@ __device__ __forceinline__ void unit_bm(IterSmem& sm, uint8_t* ring, const IterP
             const uint32_t idesc = idesc_bf16((uint32_t)p.bm_m, (uint32_t)nt);
             mbar_wait_addr(smem_u32(&sm.wfull), wseq & 1);
             if (lane == 0) {
-                unsigned long long t;
-                asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-                sm.tdbg[3] = t;
+                sm.tdbg[3] = clock64();
             }
             uint32_t s = cseq % (uint32_t)p.bm_stages, ph = (cseq / (uint32_t)p.bm_stages) & 1;
             const uint32_t full0 = smem_u32(sm.full2);
@@ -814,9 +759,7 @@ __device__ __forceinline__ void unit_bm(IterSmem& sm, uint8_t* ring, const IterP
                 const int kc = min(p.bm_kc, kb_total - c * p.bm_kc);
                 mbar_wait_addr(full0 + 8 * s, ph);
                 if (lane == 0 && (c == 0 || c == nch - 1)) {
-                    unsigned long long t;
-                    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-                    sm.tdbg[c == 0 ? 1 : 2] = t;
+                    sm.tdbg[c == 0 ? 1 : 2] = clock64();
                 }
                 tc_fence_after();
 #pragma unroll 1
@@ -838,9 +781,7 @@ __device__ __forceinline__ void unit_bm(IterSmem& sm, uint8_t* ring, const IterP
             cseq += (uint32_t)nch;
             ++wseq;
             if (lane == 0) {
-                unsigned long long t;
-                asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-                sm.tdbg[0] = t;  // MMA issue finished
+                sm.tdbg[0] = clock64();  // MMA issue finished
             }
             tc_commit_warp(&sm.acc);
         }
@@ -881,11 +822,8 @@ __device__ __forceinline__ void gemm_phase_t(const DevState& st, IterSmem& sm, u
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int U = g.m_tiles * kBM / g.nt;
     auto stamp = [&](int k) {  // dbg 64: per-CTA unit timeline of layer 1's batch-M GEMMs
-        if ((st.dbg & 64) && x.layer == 1 && threadIdx.x == 0) {
-            unsigned long long t;
-            asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-            st.dbg_ts[300000 + (size_t)blockIdx.x * 32 + K * 8 + k] = t;
-        }
+        if ((st.dbg & 64) && x.layer == 1 && threadIdx.x == 0)  // SM clock (globaltimer ticks are 256 ns)
+            st.dbg_ts[300000 + (size_t)blockIdx.x * 32 + K * 8 + k] = clock64();
     };
     stamp(0);
     for (int u = blockIdx.x; u < U; u += gridDim.x) {
@@ -896,7 +834,7 @@ __device__ __forceinline__ void gemm_phase_t(const DevState& st, IterSmem& sm, u
         wpf = false;
         stamp(2);
         if ((st.dbg & 64) && x.layer == 1 && threadIdx.x == 0)
-            for (int k = 0; k < 4; ++k) st.dbg_ts[300000 + (size_t)blockIdx.x * 32 + K * 8 + 4 + k] = sm.tdbg[k];
+            for (int k = 0; k < 5; ++k) st.dbg_ts[300000 + (size_t)blockIdx.x * 32 + K * 8 + (k < 4 ? 4 + k : 1)] = sm.tdbg[k];
         if (warp < 8) {
             // M = 128: batch row b in TMEM lane b.  M = 64: rows 16q..16q+15 in lanes 32q..32q+15.
             const bool m64 = p.bm_m == 64;
@@ -990,6 +928,7 @@ __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(DevState st, Iter
     uint8_t* ring = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     IterSmem& sm = *reinterpret_cast<IterSmem*>(ring + p.ring_bytes);
     float* tbuf = reinterpret_cast<float*>(ring + p.gemm_ring);
+    float* att_mbuf = p.att_mbuf_off > 0 ? reinterpret_cast<float*>(ring + p.att_mbuf_off) : nullptr;
     const int tid = threadIdx.x, warp = tid >> 5;
     const int G = (int)gridDim.x, cta = (int)blockIdx.x;
     const Dims& dm = st.dm;
@@ -1007,6 +946,8 @@ __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(DevState st, Iter
             mbar_init(&sm.empty2[s], 1);
         }
         mbar_init(&sm.wfull, 1);
+        sm.att.npend = 0;
+        sm.att.ids_layer[0] = sm.att.ids_layer[1] = -1;
         mbar_init(&sm.acc, 1);
         fence_barrier_init();
     }
@@ -1019,7 +960,7 @@ __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(DevState st, Iter
     }
     const int iter = *st.iter_counter;  // advanced by CTA 0 at the very end
     // generation base of this launch: no barrier of this launch can complete before every CTA read it
-    const unsigned g0 = (st.dbg & (4096 | 32768)) ? *(volatile unsigned*)(p.bar + 1025) : *(volatile unsigned*)(p.bar + 1024);
+    const unsigned g0 = *(volatile unsigned*)(p.bar + 1024);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -1043,8 +984,8 @@ __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(DevState st, Iter
             for (int b = tid & 31; b <= B; b += 32) sm.att.pref_c[b] = b * st.enc_blocks;
         __syncwarp();
     }
-    const AttnSrc self_src{st.tables, dm.bpl_max, st.kpool, st.vpool, 0, sm.att.pref};
-    const AttnSrc cross_src{st.ctables, st.enc_blocks, st.ckpool, st.cvpool, st.enc_len, sm.att.pref_c};
+    const AttnSrc self_src{st.tables, dm.bpl_max, st.kpool, st.vpool, 0, sm.att.pref, sm.pos, sm.slot, 0};
+    const AttnSrc cross_src{st.ctables, st.enc_blocks, st.ckpool, st.cvpool, st.enc_len, sm.att.pref_c, sm.pos, sm.slot, 1};
     // ---- embed (model.cpp:171-183): h_0 = embedding row of the input token ----
     for (int b = cta; b < B; b += G) {
         const uint16_t* e = st.emb + (size_t)st.rows.tok[b] * dp;
@@ -1087,6 +1028,7 @@ __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(DevState st, Iter
             }
         };
         astamp(0);
+        if ((st.dbg & 32) && tid == 0 && cta < 4) st.dbg_ts[8192 + 3072 + cta * 16] = clock64();
         if (tid == kProducerWarp * 32) wpf = bm_prefetch(sm, ring, p, maps, kIWo, layer);  // W_o under attention
         if (warp == kProducerWarp && (p.pf_flags & 1)) {  // this layer's W_o / up / down tiles -> L2
             l2_prefetch_gemm(p.g[kIWo], layer);
@@ -1094,7 +1036,7 @@ __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(DevState st, Iter
             l2_prefetch_gemm(p.g[kIDown], layer);
         }
         __syncwarp();
-        attn_body<NJ>(st, sm.att, ring, layer, aseq, true, self_src);
+        attn_body<NJ>(st, sm.att, ring, layer, aseq, true, self_src, att_mbuf);
         astamp(1);
         grid_sync(p, st, nbar, g0);
         aseq = sm.att.seq_next;
@@ -1129,7 +1071,7 @@ __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(DevState st, Iter
             }
             grid_sync(p, st, nbar, g0);
             if (tid == kProducerWarp * 32) wpf = bm_prefetch(sm, ring, p, maps, kIWoc, layer);
-            attn_body<NJ>(st, sm.att, ring, layer, aseq, true, cross_src);  // -> att_b
+            attn_body<NJ>(st, sm.att, ring, layer, aseq, true, cross_src, att_mbuf);  // -> att_b
             grid_sync(p, st, nbar, g0);
             aseq = sm.att.seq_next;
             if (p.g[kIWoc].mode) {
@@ -1220,8 +1162,7 @@ __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(DevState st, Iter
         if (cta == 0 && tid == 0) {
             for (int i = 0; i < kINumGemm * 64; ++i) p.tcnt[i] = 0u;  // all tile waits are behind us
             if (st.attn_queue) st.attn_queue[1] = 0;
-            if (!(st.dbg & (2048 | 4096 | 32768))) *(volatile unsigned*)p.bar = 0u;
-            if (st.dbg & (4096 | 32768)) *(volatile unsigned*)(p.bar + 1025) = g0 + (unsigned)nbar;
+            *(volatile unsigned*)p.bar = 0u;
         }
         tc_fence_before();
         __syncthreads();
@@ -1284,8 +1225,7 @@ __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(DevState st, Iter
     if (cta == 0 && tid == 0) {
         for (int i = 0; i < kINumGemm * 64; ++i) p.tcnt[i] = 0u;  // all tile waits are behind us
         if (st.attn_queue) st.attn_queue[1] = 0;  // layer 1 of the next launch (layer 2's is rearmed in layer 1)
-        if (!(st.dbg & (2048 | 4096 | 32768))) *(volatile unsigned*)p.bar = 0u;  // arrivals of this launch are all in
-        if (st.dbg & (4096 | 32768)) *(volatile unsigned*)(p.bar + 1025) = g0 + (unsigned)nbar;  // flag epochs continue
+        *(volatile unsigned*)p.bar = 0u;  // arrivals of this launch are all in
         rec_rec(st, iter % st.rec_cap)[2 * Bm] = e_out;
         *st.out_layer = e_out;
         *st.layer = e_out + 1;

@@ -702,6 +702,8 @@ void launch_gemm(GemmKind kind, const GemmPlan& p, const DevState& st, cudaStrea
 constexpr int kAttnWarps = 8;
 constexpr int kAttnThreads = (kAttnWarps + 1) * 32;
 
+constexpr int kAttnPend = 16;
+constexpr int kAttnIds = 256;  // deferred segment completions per CTA before a forced settle
 struct AttnDesc {
     int b, c, rows, first, last, nseg, pad[2];  // c = partial slot of this CTA's segment of sequence b
 };
@@ -716,26 +718,33 @@ struct AttnSmem {
     int pref_c[257];  // the same for the cross-attention (T5 mode) blocks: row b -> b * enc_blocks
     int last_flag;
     int seq_next;   // ring sequence base for the next pass
-    int pad;
+    int npend;      // segment partials published but not yet counted (see attn_settle)
+    int pend_b[kAttnPend], pend_n[kAttnPend], pend_last[kAttnPend];
+    // block ids of this CTA's static range, gathered before streaming (buffer 0: self
+    // attention, 1: cross attention); the persistent kernel gathers the next layer's
+    // at the end of a pass.  ids_layer / ids_g0: what a buffer holds (layer, range start)
+    int ids[2][kAttnIds];
+    int ids_layer[2], ids_g0[2];
 };
 
-__device__ __forceinline__ float dot8p(uint4 k, const float* q) {
-    const uint32_t w[4] = {k.x, k.y, k.z, k.w};
-    float a0 = 0.f, a1 = 0.f;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        a0 = fmaf(__uint_as_float(w[i] << 16), q[2 * i], a0);
-        a1 = fmaf(__uint_as_float(w[i] & 0xFFFF0000u), q[2 * i + 1], a1);
-    }
-    return a0 + a1;
+// bf16 pair -> (lo, hi) fp32 pair
+__device__ __forceinline__ float2 bf2_to_f2(uint32_t w) {
+    return make_float2(__uint_as_float(w << 16), __uint_as_float(w & 0xFFFF0000u));
 }
-__device__ __forceinline__ void axpy8(float p, uint4 v, float* o) {
-    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-        o[2 * e] = fmaf(p, __uint_as_float(w[e] << 16), o[2 * e]);
-        o[2 * e + 1] = fmaf(p, __uint_as_float(w[e] & 0xFFFF0000u), o[2 * e + 1]);
-    }
+// acc += k . q over 8 bf16 features, as (even, odd) partial sums (packed FFMA2)
+__device__ __forceinline__ float2 dot8p2(uint4 k, const float2* q, float2 acc) {
+    acc = __ffma2_rn(bf2_to_f2(k.x), q[0], acc);
+    acc = __ffma2_rn(bf2_to_f2(k.y), q[1], acc);
+    acc = __ffma2_rn(bf2_to_f2(k.z), q[2], acc);
+    return __ffma2_rn(bf2_to_f2(k.w), q[3], acc);
+}
+// o += p * v over 8 bf16 features (packed FFMA2)
+__device__ __forceinline__ void axpy8p2(float p, uint4 v, float2* o) {
+    const float2 pp = make_float2(p, p);
+    o[0] = __ffma2_rn(pp, bf2_to_f2(v.x), o[0]);
+    o[1] = __ffma2_rn(pp, bf2_to_f2(v.y), o[1]);
+    o[2] = __ffma2_rn(pp, bf2_to_f2(v.z), o[2]);
+    o[3] = __ffma2_rn(pp, bf2_to_f2(v.w), o[3]);
 }
 __device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 __device__ __forceinline__ int atom_add_acq_rel(int* p, int v) {
@@ -743,6 +752,12 @@ __device__ __forceinline__ int atom_add_acq_rel(int* p, int v) {
     asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
     return old;
 }
+
+// dbg 32: SM-clock stamps of the attention producer's start-up for CTAs 0..3 (slot k)
+#define EL_ATT_CLK(k)                                                                       \
+    do {                                                                                    \
+        if ((st.dbg & 32) && blockIdx.x < 4) st.dbg_ts[8192 + 3072 + blockIdx.x * 16 + (k)] = clock64(); \
+    } while (0)
 
 // One attention pass over layer `layer` (see the comment above). Shared by the
 // standalone kernel and the persistent iteration kernel; `seq0` continues the
@@ -758,6 +773,9 @@ struct AttnSrc {
     const uint16_t* vpool;
     int ctx_fixed;      // > 0: every row attends over this many positions (no position written this pass)
     const int* pref;    // shared-memory block prefix sum over the rows
+    const int* pos;     // rows' positions and KV slots (shared-memory copies in the persistent kernel)
+    const int* slot;
+    int idbuf;          // which a.ids buffer this pass uses (0 self, 1 cross)
 };
 
 // attn_prefix_sum: the warp-parallel prefix sum of KV blocks per row into a.pref
@@ -781,11 +799,107 @@ __device__ __forceinline__ void attn_prefix_sum(const DevState& st, AttnSmem& a)
     __syncwarp();
 }
 
+// Count the CTA's published segment partials (a.pend_*) and, for every sequence
+// whose last segment this was, combine all its partials in slot order (flash-
+// decoding) into the bf16 attention output.  Called by the 8 consumer warps
+// together: at the end of the pass (so the fence + atomic round trip and the
+// combine's L2 reads stay off the streaming loop) or when the list is full.
+__device__ __forceinline__ void attn_settle(const DevState& st, AttnSmem& a) {
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int dp = st.dm.dp, nchunk = dp / 8;
+    named_bar(1, kAttnWarps * 32);  // every partial store of this CTA is issued
+    const int np = a.npend;
+    if (np == 0) return;
+    // one acq_rel atomic per pending sequence, all in flight together (lanes of warp 0);
+    // release-cumulative over the CTA's partial stores ordered before it by bar.sync
+    if (warp == 0 && lane < np)
+        a.pend_last[lane] = (atom_add_acq_rel(&st.attn_cnt[a.pend_b[lane]], 1) == a.pend_n[lane] - 1);
+    named_bar(1, kAttnWarps * 32);
+    for (int i = 0; i < np; ++i) {
+        if (!a.pend_last[i]) continue;
+        const int b = a.pend_b[i], nch = a.pend_n[i];
+        const size_t pbase = (size_t)b * st.attn_max_chunks;
+        // the first partials' loads go out before the weights are known (one L2 round trip);
+        // indices past nch are clamped to a valid partial and weighted 0 below
+        constexpr int kPre = 4;
+        const int j = tid < nchunk ? tid : nchunk - 1;
+        float4 xp[kPre][2];
+#pragma unroll
+        for (int cc = 0; cc < kPre; ++cc) {
+            const float4* src = reinterpret_cast<const float4*>(st.attn_o + (pbase + min(cc, nch - 1)) * dp + j * 8);
+            xp[cc][0] = __ldcg(src);
+            xp[cc][1] = __ldcg(src + 1);
+        }
+        float* cw = a.cw;  // per-chunk weights exp(m_c - M) / L, computed once
+        if (warp == 0) {  // nch <= 128 (host guarantees)
+            float mc[4], lc[4];
+            float Mg = -INFINITY;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int cc = lane + 32 * u;
+                mc[u] = -INFINITY;
+                lc[u] = 0.f;
+                if (cc < nch) {
+                    const float2 ml = __ldcg(reinterpret_cast<const float2*>(st.attn_ml) + pbase + cc);
+                    mc[u] = ml.x;
+                    lc[u] = ml.y;
+                }
+                Mg = fmaxf(Mg, mc[u]);
+            }
+#pragma unroll
+            for (int off = 16; off; off >>= 1) Mg = fmaxf(Mg, __shfl_xor_sync(0xffffffffu, Mg, off));
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int cc = lane + 32 * u;
+                if (cc < nch) {
+                    cw[cc] = __expf(mc[u] - Mg);
+                    a.cl[cc] = cw[cc] * lc[u];
+                }
+            }
+            __syncwarp();
+            float Lg = 0.f;  // fixed chunk order: deterministic
+            for (int cc = 0; cc < nch; ++cc) Lg += a.cl[cc];
+            const float inv = 1.f / Lg;
+            __syncwarp();
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (lane + 32 * u < nch) cw[lane + 32 * u] *= inv;
+        }
+        named_bar(1, kAttnWarps * 32);
+        if (tid < nchunk) {  // (nchunk = dp / 8 <= 128 < 256 threads)
+            float acc[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) acc[e] = 0.f;
+            auto fma8 = [&](float w, float4 x0, float4 x1) {
+                acc[0] = fmaf(w, x0.x, acc[0]); acc[1] = fmaf(w, x0.y, acc[1]);
+                acc[2] = fmaf(w, x0.z, acc[2]); acc[3] = fmaf(w, x0.w, acc[3]);
+                acc[4] = fmaf(w, x1.x, acc[4]); acc[5] = fmaf(w, x1.y, acc[5]);
+                acc[6] = fmaf(w, x1.z, acc[6]); acc[7] = fmaf(w, x1.w, acc[7]);
+            };
+#pragma unroll
+            for (int cc = 0; cc < kPre; ++cc) fma8(cc < nch ? cw[cc] : 0.f, xp[cc][0], xp[cc][1]);
+            for (int cc = kPre; cc < nch; ++cc) {
+                const float4* src = reinterpret_cast<const float4*>(st.attn_o + (pbase + cc) * dp + j * 8);
+                fma8(cw[cc], __ldcg(src), __ldcg(src + 1));
+            }
+            uint32_t pk[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+                pk[e] = (uint32_t)f32_to_bf16(acc[2 * e]) | ((uint32_t)f32_to_bf16(acc[2 * e + 1]) << 16);
+            *reinterpret_cast<uint4*>(st.att_b + act_offset(b, j * 8, st.NR)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+        }
+        if (tid == 0) st.attn_cnt[b] = 0;
+        named_bar(1, kAttnWarps * 32);  // cw is rewritten by the next combine
+    }
+    if (tid == 0) a.npend = 0;
+    named_bar(1, kAttnWarps * 32);
+}
+
 // persistent: called from the persistent kernel -- a.pref is already valid and
 // no programmatic-dependent-launch deferral is needed (every input is ready).
 template <int NJ>
-__device__ void attn_body(const DevState& st, AttnSmem& a, uint8_t* stages, int layer, int seq0,
-                          bool persistent, const AttnSrc& src) {
+__device__ __forceinline__ void attn_body(const DevState& st, AttnSmem& a, uint8_t* stages, int layer, int seq0,
+                          bool persistent, const AttnSrc& src, float* mbuf) {
     const Dims& dm = st.dm;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int dp = dm.dp, nchunk = dp / 8;
@@ -802,6 +916,7 @@ __device__ void attn_body(const DevState& st, AttnSmem& a, uint8_t* stages, int 
         // streamed; q and the block holding `pos` (written by this layer's QKV
         // kernel) are requested after it (one pending stage).
         const int B = st.rows.B;
+        if (lane == 0) EL_ATT_CLK(1);
         if (!persistent) attn_prefix_sum(st, a);  // (standalone kernel: src.pref == a.pref)
         // Work split: the flattened (row, block) space [0, T) is cut into a static
         // head [0, Ts) -- CTA i streams [i*Ts/G, (i+1)*Ts/G), with fewer blocks than
@@ -810,24 +925,26 @@ __device__ void attn_body(const DevState& st, AttnSmem& a, uint8_t* stages, int 
         // range is done, so SMs that HBM serves faster take more of the tail.
         // Partial slots per row: static segments in CTA order, then tail items in
         // item order -- the combine order never depends on which CTA ran what.
-        const long long T = src.pref[B];
+        // (int arithmetic: T <= 256 rows x 128 blocks, products <= T * 148 -- no 64-bit division)
+        const int T = src.pref[B];
         const int cb = max(1, st.attn_dyn_cb);
-        const long long Td = (st.attn_dyn_permille > 0 && st.attn_queue)
+        const int Td = (st.attn_dyn_permille > 0 && st.attn_queue)
                                  ? min(T, (T * st.attn_dyn_permille / 1000 + cb - 1) / cb * cb) : 0;
-        const long long Ts = T - Td;
-        const long long n_items = (Td + cb - 1) / cb;
-        const long long G = min((long long)gridDim.x, Ts);
-        auto cta_of = [&](long long g) { return (int)(((g + 1) * G + Ts - 1) / Ts - 1); };
+        const int Ts = T - Td;
+        if (lane == 0) EL_ATT_CLK(10);
+        const int n_items = (Td + cb - 1) / cb;
+        const int G = min((int)gridDim.x, Ts);
+        auto cta_of = [&](int g) { return (int)(((g + 1) * G + Ts - 1) / Ts - 1); };
         // segment bookkeeping of row r: static segments and the first tail item touching it
         auto row_static = [&](int r, int& first_cta) {
-            const long long r0 = src.pref[r], r1 = min((long long)src.pref[r + 1], Ts);
+            const int r0 = src.pref[r], r1 = min((int)src.pref[r + 1], Ts);
             if (r0 >= r1) return 0;
             first_cta = cta_of(r0);
             return cta_of(r1 - 1) - first_cta + 1;
         };
-        auto row_items = [&](int r, long long& i0) {
-            const long long r0 = max((long long)src.pref[r], Ts), r1 = src.pref[r + 1];
-            if (r0 >= r1) return 0LL;
+        auto row_items = [&](int r, int& i0) {
+            const int r0 = max((int)src.pref[r], Ts), r1 = src.pref[r + 1];
+            if (r0 >= r1) return 0;
             i0 = (r0 - Ts) / cb;
             return (r1 - 1 - Ts) / cb - i0 + 1;
         };
@@ -853,24 +970,27 @@ __device__ void attn_body(const DevState& st, AttnSmem& a, uint8_t* stages, int 
         };
         int seq = seq0;
         // stream blocks [g, seg_end) of row b as one segment (partial slot `slot` of `nseg`)
-        auto emit = [&](int b, long long g, long long seg_end, int slot, int nseg) {
-            const long long sb0 = src.pref[b], sb1 = src.pref[b + 1];
+        // pid: the block ids of [g, seg_end) already in shared memory (a.ids), or nullptr
+        auto emit = [&](int b, int g, int seg_end, int slot, int nseg, const int* pid) {
+            const int sb0 = src.pref[b], sb1 = src.pref[b + 1];
             const int nblk = (int)(sb1 - sb0);
-            const int ctx = src.ctx_fixed > 0 ? src.ctx_fixed : st.rows.pos[b] + 1;
-            const int* table = src.tables + ((size_t)st.rows.slot[b] * dm.L + (layer - 1)) * src.tstride;
-            for (long long gb = g; gb < seg_end; gb += 32) {
+            const int ctx = src.ctx_fixed > 0 ? src.ctx_fixed : src.pos[b] + 1;
+            const int* table = src.tables + ((size_t)src.slot[b] * dm.L + (layer - 1)) * src.tstride;
+            for (int gb = g; gb < seg_end; gb += 32) {
                 const int blk_base = (int)(gb - sb0);
-                const int nb = (int)min(32LL, seg_end - gb);
-                const int my_id = (lane < nb) ? table[blk_base + lane] : 0;
+                const int nb = (int)min(32, seg_end - gb);
+                const int my_id = (lane < nb) ? (pid ? pid[gb - g + lane] : table[blk_base + lane]) : 0;
                 for (int u = 0; u < nb; ++u, ++seq) {
                     const int id = __shfl_sync(0xffffffffu, my_id, u);
                     const int blk = blk_base + u;
                     if (lane == 0) {
                         const int s = seq % S;
+                        if (seq == seq0) EL_ATT_CLK(8);
                         if (seq >= S) {
                             if (!waited) flush();  // the ring is full: release the deferred stage first
                             mbar_wait(&a.empty[s], ((seq / S) - 1) & 1);
                         }
+                        if (seq == seq0) EL_ATT_CLK(9);
                         const int rows = min(dm.bc, ctx - blk * dm.bc);
                         const uint32_t bytes = (uint32_t)rows * dp * 2;
                         const bool first = (gb + u) == g, newest = blk == nblk - 1;
@@ -881,6 +1001,7 @@ __device__ void attn_body(const DevState& st, AttnSmem& a, uint8_t* stages, int 
                             asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
                             st.dbg_ts[8192 + 1024 + blockIdx.x * 128 + seq] = t;
                         }
+                        if (seq == seq0) EL_ATT_CLK(3);
                         mbar_arrive_expect_tx(&a.full[s], 2 * bytes + (first ? (uint32_t)dp * 4 : 0u));
                         if (!waited && (first || newest) && ds >= 0) flush();  // one pending stage at most
                         if (!waited && (first || newest)) {
@@ -905,17 +1026,45 @@ __device__ void attn_body(const DevState& st, AttnSmem& a, uint8_t* stages, int 
             }
         };
         // ---- static head ----
-        if ((long long)blockIdx.x < G) {
-            const long long g0 = (long long)blockIdx.x * Ts / G, g1 = (long long)(blockIdx.x + 1) * Ts / G;
+        const bool has_static = (int)blockIdx.x < G;
+        const int g0 = has_static ? (int)blockIdx.x * Ts / G : 0;
+        const int g1 = has_static ? (int)(blockIdx.x + 1) * Ts / G : 0;
+        // the range's block ids are gathered before streaming (independent loads in
+        // parallel: a segment switch mid-range then costs no dependent table-load round
+        // trip); the persistent kernel gathers the next layer's at the end of this pass
+        const bool pre = has_static && g1 - g0 <= kAttnIds;
+        const int ib = src.idbuf;
+        auto gather = [&](int lay) {
+            for (int g = g0 + lane; g < g1; g += 32) {
+                int lo = 0, hi = B - 1;
+                while (lo < hi) {
+                    const int mid = (lo + hi + 1) >> 1;
+                    if (src.pref[mid] <= g) lo = mid;
+                    else hi = mid - 1;
+                }
+                a.ids[ib][g - g0] =
+                    src.tables[((size_t)src.slot[lo] * dm.L + (lay - 1)) * src.tstride + (int)(g - src.pref[lo])];
+            }
+            __syncwarp();
+            if (lane == 0) {
+                a.ids_layer[ib] = lay;
+                a.ids_g0[ib] = (int)g0;
+            }
+            __syncwarp();
+        };
+        if (lane == 0) EL_ATT_CLK(11);
+        if (pre && !(a.ids_layer[ib] == layer && a.ids_g0[ib] == (int)g0)) gather(layer);
+        if (has_static) {
+            if (lane == 0) EL_ATT_CLK(2);
             int b = 0;
             while (b < B && src.pref[b + 1] <= g0) ++b;
-            for (long long g = g0; g < g1 && b < B;) {
-                const long long seg_end = min(g1, (long long)src.pref[b + 1]);
+            for (int g = g0; g < g1 && b < B;) {
+                const int seg_end = min(g1, (int)src.pref[b + 1]);
                 int fc = 0;
                 const int ns = row_static(b, fc);
-                long long i0 = 0;
+                int i0 = 0;
                 const int nseg = ns + (int)row_items(b, i0);
-                emit(b, g, seg_end, (int)blockIdx.x - fc, nseg);
+                emit(b, g, seg_end, (int)blockIdx.x - fc, nseg, pre ? a.ids[ib] + (g - g0) : nullptr);
                 g = seg_end;
                 ++b;
             }
@@ -928,7 +1077,7 @@ __device__ void attn_body(const DevState& st, AttnSmem& a, uint8_t* stages, int 
             while (it < n_items) {
                 int nxt = 0;
                 if (lane == 0) nxt = atomicAdd(st.attn_queue + (layer & 1), 1);  // latency overlaps this item
-                const long long gs = Ts + (long long)it * cb, ge = min(T, gs + cb);
+                const int gs = Ts + (int)it * cb, ge = min(T, gs + cb);
                 int b = 0;
                 {  // row holding block gs (binary search on the prefix sums)
                     int lo = 0, hi = B - 1;
@@ -939,14 +1088,14 @@ __device__ void attn_body(const DevState& st, AttnSmem& a, uint8_t* stages, int 
                     }
                     b = lo;
                 }
-                for (long long g = gs; g < ge && b < B; ++b) {
-                    const long long seg_end = min(ge, (long long)src.pref[b + 1]);
+                for (int g = gs; g < ge && b < B; ++b) {
+                    const int seg_end = min(ge, (int)src.pref[b + 1]);
                     if (seg_end <= g) continue;
                     int fc = 0;
                     const int ns = row_static(b, fc);
-                    long long i0 = 0;
+                    int i0 = 0;
                     const int nseg = ns + (int)row_items(b, i0);
-                    emit(b, g, seg_end, ns + (int)(it - i0), nseg);
+                    emit(b, g, seg_end, ns + (int)(it - i0), nseg, nullptr);
                     g = seg_end;
                 }
                 it = __shfl_sync(0xffffffffu, nxt, 0);
@@ -959,14 +1108,16 @@ __device__ void attn_body(const DevState& st, AttnSmem& a, uint8_t* stages, int 
             a.desc[s].b = -1;
             mbar_arrive(&a.full[s]);
         }
+        if (persistent && pre && layer < dm.L) gather(layer + 1);  // while the consumers finish
     } else {
         // ---------------- consumer warps ----------------
-        float q[NJ][8], o[NJ][8];
+        float2 q[NJ][4], o[NJ][4];  // this lane's features 8j..8j+7, j = lane + 32t, as pairs
 #pragma unroll
         for (int t = 0; t < NJ; ++t)
 #pragma unroll
-            for (int i = 0; i < 8; ++i) q[t][i] = o[t][i] = 0.f;
+            for (int i = 0; i < 4; ++i) q[t][i] = o[t][i] = make_float2(0.f, 0.f);
         float m = -INFINITY, l = 0.f;
+        int npend = 0;
         const int r0 = warp, r1 = warp + kAttnWarps;
         // Persistent kernel: the consumer path is cold in the instruction cache at
         // the start of every pass (the other phases' code evicted it), so the
@@ -996,63 +1147,83 @@ __device__ void attn_body(const DevState& st, AttnSmem& a, uint8_t* stages, int 
                 if (seq == 0) st.dbg_ts[24576 + 4 * blockIdx.x + 1] = t;
                 st.dbg_ts[24576 + 4 * blockIdx.x + 2] = t;
             }
-            if (d.b < 0) break;
+            if (d.b < 0) {
+                if (tid == 0) EL_ATT_CLK(5);
+                break;
+            }
+            if (tid == 0 && seq == seq0 && !warm) EL_ATT_CLK(4);
             uint8_t* sb = stages + (size_t)s * stage_bytes;
             const uint4* sk = reinterpret_cast<const uint4*>(sb);
             const uint4* sv = reinterpret_cast<const uint4*>(sb + blk_bytes);
             if (d.first) {
-                const float* qs = reinterpret_cast<const float*>(sb + 2 * blk_bytes);
+                const float2* qs = reinterpret_cast<const float2*>(sb + 2 * blk_bytes);
 #pragma unroll
                 for (int t = 0; t < NJ; ++t) {
                     const int j = lane + 32 * t;
 #pragma unroll
-                    for (int i = 0; i < 8; ++i) {
-                        q[t][i] = (j < nchunk) ? qs[j * 8 + i] * st.attn_scale : 0.f;
-                        o[t][i] = 0.f;
+                    for (int i = 0; i < 4; ++i) {
+                        const float2 x = qs[min(j, nchunk - 1) * 4 + i];
+                        // features past dp (j >= nchunk) get q = 0: their (clamped) K loads add nothing
+                        q[t][i] = (j < nchunk) ? make_float2(x.x * st.attn_scale, x.y * st.attn_scale)
+                                               : make_float2(0.f, 0.f);
+                        o[t][i] = make_float2(0.f, 0.f);
                     }
                 }
                 m = -INFINITY;
                 l = 0.f;
             }
-            for (int rb = 0; rb < ((st.dbg & 1) ? 0 : d.rows); rb += 2 * kAttnWarps) {
-                const int ra = rb + r0, rc = rb + r1;
-                const bool va = ra < d.rows, vc = rc < d.rows;
-                float sa = 0.f, sc = 0.f;
+            // Branch-free block math: both rows' K and V are loaded up front (row indices
+            // clamped to valid rows, feature chunks clamped to the last one), an invalid
+            // second row gets score -inf (weight 0 times finite data).
+            const int nrows = (st.dbg & 1) ? 0 : d.rows;
+            for (int rb = 0; rb < nrows; rb += 2 * kAttnWarps) {
+                const int ra = rb + r0;
+                if (ra >= nrows) break;  // warp-uniform: no row of this warp left in the block
+                const bool vc = rb + r1 < nrows;
+                const int rc = vc ? rb + r1 : ra;
+                uint4 ka[NJ], kc[NJ], xa[NJ], xc[NJ];
 #pragma unroll
                 for (int t = 0; t < NJ; ++t) {
-                    const int j = lane + 32 * t;
-                    if (j < nchunk) {
-                        if (va) sa += dot8p(sk[ra * nchunk + j], q[t]);
-                        if (vc) sc += dot8p(sk[rc * nchunk + j], q[t]);
-                    }
+                    const int j = min(lane + 32 * t, nchunk - 1);
+                    ka[t] = sk[ra * nchunk + j];
+                    kc[t] = sk[rc * nchunk + j];
                 }
+#pragma unroll
+                for (int t = 0; t < NJ; ++t) {
+                    const int j = min(lane + 32 * t, nchunk - 1);
+                    xa[t] = sv[ra * nchunk + j];
+                    xc[t] = sv[rc * nchunk + j];
+                }
+                float2 a2 = make_float2(0.f, 0.f), c2 = make_float2(0.f, 0.f);
+#pragma unroll
+                for (int t = 0; t < NJ; ++t) {
+                    a2 = dot8p2(ka[t], q[t], a2);
+                    c2 = dot8p2(kc[t], q[t], c2);
+                }
+                float sa = a2.x + a2.y, sc = c2.x + c2.y;
 #pragma unroll
                 for (int off = 16; off; off >>= 1) {
                     sa += __shfl_xor_sync(0xffffffffu, sa, off);
                     sc += __shfl_xor_sync(0xffffffffu, sc, off);
                 }
-                if (!va) sa = -INFINITY;
                 if (!vc) sc = -INFINITY;
                 const float m_new = fmaxf(m, fmaxf(sa, sc));
-                if (m_new == -INFINITY) continue;  // this warp has no rows here
                 const float pa = __expf(sa - m_new), pc = __expf(sc - m_new);
-                if (m_new != m) {
+                if (m_new != m) {  // warp-uniform
                     const float alpha = __expf(m - m_new);
+                    const float2 al = make_float2(alpha, alpha);
                     l *= alpha;
 #pragma unroll
                     for (int t = 0; t < NJ; ++t)
 #pragma unroll
-                        for (int i = 0; i < 8; ++i) o[t][i] *= alpha;
+                        for (int i = 0; i < 4; ++i) o[t][i] = __fmul2_rn(o[t][i], al);
                     m = m_new;
                 }
                 l += pa + pc;
 #pragma unroll
                 for (int t = 0; t < NJ; ++t) {
-                    const int j = lane + 32 * t;
-                    if (j < nchunk) {
-                        if (va) axpy8(pa, sv[ra * nchunk + j], o[t]);
-                        if (vc) axpy8(pc, sv[rc * nchunk + j], o[t]);
-                    }
+                    axpy8p2(pa, xa[t], o[t]);
+                    axpy8p2(pc, xc[t], o[t]);
                 }
             }
             if ((st.dbg & 32) && tid == 0 && blockIdx.x < 4 && seq < 60) {  // block processed (before release)
@@ -1071,10 +1242,14 @@ __device__ void attn_body(const DevState& st, AttnSmem& a, uint8_t* stages, int 
                 continue;
             }
 
-            // ---- end of item: merge the 8 warps in fixed order inside this
-            //      (fully consumed, not yet released) stage buffer ----
-            named_bar(1, kAttnWarps * 32);
-            float* merge = reinterpret_cast<float*>(sb);  // [8][dp] fp32 <= 2 * blk_bytes
+            // ---- end of segment: merge the 8 warps in fixed order, publish the
+            //      segment's partial (o, m, l) and queue its completion count ----
+            float* merge = mbuf ? mbuf : reinterpret_cast<float*>(sb);  // [8][dp] fp32
+            if (mbuf) {  // the stage is free as soon as this warp is done with it
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&a.empty[s]);
+            }
+            named_bar(1, kAttnWarps * 32);  // (also: the previous merge's readers are done with mbuf / wm / wl)
             if (lane == 0) {
                 a.wm[warp] = m;
                 a.wl[warp] = l;
@@ -1084,8 +1259,8 @@ __device__ void attn_body(const DevState& st, AttnSmem& a, uint8_t* stages, int 
                 const int j = lane + 32 * t;
                 if (j < nchunk) {
                     float4* dst = reinterpret_cast<float4*>(merge + (size_t)warp * dp + j * 8);
-                    dst[0] = make_float4(o[t][0], o[t][1], o[t][2], o[t][3]);
-                    dst[1] = make_float4(o[t][4], o[t][5], o[t][6], o[t][7]);
+                    dst[0] = make_float4(o[t][0].x, o[t][0].y, o[t][1].x, o[t][1].y);
+                    dst[1] = make_float4(o[t][2].x, o[t][2].y, o[t][3].x, o[t][3].y);
                 }
             }
             named_bar(1, kAttnWarps * 32);
@@ -1108,75 +1283,21 @@ __device__ void attn_body(const DevState& st, AttnSmem& a, uint8_t* stages, int 
             if (tid == 0) {
                 st.attn_ml[pidx * 2 + 0] = M;
                 st.attn_ml[pidx * 2 + 1] = Lsum;
+                a.pend_b[a.npend] = d.b;
+                a.pend_n[a.npend] = d.nseg;
+                ++a.npend;
             }
-            named_bar(1, kAttnWarps * 32);  // all partial stores issued (ordered by the release below)
-            if (lane == 0) mbar_arrive(&a.empty[s]);
-            const int nch = d.nseg;
-            if (tid == 0) {
-                asm volatile("fence.acq_rel.gpu;" ::: "memory");  // publish the CTA's partial (bar.sync-ordered)
-                a.last_flag = (atom_add_acq_rel(&st.attn_cnt[d.b], 1) == nch - 1);
-            }
-            named_bar(1, kAttnWarps * 32);
-            if (a.last_flag) {
-                const size_t pbase = (size_t)d.b * st.attn_max_chunks;
-                float* cw = a.cw;  // per-chunk weights exp(m_c - M) / L, computed once
-                if (warp == 0) {  // nch <= 128 (host guarantees)
-                    float mc[4], lc[4];
-                    float Mg = -INFINITY;
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        const int cc = lane + 32 * u;
-                        mc[u] = -INFINITY;
-                        lc[u] = 0.f;
-                        if (cc < nch) {
-                            const float2 ml = __ldcg(reinterpret_cast<const float2*>(st.attn_ml) + pbase + cc);
-                            mc[u] = ml.x;
-                            lc[u] = ml.y;
-                        }
-                        Mg = fmaxf(Mg, mc[u]);
-                    }
-#pragma unroll
-                    for (int off = 16; off; off >>= 1) Mg = fmaxf(Mg, __shfl_xor_sync(0xffffffffu, Mg, off));
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        const int cc = lane + 32 * u;
-                        if (cc < nch) {
-                            cw[cc] = __expf(mc[u] - Mg);
-                            a.cl[cc] = cw[cc] * lc[u];
-                        }
-                    }
-                    __syncwarp();
-                    float Lg = 0.f;  // fixed chunk order: deterministic
-                    for (int cc = 0; cc < nch; ++cc) Lg += a.cl[cc];
-                    const float inv = 1.f / Lg;
-                    __syncwarp();
-#pragma unroll
-                    for (int u = 0; u < 4; ++u)
-                        if (lane + 32 * u < nch) cw[lane + 32 * u] *= inv;
-                }
+            if (!mbuf) {  // the merge lived in the stage: release it once every warp has read it
                 named_bar(1, kAttnWarps * 32);
-                for (int j = tid; j < nchunk; j += kAttnWarps * 32) {
-                    float acc[8];
-#pragma unroll
-                    for (int e = 0; e < 8; ++e) acc[e] = 0.f;
-                    for (int cc = 0; cc < nch; ++cc) {
-                        const float w = cw[cc];
-                        const float4* src = reinterpret_cast<const float4*>(st.attn_o + (pbase + cc) * dp + j * 8);
-                        const float4 x0 = __ldcg(src), x1 = __ldcg(src + 1);
-                        acc[0] = fmaf(w, x0.x, acc[0]); acc[1] = fmaf(w, x0.y, acc[1]);
-                        acc[2] = fmaf(w, x0.z, acc[2]); acc[3] = fmaf(w, x0.w, acc[3]);
-                        acc[4] = fmaf(w, x1.x, acc[4]); acc[5] = fmaf(w, x1.y, acc[5]);
-                        acc[6] = fmaf(w, x1.z, acc[6]); acc[7] = fmaf(w, x1.w, acc[7]);
-                    }
-                    uint32_t pk[4];
-#pragma unroll
-                    for (int e = 0; e < 4; ++e)
-                        pk[e] = (uint32_t)f32_to_bf16(acc[2 * e]) | ((uint32_t)f32_to_bf16(acc[2 * e + 1]) << 16);
-                    *reinterpret_cast<uint4*>(st.att_b + act_offset(d.b, j * 8, st.NR)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-                }
-                if (tid == 0) st.attn_cnt[d.b] = 0;
+                if (lane == 0) mbar_arrive(&a.empty[s]);
+            }
+            if (++npend == kAttnPend || (st.dbg & 8)) {  // (npend: every consumer thread's own count)
+                attn_settle(st, a);
+                npend = 0;
             }
         }
+        attn_settle(st, a);
+        if (tid == 0) EL_ATT_CLK(6);
         pdl_trigger();
     }
 }
@@ -1200,11 +1321,13 @@ __global__ void __launch_bounds__(kAttnThreads) attn_kernel(DevState st) {
             mbar_init(&a.full[s], 1);
             mbar_init(&a.empty[s], kAttnWarps);
         }
+        a.npend = 0;
+        a.ids_layer[0] = a.ids_layer[1] = -1;
         fence_barrier_init();
     }
     __syncthreads();
-    const AttnSrc src{st.tables, st.dm.bpl_max, st.kpool, st.vpool, 0, a.pref};
-    attn_body<NJ>(st, a, stages, layer, 0, false, src);
+    const AttnSrc src{st.tables, st.dm.bpl_max, st.kpool, st.vpool, 0, a.pref, st.rows.pos, st.rows.slot, 0};
+    attn_body<NJ>(st, a, stages, layer, 0, false, src, nullptr);
     if ((st.dbg & 32) && tid == 0) {
         unsigned long long t;
         asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));

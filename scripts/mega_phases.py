@@ -41,7 +41,7 @@ pi = e.plan_info()
 per_layer = []
 for nm in ("qkv", "attn", "wo", "up", "down"):
     per_layer.append(nm)
-    if nm == "down" or (nm != "attn" and not pi[f"mega_{nm}_mode"]):
+    if not opts.get("mega_fused_reduce", 1) and (nm == "down" or (nm != "attn" and not pi[f"mega_{nm}_mode"])):
         per_layer.append(nm + "_red")
 print({k: v for k, v in pi.items() if k.startswith("mega")})
 if tech == "softmax":
@@ -81,24 +81,18 @@ for layer in (0, eo - 1):
     order = np.argsort(dur)
     print("   slowest CTAs:", order[-8:].tolist(), "fastest:", order[:8].tolist())
 
-# batch-M GEMM unit timeline of layer 1 (dbg 64): [start, -, acc ready, epilogue done] per CTA
+# batch-M GEMM unit timeline of layer 1 (dbg 64), SM clock cycles:
+# [0 start, 1 producer issues, 2 acc ready, 3 epilogue done, 4 MMA issue done, 5 chunk0 full, 6 last chunk full,
+#  7 weights ready]
 U = ts[300000:300000 + 148 * 32].reshape(148, 4, 8).astype(np.float64)
-arrv = ts[65536:65536 + 148 * 1024].reshape(148, 1024).astype(np.float64)
+MHZ = 1965.0
 for k, nm in ((0, "qkv"), (1, "wo"), (2, "up")):
     u = U[:, k]
     ok = (u[:, 0] > 0) & (u[:, 2] > 0)
     if not ok.any():
         continue
-    t0 = u[ok, 0].min()
-    st_ = (u[ok, 0] - t0) / 1e3
-    acc = (u[ok, 2] - u[ok, 0]) / 1e3
-    epi = (u[ok, 3] - u[ok, 2]) / 1e3
-    # this CTA's arrival at the next grid barrier (first arrival stamp after its epilogue)
-    arr = np.array([min([a for a in arrv[c] if a >= u[c, 3]] or [np.nan]) for c in np.where(ok)[0]])
-    tail = (arr - u[ok, 3]) / 1e3
-    rel = lambda j: (u[ok, j] - u[ok, 0]) / 1e3
-    print(f"{nm}: MMA issue done p50 {np.median(rel(4)):.2f} | weights ready p50 {np.median(rel(7)):.2f} | chunk0 full p50 "
-          f"{np.median(rel(5)):.2f} | last chunk full p50 {np.median(rel(6)):.2f} max {rel(6).max():.2f}")
-    print(f"{nm}: start skew p50 {np.median(st_):.2f} max {st_.max():.2f} | start->acc p50 {np.median(acc):.2f} max "
-          f"{acc.max():.2f} | epilogue p50 {np.median(epi):.2f} max {epi.max():.2f} | epi->arrive p50 "
-          f"{np.nanmedian(tail):.2f} max {np.nanmax(tail):.2f} | last arrival {(np.nanmax(arr) - t0) / 1e3:.2f} us")
+    rel = lambda j: (u[ok, j] - u[ok, 0]) / MHZ
+    print(f"{nm:4s} (n={ok.sum():3d} CTAs, us from phase start, p50/max): producer issue {np.median(rel(1)):.2f}/{rel(1).max():.2f}"
+          f" | weights {np.median(rel(7)):.2f}/{rel(7).max():.2f} | chunk0 {np.median(rel(5)):.2f}/{rel(5).max():.2f}"
+          f" | last chunk {np.median(rel(6)):.2f}/{rel(6).max():.2f} | MMA issued {np.median(rel(4)):.2f}/{rel(4).max():.2f}"
+          f" | acc {np.median(rel(2)):.2f}/{rel(2).max():.2f} | epilogue done {np.median(rel(3)):.2f}/{rel(3).max():.2f}")
