@@ -1057,7 +1057,14 @@ __device__ __forceinline__ void attn_body(const DevState& st, AttnSmem& a, uint8
         if (has_static) {
             if (lane == 0) EL_ATT_CLK(2);
             int b = 0;
-            while (b < B && src.pref[b + 1] <= g0) ++b;
+            {  // first row of the range: largest b with pref[b] <= g0 (binary search)
+                int hi = B - 1;
+                while (b < hi) {
+                    const int mid = (b + hi + 1) >> 1;
+                    if (src.pref[mid] <= g0) b = mid;
+                    else hi = mid - 1;
+                }
+            }
             for (int g = g0; g < g1 && b < B;) {
                 const int seg_end = min(g1, (int)src.pref[b + 1]);
                 int fc = 0;
@@ -1125,7 +1132,7 @@ __device__ __forceinline__ void attn_body(const DevState& st, AttnSmem& a, uint8
         // math once on whatever the first stage holds while its data is still in
         // flight (results are discarded: the first real descriptor of a pass is
         // always a segment start, which resets q, o, m, l).
-        bool warm = persistent;
+        bool warm = persistent && !(st.dbg & (1 << 21));
         for (int seq = seq0;; ++seq) {
             const int s = seq % S;
             AttnDesc d;
@@ -1300,6 +1307,14 @@ __device__ __forceinline__ void attn_body(const DevState& st, AttnSmem& a, uint8
         if (tid == 0) EL_ATT_CLK(6);
         pdl_trigger();
     }
+}
+
+// The persistent kernel's attention pass: one out-of-line copy for the self and the
+// cross pass (st points at the kernel's shared-memory copy of the parameters).
+template <int NJ>
+__device__ __forceinline__ void attn_pass(const DevState& st, AttnSmem& a, uint8_t* stages, int layer, int seq0,
+                                       const AttnSrc src, float* mbuf) {
+    attn_body<NJ>(st, a, stages, layer, seq0, true, src, mbuf);
 }
 
 template <int NJ>

@@ -96,3 +96,19 @@ for k, nm in ((0, "qkv"), (1, "wo"), (2, "up")):
           f" | weights {np.median(rel(7)):.2f}/{rel(7).max():.2f} | chunk0 {np.median(rel(5)):.2f}/{rel(5).max():.2f}"
           f" | last chunk {np.median(rel(6)):.2f}/{rel(6).max():.2f} | MMA issued {np.median(rel(4)):.2f}/{rel(4).max():.2f}"
           f" | acc {np.median(rel(2)):.2f}/{rel(2).max():.2f} | epilogue done {np.median(rel(3)):.2f}/{rel(3).max():.2f}")
+u = U[:, 3]
+ok = (u[:, 0] > 0) & (u[:, 4] > 0)
+if ok.any():
+    rel = lambda j: (u[ok, j] - u[ok, 0]) / MHZ
+    print(f"down (fused split-K, n={ok.sum()} CTAs with a unit, us p50/max): acc ready {np.median(rel(1)):.2f}/{rel(1).max():.2f}"
+          f" | partial stored {np.median(rel(2)):.2f}/{rel(2).max():.2f} | tile complete {np.median(rel(3)):.2f}/{rel(3).max():.2f}"
+          f" | reduced {np.median(rel(4)):.2f}/{rel(4).max():.2f}")
+    print(f"     mainloop: first stage full {np.median(rel(5)):.2f}/{rel(5).max():.2f} | last stage full "
+          f"{np.median(rel(6)):.2f}/{rel(6).max():.2f} | producer done {np.median(rel(7)):.2f}/{rel(7).max():.2f}")
+R = ts[310000:310000 + 148 * 8].reshape(148, 8).astype(np.float64)
+okr = R[:, 0] > 0
+if okr.any():
+    rr = lambda j: (R[okr, j] - R[okr, 0]) / MHZ
+    print(f"down reduce (warp 0, us from reduce start p50/max): side loads issued {np.median(rr(1)):.2f}/{rr(1).max():.2f}"
+          f" | partials summed {np.median(rr(2)):.2f}/{rr(2).max():.2f} | h stored {np.median(rr(3)):.2f}/{rr(3).max():.2f}"
+          f" | exit dots {np.median(rr(4)):.2f}/{rr(4).max():.2f}")
