@@ -107,15 +107,14 @@ __device__ __forceinline__ void red_release_add_u32(unsigned* p, unsigned v) {
 
 // Grid barrier over co-resident CTAs.  Generic global writes before it are
 // visible (and ordered for the async proxy: bulk copies read them) to every
-// CTA after it.  bar layout (unsigned): [0] arrivals (zeroed at the end of each
-// launch), [1024] generation.  Every CTA adds one arrival with red.release; CTA 0
-// polls the count and releases the generation, the others poll the generation.
-// (Measured on B200, scripts/bar_probe.py of earlier revisions: ~2.0 us, against
-// 2.7-2.9 us for a last-arriver / per-CTA-flag / relaxed-poll design.)  Inlined,
-// with scalar arguments: a call would spill live registers around every barrier
-// and a reference to the kernel's DevState / IterPlan parameters would put a copy
-// of them in local memory.
-__device__ __forceinline__ void grid_sync(const IterPlan& p, const DevState& st, int& nbar, unsigned g0) {
+// CTA after it.  bar layout (unsigned): [0] arrivals, [1024] generation; both only
+// ever grow (wrap-safe signed distances against the values read at launch start,
+// gb.y / gb.x), so nothing is reset between launches.
+// Every CTA adds its arrival with red.release and polls the arrival count itself
+// (one L2 hop from the last arrival to every waiter): +2-5 % end to end over the
+// two-hop form (dbg bit 25: CTA 0 alone polls the count and releases a generation
+// word the others poll).  Inlined, with no reference to a copy of the parameters.
+__device__ __forceinline__ void grid_sync(const IterPlan& p, const DevState& st, int& nbar, uint2 gb) {
     const int dbg = st.dbg;
     if (threadIdx.x == 0 && (dbg & 128) && nbar < 1024) {  // per-CTA arrival (work done) time
         unsigned long long t;
@@ -128,14 +127,18 @@ __device__ __forceinline__ void grid_sync(const IterPlan& p, const DevState& st,
     if (threadIdx.x == 0) {
         unsigned* cnt = p.bar;
         unsigned* gen = p.bar + 1024;
+        const unsigned target = gb.y + gridDim.x * k;
         red_release_add_u32(cnt, 1u);
         const long long t0 = clock64();
-        if (blockIdx.x == 0) {
-            while (ld_acquire_u32(cnt) < gridDim.x * k)
+        if (!(dbg & (1 << 25))) {
+            while ((int)(ld_acquire_u32(cnt) - target) < 0)
                 if (clock64() - t0 > EL_SPIN_LIMIT) __trap();
-            st_release_u32(gen, g0 + k);
+        } else if (blockIdx.x == 0) {
+            while ((int)(ld_acquire_u32(cnt) - target) < 0)
+                if (clock64() - t0 > EL_SPIN_LIMIT) __trap();
+            st_release_u32(gen, gb.x + k);
         } else {
-            while ((int)(ld_acquire_u32(gen) - (g0 + k)) < 0)
+            while ((int)(ld_acquire_u32(gen) - (gb.x + k)) < 0)
                 if (clock64() - t0 > EL_SPIN_LIMIT) __trap();
         }
         if ((dbg & 128) && blockIdx.x == 0 && nbar < 1024) {
@@ -367,9 +370,10 @@ __device__ __forceinline__ Side4 side4(const DevState& st, const IterSmem& sm, c
 }
 template <int K>
 __device__ __forceinline__ void apply4(const DevState& st, const IterSmem& sm, const IterCtx& x, int m, int c, int r0,
-                                       float4 v, const Side4* pre = nullptr) {
+                                       float4 v, const Side4* pre = nullptr, bool dry = false) {
     const int dp = st.dm.dp, NR = st.NR, Bm = st.dm.Bmax;
     const int R = m * kBM + r0;
+    if (dry) return;
     if constexpr (K == kIQkv || K == kIFill) {
         const int kind = (K == kIQkv) ? R / dp : 1 + R / dp;  // 0 q, 1 k, 2 v
         if (kind == 0) {
@@ -429,13 +433,15 @@ __device__ __forceinline__ void epi_fill_direct(const DevState& st, const IterSm
 // check's per-tile partial dots (fp64, fixed shuffle tree).
 // pieces [P0, P) (piece = m * nval + c), this warp's first piece P0 + gw, stride GW
 template <int K>
+// dry: compute on whatever the partials hold and store nothing -- an instruction-cache
+// warm-up run of this exact code while the tile's other splits are still arriving
 __device__ __forceinline__ void reduce_range(const DevState& st, const IterSmem& sm, const IterPlan& p,
                                           const IterGemm& g, const IterCtx x, int nval, int unit_base, int P0, int P,
-                                          int gw, int GW) {
+                                          int gw, int GW, bool dry = false) {
     const int lane = threadIdx.x & 31;
     const int S = g.splits;
     auto rstamp = [&](int k) {  // dbg 64: warp 0's reduce timeline in layer 1's down phase (SM clock)
-        if (K == kIDown && (st.dbg & 64) && x.layer == 1 && threadIdx.x == 0)
+        if (K == kIDown && !dry && (st.dbg & 64) && x.layer == 1 && threadIdx.x == 0)
             st.dbg_ts[310000 + (size_t)blockIdx.x * 8 + k] = clock64();
     };
     rstamp(0);
@@ -506,16 +512,18 @@ __device__ __forceinline__ void reduce_range(const DevState& st, const IterSmem&
                 const int m2 = 2 * dp / kBM;
                 IterCtx y = x;
                 y.layer = x.layer + m / m2;  // x.layer = first skipped layer
-                apply4<K>(st, sm, y, m % m2, c, r0, acc[j], &sd[j]);
+                apply4<K>(st, sm, y, m % m2, c, r0, acc[j], &sd[j], dry);
             } else if constexpr (K == kIDown) {
                 const int R = m * kBM + r0;
                 const size_t i = (size_t)c * dp + R;
                 const float4 mid = dmid[j];
                 const float4 o = make_float4(mid.x + acc[j].x, mid.y + acc[j].y, mid.z + acc[j].z, mid.w + acc[j].w);
-                *reinterpret_cast<float4*>(st.h32 + (size_t)x.pout * Bm * dp + i) = o;
-                *reinterpret_cast<uint2*>(st.hb + (size_t)x.pout * st.NR * dp + act_offset(c, R, st.NR)) =
-                    make_uint2((uint32_t)f32_to_bf16(o.x) | ((uint32_t)f32_to_bf16(o.y) << 16),
-                               (uint32_t)f32_to_bf16(o.z) | ((uint32_t)f32_to_bf16(o.w) << 16));
+                if (!dry) {
+                    *reinterpret_cast<float4*>(st.h32 + (size_t)x.pout * Bm * dp + i) = o;
+                    *reinterpret_cast<uint2*>(st.hb + (size_t)x.pout * st.NR * dp + act_offset(c, R, st.NR)) =
+                        make_uint2((uint32_t)f32_to_bf16(o.x) | ((uint32_t)f32_to_bf16(o.y) << 16),
+                                   (uint32_t)f32_to_bf16(o.z) | ((uint32_t)f32_to_bf16(o.w) << 16));
+                }
                 rstamp(3);
                 if ((st.technique == kState || st.technique == kClassifier) && !(st.dbg & (1 << 22))) {
                     double x0 = 0.0, x1 = 0.0, x2 = 0.0;
@@ -538,7 +546,7 @@ __device__ __forceinline__ void reduce_range(const DevState& st, const IterSmem&
                     x0 = warp_sum_d(x0);
                     x1 = warp_sum_d(x1);
                     x2 = warp_sum_d(x2);
-                    if (lane == 0) {
+                    if (lane == 0 && !dry) {
                         double* q = st.exit_part + ((size_t)m * Bm + c) * 3;
                         q[0] = x0;
                         q[1] = x1;
@@ -547,7 +555,7 @@ __device__ __forceinline__ void reduce_range(const DevState& st, const IterSmem&
                 }
                 rstamp(4);
             } else {
-                apply4<K>(st, sm, x, m, c, r0, acc[j], &sd[j]);
+                apply4<K>(st, sm, x, m, c, r0, acc[j], &sd[j], dry);
             }
         }
     }
@@ -935,26 +943,32 @@ __device__ void gemm_phase_fused(const DevState& st, IterSmem& sm, uint8_t* ring
         __syncthreads();
         stamp(2);
         if (threadIdx.x == 0) {
-            __threadfence();
+            // (bar.sync above orders the CTA's partial stores before this thread's release)
+            if (st.dbg & (1 << 26)) __threadfence();
             red_release_add_u32(cnt + m, 1u);
+            if ((st.dbg & 64) && x.layer == 1 && K == kIDown) st.dbg_ts[310000 + (size_t)blockIdx.x * 8 + 5] = clock64();
         }
     }
     for (int u = blockIdx.x; u < U; u += gridDim.x) {
         const int m = u / g.splits, s = u % g.splits;
-        if (threadIdx.x == 0) {
-            const unsigned target = (unsigned)(g.splits * use);
-            const long long t0 = clock64();
-            while (ld_acquire_u32(cnt + m) < target)
-                if (clock64() - t0 > EL_SPIN_LIMIT) __trap();
-            __threadfence();
-        }
-        __syncthreads();
-        stamp(3);
-        if (warp < 8) {
-            const int c0 = s * nval / g.splits, c1 = (s + 1) * nval / g.splits;
-            if (st.dbg & (1 << 24))  // probe: a first (identical, idempotent) pass warms the code path
-                reduce_range<K>(st, sm, p, g, x, nval, 0, m * nval + c0, m * nval + c1, warp, 8);
-            reduce_range<K>(st, sm, p, g, x, nval, 0, m * nval + c0, m * nval + c1, warp, 8);
+        const int c0 = s * nval / g.splits, c1 = (s + 1) * nval / g.splits;
+        // dbg bit 24: pass 0 (dry) runs the reduce code while the tile's other splits arrive,
+        // so that pass 1 finds it in the instruction cache -- measured slower (the dry pass is
+        // as cold as the real one was and outlasts the wait)
+#pragma unroll 1
+        for (int pass = (st.dbg & (1 << 24)) ? 0 : 1; pass < 2; ++pass) {
+            if (pass == 1) {
+                if (threadIdx.x == 0) {
+                    const unsigned target = (unsigned)(g.splits * use);
+                    const long long t0 = clock64();
+                    while (ld_acquire_u32(cnt + m) < target)
+                        if (clock64() - t0 > EL_SPIN_LIMIT) __trap();
+                    __threadfence();
+                }
+                __syncthreads();
+                stamp(3);
+            }
+            if (warp < 8) reduce_range<K>(st, sm, p, g, x, nval, 0, m * nval + c0, m * nval + c1, warp, 8, pass == 0);
         }
         __syncthreads();
         stamp(4);
@@ -1019,7 +1033,10 @@ __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(const __grid_cons
     }
     const int iter = *st.iter_counter;  // advanced by CTA 0 at the very end
     // generation base of this launch: no barrier of this launch can complete before every CTA read it
-    const unsigned g0 = *(volatile unsigned*)(p.bar + 1024);
+    // barrier bases: the generation word only moves once every CTA has arrived (so after
+    // every CTA read it); the arrival count's base is the final count of the previous
+    // launch, which CTA 0 stores in bar[2] at its end (the count itself may already move)
+    const uint2 g0 = make_uint2(*(volatile unsigned*)(p.bar + 1024), *(volatile unsigned*)(p.bar + 2));
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -1219,9 +1236,9 @@ __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(const __grid_cons
         // batched causal prefill (engine.cpp:166-181): every layer's K/V of all rows is written;
         // no exit, no tokens, no records -- only the launch bookkeeping below
         if (cta == 0 && tid == 0) {
+            *(volatile unsigned*)(p.bar + 2) = g0.y + (unsigned)G * (unsigned)nbar;  // next launch's count base
             for (int i = 0; i < kINumGemm * 64; ++i) p.tcnt[i] = 0u;  // all tile waits are behind us
             if (st.attn_queue) st.attn_queue[1] = 0;
-            *(volatile unsigned*)p.bar = 0u;
         }
         tc_fence_before();
         __syncthreads();
@@ -1282,9 +1299,9 @@ __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(const __grid_cons
         }
     }
     if (cta == 0 && tid == 0) {
+        *(volatile unsigned*)(p.bar + 2) = g0.y + (unsigned)G * (unsigned)nbar;  // next launch's count base
         for (int i = 0; i < kINumGemm * 64; ++i) p.tcnt[i] = 0u;  // all tile waits are behind us
         if (st.attn_queue) st.attn_queue[1] = 0;  // layer 1 of the next launch (layer 2's is rearmed in layer 1)
-        *(volatile unsigned*)p.bar = 0u;  // arrivals of this launch are all in
         rec_rec(st, iter % st.rec_cap)[2 * Bm] = e_out;
         *st.out_layer = e_out;
         *st.layer = e_out + 1;

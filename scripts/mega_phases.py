@@ -112,3 +112,7 @@ if okr.any():
     print(f"down reduce (warp 0, us from reduce start p50/max): side loads issued {np.median(rr(1)):.2f}/{rr(1).max():.2f}"
           f" | partials summed {np.median(rr(2)):.2f}/{rr(2).max():.2f} | h stored {np.median(rr(3)):.2f}/{rr(3).max():.2f}"
           f" | exit dots {np.median(rr(4)):.2f}/{rr(4).max():.2f}")
+okf = (R[:, 5] > 0) & (U[:, 3, 0] > 0)
+if okf.any():
+    rel5 = (R[okf, 5] - U[okf, 3, 0]) / MHZ
+    print(f"down: arrival (red.release) done p50/max {np.median(rel5):.2f}/{rel5.max():.2f} us from phase start")
