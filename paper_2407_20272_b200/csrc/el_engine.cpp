@@ -223,10 +223,10 @@ struct el_engine {
     DevBuf<unsigned> mtcnt;              // its per-tile split-K arrival counters
     int mega_grid = 0, mega_att_stages = 2, sms = 148;
     int opt_mega_fill_splits = 0, opt_mega_att_stages = 0, opt_mega_pf = 0, opt_mega_kv_pf_mb = 0,
-        opt_mega_bm_max = 128, opt_attn_dyn_permille = 0, opt_attn_dyn_cb = 4, opt_mega_bm_prefetch = 1,
+        opt_mega_bm_max = 256, opt_attn_dyn_permille = 0, opt_attn_dyn_cb = 4, opt_mega_bm_prefetch = 1,
         opt_mega_bm_chunk_kb = 0, opt_mega_bm_act_policy = 0, opt_mega_bm_nt_min = 16,
         opt_mega_bm_m128 = 0, opt_mega_bm_down = 0, opt_mega_att_l2 = 0, opt_mega_down_splits = 0,
-        opt_mega_splits_cap = 8, opt_mega_fused_reduce = 1, opt_att_mbuf = 1;
+        opt_mega_splits_cap = 0, opt_mega_fused_reduce = 1, opt_att_mbuf = 1;
     int attn_cb = 1, attn_stages = 2, attn_max_chunks = 1, attn_grid = 148;
     int NR = 16;
 
@@ -556,9 +556,12 @@ struct el_engine {
 
     // ---- persistent decode-iteration kernel plan ----
     // split-K: aim at one unit per CTA (units = m_tiles * splits <= grid), >= 2 splits
-    int mega_splits(int m_tiles, int kb_total) const {
+    // cap (fewer splits: less partial traffic to reduce): 8, or 16 at batch >= 256 where the
+    // mainloop of a unit dominates (measured c5 -1.6 %, c3 -0.5 %, c2 +1.3 % with 16)
+    int mega_splits(int m_tiles, int kb_total, int n_pad) const {
         int s = std::max(1, mega_grid / m_tiles);
-        s = std::min({s, kb_total, opt_mega_splits_cap});  // fewer splits: less partial traffic to reduce
+        const int cap = opt_mega_splits_cap ? opt_mega_splits_cap : (n_pad >= 256 ? 16 : 8);
+        s = std::min({s, kb_total, cap});
         return std::max(s, std::min(2, kb_total));
     }
     el::IterPlan& mplan_for(int B, int nr_override = 0) {
@@ -589,29 +592,32 @@ struct el_engine {
             x.nt = 0;
             return x;
         };
-        P.g[el::kIQkv] = g(wqkv.p, 3 * dp / 128, dp / 64, 3 * dp / 128, 0, mega_splits(3 * dp / 128, dp / 64));
-        P.g[el::kIWo] = g(wo.p, dp / 128, dp / 64, dp / 128, 0, mega_splits(dp / 128, dp / 64));
-        P.g[el::kIUp] = g(wup.p, fp / 128, dp / 64, fp / 128, 0, mega_splits(fp / 128, dp / 64));
+        P.g[el::kIQkv] = g(wqkv.p, 3 * dp / 128, dp / 64, 3 * dp / 128, 0, mega_splits(3 * dp / 128, dp / 64, n_pad));
+        P.g[el::kIWo] = g(wo.p, dp / 128, dp / 64, dp / 128, 0, mega_splits(dp / 128, dp / 64, n_pad));
+        P.g[el::kIUp] = g(wup.p, fp / 128, dp / 64, fp / 128, 0, mega_splits(fp / 128, dp / 64, n_pad));
         P.g[el::kIDown] = g(wdown.p, dp / 128, fp / 64, dp / 128, 0,
                             opt_mega_down_splits ? std::min(opt_mega_down_splits, fp / 64)
-                                                 : mega_splits(dp / 128, fp / 64));
+                                                 : mega_splits(dp / 128, fp / 64, n_pad));
         // fill: full-K units (direct epilogue) at large N, where split-K partials would outweigh the weights
-        P.g[el::kIQc] = g(wqc.p, dp / 128, dp / 64, dp / 128, 0, mega_splits(dp / 128, dp / 64));
-        P.g[el::kIWoc] = g(woc.p, dp / 128, dp / 64, dp / 128, 0, mega_splits(dp / 128, dp / 64));
+        P.g[el::kIQc] = g(wqc.p, dp / 128, dp / 64, dp / 128, 0, mega_splits(dp / 128, dp / 64, n_pad));
+        P.g[el::kIWoc] = g(woc.p, dp / 128, dp / 64, dp / 128, 0, mega_splits(dp / 128, dp / 64, n_pad));
         int fs = opt_mega_fill_splits ? opt_mega_fill_splits : (n_pad >= 128 ? 1 : std::min(4, dp / 64));
         fs = std::min(fs, dp / 64);
         P.g[el::kIFill] = g(wqkv.p, 2 * dp / 128, dp / 64, 3 * dp / 128, dp / 128, fs);
         P.n_pad = n_pad;
         // batch-M full-K GEMMs (no split-K reduce phase) for QKV / W_o / up at small batch
         int nt_max = 16, bm_w = 0;  // bm_w: the largest unit weight slab (nt rows x K)
-        if (n_pad <= opt_mega_bm_max) {
+        // batch > 128: units cover 128-row groups of an activation layout with 128-row multiples
+        const bool bm = n_pad <= opt_mega_bm_max && (n_pad <= 128 || NR % 128 == 0);
+        if (bm) {
             for (int k : {el::kIQkv, el::kIWo, el::kIUp, el::kIQc, el::kIWoc, el::kIDown}) {
                 // down (K = 4d): batch-M only at batch <= 64, where its 16-row weight slab fits
                 if (k == el::kIDown && (n_pad > 64 || !opt_mega_bm_down)) continue;
                 el::IterGemm& x = P.g[k];
                 const int F = x.m_tiles * 128;
+                const int R = n_pad > 128 ? 2 : 1;  // row groups of 128 batch rows
                 int nt = k == el::kIDown ? 16 : opt_mega_bm_nt_min;
-                while (nt < 128 && F / nt > mega_grid) nt *= 2;
+                while (nt < 128 && F / nt * R > mega_grid) nt *= 2;
                 x.mode = 1;
                 x.nt = nt;
                 bm_w = std::max(bm_w, x.kb_total * nt * 128);
@@ -624,30 +630,33 @@ struct el_engine {
         // The batch-M weight buffer sits at the end of the ring region (bm_woff), past the attention
         // stages, the batch-M activation stages and the weight-streaming ring + LM transpose buffer,
         // so a prefetch into it never collides with the phase in flight.
-        const bool bm = n_pad <= opt_mega_bm_max;
         const int ring_att = mega_att_stages * att_stage;
         P.bm_rows = NR;
-        P.bm_kc = std::max(1, std::min(dp / 64, (opt_mega_bm_chunk_kb ? opt_mega_bm_chunk_kb * 1024 : 32768) / (NR * 128)));
+        P.bm_grp = n_pad > 128 ? 128 : NR;  // batch > 128: units cover one 128-row group
+        P.bm_kc = std::max(1, std::min(dp / 64, (opt_mega_bm_chunk_kb ? opt_mega_bm_chunk_kb * 1024 : 32768) /
+                                                     (P.bm_grp * 128)));
         P.bm_act_policy = opt_mega_bm_act_policy;
         P.bm_m = (n_pad <= 64 && !opt_mega_bm_m128) ? 64 : 128;
         P.att_l2_blocks = opt_mega_att_l2;
         P.fused_reduce = opt_mega_fused_reduce;
         P.tcnt = mtcnt.p;
-        P.bm_astage = P.bm_kc * NR * 128;
+        P.bm_astage = P.bm_kc * P.bm_grp * 128;
         (void)nt_max;
         P.bm_woff = (cap - bm_w) / 1024 * 1024;
         P.bm_stages = std::max(2, std::min(4, (P.bm_woff - 16384) / P.bm_astage));
         if (bm && P.bm_stages * P.bm_astage > P.bm_woff)
             fail(EL_INVALID_ARGUMENT, "persistent kernel: batch-M ring does not fit");
         P.bm_prefetch = (bm && opt_mega_bm_prefetch && ring_att <= P.bm_woff) ? 1 : 0;
-        const int ws_cap = bm ? P.bm_woff : cap;  // weight-streaming ring + transpose buffer stay below it
+        // weight-streaming ring + transpose buffer stay below the weight buffer when weights are
+        // prefetched into it during other phases
+        const int ws_cap = (bm && P.bm_prefetch) ? P.bm_woff : cap;
         P.stages = std::min(8, (ws_cap - el::kIterTbufBytes) / stage);
         if (P.stages < 2) fail(EL_INVALID_ARGUMENT, "persistent kernel: GEMM ring does not fit");
         P.gemm_ring = P.stages * stage;
         // attention merge buffer right after the attention stages (a segment's stage is released
         // before its merge) when it fits below the batch-M weight buffer
         const int mbuf = 8 * dp * 4;
-        P.att_mbuf_off = (opt_att_mbuf && ring_att + mbuf <= (bm ? P.bm_woff : cap)) ? ring_att : 0;
+        P.att_mbuf_off = (opt_att_mbuf && ring_att + mbuf <= ((bm && P.bm_prefetch) ? P.bm_woff : cap)) ? ring_att : 0;
         P.ring_bytes = round_up(std::max({ring_att + (P.att_mbuf_off ? mbuf : 0), P.gemm_ring + el::kIterTbufBytes,
                                           P.bm_stages * P.bm_astage + 16384, bm ? P.bm_woff + bm_w : 0}), 1024);
         P.lm_tiles = dm.Vp / 128;

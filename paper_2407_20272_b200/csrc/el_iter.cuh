@@ -763,7 +763,11 @@ __device__ __forceinline__ void unit_bm(IterSmem& sm, uint8_t* ring, const IterP
                                      const uint32_t wseq, const CUtensorMap* wmap, int wx, int wy, int wz,
                                      const uint16_t* act, int kb_total, int nt, uint32_t useq, bool w_ready) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t NRb = (uint32_t)p.bm_rows * 128u;  // bytes of one activation k-block
+    // act: this unit's row group (rows r*bm_grp ..) of k-block 0; one k-block of it is
+    // NRb bytes in shared memory; with several row groups a k-block's group is not
+    // contiguous with the next k-block's in global memory (stride bm_rows rows)
+    const uint32_t NRb = (uint32_t)p.bm_grp * 128u;
+    const bool grouped = p.bm_grp != p.bm_rows;
     const int nch = (kb_total + p.bm_kc - 1) / p.bm_kc;
     const uint32_t ring0 = smem_u32(ring), wbase = ring0 + (uint32_t)p.bm_woff;
     if (warp == kProducerWarp) {
@@ -785,8 +789,15 @@ __device__ __forceinline__ void unit_bm(IterSmem& sm, uint8_t* ring, const IterP
                 if (wrapped) mbar_wait_addr(empty0 + 8 * s, ph ^ 1);
                 const uint32_t fb = full0 + 8 * s, bytes = (uint32_t)kc * NRb;
                 asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(fb), "r"(bytes) : "memory");
-                bulk_load_hint(ring0 + s * (uint32_t)p.bm_astage, act + (size_t)c * p.bm_kc * p.bm_rows * kBK, bytes,
-                               fb, (p.bm_act_policy & 1) ? kL2EvictFirst : kL2EvictLast);
+                const uint64_t pol = (p.bm_act_policy & 1) ? kL2EvictFirst : kL2EvictLast;
+                if (!grouped) {
+                    bulk_load_hint(ring0 + s * (uint32_t)p.bm_astage, act + (size_t)c * p.bm_kc * p.bm_rows * kBK,
+                                   bytes, fb, pol);
+                } else {
+                    for (int j = 0; j < kc; ++j)
+                        bulk_load_hint(ring0 + s * (uint32_t)p.bm_astage + (uint32_t)j * NRb,
+                                       act + (size_t)(c * p.bm_kc + j) * p.bm_rows * kBK, NRb, fb, pol);
+                }
                 if (++s == (uint32_t)p.bm_stages) {
                     s = 0;
                     ph ^= 1;
@@ -850,8 +861,9 @@ __device__ __forceinline__ bool bm_prefetch(IterSmem& sm, uint8_t* ring, const I
                                             int gid, int layer) {
     const IterGemm& g = p.g[gid];
     if (!g.mode || !p.bm_prefetch) return false;
-    if ((int)blockIdx.x >= g.m_tiles * kBM / g.nt) return false;
-    const int f0 = (int)blockIdx.x * g.nt;
+    const int R = p.bm_rows / p.bm_grp;  // this CTA's first unit: (feature group cta / R, row group cta % R)
+    if ((int)blockIdx.x >= g.m_tiles * kBM / g.nt * R) return false;
+    const int f0 = ((int)blockIdx.x / R) * g.nt;
     const int row_block = (layer - 1) * g.layer_rows + g.row_off + f0 / kBM;
     const uint32_t wf = smem_u32(&sm.wfull);
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(wf),
@@ -869,17 +881,18 @@ __device__ __forceinline__ void gemm_phase_t(const DevState& st, IterSmem& sm, u
                                              int next_gid, int next_layer) {
     const IterGemm& g = p.g[gid];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int U = g.m_tiles * kBM / g.nt;
+    const int R = p.bm_rows / p.bm_grp;  // row groups: unit u = (feature group u / R, row group u % R)
+    const int U = g.m_tiles * kBM / g.nt * R;
     auto stamp = [&](int k) {  // dbg 64: per-CTA unit timeline of layer 1's batch-M GEMMs
         if ((st.dbg & 64) && x.layer == 1 && threadIdx.x == 0)  // SM clock (globaltimer ticks are 256 ns)
             st.dbg_ts[300000 + (size_t)blockIdx.x * 32 + K * 8 + k] = clock64();
     };
     stamp(0);
     for (int u = blockIdx.x; u < U; u += gridDim.x) {
-        const int f0 = u * g.nt;
+        const int f0 = (u / R) * g.nt, rg = u % R;
         const int row_block = (x.layer - 1) * g.layer_rows + g.row_off + f0 / kBM;
-        unit_bm(sm, ring, p, cseq, wseq, &maps.w[gid], 0, f0 % kBM, row_block * g.kb_total, act, g.kb_total, g.nt,
-                useq, wpf);
+        unit_bm(sm, ring, p, cseq, wseq, &maps.w[gid], 0, f0 % kBM, row_block * g.kb_total,
+                act + (size_t)rg * p.bm_grp * kBK, g.kb_total, g.nt, useq, wpf);
         cseq += (uint32_t)((g.kb_total + p.bm_kc - 1) / p.bm_kc);
         ++wseq;
         wpf = false;
@@ -889,7 +902,7 @@ __device__ __forceinline__ void gemm_phase_t(const DevState& st, IterSmem& sm, u
         if (warp < 8) {
             // M = 128: batch row b in TMEM lane b.  M = 64: rows 16q..16q+15 in lanes 32q..32q+15.
             const bool m64 = p.bm_m == 64;
-            const int b = m64 ? 16 * (warp & 3) + lane : 32 * (warp & 3) + lane;
+            const int b = rg * p.bm_grp + (m64 ? 16 * (warp & 3) + lane : 32 * (warp & 3) + lane);
             const bool valid = b < B && (!m64 || lane < 16);
             const uint32_t trow = sm.tmem + ((uint32_t)(32 * (warp & 3)) << 16);
             for (int c0 = 16 * (warp >> 2); c0 < g.nt; c0 += 32) {
@@ -1218,7 +1231,7 @@ __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(const __grid_cons
             e_out = layer;
             // the next layer's QKV weights were prefetched for nothing: retire that load
             const IterGemm& gq = p.g[kIQkv];
-            if (layer < L && gq.mode && p.bm_prefetch && cta < gq.m_tiles * kBM / gq.nt) {
+            if (layer < L && gq.mode && p.bm_prefetch && cta < gq.m_tiles * kBM / gq.nt * (p.bm_rows / p.bm_grp)) {
                 if (warp == 0) {  // the MMA warp retires it
                     mbar_wait(&sm.wfull, wseq & 1);
                     ++wseq;

@@ -204,6 +204,7 @@ struct IterPlan {
     int bm_prefetch;  // issue each batch-M unit's weights one phase ahead (weight buffer outside the rings)
     int bm_act_policy;  // L2 hint of the activation copies: 0 evict-last, 1 evict-first (probe)
     int bm_m;           // UMMA M of the batch-M GEMMs: 64 (batch <= 64) or 128
+    int bm_grp;         // batch rows per unit (row group): bm_rows, or 128 when the batch has 2 groups
     int map_key;        // host-side key of this plan's tensor maps
     int fused_reduce;   // split-K: per-tile arrival counters + the tile's CTAs reduce (no grid barrier)
     unsigned* tcnt;     // [kINumGemm][64] per-tile arrival counters (zeroed at the end of each launch)

@@ -279,12 +279,13 @@ def test_bench_config_c2_parity(port, mega):
     e.close()
 
 
-@pytest.mark.parametrize("B,tech", [(16, "classifier"), (136, "state")])
+@pytest.mark.parametrize("B,tech", [(16, "classifier"), (136, "state"), (256, "classifier")])
 def test_persistent_kernel_deterministic_and_matches_per_phase(B, tech):
     """The persistent kernel is run-to-run bitwise deterministic (fixed split-K
     and attention-partial reduction orders, no atomics on values) and agrees
     with the per-phase kernels within the bf16 tolerance; B = 136 exercises the
-    split-K + reduce GEMM path (batch > 128), B = 16 the batch-M path."""
+    split-K + reduce GEMM path (activation rows not a multiple of 128), B = 16
+    the batch-M path, B = 256 batch-M over two 128-row groups."""
     L, d, V = 5, 256, 1024
     outs = []
     for mega in (True, True, False):
