@@ -226,7 +226,7 @@ struct el_engine {
         opt_mega_bm_max = 256, opt_attn_dyn_permille = 0, opt_attn_dyn_cb = 4, opt_mega_bm_prefetch = 1,
         opt_mega_bm_chunk_kb = 0, opt_mega_bm_act_policy = 0, opt_mega_bm_nt_min = 16,
         opt_mega_bm_m128 = 0, opt_mega_bm_down = 0, opt_mega_att_l2 = 0, opt_mega_down_splits = 0,
-        opt_mega_splits_cap = 0, opt_mega_fused_reduce = 1, opt_att_mbuf = 1;
+        opt_mega_splits_cap = 0, opt_mega_fused_reduce = 1, opt_att_mbuf = 1, opt_mega_att_l2_late = 0;
     int attn_cb = 1, attn_stages = 2, attn_max_chunks = 1, attn_grid = 148;
     int NR = 16;
 
@@ -638,6 +638,7 @@ struct el_engine {
         P.bm_act_policy = opt_mega_bm_act_policy;
         P.bm_m = (n_pad <= 64 && !opt_mega_bm_m128) ? 64 : 128;
         P.att_l2_blocks = opt_mega_att_l2;
+        P.att_l2_late = opt_mega_att_l2_late;
         P.fused_reduce = opt_mega_fused_reduce;
         P.tcnt = mtcnt.p;
         P.bm_astage = P.bm_kc * P.bm_grp * 128;
@@ -1363,6 +1364,10 @@ int el_engine_set_option(el_engine* e, const char* key, int64_t v) {
         e->opt_attn_dyn_cb = (int)v;
     } else if (!std::strcmp(key, "mega_bm_chunk_kb") || !std::strcmp(key, "mega_bm_act_policy")) {
         (key[8] == 'c' ? e->opt_mega_bm_chunk_kb : e->opt_mega_bm_act_policy) = (int)v;
+        e->mplans.clear();
+    } else if (!std::strcmp(key, "mega_att_l2_late")) {
+        if (v < 0 || v > 64) fail(EL_INVALID_ARGUMENT, "mega_att_l2_late must be in [0, 64]");
+        e->opt_mega_att_l2_late = (int)v;
         e->mplans.clear();
     } else if (!std::strcmp(key, "att_mbuf")) {
         e->opt_att_mbuf = v != 0;

@@ -1104,6 +1104,9 @@ __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(const __grid_cons
             grid_sync(p, st, nbar, g0);
             reduce_phase<kIQkv>(st, sm, p, p.g[kIQkv], x, B, 0, p.g[kIQkv].m_tiles);
         }
+        // this CTA's first attention blocks -> L2 while the grid waits at the barrier (no
+        // competition with the QKV loads, which are done)
+        if (warp == kProducerWarp && p.att_l2_late > 0) l2_prefetch_kv(st, sm.att, layer, p.att_l2_late);
         grid_sync(p, st, nbar, g0);
         // paged attention (model.cpp:223-243)
         auto astamp = [&](int w) {
