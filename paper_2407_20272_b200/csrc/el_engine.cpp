@@ -226,7 +226,7 @@ struct el_engine {
         opt_mega_bm_max = 256, opt_attn_dyn_permille = 0, opt_attn_dyn_cb = 4, opt_mega_bm_prefetch = 1,
         opt_mega_bm_chunk_kb = 0, opt_mega_bm_act_policy = 0, opt_mega_bm_nt_min = 16,
         opt_mega_bm_m128 = 0, opt_mega_bm_down = 0, opt_mega_att_l2 = 0, opt_mega_down_splits = 0,
-        opt_mega_splits_cap = 0, opt_mega_fused_reduce = 1, opt_att_mbuf = 1, opt_mega_att_l2_late = 0;
+        opt_mega_splits_cap = 0, opt_mega_fused_reduce = 1, opt_att_mbuf = 1, opt_mega_att_l2_late = 0, opt_mega_att_early = 1;
     int attn_cb = 1, attn_stages = 2, attn_max_chunks = 1, attn_grid = 148;
     int NR = 16;
 
@@ -601,7 +601,7 @@ struct el_engine {
         // fill: full-K units (direct epilogue) at large N, where split-K partials would outweigh the weights
         P.g[el::kIQc] = g(wqc.p, dp / 128, dp / 64, dp / 128, 0, mega_splits(dp / 128, dp / 64, n_pad));
         P.g[el::kIWoc] = g(woc.p, dp / 128, dp / 64, dp / 128, 0, mega_splits(dp / 128, dp / 64, n_pad));
-        int fs = opt_mega_fill_splits ? opt_mega_fill_splits : (n_pad >= 128 ? 1 : std::min(4, dp / 64));
+        int fs = opt_mega_fill_splits ? opt_mega_fill_splits : (n_pad >= 128 ? 1 : 2);  // (c2: 2 < 3 < 4 < 1)
         fs = std::min(fs, dp / 64);
         P.g[el::kIFill] = g(wqkv.p, 2 * dp / 128, dp / 64, 3 * dp / 128, dp / 128, fs);
         P.n_pad = n_pad;
@@ -639,6 +639,7 @@ struct el_engine {
         P.bm_m = (n_pad <= 64 && !opt_mega_bm_m128) ? 64 : 128;
         P.att_l2_blocks = opt_mega_att_l2;
         P.att_l2_late = opt_mega_att_l2_late;
+        P.att_early = opt_mega_att_early;
         P.fused_reduce = opt_mega_fused_reduce;
         P.tcnt = mtcnt.p;
         P.bm_astage = P.bm_kc * P.bm_grp * 128;
@@ -1368,6 +1369,9 @@ int el_engine_set_option(el_engine* e, const char* key, int64_t v) {
     } else if (!std::strcmp(key, "mega_att_l2_late")) {
         if (v < 0 || v > 64) fail(EL_INVALID_ARGUMENT, "mega_att_l2_late must be in [0, 64]");
         e->opt_mega_att_l2_late = (int)v;
+        e->mplans.clear();
+    } else if (!std::strcmp(key, "mega_att_early")) {
+        e->opt_mega_att_early = v != 0;
         e->mplans.clear();
     } else if (!std::strcmp(key, "att_mbuf")) {
         e->opt_att_mbuf = v != 0;

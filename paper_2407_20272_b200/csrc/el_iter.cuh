@@ -152,6 +152,29 @@ __device__ __forceinline__ void grid_sync(const IterPlan& p, const DevState& st,
     fence_proxy_async_global();
 }
 
+// The same barrier for warps 0-7 only (named barrier 2): the producer warp skips it and
+// starts the next attention pass, whose q / newest-block loads wait on the count.
+__device__ __forceinline__ void grid_sync_sub(const IterPlan& p, const DevState& st, int& nbar, uint2 gb) {
+    fence_proxy_async_global();
+    asm volatile("bar.sync 2, 256;" ::: "memory");
+    const unsigned k = (unsigned)nbar + 1u;
+    if (threadIdx.x == 0) {
+        unsigned* cnt = p.bar;
+        const unsigned target = gb.y + gridDim.x * k;
+        red_release_add_u32(cnt, 1u);
+        const long long t0 = clock64();
+        while ((int)(ld_acquire_u32(cnt) - target) < 0)
+            if (clock64() - t0 > EL_SPIN_LIMIT) __trap();
+        if ((st.dbg & 128) && blockIdx.x == 0 && nbar < 1024) {
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+            st.dbg_ts[20480 + nbar] = t;
+        }
+    }
+    ++nbar;
+    asm volatile("bar.sync 2, 256;" ::: "memory");
+}
+
 // ---------------------------------------------------------------------------
 // GEMM unit: TMEM[0, n_pad) = sum_{kb in [kb0, kb0+nkb)} W_tile(kb) . X_tile(kb)^T
 // producer = warp 8 lane 0, MMA issuer = warp 0 lane 0.  On return the
@@ -1073,8 +1096,8 @@ __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(const __grid_cons
             for (int b = tid & 31; b <= B; b += 32) sm.att.pref_c[b] = b * st.enc_blocks;
         __syncwarp();
     }
-    const AttnSrc self_src{st.tables, dm.bpl_max, st.kpool, st.vpool, 0, sm.att.pref, sm.pos, sm.slot, 0};
-    const AttnSrc cross_src{st.ctables, st.enc_blocks, st.ckpool, st.cvpool, st.enc_len, sm.att.pref_c, sm.pos, sm.slot, 1};
+    const AttnSrc self_src{st.tables, dm.bpl_max, st.kpool, st.vpool, 0, sm.att.pref, sm.pos, sm.slot, 0, nullptr, 0u};
+    const AttnSrc cross_src{st.ctables, st.enc_blocks, st.ckpool, st.cvpool, st.enc_len, sm.att.pref_c, sm.pos, sm.slot, 1, nullptr, 0u};
     // ---- embed (model.cpp:171-183): h_0 = embedding row of the input token ----
     for (int b = cta; b < B; b += G) {
         const uint16_t* e = st.emb + (size_t)st.rows.tok[b] * dp;
@@ -1107,7 +1130,19 @@ __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(const __grid_cons
         // this CTA's first attention blocks -> L2 while the grid waits at the barrier (no
         // competition with the QKV loads, which are done)
         if (warp == kProducerWarp && p.att_l2_late > 0) l2_prefetch_kv(st, sm.att, layer, p.att_l2_late);
-        grid_sync(p, st, nbar, g0);
+        // early attention start (default; barrier-mode 1-hop only): the producer warp skips
+        // this barrier and streams the old K/V blocks of its range while the grid waits; q and
+        // the newest block (this phase's output) wait on the barrier count
+        AttnSrc self_l = self_src;
+        const bool early = p.att_early && !(st.dbg & ((1 << 25) | (1 << 27)));
+        if (early) {
+            self_l.gate = p.bar;
+            self_l.gate_target = g0.y + (unsigned)G * (unsigned)(nbar + 1);
+            if (warp == kProducerWarp) ++nbar;
+            else grid_sync_sub(p, st, nbar, g0);
+        } else {
+            grid_sync(p, st, nbar, g0);
+        }
         // paged attention (model.cpp:223-243)
         auto astamp = [&](int w) {
             if ((st.dbg & 128) && tid == 0 && layer <= 24) {
@@ -1128,7 +1163,7 @@ __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(const __grid_cons
             l2_prefetch_gemm(p.g[kIDown], layer);
         }
         __syncwarp();
-        attn_pass<NJ>(st, sm.att, ring, layer, aseq, self_src, att_mbuf);
+        attn_pass<NJ>(st, sm.att, ring, layer, aseq, self_l, att_mbuf);
         astamp(1);
         grid_sync(p, st, nbar, g0);
         aseq = sm.att.seq_next;

@@ -776,6 +776,10 @@ struct AttnSrc {
     const int* pos;     // rows' positions and KV slots (shared-memory copies in the persistent kernel)
     const int* slot;
     int idbuf;          // which a.ids buffer this pass uses (0 self, 1 cross)
+    // gate != nullptr: the producer starts before the grid barrier that publishes this
+    // layer's q and newest K/V rows; those loads wait until *gate reaches gate_target
+    const unsigned* gate;
+    unsigned gate_target;
 };
 
 // attn_prefix_sum: the warp-parallel prefix sum of KV blocks per row into a.pref
@@ -948,12 +952,25 @@ __device__ __forceinline__ void attn_body(const DevState& st, AttnSmem& a, uint8
             i0 = (r0 - Ts) / cb;
             return (r1 - 1 - Ts) / cb - i0 + 1;
         };
-        bool waited = persistent;  // PDL secondary: defer q / the newest block until griddepcontrol.wait
+        // PDL secondary / gated early start: defer q and the newest block until the producer
+        // kernel / the grid barrier has published them
+        bool waited = persistent && src.gate == nullptr;
         int dq = -1, ds = -1, did = 0;
         uint32_t dbytes = 0;
         auto flush = [&]() {
             if (!waited) {
-                pdl_wait();
+                if (src.gate) {
+                    unsigned v;
+                    const long long t0 = clock64();
+                    for (;;) {
+                        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(src.gate) : "memory");
+                        if ((int)(v - src.gate_target) >= 0) break;
+                        if (clock64() - t0 > EL_SPIN_LIMIT) __trap();
+                    }
+                    asm volatile("fence.proxy.async.global;" ::: "memory");  // bulk copies read them next
+                } else {
+                    pdl_wait();
+                }
                 waited = true;
             }
             if (ds >= 0) {
@@ -1341,7 +1358,7 @@ __global__ void __launch_bounds__(kAttnThreads) attn_kernel(DevState st) {
         fence_barrier_init();
     }
     __syncthreads();
-    const AttnSrc src{st.tables, st.dm.bpl_max, st.kpool, st.vpool, 0, a.pref, st.rows.pos, st.rows.slot, 0};
+    const AttnSrc src{st.tables, st.dm.bpl_max, st.kpool, st.vpool, 0, a.pref, st.rows.pos, st.rows.slot, 0, nullptr, 0u};
     attn_body<NJ>(st, a, stages, layer, 0, false, src, nullptr);
     if ((st.dbg & 32) && tid == 0) {
         unsigned long long t;

@@ -211,6 +211,7 @@ struct IterPlan {
     int att_l2_blocks;  // per CTA: first attention K/V blocks of the layer prefetched into L2 during QKV
     int att_mbuf_off;   // > 0: the attention segment merge buffer [8][dp] fp32 (else merged inside the stage)
     int att_l2_late;    // per CTA: first attention K/V blocks prefetched into L2 at the end of the QKV phase
+    int att_early;      // the attention producer starts before the QKV -> attention barrier
     int ring_bytes;  // shared ring region (attention stages / GEMM stages + LM transpose buffer)
     int gemm_ring;   // bytes of the GEMM stages inside the ring region
     int lm_tiles;    // Vp / 128
