@@ -938,13 +938,30 @@ __device__ __forceinline__ void attn_body(const DevState& st, AttnSmem& a, uint8
         if (lane == 0) EL_ATT_CLK(10);
         const int n_items = (Td + cb - 1) / cb;
         const int G = min((int)gridDim.x, Ts);
-        auto cta_of = [&](int g) { return (int)(((g + 1) * G + Ts - 1) / Ts - 1); };
+        // Cost-aware static split: every row start costs dl extra "virtual" blocks (a segment
+        // switch + one more partial merge), so CTAs whose range crosses a row boundary get
+        // fewer real blocks.  Virtual position of real block g of row r: g + dl * (r + 1);
+        // CTA i owns virtual [floor(i V / G), floor((i + 1) V / G)).  Deterministic: depends
+        // on the row structure only.
+        const int dl = (Td == 0) ? st.attn_seg_cost : 0;
+        const int V = Ts + dl * B;
+        auto cta_of = [&](int g, int r) { return (int)(((g + dl * (r + 1) + 1) * G + V - 1) / V - 1); };
+        auto real_of = [&](int vb) {  // first real block whose virtual position is >= vb
+            if (vb >= V) return Ts;
+            int lo = 0, hi = B - 1;  // first row whose virtual end exceeds vb
+            while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if (src.pref[mid + 1] + dl * (mid + 1) > vb) hi = mid;
+                else lo = mid + 1;
+            }
+            return src.pref[lo] + max(0, vb - src.pref[lo] - dl * (lo + 1));
+        };
         // segment bookkeeping of row r: static segments and the first tail item touching it
         auto row_static = [&](int r, int& first_cta) {
             const int r0 = src.pref[r], r1 = min((int)src.pref[r + 1], Ts);
             if (r0 >= r1) return 0;
-            first_cta = cta_of(r0);
-            return cta_of(r1 - 1) - first_cta + 1;
+            first_cta = cta_of(r0, r);
+            return cta_of(r1 - 1, r) - first_cta + 1;
         };
         auto row_items = [&](int r, int& i0) {
             const int r0 = max((int)src.pref[r], Ts), r1 = src.pref[r + 1];
@@ -1044,8 +1061,8 @@ __device__ __forceinline__ void attn_body(const DevState& st, AttnSmem& a, uint8
         };
         // ---- static head ----
         const bool has_static = (int)blockIdx.x < G;
-        const int g0 = has_static ? (int)blockIdx.x * Ts / G : 0;
-        const int g1 = has_static ? (int)(blockIdx.x + 1) * Ts / G : 0;
+        const int g0 = has_static ? real_of((int)blockIdx.x * V / G) : 0;
+        const int g1 = has_static ? real_of((int)(blockIdx.x + 1) * V / G) : 0;
         // the range's block ids are gathered before streaming (independent loads in
         // parallel: a segment switch mid-range then costs no dependent table-load round
         // trip); the persistent kernel gathers the next layer's at the end of this pass

@@ -73,6 +73,7 @@ struct DevState {
     int* attn_done;
     int attn_dyn_permille;  // share of the KV blocks handed out dynamically (0 = static split only)
     int attn_dyn_cb;        // blocks per dynamic item
+    int attn_seg_cost;      // static split: extra cost of a row start, in KV blocks
     int dbg;          // experiment knob (0 = normal)
     unsigned long long* dbg_ts;
     float attn_scale; // 1/sqrt(d)
