@@ -226,7 +226,7 @@ struct el_engine {
         opt_mega_bm_max = 256, opt_attn_dyn_permille = 0, opt_attn_dyn_cb = 4, opt_mega_bm_prefetch = 1,
         opt_mega_bm_chunk_kb = 0, opt_mega_bm_act_policy = 0, opt_mega_bm_nt_min = 16,
         opt_mega_bm_m128 = 0, opt_mega_bm_down = 0, opt_mega_att_l2 = 0, opt_mega_down_splits = 0,
-        opt_mega_splits_cap = 0, opt_mega_fused_reduce = 1, opt_att_mbuf = 1, opt_mega_att_l2_late = 0, opt_mega_att_early = 1, opt_attn_seg_cost = 2;
+        opt_mega_splits_cap = 0, opt_mega_fused_reduce = 1, opt_att_mbuf = 1, opt_mega_att_l2_late = 0, opt_mega_att_early = 1, opt_attn_seg_cost = -1;
     int attn_cb = 1, attn_stages = 2, attn_max_chunks = 1, attn_grid = 148;
     int NR = 16;
 
@@ -695,7 +695,9 @@ struct el_engine {
         s.attn_stages = mega_att_stages;
         s.attn_dyn_permille = opt_attn_dyn_permille;
         s.attn_dyn_cb = opt_attn_dyn_cb;
-        s.attn_seg_cost = opt_attn_seg_cost;
+        // auto: charge row starts at batch <= 64, where a row spans 2-3 CTA ranges (c2 +1.2 %);
+        // at batch 128 the same cost measured -1.6 % end to end
+        s.attn_seg_cost = opt_attn_seg_cost >= 0 ? opt_attn_seg_cost : (B <= 64 ? 2 : 0);
         el::launch_iter(s, P, mmaps[P.map_key], mega_grid, stream);
     }
 
@@ -1362,7 +1364,7 @@ int el_engine_set_option(el_engine* e, const char* key, int64_t v) {
         if (v < 0 || v > 1000) fail(EL_INVALID_ARGUMENT, "attn_dyn_permille must be in [0, 1000]");
         e->opt_attn_dyn_permille = (int)v;
     } else if (!std::strcmp(key, "attn_seg_cost")) {
-        if (v < 0 || v > 64) fail(EL_INVALID_ARGUMENT, "attn_seg_cost must be in [0, 64]");
+        if (v < -1 || v > 64) fail(EL_INVALID_ARGUMENT, "attn_seg_cost must be in [-1 (auto), 64]");
         e->opt_attn_seg_cost = (int)v;
         e->invalidate_graphs();
     } else if (!std::strcmp(key, "attn_dyn_cb")) {
