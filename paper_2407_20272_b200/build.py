@@ -18,7 +18,7 @@ HEADERS = ["el_common.cuh", "el_kernels.h", "el_iter.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-O2", "--expt-relaxed-constexpr", "-cudart", "static",
-         f"-I{os.path.join(ROOT, 'include')}"]
+         f"-I{os.path.join(ROOT, 'include')}"] + (["-DEL_DEBUG=1"] if os.environ.get("EL_DEBUG") == "1" else [])
 
 
 def _stale() -> bool:

@@ -115,7 +115,7 @@ __device__ __forceinline__ void red_release_add_u32(unsigned* p, unsigned v) {
 // two-hop form (dbg bit 25: CTA 0 alone polls the count and releases a generation
 // word the others poll).  Inlined, with no reference to a copy of the parameters.
 __device__ __forceinline__ void grid_sync(const IterPlan& p, const DevState& st, int& nbar, uint2 gb) {
-    const int dbg = st.dbg;
+    const int dbg = EL_DBG(st);
     if (threadIdx.x == 0 && (dbg & 128) && nbar < 1024) {  // per-CTA arrival (work done) time
         unsigned long long t;
         asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -165,7 +165,7 @@ __device__ __forceinline__ void grid_sync_sub(const IterPlan& p, const DevState&
         const long long t0 = clock64();
         while ((int)(ld_acquire_u32(cnt) - target) < 0)
             if (clock64() - t0 > EL_SPIN_LIMIT) __trap();
-        if ((st.dbg & 128) && blockIdx.x == 0 && nbar < 1024) {
+        if ((EL_DBG(st) & 128) && blockIdx.x == 0 && nbar < 1024) {
             unsigned long long t;
             asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
             st.dbg_ts[20480 + nbar] = t;
@@ -464,7 +464,7 @@ __device__ __forceinline__ void reduce_range(const DevState& st, const IterSmem&
     const int lane = threadIdx.x & 31;
     const int S = g.splits;
     auto rstamp = [&](int k) {  // dbg 64: warp 0's reduce timeline in layer 1's down phase (SM clock)
-        if (K == kIDown && !dry && (st.dbg & 64) && x.layer == 1 && threadIdx.x == 0)
+        if (K == kIDown && !dry && (EL_DBG(st) & 64) && x.layer == 1 && threadIdx.x == 0)
             st.dbg_ts[310000 + (size_t)blockIdx.x * 8 + k] = clock64();
     };
     rstamp(0);
@@ -493,7 +493,7 @@ __device__ __forceinline__ void reduce_range(const DevState& st, const IterSmem&
                 dh[j] = make_float4(0.f, 0.f, 0.f, 0.f);
                 dw[j] = make_float4(0.f, 0.f, 0.f, 0.f);
                 if (st.technique == kState)
-                    dh[j] = (st.dbg & (1 << 23)) ? dmid[j]
+                    dh[j] = (EL_DBG(st) & (1 << 23)) ? dmid[j]
                                                  : __ldcg(reinterpret_cast<const float4*>(st.h32 + (size_t)x.pin * Bm * dp + i));
                 else if (st.technique == kClassifier)
                     dw[j] = __ldg(reinterpret_cast<const float4*>(st.probe_w + mm[j] * kBM + 4 * lane));
@@ -548,7 +548,7 @@ __device__ __forceinline__ void reduce_range(const DevState& st, const IterSmem&
                                    (uint32_t)f32_to_bf16(o.z) | ((uint32_t)f32_to_bf16(o.w) << 16));
                 }
                 rstamp(3);
-                if ((st.technique == kState || st.technique == kClassifier) && !(st.dbg & (1 << 22))) {
+                if ((st.technique == kState || st.technique == kClassifier) && !(EL_DBG(st) & (1 << 22))) {
                     double x0 = 0.0, x1 = 0.0, x2 = 0.0;
                     const float ov[4] = {o.x, o.y, o.z, o.w};
                     if (st.technique == kState) {
@@ -907,7 +907,7 @@ __device__ __forceinline__ void gemm_phase_t(const DevState& st, IterSmem& sm, u
     const int R = p.bm_rows / p.bm_grp;  // row groups: unit u = (feature group u / R, row group u % R)
     const int U = g.m_tiles * kBM / g.nt * R;
     auto stamp = [&](int k) {  // dbg 64: per-CTA unit timeline of layer 1's batch-M GEMMs
-        if ((st.dbg & 64) && x.layer == 1 && threadIdx.x == 0)  // SM clock (globaltimer ticks are 256 ns)
+        if ((EL_DBG(st) & 64) && x.layer == 1 && threadIdx.x == 0)  // SM clock (globaltimer ticks are 256 ns)
             st.dbg_ts[300000 + (size_t)blockIdx.x * 32 + K * 8 + k] = clock64();
     };
     stamp(0);
@@ -920,7 +920,7 @@ __device__ __forceinline__ void gemm_phase_t(const DevState& st, IterSmem& sm, u
         ++wseq;
         wpf = false;
         stamp(2);
-        if ((st.dbg & 64) && x.layer == 1 && threadIdx.x == 0)
+        if ((EL_DBG(st) & 64) && x.layer == 1 && threadIdx.x == 0)
             for (int k = 0; k < 5; ++k) st.dbg_ts[300000 + (size_t)blockIdx.x * 32 + K * 8 + (k < 4 ? 4 + k : 1)] = sm.tdbg[k];
         if (warp < 8) {
             // M = 128: batch row b in TMEM lane b.  M = 64: rows 16q..16q+15 in lanes 32q..32q+15.
@@ -959,7 +959,7 @@ __device__ void gemm_phase_fused(const DevState& st, IterSmem& sm, uint8_t* ring
     const size_t bks = (size_t)st.NR * kBK;
     unsigned* cnt = p.tcnt + gid * 64;
     auto stamp = [&](int k) {  // dbg 64: per-CTA timeline of layer 1's fused split-K phase (SM clock)
-        if ((st.dbg & 64) && x.layer == 1 && threadIdx.x == 0 && K == kIDown)
+        if ((EL_DBG(st) & 64) && x.layer == 1 && threadIdx.x == 0 && K == kIDown)
             st.dbg_ts[300000 + (size_t)blockIdx.x * 32 + 3 * 8 + k] = clock64();
     };
     stamp(0);
@@ -968,9 +968,9 @@ __device__ void gemm_phase_fused(const DevState& st, IterSmem& sm, uint8_t* ring
         const int kb0 = s * g.kb_total / g.splits, kb1 = (s + 1) * g.kb_total / g.splits;
         const uint16_t* a = g.A + (size_t)((x.layer - 1) * g.layer_rows + g.row_off + m) * g.kb_total * (kBM * kBK);
         unit_ws(sm, ring, p, kseq, a, bsrc, bks, kb0, kb1 - kb0, useq,
-                (K == kIDown && x.layer == 1) ? (st.dbg & 64) : 0);
+                (K == kIDown && x.layer == 1) ? (EL_DBG(st) & 64) : 0);
         stamp(1);
-        if ((st.dbg & 64) && x.layer == 1 && threadIdx.x == 0 && K == kIDown)
+        if ((EL_DBG(st) & 64) && x.layer == 1 && threadIdx.x == 0 && K == kIDown)
             for (int k = 0; k < 3; ++k) st.dbg_ts[300000 + (size_t)blockIdx.x * 32 + 3 * 8 + 5 + k] = sm.tdbg[k == 2 ? 3 : k];
         if (warp < 8) epi_partial(sm, p, u, nval);
         ++useq;
@@ -980,9 +980,9 @@ __device__ void gemm_phase_fused(const DevState& st, IterSmem& sm, uint8_t* ring
         stamp(2);
         if (threadIdx.x == 0) {
             // (bar.sync above orders the CTA's partial stores before this thread's release)
-            if (st.dbg & (1 << 26)) __threadfence();
+            if (EL_DBG(st) & (1 << 26)) __threadfence();
             red_release_add_u32(cnt + m, 1u);
-            if ((st.dbg & 64) && x.layer == 1 && K == kIDown) st.dbg_ts[310000 + (size_t)blockIdx.x * 8 + 5] = clock64();
+            if ((EL_DBG(st) & 64) && x.layer == 1 && K == kIDown) st.dbg_ts[310000 + (size_t)blockIdx.x * 8 + 5] = clock64();
         }
     }
     for (int u = blockIdx.x; u < U; u += gridDim.x) {
@@ -992,7 +992,7 @@ __device__ void gemm_phase_fused(const DevState& st, IterSmem& sm, uint8_t* ring
         // so that pass 1 finds it in the instruction cache -- measured slower (the dry pass is
         // as cold as the real one was and outlasts the wait)
 #pragma unroll 1
-        for (int pass = (st.dbg & (1 << 24)) ? 0 : 1; pass < 2; ++pass) {
+        for (int pass = (EL_DBG(st) & (1 << 24)) ? 0 : 1; pass < 2; ++pass) {
             if (pass == 1) {
                 if (threadIdx.x == 0) {
                     const unsigned target = (unsigned)(g.splits * use);
@@ -1080,9 +1080,9 @@ __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(const __grid_cons
     uint32_t kseq = 0, kseq2 = 0, wseq = 0, useq = 0;
     bool wpf = false;  // producer lane: the next batch-M unit's weights were prefetched
     int aseq = 0, nbar = 0;
-    if (st.dbg & 256)  // barrier cost probe: 32 back-to-back grid barriers
+    if (EL_DBG(st) & 256)  // barrier cost probe: 32 back-to-back grid barriers
         for (int i = 0; i < 32; ++i) grid_sync(p, st, nbar, g0);
-    if (st.dbg & (1 << 19)) {  // TMA probe: two QKV batch-M units back to back at kernel start
+    if (EL_DBG(st) & (1 << 19)) {  // TMA probe: two QKV batch-M units back to back at kernel start
         const IterCtx x0{1, 0, 1};
         for (int rep = 0; rep < 2; ++rep) {
             gemm_phase_t<kIQkv>(st, sm, ring, p, maps, kIQkv, x0, st.hb, kseq2, wseq, useq, B, wpf, -1, 0);
@@ -1134,7 +1134,7 @@ __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(const __grid_cons
         // this barrier and streams the old K/V blocks of its range while the grid waits; q and
         // the newest block (this phase's output) wait on the barrier count
         AttnSrc self_l = self_src;
-        const bool early = p.att_early && !(st.dbg & ((1 << 25) | (1 << 27)));
+        const bool early = p.att_early && !(EL_DBG(st) & ((1 << 25) | (1 << 27)));
         if (early) {
             self_l.gate = p.bar;
             self_l.gate_target = g0.y + (unsigned)G * (unsigned)(nbar + 1);
@@ -1145,7 +1145,7 @@ __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(const __grid_cons
         }
         // paged attention (model.cpp:223-243)
         auto astamp = [&](int w) {
-            if ((st.dbg & 128) && tid == 0 && layer <= 24) {
+            if ((EL_DBG(st) & 128) && tid == 0 && layer <= 24) {
                 unsigned long long t;
                 asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
                 st.dbg_ts[40000 + (layer - 1) * 512 + cta * 2 + w] = t;
@@ -1155,7 +1155,7 @@ __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(const __grid_cons
             }
         };
         astamp(0);
-        if ((st.dbg & 32) && tid == 0 && cta < 4) st.dbg_ts[8192 + 3072 + cta * 16] = clock64();
+        if ((EL_DBG(st) & 32) && tid == 0 && cta < 4) st.dbg_ts[8192 + 3072 + cta * 16] = clock64();
         if (tid == kProducerWarp * 32) wpf = bm_prefetch(sm, ring, p, maps, kIWo, layer);  // W_o under attention
         if (warp == kProducerWarp && (p.pf_flags & 1)) {  // this layer's W_o / up / down tiles -> L2
             l2_prefetch_gemm(p.g[kIWo], layer);

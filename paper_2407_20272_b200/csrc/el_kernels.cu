@@ -49,7 +49,7 @@ __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;"
 // device-side kernel timeline (option dbg bit 64): slot = kind * 32 + layer,
 // [2 * slot] = earliest CTA start, [2 * slot + 1] = latest CTA end
 __device__ __forceinline__ void tl_mark(const DevState& st, int kind, int layer, int end) {
-    if ((st.dbg & 64) && threadIdx.x == 0) {
+    if ((EL_DBG(st) & 64) && threadIdx.x == 0) {
         unsigned long long t;
         asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
         unsigned long long* slot = st.dbg_ts + 16384 + 2 * (kind * 32 + layer) + end;
@@ -389,7 +389,7 @@ __global__ void __launch_bounds__(128, 1)
     const int tl_layer = (K == kGemmLmFinal || K == kGemmFill) ? 0 : *st.layer;
     tl_mark(st, tl_kind, tl_layer, 0);
     auto stamp = [&](int i) {
-        if ((st.dbg & 8) && tid == 0) {
+        if ((EL_DBG(st) & 8) && tid == 0) {
             unsigned long long t;
             asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
             st.dbg_ts[(blockIdx.y * gridDim.x + blockIdx.x) * 8 + i] = t;
@@ -439,7 +439,7 @@ __global__ void __launch_bounds__(128, 1)
         for (int kb = pre; kb < nkb; ++kb) {
             const int s = kb % g.stages;
             mbar_wait(&empty[s], ((kb / g.stages) - 1) & 1);
-            if ((st.dbg & 16) && blockIdx.x == 0 && blockIdx.y == 0 && kb < 64) {
+            if ((EL_DBG(st) & 16) && blockIdx.x == 0 && blockIdx.y == 0 && kb < 64) {
                 unsigned long long t;
                 asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
                 st.dbg_ts[4096 + 64 + kb] = t;
@@ -455,7 +455,7 @@ __global__ void __launch_bounds__(128, 1)
         for (int kb = 0; kb < nkb; ++kb) {
             const int s = kb % g.stages;
             mbar_wait(&full[s], (kb / g.stages) & 1);
-            if ((st.dbg & 16) && blockIdx.x == 0 && blockIdx.y == 0 && kb < 64) {
+            if ((EL_DBG(st) & 16) && blockIdx.x == 0 && blockIdx.y == 0 && kb < 64) {
                 unsigned long long t;
                 asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
                 st.dbg_ts[4096 + kb] = t;
@@ -756,7 +756,7 @@ __device__ __forceinline__ int atom_add_acq_rel(int* p, int v) {
 // dbg 32: SM-clock stamps of the attention producer's start-up for CTAs 0..3 (slot k)
 #define EL_ATT_CLK(k)                                                                       \
     do {                                                                                    \
-        if ((st.dbg & 32) && blockIdx.x < 4) st.dbg_ts[8192 + 3072 + blockIdx.x * 16 + (k)] = clock64(); \
+        if ((EL_DBG(st) & 32) && blockIdx.x < 4) st.dbg_ts[8192 + 3072 + blockIdx.x * 16 + (k)] = clock64(); \
     } while (0)
 
 // One attention pass over layer `layer` (see the comment above). Shared by the
@@ -1030,7 +1030,7 @@ __device__ __forceinline__ void attn_body(const DevState& st, AttnSmem& a, uint8
                         const bool first = (gb + u) == g, newest = blk == nblk - 1;
                         a.desc[s] = AttnDesc{b, slot, rows, first, (gb + u) == seg_end - 1, nseg, {0, 0}};
                         uint8_t* sbuf = stages + (size_t)s * stage_bytes;
-                        if ((st.dbg & 32) && blockIdx.x < 4 && seq < 60) {  // issue time of each block
+                        if ((EL_DBG(st) & 32) && blockIdx.x < 4 && seq < 60) {  // issue time of each block
                             unsigned long long t;
                             asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
                             st.dbg_ts[8192 + 1024 + blockIdx.x * 128 + seq] = t;
@@ -1166,7 +1166,7 @@ __device__ __forceinline__ void attn_body(const DevState& st, AttnSmem& a, uint8
         // math once on whatever the first stage holds while its data is still in
         // flight (results are discarded: the first real descriptor of a pass is
         // always a segment start, which resets q, o, m, l).
-        bool warm = persistent && !(st.dbg & (1 << 21));
+        bool warm = persistent && !(EL_DBG(st) & (1 << 21));
         for (int seq = seq0;; ++seq) {
             const int s = seq % S;
             AttnDesc d;
@@ -1181,7 +1181,7 @@ __device__ __forceinline__ void attn_body(const DevState& st, AttnSmem& a, uint8
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&a.empty[s]);
             }
-            if ((st.dbg & 32) && tid == 0) {
+            if ((EL_DBG(st) & 32) && tid == 0) {
                 unsigned long long t;
                 asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
                 if (blockIdx.x < 4 && seq < 60) st.dbg_ts[8192 + blockIdx.x * 128 + seq] = t;
@@ -1216,7 +1216,7 @@ __device__ __forceinline__ void attn_body(const DevState& st, AttnSmem& a, uint8
             // Branch-free block math: both rows' K and V are loaded up front (row indices
             // clamped to valid rows, feature chunks clamped to the last one), an invalid
             // second row gets score -inf (weight 0 times finite data).
-            const int nrows = (st.dbg & 1) ? 0 : d.rows;
+            const int nrows = (EL_DBG(st) & 1) ? 0 : d.rows;
             for (int rb = 0; rb < nrows; rb += 2 * kAttnWarps) {
                 const int ra = rb + r0;
                 if (ra >= nrows) break;  // warp-uniform: no row of this warp left in the block
@@ -1267,7 +1267,7 @@ __device__ __forceinline__ void attn_body(const DevState& st, AttnSmem& a, uint8
                     axpy8p2(pc, xc[t], o[t]);
                 }
             }
-            if ((st.dbg & 32) && tid == 0 && blockIdx.x < 4 && seq < 60) {  // block processed (before release)
+            if ((EL_DBG(st) & 32) && tid == 0 && blockIdx.x < 4 && seq < 60) {  // block processed (before release)
                 unsigned long long t;
                 asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
                 st.dbg_ts[8192 + 2048 + blockIdx.x * 128 + seq] = t;
@@ -1277,7 +1277,7 @@ __device__ __forceinline__ void attn_body(const DevState& st, AttnSmem& a, uint8
                 --seq;
                 continue;
             }
-            if (!d.last || (st.dbg & 4)) {
+            if (!d.last || (EL_DBG(st) & 4)) {
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&a.empty[s]);
                 continue;
@@ -1332,7 +1332,7 @@ __device__ __forceinline__ void attn_body(const DevState& st, AttnSmem& a, uint8
                 named_bar(1, kAttnWarps * 32);
                 if (lane == 0) mbar_arrive(&a.empty[s]);
             }
-            if (++npend == kAttnPend || (st.dbg & 8)) {  // (npend: every consumer thread's own count)
+            if (++npend == kAttnPend || (EL_DBG(st) & 8)) {  // (npend: every consumer thread's own count)
                 attn_settle(st, a);
                 npend = 0;
             }
@@ -1359,7 +1359,7 @@ __global__ void __launch_bounds__(kAttnThreads) attn_kernel(DevState st) {
     uint8_t* stages = smem_raw + ((sizeof(AttnSmem) + 127) & ~(size_t)127);
     const int layer = *st.layer;
     tl_mark(st, 2, layer, 0);
-    if ((st.dbg & 32) && tid == 0) {
+    if ((EL_DBG(st) & 32) && tid == 0) {
         unsigned long long t;
         asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
         if (blockIdx.x < 4) st.dbg_ts[8192 + 4 * 128 + blockIdx.x] = t;
@@ -1377,7 +1377,7 @@ __global__ void __launch_bounds__(kAttnThreads) attn_kernel(DevState st) {
     __syncthreads();
     const AttnSrc src{st.tables, st.dm.bpl_max, st.kpool, st.vpool, 0, a.pref, st.rows.pos, st.rows.slot, 0, nullptr, 0u};
     attn_body<NJ>(st, a, stages, layer, 0, false, src, nullptr);
-    if ((st.dbg & 32) && tid == 0) {
+    if ((EL_DBG(st) & 32) && tid == 0) {
         unsigned long long t;
         asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
         st.dbg_ts[24576 + 4 * blockIdx.x + 3] = t;

@@ -36,6 +36,14 @@ struct Rows {
 };
 
 // All device pointers of one engine.  POD, passed by value to every kernel.
+// Instrumentation / probe switches (DevState::dbg) compile to constant 0 unless the
+// library is built with EL_DEBUG=1 (scripts/mega_phases.py and the other timeline
+// probes need that build): the product kernels carry none of that code.
+#ifndef EL_DEBUG
+#define EL_DEBUG 0
+#endif
+#define EL_DBG(s) (EL_DEBUG ? (s).dbg : 0)
+
 struct DevState {
     Dims dm;
     // weights (bf16 bit patterns), packed per layer
