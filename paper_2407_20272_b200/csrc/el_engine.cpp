@@ -1362,6 +1362,7 @@ int el_engine_set_option(el_engine* e, const char* key, int64_t v) {
     }
     else if (!std::strcmp(key, "attn_dyn_permille")) {
         if (v < 0 || v > 1000) fail(EL_INVALID_ARGUMENT, "attn_dyn_permille must be in [0, 1000]");
+        if (!EL_DEBUG && v > 0) fail(EL_INVALID_ARGUMENT, "attn_dyn_permille > 0 needs an EL_DEBUG=1 build");
         e->opt_attn_dyn_permille = (int)v;
     } else if (!std::strcmp(key, "attn_seg_cost")) {
         if (v < -1 || v > 64) fail(EL_INVALID_ARGUMENT, "attn_seg_cost must be in [-1 (auto), 64]");
@@ -1374,6 +1375,7 @@ int el_engine_set_option(el_engine* e, const char* key, int64_t v) {
         (key[8] == 'c' ? e->opt_mega_bm_chunk_kb : e->opt_mega_bm_act_policy) = (int)v;
         e->mplans.clear();
     } else if (!std::strcmp(key, "mega_att_l2_late")) {
+        if (!EL_DEBUG && v != 0) fail(EL_INVALID_ARGUMENT, "L2 prefetch probes need an EL_DEBUG=1 build");
         if (v < 0 || v > 64) fail(EL_INVALID_ARGUMENT, "mega_att_l2_late must be in [0, 64]");
         e->opt_mega_att_l2_late = (int)v;
         e->mplans.clear();
@@ -1384,6 +1386,7 @@ int el_engine_set_option(el_engine* e, const char* key, int64_t v) {
         e->opt_att_mbuf = v != 0;
         e->mplans.clear();
     } else if (!std::strcmp(key, "mega_fused_reduce")) {
+        if (!EL_DEBUG && v == 0) fail(EL_INVALID_ARGUMENT, "mega_fused_reduce=0 needs an EL_DEBUG=1 build");
         e->opt_mega_fused_reduce = v != 0;
         e->mplans.clear();
     } else if (!std::strcmp(key, "mega_splits_cap")) {
@@ -1394,6 +1397,7 @@ int el_engine_set_option(el_engine* e, const char* key, int64_t v) {
         e->opt_mega_down_splits = (int)v;
         e->mplans.clear();
     } else if (!std::strcmp(key, "mega_att_l2")) {
+        if (!EL_DEBUG && v != 0) fail(EL_INVALID_ARGUMENT, "L2 prefetch probes need an EL_DEBUG=1 build");
         e->opt_mega_att_l2 = (int)v;
         e->mplans.clear();
     } else if (!std::strcmp(key, "mega_bm_down")) {
@@ -1413,6 +1417,7 @@ int el_engine_set_option(el_engine* e, const char* key, int64_t v) {
         e->opt_mega_bm_max = (int)v;
         e->mplans.clear();
     } else if (!std::strcmp(key, "mega_pf") || !std::strcmp(key, "mega_kv_pf_mb")) {
+        if (!EL_DEBUG && v != 0) fail(EL_INVALID_ARGUMENT, "L2 prefetch probes need an EL_DEBUG=1 build");
         if (v < 0 || v > 4096) fail(EL_INVALID_ARGUMENT, "value out of range");
         (key[5] == 'k' ? e->opt_mega_kv_pf_mb : e->opt_mega_pf) = (int)v;
         e->mplans.clear();

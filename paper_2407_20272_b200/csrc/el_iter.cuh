@@ -1115,12 +1115,12 @@ __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(const __grid_cons
         const IterCtx x{layer, (layer - 1) & 1, layer & 1};
         // q | k | v, K/V appended to the paged pool (model.cpp:218-226)
         // this layer's first attention blocks (old positions: not written by this layer) into L2
-        if (warp == kProducerWarp && p.att_l2_blocks > 0) l2_prefetch_kv(st, sm.att, layer, p.att_l2_blocks);
+        if (EL_DEBUG && warp == kProducerWarp && p.att_l2_blocks > 0) l2_prefetch_kv(st, sm.att, layer, p.att_l2_blocks);
         __syncwarp();
         if (p.g[kIQkv].mode) {
             gemm_phase_t<kIQkv>(st, sm, ring, p, maps, kIQkv, x, st.hb + (size_t)x.pin * NR * dp, kseq2, wseq, useq, B,
                                 wpf, -1, 0);
-        } else if (p.fused_reduce) {
+        } else if (!EL_DEBUG || p.fused_reduce) {  // (unfused split-K: probe builds only)
             gemm_phase_fused<kIQkv>(st, sm, ring, p, kIQkv, x, st.hb + (size_t)x.pin * NR * dp, kseq, useq, B, layer);
         } else {
             gemm_phase(st, sm, ring, p, p.g[kIQkv], layer, st.hb + (size_t)x.pin * NR * dp, kseq, useq, B);
@@ -1129,7 +1129,7 @@ __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(const __grid_cons
         }
         // this CTA's first attention blocks -> L2 while the grid waits at the barrier (no
         // competition with the QKV loads, which are done)
-        if (warp == kProducerWarp && p.att_l2_late > 0) l2_prefetch_kv(st, sm.att, layer, p.att_l2_late);
+        if (EL_DEBUG && warp == kProducerWarp && p.att_l2_late > 0) l2_prefetch_kv(st, sm.att, layer, p.att_l2_late);
         // early attention start (default; barrier-mode 1-hop only): the producer warp skips
         // this barrier and streams the old K/V blocks of its range while the grid waits; q and
         // the newest block (this phase's output) wait on the barrier count
@@ -1157,7 +1157,7 @@ __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(const __grid_cons
         astamp(0);
         if ((EL_DBG(st) & 32) && tid == 0 && cta < 4) st.dbg_ts[8192 + 3072 + cta * 16] = clock64();
         if (tid == kProducerWarp * 32) wpf = bm_prefetch(sm, ring, p, maps, kIWo, layer);  // W_o under attention
-        if (warp == kProducerWarp && (p.pf_flags & 1)) {  // this layer's W_o / up / down tiles -> L2
+        if (EL_DEBUG && warp == kProducerWarp && (p.pf_flags & 1)) {  // this layer's W_o / up / down tiles -> L2
             l2_prefetch_gemm(p.g[kIWo], layer);
             l2_prefetch_gemm(p.g[kIUp], layer);
             l2_prefetch_gemm(p.g[kIDown], layer);
@@ -1169,14 +1169,14 @@ __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(const __grid_cons
         aseq = sm.att.seq_next;
         // the next layer's dynamic-tail counter (this one's twin) is idle now: rearm it
         if (cta == 0 && tid == 0 && st.attn_queue) st.attn_queue[(layer + 1) & 1] = 0;
-        if (warp == kProducerWarp && layer < L && p.kv_pf_blocks > 0)  // next layer's K/V -> L2
+        if (EL_DEBUG && warp == kProducerWarp && layer < L && p.kv_pf_blocks > 0)  // next layer's K/V -> L2
             l2_prefetch_kv(st, sm.att, layer + 1, p.kv_pf_blocks);
         __syncwarp();
         // W_o + residual (model.cpp:245-253)
         if (p.g[kIWo].mode) {
             gemm_phase_t<kIWo>(st, sm, ring, p, maps, kIWo, x, st.att_b, kseq2, wseq, useq, B, wpf,
                                st.enc_len > 0 ? (int)kIQc : (int)kIUp, layer);
-        } else if (p.fused_reduce) {
+        } else if (!EL_DEBUG || p.fused_reduce) {  // (unfused split-K: probe builds only)
             gemm_phase_fused<kIWo>(st, sm, ring, p, kIWo, x, st.att_b, kseq, useq, B, layer);
         } else {
             gemm_phase(st, sm, ring, p, p.g[kIWo], layer, st.att_b, kseq, useq, B);
@@ -1189,7 +1189,7 @@ __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(const __grid_cons
             if (p.g[kIQc].mode) {
                 gemm_phase_t<kIQkv>(st, sm, ring, p, maps, kIQc, x, st.mid_b, kseq2, wseq, useq, B, wpf, -1,
                                     0);  // q_c -> q32
-            } else if (p.fused_reduce) {
+            } else if (!EL_DEBUG || p.fused_reduce) {  // (unfused split-K: probe builds only)
                 gemm_phase_fused<kIQkv>(st, sm, ring, p, kIQc, x, st.mid_b, kseq, useq, B, layer);
             } else {
                 gemm_phase(st, sm, ring, p, p.g[kIQc], layer, st.mid_b, kseq, useq, B);
@@ -1204,7 +1204,7 @@ __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(const __grid_cons
             if (p.g[kIWoc].mode) {
                 gemm_phase_t<kIWoc>(st, sm, ring, p, maps, kIWoc, x, st.att_b, kseq2, wseq, useq, B, wpf, kIUp,
                                     layer);
-            } else if (p.fused_reduce) {
+            } else if (!EL_DEBUG || p.fused_reduce) {  // (unfused split-K: probe builds only)
                 gemm_phase_fused<kIWoc>(st, sm, ring, p, kIWoc, x, st.att_b, kseq, useq, B, layer);
             } else {
                 gemm_phase(st, sm, ring, p, p.g[kIWoc], layer, st.att_b, kseq, useq, B);
@@ -1217,7 +1217,7 @@ __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(const __grid_cons
         if (p.g[kIUp].mode) {
             gemm_phase_t<kIUp>(st, sm, ring, p, maps, kIUp, x, st.mid_b, kseq2, wseq, useq, B, wpf,
                                p.g[kIDown].mode ? (int)kIDown : -1, layer);
-        } else if (p.fused_reduce) {
+        } else if (!EL_DEBUG || p.fused_reduce) {  // (unfused split-K: probe builds only)
             gemm_phase_fused<kIUp>(st, sm, ring, p, kIUp, x, st.mid_b, kseq, useq, B, layer);
         } else {
             gemm_phase(st, sm, ring, p, p.g[kIUp], layer, st.mid_b, kseq, useq, B);
@@ -1229,13 +1229,13 @@ __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(const __grid_cons
         if (p.g[kIDown].mode) {
             gemm_phase_t<kIDown>(st, sm, ring, p, maps, kIDown, x, st.up_b, kseq2, wseq, useq, B, wpf,
                                  layer < L ? (int)kIQkv : -1, layer + 1);
-        } else if (p.fused_reduce) {
+        } else if (!EL_DEBUG || p.fused_reduce) {  // (unfused split-K: probe builds only)
             if (tid == kProducerWarp * 32 && layer < L) wpf = bm_prefetch(sm, ring, p, maps, kIQkv, layer + 1);
             gemm_phase_fused<kIDown>(st, sm, ring, p, kIDown, x, st.up_b, kseq, useq, B, layer);
         } else {
             gemm_phase(st, sm, ring, p, p.g[kIDown], layer, st.up_b, kseq, useq, B);
             grid_sync(p, st, nbar, g0);
-            if (warp == kProducerWarp && layer < L && (p.pf_flags & 1)) l2_prefetch_gemm(p.g[kIQkv], layer + 1);
+            if (EL_DEBUG && warp == kProducerWarp && layer < L && (p.pf_flags & 1)) l2_prefetch_gemm(p.g[kIQkv], layer + 1);
             if (tid == kProducerWarp * 32 && layer < L) wpf = bm_prefetch(sm, ring, p, maps, kIQkv, layer + 1);
             reduce_phase<kIDown>(st, sm, p, p.g[kIDown], x, B, 0, p.g[kIDown].m_tiles);
         }

@@ -932,7 +932,7 @@ __device__ __forceinline__ void attn_body(const DevState& st, AttnSmem& a, uint8
         // (int arithmetic: T <= 256 rows x 128 blocks, products <= T * 148 -- no 64-bit division)
         const int T = src.pref[B];
         const int cb = max(1, st.attn_dyn_cb);
-        const int Td = (st.attn_dyn_permille > 0 && st.attn_queue)
+        const int Td = (EL_DEBUG && st.attn_dyn_permille > 0 && st.attn_queue)  // (dynamic tail: probe builds)
                                  ? min(T, (T * st.attn_dyn_permille / 1000 + cb - 1) / cb * cb) : 0;
         const int Ts = T - Td;
         if (lane == 0) EL_ATT_CLK(10);
