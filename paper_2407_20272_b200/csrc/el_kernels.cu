@@ -702,7 +702,7 @@ void launch_gemm(GemmKind kind, const GemmPlan& p, const DevState& st, cudaStrea
 constexpr int kAttnWarps = 8;
 constexpr int kAttnThreads = (kAttnWarps + 1) * 32;
 
-constexpr int kAttnPend = 16;
+constexpr int kAttnPend = 256;  // >= rows: a CTA never has more segments than rows
 constexpr int kAttnIds = 256;  // deferred segment completions per CTA before a forced settle
 struct AttnDesc {
     int b, c, rows, first, last, nseg, pad[2];  // c = partial slot of this CTA's segment of sequence b
@@ -816,8 +816,8 @@ __device__ __forceinline__ void attn_settle(const DevState& st, AttnSmem& a) {
     if (np == 0) return;
     // one acq_rel atomic per pending sequence, all in flight together (lanes of warp 0);
     // release-cumulative over the CTA's partial stores ordered before it by bar.sync
-    if (warp == 0 && lane < np)
-        a.pend_last[lane] = (atom_add_acq_rel(&st.attn_cnt[a.pend_b[lane]], 1) == a.pend_n[lane] - 1);
+    if (tid < np)
+        a.pend_last[tid] = (atom_add_acq_rel(&st.attn_cnt[a.pend_b[tid]], 1) == a.pend_n[tid] - 1);
     named_bar(1, kAttnWarps * 32);
     for (int i = 0; i < np; ++i) {
         if (!a.pend_last[i]) continue;
@@ -1332,10 +1332,11 @@ __device__ __forceinline__ void attn_body(const DevState& st, AttnSmem& a, uint8
                 named_bar(1, kAttnWarps * 32);
                 if (lane == 0) mbar_arrive(&a.empty[s]);
             }
-            if (++npend == kAttnPend || (EL_DBG(st) & 8)) {  // (npend: every consumer thread's own count)
+            if (EL_DEBUG && ((EL_DBG(st) & 8) || npend + 1 == kAttnPend)) {  // probe: settle every segment
                 attn_settle(st, a);
                 npend = 0;
             }
+            ++npend;  // (<= rows <= kAttnPend: the list cannot overflow)
         }
         attn_settle(st, a);
         if (tid == 0) EL_ATT_CLK(6);
