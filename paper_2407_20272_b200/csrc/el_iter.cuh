@@ -36,6 +36,8 @@ struct IterSmem {
     uint32_t tmem;
     int pad0;
     int pos[256], slot[256], status[256], first[256];
+    int kvrow[256];  // per row: slot * L * bpl_max + pos / bc (block-table index at layer 1)
+    int kvin[256];   // per row: (pos % bc) * dp (element offset of the position inside its block)
 };
 
 __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
@@ -363,10 +365,10 @@ struct IterCtx {
 
 // K/V element offset of (column c, layer) at the column's current position
 __device__ __forceinline__ long long kv_dst(const DevState& st, const IterSmem& sm, int c, int layer) {
+    // (the per-row division by the block capacity is done once per launch: sm.kvrow / kvin)
     const Dims& dm = st.dm;
-    const int pos = sm.pos[c];
-    const int blk = __ldg(&st.tables[((size_t)sm.slot[c] * dm.L + (layer - 1)) * dm.bpl_max + pos / dm.bc]);
-    return ((long long)blk * dm.bc + pos % dm.bc) * dm.dp;
+    const int blk = __ldg(&st.tables[sm.kvrow[c] + (layer - 1) * dm.bpl_max]);
+    return (long long)blk * dm.bc * dm.dp + sm.kvin[c];
 }
 
 // 4 consecutive rows r0..r0+3 (r0 % 4 == 0) of output tile m, column c
@@ -1063,6 +1065,8 @@ __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(const __grid_cons
     if (warp == 0) tmem_alloc(&sm.tmem, 512);
     for (int b = tid; b < 256; b += blockDim.x) {
         sm.pos[b] = b < B ? st.rows.pos[b] : 0;
+        sm.kvrow[b] = b < B ? st.rows.slot[b] * dm.L * dm.bpl_max + st.rows.pos[b] / dm.bc : 0;
+        sm.kvin[b] = b < B ? (st.rows.pos[b] % dm.bc) * dp : 0;
         sm.slot[b] = b < B ? st.rows.slot[b] : 0;
         sm.status[b] = 0;
         sm.first[b] = 0;
