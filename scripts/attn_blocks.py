@@ -1,6 +1,8 @@
 """Per-block timeline of the attention pass (layer 1) for CTAs 0..3 inside the
 persistent kernel (dbg 32 stamps: producer issue, consumer start, consumer done).
-Usage: python scripts/attn_blocks.py [config] [json options]"""
+Usage: python scripts/attn_blocks.py [config] [json options]
+Needs the instrumented library: EL_DEBUG=1 python paper_2407_20272_b200/build.py --force
+"""
 import ctypes as C
 import json
 import sys

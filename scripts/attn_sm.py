@@ -1,6 +1,8 @@
 """Per-SM attention pass durations inside the persistent kernel (dbg 128 stamps):
 which SMs are slow, is it stable across layers / iterations, and does it follow
-the GPC / die layout?  Usage: python scripts/attn_sm.py [config] [json options]"""
+the GPC / die layout?  Usage: python scripts/attn_sm.py [config] [json options]
+Needs the instrumented library: EL_DEBUG=1 python paper_2407_20272_b200/build.py --force
+"""
 import ctypes as C
 import json
 import sys

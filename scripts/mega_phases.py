@@ -1,7 +1,9 @@
 """Phase timeline of the persistent decode-iteration kernel (dbg bit 128: CTA 0
 stamps %globaltimer at every grid barrier).  Usage:
     python scripts/mega_phases.py [config c2|c5|c1|c3] [technique] [json options]
-Prints per-phase durations of one iteration, averaged per layer."""
+Prints per-phase durations of one iteration, averaged per layer.
+Needs the instrumented library: EL_DEBUG=1 python paper_2407_20272_b200/build.py --force
+"""
 import ctypes as C
 import json
 import sys
