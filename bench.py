@@ -35,7 +35,7 @@ PROMPT, OUT_LEN = 512, 128
 CONFIGS = {
     # BASELINE.json configs[0..4]; thresholds calibrated on the seeded random-init model
     # (the Table-1 values give all-or-nothing exits here) -- see DESIGN.md
-    "c1": dict(L=6, d=512, B=8, tech="softmax", lam=1e-7, gamma=1.0,
+    "c1": dict(L=6, d=512, B=8, tech="softmax", lam=4.5e-8, gamma=1.0,
                name="configs[0]: CALM-T5-small dims (L=6, d=512), softmax-response exit, batch 8"),
     "c2": dict(L=12, d=768, B=64, tech="state", lam=0.981, gamma=0.997,
                name="configs[1]: CALM-T5-base dims (L=12, d=768), hidden-state-similarity exit, batch 64, paged KV"),
@@ -43,6 +43,12 @@ CONFIGS = {
                name="configs[2]: CALM-T5-large dims (L=24, d=1024), exit classifier, batch 128, skipped-layer KV fill"),
     "c5": dict(L=24, d=1024, B=256, tech="classifier", lam=0.41, gamma=0.997,
                name="configs[4]: CALM-T5-large dims, request-sharded batch 256/GPU"),
+    # configs[3] (C4): CALM-T5-large dims, batch 128, full layers vs each criterion on the same inputs
+    # (the classifier leg is c3); thresholds from scripts/calibrate_oracle.py (target e ~ L/2)
+    "c4s": dict(L=24, d=1024, B=128, tech="state", lam=0.9819, gamma=0.999,
+                name="configs[3]: CALM-T5-large dims, batch 128, hidden-state-similarity exit"),
+    "c4m": dict(L=24, d=1024, B=128, tech="softmax", lam=8.2e-8, gamma=1.0,
+                name="configs[3]: CALM-T5-large dims, batch 128, softmax-response exit"),
     # T5 mode (north_star (1); not in the reference): the 512-token input goes through cross-attention
     # over 512 synthetic encoder states; the decoder self-attention holds the generated tokens
     # (seeded prefix of 63 = mid-generation of the 128-token outputs)

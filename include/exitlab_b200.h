@@ -25,6 +25,7 @@
  *   el_session_block_table  KvStore block_table (kv_cache.hpp:83), read back from the device
  *   el_kv_block_trace       KvStore::allocate / release LIFO order (kv_cache.cpp:53-55, 78-106, 182-194)
  *   el_model_tensor         ModelWeights tensors (model.hpp:38-55), bf16 on the device
+ *   el_*metrics*            MetricsReport compute_metrics (metrics.hpp:20-40, metrics.cpp:13-58)
  */
 #ifndef EXITLAB_B200_H
 #define EXITLAB_B200_H
@@ -122,7 +123,8 @@ int el_session_block_table(el_engine* e, int row, int32_t* out /* [L][bpl] */, i
 /* timing on the engine's stream with CUDA events (synchronised on both sides) */
 int el_time_decode(el_engine* e, int n_iters, float* ms);
 /* standalone kernel timing on the current session state: kind 0 attention,
- * 1 qkv gemm, 2 wo, 3 up, 4 down, 5 lm head; layer fixed; reps launches */
+ * 1 qkv gemm, 2 wo, 3 up, 4 down, 5 lm head; layer fixed; reps launches;
+ * kind | 0x100: write 256 MB (2x L2) before each launch and time the launches alone */
 int el_time_kernel(el_engine* e, int kind, int layer, int reps, float* ms);
 int el_sync(el_engine* e);
 /* experiment support: per-CTA phase timestamps (option "dbg" bit 8) */
@@ -132,6 +134,24 @@ int el_debug_timeline_reset(el_engine* e);
 int el_launches_per_iteration(el_engine* e, int output_layer);
 /* plan details: attention chunking, GEMM splits (for DESIGN / bench reporting) */
 int el_plan_info(el_engine* e, int64_t* out, int cap);
+
+/* MetricsReport (metrics.hpp:20-34) and compute_metrics (metrics.cpp:13-58) over a transcript:
+ * throughput = tokens / final clock, inner-token latency = sum(finish - first) / tokens,
+ * early-exit rate = % of tokens decoded by iterations with output_layer < L, mean layers per
+ * token, exit-layer (by iteration) and accept-layer (by sequence) histograms [n_layers]. */
+typedef struct {
+    double throughput, inner_token_latency, early_exit_rate_pct, mean_layers_per_token;
+    double total_sim_time, total_idle_time, wall_clock_info_s;
+    int64_t total_tokens, iterations;
+    int n_layers, pool_blocks, free_blocks, peak_blocks;
+} el_metrics;
+int el_transcript_metrics(const el_transcript* t, el_metrics* out, int64_t* exit_hist, int64_t* accept_hist);
+/* the same over flat transcript fields (any engine's transcript; meta = {final clock, idle,
+ * pool blocks, free blocks, peak blocks}) */
+int el_metrics_compute(int n_layers, int n_iters, const int32_t* it_output_layer, const int32_t* it_batch_off,
+                       int n_seqs, const int32_t* sq_id, const int32_t* sq_tok_off, const int32_t* sq_exit_layers,
+                       const double* sq_first, const double* sq_finish, const double* meta, el_metrics* out,
+                       int64_t* exit_hist, int64_t* accept_hist);
 
 /* LIFO allocator on the host mirror (same arithmetic the device kernels run) */
 int el_kv_block_trace(int n_layers, int pool_blocks, int block_capacity, int n_ops, const int32_t* ops,

@@ -289,6 +289,14 @@ class _Lib:
         if rc:
             raise RuntimeError(self.err())
 
+    def write_report(self, t, path, fmt, wall=0.0):
+        """compute_metrics + write_report of the reference itself (oracle/_ref only)"""
+        f = self.fn("transcript_write_report")
+        f.argtypes = [C.c_void_p, C.c_char_p, C.c_char_p, C.c_double]
+        rc = f(t.handle, path.encode(), fmt.encode(), wall)
+        if rc:
+            raise RuntimeError(self.err())
+
     def free_transcript(self, t):
         if getattr(t, "handle", None):
             self.fn("transcript_free")(t.handle)
@@ -429,6 +437,25 @@ class Session:
             raise RuntimeError(lib.err())
         return dict(output_layer=e, tokens=toks, accept=acc, conf=conf, h_exit=hx)
 
+    # layer-stepped iteration (reference only): a batch sharded over processes keeps the
+    # reference's batch-wide exit barrier (oracle/ref_capi.cpp ref_session_iter_*)
+    def iter_begin(self, tokens_in=None):
+        tin = np.ascontiguousarray(tokens_in, dtype=np.int32) if tokens_in is not None else None
+        if self.m.lib.fn("session_iter_begin")(self.h, _p(tin, C.c_int32)):
+            raise RuntimeError(self.m.lib.err())
+
+    def iter_layer(self, layer) -> bool:
+        r = self.m.lib.fn("session_iter_layer")(self.h, layer)
+        if r < 0:
+            raise RuntimeError(self.m.lib.err())
+        return bool(r)
+
+    def iter_finish(self, output_layer):
+        toks = np.zeros(self.B, np.int32); acc = np.zeros(self.B, np.int32)
+        if self.m.lib.fn("session_iter_finish")(self.h, output_layer, _p(toks, C.c_int32), _p(acc, C.c_int32)):
+            raise RuntimeError(self.m.lib.err())
+        return toks, acc
+
     def kv(self, row, layer, pos):
         d = self.m.d
         k = np.zeros(d); v = np.zeros(d)
@@ -497,6 +524,9 @@ class Ref(_Lib):
         L.ref_session_step.argtypes = [C.c_void_p, C.c_int, C.POINTER(C.c_int32), C.POINTER(C.c_int32),
                                        C.POINTER(C.c_int32), C.POINTER(C.c_double), C.POINTER(C.c_double)]
         L.ref_greedy_token.argtypes = [C.POINTER(C.c_double), C.c_int]
+        L.ref_session_iter_begin.argtypes = [C.c_void_p, C.POINTER(C.c_int32)]
+        L.ref_session_iter_layer.argtypes = [C.c_void_p, C.c_int]
+        L.ref_session_iter_finish.argtypes = [C.c_void_p, C.c_int, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]
 
     def engine_run(self, model, cfg, wl: Workload, fixed_conf=None) -> Transcript:
         if fixed_conf is not None:

@@ -22,6 +22,7 @@
 #include "exitlab/engine.hpp"
 #include "exitlab/exit_policy.hpp"
 #include "exitlab/kv_cache.hpp"
+#include "exitlab/metrics.hpp"
 #include "exitlab/model.hpp"
 #include "exitlab/numerics.hpp"
 #include "exitlab/oracle.hpp"
@@ -187,6 +188,9 @@ struct Session {
     EngineConfig ec;
     std::unique_ptr<KvStore> cache;
     std::vector<int> ids, next_input;
+    // layer-stepped iteration state (ref_session_iter_*)
+    std::vector<std::pair<int, Vector>> states;
+    std::unique_ptr<ExitStatusVector> status;
 };
 
 }  // namespace
@@ -291,6 +295,18 @@ int ref_transcript_write_jsonl(void* tp, const char* path) {
     return EO_OK;
     GUARD_END(ret_code)
 }
+
+// compute_metrics + write_report (metrics.cpp:13-58, 178-195) of a reference transcript;
+// wall_clock_info_s (a host wall-clock reading) is set to `wall` so reports compare byte for byte
+int ref_transcript_write_report(void* tp, const char* path, const char* format, double wall) {
+    GUARD_BEGIN
+    MetricsReport r = compute_metrics(static_cast<FlatTranscript*>(tp)->t);
+    r.wall_clock_info_s = wall;
+    write_report(r, path, format);
+    return EO_OK;
+    GUARD_END(ret_code)
+}
+
 int64_t ref_transcript_len(void* tp, const char* f) {
     auto* t = static_cast<FlatTranscript*>(tp);
     if (auto* a = t->i32(f)) return (int64_t)a->size();
@@ -559,6 +575,79 @@ int ref_session_step(void* sp, int forced, const int32_t* tokens_in, int32_t* to
         g_err = e.what();
         return -code_of(e);
     }
+}
+
+
+// ---- the same decode_iteration, stepped one layer at a time, so a batch sharded over several
+//      processes keeps the reference's batch-wide barrier: each shard reports whether all of
+//      ITS sequences are accepted after `layer` (ExitStatusVector::observe_layer, engine.cpp:55-66);
+//      the coordinator ends the iteration at the first layer where every shard is all-set
+//      (the AND over shards is all_set() of the whole batch) and calls finish with it ----
+int ref_session_iter_begin(void* sp, const int32_t* tokens_in) {
+    GUARD_BEGIN
+    auto* s = static_cast<Session*>(sp);
+    if (tokens_in)
+        for (size_t b = 0; b < s->ids.size(); ++b) s->next_input[b] = tokens_in[b];
+    s->states.clear();
+    for (size_t b = 0; b < s->ids.size(); ++b) s->states.emplace_back(s->ids[b], embed(*s->w, s->next_input[b]));
+    s->status = std::make_unique<ExitStatusVector>((int)s->ids.size());
+    return EO_OK;
+    GUARD_END(ret_code)
+}
+// returns 1 when every sequence of this shard has accepted at some layer <= `layer`, 0 if not, <0 on error
+int ref_session_iter_layer(void* sp, int layer) {
+    try {
+        auto* s = static_cast<Session*>(sp);
+        const ModelWeights& w = *s->w;
+        const int B = (int)s->ids.size();
+        const ExitTechnique& technique = s->ec.technique;
+        std::vector<Vector> next = layer_forward(w, layer, s->states, *s->cache);
+        std::vector<bool> accepted((size_t)B, false);
+        const double lambda = threshold_at(s->ec.schedule, layer);
+        for (int b = 0; b < B; ++b) {
+            ExitEvidence ev;
+            ev.layer = layer;
+            Vector logits;
+            switch (technique.kind) {
+                case TechniqueKind::softmax_response:
+                    logits = lm_head_logits(w, next[(size_t)b]);
+                    ev.logits = &logits;
+                    break;
+                case TechniqueKind::state_similarity:
+                    ev.h_prev = &s->states[(size_t)b].second;
+                    ev.h_cur = &next[(size_t)b];
+                    break;
+                case TechniqueKind::classifier:
+                    ev.h_cur = &next[(size_t)b];
+                    ev.probe = &w.probe;
+                    break;
+                default: break;
+            }
+            accepted[(size_t)b] = decide(technique, ev, lambda);
+        }
+        for (int b = 0; b < B; ++b) s->states[(size_t)b].second = std::move(next[(size_t)b]);
+        return s->status->observe_layer(layer, accepted) ? 1 : 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return -code_of(e);
+    }
+}
+int ref_session_iter_finish(void* sp, int output_layer, int32_t* tokens, int32_t* accept) {
+    GUARD_BEGIN
+    auto* s = static_cast<Session*>(sp);
+    const ModelWeights& w = *s->w;
+    const int L = s->cfg.n_layers, B = (int)s->ids.size();
+    const KvPairFn kv_fn = [&w](int layer, const Vector& h) { return compute_kv_pair(w, layer, h); };
+    fill_skipped(*s->cache, s->states, output_layer, kv_fn);
+    for (int b = 0; b < B; ++b) s->cache->commit(s->ids[(size_t)b]);
+    for (int b = 0; b < B; ++b) {
+        const int tok = greedy_token(lm_head_logits(w, s->states[(size_t)b].second));
+        if (tokens) tokens[b] = tok;
+        if (accept) accept[b] = s->status->first_accept_layer(b, L);
+        s->next_input[(size_t)b] = tok;
+    }
+    return EO_OK;
+    GUARD_END(ret_code)
 }
 
 int ref_session_kv(void* sp, int row, int layer, int pos, double* k, double* v) {

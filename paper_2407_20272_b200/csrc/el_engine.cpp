@@ -163,8 +163,8 @@ struct el_engine {
     bool fuse_exit = true;
     bool fuse_exit_all = false;
     // decode-iteration strategy: 0 per-phase kernels (graph / eager), 1 persistent kernel
-    // (el_iter.cuh), 2 auto: persistent at batch >= 128 (measured faster there: weight
-    // streaming and the exit check amortise its grid barriers), per-phase kernels below
+    // (el_iter.cuh), 2 auto: persistent at batch >= 64 outside softmax exit (measured faster
+    // there: weight streaming and the exit check amortise its grid barriers), per-phase below
     int use_mega = 2;
     bool mega_for(int B) const {
         if (cfg.encoder_len > 0) {  // T5 mode: the cross-attention sub-layer lives in the persistent kernel
@@ -207,6 +207,7 @@ struct el_engine {
     DevBuf<double> lambdas, exit_part;
     DevBuf<unsigned long long> dbg_ts;
     DevBuf<float> fixed_conf;
+    DevBuf<uint8_t> l2flush;  // cold-L2 kernel timing (el_time_kernel kind | 0x100)
     int* cont_host = nullptr;
     int* cont_dev = nullptr;
 
@@ -1442,6 +1443,7 @@ int el_engine_set_option(el_engine* e, const char* key, int64_t v) {
         e->invalidate_graphs();
     }
     else if (!std::strcmp(key, "attn_cb") || !std::strcmp(key, "attn_stages")) {
+        if (v < 0 || v > 8) fail(EL_INVALID_ARGUMENT, "%s must be in [0 (auto), 8]", key);
         (key[5] == 'c' ? e->opt_attn_cb : e->opt_attn_stages) = (int)v;
         e->plan_attention();
     } else if (!std::strcmp(key, "nsplit") || !std::strcmp(key, "cta_target")) {
@@ -1536,6 +1538,10 @@ int el_decode_iteration(el_engine* e, const int32_t* tokens_in, int32_t* tokens_
     e->need_session();
     e->check_capacity(1);
     const int B = e->sess_B;
+    if (tokens_in)  // embed() rejects ids outside the vocabulary (model.cpp:171-183)
+        for (int b = 0; b < B; ++b)
+            if (tokens_in[b] < 0 || tokens_in[b] >= e->cfg.vocab_size)
+                fail(EL_INVALID_ARGUMENT, "embed: token id %d outside vocab", tokens_in[b]);
     if (tokens_in) CK(cudaMemcpyAsync(e->row_tok.p, tokens_in, sizeof(int) * B, cudaMemcpyHostToDevice, e->stream));
     e->iteration(B);
     const auto o = e->read_iteration(e->sess_iters, B);
@@ -1652,6 +1658,8 @@ int el_time_kernel(el_engine* e, int kind, int layer, int reps, float* ms) {
     API_BEGIN
     e->need_session();
     if (layer < 1 || layer > e->dm.L) fail(EL_INVALID_ARGUMENT, "layer out of range");
+    const bool flush = (kind & 0x100) != 0;
+    kind &= 0xff;
     const int B = e->sess_B;
     auto& P = e->plans_for(B);
     el::DevState s = e->state(false, B);
@@ -1675,12 +1683,30 @@ int el_time_kernel(el_engine* e, int kind, int layer, int reps, float* ms) {
     // values the iteration would write (idempotent for timing purposes)
     one();
     CK(cudaStreamSynchronize(e->stream));
-    CK(cudaEventRecord(a, e->stream));
-    for (int i = 0; i < reps; ++i) one();
-    CK(cudaEventRecord(b, e->stream));
-    CK(cudaEventSynchronize(b));
-    CK(cudaEventElapsedTime(ms, a, b));
-    *ms /= (float)reps;
+    if (flush) {
+        // cold-L2 timing: a 256 MB write (2x the 126 MB L2) before every launch, each
+        // launch bracketed by its own events on the engine stream
+        if (!e->l2flush.p) e->l2flush.alloc((size_t)256 << 20, false);
+        float total = 0.f;
+        for (int i = 0; i < reps; ++i) {
+            CK(cudaMemsetAsync(e->l2flush.p, i & 0xff, e->l2flush.n, e->stream));
+            CK(cudaEventRecord(a, e->stream));
+            one();
+            CK(cudaEventRecord(b, e->stream));
+            CK(cudaEventSynchronize(b));
+            float t = 0.f;
+            CK(cudaEventElapsedTime(&t, a, b));
+            total += t;
+        }
+        *ms = total / (float)reps;
+    } else {
+        CK(cudaEventRecord(a, e->stream));
+        for (int i = 0; i < reps; ++i) one();
+        CK(cudaEventRecord(b, e->stream));
+        CK(cudaEventSynchronize(b));
+        CK(cudaEventElapsedTime(ms, a, b));
+        *ms /= (float)reps;
+    }
     cudaEventDestroy(a);
     cudaEventDestroy(b);
     API_END
@@ -1774,6 +1800,63 @@ int el_kv_block_trace(int L, int pool, int cap, int n_ops, const int32_t* ops, c
         g_err = e.msg;
         return -e.code;
     }
+}
+
+
+// compute_metrics (metrics.cpp:13-58) over flat transcript fields
+int el_metrics_compute(int L, int n_iters, const int32_t* it_out, const int32_t* it_off, int n_seqs,
+                       const int32_t* sq_id, const int32_t* tok_off, const int32_t* sq_exit, const double* sq_first,
+                       const double* sq_finish, const double* meta, el_metrics* r, int64_t* exit_hist,
+                       int64_t* accept_hist) {
+    API_BEGIN
+    if (L < 1 || n_iters < 0 || n_seqs < 0 || !r) fail(EL_INVALID_ARGUMENT, "compute_metrics: bad arguments");
+    *r = el_metrics{};
+    r->n_layers = L;
+    std::vector<int64_t> eh((size_t)L, 0), ah((size_t)L, 0);
+    r->total_sim_time = meta[0];
+    r->total_idle_time = meta[1];
+    r->iterations = n_iters;
+    r->pool_blocks = (int)meta[2];
+    r->free_blocks = (int)meta[3];
+    r->peak_blocks = (int)meta[4];
+    double latency_sum = 0.0;
+    for (int s = 0; s < n_seqs; ++s) {
+        if (sq_finish[s] < 0.0 || sq_first[s] < 0.0)
+            fail(EL_INVALID_ARGUMENT, "compute_metrics: sequence %d is unfinished", sq_id ? sq_id[s] : s);
+        r->total_tokens += tok_off[s + 1] - tok_off[s];
+        latency_sum += sq_finish[s] - sq_first[s];
+        for (int i = tok_off[s]; i < tok_off[s + 1]; ++i) {
+            if (sq_exit[i] < 1 || sq_exit[i] > L) fail(EL_INVALID_ARGUMENT, "compute_metrics: accept layer out of range");
+            ++ah[(size_t)sq_exit[i] - 1];
+        }
+    }
+    int64_t early = 0, layer_sum = 0;
+    for (int i = 0; i < n_iters; ++i) {
+        const int64_t batch = it_off[i + 1] - it_off[i];
+        if (it_out[i] < 1 || it_out[i] > L) fail(EL_INVALID_ARGUMENT, "compute_metrics: output layer out of range");
+        eh[(size_t)it_out[i] - 1] += batch;
+        layer_sum += batch * it_out[i];
+        if (it_out[i] < L) early += batch;
+    }
+    if (r->total_tokens > 0) {
+        r->inner_token_latency = latency_sum / (double)r->total_tokens;
+        r->early_exit_rate_pct = 100.0 * (double)early / (double)r->total_tokens;
+        r->mean_layers_per_token = (double)layer_sum / (double)r->total_tokens;
+        if (r->total_sim_time > 0.0) r->throughput = (double)r->total_tokens / r->total_sim_time;
+    }
+    if (exit_hist) std::memcpy(exit_hist, eh.data(), sizeof(int64_t) * (size_t)L);
+    if (accept_hist) std::memcpy(accept_hist, ah.data(), sizeof(int64_t) * (size_t)L);
+    API_END
+}
+
+int el_transcript_metrics(const el_transcript* t, el_metrics* out, int64_t* exit_hist, int64_t* accept_hist) {
+    if (!t) {
+        g_err = "null transcript";
+        return EL_INVALID_ARGUMENT;
+    }
+    return el_metrics_compute(t->L, (int)t->it_output_layer.size(), t->it_output_layer.data(), t->it_batch_off.data(),
+                              (int)t->sq_id.size(), t->sq_id.data(), t->sq_tok_off.data(), t->sq_exit_layers.data(),
+                              t->sq_first.data(), t->sq_finish.data(), t->meta.data(), out, exit_hist, accept_hist);
 }
 
 int el_model_tensor(el_engine* e, int which, int layer, uint16_t* out, int64_t cap) {

@@ -1138,7 +1138,9 @@ __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(const __grid_cons
         // this barrier and streams the old K/V blocks of its range while the grid waits; q and
         // the newest block (this phase's output) wait on the barrier count
         AttnSrc self_l = self_src;
-        const bool early = p.att_early && !(EL_DBG(st) & ((1 << 25) | (1 << 27)));
+        // not in batched prefill: one launch holds several positions of a sequence, so blocks
+        // older than a row's newest one may be written by this launch's QKV phase
+        const bool early = p.att_early && !st.prefill && !(EL_DBG(st) & ((1 << 25) | (1 << 27)));
         if (early) {
             self_l.gate = p.bar;
             self_l.gate_target = g0.y + (unsigned)G * (unsigned)(nbar + 1);

@@ -82,6 +82,8 @@ def lib():
         L.el_model_tensor.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_int64]
         L.el_set_device.argtypes = [C.c_int]
         L.el_device_count.argtypes = [C.c_void_p]
+        L.el_transcript_metrics.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+        L.el_metrics_compute.argtypes = [C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_int] + [C.c_void_p] * 9
         _lib = L
     return _lib
 
@@ -424,6 +426,175 @@ def read_transcript_jsonl(path):
     if out["meta"] is None:
         raise RuntimeError(f"transcript: missing meta record in {path}")
     return out
+
+
+# ---------------------------------------------------------------- metrics (metrics.hpp:20-45)
+class _CMetrics(C.Structure):
+    _fields_ = [("throughput", C.c_double), ("inner_token_latency", C.c_double), ("early_exit_rate_pct", C.c_double),
+                ("mean_layers_per_token", C.c_double), ("total_sim_time", C.c_double),
+                ("total_idle_time", C.c_double), ("wall_clock_info_s", C.c_double), ("total_tokens", C.c_int64),
+                ("iterations", C.c_int64), ("n_layers", C.c_int), ("pool_blocks", C.c_int),
+                ("free_blocks", C.c_int), ("peak_blocks", C.c_int)]
+
+
+@dataclass
+class MetricsReport:
+    """MetricsReport (metrics.hpp:20-34)."""
+    throughput: float = 0.0
+    inner_token_latency: float = 0.0
+    early_exit_rate_pct: float = 0.0
+    exit_layer_histogram: list = field(default_factory=list)
+    accept_layer_histogram: list = field(default_factory=list)
+    mean_layers_per_token: float = 0.0
+    total_sim_time: float = 0.0
+    total_idle_time: float = 0.0
+    total_tokens: int = 0
+    iterations: int = 0
+    n_layers: int = 0
+    cache: dict = field(default_factory=lambda: {"pool_blocks": 0, "free_blocks": 0, "peak_blocks": 0})
+    wall_clock_info_s: float = 0.0
+
+
+def _metrics_from_c(m, eh, ah):
+    return MetricsReport(m.throughput, m.inner_token_latency, m.early_exit_rate_pct, eh.tolist(), ah.tolist(),
+                         m.mean_layers_per_token, m.total_sim_time, m.total_idle_time, int(m.total_tokens),
+                         int(m.iterations), int(m.n_layers),
+                         {"pool_blocks": m.pool_blocks, "free_blocks": m.free_blocks, "peak_blocks": m.peak_blocks},
+                         m.wall_clock_info_s)
+
+
+def compute_metrics(t, n_layers=None) -> MetricsReport:
+    """compute_metrics (metrics.cpp:13-58) -- native (libexitlab_b200) over any flat transcript:
+    this engine's Transcript, or the oracle's / reference's (then pass n_layers)."""
+    L = n_layers or t.L
+    m = _CMetrics()
+    eh = np.zeros(L, np.int64)
+    ah = np.zeros(L, np.int64)
+    if isinstance(t, Transcript):
+        _check(lib().el_transcript_metrics(t._h, C.byref(m), _ptr(eh), _ptr(ah)))
+    else:
+        f = {k: np.ascontiguousarray(t[k]) for k in ("it_output_layer", "it_batch_off", "sq_id", "sq_tok_off",
+                                                     "sq_exit_layers", "sq_first", "sq_finish", "meta")}
+        _check(lib().el_metrics_compute(L, len(f["it_output_layer"]), _ptr(f["it_output_layer"].astype(np.int32)),
+                                        _ptr(f["it_batch_off"].astype(np.int32)), len(f["sq_id"]),
+                                        _ptr(f["sq_id"].astype(np.int32)), _ptr(f["sq_tok_off"].astype(np.int32)),
+                                        _ptr(f["sq_exit_layers"].astype(np.int32)),
+                                        _ptr(f["sq_first"].astype(np.float64)), _ptr(f["sq_finish"].astype(np.float64)),
+                                        _ptr(f["meta"].astype(np.float64)), C.byref(m), _ptr(eh), _ptr(ah)))
+    return _metrics_from_c(m, eh, ah)
+
+
+def session_metrics(output_layers, accept, n_layers) -> dict:
+    """compute_metrics' token-weighted exit statistics for fixed-batch decode records
+    (every iteration decodes the whole batch): early-exit rate, mean layers per token and the
+    exit / accept histograms (metrics.cpp:33-55)."""
+    e = np.asarray(output_layers, np.int64)
+    a = np.asarray(accept, np.int64).reshape(len(e), -1)
+    B = a.shape[1]
+    return {"early_exit_rate_pct": float(100.0 * np.mean(e < n_layers)) if len(e) else 0.0,
+            "mean_layers_per_token": float(e.mean()) if len(e) else 0.0,
+            "exit_layer_histogram": (np.bincount(e - 1, minlength=n_layers) * B).tolist(),
+            "accept_layer_histogram": np.bincount(a.ravel() - 1, minlength=n_layers).tolist()}
+
+
+def _json_pretty(v, ind=0):
+    """nlohmann::ordered_json::dump(2) formatting of the report object."""
+    import json
+    pad, pad2 = " " * ind, " " * (ind + 2)
+    if isinstance(v, dict):
+        if not v:
+            return "{}"
+        return "{\n" + ",\n".join(pad2 + json.dumps(k) + ": " + _json_pretty(x, ind + 2) for k, x in v.items()) + \
+            "\n" + pad + "}"
+    return _json_dump(v)  # arrays stay on one line in this nlohmann build (observed, tests/test_metrics_cpu.py)
+
+
+def _g17(x):
+    return "%.17g" % float(x)
+
+
+def write_report(r: MetricsReport, path, fmt):
+    """write_report (metrics.cpp:178-195): JSON (ordered keys, dump(2)) or CSV (metric,value with
+    %.17g doubles), byte-identical to the reference's writer."""
+    if fmt not in ("json", "csv"):
+        raise ValueError(f"write_report: unsupported format '{fmt}' (expected json or csv)")
+    if fmt == "json":
+        j = {"throughput_tokens_per_s": float(r.throughput), "inner_token_latency_s": float(r.inner_token_latency),
+             "early_exit_rate_pct": float(r.early_exit_rate_pct),
+             "exit_layer_histogram": [int(x) for x in r.exit_layer_histogram],
+             "accept_layer_histogram": [int(x) for x in r.accept_layer_histogram],
+             "mean_layers_per_token": float(r.mean_layers_per_token), "total_sim_time_s": float(r.total_sim_time),
+             "total_idle_time_s": float(r.total_idle_time), "total_tokens": int(r.total_tokens),
+             "iterations": int(r.iterations), "n_layers": int(r.n_layers),
+             "cache": {"pool_blocks": int(r.cache["pool_blocks"]), "free_blocks": int(r.cache["free_blocks"]),
+                       "peak_blocks": int(r.cache["peak_blocks"])},
+             "wall_clock_info_s": float(r.wall_clock_info_s)}
+        text = _json_pretty(j) + "\n"
+    else:
+        rows = [("throughput_tokens_per_s", _g17(r.throughput)), ("inner_token_latency_s", _g17(r.inner_token_latency)),
+                ("early_exit_rate_pct", _g17(r.early_exit_rate_pct)),
+                ("mean_layers_per_token", _g17(r.mean_layers_per_token)), ("total_sim_time_s", _g17(r.total_sim_time)),
+                ("total_idle_time_s", _g17(r.total_idle_time)), ("total_tokens", str(int(r.total_tokens))),
+                ("iterations", str(int(r.iterations))), ("n_layers", str(int(r.n_layers))),
+                ("cache_pool_blocks", str(int(r.cache["pool_blocks"]))),
+                ("cache_free_blocks", str(int(r.cache["free_blocks"]))),
+                ("cache_peak_blocks", str(int(r.cache["peak_blocks"]))),
+                ("wall_clock_info_s", _g17(r.wall_clock_info_s))]
+        rows += [(f"exit_layer_{i + 1}", str(int(x))) for i, x in enumerate(r.exit_layer_histogram)]
+        rows += [(f"accept_layer_{i + 1}", str(int(x))) for i, x in enumerate(r.accept_layer_histogram)]
+        text = "metric,value\n" + "".join(f"{k},{v}\n" for k, v in rows)
+    with open(path, "w") as f:
+        f.write(text)
+
+
+def read_report(path, fmt) -> MetricsReport:
+    """read_report (metrics.cpp:197-210): the inverse of write_report, reference error messages."""
+    import json
+    if fmt not in ("json", "csv"):
+        raise ValueError(f"read_report: unsupported format '{fmt}'")
+    if not os.path.exists(path):
+        raise RuntimeError(f"read_report: cannot open {path}")
+    if fmt == "json":
+        try:
+            with open(path) as f:
+                j = json.load(f)
+        except json.JSONDecodeError as e:
+            raise ValueError(f"report: {path}: {e}") from None
+        try:
+            return MetricsReport(float(j["throughput_tokens_per_s"]), float(j["inner_token_latency_s"]),
+                                 float(j["early_exit_rate_pct"]), [int(x) for x in j["exit_layer_histogram"]],
+                                 [int(x) for x in j["accept_layer_histogram"]], float(j["mean_layers_per_token"]),
+                                 float(j["total_sim_time_s"]), float(j["total_idle_time_s"]), int(j["total_tokens"]),
+                                 int(j["iterations"]), int(j["n_layers"]),
+                                 {k: int(j["cache"][k]) for k in ("pool_blocks", "free_blocks", "peak_blocks")},
+                                 float(j["wall_clock_info_s"]))
+        except KeyError as e:
+            raise ValueError(f"report: {path}: missing key {e}") from None
+    with open(path) as f:
+        lines = f.read().split("\n")
+    if not lines or lines[0] != "metric,value":
+        raise ValueError(f"report: {path}: missing 'metric,value' header")
+    rows = {}
+    for line in lines[1:]:
+        if not line:
+            continue
+        if "," not in line:
+            raise ValueError(f"report: {path}: bad row '{line}'")
+        k, v = line.split(",", 1)
+        rows.setdefault(k, v)
+
+    def take(k):
+        if k not in rows:
+            raise ValueError(f"report: {path}: missing metric '{k}'")
+        return rows[k]
+    n = int(take("n_layers"))
+    return MetricsReport(float(take("throughput_tokens_per_s")), float(take("inner_token_latency_s")),
+                         float(take("early_exit_rate_pct")), [int(take(f"exit_layer_{i}")) for i in range(1, n + 1)],
+                         [int(take(f"accept_layer_{i}")) for i in range(1, n + 1)],
+                         float(take("mean_layers_per_token")), float(take("total_sim_time_s")),
+                         float(take("total_idle_time_s")), int(take("total_tokens")), int(take("iterations")), n,
+                         {"pool_blocks": int(take("cache_pool_blocks")), "free_blocks": int(take("cache_free_blocks")),
+                          "peak_blocks": int(take("cache_peak_blocks"))}, float(take("wall_clock_info_s")))
 
 
 # ---------------------------------------------------------------- engine
