@@ -58,3 +58,34 @@ def test_two_rank_gloo_sharding_and_max_time():
     ids = [r[1] for r in res]
     assert ids[0] == [0, 1, 2, 3] and ids[1] == [4, 5, 6, 7]  # disjoint, covering, contiguous
     assert all(r[2] == 11.0 for r in res)  # max over ranks on every rank
+
+
+@pytest.mark.timeout(300)
+def test_bench_self_launches_two_ranks_and_reports():
+    """`python bench.py --gpus 2` re-launches itself under torchrun (one rank per device), shards
+    the requests, takes the max over ranks and prints ONE JSON line from rank 0 -- exercised with
+    the CPU stub engine (EL_BENCH_STUB=1) over gloo."""
+    import json
+    import subprocess
+    import sys
+    env = dict(os.environ, EL_BENCH_STUB="1")
+    r = subprocess.run([sys.executable, os.path.join(bench.ROOT, "bench.py"), "--gpus", "2", "--steps", "3",
+                        "--warmup", "3", "--config", "c2"], capture_output=True, text=True, env=env, timeout=280)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [x for x in r.stdout.splitlines() if x.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    j = json.loads(lines[0])
+    assert j["n_gpus"] == 2 and j["config"]["global_batch"] == 128 and j["scaling"] == "weak"
+    # stub: rank r takes 3 * (1 + 0.1 r) ms for 3 steps -> max over ranks = 3.3 ms
+    assert abs(j["value"] - 64 * 2 * 3 / 3.3e-3) < 1.0
+    assert j["layers_per_token"] == 6 and j["metrics"]["early_exit_rate_pct"] == 100.0
+    assert j["full_layer"]["layers_per_token"] == 12
+
+
+def test_bench_rejects_world_size_mismatch():
+    import subprocess
+    import sys
+    env = dict(os.environ, EL_BENCH_STUB="1", WORLD_SIZE="1", RANK="0")
+    r = subprocess.run([sys.executable, os.path.join(bench.ROOT, "bench.py"), "--gpus", "2", "--steps", "3",
+                        "--warmup", "3"], capture_output=True, text=True, env=env, timeout=60)
+    assert r.returncode != 0 and "WORLD_SIZE" in r.stderr

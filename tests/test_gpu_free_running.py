@@ -32,9 +32,14 @@ pytestmark = [pytest.mark.gpu, pytest.mark.slow]
 
 V = 32128
 # tolerances (bf16 weights and GEMM operands, fp32 accumulation / residual stream, against fp64)
-CONF_TOL = {"state": 6e-4, "classifier": 6e-4}  # absolute
-SM_RTOL = 0.05  # softmax response (p1 - p2 ~ 1e-7 at V = 32128): relative to the oracle's value
-HID_TOL = 8e-3  # max|diff| / max|ref| of the exit hidden state when both engines exit at the same layer
+CONF_TOL = {"state": 1e-4, "classifier": 1e-4}  # absolute (observed max 3.3e-5 over C2-C5, 16 iterations)
+# softmax response p1 - p2 = (1 - exp(-(l1 - l2))) / sum exp(l - l1) ~ (l1 - l2) / V at V = 32128 with
+# near-equal logits: bf16 hidden states move the top-2 logit gap by ~1e-4..3e-4 logit units, i.e.
+# ~5e-9 in the confidence (observed max 4.7e-9 at C1, 8.6e-9 at C4 dims, 16 iterations) -> an
+# absolute tolerance; at these dims the criterion itself sits below bf16 resolution
+SM_ATOL = 1.5e-8
+HID_TOL = 5e-3  # max|diff| / max|ref| of the exit hidden state when both engines exit at the same layer
+KV_TOL = 8e-3   # the same for K/V rows (computed: vs the oracle; filled: vs fp64 W_kv h_e of the B200's h_e)
 TIE_GAP = 2e-2  # oracle top-2 logit gap below which a greedy-token disagreement is a tie
 ITERS = 16
 
@@ -86,9 +91,7 @@ def oracle_run(port, name):
 
 
 def conf_tol(tech, conf_o):
-    if tech == "softmax":
-        return SM_RTOL * np.abs(conf_o) + 1e-12
-    return np.full_like(conf_o, CONF_TOL[tech])
+    return np.full_like(conf_o, SM_ATOL if tech == "softmax" else CONF_TOL[tech])
 
 
 @pytest.mark.parametrize("name,mega", CASES)
@@ -166,7 +169,7 @@ def test_free_running_parity(port, name, mega):
                    max_conf_abs_err=max_conf_err, max_conf_rel_err=max_conf_rel, max_h_relerr=max_h,
                    kv_relerr_last_pos=kv_err, fill_relerr_last_pos=fill_err,
                    n_near_threshold=len(ties), n_flipped=len(flips),
-                   tolerances=dict(conf=("rel %g" % SM_RTOL) if tech == "softmax" else CONF_TOL[tech], h=HID_TOL,
+                   tolerances=dict(conf=SM_ATOL if tech == "softmax" else CONF_TOL[tech], h=HID_TOL, kv=KV_TOL,
                                    tie_gap=TIE_GAP),
                    iterations_detail=rows, near_threshold_ties=ties[:200], flipped=flips[:200],
                    token_disagreements_not_ties=tok_untied_bad[:50])
@@ -177,4 +180,4 @@ def test_free_running_parity(port, name, mega):
     assert all(f["tie"] for f in flips), flips[:5]
     assert max_h <= HID_TOL, max_h
     assert not tok_untied_bad, tok_untied_bad[:5]
-    assert kv_err <= HID_TOL and fill_err <= HID_TOL, (kv_err, fill_err)
+    assert kv_err <= KV_TOL and fill_err <= KV_TOL, (kv_err, fill_err)
