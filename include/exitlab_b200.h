@@ -99,6 +99,9 @@ int el_transcript_get_i32(const el_transcript* t, const char* field, int32_t* ou
 int el_transcript_get_f64(const el_transcript* t, const char* field, double* out);
 int el_transcript_kv(const el_transcript* t, int seq_id, int layer, double* k, double* v, int64_t cap);
 int el_transcript_exit_states(const el_transcript* t, int seq_id, double* out, int64_t cap);
+/* capture_kv: the device block table [L][bpl] of a sequence at eviction (KvStore block_table,
+ * kv_cache.hpp:79-84, LIFO order kv_cache.cpp:53-55/182-194); returns bpl (<0 on error) */
+int el_transcript_block_table(const el_transcript* t, int seq_id, int32_t* out, int64_t cap);
 void el_transcript_free(el_transcript* t);
 
 /* fixed batch of B sequences (ids seq_ids[b]) whose KV holds prefix_len seeded

@@ -275,6 +275,16 @@ class _Lib:
             raise ValueError(self.err())
         return k[: c * d].reshape(c, d), v[: c * d].reshape(c, d)
 
+    def transcript_block_table(self, t, seq, n_layers):
+        """block table [L][bpl] of a captured sequence at eviction (C port only)"""
+        f = self.fn("transcript_block_table")
+        f.argtypes = [C.c_void_p, C.c_int, C.POINTER(C.c_int32), C.c_int64]
+        out = np.zeros(1 << 20, np.int32)
+        n = f(t.handle, seq, _p(out, C.c_int32), out.size)
+        if n < 0:
+            raise ValueError(self.err())
+        return out[: n_layers * n].reshape(n_layers, n)
+
     def transcript_exit_states(self, t, seq, d):
         n = 1 << 22
         o = np.zeros(n)

@@ -585,6 +585,8 @@ typedef struct {
     double* v;
     vf64 exit_states;
     int have_kv;
+    int bpl;
+    int* table; /* [L][bpl] block ids at eviction (KvStore block_table, kv_cache.hpp:79-84) */
 } kv_capture;
 
 struct eo_transcript {
@@ -603,7 +605,7 @@ void eo_transcript_free(eo_transcript* t) {
     vf64* fs[] = {&t->pf_clock, &t->pf_charge, &t->it_clock, &t->it_charge, &t->sq_arrival, &t->sq_first,
                   &t->sq_finish, &t->meta, &t->it_conf};
     for (size_t i = 0; i < sizeof fs / sizeof *fs; ++i) free(fs[i]->p);
-    for (int i = 0; i < t->n_caps; ++i) { free(t->caps[i].k); free(t->caps[i].v); free(t->caps[i].exit_states.p); }
+    for (int i = 0; i < t->n_caps; ++i) { free(t->caps[i].k); free(t->caps[i].v); free(t->caps[i].exit_states.p); free(t->caps[i].table); }
     free(t->caps);
     free(t);
 }
@@ -648,6 +650,13 @@ int eo_transcript_kv(const eo_transcript* t, int id, int layer, double* k, doubl
     memcpy(k, c->k + (size_t)(layer - 1) * n, sizeof(double) * n);
     memcpy(v, c->v + (size_t)(layer - 1) * n, sizeof(double) * n);
     return c->committed;
+}
+int eo_transcript_block_table(const eo_transcript* t, int id, int32_t* out, int64_t cap) {
+    if (id < 0 || id >= t->n_caps || !t->caps[id].have_kv) { set_err("no capture for seq %d", id); return -EO_INVALID_ARGUMENT; }
+    const kv_capture* c = &t->caps[id];
+    if ((int64_t)c->bpl * t->L > cap) { set_err("buffer too small"); return -EO_INVALID_ARGUMENT; }
+    for (int i = 0; i < c->bpl * t->L; ++i) out[i] = c->table[i];
+    return c->bpl;
 }
 int eo_transcript_exit_states(const eo_transcript* t, int id, double* out, int64_t cap) {
     if (id < 0 || id >= t->n_caps) { set_err("no capture for seq %d", id); return EO_INVALID_ARGUMENT; }
@@ -788,6 +797,9 @@ int eo_engine_run(const eo_model* m, const eo_engine_config* c, int n_req, const
                         memcpy(cap->v + ((size_t)(layer - 1) * committed + p) * d, kv_slot(&cache, 1, s->id, layer, p), sizeof(double) * (size_t)d);
                     }
                 cap->have_kv = 1;
+                cap->bpl = cache.seqs[s->id].bpl;
+                cap->table = (int*)malloc(sizeof(int) * (size_t)(cap->bpl * L + 1));
+                memcpy(cap->table, cache.seqs[s->id].table, sizeof(int) * (size_t)cap->bpl * L);
             }
             kv_release(&cache, s->id);
             pi(&t->sq_id, s->id);

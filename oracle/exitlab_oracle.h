@@ -122,6 +122,8 @@ int eo_transcript_get_f64(const eo_transcript* t, const char* field, double* out
  * positions ([committed][d]) and the exit states ([tokens][d]) */
 int eo_transcript_kv(const eo_transcript* t, int seq_id, int layer, double* k, double* v,
                      int64_t cap);
+/* block table [L][bpl] of a captured sequence at eviction; returns bpl (<0 on error) */
+int eo_transcript_block_table(const eo_transcript* t, int seq_id, int32_t* out, int64_t cap);
 int eo_transcript_exit_states(const eo_transcript* t, int seq_id, double* out, int64_t cap);
 
 /* ---- single-function checks ---- */

@@ -127,6 +127,8 @@ struct Capture {
     std::vector<double> k, v;  // [L][committed][d]
     std::vector<double> exit_states;
     bool have_kv = false;
+    int bpl = 0;
+    std::vector<int32_t> table;  // [L][bpl] device block table at eviction
 };
 }  // namespace
 
@@ -1073,6 +1075,12 @@ struct el_engine {
                             }
                         }
                     c.have_kv = true;
+                    c.bpl = slot_bpl[(size_t)it->slot];
+                    c.table.resize((size_t)L * c.bpl);
+                    for (int l = 0; l < L; ++l)
+                        CK(cudaMemcpy(c.table.data() + (size_t)l * c.bpl,
+                                      tables.p + ((size_t)it->slot * L + l) * dm.bpl_max, sizeof(int) * c.bpl,
+                                      cudaMemcpyDeviceToHost));
                 }
                 release(it->slot);
                 t->sq_id.push_back(it->id);
@@ -1509,6 +1517,14 @@ int el_transcript_kv(const el_transcript* t, int seq, int layer, double* k, doub
     std::memcpy(k, c.k.data() + (size_t)(layer - 1) * n, sizeof(double) * n);
     std::memcpy(v, c.v.data() + (size_t)(layer - 1) * n, sizeof(double) * n);
     return c.committed;
+}
+int el_transcript_block_table(const el_transcript* t, int seq, int32_t* out, int64_t cap) {
+    auto it = t->caps.find(seq);
+    if (it == t->caps.end() || !it->second.have_kv) { g_err = "no capture for seq"; return -EL_INVALID_ARGUMENT; }
+    const Capture& c = it->second;
+    if ((int64_t)c.table.size() > cap) { g_err = "buffer too small"; return -EL_INVALID_ARGUMENT; }
+    std::memcpy(out, c.table.data(), sizeof(int32_t) * c.table.size());
+    return c.bpl;
 }
 int el_transcript_exit_states(const el_transcript* t, int seq, double* out, int64_t cap) {
     auto it = t->caps.find(seq);

@@ -61,6 +61,7 @@ def lib():
         L.el_transcript_get_f64.argtypes = [C.c_void_p, C.c_char_p, C.c_void_p]
         L.el_transcript_kv.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_int64]
         L.el_transcript_exit_states.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_int64]
+        L.el_transcript_block_table.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_int64]
         L.el_transcript_free.argtypes = [C.c_void_p]
         L.el_transcript_free.restype = None
         L.el_session_begin.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_int, C.c_uint64, C.c_void_p]
@@ -337,6 +338,14 @@ class Transcript:
         if c < 0:
             _check(-c)
         return k[: c * self.d].reshape(c, self.d), v[: c * self.d].reshape(c, self.d)
+
+    def block_table(self, seq_id):
+        """capture_kv: the device block table [L][bpl] of the sequence at eviction"""
+        out = np.zeros(1 << 20, np.int32)
+        n = lib().el_transcript_block_table(self._h, seq_id, _ptr(out), out.size)
+        if n < 0:
+            _check(-n)
+        return out[: self.L * n].reshape(self.L, n)
 
     def exit_states(self, seq_id):
         n = 1 << 22
