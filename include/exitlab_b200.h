@@ -26,6 +26,8 @@
  *   el_kv_block_trace       KvStore::allocate / release LIFO order (kv_cache.cpp:53-55, 78-106, 182-194)
  *   el_model_tensor         ModelWeights tensors (model.hpp:38-55), bf16 on the device
  *   el_*metrics*            MetricsReport compute_metrics (metrics.hpp:20-40, metrics.cpp:13-58)
+ *   el_kv_* el_layer_forward el_kv_fill el_exit_confidence el_greedy_tokens: the sub-engine API
+ *                           (KvStore, layer_forward, fill_skipped, decide, greedy_token; see below)
  */
 #ifndef EXITLAB_B200_H
 #define EXITLAB_B200_H
@@ -155,6 +157,36 @@ int el_metrics_compute(int n_layers, int n_iters, const int32_t* it_output_layer
                        int n_seqs, const int32_t* sq_id, const int32_t* sq_tok_off, const int32_t* sq_exit_layers,
                        const double* sq_first, const double* sq_finish, const double* meta, el_metrics* out,
                        int64_t* exit_hist, int64_t* accept_hist);
+
+/* ---- sub-engine API on the engine's device pool (outside a session or run; a run or a
+ * session resets the pool).  Vectors are fp32 host arrays of d_model values; K/V are stored
+ * in bf16 like every other device K/V row.  At most max_batch sequences live at a time
+ * (device block-table slots).
+ *   el_kv_allocate/append/view/commit/release  KvStore::allocate/append/view/commit/release
+ *                                              (kv_cache.hpp:45-75, kv_cache.cpp:78-194): the same
+ *                                              LIFO block order, write-once/contiguity/capacity
+ *                                              checks and error classes
+ *   el_kv_lengths / el_kv_stats                KvStore::committed_len/written_len/stats
+ *   el_layer_forward   layer_forward(weights, layer, batch, cache) (model.hpp:64-66, model.cpp:197-272):
+ *                      K/V appended at each sequence's committed length, attention over 0..pos
+ *   el_kv_fill         fill_skipped(cache, batch, output_layer, compute_kv_pair) (kv_cache.hpp:107-115,
+ *                      model.cpp:274-282): one grouped GEMM, K/V written into the paged blocks
+ *   el_exit_confidence the engine technique's *_confidence (exit_policy.hpp:46-70) of n states at
+ *                      `layer` and decide's strict '>' threshold_at(layer) (exit_policy.cpp:89-115)
+ *   el_greedy_tokens   greedy_token(lm_head_logits(h)) (model.hpp:71-76): lowest index on ties */
+int el_kv_allocate(el_engine* e, int seq_id, int capacity_tokens);
+int el_kv_release(el_engine* e, int seq_id);
+int el_kv_append(el_engine* e, int seq_id, int layer, int position, const float* k, const float* v);
+int el_kv_view(el_engine* e, int seq_id, int layer, int upto_position, float* k /* [upto][d] */, float* v);
+int el_kv_commit(el_engine* e, int seq_id);
+int el_kv_lengths(el_engine* e, int seq_id, int32_t* committed, int32_t* written /* [L] */);
+int el_kv_stats(el_engine* e, int32_t* out4 /* pool, free, peak in use, live sequences */);
+int el_layer_forward(el_engine* e, int layer, int n, const int32_t* seq_ids, const float* h_in /* [n][d] */,
+                     float* h_out /* [n][d] */);
+int el_kv_fill(el_engine* e, int n, const int32_t* seq_ids, const float* h_exit /* [n][d] */, int output_layer);
+int el_exit_confidence(el_engine* e, int layer, int n, const float* h_prev, const float* h_cur, float* conf /* [n] */,
+                       int32_t* accept /* [n] */);
+int el_greedy_tokens(el_engine* e, int n, const float* h /* [n][d] */, int32_t* tokens /* [n] */);
 
 /* LIFO allocator on the host mirror (same arithmetic the device kernels run) */
 int el_kv_block_trace(int n_layers, int pool_blocks, int block_capacity, int n_ops, const int32_t* ops,

@@ -165,8 +165,8 @@ struct el_engine {
     bool fuse_exit = true;
     bool fuse_exit_all = false;
     // decode-iteration strategy: 0 per-phase kernels (graph / eager), 1 persistent kernel
-    // (el_iter.cuh), 2 auto: persistent at batch >= 64 outside softmax exit (measured faster
-    // there: weight streaming and the exit check amortise its grid barriers), per-phase below
+    // (el_iter.cuh), 2 auto: persistent at batch >= 64 (measured faster there: weight streaming
+    // and the exit check amortise its grid barriers), per-phase below
     int use_mega = 2;
     bool mega_for(int B) const {
         if (cfg.encoder_len > 0) {  // T5 mode: the cross-attention sub-layer lives in the persistent kernel
@@ -174,7 +174,9 @@ struct el_engine {
             return true;
         }
         if (use_mega != 2) return use_mega == 1;
-        return B >= 64 && cfg.technique != EL_TECH_SOFTMAX;
+        // softmax included: at batch 128 the persistent kernel measured 1.85 ms vs 2.10 ms per
+        // iteration (c4m), at batch 8 the per-phase graph wins (c1: 0.163 vs 0.183 ms)
+        return B >= 64;
     }
     int dbg = 0;
     int rec_cap = 4096;
@@ -245,7 +247,7 @@ struct el_engine {
     int sess_B = 0;
     int sess_iters = 0;
     std::vector<int> sess_ids;
-    std::vector<int> slot_bpl;  // per slot blocks per layer (0 = free)
+    std::vector<int> slot_bpl;  // per slot blocks per layer (-1 = free; 0 = a zero-capacity sequence)
 
     ~el_engine() {
         for (auto& kv : graphs) {
@@ -440,10 +442,10 @@ struct el_engine {
         mbar.alloc(2048 + 32 * 1024);
         mtcnt.alloc(el::kINumGemm * 64);
         CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
-        slot_bpl.assign((size_t)dm.slots, 0);
+        slot_bpl.assign((size_t)dm.slots, -1);
         ensure_bpl(1);
         CK(cudaStreamSynchronize(stream));
-        slot_bpl.assign((size_t)dm.slots, 0);
+        slot_bpl.assign((size_t)dm.slots, -1);
     }
 
     void reset_allocator() {
@@ -453,14 +455,16 @@ struct el_engine {
         CK(cudaStreamSynchronize(stream));
         top = cfg.pool_blocks;
         peak = 0;
-        slot_bpl.assign((size_t)dm.slots, 0);
+        slot_bpl.assign((size_t)dm.slots, -1);
+        store.clear();
+        store_ready = false;
     }
 
     // tables / attention workspace sized for bpl blocks per (seq, layer)
     void ensure_bpl(int bpl) {
         if (bpl <= dm.bpl_max) return;
         for (int b : slot_bpl)
-            if (b) fail(EL_LOGIC_ERROR, "block tables cannot grow while sequences are live");
+            if (b >= 0) fail(EL_LOGIC_ERROR, "block tables cannot grow while sequences are live");
         dm.bpl_max = bpl;
         tables.alloc((size_t)dm.slots * dm.L * bpl);
         plan_attention();
@@ -862,7 +866,7 @@ struct el_engine {
     bool can_allocate(int capacity_tokens) const { return (long)bpl_for(capacity_tokens) * dm.L <= top; }
     int free_slot() const {
         for (int s = 0; s < dm.slots; ++s)
-            if (slot_bpl[(size_t)s] == 0) return s;
+            if (slot_bpl[(size_t)s] < 0) return s;
         fail(EL_RUNTIME_ERROR, "no free sequence slot");
     }
     int allocate(int capacity_tokens) {
@@ -881,7 +885,7 @@ struct el_engine {
         const int bpl = slot_bpl[(size_t)slot];
         el::launch_kv_release(stack.p, top, tables.p, dm, slot, bpl, stream);
         top += bpl * dm.L;
-        slot_bpl[(size_t)slot] = 0;
+        slot_bpl[(size_t)slot] = -1;
     }
 
     // ---- prefill of newly admitted sequences (engine.cpp:166-181), batched
@@ -1265,6 +1269,245 @@ struct el_engine {
         el::DevState s = state(true, B);
         el::launch_kv_prefix(s, seq_ids_dev.p, P, kv_seed, 1, stream);
         CK(cudaStreamSynchronize(stream));
+    }
+
+
+    // ------------------------------------------------------------------
+    // Sub-engine API on the device pool (outside a session / run): KvStore
+    // (kv_cache.hpp:45-115), layer_forward / compute_kv_pair + fill_skipped
+    // (model.hpp:64-76, kv_cache.hpp:107-115), the exit confidences + decide
+    // (exit_policy.hpp:46-70) and lm_head_logits + greedy_token (model.hpp:71-76).
+    // Sequences live in device slots (at most max_batch at a time); the host
+    // keeps the reference's invariant counters (written per layer, committed).
+    // ------------------------------------------------------------------
+    struct StoreSeq {
+        int slot = 0, capacity = 0, committed = 0, bpl = 0;
+        std::vector<int> written;  // per layer
+        std::vector<int> table;    // [L][bpl] block ids (device table mirror)
+    };
+    std::map<int, StoreSeq> store;
+    bool store_ready = false;
+    void store_begin() {
+        if (in_session) fail(EL_LOGIC_ERROR, "KvStore API: a decode session is active");
+        if (!store_ready) {
+            reset_allocator();
+            ensure_bpl(std::min(128, std::max(1, cfg.pool_blocks / dm.L)));
+            store_ready = true;
+        }
+    }
+    StoreSeq& store_entry(int id, const char* op) {
+        auto it = store.find(id);
+        if (it == store.end()) fail(EL_INVALID_ARGUMENT, "%s: unknown seq_id %d", op, id);
+        return it->second;
+    }
+    void store_allocate(int id, int capacity_tokens) {  // kv_cache.cpp:78-106
+        store_begin();
+        if (store.count(id)) fail(EL_INVALID_ARGUMENT, "allocate: seq_id %d already allocated", id);
+        if (capacity_tokens < 0) fail(EL_INVALID_ARGUMENT, "allocate: negative capacity");
+        const int bpl = bpl_for(capacity_tokens);
+        if ((long)bpl * dm.L > top) fail(EL_KV_OUT_OF_MEMORY, "allocate: need %ld blocks, %d free", (long)bpl * dm.L, top);
+        StoreSeq q;
+        q.slot = allocate(capacity_tokens);
+        q.capacity = bpl * dm.bc;
+        q.bpl = bpl;
+        q.written.assign((size_t)dm.L, 0);
+        q.table.assign((size_t)dm.L * bpl, 0);
+        for (int l = 0; l < dm.L && bpl > 0; ++l)
+            CK(cudaMemcpyAsync(q.table.data() + (size_t)l * bpl, tables.p + ((size_t)q.slot * dm.L + l) * dm.bpl_max,
+                               sizeof(int) * bpl, cudaMemcpyDeviceToHost, stream));
+        CK(cudaStreamSynchronize(stream));
+        store.emplace(id, std::move(q));
+    }
+    void store_release(int id) {  // kv_cache.cpp:182-194
+        auto it = store.find(id);
+        if (it == store.end()) fail(EL_INVALID_ARGUMENT, "release: unknown or already released seq_id %d", id);
+        release(it->second.slot);
+        store.erase(it);
+    }
+    // append-position checks of KvStore::append (kv_cache.cpp:108-145) for position `pos` at `layer`
+    void store_check_append(int id, const StoreSeq& q, int layer, int pos) const {
+        if (layer < 1 || layer > dm.L) fail(EL_INVALID_ARGUMENT, "append: layer %d outside [1, %d]", layer, dm.L);
+        const int w = q.written[(size_t)layer - 1];
+        if (pos < w) fail(EL_RUNTIME_ERROR, "append: slot already written at (seq %d, layer %d, position %d)", id, layer, pos);
+        if (pos > w)
+            fail(EL_RUNTIME_ERROR, "append: position gap at (seq %d, layer %d, position %d), next unwritten is %d", id,
+                 layer, pos, w);
+        if (pos >= q.capacity)
+            fail(EL_KV_OUT_OF_MEMORY, "append: position %d exceeds reserved capacity %d for seq %d", pos, q.capacity, id);
+    }
+    size_t store_row(const StoreSeq& q, int layer, int pos) const {
+        const int blk = q.table[(size_t)(layer - 1) * q.bpl + pos / dm.bc];
+        return ((size_t)blk * dm.bc + pos % dm.bc) * dm.dp;
+    }
+    void store_append(int id, int layer, int pos, const float* k, const float* v) {
+        StoreSeq& q = store_entry(id, "append");
+        store_check_append(id, q, layer, pos);
+        std::vector<uint16_t> kb((size_t)dm.dp, 0), vb((size_t)dm.dp, 0);
+        for (int i = 0; i < dm.d; ++i) {
+            kb[(size_t)i] = el::bf16_bits_rne((double)k[i]);
+            vb[(size_t)i] = el::bf16_bits_rne((double)v[i]);
+        }
+        const size_t r = store_row(q, layer, pos);
+        CK(cudaMemcpy(kpool.p + r, kb.data(), sizeof(uint16_t) * dm.dp, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(vpool.p + r, vb.data(), sizeof(uint16_t) * dm.dp, cudaMemcpyHostToDevice));
+        ++q.written[(size_t)layer - 1];
+    }
+    void store_view(int id, int layer, int upto, float* k, float* v) {  // kv_cache.cpp:147-163
+        StoreSeq& q = store_entry(id, "view");
+        if (layer < 1 || layer > dm.L) fail(EL_INVALID_ARGUMENT, "view: layer %d outside [1, %d]", layer, dm.L);
+        if (upto < 0) fail(EL_INVALID_ARGUMENT, "view: negative upto_position");
+        if (upto > q.written[(size_t)layer - 1])
+            fail(EL_RUNTIME_ERROR, "view: entries missing at (seq %d, layer %d): requested %d, written %d", id, layer,
+                 upto, q.written[(size_t)layer - 1]);
+        CK(cudaStreamSynchronize(stream));
+        std::vector<uint16_t> raw((size_t)dm.dp);
+        for (int p = 0; p < upto; ++p)
+            for (int which = 0; which < 2; ++which) {
+                CK(cudaMemcpy(raw.data(), (which ? vpool.p : kpool.p) + store_row(q, layer, p), sizeof(uint16_t) * dm.dp,
+                              cudaMemcpyDeviceToHost));
+                float* out = (which ? v : k) + (size_t)p * dm.d;
+                for (int i = 0; i < dm.d; ++i) {
+                    const uint32_t f = (uint32_t)raw[(size_t)i] << 16;
+                    std::memcpy(&out[i], &f, 4);
+                }
+            }
+    }
+    void store_commit(int id) {  // kv_cache.cpp:165-180
+        StoreSeq& q = store_entry(id, "commit");
+        for (int l = 1; l <= dm.L; ++l)
+            if (q.written[(size_t)l - 1] != q.committed + 1)
+                fail(EL_RUNTIME_ERROR, "commit: layer %d of seq %d has %d entries, expected %d", l, id,
+                     q.written[(size_t)l - 1], q.committed + 1);
+        ++q.committed;
+    }
+    // rows of a batch of store sequences: slot, position = committed length
+    void store_rows(int n, const int32_t* ids, std::vector<StoreSeq*>& qs) {
+        if (n < 1) fail(EL_LOGIC_ERROR, "decode_iteration: empty batch");
+        if (n > dm.Bmax) fail(EL_INVALID_ARGUMENT, "batch %d > max_batch %d", n, dm.Bmax);
+        std::vector<int> hs((size_t)n), hp((size_t)n);
+        qs.assign((size_t)n, nullptr);
+        for (int b = 0; b < n; ++b) {
+            for (int c = 0; c < b; ++c)
+                if (ids[c] == ids[b]) fail(EL_INVALID_ARGUMENT, "batch: seq_id %d appears twice", ids[b]);
+            qs[(size_t)b] = &store_entry(ids[b], "layer_forward");
+            hs[(size_t)b] = qs[(size_t)b]->slot;
+            hp[(size_t)b] = qs[(size_t)b]->committed;
+        }
+        CK(cudaMemcpyAsync(row_slot.p, hs.data(), sizeof(int) * n, cudaMemcpyHostToDevice, stream));
+        CK(cudaMemcpyAsync(row_pos.p, hp.data(), sizeof(int) * n, cudaMemcpyHostToDevice, stream));
+        CK(cudaStreamSynchronize(stream));
+    }
+    // host states [n][d] -> residual stream parity `par` (fp32) and its bf16 GEMM operand copy
+    void put_states(int n, const float* h, int par, bool f32, bool b16) {
+        const int dp = dm.dp, d = dm.d;
+        if (f32) {
+            std::vector<float> buf((size_t)n * dp, 0.f);
+            for (int b = 0; b < n; ++b) std::memcpy(buf.data() + (size_t)b * dp, h + (size_t)b * d, sizeof(float) * d);
+            CK(cudaMemcpy(h32.p + (size_t)par * dm.Bmax * dp, buf.data(), sizeof(float) * buf.size(),
+                          cudaMemcpyHostToDevice));
+        }
+        if (b16) {
+            std::vector<uint16_t> buf((size_t)NR * dp, 0);
+            for (int b = 0; b < n; ++b)
+                for (int i = 0; i < d; ++i) buf[el::act_offset(b, i, NR)] = el::bf16_bits_rne((double)h[(size_t)b * d + i]);
+            CK(cudaMemcpy(hb.p + (size_t)par * NR * dp, buf.data(), sizeof(uint16_t) * buf.size(),
+                          cudaMemcpyHostToDevice));
+        }
+    }
+    void set_dev_int(int* dst, int v) {
+        CK(cudaMemcpy(dst, &v, sizeof(int), cudaMemcpyHostToDevice));
+    }
+    el::DevState store_state(int n) {
+        el::DevState s = state(false, n);
+        s.cont_host = nullptr;
+        s.fuse_exit = 0;
+        s.use_cond = 0;
+        return s;
+    }
+    // layer_forward (model.cpp:197-272) for n store sequences at their committed positions
+    void layer_forward(int layer, int n, const int32_t* ids, const float* h_in, float* h_out) {
+        if (in_session) fail(EL_LOGIC_ERROR, "layer_forward: a decode session is active");
+        if (layer < 1 || layer > dm.L) fail(EL_INVALID_ARGUMENT, "layer_forward: layer %d outside [1, %d]", layer, dm.L);
+        std::vector<StoreSeq*> qs;
+        store_rows(n, ids, qs);
+        for (int b = 0; b < n; ++b) store_check_append(ids[b], *qs[(size_t)b], layer, qs[(size_t)b]->committed);
+        put_states(n, h_in, (layer - 1) & 1, true, true);
+        set_dev_int(layer_ptr(), layer);
+        Plans& P = plans_for(n);
+        el::DevState s = store_state(n);
+        s.technique = el::kNever;
+        el::launch_gemm(el::kGemmQkv, P.qkv, s, stream, false);
+        el::launch_attention(s, stream, false);
+        el::launch_gemm(el::kGemmWo, P.wo, s, stream, false);
+        el::launch_gemm(el::kGemmUp, P.up, s, stream, false);
+        el::launch_gemm(el::kGemmDown, P.down, s, stream, false);
+        CK(cudaStreamSynchronize(stream));
+        get_states(n, layer & 1, h_out);
+        for (int b = 0; b < n; ++b) ++qs[(size_t)b]->written[(size_t)layer - 1];
+    }
+    int* layer_ptr() { return layer.p; }
+    void get_states(int n, int par, float* out) {
+        const int dp = dm.dp, d = dm.d;
+        std::vector<float> buf((size_t)n * dp);
+        CK(cudaMemcpy(buf.data(), h32.p + (size_t)par * dm.Bmax * dp, sizeof(float) * buf.size(), cudaMemcpyDeviceToHost));
+        for (int b = 0; b < n; ++b) std::memcpy(out + (size_t)b * d, buf.data() + (size_t)b * dp, sizeof(float) * d);
+    }
+    // fill_skipped (kv_cache.cpp:222-234): K_j, V_j = W_k^(j) h_e, W_v^(j) h_e for j in (e, L]
+    void kv_fill(int n, const int32_t* ids, const float* h_exit, int e_out) {
+        if (in_session) fail(EL_LOGIC_ERROR, "fill_skipped: a decode session is active");
+        if (e_out < 1 || e_out > dm.L) fail(EL_INVALID_ARGUMENT, "fill_skipped: output_layer out of range");
+        std::vector<StoreSeq*> qs;
+        store_rows(n, ids, qs);
+        for (int b = 0; b < n; ++b)
+            for (int j = e_out + 1; j <= dm.L; ++j) store_check_append(ids[b], *qs[(size_t)b], j, qs[(size_t)b]->committed);
+        if (e_out == dm.L) return;  // no-op at the last layer (kv_cache.hpp:110-115)
+        put_states(n, h_exit, e_out & 1, false, true);
+        set_dev_int(out_layer.p, e_out);
+        Plans& P = plans_for(n);
+        el::DevState s = store_state(n);
+        el::launch_gemm(el::kGemmFill, P.fill, s, stream, false);
+        CK(cudaStreamSynchronize(stream));
+        for (int b = 0; b < n; ++b)
+            for (int j = e_out + 1; j <= dm.L; ++j) ++qs[(size_t)b]->written[(size_t)j - 1];
+    }
+    // the configured technique's confidence of n states at `layer` and decide's strict '>' against
+    // threshold_at(layer) (exit_policy.cpp:57-115); h_prev only for state similarity
+    void exit_confidence(int layer, int n, const float* h_prev, const float* h_cur, float* conf_out, int32_t* acc_out) {
+        if (in_session) fail(EL_LOGIC_ERROR, "exit_confidence: a decode session is active");
+        if (layer < 1 || layer > dm.L) fail(EL_INVALID_ARGUMENT, "exit_confidence: layer %d outside [1, %d]", layer, dm.L);
+        if (n < 1 || n > dm.Bmax) fail(EL_INVALID_ARGUMENT, "exit_confidence: batch %d outside [1, %d]", n, dm.Bmax);
+        if (cfg.technique == EL_TECH_STATE && !h_prev) fail(EL_INVALID_ARGUMENT, "state_similarity needs h_prev");
+        if (cfg.technique == EL_TECH_FIXED) fail(EL_INVALID_ARGUMENT, "exit_confidence: technique fixed has no evidence");
+        if (cfg.technique == EL_TECH_STATE) put_states(n, h_prev, (layer - 1) & 1, true, false);
+        put_states(n, h_cur, layer & 1, true, cfg.technique == EL_TECH_SOFTMAX);
+        set_dev_int(layer_ptr(), layer);
+        set_dev_int(exit_cnt.p, 0);
+        CK(cudaMemset(status.p, 0, sizeof(int) * dm.Bmax));
+        el::DevState s = store_state(n);
+        if (cfg.technique == EL_TECH_SOFTMAX) el::launch_gemm(el::kGemmLmCheck, plans_for(n).lm, s, stream, false);
+        el::launch_exit(s, stream, false);
+        CK(cudaStreamSynchronize(stream));
+        std::vector<float> cf((size_t)n);
+        std::vector<int> ac((size_t)n);
+        CK(cudaMemcpy(cf.data(), conf.p + (size_t)(layer - 1) * dm.Bmax, sizeof(float) * n, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(ac.data(), accept.p, sizeof(int) * n, cudaMemcpyDeviceToHost));
+        if (conf_out) std::memcpy(conf_out, cf.data(), sizeof(float) * n);
+        if (acc_out) for (int b = 0; b < n; ++b) acc_out[b] = ac[(size_t)b];
+    }
+    // lm_head_logits + greedy_token (model.cpp:284-299): argmax over the vocabulary, lowest index on ties
+    void greedy_tokens(int n, const float* h, int32_t* tokens) {
+        if (in_session) fail(EL_LOGIC_ERROR, "greedy_token: a decode session is active");
+        if (n < 1 || n > dm.Bmax) fail(EL_INVALID_ARGUMENT, "greedy_token: batch %d outside [1, %d]", n, dm.Bmax);
+        const int par = dm.L & 1;
+        put_states(n, h, par, false, true);
+        set_dev_int(out_layer.p, dm.L);
+        std::vector<int> zeros((size_t)n, 0);
+        CK(cudaMemcpy(row_pos.p, zeros.data(), sizeof(int) * n, cudaMemcpyHostToDevice));
+        el::DevState s = store_state(n);
+        el::launch_gemm(el::kGemmLmFinal, plans_for(n).lm, s, stream, false);
+        el::launch_finish(s, stream, false);
+        CK(cudaStreamSynchronize(stream));
+        CK(cudaMemcpy(tokens, row_tok.p, sizeof(int) * n, cudaMemcpyDeviceToHost));
     }
 
     // ------------------------------------------------------------------
@@ -1873,6 +2116,71 @@ int el_transcript_metrics(const el_transcript* t, el_metrics* out, int64_t* exit
     return el_metrics_compute(t->L, (int)t->it_output_layer.size(), t->it_output_layer.data(), t->it_batch_off.data(),
                               (int)t->sq_id.size(), t->sq_id.data(), t->sq_tok_off.data(), t->sq_exit_layers.data(),
                               t->sq_first.data(), t->sq_finish.data(), t->meta.data(), out, exit_hist, accept_hist);
+}
+
+
+// ---- sub-engine API (KvStore / layer_forward / fill_skipped / confidences / greedy) ----
+int el_kv_allocate(el_engine* e, int seq_id, int capacity_tokens) {
+    API_BEGIN
+    e->store_allocate(seq_id, capacity_tokens);
+    API_END
+}
+int el_kv_release(el_engine* e, int seq_id) {
+    API_BEGIN
+    e->store_release(seq_id);
+    API_END
+}
+int el_kv_append(el_engine* e, int seq_id, int layer, int position, const float* k, const float* v) {
+    API_BEGIN
+    if (!k || !v) fail(EL_INVALID_ARGUMENT, "append: null K/V");
+    e->store_append(seq_id, layer, position, k, v);
+    API_END
+}
+int el_kv_view(el_engine* e, int seq_id, int layer, int upto_position, float* k, float* v) {
+    API_BEGIN
+    e->store_view(seq_id, layer, upto_position, k, v);
+    API_END
+}
+int el_kv_commit(el_engine* e, int seq_id) {
+    API_BEGIN
+    e->store_commit(seq_id);
+    API_END
+}
+int el_kv_lengths(el_engine* e, int seq_id, int32_t* committed, int32_t* written) {
+    API_BEGIN
+    auto& q = e->store_entry(seq_id, "committed_len");
+    if (committed) *committed = q.committed;
+    if (written) for (int l = 0; l < e->dm.L; ++l) written[l] = q.written[(size_t)l];
+    API_END
+}
+int el_kv_stats(el_engine* e, int32_t* out4) {
+    API_BEGIN
+    out4[0] = e->cfg.pool_blocks;
+    out4[1] = e->top;
+    out4[2] = e->peak;
+    out4[3] = (int32_t)e->store.size();
+    API_END
+}
+int el_layer_forward(el_engine* e, int layer, int n, const int32_t* seq_ids, const float* h_in, float* h_out) {
+    API_BEGIN
+    e->layer_forward(layer, n, seq_ids, h_in, h_out);
+    API_END
+}
+int el_kv_fill(el_engine* e, int n, const int32_t* seq_ids, const float* h_exit, int output_layer) {
+    API_BEGIN
+    e->kv_fill(n, seq_ids, h_exit, output_layer);
+    API_END
+}
+int el_exit_confidence(el_engine* e, int layer, int n, const float* h_prev, const float* h_cur, float* conf,
+                       int32_t* accept) {
+    API_BEGIN
+    e->exit_confidence(layer, n, h_prev, h_cur, conf, accept);
+    API_END
+}
+int el_greedy_tokens(el_engine* e, int n, const float* h, int32_t* tokens) {
+    API_BEGIN
+    e->greedy_tokens(n, h, tokens);
+    API_END
 }
 
 int el_model_tensor(el_engine* e, int which, int layer, uint16_t* out, int64_t cap) {

@@ -85,6 +85,17 @@ def lib():
         L.el_device_count.argtypes = [C.c_void_p]
         L.el_transcript_metrics.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
         L.el_metrics_compute.argtypes = [C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_int] + [C.c_void_p] * 9
+        L.el_kv_allocate.argtypes = [C.c_void_p, C.c_int, C.c_int]
+        L.el_kv_release.argtypes = [C.c_void_p, C.c_int]
+        L.el_kv_append.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p]
+        L.el_kv_view.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p]
+        L.el_kv_commit.argtypes = [C.c_void_p, C.c_int]
+        L.el_kv_lengths.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p]
+        L.el_kv_stats.argtypes = [C.c_void_p, C.c_void_p]
+        L.el_layer_forward.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p]
+        L.el_kv_fill.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_int]
+        L.el_exit_confidence.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+        L.el_greedy_tokens.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p]
         _lib = L
     return _lib
 
@@ -731,6 +742,10 @@ class Engine:
                  "mega_stages", "mega_stages2", "mega_att_stages", "mega"]
         return dict(zip(names, out[:n].tolist()))
 
+    def kv_store(self) -> "KvStore":
+        """the device pool as a KvStore (sub-engine API; reset by run() / session_begin())"""
+        return KvStore(self)
+
     def model_tensor(self, which, layer=0):
         names = {"embedding": 0, "lm_head": 1, "probe_w": 2, "probe_b": 3, "w_q": 4, "w_k": 5, "w_v": 6,
                  "w_o": 7, "w_up": 8, "w_down": 9}
@@ -767,3 +782,100 @@ def kv_block_trace(n_layers, pool, cap, ops, caps, n_ids, bpl_max):
     if nf < 0:
         _check(-nf)
     return tab, nf
+
+
+# ---------------------------------------------------------------- sub-engine API (device pool)
+def _f32(a, shape=None):
+    a = np.ascontiguousarray(a, dtype=np.float32)
+    return a if shape is None else a.reshape(shape)
+
+
+class KvStore:
+    """KvStore (kv_cache.hpp:45-75) on an Engine's device pool: the same LIFO block order,
+    write-once / contiguity / capacity / commit-completeness checks and exception classes
+    (ValueError = std::invalid_argument, RuntimeError = std::runtime_error, KvOutOfMemory).
+    Values are stored in bf16 (the engine's K/V precision)."""
+
+    def __init__(self, engine: "Engine"):
+        self.e = engine
+
+    def allocate(self, seq_id, capacity_tokens):
+        _check(lib().el_kv_allocate(self.e._h, int(seq_id), int(capacity_tokens)))
+
+    def append(self, seq_id, layer, position, k, v):
+        d = self.e.d
+        _check(lib().el_kv_append(self.e._h, int(seq_id), int(layer), int(position), _ptr(_f32(k, (d,))),
+                                  _ptr(_f32(v, (d,)))))
+
+    def view(self, seq_id, layer, upto_position):
+        d = self.e.d
+        k = np.zeros((max(int(upto_position), 0), d), np.float32)
+        v = np.zeros_like(k)
+        _check(lib().el_kv_view(self.e._h, int(seq_id), int(layer), int(upto_position), _ptr(k), _ptr(v)))
+        return k, v
+
+    def commit(self, seq_id):
+        _check(lib().el_kv_commit(self.e._h, int(seq_id)))
+
+    def release(self, seq_id):
+        _check(lib().el_kv_release(self.e._h, int(seq_id)))
+
+    def committed_len(self, seq_id):
+        c = np.zeros(1, np.int32)
+        _check(lib().el_kv_lengths(self.e._h, int(seq_id), _ptr(c), None))
+        return int(c[0])
+
+    def written_len(self, seq_id, layer):
+        w = np.zeros(self.e.L, np.int32)
+        _check(lib().el_kv_lengths(self.e._h, int(seq_id), None, _ptr(w)))
+        if not 1 <= layer <= self.e.L:
+            raise ValueError("written_len: layer out of range")
+        return int(w[layer - 1])
+
+    def stats(self):
+        o = np.zeros(4, np.int32)
+        _check(lib().el_kv_stats(self.e._h, _ptr(o)))
+        return {"pool_blocks": int(o[0]), "free_blocks": int(o[1]), "peak_blocks_in_use": int(o[2]),
+                "sequences": int(o[3])}
+
+
+def _batch(batch, d):
+    ids = np.ascontiguousarray([int(s) for s, _ in batch], dtype=np.int32)
+    h = _f32(np.stack([np.asarray(x, np.float32).reshape(d) for _, x in batch]))
+    return ids, h
+
+
+def layer_forward(engine: "Engine", layer, batch):
+    """layer_forward(weights, layer, batch, cache) (model.hpp:64-66) on the device: batch =
+    [(seq_id, h)], K/V appended to engine.kv_store() at each sequence's committed length."""
+    ids, h = _batch(batch, engine.d)
+    out = np.zeros_like(h)
+    _check(lib().el_layer_forward(engine._h, int(layer), len(ids), _ptr(ids), _ptr(h), _ptr(out)))
+    return [out[i] for i in range(len(ids))]
+
+
+def fill_skipped(engine: "Engine", batch, output_layer):
+    """fill_skipped(cache, batch, output_layer, compute_kv_pair) (kv_cache.hpp:107-115): K/V of the
+    layers after output_layer projected from each exit state, one grouped GEMM on the device."""
+    ids, h = _batch(batch, engine.d)
+    _check(lib().el_kv_fill(engine._h, len(ids), _ptr(ids), _ptr(h), int(output_layer)))
+
+
+def exit_confidence(engine: "Engine", layer, h_cur, h_prev=None):
+    """The engine technique's confidence (exit_policy.hpp:46-70) for states h_cur [n][d] (h_prev for
+    state similarity) and decide's strict '>' against threshold_at(layer); returns (conf, accept)."""
+    hc = _f32(np.atleast_2d(h_cur))
+    hp = None if h_prev is None else _f32(np.atleast_2d(h_prev))
+    n = hc.shape[0]
+    conf = np.zeros(n, np.float32)
+    acc = np.zeros(n, np.int32)
+    _check(lib().el_exit_confidence(engine._h, int(layer), n, _ptr(hp), _ptr(hc), _ptr(conf), _ptr(acc)))
+    return conf, acc.astype(bool)
+
+
+def greedy_tokens(engine: "Engine", h):
+    """greedy_token(lm_head_logits(h)) (model.hpp:71-76) for states h [n][d]."""
+    hh = _f32(np.atleast_2d(h))
+    out = np.zeros(hh.shape[0], np.int32)
+    _check(lib().el_greedy_tokens(engine._h, hh.shape[0], _ptr(hh), _ptr(out)))
+    return out
