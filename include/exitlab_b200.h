@@ -188,6 +188,23 @@ int el_exit_confidence(el_engine* e, int layer, int n, const float* h_prev, cons
                        int32_t* accept /* [n] */);
 int el_greedy_tokens(el_engine* e, int n, const float* h /* [n][d] */, int32_t* tokens /* [n] */);
 
+/* ---- layer-level scheduling (the occupancy MDP of layer_sched.hpp:13-60
+ * driving real batches) over the current session's batch.  A turn runs ONE layer for every
+ * sequence whose next layer it is (one persistent-kernel launch); each sequence exits on its own
+ * accept (no batch barrier) -- per sequence exactly decode_iteration for a batch of one --,
+ * fills its skipped layers' K/V, emits its token and restarts at layer 1.
+ *   policy 0 greedy: argmax_a v[a], ties toward the lowest layer (greedy_action, layer_sched.cpp:95-105)
+ *   policy 1 linear: argmax_a M[a].v (LinearQ::predict / TrainedPolicy::action, layer_sched.cpp:189-199,
+ *            311-325), lin_m = M [L][L] row-major; greedy when the chosen layer is empty
+ * el_sched_run runs n turns (one host round trip per turn: the next turn's rows depend on this
+ * one's exits) and returns their elapsed time (CUDA events on the engine stream). */
+int el_sched_begin(el_engine* e, int policy, const double* lin_m);
+int el_sched_run(el_engine* e, int n_turns, float* ms);
+/* tokens and exit layers of a row so far (returns the count; fills up to cap) */
+int el_sched_tokens(el_engine* e, int row, int32_t* tokens, int32_t* exit_layers, int cap);
+/* the layer and row count of every turn so far (returns the count) */
+int el_sched_turns(el_engine* e, int32_t* layers, int32_t* rows, int cap);
+
 /* LIFO allocator on the host mirror (same arithmetic the device kernels run) */
 int el_kv_block_trace(int n_layers, int pool_blocks, int block_capacity, int n_ops, const int32_t* ops,
                       const int32_t* caps, int n_ids, int bpl_max, int32_t* tables);

@@ -447,6 +447,11 @@ class Session:
             raise RuntimeError(lib.err())
         return dict(output_layer=e, tokens=toks, accept=acc, conf=conf, h_exit=hx)
 
+    def set_per_seq_exit(self, on=True):
+        """layer-level scheduling semantics: each row exits at its own first accept (C port only)"""
+        if self.m.lib.fn("session_set_per_seq_exit")(self.h, int(on)):
+            raise ValueError(self.m.lib.err())
+
     # layer-stepped iteration (reference only): a batch sharded over processes keeps the
     # reference's batch-wide exit barrier (oracle/ref_capi.cpp ref_session_iter_*)
     def iter_begin(self, tokens_in=None):

@@ -1204,6 +1204,10 @@ struct fast_session {
     /* current task arguments */
     const double* w; int rows, cols; const double* x; double* y; int layer; int rc;
     uint64_t kv_seed;
+    /* layer-level scheduling semantics: every row exits at its OWN first
+       accept -- B independent decode_iterations of one sequence each */
+    int per_seq;
+    unsigned char* active; /* [B] rows still running layers this step */
 };
 
 static int fs_threads(void) {
@@ -1302,6 +1306,7 @@ static void fs_attn_task(fast_session* s, int lo, int hi, int tid) {
     double* probs = scores + s->cap;
     double* rb = probs + s->cap; /* 4 rows of d */
     for (int b = lo; b < hi; ++b) {
+        if (s->per_seq && !s->active[b]) continue;
         const int pos = s->committed[b];
         int rc = fs_append(s, b, layer, pos, s->k + (size_t)b * d, s->v + (size_t)b * d);
         if (rc) { s->rc = rc; return; }
@@ -1425,6 +1430,7 @@ static fast_session* fast_session_create(const eo_model* m, const eo_engine_conf
     s->logits = (double*)malloc(sizeof(double) * (size_t)B * m->V);
     s->tstride = 2 * s->cap + 4 * d;
     s->tscratch = (double*)malloc(sizeof(double) * (size_t)s->tstride * s->nthreads);
+    s->active = (unsigned char*)calloc((size_t)B, 1);
     return s;
 }
 
@@ -1433,7 +1439,7 @@ static void fast_session_free(fast_session* s) {
     free(s->ids); free(s->next_input); free(s->committed); free(s->written);
     free(s->pk16); free(s->pv16); free(s->pk64); free(s->pv64); free(s->tk); free(s->tv);
     free(s->states); free(s->next); free(s->q); free(s->k); free(s->v); free(s->att); free(s->mid); free(s->down);
-    free(s->up); free(s->xT); free(s->logits); free(s->tscratch);
+    free(s->up); free(s->xT); free(s->logits); free(s->tscratch); free(s->active);
     free(s);
 }
 
@@ -1442,6 +1448,40 @@ static void fs_conf_task(fast_session* s, int lo, int hi, int tid) {
     (void)tid;
     for (int b = lo; b < hi; ++b)
         s->down[b] = eo_softmax_response_confidence(s->logits + (size_t)b * s->m->V, s->m->V);
+}
+
+/* layer loop with per-row exits: rows run layers until their own first accept (or L); a row's
+   state freezes at its exit layer (s->states), fa[b] = its exit layer */
+static int fs_per_seq_layers(fast_session* s, const double* fixed_conf, double* conf, int* fa) {
+    const eo_model* m = s->m;
+    const eo_engine_config* c = &s->cfg;
+    const int L = c->n_layers, d = c->d_model, B = s->B, V = m->V;
+    int n_active = B;
+    for (int b = 0; b < B; ++b) s->active[b] = 1;
+    for (int layer = 1; layer <= L && n_active > 0; ++layer) {
+        int rc = fs_layer(s, layer);
+        if (rc) return rc;
+        const double lambda = eo_threshold_at(c->lambda0, c->gamma, c->lambda_min, layer);
+        if (c->technique == EO_TECH_SOFTMAX) {
+            fs_mm(s, m->lm, V, d, s->next, s->logits);
+            fs_parallel(s, B, fs_conf_task);
+        }
+        for (int b = 0; b < B; ++b) {
+            if (!s->active[b]) continue;
+            double cf;
+            if (c->technique == EO_TECH_FIXED) cf = fixed_conf[(size_t)(layer - 1) * B + b];
+            else if (c->technique == EO_TECH_SOFTMAX) cf = s->down[b];
+            else cf = confidence(m, c, s->states + (size_t)b * d, s->next + (size_t)b * d, NULL);
+            if (conf) conf[(size_t)(layer - 1) * B + b] = cf;
+            memcpy(s->states + (size_t)b * d, s->next + (size_t)b * d, sizeof(double) * (size_t)d);
+            if (decide(c, layer, cf, lambda) || layer == L) {
+                fa[b] = layer;
+                s->active[b] = 0;
+                --n_active;
+            }
+        }
+    }
+    return EO_OK;
 }
 
 /* decode_iteration (engine.cpp:208-310) -- same contract as slow_session_step */
@@ -1460,6 +1500,7 @@ static int fast_session_step(fast_session* s, int forced, const double* fixed_co
     double* cf_b = (double*)malloc(sizeof(double) * (size_t)B);
     if (conf) for (int i = 0; i < L * B; ++i) conf[i] = NAN;
     int output_layer = L, rc = EO_OK;
+    if (s->per_seq) { rc = fs_per_seq_layers(s, fixed_conf, conf, fa); if (rc) goto done; goto tail; }
     for (int layer = 1; layer <= L; ++layer) {
         rc = fs_layer(s, layer);
         if (rc) goto done;
@@ -1485,6 +1526,25 @@ static int fast_session_step(fast_session* s, int forced, const double* fixed_co
         else if (all) { output_layer = layer; break; }
     }
     /* fill_skipped (kv_cache.cpp:222-234): K_j, V_j = W_k^(j) h_e, W_v^(j) h_e */
+    if (0) {
+    tail:
+        /* per-row exits: each row's skipped layers from its own exit state */
+        output_layer = 0;
+        for (int b = 0; b < B; ++b) if (fa[b] > output_layer) output_layer = fa[b];
+        for (int layer = 2; layer <= L; ++layer) {
+            int need = 0;
+            for (int b = 0; b < B; ++b) need |= fa[b] < layer;
+            if (!need) continue;
+            fs_mm(s, layer_tensor(m, layer, 1), d, d, s->states, s->k);
+            fs_mm(s, layer_tensor(m, layer, 2), d, d, s->states, s->v);
+            for (int b = 0; b < B; ++b)
+                if (fa[b] < layer) {
+                    rc = fs_append(s, b, layer, s->committed[b], s->k + (size_t)b * d, s->v + (size_t)b * d);
+                    if (rc) goto done;
+                }
+        }
+        goto commit;
+    }
     for (int layer = output_layer + 1; layer <= L; ++layer) {
         fs_mm(s, layer_tensor(m, layer, 1), d, d, s->states, s->k);
         fs_mm(s, layer_tensor(m, layer, 2), d, d, s->states, s->v);
@@ -1493,6 +1553,7 @@ static int fast_session_step(fast_session* s, int forced, const double* fixed_co
             if (rc) goto done;
         }
     }
+commit:
     /* KvStore::commit (kv_cache.cpp:165-180) */
     for (int b = 0; b < B; ++b) {
         for (int l = 0; l < L; ++l)
@@ -1554,6 +1615,11 @@ int eo_session_step(eo_session* s, int forced, const double* fixed_conf, const i
                     int32_t* accept, double* conf, double* h_exit) {
     return s->fast ? fast_session_step(s->fast, forced, fixed_conf, tokens_in, tokens, accept, conf, h_exit)
                    : slow_session_step(s->slow, forced, fixed_conf, tokens_in, tokens, accept, conf, h_exit);
+}
+int eo_session_set_per_seq_exit(eo_session* s, int on) {
+    if (!s->fast) { set_err("per-sequence exits: decoder-only sessions only"); return EO_INVALID_ARGUMENT; }
+    s->fast->per_seq = on != 0;
+    return EO_OK;
 }
 int eo_session_kv(const eo_session* s, int row, int layer, int pos, double* k, double* v) {
     return s->fast ? fast_session_kv(s->fast, row, layer, pos, k, v) : slow_session_kv(s->slow, row, layer, pos, k, v);

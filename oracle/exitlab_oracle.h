@@ -166,6 +166,9 @@ void eo_session_free(eo_session* s);
 int eo_session_step(eo_session* s, int forced_output_layer, const double* fixed_conf,
                     const int32_t* tokens_in, int32_t* tokens, int32_t* accept, double* conf,
                     double* h_exit);
+/* layer-level scheduling semantics: every row exits at its own first accept (B independent
+ * single-sequence decode iterations) */
+int eo_session_set_per_seq_exit(eo_session* s, int on);
 /* copy K/V at (row, layer, position) */
 int eo_session_kv(const eo_session* s, int row, int layer, int position, double* k, double* v);
 

@@ -745,6 +745,9 @@ struct el_engine {
         s.enc_blocks = enc_blocks;
         s.wqc = wqc.p; s.wkvc = wkvc.p; s.woc = woc.p;
         s.ckpool = ckpool.p; s.cvpool = cvpool.p; s.ctables = ctables.p;
+        s.turn_layer = 0;
+        s.hstore = hstore.p;
+        s.row_seq = row_seq.p;
         return s;
     }
 
@@ -1510,6 +1513,119 @@ struct el_engine {
         CK(cudaMemcpy(tokens, row_tok.p, sizeof(int) * n, cudaMemcpyDeviceToHost));
     }
 
+
+    // ------------------------------------------------------------------
+    // Layer-level scheduling (the occupancy MDP of layer_sched.hpp:13-60
+    // driving real batches -- f4).  Each sequence of the session has its own next layer; a
+    // TURN runs one layer for every sequence whose next layer it is (one persistent-kernel
+    // launch in turn mode), each of them exiting on its own accept (no batch-wide barrier):
+    // an exiting sequence fills its skipped layers' K/V from its exit state, emits its token
+    // and restarts at layer 1; the others carry their state to the next layer.  Per sequence
+    // the arithmetic is exactly the reference's decode_iteration for a batch of one.  The
+    // policy picks the turn's layer from the occupancy vector v (v[i] = sequences whose next
+    // layer is i+1): greedy = argmax v, ties toward the lowest layer (greedy_action,
+    // layer_sched.cpp:95-105), or linear = argmax_a M[a].v (LinearQ / TrainedPolicy::action,
+    // layer_sched.cpp:189-199, 311-325), falling back to greedy when that layer is empty.
+    // ------------------------------------------------------------------
+    struct Sched {
+        bool on = false;
+        int policy = 0;
+        std::vector<double> M;  // [L][L] (linear policy)
+        std::vector<int> next, pos, tok;
+        std::vector<std::vector<int>> toks, exits;
+        std::vector<int> turn_layer, turn_n;
+    } sch;
+    DevBuf<float> hstore;
+    DevBuf<int> row_seq;
+    void sched_begin(int policy, const double* M) {
+        need_session();
+        if (cfg.encoder_len > 0) fail(EL_INVALID_ARGUMENT, "layer-level scheduling: T5 mode not supported");
+        if (policy < 0 || policy > 1) fail(EL_INVALID_ARGUMENT, "layer-level scheduling: policy 0 (greedy) or 1 (linear)");
+        if (policy == 1 && !M) fail(EL_INVALID_ARGUMENT, "linear policy needs its L x L matrix");
+        const int B = sess_B, L = dm.L;
+        sch = Sched{};
+        sch.on = true;
+        sch.policy = policy;
+        if (M) sch.M.assign(M, M + (size_t)L * L);
+        sch.next.assign((size_t)B, 1);
+        sch.pos.assign((size_t)B, sess_prefix + sess_iters);
+        if (sess_iters != 0) fail(EL_LOGIC_ERROR, "layer-level scheduling must start on a fresh session");
+        sch.tok = sess_first;
+        sch.toks.assign((size_t)B, {});
+        sch.exits.assign((size_t)B, {});
+        if (hstore.n < (size_t)dm.Bmax * dm.dp) hstore.alloc((size_t)dm.Bmax * dm.dp);
+        if (row_seq.n < (size_t)dm.Bmax) row_seq.alloc((size_t)dm.Bmax);
+    }
+    int sched_pick(const std::vector<int>& v) const {
+        const int L = dm.L;
+        int best = 1;
+        for (int a = 2; a <= L; ++a)
+            if (v[(size_t)a - 1] > v[(size_t)best - 1]) best = a;
+        if (sch.policy == 1) {
+            auto pred = [&](int a) {
+                double acc = 0.0;
+                for (int i = 0; i < L; ++i) acc += sch.M[(size_t)(a - 1) * L + i] * v[(size_t)i];
+                return acc;
+            };
+            int lb = 1;
+            double bv = pred(1);
+            for (int a = 2; a <= L; ++a) {
+                const double x = pred(a);
+                if (x > bv) { lb = a; bv = x; }
+            }
+            if (v[(size_t)lb - 1] > 0) best = lb;
+        }
+        return best;
+    }
+    void sched_turn() {
+        const int B = sess_B, L = dm.L, Bm = dm.Bmax;
+        std::vector<int> v((size_t)L, 0);
+        for (int b = 0; b < B; ++b) ++v[(size_t)sch.next[(size_t)b] - 1];
+        const int a = sched_pick(v);
+        std::vector<int> rs, rp, rt, rq;
+        for (int b = 0; b < B; ++b)
+            if (sch.next[(size_t)b] == a) {
+                if (sch.pos[(size_t)b] >= sess_capacity)
+                    fail(EL_KV_OUT_OF_MEMORY, "append: position %d exceeds reserved capacity %d", sch.pos[(size_t)b],
+                         sess_capacity);
+                rs.push_back(sess_slots[(size_t)b]);
+                rp.push_back(sch.pos[(size_t)b]);
+                rt.push_back(sch.tok[(size_t)b]);
+                rq.push_back(b);
+            }
+        const int n = (int)rs.size();
+        CK(cudaMemcpyAsync(row_slot.p, rs.data(), sizeof(int) * n, cudaMemcpyHostToDevice, stream));
+        CK(cudaMemcpyAsync(row_pos.p, rp.data(), sizeof(int) * n, cudaMemcpyHostToDevice, stream));
+        CK(cudaMemcpyAsync(row_tok.p, rt.data(), sizeof(int) * n, cudaMemcpyHostToDevice, stream));
+        CK(cudaMemcpyAsync(row_seq.p, rq.data(), sizeof(int) * n, cudaMemcpyHostToDevice, stream));
+        el::IterPlan& P = mplan_for(n);
+        el::DevState s = state(false, n);
+        s.attn_stages = mega_att_stages;
+        s.attn_seg_cost = opt_attn_seg_cost >= 0 ? opt_attn_seg_cost : (n <= 64 ? 2 : 0);
+        s.turn_layer = a;
+        el::launch_iter(s, P, mmaps[P.map_key], mega_grid, stream);
+        const int cur = sess_iters % rec_cap;
+        CK(cudaMemcpyAsync(rec_host, rec.p + (size_t)cur * rec_stride, sizeof(int) * rec_stride, cudaMemcpyDeviceToHost,
+                           stream));
+        CK(cudaStreamSynchronize(stream));
+        ++sess_iters;
+        for (int r = 0; r < n; ++r) {
+            const int b = rq[(size_t)r];
+            const int ex = rec_host[Bm + r];
+            if (ex) {
+                sch.toks[(size_t)b].push_back(rec_host[r]);
+                sch.exits[(size_t)b].push_back(ex);
+                sch.tok[(size_t)b] = rec_host[r];
+                ++sch.pos[(size_t)b];
+                sch.next[(size_t)b] = 1;
+            } else {
+                ++sch.next[(size_t)b];
+            }
+        }
+        sch.turn_layer.push_back(a);
+        sch.turn_n.push_back(n);
+    }
+
     // ------------------------------------------------------------------
     // decode session: fixed batch over a seeded KV prefix (bench workload)
     // ------------------------------------------------------------------
@@ -1540,10 +1656,15 @@ struct el_engine {
         sess_ids = idv;
         sess_capacity = capacity;
         sess_prefix = prefix_len;
+        sess_slots = slots;
+        sess_first.assign(first, first + B);
+        sch = Sched{};
     }
     int sess_capacity = 0, sess_prefix = 0;
+    std::vector<int> sess_slots, sess_first;
     void session_end() {
         in_session = false;
+        sch = Sched{};
         reset_allocator();
     }
     void need_session() const {
@@ -2181,6 +2302,59 @@ int el_greedy_tokens(el_engine* e, int n, const float* h, int32_t* tokens) {
     API_BEGIN
     e->greedy_tokens(n, h, tokens);
     API_END
+}
+
+
+// ---- layer-level scheduling (f4) over a session's batch ----
+int el_sched_begin(el_engine* e, int policy, const double* lin_m) {
+    API_BEGIN
+    e->sched_begin(policy, lin_m);
+    API_END
+}
+int el_sched_run(el_engine* e, int n_turns, float* ms) {
+    API_BEGIN
+    if (!e->sch.on) fail(EL_LOGIC_ERROR, "layer-level scheduling not started (el_sched_begin)");
+    cudaEvent_t a, b;
+    CK(cudaEventCreate(&a));
+    CK(cudaEventCreate(&b));
+    CK(cudaStreamSynchronize(e->stream));
+    CK(cudaEventRecord(a, e->stream));
+    for (int i = 0; i < n_turns; ++i) e->sched_turn();
+    CK(cudaEventRecord(b, e->stream));
+    CK(cudaEventSynchronize(b));
+    float t = 0.f;
+    CK(cudaEventElapsedTime(&t, a, b));
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    if (ms) *ms = t;
+    API_END
+}
+int el_sched_tokens(el_engine* e, int row, int32_t* tokens, int32_t* exit_layers, int cap) {
+    // returns the count (>= 0) or -EL_* on error
+    if (!e->sch.on || row < 0 || row >= e->sess_B) {
+        g_err = "sched_tokens: layer-level scheduling not started or bad row";
+        return -EL_INVALID_ARGUMENT;
+    }
+    const auto& t = e->sch.toks[(size_t)row];
+    const auto& x = e->sch.exits[(size_t)row];
+    const int n = std::min(cap, (int)t.size());
+    for (int i = 0; i < n; ++i) {
+        if (tokens) tokens[i] = t[(size_t)i];
+        if (exit_layers) exit_layers[i] = x[(size_t)i];
+    }
+    return (int)t.size();
+}
+int el_sched_turns(el_engine* e, int32_t* layers, int32_t* rows, int cap) {
+    if (!e->sch.on) {
+        g_err = "layer-level scheduling not started";
+        return -EL_LOGIC_ERROR;
+    }
+    const int n = std::min(cap, (int)e->sch.turn_layer.size());
+    for (int i = 0; i < n; ++i) {
+        if (layers) layers[i] = e->sch.turn_layer[(size_t)i];
+        if (rows) rows[i] = e->sch.turn_n[(size_t)i];
+    }
+    return (int)e->sch.turn_layer.size();
 }
 
 int el_model_tensor(el_engine* e, int which, int layer, uint16_t* out, int64_t cap) {

@@ -1102,20 +1102,37 @@ __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(const __grid_cons
     }
     const AttnSrc self_src{st.tables, dm.bpl_max, st.kpool, st.vpool, 0, sm.att.pref, sm.pos, sm.slot, 0, nullptr, 0u};
     const AttnSrc cross_src{st.ctables, st.enc_blocks, st.ckpool, st.cvpool, st.enc_len, sm.att.pref_c, sm.pos, sm.slot, 1, nullptr, 0u};
-    // ---- embed (model.cpp:171-183): h_0 = embedding row of the input token ----
-    for (int b = cta; b < B; b += G) {
-        const uint16_t* e = st.emb + (size_t)st.rows.tok[b] * dp;
-        float* h = st.h32 + (size_t)b * dp;
-        for (int i = tid; i < dp; i += blockDim.x) {
-            const uint16_t v = e[i];
-            st.hb[act_offset(b, i, NR)] = v;
-            h[i] = bf16_to_f32(v);
+    // layers of this launch: 1..L (decode iteration / prefill), or the one layer of a turn
+    const int lfirst = st.turn_layer > 0 ? st.turn_layer : 1, llast = st.turn_layer > 0 ? st.turn_layer : L;
+    if (st.turn_layer > 1) {
+        // layer-level turn past layer 1: each row's state entering this layer, kept per sequence
+        const int pin = (lfirst - 1) & 1;
+        for (int b = cta; b < B; b += G) {
+            const float* src = st.hstore + (size_t)st.row_seq[b] * dp;
+            float* h = st.h32 + ((size_t)pin * Bm + b) * dp;
+            uint16_t* hbp = st.hb + (size_t)pin * NR * dp;
+            for (int i = tid; i < dp; i += blockDim.x) {
+                const float v = __ldcg(src + i);
+                h[i] = v;
+                hbp[act_offset(b, i, NR)] = f32_to_bf16(v);
+            }
+        }
+    } else {
+        // ---- embed (model.cpp:171-183): h_0 = embedding row of the input token ----
+        for (int b = cta; b < B; b += G) {
+            const uint16_t* e = st.emb + (size_t)st.rows.tok[b] * dp;
+            float* h = st.h32 + (size_t)b * dp;
+            for (int i = tid; i < dp; i += blockDim.x) {
+                const uint16_t v = e[i];
+                st.hb[act_offset(b, i, NR)] = v;
+                h[i] = bf16_to_f32(v);
+            }
         }
     }
     grid_sync(p, st, nbar, g0);
 
-    int e_out = L;
-    for (int layer = 1; layer <= L; ++layer) {
+    int e_out = llast;
+    for (int layer = lfirst; layer <= llast; ++layer) {
         const IterCtx x{layer, (layer - 1) & 1, layer & 1};
         // q | k | v, K/V appended to the paged pool (model.cpp:218-226)
         // this layer's first attention blocks (old positions: not written by this layer) into L2
@@ -1234,15 +1251,15 @@ __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(const __grid_cons
         // down + residual (model.cpp:261-270) + exit-check partial dots
         if (p.g[kIDown].mode) {
             gemm_phase_t<kIDown>(st, sm, ring, p, maps, kIDown, x, st.up_b, kseq2, wseq, useq, B, wpf,
-                                 layer < L ? (int)kIQkv : -1, layer + 1);
+                                 layer < llast ? (int)kIQkv : -1, layer + 1);
         } else if (!EL_DEBUG || p.fused_reduce) {  // (unfused split-K: probe builds only)
-            if (tid == kProducerWarp * 32 && layer < L) wpf = bm_prefetch(sm, ring, p, maps, kIQkv, layer + 1);
+            if (tid == kProducerWarp * 32 && layer < llast) wpf = bm_prefetch(sm, ring, p, maps, kIQkv, layer + 1);
             gemm_phase_fused<kIDown>(st, sm, ring, p, kIDown, x, st.up_b, kseq, useq, B, layer);
         } else {
             gemm_phase(st, sm, ring, p, p.g[kIDown], layer, st.up_b, kseq, useq, B);
             grid_sync(p, st, nbar, g0);
             if (EL_DEBUG && warp == kProducerWarp && layer < L && (p.pf_flags & 1)) l2_prefetch_gemm(p.g[kIQkv], layer + 1);
-            if (tid == kProducerWarp * 32 && layer < L) wpf = bm_prefetch(sm, ring, p, maps, kIQkv, layer + 1);
+            if (tid == kProducerWarp * 32 && layer < llast) wpf = bm_prefetch(sm, ring, p, maps, kIQkv, layer + 1);
             reduce_phase<kIDown>(st, sm, p, p.g[kIDown], x, B, 0, p.g[kIDown].m_tiles);
         }
         grid_sync(p, st, nbar, g0);
@@ -1275,7 +1292,7 @@ __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(const __grid_cons
             e_out = layer;
             // the next layer's QKV weights were prefetched for nothing: retire that load
             const IterGemm& gq = p.g[kIQkv];
-            if (layer < L && gq.mode && p.bm_prefetch && cta < gq.m_tiles * kBM / gq.nt * (p.bm_rows / p.bm_grp)) {
+            if (layer < llast && gq.mode && p.bm_prefetch && cta < gq.m_tiles * kBM / gq.nt * (p.bm_rows / p.bm_grp)) {
                 if (warp == 0) {  // the MMA warp retires it
                     mbar_wait(&sm.wfull, wseq & 1);
                     ++wseq;
@@ -1305,9 +1322,17 @@ __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(const __grid_cons
     // ---- tail: greedy LM head over h_e and the skipped-layer fill (kv_cache.cpp:222-234) ----
     const int pe = e_out & 1;
     const IterGemm& gf = p.g[kIFill];
-    const int n_lm = (st.technique == kSoftmax) ? 0 : p.lm_tiles;  // softmax: the last check's partials
+    // a layer-level turn decodes a token only for rows that exit here (own accept, or the last
+    // layer); every CTA holds the same decisions in sm.status, so this is grid-uniform
+    bool any_exit = true;
+    if (st.turn_layer > 0 && e_out < L) {
+        int a = 0;
+        for (int b = tid; b < B; b += blockDim.x) a |= sm.status[b];
+        any_exit = __syncthreads_or(a) != 0;
+    }
+    const int n_lm = (st.technique == kSoftmax || !any_exit) ? 0 : p.lm_tiles;  // softmax: the last check's partials
     const int m2 = 2 * dp / kBM;
-    const int fill_units = (L - e_out) * m2 * gf.splits;
+    const int fill_units = any_exit ? (L - e_out) * m2 * gf.splits : 0;
     {
         const uint16_t* bsrc = st.hb + (size_t)pe * NR * dp;
         for (int it = cta; it < n_lm + fill_units; it += G) {
@@ -1343,6 +1368,24 @@ __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(const __grid_cons
         const int lane = tid & 31;
         const int cur = iter % st.rec_cap;
         for (int b = cta + G * warp; b < B; b += G * 8) {
+            if (st.turn_layer > 0) {
+                // turn record: the token of a row that exits at this layer, -1 for a row that
+                // continues (its state goes to the per-sequence store for the next layer)
+                const bool ex = e_out == L || sm.status[b];
+                const LmPart r = ex ? lm_col_warp(st, b) : LmPart{0.f, 0.f, 0.f, -1};
+                if (!ex) {
+                    const float* src = st.h32 + ((size_t)(e_out & 1) * Bm + b) * dp;
+                    float* dst = st.hstore + (size_t)st.row_seq[b] * dp;
+                    for (int i = lane * 4; i < dp; i += 128)
+                        *reinterpret_cast<float4*>(dst + i) = __ldcg(reinterpret_cast<const float4*>(src + i));
+                }
+                if (lane == 0) {
+                    rec_rec(st, cur)[b] = r.idx;
+                    rec_rec(st, cur)[Bm + b] = ex ? e_out : 0;
+                    rec_conf(st, cur)[(size_t)(e_out - 1) * Bm + b] = __ldcg(&st.conf[(size_t)(e_out - 1) * Bm + b]);
+                }
+                continue;
+            }
             const LmPart r = lm_col_warp(st, b);
             for (int l = lane; l < L; l += 32)
                 rec_conf(st, cur)[(size_t)l * Bm + b] = __ldcg(&st.conf[(size_t)l * Bm + b]);

@@ -113,6 +113,13 @@ struct DevState {
     int rec_stride;
     int rec_cap;
     int prefill;  // persistent kernel in batched-prefill mode (rows = prompt positions; K/V only)
+    // layer-level scheduling (f4): > 0 = this launch is one TURN that runs only
+    // layer turn_layer for its rows (the sequences whose next layer it is); each row exits on its
+    // own accept (no batch barrier) and the hidden state of a row that continues is kept per
+    // sequence in hstore (row b is sequence row_seq[b])
+    int turn_layer;
+    float* hstore;        // [Bmax][dp] fp32 state entering each sequence's next layer
+    const int* row_seq;   // [Bmax] sequence index of each row of the turn
     // T5 mode (encoder_len > 0): cross-attention weights and the static encoder K/V
     int enc_len, enc_blocks;    // encoder states per sequence; KV blocks they occupy
     const uint16_t* wqc;        // [L][dp][dp]   tiled

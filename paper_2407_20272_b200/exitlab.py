@@ -96,6 +96,10 @@ def lib():
         L.el_kv_fill.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_int]
         L.el_exit_confidence.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
         L.el_greedy_tokens.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p]
+        L.el_sched_begin.argtypes = [C.c_void_p, C.c_int, C.c_void_p]
+        L.el_sched_run.argtypes = [C.c_void_p, C.c_int, C.POINTER(C.c_float)]
+        L.el_sched_tokens.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_int]
+        L.el_sched_turns.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int]
         _lib = L
     return _lib
 
@@ -741,6 +745,39 @@ class Engine:
                  "mega_up_splits", "mega_down_splits", "mega_fill_splits", "mega_qkv_nt", "mega_wo_nt", "mega_up_nt",
                  "mega_stages", "mega_stages2", "mega_att_stages", "mega"]
         return dict(zip(names, out[:n].tolist()))
+
+    # ---- layer-level scheduling over the session's batch ----
+    def sched_begin(self, policy="greedy", M=None):
+        """Switch the (fresh) session to layer-level scheduling: turns run one layer for the
+        sequences whose next layer it is, each exiting on its own accept.  policy "greedy"
+        (greedy_action) or "linear" (argmax_a M[a].v, LinearQ; M = L x L)."""
+        pol = {"greedy": 0, "linear": 1}[policy]
+        m = None if M is None else np.ascontiguousarray(M, dtype=np.float64).reshape(self.L, self.L)
+        _check(lib().el_sched_begin(self._h, pol, _ptr(m)))
+
+    def sched_run(self, n_turns):
+        """run n turns; returns their elapsed milliseconds (CUDA events, host round trips included)"""
+        ms = C.c_float()
+        _check(lib().el_sched_run(self._h, int(n_turns), C.byref(ms)))
+        return ms.value
+
+    def sched_tokens(self, row):
+        n = lib().el_sched_tokens(self._h, int(row), None, None, 0)
+        if n < 0:
+            _check(-n)
+        t = np.zeros(max(n, 1), np.int32)
+        x = np.zeros(max(n, 1), np.int32)
+        lib().el_sched_tokens(self._h, int(row), _ptr(t), _ptr(x), n)
+        return t[:n], x[:n]
+
+    def sched_turns(self):
+        n = lib().el_sched_turns(self._h, None, None, 0)
+        if n < 0:
+            _check(-n)
+        a = np.zeros(max(n, 1), np.int32)
+        r = np.zeros(max(n, 1), np.int32)
+        lib().el_sched_turns(self._h, _ptr(a), _ptr(r), n)
+        return a[:n], r[:n]
 
     def kv_store(self) -> "KvStore":
         """the device pool as a KvStore (sub-engine API; reset by run() / session_begin())"""
