@@ -372,6 +372,31 @@ def run_ours(args, rank, world, local_rank, dist, stub=False):
         for key in ("softmax", "state", "classifier"):
             c4[key]["speedup_vs_full_layer"] = round(c4[key]["value"] / c4["full_layer"]["value"], 3)
 
+    # 5. layer-level scheduling (f4): the same batch and inputs, turns of one
+    #    layer for the sequences at it, each sequence exiting on its own accept (no batch barrier);
+    #    timed over 4 * steps turns after 2 * L warm-up turns, host round trip per turn included
+    ll = None
+    if not enc and not stub and not args.no_layer_level:
+        warm_t, timed_t = 2 * L, 4 * args.steps
+        cap_ll = prefix + 1 + warm_t + timed_t + 1
+        eng = _engine(c, c["tech"], c["lam"], c["gamma"], B, cap_ll, args, rank, stub)
+        eng.session_begin(first, prefix, cap_ll, 1, ids)
+        eng.sched_begin("greedy")
+        eng.sched_run(warm_t)
+        c0 = [len(eng.sched_tokens(b)[0]) for b in range(B)]
+        barrier()
+        ms_ll = max_over_ranks(eng.sched_run(timed_t))
+        new_exits = np.concatenate([eng.sched_tokens(b)[1][c0[b]:] for b in range(B)])
+        tl, tr = eng.sched_turns()
+        eng.close()
+        ntok = len(new_exits)
+        ll = {"policy": "greedy (greedy_action, layer_sched.cpp:95-105)", "turns": timed_t,
+              "value": round(ntok * world / (ms_ll * 1e-3), 1), "unit": "tokens/s",
+              "ms_per_turn": round(ms_ll / timed_t, 4), "tokens": int(ntok),
+              "mean_layers_per_token": round(float(new_exits.mean()), 3) if ntok else None,
+              "mean_rows_per_turn": round(float(tr[warm_t:].mean()), 2),
+              "note": "one host round trip per turn (the next turn's rows depend on this turn's exits)"}
+
     if rank != 0:
         return None
     peak, peak_kind = load_peaks()
@@ -430,6 +455,9 @@ def run_ours(args, rank, world, local_rank, dist, stub=False):
     }
     if c4:
         out["c4"] = c4
+    if ll:
+        ll["speedup_vs_iteration_level"] = round(ll["value"] / value, 3)
+        out["layer_level"] = ll
     return out
 
 
@@ -597,6 +625,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-c4", action="store_true", help="skip the configs[3] comparison (c5 only)")
+    ap.add_argument("--no-layer-level", action="store_true", help="skip the layer-level scheduling leg")
     ap.add_argument("--ref-budget-s", type=float, default=150.0,
                     help="reference arm: bound on the timed CPU iterations (seconds)")
     ap.add_argument("--eager", action="store_true", help="host-driven layer loop (for ncu, which cannot "

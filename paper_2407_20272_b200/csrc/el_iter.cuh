@@ -951,6 +951,8 @@ __device__ __forceinline__ void gemm_phase_t(const DevState& st, IterSmem& sm, u
 // the tile each reduce their own 1/S of the columns (in split order: deterministic)
 // and apply the epilogue.  Replaces a grid barrier + a separate reduce phase by a
 // wait on the S - 1 peers of the tile.
+// `use`: 1-based count of this GEMM's phases in the launch (the tile counters only grow within
+// a launch and are zeroed at its end)
 template <int K>
 __device__ void gemm_phase_fused(const DevState& st, IterSmem& sm, uint8_t* ring, const IterPlan& p, int gid,
                                  const IterCtx& x, const uint16_t* bsrc, uint32_t& kseq, uint32_t& useq, int nval,
@@ -1142,7 +1144,7 @@ __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(const __grid_cons
             gemm_phase_t<kIQkv>(st, sm, ring, p, maps, kIQkv, x, st.hb + (size_t)x.pin * NR * dp, kseq2, wseq, useq, B,
                                 wpf, -1, 0);
         } else if (!EL_DEBUG || p.fused_reduce) {  // (unfused split-K: probe builds only)
-            gemm_phase_fused<kIQkv>(st, sm, ring, p, kIQkv, x, st.hb + (size_t)x.pin * NR * dp, kseq, useq, B, layer);
+            gemm_phase_fused<kIQkv>(st, sm, ring, p, kIQkv, x, st.hb + (size_t)x.pin * NR * dp, kseq, useq, B, layer - lfirst + 1);
         } else {
             gemm_phase(st, sm, ring, p, p.g[kIQkv], layer, st.hb + (size_t)x.pin * NR * dp, kseq, useq, B);
             grid_sync(p, st, nbar, g0);
@@ -1200,7 +1202,7 @@ __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(const __grid_cons
             gemm_phase_t<kIWo>(st, sm, ring, p, maps, kIWo, x, st.att_b, kseq2, wseq, useq, B, wpf,
                                st.enc_len > 0 ? (int)kIQc : (int)kIUp, layer);
         } else if (!EL_DEBUG || p.fused_reduce) {  // (unfused split-K: probe builds only)
-            gemm_phase_fused<kIWo>(st, sm, ring, p, kIWo, x, st.att_b, kseq, useq, B, layer);
+            gemm_phase_fused<kIWo>(st, sm, ring, p, kIWo, x, st.att_b, kseq, useq, B, layer - lfirst + 1);
         } else {
             gemm_phase(st, sm, ring, p, p.g[kIWo], layer, st.att_b, kseq, useq, B);
             grid_sync(p, st, nbar, g0);
@@ -1213,7 +1215,7 @@ __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(const __grid_cons
                 gemm_phase_t<kIQkv>(st, sm, ring, p, maps, kIQc, x, st.mid_b, kseq2, wseq, useq, B, wpf, -1,
                                     0);  // q_c -> q32
             } else if (!EL_DEBUG || p.fused_reduce) {  // (unfused split-K: probe builds only)
-                gemm_phase_fused<kIQkv>(st, sm, ring, p, kIQc, x, st.mid_b, kseq, useq, B, layer);
+                gemm_phase_fused<kIQkv>(st, sm, ring, p, kIQc, x, st.mid_b, kseq, useq, B, layer - lfirst + 1);
             } else {
                 gemm_phase(st, sm, ring, p, p.g[kIQc], layer, st.mid_b, kseq, useq, B);
                 grid_sync(p, st, nbar, g0);
@@ -1228,7 +1230,7 @@ __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(const __grid_cons
                 gemm_phase_t<kIWoc>(st, sm, ring, p, maps, kIWoc, x, st.att_b, kseq2, wseq, useq, B, wpf, kIUp,
                                     layer);
             } else if (!EL_DEBUG || p.fused_reduce) {  // (unfused split-K: probe builds only)
-                gemm_phase_fused<kIWoc>(st, sm, ring, p, kIWoc, x, st.att_b, kseq, useq, B, layer);
+                gemm_phase_fused<kIWoc>(st, sm, ring, p, kIWoc, x, st.att_b, kseq, useq, B, layer - lfirst + 1);
             } else {
                 gemm_phase(st, sm, ring, p, p.g[kIWoc], layer, st.att_b, kseq, useq, B);
                 grid_sync(p, st, nbar, g0);
@@ -1241,7 +1243,7 @@ __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(const __grid_cons
             gemm_phase_t<kIUp>(st, sm, ring, p, maps, kIUp, x, st.mid_b, kseq2, wseq, useq, B, wpf,
                                p.g[kIDown].mode ? (int)kIDown : -1, layer);
         } else if (!EL_DEBUG || p.fused_reduce) {  // (unfused split-K: probe builds only)
-            gemm_phase_fused<kIUp>(st, sm, ring, p, kIUp, x, st.mid_b, kseq, useq, B, layer);
+            gemm_phase_fused<kIUp>(st, sm, ring, p, kIUp, x, st.mid_b, kseq, useq, B, layer - lfirst + 1);
         } else {
             gemm_phase(st, sm, ring, p, p.g[kIUp], layer, st.mid_b, kseq, useq, B);
             grid_sync(p, st, nbar, g0);
@@ -1254,7 +1256,7 @@ __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(const __grid_cons
                                  layer < llast ? (int)kIQkv : -1, layer + 1);
         } else if (!EL_DEBUG || p.fused_reduce) {  // (unfused split-K: probe builds only)
             if (tid == kProducerWarp * 32 && layer < llast) wpf = bm_prefetch(sm, ring, p, maps, kIQkv, layer + 1);
-            gemm_phase_fused<kIDown>(st, sm, ring, p, kIDown, x, st.up_b, kseq, useq, B, layer);
+            gemm_phase_fused<kIDown>(st, sm, ring, p, kIDown, x, st.up_b, kseq, useq, B, layer - lfirst + 1);
         } else {
             gemm_phase(st, sm, ring, p, p.g[kIDown], layer, st.up_b, kseq, useq, B);
             grid_sync(p, st, nbar, g0);

@@ -38,7 +38,7 @@ def _run(port, L, d, V, B, tech, lam, gamma, turns, policy="greedy", M=None, pre
 
 @pytest.mark.parametrize("L,d,V,B,tech,lam,gamma", [(6, 256, 1024, 24, "state", 0.97, 0.998),
                                                    (12, 768, 32128, 64, "state", 0.981, 0.997),
-                                                   (8, 512, 4096, 40, "classifier", 0.45, 0.99)])
+                                                   (8, 512, 4096, 40, "classifier", 0.406, 0.999)])
 def test_layer_level_schedule_matches_single_sequence_decoding(port, L, d, V, B, tech, lam, gamma):
     e, first, got, layers, rows, cap = _run(port, L, d, V, B, tech, lam, gamma, turns=8 * L)
     # every turn engages exactly the sequences at its layer; the greedy layer is the most occupied
