@@ -16,7 +16,7 @@ CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libexitlab_b200.so")
 STAMP = LIB + ".flags"
 SOURCES = ["el_kernels.cu", "el_engine.cpp"]
-HEADERS = ["el_common.cuh", "el_kernels.h", "el_iter.cuh"]
+HEADERS = ["el_common.cuh", "el_kernels.h", "el_iter.cuh", "el_pipe.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 

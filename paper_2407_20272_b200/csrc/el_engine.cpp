@@ -14,6 +14,8 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -180,6 +182,13 @@ struct el_engine {
     }
     int dbg = 0;
     int rec_cap = 4096;
+    // pipelined iteration kernel (el_pipe.cuh) for batch 129..256: 0 off, 1 on, 2 auto (on outside
+    // softmax exit / T5 mode); attention CTAs of its grid (the rest run the projection GEMMs)
+    int use_pipe = 2, pipe_att = 92;
+    bool pipe_for(int B) const {
+        if (use_pipe == 0 || B <= 128 || B > 256 || cfg.encoder_len > 0 || cfg.technique == EL_TECH_SOFTMAX) return false;
+        return true;
+    }
 
     // weights
     DevBuf<uint16_t> wqkv, wo, wup, wdown, emb, lm;
@@ -439,6 +448,7 @@ struct el_engine {
 
         el::init_kernel_attributes();
         el::init_iter_attributes();
+        el::init_pipe_attributes();
         mbar.alloc(2048 + 32 * 1024);
         mtcnt.alloc(el::kINumGemm * 64);
         CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
@@ -565,16 +575,19 @@ struct el_engine {
     // split-K: aim at one unit per CTA (units = m_tiles * splits <= grid), >= 2 splits
     // cap (fewer splits: less partial traffic to reduce): 8, or 16 at batch >= 256 where the
     // mainloop of a unit dominates (measured c5 -1.6 %, c3 -0.5 %, c2 +1.3 % with 16)
-    int mega_splits(int m_tiles, int kb_total, int n_pad) const {
-        int s = std::max(1, mega_grid / m_tiles);
+    int mega_splits(int m_tiles, int kb_total, int n_pad, int grid = 0) const {
+        int s = std::max(1, (grid ? grid : mega_grid) / m_tiles);
         const int cap = opt_mega_splits_cap ? opt_mega_splits_cap : (n_pad >= 256 ? 16 : 8);
         s = std::min({s, kb_total, cap});
         return std::max(s, std::min(2, kb_total));
     }
-    el::IterPlan& mplan_for(int B, int nr_override = 0) {
+    // pipe_grid > 0: the plan of the pipelined kernel -- its GEMMs run on pipe_grid CTAs, one
+    // 128-row half of the batch at a time (batch-M units over one row group, split-K units sized
+    // for that CTA count)
+    el::IterPlan& mplan_for(int B, int nr_override = 0, int pipe_grid = 0) {
         const int n_pad = std::max(16, round_up(B, 16));
         const int NR = nr_override ? nr_override : this->NR;  // activation rows of the operand layout
-        const int key = n_pad + (nr_override ? 100000 : 0);
+        const int key = n_pad + (nr_override ? 100000 : 0) + (pipe_grid ? 1000000 * pipe_grid : 0);
         auto it = mplans.find(key);
         if (it != mplans.end()) return it->second;
         const int dp = dm.dp, fp = dm.fp, L = dm.L;
@@ -589,7 +602,9 @@ struct el_engine {
                                                                         : (dp <= 768 && cfg.encoder_len == 0 ? 3 : 2));
         if (mega_att_stages < 2) fail(EL_INVALID_ARGUMENT, "persistent kernel: attention ring does not fit");
         mega_grid = sms;
+        const int ggrid = pipe_grid ? pipe_grid : mega_grid;  // CTAs running the GEMM phases
         el::IterPlan P{};
+        P.pipe_att_ctas = pipe_grid ? mega_grid - pipe_grid : 0;
         auto g = [&](const uint16_t* A, int m_tiles, int kb_total, int layer_rows, int row_off, int splits) {
             el::IterGemm x;
             x.A = A;
@@ -602,12 +617,12 @@ struct el_engine {
             x.nt = 0;
             return x;
         };
-        P.g[el::kIQkv] = g(wqkv.p, 3 * dp / 128, dp / 64, 3 * dp / 128, 0, mega_splits(3 * dp / 128, dp / 64, n_pad));
-        P.g[el::kIWo] = g(wo.p, dp / 128, dp / 64, dp / 128, 0, mega_splits(dp / 128, dp / 64, n_pad));
-        P.g[el::kIUp] = g(wup.p, fp / 128, dp / 64, fp / 128, 0, mega_splits(fp / 128, dp / 64, n_pad));
+        P.g[el::kIQkv] = g(wqkv.p, 3 * dp / 128, dp / 64, 3 * dp / 128, 0, mega_splits(3 * dp / 128, dp / 64, n_pad, ggrid));
+        P.g[el::kIWo] = g(wo.p, dp / 128, dp / 64, dp / 128, 0, mega_splits(dp / 128, dp / 64, n_pad, ggrid));
+        P.g[el::kIUp] = g(wup.p, fp / 128, dp / 64, fp / 128, 0, mega_splits(fp / 128, dp / 64, n_pad, ggrid));
         P.g[el::kIDown] = g(wdown.p, dp / 128, fp / 64, dp / 128, 0,
                             opt_mega_down_splits ? std::min(opt_mega_down_splits, fp / 64)
-                                                 : mega_splits(dp / 128, fp / 64, n_pad));
+                                                 : mega_splits(dp / 128, fp / 64, n_pad, ggrid));
         // fill: full-K units (direct epilogue) at large N, where split-K partials would outweigh the weights
         P.g[el::kIQc] = g(wqc.p, dp / 128, dp / 64, dp / 128, 0, mega_splits(dp / 128, dp / 64, n_pad));
         P.g[el::kIWoc] = g(woc.p, dp / 128, dp / 64, dp / 128, 0, mega_splits(dp / 128, dp / 64, n_pad));
@@ -625,9 +640,23 @@ struct el_engine {
                 if (k == el::kIDown && (n_pad > 64 || !opt_mega_bm_down)) continue;
                 el::IterGemm& x = P.g[k];
                 const int F = x.m_tiles * 128;
-                const int R = n_pad > 128 ? 2 : 1;  // row groups of 128 batch rows
+                // row groups of 128 batch rows (the pipelined kernel runs one group per phase)
+                const int R = (n_pad > 128 && !pipe_grid) ? 2 : 1;
                 int nt = k == el::kIDown ? 16 : opt_mega_bm_nt_min;
-                while (nt < 128 && F / nt * R > mega_grid) nt *= 2;
+                if (pipe_grid) {
+                    // the fewest waves over the GEMM CTAs, then the smallest N (multiple of 16 dividing
+                    // F) with a unit weight slab of at most 96 KB
+                    const int max_nt = std::max(16, std::min(128, (96 * 1024) / (x.kb_total * 128) / 16 * 16));
+                    int best = 16, best_w = 1 << 30;
+                    for (int c = 16; c <= max_nt; c += 16) {
+                        if (F % c) continue;
+                        const int w = ceil_div(F / c, ggrid);
+                        if (w < best_w) { best_w = w; best = c; }
+                    }
+                    nt = best;
+                } else {
+                    while (nt < 128 && F / nt * R > ggrid) nt *= 2;
+                }
                 x.mode = 1;
                 x.nt = nt;
                 bm_w = std::max(bm_w, x.kb_total * nt * 128);
@@ -699,7 +728,26 @@ struct el_engine {
         P.kv_pf_blocks = (int)std::min<long long>(1 << 20, (long long)opt_mega_kv_pf_mb * (1 << 20) / (blk2 * mega_grid));
         return mplans.emplace(key, P).first->second;
     }
+    void launch_pipe(int B) {
+        const int ga = std::min(std::max(pipe_att, 16), sms - 16);
+        el::IterPlan& P = mplan_for(B, 0, sms - ga);
+        el::DevState s = state(false, B);
+        // attention CTAs have the whole ring region to themselves: as many stages as fit
+        s.attn_stages = std::min(8, P.ring_bytes / el::attn_stage_bytes(dm));
+        if (s.attn_stages < 2) fail(EL_INVALID_ARGUMENT, "pipelined kernel: attention ring does not fit");
+        s.attn_seg_cost = opt_attn_seg_cost >= 0 ? opt_attn_seg_cost : 0;
+        if (std::getenv("EL_PIPE_DEBUG"))
+            fprintf(stderr, "pipe: grid %d att %d ring %d att_stages %d stages %d stage_bytes %d n_pad %d bm_grp %d "
+                    "nt %d/%d/%d splits down %d fill %d\n", mega_grid, P.pipe_att_ctas, P.ring_bytes, s.attn_stages,
+                    P.stages, P.stage_bytes, P.n_pad, P.bm_grp, P.g[el::kIQkv].nt, P.g[el::kIWo].nt, P.g[el::kIUp].nt,
+                    P.g[el::kIDown].splits, P.g[el::kIFill].splits);
+        el::launch_pipe(s, P, mmaps[P.map_key], mega_grid, stream);
+    }
     void launch_mega(int B) {
+        if (pipe_for(B)) {
+            launch_pipe(B);
+            return;
+        }
         el::IterPlan& P = mplan_for(B);
         el::DevState s = state(false, B);
         s.attn_stages = mega_att_stages;
@@ -1732,6 +1780,13 @@ int el_engine_destroy(el_engine* e) {
 int el_engine_set_option(el_engine* e, const char* key, int64_t v) {
     API_BEGIN
     if (!std::strcmp(key, "graph")) e->use_graph = v != 0;
+    else if (!std::strcmp(key, "pipe")) {
+        if (v < 0 || v > 2) fail(EL_INVALID_ARGUMENT, "pipe must be 0 (off), 1 (on) or 2 (auto)");
+        e->use_pipe = (int)v;
+    } else if (!std::strcmp(key, "pipe_att_ctas")) {
+        if (v < 16 || v > 132) fail(EL_INVALID_ARGUMENT, "pipe_att_ctas must be in [16, 132]");
+        e->pipe_att = (int)v;
+    }
     else if (!std::strcmp(key, "mega")) {
         if (v < 0 || v > 2) fail(EL_INVALID_ARGUMENT, "mega must be 0 (off), 1 (on) or 2 (auto)");
         e->use_mega = (int)v;

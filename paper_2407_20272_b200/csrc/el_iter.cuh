@@ -255,13 +255,15 @@ __device__ __forceinline__ void unit_mainloop(IterSmem& sm, uint8_t* ring, const
         tc_fence_after();
     }
 }
-// weight-streaming unit (swap-AB): weights = A (16 KB tile per k-block), activations = B (n_pad rows)
+// weight-streaming unit (swap-AB): weights = A (16 KB tile per k-block), activations = B (n_rows
+// rows, default n_pad; the ring stage always has room for n_pad)
 __device__ __forceinline__ void unit_ws(IterSmem& sm, uint8_t* ring, const IterPlan& p, uint32_t& kseq,
                                         const uint16_t* a_row, const uint16_t* b_src, size_t b_kstride, int kb0,
-                                        int nkb, uint32_t useq, int dbg = 0) {
+                                        int nkb, uint32_t useq, int dbg = 0, int n_rows = 0) {
     const RingDesc r{sm.full, sm.empty, (uint32_t)p.stages, (uint32_t)p.stage_bytes, (uint32_t)kAStage};
-    unit_mainloop(sm, ring, r, kseq, a_row, kAStage, (size_t)(kBM * kBK), b_src, (uint32_t)p.n_pad * 128u, b_kstride,
-                  kb0, nkb, (uint32_t)p.n_pad, useq, kL2EvictFirst, kL2EvictLast, dbg);
+    const uint32_t n = (uint32_t)(n_rows > 0 ? n_rows : p.n_pad);
+    unit_mainloop(sm, ring, r, kseq, a_row, kAStage, (size_t)(kBM * kBK), b_src, n * 128u, b_kstride,
+                  kb0, nkb, n, useq, kL2EvictFirst, kL2EvictLast, dbg);
     kseq += (uint32_t)nkb;
 }
 
@@ -460,9 +462,10 @@ __device__ __forceinline__ void epi_fill_direct(const DevState& st, const IterSm
 template <int K>
 // dry: compute on whatever the partials hold and store nothing -- an instruction-cache
 // warm-up run of this exact code while the tile's other splits are still arriving
+// row0: batch row of column 0 (the pipelined kernel reduces one half of the batch at a time)
 __device__ __forceinline__ void reduce_range(const DevState& st, const IterSmem& sm, const IterPlan& p,
                                           const IterGemm& g, const IterCtx x, int nval, int unit_base, int P0, int P,
-                                          int gw, int GW, bool dry = false) {
+                                          int gw, int GW, bool dry = false, int row0 = 0) {
     const int lane = threadIdx.x & 31;
     const int S = g.splits;
     auto rstamp = [&](int k) {  // dbg 64: warp 0's reduce timeline in layer 1's down phase (SM clock)
@@ -488,9 +491,9 @@ __device__ __forceinline__ void reduce_range(const DevState& st, const IterSmem&
                 const int m2 = 2 * dp / kBM;
                 IterCtx y = x;
                 y.layer = x.layer + mm[j] / m2;
-                sd[j] = side4<K>(st, sm, y, mm[j] % m2, cc[j], 4 * lane);
+                sd[j] = side4<K>(st, sm, y, mm[j] % m2, cc[j] + row0, 4 * lane);
             } else if constexpr (K == kIDown) {
-                const size_t i = (size_t)cc[j] * dp + mm[j] * kBM + 4 * lane;
+                const size_t i = (size_t)(cc[j] + row0) * dp + mm[j] * kBM + 4 * lane;
                 dmid[j] = __ldcg(reinterpret_cast<const float4*>(st.mid32 + i));
                 dh[j] = make_float4(0.f, 0.f, 0.f, 0.f);
                 dw[j] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -500,7 +503,7 @@ __device__ __forceinline__ void reduce_range(const DevState& st, const IterSmem&
                 else if (st.technique == kClassifier)
                     dw[j] = __ldg(reinterpret_cast<const float4*>(st.probe_w + mm[j] * kBM + 4 * lane));
             } else {
-                sd[j] = side4<K>(st, sm, x, mm[j], cc[j], 4 * lane);
+                sd[j] = side4<K>(st, sm, x, mm[j], cc[j] + row0, 4 * lane);
             }
         }
         rstamp(1);
@@ -532,7 +535,7 @@ __device__ __forceinline__ void reduce_range(const DevState& st, const IterSmem&
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
             if (!ok[j]) continue;  // warp-uniform
-            const int m = mm[j], c = cc[j], r0 = 4 * lane;
+            const int m = mm[j], c = cc[j] + row0, r0 = 4 * lane;
             if constexpr (K == kIFill) {
                 const int m2 = 2 * dp / kBM;
                 IterCtx y = x;
@@ -597,7 +600,7 @@ __device__ void reduce_phase(const DevState& st, const IterSmem& sm, const IterP
 
 // exit decision of `layer` for every row, computed identically by every CTA
 // (exit_policy.cpp:89-115, engine.cpp:55-66); returns "stop here".
-__device__ bool exit_decide(const DevState& st, IterSmem& sm, int layer, int B, int mt) {
+__device__ bool exit_decide(const DevState& st, IterSmem& sm, int layer, int B, int mt, int cta0 = 0) {
     const int tid = threadIdx.x, Bm = st.dm.Bmax;
     int all = 1;
     if (tid < B) {
@@ -640,7 +643,7 @@ __device__ bool exit_decide(const DevState& st, IterSmem& sm, int layer, int B, 
             sm.first[b] = layer;
         }
         all = s;
-        if (blockIdx.x == 0 && !st.prefill) {  // (prefill rows may exceed max_batch: no decode records)
+        if ((int)blockIdx.x == cta0 && !st.prefill) {  // (prefill rows may exceed max_batch: no decode records)
             if (st.technique != kSoftmax) {  // softmax: written by the distributed decide phase
                 st.conf[(size_t)(layer - 1) * Bm + b] = conf;
                 st.accept[b] = acc;
@@ -883,12 +886,14 @@ __device__ __forceinline__ void unit_bm(IterSmem& sm, uint8_t* ring, const IterP
 // producer lane; weights never depend on the previous phase, so their HBM latency
 // overlaps the phase in flight and the grid barrier.  Returns whether it issued.
 __device__ __forceinline__ bool bm_prefetch(IterSmem& sm, uint8_t* ring, const IterPlan& p, const IterMaps& maps,
-                                            int gid, int layer) {
+                                            int gid, int layer, int ci = -1, int rg_only = -1) {
     const IterGemm& g = p.g[gid];
     if (!g.mode || !p.bm_prefetch) return false;
-    const int R = p.bm_rows / p.bm_grp;  // this CTA's first unit: (feature group cta / R, row group cta % R)
-    if ((int)blockIdx.x >= g.m_tiles * kBM / g.nt * R) return false;
-    const int f0 = ((int)blockIdx.x / R) * g.nt;
+    const int CI = ci < 0 ? (int)blockIdx.x : ci;
+    // this CTA's first unit: (feature group CI / R, row group CI % R); one row group: feature group CI
+    const int R = rg_only >= 0 ? 1 : p.bm_rows / p.bm_grp;
+    if (CI >= g.m_tiles * kBM / g.nt * R) return false;
+    const int f0 = (CI / R) * g.nt;
     const int row_block = (layer - 1) * g.layer_rows + g.row_off + f0 / kBM;
     const uint32_t wf = smem_u32(&sm.wfull);
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(wf),
@@ -903,18 +908,22 @@ template <int K>
 __device__ __forceinline__ void gemm_phase_t(const DevState& st, IterSmem& sm, uint8_t* ring, const IterPlan& p,
                                              const IterMaps& maps, int gid, const IterCtx& x, const uint16_t* act,
                                              uint32_t& cseq, uint32_t& wseq, uint32_t& useq, int B, bool& wpf,
-                                             int next_gid, int next_layer) {
+                                             int next_gid, int next_layer, int ci = -1, int cn = -1,
+                                             int rg_only = -1, int next_rg = -1) {
     const IterGemm& g = p.g[gid];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int R = p.bm_rows / p.bm_grp;  // row groups: unit u = (feature group u / R, row group u % R)
+    const int CI = ci < 0 ? (int)blockIdx.x : ci, CN = cn < 0 ? (int)gridDim.x : cn;
+    const int Rall = p.bm_rows / p.bm_grp;
+    // row groups: unit u = (feature group u / R, row group u % R); rg_only >= 0: that row group only
+    const int R = rg_only >= 0 ? 1 : Rall;
     const int U = g.m_tiles * kBM / g.nt * R;
     auto stamp = [&](int k) {  // dbg 64: per-CTA unit timeline of layer 1's batch-M GEMMs
         if ((EL_DBG(st) & 64) && x.layer == 1 && threadIdx.x == 0)  // SM clock (globaltimer ticks are 256 ns)
             st.dbg_ts[300000 + (size_t)blockIdx.x * 32 + K * 8 + k] = clock64();
     };
     stamp(0);
-    for (int u = blockIdx.x; u < U; u += gridDim.x) {
-        const int f0 = (u / R) * g.nt, rg = u % R;
+    for (int u = CI; u < U; u += CN) {
+        const int f0 = (u / R) * g.nt, rg = rg_only >= 0 ? rg_only : u % R;
         const int row_block = (x.layer - 1) * g.layer_rows + g.row_off + f0 / kBM;
         unit_bm(sm, ring, p, cseq, wseq, &maps.w[gid], 0, f0 % kBM, row_block * g.kb_total,
                 act + (size_t)rg * p.bm_grp * kBK, g.kb_total, g.nt, useq, wpf);
@@ -942,7 +951,8 @@ __device__ __forceinline__ void gemm_phase_t(const DevState& st, IterSmem& sm, u
         __syncthreads();
     }
     // this phase's MMAs are done: the weight buffer is free for the next batch-M GEMM's weights
-    if (next_gid >= 0 && threadIdx.x == kProducerWarp * 32) wpf = bm_prefetch(sm, ring, p, maps, next_gid, next_layer);
+    if (next_gid >= 0 && threadIdx.x == kProducerWarp * 32)
+        wpf = bm_prefetch(sm, ring, p, maps, next_gid, next_layer, ci, next_rg);
 }
 
 // Split-K GEMM phase with the reduction fused per output tile: every unit's CTA
@@ -953,12 +963,15 @@ __device__ __forceinline__ void gemm_phase_t(const DevState& st, IterSmem& sm, u
 // wait on the S - 1 peers of the tile.
 // `use`: 1-based count of this GEMM's phases in the launch (the tile counters only grow within
 // a launch and are zeroed at its end)
+// ci / cn: this CTA's index in the set of CTAs running the phase; row0 / n_rows: the batch rows
+// of the phase (bsrc must point at row row0 of the activation layout; n_rows 0 = n_pad)
 template <int K>
 __device__ void gemm_phase_fused(const DevState& st, IterSmem& sm, uint8_t* ring, const IterPlan& p, int gid,
                                  const IterCtx& x, const uint16_t* bsrc, uint32_t& kseq, uint32_t& useq, int nval,
-                                 int use) {
+                                 int use, int ci = -1, int cn = -1, int row0 = 0, int n_rows = 0) {
     const IterGemm& g = p.g[gid];
     const int warp = threadIdx.x >> 5;
+    const int CI = ci < 0 ? (int)blockIdx.x : ci, CN = cn < 0 ? (int)gridDim.x : cn;
     const int U = g.m_tiles * g.splits;
     const size_t bks = (size_t)st.NR * kBK;
     unsigned* cnt = p.tcnt + gid * 64;
@@ -967,12 +980,12 @@ __device__ void gemm_phase_fused(const DevState& st, IterSmem& sm, uint8_t* ring
             st.dbg_ts[300000 + (size_t)blockIdx.x * 32 + 3 * 8 + k] = clock64();
     };
     stamp(0);
-    for (int u = blockIdx.x; u < U; u += gridDim.x) {
+    for (int u = CI; u < U; u += CN) {
         const int m = u / g.splits, s = u % g.splits;
         const int kb0 = s * g.kb_total / g.splits, kb1 = (s + 1) * g.kb_total / g.splits;
         const uint16_t* a = g.A + (size_t)((x.layer - 1) * g.layer_rows + g.row_off + m) * g.kb_total * (kBM * kBK);
         unit_ws(sm, ring, p, kseq, a, bsrc, bks, kb0, kb1 - kb0, useq,
-                (K == kIDown && x.layer == 1) ? (EL_DBG(st) & 64) : 0);
+                (K == kIDown && x.layer == 1) ? (EL_DBG(st) & 64) : 0, n_rows);
         stamp(1);
         if ((EL_DBG(st) & 64) && x.layer == 1 && threadIdx.x == 0 && K == kIDown)
             for (int k = 0; k < 3; ++k) st.dbg_ts[300000 + (size_t)blockIdx.x * 32 + 3 * 8 + 5 + k] = sm.tdbg[k == 2 ? 3 : k];
@@ -989,7 +1002,7 @@ __device__ void gemm_phase_fused(const DevState& st, IterSmem& sm, uint8_t* ring
             if ((EL_DBG(st) & 64) && x.layer == 1 && K == kIDown) st.dbg_ts[310000 + (size_t)blockIdx.x * 8 + 5] = clock64();
         }
     }
-    for (int u = blockIdx.x; u < U; u += gridDim.x) {
+    for (int u = CI; u < U; u += CN) {
         const int m = u / g.splits, s = u % g.splits;
         const int c0 = s * nval / g.splits, c1 = (s + 1) * nval / g.splits;
         // dbg bit 24: pass 0 (dry) runs the reduce code while the tile's other splits arrive,
@@ -1008,7 +1021,8 @@ __device__ void gemm_phase_fused(const DevState& st, IterSmem& sm, uint8_t* ring
                 __syncthreads();
                 stamp(3);
             }
-            if (warp < 8) reduce_range<K>(st, sm, p, g, x, nval, 0, m * nval + c0, m * nval + c1, warp, 8, pass == 0);
+            if (warp < 8)
+                reduce_range<K>(st, sm, p, g, x, nval, 0, m * nval + c0, m * nval + c1, warp, 8, pass == 0, row0);
         }
         __syncthreads();
         stamp(4);

@@ -780,6 +780,9 @@ struct AttnSrc {
     // layer's q and newest K/V rows; those loads wait until *gate reaches gate_target
     const unsigned* gate;
     unsigned gate_target;
+    // work range (the pipelined kernel runs attention for one half of the batch on a subset of
+    // the CTAs): rows [r0, r1) (r1 < 0: all rows), CTA cta of ncta (< 0: blockIdx.x / gridDim.x)
+    int r0 = 0, r1 = -1, cta = -1, ncta = -1;
 };
 
 // attn_prefix_sum: the warp-parallel prefix sum of KV blocks per row into a.pref
@@ -920,51 +923,56 @@ __device__ __forceinline__ void attn_body(const DevState& st, AttnSmem& a, uint8
         // streamed; q and the block holding `pos` (written by this layer's QKV
         // kernel) are requested after it (one pending stage).
         const int B = st.rows.B;
+        const int R0 = src.r0, R1 = src.r1 < 0 ? B : src.r1;  // rows of this pass
+        const int CI = src.cta < 0 ? (int)blockIdx.x : src.cta, CN = src.ncta < 0 ? (int)gridDim.x : src.ncta;
         if (lane == 0) EL_ATT_CLK(1);
         if (!persistent) attn_prefix_sum(st, a);  // (standalone kernel: src.pref == a.pref)
-        // Work split: the flattened (row, block) space [0, T) is cut into a static
-        // head [0, Ts) -- CTA i streams [i*Ts/G, (i+1)*Ts/G), with fewer blocks than
+        // Work split: the flattened (row, block) space of rows [R0, R1) -- blocks
+        // [pref[R0], pref[R1]), relative index g in [0, T) -- is cut into a static
+        // head [0, Ts) -- CTA i streams its share [i*Ts/G, (i+1)*Ts/G), with fewer blocks than
         // CTAs only the first Ts CTAs work -- and a dynamic tail [Ts, T) of items
         // of `cb` blocks that CTAs grab from an atomic counter when their static
         // range is done, so SMs that HBM serves faster take more of the tail.
         // Partial slots per row: static segments in CTA order, then tail items in
         // item order -- the combine order never depends on which CTA ran what.
         // (int arithmetic: T <= 256 rows x 128 blocks, products <= T * 148 -- no 64-bit division)
-        const int T = src.pref[B];
+        const int gA = src.pref[R0];
+        auto PR = [&](int r) { return (int)src.pref[r] - gA; };  // relative block prefix of row r
+        const int T = PR(R1);
         const int cb = max(1, st.attn_dyn_cb);
-        const int Td = (EL_DEBUG && st.attn_dyn_permille > 0 && st.attn_queue)  // (dynamic tail: probe builds)
-                                 ? min(T, (T * st.attn_dyn_permille / 1000 + cb - 1) / cb * cb) : 0;
+        const int Td = (EL_DEBUG && st.attn_dyn_permille > 0 && st.attn_queue && R0 == 0 && R1 == B && CN == (int)gridDim.x)
+                           ? min(T, (T * st.attn_dyn_permille / 1000 + cb - 1) / cb * cb) : 0;  // (probe builds)
         const int Ts = T - Td;
         if (lane == 0) EL_ATT_CLK(10);
         const int n_items = (Td + cb - 1) / cb;
-        const int G = min((int)gridDim.x, Ts);
+        const int G = min(CN, Ts);
         // Cost-aware static split: every row start costs dl extra "virtual" blocks (a segment
         // switch + one more partial merge), so CTAs whose range crosses a row boundary get
-        // fewer real blocks.  Virtual position of real block g of row r: g + dl * (r + 1);
+        // fewer real blocks.  Virtual position of real block g of row r: g + dl * (r - R0 + 1);
         // CTA i owns virtual [floor(i V / G), floor((i + 1) V / G)).  Deterministic: depends
         // on the row structure only.
         const int dl = (Td == 0) ? st.attn_seg_cost : 0;
-        const int V = Ts + dl * B;
-        auto cta_of = [&](int g, int r) { return (int)(((g + dl * (r + 1) + 1) * G + V - 1) / V - 1); };
+        const int V = Ts + dl * (R1 - R0);
+        auto cta_of = [&](int g, int r) { return (int)(((g + dl * (r - R0 + 1) + 1) * G + V - 1) / V - 1); };
         auto real_of = [&](int vb) {  // first real block whose virtual position is >= vb
             if (vb >= V) return Ts;
-            int lo = 0, hi = B - 1;  // first row whose virtual end exceeds vb
+            int lo = R0, hi = R1 - 1;  // first row whose virtual end exceeds vb
             while (lo < hi) {
                 const int mid = (lo + hi) >> 1;
-                if (src.pref[mid + 1] + dl * (mid + 1) > vb) hi = mid;
+                if (PR(mid + 1) + dl * (mid - R0 + 1) > vb) hi = mid;
                 else lo = mid + 1;
             }
-            return src.pref[lo] + max(0, vb - src.pref[lo] - dl * (lo + 1));
+            return PR(lo) + max(0, vb - PR(lo) - dl * (lo - R0 + 1));
         };
         // segment bookkeeping of row r: static segments and the first tail item touching it
         auto row_static = [&](int r, int& first_cta) {
-            const int r0 = src.pref[r], r1 = min((int)src.pref[r + 1], Ts);
+            const int r0 = PR(r), r1 = min(PR(r + 1), Ts);
             if (r0 >= r1) return 0;
             first_cta = cta_of(r0, r);
             return cta_of(r1 - 1, r) - first_cta + 1;
         };
         auto row_items = [&](int r, int& i0) {
-            const int r0 = max((int)src.pref[r], Ts), r1 = src.pref[r + 1];
+            const int r0 = max(PR(r), Ts), r1 = PR(r + 1);
             if (r0 >= r1) return 0;
             i0 = (r0 - Ts) / cb;
             return (r1 - 1 - Ts) / cb - i0 + 1;
@@ -1003,8 +1011,9 @@ __device__ __forceinline__ void attn_body(const DevState& st, AttnSmem& a, uint8
             }
         };
         int seq = seq0;
-        // stream blocks [g, seg_end) of row b as one segment (partial slot `slot` of `nseg`)
-        // pid: the block ids of [g, seg_end) already in shared memory (a.ids), or nullptr
+        // stream blocks [g, seg_end) (absolute flattened indices) of row b as one segment
+        // (partial slot `slot` of `nseg`); pid: the block ids of [g, seg_end) already in shared
+        // memory (a.ids), or nullptr
         auto emit = [&](int b, int g, int seg_end, int slot, int nseg, const int* pid) {
             const int sb0 = src.pref[b], sb1 = src.pref[b + 1];
             const int nblk = (int)(sb1 - sb0);
@@ -1060,9 +1069,9 @@ __device__ __forceinline__ void attn_body(const DevState& st, AttnSmem& a, uint8
             }
         };
         // ---- static head ----
-        const bool has_static = (int)blockIdx.x < G;
-        const int g0 = has_static ? real_of((int)blockIdx.x * V / G) : 0;
-        const int g1 = has_static ? real_of((int)(blockIdx.x + 1) * V / G) : 0;
+        const bool has_static = CI < G;
+        const int g0 = gA + (has_static ? real_of(CI * V / G) : 0);  // absolute flattened range [g0, g1)
+        const int g1 = gA + (has_static ? real_of((CI + 1) * V / G) : 0);
         // the range's block ids are gathered before streaming (independent loads in
         // parallel: a segment switch mid-range then costs no dependent table-load round
         // trip); the persistent kernel gathers the next layer's at the end of this pass
@@ -1070,7 +1079,7 @@ __device__ __forceinline__ void attn_body(const DevState& st, AttnSmem& a, uint8
         const int ib = src.idbuf;
         auto gather = [&](int lay) {
             for (int g = g0 + lane; g < g1; g += 32) {
-                int lo = 0, hi = B - 1;
+                int lo = R0, hi = R1 - 1;
                 while (lo < hi) {
                     const int mid = (lo + hi + 1) >> 1;
                     if (src.pref[mid] <= g) lo = mid;
@@ -1090,22 +1099,22 @@ __device__ __forceinline__ void attn_body(const DevState& st, AttnSmem& a, uint8
         if (pre && !(a.ids_layer[ib] == layer && a.ids_g0[ib] == (int)g0)) gather(layer);
         if (has_static) {
             if (lane == 0) EL_ATT_CLK(2);
-            int b = 0;
+            int b = R0;
             {  // first row of the range: largest b with pref[b] <= g0 (binary search)
-                int hi = B - 1;
+                int hi = R1 - 1;
                 while (b < hi) {
                     const int mid = (b + hi + 1) >> 1;
                     if (src.pref[mid] <= g0) b = mid;
                     else hi = mid - 1;
                 }
             }
-            for (int g = g0; g < g1 && b < B;) {
+            for (int g = g0; g < g1 && b < R1;) {
                 const int seg_end = min(g1, (int)src.pref[b + 1]);
                 int fc = 0;
                 const int ns = row_static(b, fc);
                 int i0 = 0;
                 const int nseg = ns + (int)row_items(b, i0);
-                emit(b, g, seg_end, (int)blockIdx.x - fc, nseg, pre ? a.ids[ib] + (g - g0) : nullptr);
+                emit(b, g, seg_end, CI - fc, nseg, pre ? a.ids[ib] + (g - g0) : nullptr);
                 g = seg_end;
                 ++b;
             }
@@ -1737,5 +1746,6 @@ void init_kernel_attributes() {
 }
 
 #include "el_iter.cuh"
+#include "el_pipe.cuh"
 
 }  // namespace el

@@ -235,6 +235,7 @@ struct IterPlan {
     int pf_flags;      // bit 0: L2 prefetch of GEMM weight tiles one phase ahead
     float* part;     // split-K partials [unit][n_pad][128] fp32
     unsigned* bar;   // grid barrier: [0] arrivals, [32] generation
+    int pipe_att_ctas;  // pipelined kernel (el_pipe.cuh): CTAs [0, pipe_att_ctas) run attention
 };
 
 // 3-D (64 x 128 rows x tiles, no swizzle: the tiles are pre-swizzled) tensor maps over the
@@ -247,6 +248,10 @@ int iter_smem_fixed();                 // bytes outside the ring region (alignme
 int iter_max_ctas_per_sm(const Dims& dm, int ring_bytes);
 void init_iter_attributes();
 void launch_iter(const DevState& st, const IterPlan& p, const IterMaps& maps, int grid, cudaStream_t s);
+// the pipelined iteration (el_pipe.cuh): attention and projection GEMMs of the two batch halves
+// on disjoint CTA sets, overlapped (batch 129..256)
+void launch_pipe(const DevState& st, const IterPlan& p, const IterMaps& maps, int grid, cudaStream_t s);
+void init_pipe_attributes();
 constexpr int kIterTbufBytes = 32 * 129 * 4;
 
 // host+device mirror of the allocator arithmetic (used by el_kv_block_trace)

@@ -401,3 +401,29 @@ def test_transcript_jsonl_byte_identical_on_device(port, tmp_path):
         X.write_transcript_jsonl(tp, str(b), g.model, g.technique)
         assert a.read_bytes() == b.read_bytes(), tech
         e.close()
+
+
+@pytest.mark.parametrize("B", [200, 256])
+def test_pipelined_kernel_matches_persistent_kernel(B):
+    """The pipelined iteration kernel (el_pipe.cuh: attention and projection GEMMs of the two
+    batch halves overlapped on disjoint CTA sets) against the plain persistent kernel on the same
+    session: identical exit decisions and tokens up to split-K summation order (the down
+    projection's K splits differ), run-to-run bitwise deterministic; B = 200 has a ragged second
+    half."""
+    L, d, V = 6, 1024, 2048
+    outs = []
+    for pipe in (1, 1, 0):
+        g, _ = cfg_pair(L, d, V, 8, "classifier", lam=0.6, gamma=0.97, B=B)
+        e = X.Engine(g, mega=True)
+        e.set_option("pipe", pipe)
+        e.session_begin(np.arange(B) * 7 % V + 1, 60, 100, 5)
+        rs = [e.decode_iteration() for _ in range(4)]
+        outs.append((rs, e.hidden(rs[-1]["output_layer"] & 1), e.kv(B - 1, L, 63), e.kv(3, 1, 63)))
+        e.close()
+    (ra, ha, ka, qa), (rb, hb, kb, qb), (rc, hc, kc, qc) = outs
+    for x, y in zip(ra, rb):
+        assert x["output_layer"] == y["output_layer"] and np.array_equal(x["tokens"], y["tokens"])
+    assert np.array_equal(ha, hb) and np.array_equal(ka[0], kb[0]) and np.array_equal(qa[1], qb[1])
+    assert [x["output_layer"] for x in ra] == [x["output_layer"] for x in rc]
+    assert np.mean([np.mean(x["tokens"] == y["tokens"]) for x, y in zip(ra, rc)]) >= 0.97
+    assert relerr(qa[0], qc[0]) <= 1e-2  # layer-1 K of the last position: same inputs, same GEMM
