@@ -415,7 +415,9 @@ struct el_engine {
         pf_mid32.alloc((size_t)kPfRows * dp);
         pf_mid_b.alloc((size_t)kPfRows * dp);
         pf_up_b.alloc((size_t)kPfRows * fp);
-        NR = std::max(16, round_up(Bm, 16));
+        // activation rows of the GEMM operand layout: batch rounded to 16, or to 128 above 128 (two
+        // whole 128-row groups for the batch-M GEMMs and the pipelined kernel's halves)
+        NR = Bm > 128 ? round_up(Bm, 128) : std::max(16, round_up(Bm, 16));
         h32.alloc((size_t)2 * Bm * dp);
         hb.alloc((size_t)2 * NR * dp);
         q32.alloc((size_t)Bm * dp);
@@ -731,6 +733,8 @@ struct el_engine {
     void launch_pipe(int B) {
         const int ga = std::min(std::max(pipe_att, 16), sms - 16);
         el::IterPlan& P = mplan_for(B, 0, sms - ga);
+        if (!P.g[el::kIQkv].mode || !P.g[el::kIWo].mode || !P.g[el::kIUp].mode)
+            fail(EL_RUNTIME_ERROR, "pipelined kernel: needs batch-M QKV / W_o / up phases");
         el::DevState s = state(false, B);
         // attention CTAs have the whole ring region to themselves: as many stages as fit
         s.attn_stages = std::min(8, P.ring_bytes / el::attn_stage_bytes(dm));
