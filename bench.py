@@ -397,6 +397,34 @@ def run_ours(args, rank, world, local_rank, dist, stub=False):
               "mean_rows_per_turn": round(float(tr[warm_t:].mean()), 2),
               "note": "one host round trip per turn (the next turn's rows depend on this turn's exits)"}
 
+    # 6. Engine::run (the reference's API, engine.cpp:110-330) end to end: this rank's requests with
+    #    their real 512-token prompts (batched causal prefill on the device, no seeded KV), 128 new
+    #    tokens each, through the public call with host workload in and transcript out
+    er = None
+    if not enc and not stub and not args.no_engine_run:
+        from paper_2407_20272_b200 import exitlab as X
+        cap_er = PROMPT + OUT_LEN
+        cfg = X.EngineConfig(model=X.ModelConfig(L, d, V, 0), technique=X.ExitTechnique(c["tech"]),
+                             schedule=X.ThresholdSchedule(c["lam"], c["gamma"], 0.0), max_batch=B,
+                             pool_blocks=B * L * (-(-cap_er // 16)), eos_token=-1)
+        eng = X.Engine(cfg)
+        wl = X.Workload([X.Request(0.0, prompts[i], OUT_LEN) for i in mine])
+        barrier()
+        t0 = time.perf_counter()
+        tr = eng.run(wl)
+        er_s = max_over_ranks(time.perf_counter() - t0)
+        m = X.compute_metrics(tr)
+        er = {"value": round(m.total_tokens * world / er_s, 1), "unit": "tokens/s", "wall_s": round(er_s, 4),
+              "requests_per_gpu": B, "prompt_len": PROMPT, "new_tokens": OUT_LEN,
+              "prefill_positions_per_gpu": B * (PROMPT - 1), "iterations": m.iterations,
+              "mean_layers_per_token": round(m.mean_layers_per_token, 3),
+              "early_exit_rate_pct": round(m.early_exit_rate_pct, 2),
+              "simulated_clock_s": round(m.total_sim_time, 6),
+              "note": "wall clock of Engine::run incl. workload upload, batched prefill, decode and transcript read-back; "
+                      "decode iterations run back to back on the device between scheduling events"}
+        del tr
+        eng.close()
+
     if rank != 0:
         return None
     peak, peak_kind = load_peaks()
@@ -430,7 +458,9 @@ def run_ours(args, rank, world, local_rank, dist, stub=False):
         "early_exit_speedup": round(value / full, 3),
         # dominant kernel: the persistent decode-iteration kernel (one launch = one step), so its
         # algorithmic bytes per launch are the iteration's and its launch time is ms_per_step
-        "roofline": ({"kernel": "persistent decode-iteration kernel (iter_kernel, 1 launch per step)", "bound": "hbm",
+        "roofline": ({"kernel": ("pipelined decode-iteration kernel (pipe_kernel, 1 launch per step)" if plan.get("pipe")
+                                 else "persistent decode-iteration kernel (iter_kernel, 1 launch per step)"),
+                      "bound": "hbm",
                       "achieved": round(it_gbs, 1), "peak": peak, "unit": "GB/s", "frac": round(it_gbs / peak, 4),
                       "traffic": traffic_of(f"iter_traffic_{args.config}.json"), "peak_source": peak_kind,
                       "algorithmic_bytes_per_launch": int(it_bytes), "launch_ms": round(ms / args.steps, 5)}
@@ -458,6 +488,8 @@ def run_ours(args, rank, world, local_rank, dist, stub=False):
     if ll:
         ll["speedup_vs_iteration_level"] = round(ll["value"] / value, 3)
         out["layer_level"] = ll
+    if er:
+        out["engine_run"] = er
     return out
 
 
@@ -626,6 +658,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-c4", action="store_true", help="skip the configs[3] comparison (c5 only)")
     ap.add_argument("--no-layer-level", action="store_true", help="skip the layer-level scheduling leg")
+    ap.add_argument("--no-engine-run", action="store_true", help="skip the Engine::run (real prefill) leg")
     ap.add_argument("--ref-budget-s", type=float, default=150.0,
                     help="reference arm: bound on the timed CPU iterations (seconds)")
     ap.add_argument("--eager", action="store_true", help="host-driven layer loop (for ncu, which cannot "

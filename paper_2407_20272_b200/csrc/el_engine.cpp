@@ -221,6 +221,10 @@ struct el_engine {
     DevBuf<unsigned long long> dbg_ts;
     DevBuf<float> fixed_conf;
     DevBuf<uint8_t> l2flush;  // cold-L2 kernel timing (el_time_kernel kind | 0x100)
+    // Engine::run between scheduling events: queued iterations run while *run_ctl[0] != 0
+    // (run_ctl[1] counts those that ran); simulated clock, its per-iteration log, tokens left
+    DevBuf<int> run_ctl, run_rem;
+    DevBuf<double> run_clock, run_log;
     int* cont_host = nullptr;
     int* cont_dev = nullptr;
 
@@ -445,6 +449,11 @@ struct el_engine {
             lambdas.alloc((size_t)L);
             CK(cudaMemcpy(lambdas.p, lam.data(), sizeof(double) * L, cudaMemcpyHostToDevice));
         }
+        run_ctl.alloc(4);
+        set_run_active(1);
+        run_rem.alloc((size_t)Bm);
+        run_clock.alloc(1);
+        run_log.alloc((size_t)2 * rec_cap);
         CK(cudaHostAlloc(&cont_host, sizeof(int) * 4, cudaHostAllocMapped));
         CK(cudaHostGetDevicePointer((void**)&cont_dev, cont_host, 0));
 
@@ -460,6 +469,10 @@ struct el_engine {
         slot_bpl.assign((size_t)dm.slots, -1);
     }
 
+    void set_run_active(int v) {
+        const int w[2] = {v, 0};
+        CK(cudaMemcpy(run_ctl.p, w, sizeof w, cudaMemcpyHostToDevice));
+    }
     void reset_allocator() {
         std::vector<int> st((size_t)cfg.pool_blocks);
         for (int i = 0; i < cfg.pool_blocks; ++i) st[(size_t)i] = cfg.pool_blocks - 1 - i;  // pops 0 first
@@ -800,6 +813,7 @@ struct el_engine {
         s.turn_layer = 0;
         s.hstore = hstore.p;
         s.row_seq = row_seq.p;
+        s.run_active = run_ctl.p;
         return s;
     }
 
@@ -1232,63 +1246,106 @@ struct el_engine {
                 continue;
             }
 
-            // decode_iteration (engine.cpp:208-310)
+            // decode_iteration (engine.cpp:208-310).  Between scheduling events the batch is fixed,
+            // so up to k iterations (k = the fewest tokens any running sequence may still emit) are
+            // queued back to back on the device; after each, run_step_kernel charges the simulated
+            // clock and stops the rest once a sequence finishes (max_new / EOS) or the pending head
+            // becomes admissible -- one host synchronisation per event instead of per iteration.
             const int B = (int)running.size();
             hs.assign((size_t)B, 0); hp.assign((size_t)B, 0); ht.assign((size_t)B, 0);
+            std::vector<int> rem((size_t)B, 0);
+            int k = rec_cap;
             for (int b = 0; b < B; ++b) {
                 hs[(size_t)b] = running[(size_t)b].slot;
                 hp[(size_t)b] = running[(size_t)b].committed;
                 ht[(size_t)b] = running[(size_t)b].next_input;
+                rem[(size_t)b] = running[(size_t)b].max_new - (int)running[(size_t)b].tokens.size();
+                k = std::min(k, rem[(size_t)b]);
+            }
+            const bool chunked = !cfg.capture_kv && (mega_for(B) || use_graph);
+            if (!chunked) k = 1;
+            double next_arrival = INFINITY;
+            if (next_pending < n && (int)running.size() < cfg.max_batch) {
+                const int r = order[(size_t)next_pending];
+                if (can_allocate(off[r + 1] - off[r] + max_new[r])) next_arrival = arrival[r];
             }
             CK(cudaMemcpyAsync(row_slot.p, hs.data(), sizeof(int) * B, cudaMemcpyHostToDevice, stream));
             CK(cudaMemcpyAsync(row_pos.p, hp.data(), sizeof(int) * B, cudaMemcpyHostToDevice, stream));
             CK(cudaMemcpyAsync(row_tok.p, ht.data(), sizeof(int) * B, cudaMemcpyHostToDevice, stream));
-            iteration(B);
-            const IterOut o = read_iteration(iteration_no, B);
-            ++iteration_no;
-            const int e = o.out_layer;
-            if (e < 1 || e > L) fail(EL_RUNTIME_ERROR, "decode_iteration: bad output layer %d", e);
-            for (auto& q : running) q.committed += 1;  // commit (engine.cpp:262-264)
+            CK(cudaMemcpyAsync(run_rem.p, rem.data(), sizeof(int) * B, cudaMemcpyHostToDevice, stream));
+            CK(cudaMemcpyAsync(run_clock.p, &clock, sizeof(double), cudaMemcpyHostToDevice, stream));
+            const int ctl1[2] = {1, 0};
+            CK(cudaMemcpyAsync(run_ctl.p, ctl1, sizeof ctl1, cudaMemcpyHostToDevice, stream));
+            el::RunCtl rc{run_clock.p, run_log.p, run_rem.p, run_ctl.p, run_ctl.p + 1, cfg.eos_token, L, next_arrival,
+                          cfg.c_layer_fixed, cfg.c_layer_per_seq, check_cost(), cfg.c_fill_per_seq_layer};
+            const el::DevState sd = state(false, B);
+            for (int i = 0; i < k; ++i) {
+                iteration(B);
+                el::launch_run_step(sd, rc, stream);
+            }
+            int ctl[2] = {0, 0};
+            CK(cudaMemcpyAsync(ctl, run_ctl.p, sizeof ctl, cudaMemcpyDeviceToHost, stream));
+            CK(cudaStreamSynchronize(stream));
+            const int n_done = ctl[1];
+            if (n_done < 1 || n_done > k) fail(EL_RUNTIME_ERROR, "run: %d of %d queued iterations ran", n_done, k);
+            set_run_active(1);
+            std::vector<double> dlog((size_t)2 * rec_cap);
+            CK(cudaMemcpy(dlog.data(), run_log.p, sizeof(double) * dlog.size(), cudaMemcpyDeviceToHost));
+            for (int it = 0; it < n_done; ++it) {
+                const IterOut o = read_iteration(iteration_no, B);
+                const int cur = iteration_no % rec_cap;
+                ++iteration_no;
+                const int e = o.out_layer;
+                if (e < 1 || e > L) fail(EL_RUNTIME_ERROR, "decode_iteration: bad output layer %d", e);
+                for (auto& q : running) q.committed += 1;  // commit (engine.cpp:262-264)
 
-            const double charge = e * (cfg.c_layer_fixed + cfg.c_layer_per_seq * B) + e * B * check_cost() +
-                                  (double)(L - e) * B * cfg.c_fill_per_seq_layer;
-            clock += charge;
-            t->it_clock.push_back(clock);
-            t->it_charge.push_back(charge);
-            t->it_output_layer.push_back(e);
-            for (int l = 0; l < L; ++l)
-                for (int b = 0; b < B; ++b) t->it_conf.push_back((double)o.conf[(size_t)l * B + b]);
-            std::vector<float> hexit;
-            if (cfg.capture_kv) {
-                hexit.resize((size_t)B * dm.dp);
-                CK(cudaMemcpy(hexit.data(), h32.p + (size_t)(e & 1) * dm.Bmax * dm.dp, sizeof(float) * B * dm.dp,
-                              cudaMemcpyDeviceToHost));
-            }
-            int max_accept = 0;
-            for (int b = 0; b < B; ++b) {
-                Live& q = running[(size_t)b];
-                const int token = o.tok[(size_t)b];
-                const int acc = o.acc[(size_t)b];
-                max_accept = std::max(max_accept, acc);
-                t->ps_seq.push_back(q.id);
-                t->ps_accept.push_back(acc);
-                t->ps_token.push_back(token);
-                q.tokens.push_back(token);
-                q.exit_layers.push_back(acc);
-                q.iter_out.push_back(e);
-                if (cfg.capture_kv)
-                    for (int i = 0; i < d; ++i) t->caps[q.id].exit_states.push_back(hexit[(size_t)b * dm.dp + i]);
-                if (q.tokens.size() == 1) q.first_token = clock;
-                const bool hit_eos = cfg.eos_token >= 0 && token == cfg.eos_token;
-                if (hit_eos || (int)q.tokens.size() >= q.max_new) {
-                    q.finished = true;
-                    q.finish = clock;
-                } else {
-                    q.next_input = token;
+                const double charge = e * (cfg.c_layer_fixed + cfg.c_layer_per_seq * B) + e * B * check_cost() +
+                                      (double)(L - e) * B * cfg.c_fill_per_seq_layer;
+                clock += charge;
+                if (chunked && (dlog[2 * (size_t)cur] != clock || dlog[2 * (size_t)cur + 1] != charge))
+                    fail(EL_RUNTIME_ERROR, "run: device clock %.17g (charge %.17g) != host %.17g (%.17g)",
+                         dlog[2 * (size_t)cur], dlog[2 * (size_t)cur + 1], clock, charge);
+                t->it_clock.push_back(clock);
+                t->it_charge.push_back(charge);
+                t->it_output_layer.push_back(e);
+                for (int l = 0; l < L; ++l)
+                    for (int b = 0; b < B; ++b) t->it_conf.push_back((double)o.conf[(size_t)l * B + b]);
+                std::vector<float> hexit;
+                if (cfg.capture_kv) {
+                    hexit.resize((size_t)B * dm.dp);
+                    CK(cudaMemcpy(hexit.data(), h32.p + (size_t)(e & 1) * dm.Bmax * dm.dp, sizeof(float) * B * dm.dp,
+                                  cudaMemcpyDeviceToHost));
                 }
+                int max_accept = 0;
+                bool any_finished = false;
+                for (int b = 0; b < B; ++b) {
+                    Live& q = running[(size_t)b];
+                    const int token = o.tok[(size_t)b];
+                    const int acc = o.acc[(size_t)b];
+                    max_accept = std::max(max_accept, acc);
+                    t->ps_seq.push_back(q.id);
+                    t->ps_accept.push_back(acc);
+                    t->ps_token.push_back(token);
+                    q.tokens.push_back(token);
+                    q.exit_layers.push_back(acc);
+                    q.iter_out.push_back(e);
+                    if (cfg.capture_kv)
+                        for (int i = 0; i < d; ++i) t->caps[q.id].exit_states.push_back(hexit[(size_t)b * dm.dp + i]);
+                    if (q.tokens.size() == 1) q.first_token = clock;
+                    const bool hit_eos = cfg.eos_token >= 0 && token == cfg.eos_token;
+                    if (hit_eos || (int)q.tokens.size() >= q.max_new) {
+                        q.finished = true;
+                        q.finish = clock;
+                        any_finished = true;
+                    } else {
+                        q.next_input = token;
+                    }
+                }
+                if (max_accept != e) fail(EL_RUNTIME_ERROR, "decode_iteration: output_layer %d != max accept %d", e, max_accept);
+                t->it_batch_off.push_back((int32_t)t->ps_seq.size());
+                if (any_finished && it + 1 < n_done)
+                    fail(EL_RUNTIME_ERROR, "run: the device ran past a finished sequence (iteration %d of %d)", it, n_done);
             }
-            if (max_accept != e) fail(EL_RUNTIME_ERROR, "decode_iteration: output_layer %d != max accept %d", e, max_accept);
-            t->it_batch_off.push_back((int32_t)t->ps_seq.size());
         }
         t->meta = {clock, total_idle, (double)cfg.pool_blocks, (double)top, (double)peak};
         return t.release();
@@ -1901,6 +1958,7 @@ int el_engine_set_option(el_engine* e, const char* key, int64_t v) {
         if (v < 1) fail(EL_INVALID_ARGUMENT, "rec_cap must be >= 1");
         e->rec_cap = (int)v;
         e->rec.alloc((size_t)v * e->rec_stride);
+        e->run_log.alloc((size_t)2 * v);
         e->invalidate_graphs();
     } else fail(EL_INVALID_ARGUMENT, "unknown option %s", key);
     API_END
@@ -2191,7 +2249,9 @@ int el_plan_info(el_engine* e, int64_t* out, int cap) {
                          M.g[el::kIQkv].splits, M.g[el::kIWo].splits, M.g[el::kIUp].splits, M.g[el::kIDown].splits,
                          M.g[el::kIFill].splits, M.g[el::kIQkv].nt, M.g[el::kIWo].nt, M.g[el::kIUp].nt,
                          M.stages, M.bm_stages, e->mega_att_stages,
-                         e->mega_for(e->in_session ? e->sess_B : e->dm.Bmax) ? 1 : 0};
+                         e->mega_for(e->in_session ? e->sess_B : e->dm.Bmax) ? 1 : 0,
+                         (e->mega_for(e->in_session ? e->sess_B : e->dm.Bmax) &&
+                          e->pipe_for(e->in_session ? e->sess_B : e->dm.Bmax)) ? 1 : 0};
     const int n = (int)(sizeof v / sizeof v[0]);
     for (int i = 0; i < std::min(n, cap); ++i) out[i] = v[i];
     return n;

@@ -365,6 +365,8 @@ template <GemmKind K>
 __global__ void __launch_bounds__(128, 1)
     gemm_kernel(GemmArgs g, DevState st) {
     using E = Epi<K>;
+    if constexpr (K == kGemmFill || K == kGemmLmFinal)  // the iteration's tail: skipped with the iteration
+        if (st.run_active && *(volatile const int*)st.run_active == 0) return;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // 1024-byte alignment by pointer offset (keeps the shared address space visible to the compiler)
     uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -1564,6 +1566,10 @@ void launch_exit(const DevState& st, cudaStream_t s, bool pdl) {
 // ===========================================================================
 __global__ void embed_kernel(DevState st) {
     const int b = blockIdx.x;
+    if (st.run_active && *(volatile const int*)st.run_active == 0) {  // Engine::run chunk over: skip
+        if (b == 0 && threadIdx.x == 0 && st.use_cond) cudaGraphSetConditional(st.cond, 0u);
+        return;
+    }
     tl_mark(st, 0, 0, 0);
     const int dp = st.dm.dp;
     const int tok = st.rows.tok[b];
@@ -1612,6 +1618,7 @@ void launch_embed(const DevState& st, cudaStream_t s) {
 __global__ void __launch_bounds__(256) finish_kernel(DevState st) {
     const int b = blockIdx.x, tid = threadIdx.x;
     pdl_wait();
+    if (st.run_active && *(volatile const int*)st.run_active == 0) return;
     tl_mark(st, 9, 0, 0);
     const int L = st.dm.L, Bm = st.dm.Bmax;
     const LmRed r = lm_reduce_col(st, b);
@@ -1743,6 +1750,40 @@ void init_kernel_attributes() {
     cudaFuncSetAttribute(attn_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, m);
     cudaFuncSetAttribute(attn_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, m);
     cudaFuncSetAttribute(attn_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, m);
+}
+
+// ---- Engine::run between scheduling events (engine.cpp:266-305 on the device) ----
+__global__ void __launch_bounds__(256) run_step_kernel(DevState st, RunCtl c) {
+    if (*(volatile const int*)c.active == 0) return;
+    const int B = st.rows.B, tid = threadIdx.x;
+    int fin = 0;
+    for (int b = tid; b < B; b += blockDim.x) {
+        const int r = c.rem[b] - 1;
+        c.rem[b] = r;
+        const int tok = st.rows.tok[b];  // the token this iteration emitted (the next input)
+        fin |= (r <= 0) || (c.eos >= 0 && tok == c.eos);
+    }
+    fin = __syncthreads_or(fin);
+    if (tid == 0) {
+        // charge = e (c_fixed + c_seq B) + e B c_check + (L - e) B c_fill, in the host's (the
+        // reference's) operation order, every product and sum rounded on its own (no FMA)
+        const int e = *st.out_layer;
+        const double t1 = __dmul_rn((double)e, __dadd_rn(c.c_fixed, __dmul_rn(c.c_seq, (double)B)));
+        const double t2 = __dmul_rn((double)(e * B), c.c_check);
+        const double t3 = __dmul_rn(__dmul_rn((double)(c.L - e), (double)B), c.c_fill);
+        const double charge = __dadd_rn(__dadd_rn(t1, t2), t3);
+        const double clock = __dadd_rn(*c.clock, charge);
+        *c.clock = clock;
+        const int cur = *st.cur_iter % st.rec_cap;
+        c.log[2 * cur] = clock;
+        c.log[2 * cur + 1] = charge;
+        *c.done += 1;
+        if (fin || c.next_arrival <= clock) *c.active = 0;  // a finish or an admission: back to the host
+    }
+}
+void launch_run_step(const DevState& st, const RunCtl& c, cudaStream_t s) {
+    run_step_kernel<<<1, 256, 0, s>>>(st, c);
+    EL_CUDA_LAUNCH_CHECK();
 }
 
 #include "el_iter.cuh"

@@ -120,6 +120,9 @@ struct DevState {
     int turn_layer;
     float* hstore;        // [Bmax][dp] fp32 state entering each sequence's next layer
     const int* row_seq;   // [Bmax] sequence index of each row of the turn
+    // Engine::run between scheduling events: iterations queued back to back on the device skip
+    // themselves once *run_active is 0 (set by run_step_kernel); nullptr = always run
+    const int* run_active;
     // T5 mode (encoder_len > 0): cross-attention weights and the static encoder K/V
     int enc_len, enc_blocks;    // encoder states per sequence; KV blocks they occupy
     const uint16_t* wqc;        // [L][dp][dp]   tiled
@@ -189,6 +192,20 @@ void launch_attention(const DevState& st, cudaStream_t s, bool pdl);
 void launch_exit(const DevState& st, cudaStream_t s, bool pdl);
 void launch_finish(const DevState& st, cudaStream_t s, bool pdl);
 void launch_advance(const DevState& st, cudaStream_t s);
+// Engine::run (engine.cpp:266-305) on the device between scheduling events: after each iteration,
+// the simulated-clock charge of its output layer, the per-sequence max_new / EOS stop and the next
+// admissible arrival decide whether the next queued iteration runs
+struct RunCtl {
+    double* clock;        // simulated clock (bit-exact with the host formula)
+    double* log;          // [rec_cap][2] (clock after, charge) per iteration
+    int* rem;             // [Bmax] tokens each row may still emit
+    int* active;          // 1 while the queued iterations run
+    int* done;            // iterations run in this chunk
+    int eos, L;
+    double next_arrival;  // arrival of the admissible pending head (+inf: none)
+    double c_fixed, c_seq, c_check, c_fill;
+};
+void launch_run_step(const DevState& st, const RunCtl& c, cudaStream_t s);
 void launch_layer_head(const DevState& st, cudaStream_t s);  // prefill commit: pos += 1
 // LIFO block allocator on the device (kv_cache.cpp:78-106, 182-194)
 void launch_kv_alloc(int* stack, int top, int* tables, const Dims& dm, int slot, int bpl, cudaStream_t s);

@@ -62,6 +62,7 @@ template <int NJ>
 __global__ void __launch_bounds__(kIterThreads, 1) pipe_kernel(const __grid_constant__ DevState st,
                                                                 const __grid_constant__ IterPlan p,
                                                                 const __grid_constant__ IterMaps maps) {
+    if (st.run_active && *(volatile const int*)st.run_active == 0) return;  // Engine::run chunk over
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* ring = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     IterSmem& sm = *reinterpret_cast<IterSmem*>(ring + p.ring_bytes);
