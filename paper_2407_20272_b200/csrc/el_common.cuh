@@ -162,6 +162,10 @@ __device__ __forceinline__ void bulk_load_hint(uint32_t dst, const void* src, ui
         "l"(src), "r"(bytes), "r"(bar), "l"(policy)
         : "memory");
 }
+// request [src, src + bytes) into L2 (no completion tracking)
+__device__ __forceinline__ void l2_prefetch_bulk(const void* src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ void bulk_load_ef(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
     bulk_load_hint(smem_u32(dst), src, bytes, smem_u32(bar), kL2EvictFirst);
 }

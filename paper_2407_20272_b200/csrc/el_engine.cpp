@@ -184,7 +184,7 @@ struct el_engine {
     int rec_cap = 4096;
     // pipelined iteration kernel (el_pipe.cuh) for batch 129..256: 0 off, 1 on, 2 auto (on outside
     // softmax exit / T5 mode); attention CTAs of its grid (the rest run the projection GEMMs)
-    int use_pipe = 2, pipe_att = 92;
+    int use_pipe = 2, pipe_att = 100;  // attention CTAs of the pipelined kernel (the rest run GEMMs)
     bool pipe_for(int B) const {
         if (use_pipe == 0 || B <= 128 || B > 256 || cfg.encoder_len > 0 || cfg.technique == EL_TECH_SOFTMAX) return false;
         return true;
@@ -244,7 +244,8 @@ struct el_engine {
         opt_mega_bm_max = 256, opt_attn_dyn_permille = 0, opt_attn_dyn_cb = 4, opt_mega_bm_prefetch = 1,
         opt_mega_bm_chunk_kb = 0, opt_mega_bm_act_policy = 0, opt_mega_bm_nt_min = 16,
         opt_mega_bm_m128 = 0, opt_mega_bm_down = 0, opt_mega_att_l2 = 0, opt_mega_down_splits = 0,
-        opt_mega_splits_cap = 0, opt_mega_fused_reduce = 1, opt_att_mbuf = 1, opt_mega_att_l2_late = 0, opt_mega_att_early = 1, opt_attn_seg_cost = -1;
+        opt_mega_splits_cap = 0, opt_mega_fused_reduce = 1, opt_att_mbuf = 1, opt_mega_att_l2_late = 0, opt_mega_att_early = 1, opt_attn_seg_cost = -1,
+        opt_attn_grid = 0;
     int attn_cb = 1, attn_stages = 2, attn_max_chunks = 1, attn_grid = 148;
     int NR = 16;
 
@@ -520,6 +521,7 @@ struct el_engine {
         int sms = 148;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
         attn_grid = sms * el::attn_ctas_per_sm(dm, attn_stages);
+        if (opt_attn_grid > 0) attn_grid = std::min(attn_grid, opt_attn_grid);  // probe: fewer CTAs
         attn_o.alloc((size_t)std::max(B, kPfRows) * attn_max_chunks * dm.dp, false);
         attn_ml.alloc((size_t)std::max(B, kPfRows) * attn_max_chunks * 2, false);
         invalidate_graphs();
@@ -660,8 +662,10 @@ struct el_engine {
                 int nt = k == el::kIDown ? 16 : opt_mega_bm_nt_min;
                 if (pipe_grid) {
                     // the fewest waves over the GEMM CTAs, then the smallest N (multiple of 16 dividing
-                    // F) with a unit weight slab of at most 96 KB
-                    const int max_nt = std::max(16, std::min(128, (96 * 1024) / (x.kb_total * 128) / 16 * 16));
+                    // F) with a unit weight slab of at most 128 KB (c5: nt 64 / 32 / 64 for QKV / W_o /
+                    // up -- QKV in one wave of 48 units -- with 100 attention CTAs: -5.2 % iteration
+                    // time vs 96 KB slabs and 92 attention CTAs, scripts/_call13.sh)
+                    const int max_nt = std::max(16, std::min(128, (128 * 1024) / (x.kb_total * 128) / 16 * 16));
                     int best = 16, best_w = 1 << 30;
                     for (int c = 16; c <= max_nt; c += 16) {
                         if (F % c) continue;
@@ -1933,6 +1937,10 @@ int el_engine_set_option(el_engine* e, const char* key, int64_t v) {
     else if (!std::strcmp(key, "attn_cb") || !std::strcmp(key, "attn_stages")) {
         if (v < 0 || v > 8) fail(EL_INVALID_ARGUMENT, "%s must be in [0 (auto), 8]", key);
         (key[5] == 'c' ? e->opt_attn_cb : e->opt_attn_stages) = (int)v;
+        e->plan_attention();
+    } else if (!std::strcmp(key, "attn_grid")) {  // standalone attention kernel on at most v CTAs (0 = all)
+        if (v < 0) fail(EL_INVALID_ARGUMENT, "attn_grid must be >= 0");
+        e->opt_attn_grid = (int)v;
         e->plan_attention();
     } else if (!std::strcmp(key, "nsplit") || !std::strcmp(key, "cta_target")) {
         if (v < 1) fail(EL_INVALID_ARGUMENT, "value must be >= 1");

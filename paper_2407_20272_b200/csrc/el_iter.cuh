@@ -198,31 +198,36 @@ __device__ __forceinline__ void unit_mainloop(IterSmem& sm, uint8_t* ring, const
     // single-thread issue loops: stage index / phase / addresses are strength-reduced (no div/mod per
     // k-block -- a lone thread cannot hide the latency of that arithmetic)
     if (warp == kProducerWarp) {
-        if (lane == 0) {
-            uint32_t s = kseq % r.stages, ph = (kseq / r.stages) & 1;
-            bool wrapped = kseq >= r.stages;
-            const uint32_t ring0 = smem_u32(ring), full0 = smem_u32(r.full), empty0 = smem_u32(r.empty);
-            const uint8_t* ap = reinterpret_cast<const uint8_t*>(a_src + (size_t)kb0 * a_kstride);
-            const uint8_t* bp = reinterpret_cast<const uint8_t*>(b_src + (size_t)kb0 * b_kstride);
-            const size_t ast = a_kstride * 2, bst = b_kstride * 2;
-            const uint32_t tx = a_bytes + b_bytes;
+        // lane 0 drives the ring; the two copies of ring slot s are issued by lanes 1 + 2 (s % 15) and
+        // 2 + 2 (s % 15): one thread's bulk copies are processed one after another (~0.4 us each,
+        // scripts/ingest_probe*.cu), copies of different lanes overlap
+        uint32_t s = kseq % r.stages, ph = (kseq / r.stages) & 1;
+        bool wrapped = kseq >= r.stages;
+        const uint32_t ring0 = smem_u32(ring), full0 = smem_u32(r.full), empty0 = smem_u32(r.empty);
+        const uint8_t* ap = reinterpret_cast<const uint8_t*>(a_src + (size_t)kb0 * a_kstride);
+        const uint8_t* bp = reinterpret_cast<const uint8_t*>(b_src + (size_t)kb0 * b_kstride);
+        const size_t ast = a_kstride * 2, bst = b_kstride * 2;
+        const uint32_t tx = a_bytes + b_bytes;
 #pragma unroll 1
-            for (int i = 0; i < nkb; ++i) {
+        for (int i = 0; i < nkb; ++i) {
+            const uint32_t fb = full0 + 8 * s, sb = ring0 + s * r.stride;
+            if (lane == 0) {
                 if (wrapped) mbar_wait_addr(empty0 + 8 * s, ph ^ 1);
-                const uint32_t fb = full0 + 8 * s, sb = ring0 + s * r.stride;
                 asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(fb), "r"(tx) : "memory");
-                bulk_load_hint(sb, ap, a_bytes, fb, a_policy);
-                bulk_load_hint(sb + r.b_off, bp, b_bytes, fb, b_policy);
-                ap += ast;
-                bp += bst;
-                if (++s == r.stages) {
-                    s = 0;
-                    ph ^= 1;
-                    wrapped = true;
-                }
             }
-            if (dbg & 64) sm.tdbg[3] = clock64();
+            __syncwarp();
+            const int il = 1 + 2 * (int)(s % 15u);
+            if (lane == il) bulk_load_hint(sb, ap, a_bytes, fb, a_policy);
+            else if (lane == il + 1) bulk_load_hint(sb + r.b_off, bp, b_bytes, fb, b_policy);
+            ap += ast;
+            bp += bst;
+            if (++s == r.stages) {
+                s = 0;
+                ph ^= 1;
+                wrapped = true;
+            }
         }
+        if (lane == 0 && (dbg & 64)) sm.tdbg[3] = clock64();
     } else if (warp == 0) {
         {  // whole warp 0, one elected lane issues (uniform descriptors)
             const uint32_t idesc = idesc_bf16_m128(n_mma);
@@ -799,38 +804,45 @@ __device__ __forceinline__ void unit_bm(IterSmem& sm, uint8_t* ring, const IterP
     const int nch = (kb_total + p.bm_kc - 1) / p.bm_kc;
     const uint32_t ring0 = smem_u32(ring), wbase = ring0 + (uint32_t)p.bm_woff;
     if (warp == kProducerWarp) {
-        if (lane == 0) {
-            if (!w_ready) {  // (else: prefetched into the weight buffer one phase ahead by bm_prefetch)
-                const uint32_t wf = smem_u32(&sm.wfull);
-                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(wf),
-                             "r"((uint32_t)(nt * 128 * kb_total))
-                             : "memory");
-                tma_load_3d(wbase, wmap, wf, wx, wy, wz, kL2EvictFirst);
-            }
-            sm.tdbg[4] = clock64();  // producer starts issuing
-            uint32_t s = cseq % (uint32_t)p.bm_stages, ph = (cseq / (uint32_t)p.bm_stages) & 1;
-            bool wrapped = cseq >= (uint32_t)p.bm_stages;
-            const uint32_t full0 = smem_u32(sm.full2), empty0 = smem_u32(sm.empty2);
+        if (lane == 0 && !w_ready) {  // (else: prefetched into the weight buffer one phase ahead by bm_prefetch)
+            const uint32_t wf = smem_u32(&sm.wfull);
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(wf),
+                         "r"((uint32_t)(nt * 128 * kb_total))
+                         : "memory");
+            tma_load_3d(wbase, wmap, wf, wx, wy, wz, kL2EvictFirst);
+        }
+        if (lane == 0) sm.tdbg[4] = clock64();  // producer starts issuing
+        // lane 0 drives the ring; the activation copies go out from lanes 1..31 in turn (one
+        // thread's bulk copies are processed one after another: scripts/ingest_probe*.cu)
+        uint32_t s = cseq % (uint32_t)p.bm_stages, ph = (cseq / (uint32_t)p.bm_stages) & 1;
+        bool wrapped = cseq >= (uint32_t)p.bm_stages;
+        const uint32_t full0 = smem_u32(sm.full2), empty0 = smem_u32(sm.empty2);
+        const uint64_t pol = (p.bm_act_policy & 1) ? kL2EvictFirst : kL2EvictLast;
+        int issued = 0;  // copies so far (their lane rotates)
 #pragma unroll 1
-            for (int c = 0; c < nch; ++c) {
-                const int kc = min(p.bm_kc, kb_total - c * p.bm_kc);
+        for (int c = 0; c < nch; ++c) {
+            const int kc = min(p.bm_kc, kb_total - c * p.bm_kc);
+            const uint32_t fb = full0 + 8 * s, bytes = (uint32_t)kc * NRb;
+            if (lane == 0) {
                 if (wrapped) mbar_wait_addr(empty0 + 8 * s, ph ^ 1);
-                const uint32_t fb = full0 + 8 * s, bytes = (uint32_t)kc * NRb;
                 asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(fb), "r"(bytes) : "memory");
-                const uint64_t pol = (p.bm_act_policy & 1) ? kL2EvictFirst : kL2EvictLast;
-                if (!grouped) {
+            }
+            __syncwarp();
+            if (!grouped) {
+                if (lane == 1 + issued % 31)
                     bulk_load_hint(ring0 + s * (uint32_t)p.bm_astage, act + (size_t)c * p.bm_kc * p.bm_rows * kBK,
                                    bytes, fb, pol);
-                } else {
-                    for (int j = 0; j < kc; ++j)
+                ++issued;
+            } else {
+                for (int j = 0; j < kc; ++j, ++issued)
+                    if (lane == 1 + issued % 31)
                         bulk_load_hint(ring0 + s * (uint32_t)p.bm_astage + (uint32_t)j * NRb,
                                        act + (size_t)(c * p.bm_kc + j) * p.bm_rows * kBK, NRb, fb, pol);
-                }
-                if (++s == (uint32_t)p.bm_stages) {
-                    s = 0;
-                    ph ^= 1;
-                    wrapped = true;
-                }
+            }
+            if (++s == (uint32_t)p.bm_stages) {
+                s = 0;
+                ph ^= 1;
+                wrapped = true;
             }
         }
     } else if (warp == 0) {

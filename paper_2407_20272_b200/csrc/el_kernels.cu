@@ -422,34 +422,43 @@ __global__ void __launch_bounds__(128, 1)
     const uint32_t tmem = *tmem_slot;
     stamp(1);
 
-    if (warp == 0 && lane == 0) {
-        // ---- TMA producer ----
+    if (warp == 0) {
+        // ---- TMA producer: lane 0 drives the ring, the copies of ring slot s are issued by lanes
+        //      1 + 2 (s % 15) and 2 + 2 (s % 15) (one thread's bulk copies run one after another) ----
         const int pre = min(nkb, g.stages);
         // weights: one contiguous 16 KB bulk copy per 128x64 tile (stored pre-swizzled)
         const uint16_t* a_tiles = g.A + (size_t)(a_row / kBM) * g.kb_total * (kBM * kBK);
-        for (int kb = 0; kb < pre; ++kb) {  // weights first: independent of the previous kernel
-            mbar_arrive_expect_tx(&full[kb], kAStage + b_stage);
-            bulk_load(sA + (size_t)kb * kAStage, a_tiles + (size_t)(kb0 + kb) * (kBM * kBK), kAStage, &full[kb]);
-        }
+        if (lane == 0)
+            for (int kb = 0; kb < pre; ++kb) mbar_arrive_expect_tx(&full[kb], kAStage + b_stage);
+        __syncwarp();
+        for (int kb = 0; kb < pre; ++kb)  // weights first: independent of the previous kernel
+            if (lane == 1 + 2 * (kb % 15))
+                bulk_load(sA + (size_t)kb * kAStage, a_tiles + (size_t)(kb0 + kb) * (kBM * kBK), kAStage, &full[kb]);
         // activations: the first n_pad rows of a k-block tile are contiguous
         const uint16_t* b_tiles = g.Bp + (size_t)b_row * g.b_par_stride;
         const size_t b_kstride = (size_t)g.NR * kBK;
         pdl_wait();  // no-op unless launched as a PDL secondary
         for (int kb = 0; kb < pre; ++kb)
-            bulk_load(sB + (size_t)kb * b_stage, b_tiles + (size_t)(kb0 + kb) * b_kstride + (size_t)n0 * kBK, b_stage,
-                      &full[kb]);
+            if (lane == 2 + 2 * (kb % 15))
+                bulk_load(sB + (size_t)kb * b_stage, b_tiles + (size_t)(kb0 + kb) * b_kstride + (size_t)n0 * kBK,
+                          b_stage, &full[kb]);
         for (int kb = pre; kb < nkb; ++kb) {
             const int s = kb % g.stages;
-            mbar_wait(&empty[s], ((kb / g.stages) - 1) & 1);
-            if ((EL_DBG(st) & 16) && blockIdx.x == 0 && blockIdx.y == 0 && kb < 64) {
-                unsigned long long t;
-                asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-                st.dbg_ts[4096 + 64 + kb] = t;
+            if (lane == 0) {
+                mbar_wait(&empty[s], ((kb / g.stages) - 1) & 1);
+                if ((EL_DBG(st) & 16) && blockIdx.x == 0 && blockIdx.y == 0 && kb < 64) {
+                    unsigned long long t;
+                    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+                    st.dbg_ts[4096 + 64 + kb] = t;
+                }
+                mbar_arrive_expect_tx(&full[s], kAStage + b_stage);
             }
-            mbar_arrive_expect_tx(&full[s], kAStage + b_stage);
-            bulk_load(sA + (size_t)s * kAStage, a_tiles + (size_t)(kb0 + kb) * (kBM * kBK), kAStage, &full[s]);
-            bulk_load(sB + (size_t)s * b_stage, b_tiles + (size_t)(kb0 + kb) * b_kstride + (size_t)n0 * kBK, b_stage,
-                      &full[s]);
+            __syncwarp();
+            if (lane == 1 + 2 * (s % 15))
+                bulk_load(sA + (size_t)s * kAStage, a_tiles + (size_t)(kb0 + kb) * (kBM * kBK), kAStage, &full[s]);
+            else if (lane == 2 + 2 * (s % 15))
+                bulk_load(sB + (size_t)s * b_stage, b_tiles + (size_t)(kb0 + kb) * b_kstride + (size_t)n0 * kBK,
+                          b_stage, &full[s]);
         }
     } else if (warp == 1 && lane == 0) {
         // ---- MMA issuer (single thread) ----
@@ -1028,6 +1037,8 @@ __device__ __forceinline__ void attn_body(const DevState& st, AttnSmem& a, uint8
                 for (int u = 0; u < nb; ++u, ++seq) {
                     const int id = __shfl_sync(0xffffffffu, my_id, u);
                     const int blk = blk_base + u;
+                    // 0: nothing for the issue lanes; bit 0: K|V of this block; bit 1: q too
+                    int xgo = 0;
                     if (lane == 0) {
                         const int s = seq % S;
                         if (seq == seq0) EL_ATT_CLK(8);
@@ -1056,15 +1067,30 @@ __device__ __forceinline__ void attn_body(const DevState& st, AttnSmem& a, uint8
                                 did = id;
                                 dbytes = bytes;
                             } else {
-                                bulk_load_ef(sbuf, src.kpool + (size_t)id * dm.bc * dp, bytes, &a.full[s]);
-                                bulk_load_ef(sbuf + blk_bytes, src.vpool + (size_t)id * dm.bc * dp, bytes, &a.full[s]);
+                                xgo = 1;
                             }
                         } else {
-                            if (first)
-                                bulk_load(sbuf + 2 * blk_bytes, st.q32 + (size_t)b * dp, (uint32_t)dp * 4, &a.full[s]);
-                            bulk_load_ef(sbuf, src.kpool + (size_t)id * dm.bc * dp, bytes, &a.full[s]);
-                            bulk_load_ef(sbuf + blk_bytes, src.vpool + (size_t)id * dm.bc * dp, bytes, &a.full[s]);
+                            xgo = first ? 3 : 1;
                         }
+                    }
+                    // The block's copies are issued by lanes other than 0, a different lane triple per
+                    // ring slot: one thread's bulk copies are processed one after another (~0.4 us each
+                    // from L2 / HBM whatever their size, scripts/ingest_probe*.cu), so a lone issuing
+                    // lane caps a CTA at ~80 GB/s; copies of different lanes overlap.
+                    xgo = __shfl_sync(0xffffffffu, xgo, 0);
+                    __syncwarp();  // (orders lane 0's empty-slot acquire before the other lanes' copies)
+                    if (xgo) {
+                        const int il = 1 + 3 * (seq % 10);  // lanes 1..30
+                        const int s = seq % S;
+                        const uint32_t sb = smem_u32(stages + (size_t)s * stage_bytes), fb = smem_u32(&a.full[s]);
+                        const uint32_t bytes = (uint32_t)min(dm.bc, ctx - blk * dm.bc) * dp * 2;
+                        if (lane == il)
+                            bulk_load_hint(sb, src.kpool + (size_t)id * dm.bc * dp, bytes, fb, kL2EvictFirst);
+                        else if (lane == il + 1)
+                            bulk_load_hint(sb + blk_bytes, src.vpool + (size_t)id * dm.bc * dp, bytes, fb, kL2EvictFirst);
+                        else if (lane == il + 2 && (xgo & 2))
+                            bulk_load(stages + (size_t)s * stage_bytes + 2 * blk_bytes, st.q32 + (size_t)b * dp,
+                                      (uint32_t)dp * 4, &a.full[s]);
                     }
                 }
                 __syncwarp();
