@@ -253,7 +253,11 @@ def _engine(c, tech, lam, gamma, B, cap, args, rank, stub):
     cfg = X.EngineConfig(model=X.ModelConfig(L, d, V, 0, encoder_len=c.get("enc", 0)), technique=X.ExitTechnique(tech),
                          schedule=X.ThresholdSchedule(lam, gamma, 0.0), max_batch=B,
                          pool_blocks=B * L * (-(-cap // 16)), eos_token=-1)
-    return X.Engine(cfg, graph=not args.eager, mega=False if args.no_mega else (True if args.mega else None))
+    e = X.Engine(cfg, graph=not args.eager, mega=False if args.no_mega else (True if args.mega else None))
+    for kv in args.opt:  # engine tuning options (A/B runs), key=value
+        k, v = kv.split("=")
+        e.set_option(k, int(v))
+    return e
 
 
 def _timed_session(eng, first, ids, prefix, cap, args, barrier, max_over_ranks):
@@ -656,6 +660,7 @@ def main():
     ap.add_argument("--config", default="c5", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--opt", action="append", default=[], help="engine option key=value (A/B runs; repeatable)")
     ap.add_argument("--no-c4", action="store_true", help="skip the configs[3] comparison (c5 only)")
     ap.add_argument("--no-layer-level", action="store_true", help="skip the layer-level scheduling leg")
     ap.add_argument("--no-engine-run", action="store_true", help="skip the Engine::run (real prefill) leg")

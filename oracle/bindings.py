@@ -498,6 +498,8 @@ class Port(_Lib):
         L.eo_session_step.argtypes = [C.c_void_p, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_int32),
                                       C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.POINTER(C.c_double),
                                       C.POINTER(C.c_double)]
+        # (a handle passed without argtypes would be truncated to a C int)
+        L.eo_session_set_per_seq_exit.argtypes = [C.c_void_p, C.c_int]
         L.eo_round_bf16.restype = C.c_double
         L.eo_round_bf16.argtypes = [C.c_double]
         L.eo_splitmix64_at.restype = C.c_uint64

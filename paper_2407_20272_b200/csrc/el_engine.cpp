@@ -245,7 +245,7 @@ struct el_engine {
         opt_mega_bm_chunk_kb = 0, opt_mega_bm_act_policy = 0, opt_mega_bm_nt_min = 16,
         opt_mega_bm_m128 = 0, opt_mega_bm_down = 0, opt_mega_att_l2 = 0, opt_mega_down_splits = 0,
         opt_mega_splits_cap = 0, opt_mega_fused_reduce = 1, opt_att_mbuf = 1, opt_mega_att_l2_late = 0, opt_mega_att_early = 1, opt_attn_seg_cost = -1,
-        opt_attn_grid = 0;
+        opt_attn_grid = 0, opt_mega_bm_wstream = -1;
     int attn_cb = 1, attn_stages = 2, attn_max_chunks = 1, attn_grid = 148;
     int NR = 16;
 
@@ -649,12 +649,16 @@ struct el_engine {
         P.n_pad = n_pad;
         // batch-M full-K GEMMs (no split-K reduce phase) for QKV / W_o / up at small batch
         int nt_max = 16, bm_w = 0;  // bm_w: the largest unit weight slab (nt rows x K)
+        // streamed batch-M weights (auto: the pipelined kernel)
+        const bool wstream = opt_mega_bm_wstream < 0 ? pipe_grid > 0 : opt_mega_bm_wstream != 0;
         // batch > 128: units cover 128-row groups of an activation layout with 128-row multiples
         const bool bm = n_pad <= opt_mega_bm_max && (n_pad <= 128 || NR % 128 == 0);
         if (bm) {
             for (int k : {el::kIQkv, el::kIWo, el::kIUp, el::kIQc, el::kIWoc, el::kIDown}) {
-                // down (K = 4d): batch-M only at batch <= 64, where its 16-row weight slab fits
-                if (k == el::kIDown && (n_pad > 64 || !opt_mega_bm_down)) continue;
+                // down (K = 4d): batch-M only at batch <= 64, where its 16-row weight slab fits (the
+                // pipelined kernel's down stays split-K: a batch-M down with streamed weights, 1 MB of
+                // activations per full-K unit, measured +21 % iteration time at c5)
+                if (k == el::kIDown && (n_pad > 64 || !opt_mega_bm_down || pipe_grid)) continue;
                 el::IterGemm& x = P.g[k];
                 const int F = x.m_tiles * 128;
                 // row groups of 128 batch rows (the pipelined kernel runs one group per phase)
@@ -665,10 +669,11 @@ struct el_engine {
                     // F) with a unit weight slab of at most 128 KB (c5: nt 64 / 32 / 64 for QKV / W_o /
                     // up -- QKV in one wave of 48 units -- with 100 attention CTAs: -5.2 % iteration
                     // time vs 96 KB slabs and 92 attention CTAs, scripts/_call13.sh)
-                    const int max_nt = std::max(16, std::min(128, (128 * 1024) / (x.kb_total * 128) / 16 * 16));
+                    const int max_nt = wstream ? 128 : std::max(16, std::min(128, (128 * 1024) / (x.kb_total * 128) / 16 * 16));
                     int best = 16, best_w = 1 << 30;
                     for (int c = 16; c <= max_nt; c += 16) {
                         if (F % c) continue;
+                        if (128 % c) continue;  // a unit's rows stay inside one 128-row weight tile
                         const int w = ceil_div(F / c, ggrid);
                         if (w < best_w) { best_w = w; best = c; }
                     }
@@ -678,7 +683,8 @@ struct el_engine {
                 }
                 x.mode = 1;
                 x.nt = nt;
-                bm_w = std::max(bm_w, x.kb_total * nt * 128);
+                nt_max = std::max(nt_max, nt);
+                if (!wstream) bm_w = std::max(bm_w, x.kb_total * nt * 128);
             }
         }
         const int stage = 128 * 64 * 2 + n_pad * 128;
@@ -700,13 +706,14 @@ struct el_engine {
         P.att_early = opt_mega_att_early;
         P.fused_reduce = opt_mega_fused_reduce;
         P.tcnt = mtcnt.p;
-        P.bm_astage = P.bm_kc * P.bm_grp * 128;
-        (void)nt_max;
+        P.bm_wstream = (bm && wstream) ? 1 : 0;
+        // a stage: bm_kc activation k-blocks (+ with streamed weights bm_kc weight k-blocks of nt_max rows)
+        P.bm_astage = P.bm_kc * (P.bm_grp + (P.bm_wstream ? nt_max : 0)) * 128;
         P.bm_woff = (cap - bm_w) / 1024 * 1024;
-        P.bm_stages = std::max(2, std::min(4, (P.bm_woff - 16384) / P.bm_astage));
+        P.bm_stages = std::max(2, std::min(P.bm_wstream ? 6 : 4, (P.bm_woff - 16384) / P.bm_astage));
         if (bm && P.bm_stages * P.bm_astage > P.bm_woff)
             fail(EL_INVALID_ARGUMENT, "persistent kernel: batch-M ring does not fit");
-        P.bm_prefetch = (bm && opt_mega_bm_prefetch && ring_att <= P.bm_woff) ? 1 : 0;
+        P.bm_prefetch = (bm && !P.bm_wstream && opt_mega_bm_prefetch && ring_att <= P.bm_woff) ? 1 : 0;
         // weight-streaming ring + transpose buffer stay below the weight buffer when weights are
         // prefetched into it during other phases
         const int ws_cap = (bm && P.bm_prefetch) ? P.bm_woff : cap;
@@ -736,7 +743,7 @@ struct el_engine {
         el::IterMaps MM{};
         for (int k : {el::kIQkv, el::kIWo, el::kIUp, el::kIQc, el::kIWoc, el::kIDown}) {
             const el::IterGemm& x = P.g[k];
-            if (!x.mode || !x.A) continue;
+            if (!x.mode || !x.A || P.bm_wstream) continue;  // (streamed weights: 1-D copies, no tensor map)
             MM.w[k] = make_bm_map(x.A, (size_t)L * x.layer_rows * x.kb_total, x.nt, x.kb_total);
         }
         mmaps[key] = MM;
@@ -1938,6 +1945,10 @@ int el_engine_set_option(el_engine* e, const char* key, int64_t v) {
         if (v < 0 || v > 8) fail(EL_INVALID_ARGUMENT, "%s must be in [0 (auto), 8]", key);
         (key[5] == 'c' ? e->opt_attn_cb : e->opt_attn_stages) = (int)v;
         e->plan_attention();
+    } else if (!std::strcmp(key, "mega_bm_wstream")) {  // -1 auto (pipelined kernel), 0 off, 1 on
+        if (v < -1 || v > 1) fail(EL_INVALID_ARGUMENT, "mega_bm_wstream must be -1, 0 or 1");
+        e->opt_mega_bm_wstream = (int)v;
+        e->mplans.clear();
     } else if (!std::strcmp(key, "attn_grid")) {  // standalone attention kernel on at most v CTAs (0 = all)
         if (v < 0) fail(EL_INVALID_ARGUMENT, "attn_grid must be >= 0");
         e->opt_attn_grid = (int)v;

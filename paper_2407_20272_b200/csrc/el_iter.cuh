@@ -794,8 +794,16 @@ __device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map
 // (the caller advances cseq by the chunk count and wseq by 1)
 __device__ __forceinline__ void unit_bm(IterSmem& sm, uint8_t* ring, const IterPlan& p, const uint32_t cseq,
                                      const uint32_t wseq, const CUtensorMap* wmap, int wx, int wy, int wz,
-                                     const uint16_t* act, int kb_total, int nt, uint32_t useq, bool w_ready) {
+                                     const uint16_t* act, int kb_total, int nt, uint32_t useq, bool w_ready,
+                                     const uint16_t* wsrc) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // p.bm_wstream: the weights stream through the ring next to the activations (stage = bm_kc act
+    // k-blocks, then bm_kc weight k-blocks of nt rows = nt * 128 bytes each, copied from the
+    // pre-swizzled tiles at wsrc + kb * 128 x 64), L2-prefetched one phase ahead by bm_prefetch:
+    // no resident weight slab, so the ring holds more bytes in flight (a CTA's L2 stream is
+    // bounded by bytes in flight / L2 latency under the attention CTAs' HBM load)
+    const bool ws = p.bm_wstream != 0;
+    const uint32_t wrow = (uint32_t)nt * 128u, wst = (uint32_t)p.bm_kc * (uint32_t)p.bm_grp * 128u;
     // act: this unit's row group (rows r*bm_grp ..) of k-block 0; one k-block of it is
     // NRb bytes in shared memory; with several row groups a k-block's group is not
     // contiguous with the next k-block's in global memory (stride bm_rows rows)
@@ -804,7 +812,7 @@ __device__ __forceinline__ void unit_bm(IterSmem& sm, uint8_t* ring, const IterP
     const int nch = (kb_total + p.bm_kc - 1) / p.bm_kc;
     const uint32_t ring0 = smem_u32(ring), wbase = ring0 + (uint32_t)p.bm_woff;
     if (warp == kProducerWarp) {
-        if (lane == 0 && !w_ready) {  // (else: prefetched into the weight buffer one phase ahead by bm_prefetch)
+        if (lane == 0 && !w_ready && !ws) {  // (else: prefetched into the weight buffer one phase ahead by bm_prefetch)
             const uint32_t wf = smem_u32(&sm.wfull);
             asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(wf),
                          "r"((uint32_t)(nt * 128 * kb_total))
@@ -825,9 +833,16 @@ __device__ __forceinline__ void unit_bm(IterSmem& sm, uint8_t* ring, const IterP
             const uint32_t fb = full0 + 8 * s, bytes = (uint32_t)kc * NRb;
             if (lane == 0) {
                 if (wrapped) mbar_wait_addr(empty0 + 8 * s, ph ^ 1);
-                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(fb), "r"(bytes) : "memory");
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(fb),
+                             "r"(bytes + (ws ? (uint32_t)kc * wrow : 0u))
+                             : "memory");
             }
             __syncwarp();
+            if (ws)
+                for (int j = 0; j < kc; ++j, ++issued)
+                    if (lane == 1 + issued % 31)
+                        bulk_load_hint(ring0 + s * (uint32_t)p.bm_astage + wst + (uint32_t)j * wrow,
+                                       wsrc + (size_t)(c * p.bm_kc + j) * (kBM * kBK), wrow, fb, kL2EvictFirst);
             if (!grouped) {
                 if (lane == 1 + issued % 31)
                     bulk_load_hint(ring0 + s * (uint32_t)p.bm_astage, act + (size_t)c * p.bm_kc * p.bm_rows * kBK,
@@ -849,7 +864,7 @@ __device__ __forceinline__ void unit_bm(IterSmem& sm, uint8_t* ring, const IterP
         {  // whole warp 0, one elected lane issues (uniform descriptors)
             // M = 64 when the batch fits (half the A-operand shared-memory reads of M = 128)
             const uint32_t idesc = idesc_bf16((uint32_t)p.bm_m, (uint32_t)nt);
-            mbar_wait_addr(smem_u32(&sm.wfull), wseq & 1);
+            if (!ws) mbar_wait_addr(smem_u32(&sm.wfull), wseq & 1);
             if (lane == 0) {
                 sm.tdbg[3] = clock64();
             }
@@ -869,7 +884,8 @@ __device__ __forceinline__ void unit_bm(IterSmem& sm, uint8_t* ring, const IterP
                     if (p.bm_act_policy & 2) continue;  // timing probe: no MMAs (wrong results)
                     // rows >= n_pad of the A tile read the next k-block / stage / weights: ignored output rows
                     const uint64_t ad = sdesc_k_sw128(ring0 + s * (uint32_t)p.bm_astage + (uint32_t)j * NRb);
-                    const uint64_t bd = sdesc_k_sw128(wbase + (uint32_t)(kb * nt * 128));
+                    const uint64_t bd = sdesc_k_sw128(ws ? ring0 + s * (uint32_t)p.bm_astage + wst + (uint32_t)j * wrow
+                                                         : wbase + (uint32_t)(kb * nt * 128));
 #pragma unroll
                     for (int k = 0; k < kBK / 16; ++k)
                         tc_mma_bf16_warp(sm.tmem, ad + (uint64_t)(2 * k), bd + (uint64_t)(2 * k), idesc, (kb | k) != 0);
@@ -898,8 +914,21 @@ __device__ __forceinline__ void unit_bm(IterSmem& sm, uint8_t* ring, const IterP
 // producer lane; weights never depend on the previous phase, so their HBM latency
 // overlaps the phase in flight and the grid barrier.  Returns whether it issued.
 __device__ __forceinline__ bool bm_prefetch(IterSmem& sm, uint8_t* ring, const IterPlan& p, const IterMaps& maps,
-                                            int gid, int layer, int ci = -1, int rg_only = -1) {
+                                            int gid, int layer, int ci = -1, int rg_only = -1, int cn = -1) {
     const IterGemm& g = p.g[gid];
+    if (g.mode && p.bm_wstream) {  // streamed weights: this CTA's units of the phase -> L2 (no completion)
+        const int CI = ci < 0 ? (int)blockIdx.x : ci, CN = cn < 0 ? (int)gridDim.x : cn;
+        const int R = rg_only >= 0 ? 1 : p.bm_rows / p.bm_grp;
+        const int U = g.m_tiles * kBM / g.nt * R;
+        for (int u = CI; u < U; u += CN) {
+            const int f0 = (u / R) * g.nt;
+            const int row_block = (layer - 1) * g.layer_rows + g.row_off + f0 / kBM;
+            const uint16_t* w = g.A + (size_t)row_block * g.kb_total * (kBM * kBK) + (size_t)(f0 % kBM) * kBK;
+            for (int kb = 0; kb < g.kb_total; ++kb)
+                l2_prefetch_bulk(w + (size_t)kb * (kBM * kBK), (uint32_t)g.nt * 128u);
+        }
+        return false;
+    }
     if (!g.mode || !p.bm_prefetch) return false;
     const int CI = ci < 0 ? (int)blockIdx.x : ci;
     // this CTA's first unit: (feature group CI / R, row group CI % R); one row group: feature group CI
@@ -938,7 +967,8 @@ __device__ __forceinline__ void gemm_phase_t(const DevState& st, IterSmem& sm, u
         const int f0 = (u / R) * g.nt, rg = rg_only >= 0 ? rg_only : u % R;
         const int row_block = (x.layer - 1) * g.layer_rows + g.row_off + f0 / kBM;
         unit_bm(sm, ring, p, cseq, wseq, &maps.w[gid], 0, f0 % kBM, row_block * g.kb_total,
-                act + (size_t)rg * p.bm_grp * kBK, g.kb_total, g.nt, useq, wpf);
+                act + (size_t)rg * p.bm_grp * kBK, g.kb_total, g.nt, useq, wpf,
+                g.A + (size_t)row_block * g.kb_total * (kBM * kBK) + (size_t)(f0 % kBM) * kBK);
         cseq += (uint32_t)((g.kb_total + p.bm_kc - 1) / p.bm_kc);
         ++wseq;
         wpf = false;
@@ -964,7 +994,7 @@ __device__ __forceinline__ void gemm_phase_t(const DevState& st, IterSmem& sm, u
     }
     // this phase's MMAs are done: the weight buffer is free for the next batch-M GEMM's weights
     if (next_gid >= 0 && threadIdx.x == kProducerWarp * 32)
-        wpf = bm_prefetch(sm, ring, p, maps, next_gid, next_layer, ci, next_rg);
+        wpf = bm_prefetch(sm, ring, p, maps, next_gid, next_layer, ci, next_rg, cn);
 }
 
 // Split-K GEMM phase with the reduction fused per output tile: every unit's CTA

@@ -235,6 +235,7 @@ struct IterPlan {
     // batch rows per k-block), the unit's weights at bm_woff
     int bm_rows, bm_kc, bm_astage, bm_stages, bm_woff;
     int bm_prefetch;  // issue each batch-M unit's weights one phase ahead (weight buffer outside the rings)
+    int bm_wstream;   // batch-M weights streamed through the ring (L2-prefetched a phase ahead), no weight slab
     int bm_act_policy;  // L2 hint of the activation copies: 0 evict-last, 1 evict-first (probe)
     int bm_m;           // UMMA M of the batch-M GEMMs: 64 (batch <= 64) or 128
     int bm_grp;         // batch rows per unit (row group): bm_rows, or 128 when the batch has 2 groups

@@ -194,7 +194,7 @@ __global__ void __launch_bounds__(kIterThreads, 1) pipe_kernel(const __grid_cons
             for (int h = 0; h < 2; ++h) {
                 const int r0 = h ? H1 : 0;
                 // the weights of this W_o unit stream in while the attention of half h finishes
-                if (tid == kProducerWarp * 32 && !wpf) wpf = bm_prefetch(sm, ring, p, maps, kIWo, layer, gi, h);
+                if (tid == kProducerWarp * 32 && !wpf) wpf = bm_prefetch(sm, ring, p, maps, kIWo, layer, gi, h, GG);
                 if (tid == 0) pipe_wait_ge(att_cnt + 32 * h, (unsigned)GA * (unsigned)layer);
                 __syncthreads();
                 fence_proxy_async_global();
@@ -210,7 +210,7 @@ __global__ void __launch_bounds__(kIterThreads, 1) pipe_kernel(const __grid_cons
                 if (gi == 0) pipe_stamp(st, layer, h, 4);
                 // down + residual (261-270) + exit-check partial dots of these rows (split-K, fused reduce)
                 if (tid == kProducerWarp * 32 && layer < L)
-                    wpf = bm_prefetch(sm, ring, p, maps, kIQkv, layer + 1, gi, h);
+                    wpf = bm_prefetch(sm, ring, p, maps, kIQkv, layer + 1, gi, h, GG);
                 gemm_phase_fused<kIDown>(st, sm, ring, p, kIDown, x, st.up_b + (size_t)r0 * kBK, kseq, useq, hrows[h],
                                          ++down_uses, gi, GG, r0, H1);
                 group_sync(gbar, (unsigned)GG, ++gk);
