@@ -212,7 +212,7 @@ struct el_engine {
     DevBuf<float> pf_h32, pf_q32, pf_mid32;
     DevBuf<uint16_t> pf_hb, pf_att_b, pf_mid_b, pf_up_b;
     DevBuf<uint16_t> hb, att_b, mid_b, up_b;
-    DevBuf<int> attn_cnt, attn_queue, layer, out_layer, status, first_accept, accept, exit_cnt, iter_counter,
+    DevBuf<int> attn_cnt, layer, out_layer, status, first_accept, accept, exit_cnt, iter_counter,
         cur_iter, rec;
     int rec_stride = 0;
     int* rec_host = nullptr;  // pinned staging for one packed record
@@ -240,11 +240,11 @@ struct el_engine {
     DevBuf<unsigned> mbar;               // its grid barrier (arrivals, generation)
     DevBuf<unsigned> mtcnt;              // its per-tile split-K arrival counters
     int mega_grid = 0, mega_att_stages = 2, sms = 148;
-    int opt_mega_fill_splits = 0, opt_mega_att_stages = 0, opt_mega_pf = 0, opt_mega_kv_pf_mb = 0,
-        opt_mega_bm_max = 256, opt_attn_dyn_permille = 0, opt_attn_dyn_cb = 4, opt_mega_bm_prefetch = 1,
-        opt_mega_bm_chunk_kb = 0, opt_mega_bm_act_policy = 0, opt_mega_bm_nt_min = 16,
-        opt_mega_bm_m128 = 0, opt_mega_bm_down = 0, opt_mega_att_l2 = 0, opt_mega_down_splits = 0,
-        opt_mega_splits_cap = 0, opt_mega_fused_reduce = 1, opt_att_mbuf = 1, opt_mega_att_l2_late = 0, opt_mega_att_early = 1, opt_attn_seg_cost = -1,
+    int opt_mega_fill_splits = 0, opt_mega_att_stages = 0, 
+        opt_mega_bm_max = 256, opt_mega_bm_prefetch = 1,
+        opt_mega_bm_chunk_kb = 0, opt_mega_bm_nt_min = 16,
+        opt_mega_bm_m128 = 0, opt_mega_bm_down = 0, opt_mega_down_splits = 0,
+        opt_mega_splits_cap = 0, opt_att_mbuf = 1, opt_mega_att_early = 1, opt_attn_seg_cost = -1,
         opt_attn_grid = 0, opt_mega_bm_wstream = -1;
     int attn_cb = 1, attn_stages = 2, attn_max_chunks = 1, attn_grid = 148;
     int NR = 16;
@@ -431,7 +431,6 @@ struct el_engine {
         mid_b.alloc((size_t)NR * dp);
         up_b.alloc((size_t)NR * fp);
         attn_cnt.alloc((size_t)std::max(Bm, kPfRows));
-        attn_queue.alloc(4);
         lm_part.alloc((size_t)(dm.Vp / 128) * Bm);
         dbg_ts.alloc(65536 + 256 * 1024);
         exit_part.alloc((size_t)(dp / 16 + 1) * Bm * 3);  // per 128-row tile (split-K) or 16-feature slice (batch-M)
@@ -668,7 +667,7 @@ struct el_engine {
                     // the fewest waves over the GEMM CTAs, then the smallest N (multiple of 16 dividing
                     // F) with a unit weight slab of at most 128 KB (c5: nt 64 / 32 / 64 for QKV / W_o /
                     // up -- QKV in one wave of 48 units -- with 100 attention CTAs: -5.2 % iteration
-                    // time vs 96 KB slabs and 92 attention CTAs, scripts/_call13.sh)
+                    // time vs 96 KB slabs and 92 attention CTAs, scripts/pipe_sweep.py)
                     const int max_nt = wstream ? 128 : std::max(16, std::min(128, (128 * 1024) / (x.kb_total * 128) / 16 * 16));
                     int best = 16, best_w = 1 << 30;
                     for (int c = 16; c <= max_nt; c += 16) {
@@ -699,12 +698,8 @@ struct el_engine {
         P.bm_grp = n_pad > 128 ? 128 : NR;  // batch > 128: units cover one 128-row group
         P.bm_kc = std::max(1, std::min(dp / 64, (opt_mega_bm_chunk_kb ? opt_mega_bm_chunk_kb * 1024 : 32768) /
                                                      (P.bm_grp * 128)));
-        P.bm_act_policy = opt_mega_bm_act_policy;
         P.bm_m = (n_pad <= 64 && !opt_mega_bm_m128) ? 64 : 128;
-        P.att_l2_blocks = opt_mega_att_l2;
-        P.att_l2_late = opt_mega_att_l2_late;
         P.att_early = opt_mega_att_early;
-        P.fused_reduce = opt_mega_fused_reduce;
         P.tcnt = mtcnt.p;
         P.bm_wstream = (bm && wstream) ? 1 : 0;
         // a stage: bm_kc activation k-blocks (+ with streamed weights bm_kc weight k-blocks of nt_max rows)
@@ -748,10 +743,6 @@ struct el_engine {
         }
         mmaps[key] = MM;
         P.map_key = key;
-        P.pf_flags = opt_mega_pf & 1;
-        // next-layer K/V into L2: a budget of opt_mega_kv_pf_mb MB spread over the grid
-        const long long blk2 = 2LL * dm.bc * dp * 2;
-        P.kv_pf_blocks = (int)std::min<long long>(1 << 20, (long long)opt_mega_kv_pf_mb * (1 << 20) / (blk2 * mega_grid));
         return mplans.emplace(key, P).first->second;
     }
     void launch_pipe(int B) {
@@ -779,8 +770,6 @@ struct el_engine {
         el::IterPlan& P = mplan_for(B);
         el::DevState s = state(false, B);
         s.attn_stages = mega_att_stages;
-        s.attn_dyn_permille = opt_attn_dyn_permille;
-        s.attn_dyn_cb = opt_attn_dyn_cb;
         // auto: charge row starts at batch <= 64, where a row spans 2-3 CTA ranges (c2 +1.2 %);
         // at batch 128 the same cost measured -1.6 % end to end
         s.attn_seg_cost = opt_attn_seg_cost >= 0 ? opt_attn_seg_cost : (B <= 64 ? 2 : 0);
@@ -802,7 +791,7 @@ struct el_engine {
         s.attn_max_chunks = attn_max_chunks; s.attn_cb = attn_cb; s.attn_stages = attn_stages;
         s.dbg = dbg;
         s.dbg_ts = dbg_ts.p;
-        s.attn_grid = attn_grid; s.attn_queue = attn_queue.p; s.attn_done = attn_queue.p + 1;
+        s.attn_grid = attn_grid;
         s.attn_scale = (float)(1.0 / std::sqrt((double)dm.d));
         s.lm_part = lm_part.p;
         s.layer = layer.p; s.out_layer = out_layer.p; s.status = status.p; s.first_accept = first_accept.p;
@@ -1863,24 +1852,13 @@ int el_engine_set_option(el_engine* e, const char* key, int64_t v) {
         if (v < 0 || v > 2) fail(EL_INVALID_ARGUMENT, "mega must be 0 (off), 1 (on) or 2 (auto)");
         e->use_mega = (int)v;
     }
-    else if (!std::strcmp(key, "attn_dyn_permille")) {
-        if (v < 0 || v > 1000) fail(EL_INVALID_ARGUMENT, "attn_dyn_permille must be in [0, 1000]");
-        if (!EL_DEBUG && v > 0) fail(EL_INVALID_ARGUMENT, "attn_dyn_permille > 0 needs an EL_DEBUG=1 build");
-        e->opt_attn_dyn_permille = (int)v;
-    } else if (!std::strcmp(key, "attn_seg_cost")) {
+    else if (!std::strcmp(key, "attn_seg_cost")) {
         if (v < -1 || v > 64) fail(EL_INVALID_ARGUMENT, "attn_seg_cost must be in [-1 (auto), 64]");
         e->opt_attn_seg_cost = (int)v;
         e->invalidate_graphs();
-    } else if (!std::strcmp(key, "attn_dyn_cb")) {
-        if (v < 1 || v > 64) fail(EL_INVALID_ARGUMENT, "attn_dyn_cb must be in [1, 64]");
-        e->opt_attn_dyn_cb = (int)v;
-    } else if (!std::strcmp(key, "mega_bm_chunk_kb") || !std::strcmp(key, "mega_bm_act_policy")) {
-        (key[8] == 'c' ? e->opt_mega_bm_chunk_kb : e->opt_mega_bm_act_policy) = (int)v;
-        e->mplans.clear();
-    } else if (!std::strcmp(key, "mega_att_l2_late")) {
-        if (!EL_DEBUG && v != 0) fail(EL_INVALID_ARGUMENT, "L2 prefetch probes need an EL_DEBUG=1 build");
-        if (v < 0 || v > 64) fail(EL_INVALID_ARGUMENT, "mega_att_l2_late must be in [0, 64]");
-        e->opt_mega_att_l2_late = (int)v;
+    } else if (!std::strcmp(key, "mega_bm_chunk_kb")) {
+        if (v < 0 || v > 64) fail(EL_INVALID_ARGUMENT, "mega_bm_chunk_kb must be in [0 (auto), 64]");
+        e->opt_mega_bm_chunk_kb = (int)v;
         e->mplans.clear();
     } else if (!std::strcmp(key, "mega_att_early")) {
         e->opt_mega_att_early = v != 0;
@@ -1888,20 +1866,12 @@ int el_engine_set_option(el_engine* e, const char* key, int64_t v) {
     } else if (!std::strcmp(key, "att_mbuf")) {
         e->opt_att_mbuf = v != 0;
         e->mplans.clear();
-    } else if (!std::strcmp(key, "mega_fused_reduce")) {
-        if (!EL_DEBUG && v == 0) fail(EL_INVALID_ARGUMENT, "mega_fused_reduce=0 needs an EL_DEBUG=1 build");
-        e->opt_mega_fused_reduce = v != 0;
-        e->mplans.clear();
     } else if (!std::strcmp(key, "mega_splits_cap")) {
         if (v < 1) fail(EL_INVALID_ARGUMENT, "mega_splits_cap must be >= 1");
         e->opt_mega_splits_cap = (int)v;
         e->mplans.clear();
     } else if (!std::strcmp(key, "mega_down_splits")) {
         e->opt_mega_down_splits = (int)v;
-        e->mplans.clear();
-    } else if (!std::strcmp(key, "mega_att_l2")) {
-        if (!EL_DEBUG && v != 0) fail(EL_INVALID_ARGUMENT, "L2 prefetch probes need an EL_DEBUG=1 build");
-        e->opt_mega_att_l2 = (int)v;
         e->mplans.clear();
     } else if (!std::strcmp(key, "mega_bm_down")) {
         e->opt_mega_bm_down = v != 0;
@@ -1919,13 +1889,7 @@ int el_engine_set_option(el_engine* e, const char* key, int64_t v) {
     } else if (!std::strcmp(key, "mega_bm_max")) {
         e->opt_mega_bm_max = (int)v;
         e->mplans.clear();
-    } else if (!std::strcmp(key, "mega_pf") || !std::strcmp(key, "mega_kv_pf_mb")) {
-        if (!EL_DEBUG && v != 0) fail(EL_INVALID_ARGUMENT, "L2 prefetch probes need an EL_DEBUG=1 build");
-        if (v < 0 || v > 4096) fail(EL_INVALID_ARGUMENT, "value out of range");
-        (key[5] == 'k' ? e->opt_mega_kv_pf_mb : e->opt_mega_pf) = (int)v;
-        e->mplans.clear();
-    }
-    else if (!std::strcmp(key, "mega_fill_splits") || !std::strcmp(key, "mega_att_stages")) {
+    } else if (!std::strcmp(key, "mega_fill_splits") || !std::strcmp(key, "mega_att_stages")) {
         if (v < 0 || v > 16) fail(EL_INVALID_ARGUMENT, "value out of range");
         (key[5] == 'f' ? e->opt_mega_fill_splits : e->opt_mega_att_stages) = (int)v;
         e->mplans.clear();

@@ -56,46 +56,6 @@ __device__ __forceinline__ unsigned atom_add_acq_rel_u32(unsigned* p, unsigned v
 __device__ __forceinline__ void fence_proxy_async_global() {
     asm volatile("fence.proxy.async.global;" ::: "memory");
 }
-__device__ __forceinline__ void l2_prefetch(const void* src, uint32_t bytes) {
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
-}
-
-// L2 prefetch of the weight tiles of this CTA's units of a GEMM phase (issued by
-// one warp one phase ahead: the GEMM then streams its A operand from L2)
-__device__ __forceinline__ void l2_prefetch_gemm(const IterGemm& g, int layer) {
-    const int lane = threadIdx.x & 31;
-    const int U = g.m_tiles * g.splits;
-    for (int u = blockIdx.x; u < U; u += gridDim.x) {
-        const int m = u / g.splits, s = u % g.splits;
-        const int kb0 = s * g.kb_total / g.splits, kb1 = (s + 1) * g.kb_total / g.splits;
-        const uint16_t* a = g.A + (size_t)((layer - 1) * g.layer_rows + g.row_off + m) * g.kb_total * (kBM * kBK);
-        for (int kb = kb0 + lane; kb < kb1; kb += 32) l2_prefetch(a + (size_t)kb * (kBM * kBK), kAStage);
-    }
-}
-
-// L2 prefetch of the first `nblk` KV blocks of this CTA's attention range of
-// `layer` (same static split as attn_body; a.pref holds the block prefix sum
-// of the last attention pass).  Old positions only change when written, so the
-// next layer's blocks can stream into the 126 MB L2 while HBM would otherwise
-// idle (GEMM / reduce / barrier phases).
-__device__ __forceinline__ void l2_prefetch_kv(const DevState& st, const AttnSmem& a, int layer, int nblk) {
-    const int lane = threadIdx.x & 31;
-    const Dims& dm = st.dm;
-    const int B = st.rows.B;
-    const long long T = a.pref[B], G = min((long long)gridDim.x, T);
-    if ((long long)blockIdx.x >= G) return;
-    const long long g0 = (long long)blockIdx.x * T / G, g1 = (long long)(blockIdx.x + 1) * T / G;
-    const long long ge = min(g1, g0 + nblk);
-    const uint32_t bytes = (uint32_t)dm.bc * dm.dp * 2;
-    int b = 0;
-    for (long long g = g0 + lane; g < ge; g += 32) {
-        while (b < B && a.pref[b + 1] <= g) ++b;
-        const int blk = (int)(g - a.pref[b]);
-        const int id = st.tables[((size_t)st.rows.slot[b] * dm.L + (layer - 1)) * dm.bpl_max + blk];
-        l2_prefetch(st.kpool + (size_t)id * dm.bc * dm.dp, bytes);
-        l2_prefetch(st.vpool + (size_t)id * dm.bc * dm.dp, bytes);
-    }
-}
 
 __device__ __forceinline__ unsigned ld_relaxed_u32(const unsigned* p) {
     unsigned v;
@@ -825,7 +785,7 @@ __device__ __forceinline__ void unit_bm(IterSmem& sm, uint8_t* ring, const IterP
         uint32_t s = cseq % (uint32_t)p.bm_stages, ph = (cseq / (uint32_t)p.bm_stages) & 1;
         bool wrapped = cseq >= (uint32_t)p.bm_stages;
         const uint32_t full0 = smem_u32(sm.full2), empty0 = smem_u32(sm.empty2);
-        const uint64_t pol = (p.bm_act_policy & 1) ? kL2EvictFirst : kL2EvictLast;
+        const uint64_t pol = kL2EvictLast;  // activations: re-read by every unit of the phase
         int issued = 0;  // copies so far (their lane rotates)
 #pragma unroll 1
         for (int c = 0; c < nch; ++c) {
@@ -881,7 +841,6 @@ __device__ __forceinline__ void unit_bm(IterSmem& sm, uint8_t* ring, const IterP
                 tc_fence_after();
 #pragma unroll 1
                 for (int j = 0; j < kc; ++j, ++kb) {
-                    if (p.bm_act_policy & 2) continue;  // timing probe: no MMAs (wrong results)
                     // rows >= n_pad of the A tile read the next k-block / stage / weights: ignored output rows
                     const uint64_t ad = sdesc_k_sw128(ring0 + s * (uint32_t)p.bm_astage + (uint32_t)j * NRb);
                     const uint64_t bd = sdesc_k_sw128(ws ? ring0 + s * (uint32_t)p.bm_astage + wst + (uint32_t)j * wrow
@@ -1071,24 +1030,6 @@ __device__ void gemm_phase_fused(const DevState& st, IterSmem& sm, uint8_t* ring
     }
 }
 
-// weight-streaming GEMM phase: this CTA's units (u = cta, cta + G, ...)
-__device__ __forceinline__ void gemm_phase(const DevState& st, IterSmem& sm, uint8_t* ring, const IterPlan& p,
-                                           const IterGemm& g, int layer, const uint16_t* bsrc, uint32_t& kseq,
-                                           uint32_t& useq, int nval) {
-    const int U = g.m_tiles * g.splits;
-    const size_t bks = (size_t)st.NR * kBK;
-    for (int u = blockIdx.x; u < U; u += gridDim.x) {
-        const int m = u / g.splits, s = u % g.splits;
-        const int kb0 = s * g.kb_total / g.splits, kb1 = (s + 1) * g.kb_total / g.splits;
-        const uint16_t* a = g.A + (size_t)((layer - 1) * g.layer_rows + g.row_off + m) * g.kb_total * (kBM * kBK);
-        unit_ws(sm, ring, p, kseq, a, bsrc, bks, kb0, kb1 - kb0, useq);
-        if ((threadIdx.x >> 5) < 8) epi_partial(sm, p, u, nval);
-        ++useq;
-        tc_fence_before();
-        __syncthreads();
-    }
-}
-
 template <int NJ>
 __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(const __grid_constant__ DevState st,
                                                                 const __grid_constant__ IterPlan p,
@@ -1194,22 +1135,12 @@ __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(const __grid_cons
     for (int layer = lfirst; layer <= llast; ++layer) {
         const IterCtx x{layer, (layer - 1) & 1, layer & 1};
         // q | k | v, K/V appended to the paged pool (model.cpp:218-226)
-        // this layer's first attention blocks (old positions: not written by this layer) into L2
-        if (EL_DEBUG && warp == kProducerWarp && p.att_l2_blocks > 0) l2_prefetch_kv(st, sm.att, layer, p.att_l2_blocks);
-        __syncwarp();
         if (p.g[kIQkv].mode) {
             gemm_phase_t<kIQkv>(st, sm, ring, p, maps, kIQkv, x, st.hb + (size_t)x.pin * NR * dp, kseq2, wseq, useq, B,
                                 wpf, -1, 0);
-        } else if (!EL_DEBUG || p.fused_reduce) {  // (unfused split-K: probe builds only)
-            gemm_phase_fused<kIQkv>(st, sm, ring, p, kIQkv, x, st.hb + (size_t)x.pin * NR * dp, kseq, useq, B, layer - lfirst + 1);
         } else {
-            gemm_phase(st, sm, ring, p, p.g[kIQkv], layer, st.hb + (size_t)x.pin * NR * dp, kseq, useq, B);
-            grid_sync(p, st, nbar, g0);
-            reduce_phase<kIQkv>(st, sm, p, p.g[kIQkv], x, B, 0, p.g[kIQkv].m_tiles);
+            gemm_phase_fused<kIQkv>(st, sm, ring, p, kIQkv, x, st.hb + (size_t)x.pin * NR * dp, kseq, useq, B, layer - lfirst + 1);
         }
-        // this CTA's first attention blocks -> L2 while the grid waits at the barrier (no
-        // competition with the QKV loads, which are done)
-        if (EL_DEBUG && warp == kProducerWarp && p.att_l2_late > 0) l2_prefetch_kv(st, sm.att, layer, p.att_l2_late);
         // early attention start (default; barrier-mode 1-hop only): the producer warp skips
         // this barrier and streams the old K/V blocks of its range while the grid waits; q and
         // the newest block (this phase's output) wait on the barrier count
@@ -1239,31 +1170,18 @@ __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(const __grid_cons
         astamp(0);
         if ((EL_DBG(st) & 32) && tid == 0 && cta < 4) st.dbg_ts[8192 + 3072 + cta * 16] = clock64();
         if (tid == kProducerWarp * 32) wpf = bm_prefetch(sm, ring, p, maps, kIWo, layer);  // W_o under attention
-        if (EL_DEBUG && warp == kProducerWarp && (p.pf_flags & 1)) {  // this layer's W_o / up / down tiles -> L2
-            l2_prefetch_gemm(p.g[kIWo], layer);
-            l2_prefetch_gemm(p.g[kIUp], layer);
-            l2_prefetch_gemm(p.g[kIDown], layer);
-        }
         __syncwarp();
         attn_pass<NJ>(st, sm.att, ring, layer, aseq, self_l, att_mbuf);
         astamp(1);
         grid_sync(p, st, nbar, g0);
         aseq = sm.att.seq_next;
-        // the next layer's dynamic-tail counter (this one's twin) is idle now: rearm it
-        if (cta == 0 && tid == 0 && st.attn_queue) st.attn_queue[(layer + 1) & 1] = 0;
-        if (EL_DEBUG && warp == kProducerWarp && layer < L && p.kv_pf_blocks > 0)  // next layer's K/V -> L2
-            l2_prefetch_kv(st, sm.att, layer + 1, p.kv_pf_blocks);
         __syncwarp();
         // W_o + residual (model.cpp:245-253)
         if (p.g[kIWo].mode) {
             gemm_phase_t<kIWo>(st, sm, ring, p, maps, kIWo, x, st.att_b, kseq2, wseq, useq, B, wpf,
                                st.enc_len > 0 ? (int)kIQc : (int)kIUp, layer);
-        } else if (!EL_DEBUG || p.fused_reduce) {  // (unfused split-K: probe builds only)
-            gemm_phase_fused<kIWo>(st, sm, ring, p, kIWo, x, st.att_b, kseq, useq, B, layer - lfirst + 1);
         } else {
-            gemm_phase(st, sm, ring, p, p.g[kIWo], layer, st.att_b, kseq, useq, B);
-            grid_sync(p, st, nbar, g0);
-            reduce_phase<kIWo>(st, sm, p, p.g[kIWo], x, B, 0, p.g[kIWo].m_tiles);
+            gemm_phase_fused<kIWo>(st, sm, ring, p, kIWo, x, st.att_b, kseq, useq, B, layer - lfirst + 1);
         }
         grid_sync(p, st, nbar, g0);
         if (st.enc_len > 0) {
@@ -1271,12 +1189,8 @@ __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(const __grid_cons
             if (p.g[kIQc].mode) {
                 gemm_phase_t<kIQkv>(st, sm, ring, p, maps, kIQc, x, st.mid_b, kseq2, wseq, useq, B, wpf, -1,
                                     0);  // q_c -> q32
-            } else if (!EL_DEBUG || p.fused_reduce) {  // (unfused split-K: probe builds only)
-                gemm_phase_fused<kIQkv>(st, sm, ring, p, kIQc, x, st.mid_b, kseq, useq, B, layer - lfirst + 1);
             } else {
-                gemm_phase(st, sm, ring, p, p.g[kIQc], layer, st.mid_b, kseq, useq, B);
-                grid_sync(p, st, nbar, g0);
-                reduce_phase<kIQkv>(st, sm, p, p.g[kIQc], x, B, 0, p.g[kIQc].m_tiles);
+                gemm_phase_fused<kIQkv>(st, sm, ring, p, kIQc, x, st.mid_b, kseq, useq, B, layer - lfirst + 1);
             }
             grid_sync(p, st, nbar, g0);
             if (tid == kProducerWarp * 32) wpf = bm_prefetch(sm, ring, p, maps, kIWoc, layer);
@@ -1286,12 +1200,8 @@ __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(const __grid_cons
             if (p.g[kIWoc].mode) {
                 gemm_phase_t<kIWoc>(st, sm, ring, p, maps, kIWoc, x, st.att_b, kseq2, wseq, useq, B, wpf, kIUp,
                                     layer);
-            } else if (!EL_DEBUG || p.fused_reduce) {  // (unfused split-K: probe builds only)
-                gemm_phase_fused<kIWoc>(st, sm, ring, p, kIWoc, x, st.att_b, kseq, useq, B, layer - lfirst + 1);
             } else {
-                gemm_phase(st, sm, ring, p, p.g[kIWoc], layer, st.att_b, kseq, useq, B);
-                grid_sync(p, st, nbar, g0);
-                reduce_phase<kIWoc>(st, sm, p, p.g[kIWoc], x, B, 0, p.g[kIWoc].m_tiles);
+                gemm_phase_fused<kIWoc>(st, sm, ring, p, kIWoc, x, st.att_b, kseq, useq, B, layer - lfirst + 1);
             }
             grid_sync(p, st, nbar, g0);
         }
@@ -1299,27 +1209,17 @@ __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(const __grid_cons
         if (p.g[kIUp].mode) {
             gemm_phase_t<kIUp>(st, sm, ring, p, maps, kIUp, x, st.mid_b, kseq2, wseq, useq, B, wpf,
                                p.g[kIDown].mode ? (int)kIDown : -1, layer);
-        } else if (!EL_DEBUG || p.fused_reduce) {  // (unfused split-K: probe builds only)
-            gemm_phase_fused<kIUp>(st, sm, ring, p, kIUp, x, st.mid_b, kseq, useq, B, layer - lfirst + 1);
         } else {
-            gemm_phase(st, sm, ring, p, p.g[kIUp], layer, st.mid_b, kseq, useq, B);
-            grid_sync(p, st, nbar, g0);
-            reduce_phase<kIUp>(st, sm, p, p.g[kIUp], x, B, 0, p.g[kIUp].m_tiles);
+            gemm_phase_fused<kIUp>(st, sm, ring, p, kIUp, x, st.mid_b, kseq, useq, B, layer - lfirst + 1);
         }
         grid_sync(p, st, nbar, g0);
         // down + residual (model.cpp:261-270) + exit-check partial dots
         if (p.g[kIDown].mode) {
             gemm_phase_t<kIDown>(st, sm, ring, p, maps, kIDown, x, st.up_b, kseq2, wseq, useq, B, wpf,
                                  layer < llast ? (int)kIQkv : -1, layer + 1);
-        } else if (!EL_DEBUG || p.fused_reduce) {  // (unfused split-K: probe builds only)
+        } else {
             if (tid == kProducerWarp * 32 && layer < llast) wpf = bm_prefetch(sm, ring, p, maps, kIQkv, layer + 1);
             gemm_phase_fused<kIDown>(st, sm, ring, p, kIDown, x, st.up_b, kseq, useq, B, layer - lfirst + 1);
-        } else {
-            gemm_phase(st, sm, ring, p, p.g[kIDown], layer, st.up_b, kseq, useq, B);
-            grid_sync(p, st, nbar, g0);
-            if (EL_DEBUG && warp == kProducerWarp && layer < L && (p.pf_flags & 1)) l2_prefetch_gemm(p.g[kIQkv], layer + 1);
-            if (tid == kProducerWarp * 32 && layer < llast) wpf = bm_prefetch(sm, ring, p, maps, kIQkv, layer + 1);
-            reduce_phase<kIDown>(st, sm, p, p.g[kIDown], x, B, 0, p.g[kIDown].m_tiles);
         }
         grid_sync(p, st, nbar, g0);
         if (st.technique == kSoftmax) {
@@ -1371,7 +1271,6 @@ __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(const __grid_cons
         if (cta == 0 && tid == 0) {
             *(volatile unsigned*)(p.bar + 2) = g0.y + (unsigned)G * (unsigned)nbar;  // next launch's count base
             for (int i = 0; i < kINumGemm * 64; ++i) p.tcnt[i] = 0u;  // all tile waits are behind us
-            if (st.attn_queue) st.attn_queue[1] = 0;
         }
         tc_fence_before();
         __syncthreads();
@@ -1460,7 +1359,6 @@ __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(const __grid_cons
     if (cta == 0 && tid == 0) {
         *(volatile unsigned*)(p.bar + 2) = g0.y + (unsigned)G * (unsigned)nbar;  // next launch's count base
         for (int i = 0; i < kINumGemm * 64; ++i) p.tcnt[i] = 0u;  // all tile waits are behind us
-        if (st.attn_queue) st.attn_queue[1] = 0;  // layer 1 of the next launch (layer 2's is rearmed in layer 1)
         rec_rec(st, iter % st.rec_cap)[2 * Bm] = e_out;
         *st.out_layer = e_out;
         *st.layer = e_out + 1;

@@ -939,30 +939,23 @@ __device__ __forceinline__ void attn_body(const DevState& st, AttnSmem& a, uint8
         if (lane == 0) EL_ATT_CLK(1);
         if (!persistent) attn_prefix_sum(st, a);  // (standalone kernel: src.pref == a.pref)
         // Work split: the flattened (row, block) space of rows [R0, R1) -- blocks
-        // [pref[R0], pref[R1]), relative index g in [0, T) -- is cut into a static
-        // head [0, Ts) -- CTA i streams its share [i*Ts/G, (i+1)*Ts/G), with fewer blocks than
-        // CTAs only the first Ts CTAs work -- and a dynamic tail [Ts, T) of items
-        // of `cb` blocks that CTAs grab from an atomic counter when their static
-        // range is done, so SMs that HBM serves faster take more of the tail.
-        // Partial slots per row: static segments in CTA order, then tail items in
-        // item order -- the combine order never depends on which CTA ran what.
-        // (int arithmetic: T <= 256 rows x 128 blocks, products <= T * 148 -- no 64-bit division)
+        // [pref[R0], pref[R1]), relative index g in [0, T) -- is cut statically: CTA i streams
+        // its share of [0, T) (with fewer blocks than CTAs only the first T CTAs work).
+        // Partial slots per row: segments in CTA order -- the combine order never depends on
+        // timing.  (int arithmetic: T <= 256 rows x 128 blocks, products <= T * 148 -- no 64-bit
+        // division)
         const int gA = src.pref[R0];
         auto PR = [&](int r) { return (int)src.pref[r] - gA; };  // relative block prefix of row r
         const int T = PR(R1);
-        const int cb = max(1, st.attn_dyn_cb);
-        const int Td = (EL_DEBUG && st.attn_dyn_permille > 0 && st.attn_queue && R0 == 0 && R1 == B && CN == (int)gridDim.x)
-                           ? min(T, (T * st.attn_dyn_permille / 1000 + cb - 1) / cb * cb) : 0;  // (probe builds)
-        const int Ts = T - Td;
+        const int Ts = T;
         if (lane == 0) EL_ATT_CLK(10);
-        const int n_items = (Td + cb - 1) / cb;
         const int G = min(CN, Ts);
         // Cost-aware static split: every row start costs dl extra "virtual" blocks (a segment
         // switch + one more partial merge), so CTAs whose range crosses a row boundary get
         // fewer real blocks.  Virtual position of real block g of row r: g + dl * (r - R0 + 1);
         // CTA i owns virtual [floor(i V / G), floor((i + 1) V / G)).  Deterministic: depends
         // on the row structure only.
-        const int dl = (Td == 0) ? st.attn_seg_cost : 0;
+        const int dl = st.attn_seg_cost;
         const int V = Ts + dl * (R1 - R0);
         auto cta_of = [&](int g, int r) { return (int)(((g + dl * (r - R0 + 1) + 1) * G + V - 1) / V - 1); };
         auto real_of = [&](int vb) {  // first real block whose virtual position is >= vb
@@ -975,18 +968,12 @@ __device__ __forceinline__ void attn_body(const DevState& st, AttnSmem& a, uint8
             }
             return PR(lo) + max(0, vb - PR(lo) - dl * (lo - R0 + 1));
         };
-        // segment bookkeeping of row r: static segments and the first tail item touching it
+        // segment bookkeeping of row r: its segments (CTA ranges) and the first CTA
         auto row_static = [&](int r, int& first_cta) {
             const int r0 = PR(r), r1 = min(PR(r + 1), Ts);
             if (r0 >= r1) return 0;
             first_cta = cta_of(r0, r);
             return cta_of(r1 - 1, r) - first_cta + 1;
-        };
-        auto row_items = [&](int r, int& i0) {
-            const int r0 = max(PR(r), Ts), r1 = PR(r + 1);
-            if (r0 >= r1) return 0;
-            i0 = (r0 - Ts) / cb;
-            return (r1 - 1 - Ts) / cb - i0 + 1;
         };
         // PDL secondary / gated early start: defer q and the newest block until the producer
         // kernel / the grid barrier has published them
@@ -1096,7 +1083,7 @@ __device__ __forceinline__ void attn_body(const DevState& st, AttnSmem& a, uint8
                 __syncwarp();
             }
         };
-        // ---- static head ----
+        // ---- this CTA's range ----
         const bool has_static = CI < G;
         const int g0 = gA + (has_static ? real_of(CI * V / G) : 0);  // absolute flattened range [g0, g1)
         const int g1 = gA + (has_static ? real_of((CI + 1) * V / G) : 0);
@@ -1139,44 +1126,10 @@ __device__ __forceinline__ void attn_body(const DevState& st, AttnSmem& a, uint8
             for (int g = g0; g < g1 && b < R1;) {
                 const int seg_end = min(g1, (int)src.pref[b + 1]);
                 int fc = 0;
-                const int ns = row_static(b, fc);
-                int i0 = 0;
-                const int nseg = ns + (int)row_items(b, i0);
+                const int nseg = row_static(b, fc);
                 emit(b, g, seg_end, CI - fc, nseg, pre ? a.ids[ib] + (g - g0) : nullptr);
                 g = seg_end;
                 ++b;
-            }
-        }
-        // ---- dynamic tail: grab items until the counter runs past the end ----
-        if (n_items > 0) {
-            int it = 0;
-            if (lane == 0) it = atomicAdd(st.attn_queue + (layer & 1), 1);
-            it = __shfl_sync(0xffffffffu, it, 0);
-            while (it < n_items) {
-                int nxt = 0;
-                if (lane == 0) nxt = atomicAdd(st.attn_queue + (layer & 1), 1);  // latency overlaps this item
-                const int gs = Ts + (int)it * cb, ge = min(T, gs + cb);
-                int b = 0;
-                {  // row holding block gs (binary search on the prefix sums)
-                    int lo = 0, hi = B - 1;
-                    while (lo < hi) {
-                        const int mid = (lo + hi + 1) >> 1;
-                        if (src.pref[mid] <= gs) lo = mid;
-                        else hi = mid - 1;
-                    }
-                    b = lo;
-                }
-                for (int g = gs; g < ge && b < B; ++b) {
-                    const int seg_end = min(ge, (int)src.pref[b + 1]);
-                    if (seg_end <= g) continue;
-                    int fc = 0;
-                    const int ns = row_static(b, fc);
-                    int i0 = 0;
-                    const int nseg = ns + (int)row_items(b, i0);
-                    emit(b, g, seg_end, ns + (int)(it - i0), nseg, nullptr);
-                    g = seg_end;
-                }
-                it = __shfl_sync(0xffffffffu, nxt, 0);
             }
         }
         if (lane == 0) flush();  // short run: anything still deferred

@@ -77,10 +77,6 @@ struct DevState {
     int attn_cb;      // blocks per chunk
     int attn_stages;
     int attn_grid;    // persistent CTAs
-    int* attn_queue;  // [2] dynamic-tail item counters (by layer parity; persistent kernel only)
-    int* attn_done;
-    int attn_dyn_permille;  // share of the KV blocks handed out dynamically (0 = static split only)
-    int attn_dyn_cb;        // blocks per dynamic item
     int attn_seg_cost;      // static split: extra cost of a row start, in KV blocks
     int dbg;          // experiment knob (0 = normal)
     unsigned long long* dbg_ts;
@@ -236,21 +232,15 @@ struct IterPlan {
     int bm_rows, bm_kc, bm_astage, bm_stages, bm_woff;
     int bm_prefetch;  // issue each batch-M unit's weights one phase ahead (weight buffer outside the rings)
     int bm_wstream;   // batch-M weights streamed through the ring (L2-prefetched a phase ahead), no weight slab
-    int bm_act_policy;  // L2 hint of the activation copies: 0 evict-last, 1 evict-first (probe)
     int bm_m;           // UMMA M of the batch-M GEMMs: 64 (batch <= 64) or 128
     int bm_grp;         // batch rows per unit (row group): bm_rows, or 128 when the batch has 2 groups
     int map_key;        // host-side key of this plan's tensor maps
-    int fused_reduce;   // split-K: per-tile arrival counters + the tile's CTAs reduce (no grid barrier)
     unsigned* tcnt;     // [kINumGemm][64] per-tile arrival counters (zeroed at the end of each launch)
-    int att_l2_blocks;  // per CTA: first attention K/V blocks of the layer prefetched into L2 during QKV
     int att_mbuf_off;   // > 0: the attention segment merge buffer [8][dp] fp32 (else merged inside the stage)
-    int att_l2_late;    // per CTA: first attention K/V blocks prefetched into L2 at the end of the QKV phase
     int att_early;      // the attention producer starts before the QKV -> attention barrier
     int ring_bytes;  // shared ring region (attention stages / GEMM stages + LM transpose buffer)
     int gemm_ring;   // bytes of the GEMM stages inside the ring region
     int lm_tiles;    // Vp / 128
-    int kv_pf_blocks;  // per CTA: K/V blocks of the next layer prefetched into L2 after attention
-    int pf_flags;      // bit 0: L2 prefetch of GEMM weight tiles one phase ahead
     float* part;     // split-K partials [unit][n_pad][128] fp32
     unsigned* bar;   // grid barrier: [0] arrivals, [32] generation
     int pipe_att_ctas;  // pipelined kernel (el_pipe.cuh): CTAs [0, pipe_att_ctas) run attention

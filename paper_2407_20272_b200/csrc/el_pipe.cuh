@@ -307,7 +307,6 @@ __global__ void __launch_bounds__(kIterThreads, 1) pipe_kernel(const __grid_cons
     if (cta == 0 && tid == 0) {
         *(volatile unsigned*)(p.bar + 2) = g0.y + (unsigned)G * (unsigned)nbar;  // next launch's count base
         for (int i = 0; i < kINumGemm * 64; ++i) p.tcnt[i] = 0u;
-        if (st.attn_queue) st.attn_queue[1] = 0;
         rec_rec(st, iter % st.rec_cap)[2 * Bm] = e_out;
         *st.out_layer = e_out;
         *st.layer = e_out + 1;

@@ -43,8 +43,6 @@ pi = e.plan_info()
 per_layer = []
 for nm in ("qkv", "attn", "wo", "up", "down"):
     per_layer.append(nm)
-    if not opts.get("mega_fused_reduce", 1) and (nm == "down" or (nm != "attn" and not pi[f"mega_{nm}_mode"])):
-        per_layer.append(nm + "_red")
 print({k: v for k, v in pi.items() if k.startswith("mega")})
 if tech == "softmax":
     per_layer += ["lmchk", "sm_decide"]

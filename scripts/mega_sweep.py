@@ -1,5 +1,5 @@
 """Option sweep of the persistent decode-iteration kernel: us/iteration (full depth, technique never)
-and the early-exit bench technique.  python scripts/mega_sweep.py c2 '[{"mega_kv_pf_mb": 0}, ...]'"""
+and the early-exit bench technique.  python scripts/mega_sweep.py c2 '[{"mega_att_stages": 2}, ...]'"""
 import json
 import sys
 
