@@ -71,6 +71,10 @@ typedef struct {
      * cross-attention sub-layer over this many synthetic encoder states per sequence
      * (static cross K/V written once at admission; the skipped-layer fill is unchanged). */
     int encoder_len;
+    /* Extension (NOT in the reference; CALM-T5 attention): self- and, in T5 mode, cross-attention
+     * split into n_heads heads of d_model / n_heads features (own softmax, scale 1/sqrt(head_dim));
+     * 0 or 1 = the reference's single head.  head_dim: 8, 16, 32, 64, 128 or 256; n_heads <= 32. */
+    int n_heads;
 } el_engine_config;
 
 typedef struct el_engine el_engine;

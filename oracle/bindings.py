@@ -231,10 +231,11 @@ class _Lib:
         return self.fn("last_error")().decode()
 
     # ---- model ----
-    def model(self, n_layers, d_model, vocab, seed, round_bf16=False, encoder_len=0):
+    def model(self, n_layers, d_model, vocab, seed, round_bf16=False, encoder_len=0, n_heads=1):
         """encoder_len > 0: the T5-mode extension (cross-attention over synthetic
         encoder states) -- the C restatement only; the compiled reference has no
-        encoder, so parity of that mode is not pinned by it."""
+        encoder, so parity of that mode is not pinned by it.  n_heads > 1 (extension, not in
+        the reference): self- and cross-attention split into heads of d_model / n_heads features."""
         if encoder_len:
             if self.prefix != "eo_":
                 raise ValueError("the reference has no encoder / cross-attention (SPEC.md:13, 184)")
@@ -246,6 +247,9 @@ class _Lib:
             raise ValueError(self.err())
         m = Model(self, h, n_layers, d_model, vocab, seed)
         m.encoder_len = encoder_len
+        m.n_heads = n_heads
+        if n_heads != 1 and self.fn("model_set_heads")(C.c_void_p(h), int(n_heads)):
+            raise ValueError(self.err())
         return m
 
     def gen_workload(self, n_requests=8, mean_interarrival=0.0, prompt_len_min=1, prompt_len_max=8,

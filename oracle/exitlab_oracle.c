@@ -85,6 +85,10 @@ struct eo_model {
     int round_bf16;
     uint64_t enc_seed;
     double** wc;   /* per layer: q_c, k_c, v_c, o_c (d x d) */
+    /* extension (not in the reference): self- and, in T5 mode, cross-attention split into n_heads
+       heads of d / n_heads features, each with its own softmax and scale 1 / sqrt(d / n_heads);
+       1 = the reference's single head.  Sessions with heads use the layer_forward restatement. */
+    int n_heads;
 };
 static const int kLayerTensors = 6;
 
@@ -106,6 +110,12 @@ eo_model* eo_model_seeded(int L, int d, int V, uint64_t seed, int round_bf16) {
    (sequence id, position) from their own stream; bf16-rounded like the weights. */
 static const int kCrossTensors = 4;
 uint64_t eo_encoder_seed(uint64_t model_seed) { return eo_splitmix64_at(model_seed, 0x454E43u); }
+int eo_model_set_heads(eo_model* m, int n_heads) {
+    if (n_heads < 1 || m->d % n_heads) { set_err("ModelConfig: n_heads must divide d_model"); return EO_INVALID_ARGUMENT; }
+    m->n_heads = n_heads;
+    return EO_OK;
+}
+
 void eo_encoder_state(const eo_model* m, int seq_id, int t, double* out) {
     eo_seeded_vector(m->d, eo_splitmix64_at(m->enc_seed, ((uint64_t)seq_id << 20) | (uint64_t)t), out);
     if (m->round_bf16) round_all(out, (size_t)m->d);
@@ -116,7 +126,7 @@ eo_model* eo_model_seeded_t5(int L, int d, int V, uint64_t seed, int round_bf16,
     if (enc_len < 0) { set_err("ModelConfig: encoder_len must be >= 0"); return NULL; }
     eo_model* m = (eo_model*)calloc(1, sizeof(eo_model));
     m->L = L; m->d = d; m->V = V; m->seed = seed;
-    m->enc_len = enc_len; m->round_bf16 = round_bf16; m->enc_seed = eo_encoder_seed(seed);
+    m->enc_len = enc_len; m->round_bf16 = round_bf16; m->enc_seed = eo_encoder_seed(seed); m->n_heads = 1;
     if (enc_len > 0) {
         m->wc = (double**)calloc((size_t)L * kCrossTensors, sizeof(double*));
         for (int i = 0; i < L; ++i)
@@ -401,6 +411,53 @@ static void scratch_scores(scratch_t* w, int n) {
     }
 }
 
+/* Attention of one query over n key/value rows, split into heads (T5 mode; heads = 1 is
+   model.cpp:223-243 exactly): per head h over features [h hd, (h+1) hd):
+   a_h = softmax(q_h K_h^T / sqrt(hd)) V_h.  key(p) / val(p) give row p. */
+typedef const double* (*row_fn)(const void* ctx, int p);
+static int attend_heads(int d, int heads, const double* q, int n, row_fn key, row_fn val, const void* ctx,
+                        double* scores, double* probs, double* a) {
+    const int hd = d / heads;
+    const double scale = 1.0 / sqrt((double)hd);
+    for (int i = 0; i < d; ++i) a[i] = 0.0;
+    for (int h = 0; h < heads; ++h) {
+        const int f0 = h * hd;
+        for (int p = 0; p < n; ++p) {
+            const double* kr = key(ctx, p);
+            double acc = 0.0;
+            for (int i = f0; i < f0 + hd; ++i) acc += kr[i] * q[i];
+            scores[p] = acc * scale;
+        }
+        int rc = softmax(scores, n, probs);
+        if (rc) return rc;
+        for (int p = 0; p < n; ++p) {
+            const double* vr = val(ctx, p);
+            for (int i = f0; i < f0 + hd; ++i) a[i] += probs[p] * vr[i];
+        }
+    }
+    return EO_OK;
+}
+
+/* row accessors of attend_heads: the paged cache of (seq, layer), or two row-major matrices */
+typedef struct { kv_store* cache; int id, layer; } kv_ctx;
+static const double* kv_key_row(const void* c, int p) {
+    const kv_ctx* x = (const kv_ctx*)c;
+    return kv_slot(x->cache, 0, x->id, x->layer, p);
+}
+static const double* kv_val_row(const void* c, int p) {
+    const kv_ctx* x = (const kv_ctx*)c;
+    return kv_slot(x->cache, 1, x->id, x->layer, p);
+}
+typedef struct { const double* rows; int d; } mat_ctx;
+static const double* mat_key_row(const void* c, int p) {
+    const mat_ctx* x = ((const mat_ctx* const*)c)[0];
+    return x->rows + (size_t)p * x->d;
+}
+static const double* mat_val_row(const void* c, int p) {
+    const mat_ctx* x = ((const mat_ctx* const*)c)[1];
+    return x->rows + (size_t)p * x->d;
+}
+
 /* h[B][d] in, out[B][d] out (out may not alias h). ids[B] are seq ids. */
 static int layer_forward(const eo_model* m, int layer, int B, const int* ids, const double* h,
                          kv_store* cache, scratch_t* w, double* out) {
@@ -420,6 +477,13 @@ static int layer_forward(const eo_model* m, int layer, int B, const int* ids, co
         const int n = pos + 1;
         scratch_scores(w, n);
         const double* q = w->q + (size_t)b * d;
+        if (m->n_heads > 1) {  /* extension: heads (attend_heads) */
+            const kv_ctx cx = {cache, id, layer};
+            rc = attend_heads(d, m->n_heads, q, n, kv_key_row, kv_val_row, &cx, w->scores, w->probs,
+                              w->att + (size_t)b * d);
+            if (rc) return rc;
+            continue;
+        }
         for (int p = 0; p < n; ++p) {
             const double* key = kv_slot(cache, 0, id, layer, p);
             double acc = 0.0;
@@ -457,17 +521,24 @@ static int layer_forward(const eo_model* m, int layer, int B, const int* ids, co
             }
             double* q = w->q + (size_t)b * d;
             matvec(wqc, d, d, w->mid + (size_t)b * d, q);
-            for (int t = 0; t < T; ++t) {
-                double acc = 0.0;
-                for (int i = 0; i < d; ++i) acc += kc[(size_t)t * d + i] * q[i];
-                w->scores[t] = acc * scale;
-            }
-            int rc = softmax(w->scores, T, w->probs);
-            if (rc) { free(e); free(kc); free(vc); return rc; }
             double* a = w->att + (size_t)b * d;
-            for (int i = 0; i < d; ++i) a[i] = 0.0;
-            for (int t = 0; t < T; ++t)
-                for (int i = 0; i < d; ++i) a[i] += w->probs[t] * vc[(size_t)t * d + i];
+            if (m->n_heads > 1) {
+                const mat_ctx ck = {kc, d}, cv = {vc, d};
+                const mat_ctx* both[2] = {&ck, &cv};
+                int rc = attend_heads(d, m->n_heads, q, T, mat_key_row, mat_val_row, both, w->scores, w->probs, a);
+                if (rc) { free(e); free(kc); free(vc); return rc; }
+            } else {
+                for (int t = 0; t < T; ++t) {
+                    double acc = 0.0;
+                    for (int i = 0; i < d; ++i) acc += kc[(size_t)t * d + i] * q[i];
+                    w->scores[t] = acc * scale;
+                }
+                int rc = softmax(w->scores, T, w->probs);
+                if (rc) { free(e); free(kc); free(vc); return rc; }
+                for (int i = 0; i < d; ++i) a[i] = 0.0;
+                for (int t = 0; t < T; ++t)
+                    for (int i = 0; i < d; ++i) a[i] += w->probs[t] * vc[(size_t)t * d + i];
+            }
             matvec(woc, d, d, a, w->proj + (size_t)b * d);
             for (int i = 0; i < d; ++i) w->mid[(size_t)b * d + i] += w->proj[(size_t)b * d + i];
         }
@@ -1598,7 +1669,7 @@ eo_session* eo_session_create(const eo_model* m, const eo_engine_config* c, int 
     if (validate_config(m, c)) return NULL;
     eo_session* s = (eo_session*)calloc(1, sizeof(eo_session));
     const char* slow = getenv("EO_SLOW_SESSION");
-    if (m->enc_len > 0 || (slow && atoi(slow)))
+    if (m->enc_len > 0 || m->n_heads > 1 || (slow && atoi(slow)))
         s->slow = slow_session_create(m, c, B, first_tokens, prefix_len, capacity, kv_seed, seq_ids);
     else
         s->fast = fast_session_create(m, c, B, first_tokens, prefix_len, capacity, kv_seed, seq_ids);

@@ -65,6 +65,9 @@ eo_model* eo_model_seeded(int n_layers, int d_model, int vocab, uint64_t seed, i
 eo_model* eo_model_seeded_t5(int n_layers, int d_model, int vocab, uint64_t seed, int round_bf16, int encoder_len);
 uint64_t eo_encoder_seed(uint64_t model_seed);
 void eo_encoder_state(const eo_model* m, int seq_id, int t, double* out);
+/* Extension: split self- (and in T5 mode cross-) attention into n_heads heads (d_model / n_heads
+   features each, own softmax, scale 1 / sqrt(d_model / n_heads)); the reference has one head. */
+int eo_model_set_heads(eo_model* m, int n_heads);
 void eo_model_free(eo_model* m);
 /* which: 0 embedding, 1 lm_head, 2 probe_w, 3 probe_b, 4+k: layer tensor k in
  * {q,k,v,o,up,down}; layer is 1-based (ignored for globals). Copies into out. */

@@ -300,6 +300,14 @@ struct el_engine {
         if (c.d_model > 1024) fail(EL_INVALID_ARGUMENT, "d_model > 1024 unsupported on this engine");
         if (c.encoder_len < 0 || c.encoder_len > 2048)
             fail(EL_INVALID_ARGUMENT, "ModelConfig: encoder_len must be in [0, 2048]");
+        if (c.n_heads > 1) {  // extension: the reference has one head
+            const int hd = c.d_model % c.n_heads ? 0 : c.d_model / c.n_heads;
+            if (c.n_heads > 32 || !hd || hd < 8 || hd > 256 || (hd & (hd - 1)))
+                fail(EL_INVALID_ARGUMENT, "ModelConfig: n_heads must divide d_model into heads of 8..256 (power of 2) "
+                                          "features, n_heads <= 32");
+        } else if (c.n_heads < 0) {
+            fail(EL_INVALID_ARGUMENT, "ModelConfig: n_heads must be >= 0");
+        }
     }
 
     double check_cost() const {
@@ -522,7 +530,7 @@ struct el_engine {
         attn_grid = sms * el::attn_ctas_per_sm(dm, attn_stages);
         if (opt_attn_grid > 0) attn_grid = std::min(attn_grid, opt_attn_grid);  // probe: fewer CTAs
         attn_o.alloc((size_t)std::max(B, kPfRows) * attn_max_chunks * dm.dp, false);
-        attn_ml.alloc((size_t)std::max(B, kPfRows) * attn_max_chunks * 2, false);
+        attn_ml.alloc((size_t)std::max(B, kPfRows) * attn_max_chunks * 2 * std::max(1, cfg.n_heads), false);
         invalidate_graphs();
     }
 
@@ -792,7 +800,9 @@ struct el_engine {
         s.dbg = dbg;
         s.dbg_ts = dbg_ts.p;
         s.attn_grid = attn_grid;
-        s.attn_scale = (float)(1.0 / std::sqrt((double)dm.d));
+        s.attn_heads = std::max(1, cfg.n_heads);
+        s.attn_hd = dm.d / s.attn_heads;
+        s.attn_scale = (float)(1.0 / std::sqrt((double)s.attn_hd));
         s.lm_part = lm_part.p;
         s.layer = layer.p; s.out_layer = out_layer.p; s.status = status.p; s.first_accept = first_accept.p;
         s.accept = accept.p; s.conf = conf.p; s.exit_cnt = exit_cnt.p; s.cont_host = cont_dev;

@@ -714,6 +714,7 @@ constexpr int kAttnWarps = 8;
 constexpr int kAttnThreads = (kAttnWarps + 1) * 32;
 
 constexpr int kAttnPend = 256;  // >= rows: a CTA never has more segments than rows
+constexpr int kAttnMaxHeads = 32;  // T5 mode: heads of d / n_heads features (head_dim 8..256)
 constexpr int kAttnIds = 256;  // deferred segment completions per CTA before a forced settle
 struct AttnDesc {
     int b, c, rows, first, last, nseg, pad[2];  // c = partial slot of this CTA's segment of sequence b
@@ -723,6 +724,7 @@ struct AttnSmem {
     uint64_t empty[8];
     AttnDesc desc[8];
     float wm[kAttnWarps], wl[kAttnWarps];
+    float wmh[kAttnWarps][kAttnMaxHeads], wlh[kAttnWarps][kAttnMaxHeads];  // multi-head (T5 mode) merge
     float cw[128];
     float cl[128];
     int pref[257];  // block prefix sum over the batch rows
@@ -837,6 +839,36 @@ __device__ __forceinline__ void attn_settle(const DevState& st, AttnSmem& a) {
         if (!a.pend_last[i]) continue;
         const int b = a.pend_b[i], nch = a.pend_n[i];
         const size_t pbase = (size_t)b * st.attn_max_chunks;
+        if (st.attn_heads > 1) {  // multi-head: every feature chunk weights the partials by its head's (m, l)
+            if (tid < nchunk) {
+                const int H = st.attn_heads, h = tid * 8 / st.attn_hd;
+                float Mg = -INFINITY;
+                for (int cc = 0; cc < nch; ++cc) Mg = fmaxf(Mg, __ldcg(&st.attn_ml[((pbase + cc) * H + h) * 2]));
+                float Lg = 0.f, acc[8];
+#pragma unroll
+                for (int e = 0; e < 8; ++e) acc[e] = 0.f;
+                for (int cc = 0; cc < nch; ++cc) {  // fixed chunk order: deterministic
+                    const float2 ml = __ldcg(reinterpret_cast<const float2*>(st.attn_ml) + (pbase + cc) * H + h);
+                    const float w = __expf(ml.x - Mg);
+                    Lg += w * ml.y;
+                    const float4* src = reinterpret_cast<const float4*>(st.attn_o + (pbase + cc) * dp + tid * 8);
+                    const float4 x0 = __ldcg(src), x1 = __ldcg(src + 1);
+                    acc[0] = fmaf(w, x0.x, acc[0]); acc[1] = fmaf(w, x0.y, acc[1]);
+                    acc[2] = fmaf(w, x0.z, acc[2]); acc[3] = fmaf(w, x0.w, acc[3]);
+                    acc[4] = fmaf(w, x1.x, acc[4]); acc[5] = fmaf(w, x1.y, acc[5]);
+                    acc[6] = fmaf(w, x1.z, acc[6]); acc[7] = fmaf(w, x1.w, acc[7]);
+                }
+                const float inv = 1.f / Lg;
+                uint32_t pk[4];
+#pragma unroll
+                for (int e = 0; e < 4; ++e)
+                    pk[e] = (uint32_t)f32_to_bf16(acc[2 * e] * inv) | ((uint32_t)f32_to_bf16(acc[2 * e + 1] * inv) << 16);
+                *reinterpret_cast<uint4*>(st.att_b + act_offset(b, tid * 8, st.NR)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+            }
+            if (tid == 0) st.attn_cnt[b] = 0;
+            named_bar(1, kAttnWarps * 32);
+            continue;
+        }
         // the first partials' loads go out before the weights are known (one L2 round trip);
         // indices past nch are clamped to a valid partial and weighted 0 below
         constexpr int kPre = 4;
@@ -1148,6 +1180,12 @@ __device__ __forceinline__ void attn_body(const DevState& st, AttnSmem& a, uint8
 #pragma unroll
             for (int i = 0; i < 4; ++i) q[t][i] = o[t][i] = make_float2(0.f, 0.f);
         float m = -INFINITY, l = 0.f;
+        // multi-head (T5 mode, st.attn_heads > 1): head of feature chunk j = j / cph, cph =
+        // head_dim / 8 lanes of one chunk group t; every lane keeps its head's (m, l) per t
+        const int heads = st.attn_heads, cph = st.attn_hd >> 3;
+        float mh[NJ], lh[NJ];
+#pragma unroll
+        for (int t = 0; t < NJ; ++t) mh[t] = -INFINITY, lh[t] = 0.f;
         int npend = 0;
         const int r0 = warp, r1 = warp + kAttnWarps;
         // Persistent kernel: the consumer path is cold in the instruction cache at
@@ -1202,6 +1240,8 @@ __device__ __forceinline__ void attn_body(const DevState& st, AttnSmem& a, uint8
                 }
                 m = -INFINITY;
                 l = 0.f;
+#pragma unroll
+                for (int t = 0; t < NJ; ++t) mh[t] = -INFINITY, lh[t] = 0.f;
             }
             // Branch-free block math: both rows' K and V are loaded up front (row indices
             // clamped to valid rows, feature chunks clamped to the last one), an invalid
@@ -1224,6 +1264,36 @@ __device__ __forceinline__ void attn_body(const DevState& st, AttnSmem& a, uint8
                     const int j = min(lane + 32 * t, nchunk - 1);
                     xa[t] = sv[ra * nchunk + j];
                     xc[t] = sv[rc * nchunk + j];
+                }
+                if (heads > 1) {  // (warp-uniform) per-head scores, softmax state and rescale
+                    float sa[NJ], sc[NJ];
+#pragma unroll
+                    for (int t = 0; t < NJ; ++t) {
+                        const float2 x = dot8p2(ka[t], q[t], make_float2(0.f, 0.f));
+                        const float2 y = dot8p2(kc[t], q[t], make_float2(0.f, 0.f));
+                        sa[t] = x.x + x.y;
+                        sc[t] = y.x + y.y;
+                    }
+                    for (int off = 1; off < cph; off <<= 1)
+#pragma unroll
+                        for (int t = 0; t < NJ; ++t) {
+                            sa[t] += __shfl_xor_sync(0xffffffffu, sa[t], off);
+                            sc[t] += __shfl_xor_sync(0xffffffffu, sc[t], off);
+                        }
+#pragma unroll
+                    for (int t = 0; t < NJ; ++t) {
+                        if (!vc) sc[t] = -INFINITY;
+                        const float mn = fmaxf(mh[t], fmaxf(sa[t], sc[t]));
+                        const float pa = __expf(sa[t] - mn), pc = __expf(sc[t] - mn), alpha = __expf(mh[t] - mn);
+                        const float2 al = make_float2(alpha, alpha);
+                        lh[t] = lh[t] * alpha + (pa + pc);
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) o[t][i] = __fmul2_rn(o[t][i], al);
+                        axpy8p2(pa, xa[t], o[t]);
+                        axpy8p2(pc, xc[t], o[t]);
+                        mh[t] = mn;
+                    }
+                    continue;
                 }
                 float2 a2 = make_float2(0.f, 0.f), c2 = make_float2(0.f, 0.f);
 #pragma unroll
@@ -1281,7 +1351,16 @@ __device__ __forceinline__ void attn_body(const DevState& st, AttnSmem& a, uint8
                 if (lane == 0) mbar_arrive(&a.empty[s]);
             }
             named_bar(1, kAttnWarps * 32);  // (also: the previous merge's readers are done with mbuf / wm / wl)
-            if (lane == 0) {
+            if (heads > 1) {
+#pragma unroll
+                for (int t = 0; t < NJ; ++t) {
+                    const int j = lane + 32 * t;
+                    if (j < nchunk && j % cph == 0) {
+                        a.wmh[warp][j / cph] = mh[t];
+                        a.wlh[warp][j / cph] = lh[t];
+                    }
+                }
+            } else if (lane == 0) {
                 a.wm[warp] = m;
                 a.wl[warp] = l;
             }
@@ -1295,6 +1374,39 @@ __device__ __forceinline__ void attn_body(const DevState& st, AttnSmem& a, uint8
                 }
             }
             named_bar(1, kAttnWarps * 32);
+            if (heads > 1) {  // per feature: its head's max / weights over the 8 warps (fixed order)
+                const size_t pidx = (size_t)d.b * st.attn_max_chunks + d.c;
+                const int hd = st.attn_hd;
+                for (int i = tid; i < dp; i += kAttnWarps * 32) {
+                    const int h = i / hd;
+                    float M = -INFINITY;
+#pragma unroll
+                    for (int w = 0; w < kAttnWarps; ++w) M = fmaxf(M, a.wmh[w][h]);
+                    float acc = 0.f, Lsum = 0.f;
+#pragma unroll
+                    for (int w = 0; w < kAttnWarps; ++w) {
+                        const float sw = (a.wmh[w][h] == -INFINITY) ? 0.f : __expf(a.wmh[w][h] - M);
+                        acc += sw * merge[(size_t)w * dp + i];
+                        Lsum += sw * a.wlh[w][h];
+                    }
+                    st.attn_o[pidx * dp + i] = acc;
+                    if (i % hd == 0) {
+                        st.attn_ml[(pidx * heads + h) * 2 + 0] = M;
+                        st.attn_ml[(pidx * heads + h) * 2 + 1] = Lsum;
+                    }
+                }
+                if (tid == 0) {
+                    a.pend_b[a.npend] = d.b;
+                    a.pend_n[a.npend] = d.nseg;
+                    ++a.npend;
+                }
+                if (!mbuf) {
+                    named_bar(1, kAttnWarps * 32);
+                    if (lane == 0) mbar_arrive(&a.empty[s]);
+                }
+                ++npend;
+                continue;
+            }
             float M = -INFINITY;
 #pragma unroll
             for (int w = 0; w < kAttnWarps; ++w) M = fmaxf(M, a.wm[w]);

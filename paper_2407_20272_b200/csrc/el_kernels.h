@@ -80,7 +80,9 @@ struct DevState {
     int attn_seg_cost;      // static split: extra cost of a row start, in KV blocks
     int dbg;          // experiment knob (0 = normal)
     unsigned long long* dbg_ts;
-    float attn_scale; // 1/sqrt(d)
+    float attn_scale; // 1/sqrt(d), or 1/sqrt(head_dim) with heads
+    int attn_heads;   // attention heads (T5 mode; 1 = the reference's single head)
+    int attn_hd;      // features per head (d when attn_heads == 1)
     // split-K GEMM workspace
     // LM-head per-tile partials [Vp/128][Bmax] {max1, max2, sumexp(rel max1), argmax}
     float4* lm_part;

@@ -131,6 +131,7 @@ class ModelConfig:  # model.hpp:18-25
     vocab_size: int = 256
     seed: int = 0
     encoder_len: int = 0  # T5 mode (not in the reference): cross-attention over this many encoder states
+    n_heads: int = 1  # extension: attention heads of d_model / n_heads features (the reference: 1)
 
 
 @dataclass
@@ -222,7 +223,7 @@ class _CConfig(C.Structure):
                 ("c_check_classifier", C.c_double), ("c_check_state", C.c_double),
                 ("max_batch", C.c_int), ("pool_blocks", C.c_int), ("block_capacity", C.c_int),
                 ("eos_token", C.c_int), ("capture_kv", C.c_int), ("round_bf16", C.c_int),
-                ("synthetic_kv_seed", C.c_int64), ("encoder_len", C.c_int)]
+                ("synthetic_kv_seed", C.c_int64), ("encoder_len", C.c_int), ("n_heads", C.c_int)]
 
 
 def to_c_config(cfg: EngineConfig) -> _CConfig:
@@ -241,6 +242,7 @@ def to_c_config(cfg: EngineConfig) -> _CConfig:
     c.round_bf16 = 1
     c.synthetic_kv_seed = cfg.synthetic_kv_seed
     c.encoder_len = cfg.model.encoder_len
+    c.n_heads = cfg.model.n_heads
     return c
 
 

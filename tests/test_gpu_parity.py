@@ -336,6 +336,42 @@ def test_t5_cross_attention_parity(port, tech, lam, gamma, B):
     e.close()
 
 
+@pytest.mark.parametrize("L,d,heads,B,T", [(4, 128, 4, 8, 24), (3, 128, 16, 136, 40), (3, 512, 8, 16, 48),
+                                           (2, 1024, 16, 64, 32), (3, 256, 4, 24, 0)])
+def test_multi_head_parity(port, L, d, heads, B, T):
+    """Attention split into heads (extension; head_dim 32 / 8 / 64 / 64 / 64: 4 / 1 / 8 / 8 / 8 lanes
+    per head and chunk group; batch-M and split-K phases; T5 mode, and decoder-only with T = 0) vs
+    the oracle's per-head restatement (pinned to an independent numpy decoder,
+    tests/test_t5_oracle_cpu.py)."""
+    V = 512
+    g = X.EngineConfig(model=X.ModelConfig(L, d, V, 5, encoder_len=T, n_heads=heads),
+                       technique=X.ExitTechnique("state"), schedule=X.ThresholdSchedule(0.972, 0.998, 0.0),
+                       max_batch=B, pool_blocks=B * L * 8, eos_token=-1)
+    o = OB.engine_config(L, d, V, 5, "state", lambda0=0.972, gamma=0.998, max_batch=B, pool_blocks=B * L * 8,
+                         eos_token=-1, round_bf16=True)
+    e = X.Engine(g)
+    first = (np.arange(B) * 37 + 3) % V
+    e.session_begin(first, 30, 60, 1234)
+    m = port.model(L, d, V, 5, True, encoder_len=T, n_heads=heads)
+    s = m.session(o, first, 30, 60, 1234)
+    st = _teacher_forced(e, s, 3, m.tensor("lm_head"), V, d)
+    for x in st:
+        assert x["h"] <= HID_TOL, x["h"]
+        assert x["conf"] <= CONF_TOL, x["conf"]
+        assert np.all(x["agree"] | (x["gap"] < TIE_GAP)), x["gap"][~x["agree"]]
+    assert np.mean([x["agree"].mean() for x in st]) >= 0.9
+    # (random-init attention is near-uniform, so this only shows the split does no harm; the
+    #  per-head softmax itself is checked with sharp attention in test_gpu_subengine.py)
+    e.close()
+
+
+def test_multi_head_config_checks():
+    for heads, enc in ((3, 16), (64, 16), (32, 0)):  # no divisor; > 32 heads; head_dim 4 < 8
+        with pytest.raises(ValueError):
+            X.Engine(X.EngineConfig(model=X.ModelConfig(2, 128, 64, 1, encoder_len=enc, n_heads=heads),
+                                    technique=X.ExitTechnique("never"), max_batch=2, pool_blocks=64))
+
+
 def test_t5_engine_run_matches_oracle(port):
     """Engine::run in T5 mode (decoder prompt = start token, input in the encoder)."""
     L, d, V, T = 3, 64, 256, 16

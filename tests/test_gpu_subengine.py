@@ -201,3 +201,47 @@ def test_subengine_rejected_during_a_session():
     e.session_end()
     e.kv_store().allocate(1, 4)  # fine once the session is over
     e.close()
+
+
+@pytest.mark.parametrize("heads", [4, 16])
+def test_layer_forward_multi_head_sharp_attention(port, heads):
+    """The head split (extension: CALM-T5 attention; the reference has one head) with SHARP
+    attention: large cached keys make each head's softmax peak on different positions, so a
+    single softmax over d features would give a different output.  Per-head fp64 reference."""
+    L, d, V = 2, 128, 256
+    hd = d // heads
+    e = X.Engine(X.EngineConfig(model=X.ModelConfig(L, d, V, 3, n_heads=heads), technique=X.ExitTechnique("never"),
+                                max_batch=8, pool_blocks=256, eos_token=-1))
+    m = port.model(L, d, V, 3, True)
+    kv = e.kv_store()
+    rng = np.random.default_rng(7)
+    ids, P = [1, 4], [9, 21]
+    for sid, n in zip(ids, P):
+        kv.allocate(sid, 40)
+        for p in range(n):
+            for layer in range(1, L + 1):
+                kv.append(sid, layer, p, rng.standard_normal(d) * 4.0, rng.standard_normal(d))
+            kv.commit(sid)
+    h = [rng.standard_normal(d).astype(np.float32) * 2.0 for _ in ids]
+    out = X.layer_forward(e, 1, list(zip(ids, h)))
+    for i, sid in enumerate(ids):
+        K, Vv = kv.view(sid, 1, P[i] + 1)
+        K, Vv = K.astype(np.float64), Vv.astype(np.float64)
+        hb = bf16(h[i].astype(np.float64))
+        q = m.tensor("w_q", 1) @ hb
+        att = np.zeros(d)
+        for f in range(0, d, hd):
+            s = K[:, f:f + hd] @ q[f:f + hd] / np.sqrt(hd)
+            p = np.exp(s - s.max())
+            att[f:f + hd] = (p / p.sum()) @ Vv[:, f:f + hd]
+        s1 = K @ q / np.sqrt(d)
+        p1 = np.exp(s1 - s1.max())
+        att1 = (p1 / p1.sum()) @ Vv
+        assert relerr(att1, att) > 0.2  # the heads genuinely attend differently
+        mid = h[i] + m.tensor("w_o", 1) @ bf16(att)
+        want = mid + m.tensor("w_down", 1) @ bf16(np.maximum(m.tensor("w_up", 1) @ bf16(mid), 0.0))
+        assert relerr(out[i], want) <= TOL, (heads, sid, relerr(out[i], want))
+        mid1 = h[i] + m.tensor("w_o", 1) @ bf16(att1)
+        want1 = mid1 + m.tensor("w_down", 1) @ bf16(np.maximum(m.tensor("w_up", 1) @ bf16(mid1), 0.0))
+        assert relerr(out[i], want) < relerr(out[i], want1) / 3
+    e.close()

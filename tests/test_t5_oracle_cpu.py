@@ -9,8 +9,9 @@ import numpy as np
 from oracle import bindings as OB
 
 
-def np_t5_decode(m, prompt, max_new, seq_id, T):
-    """token-by-token greedy decode (technique never) of the T5-mode model, fp64."""
+def np_t5_decode(m, prompt, max_new, seq_id, T, heads=1):
+    """token-by-token greedy decode (technique never) of the T5-mode model, fp64; heads > 1:
+    self- and cross-attention per head of d / heads features, scale 1 / sqrt(d / heads)."""
     L, d = m.L, m.d
     W = {(n, l): m.tensor(n, l) for l in range(1, L + 1)
          for n in ("w_q", "w_k", "w_v", "w_o", "w_up", "w_down", "w_qc", "w_kc", "w_vc", "w_oc")}
@@ -18,21 +19,25 @@ def np_t5_decode(m, prompt, max_new, seq_id, T):
     E = np.stack([m.encoder_state(seq_id, t) for t in range(T)])
     K = [[] for _ in range(L)]
     Vv = [[] for _ in range(L)]
-    sc = 1.0 / np.sqrt(d)
+    hd = d // heads
+    sc = 1.0 / np.sqrt(hd)
 
     def softmax(x):
         e = np.exp(x - x.max())
         return e / e.sum()
 
+    def attend(Km, Vm, q):  # Km, Vm [n][d]
+        return np.concatenate([softmax(Km[:, f:f + hd] @ q[f:f + hd] * sc) @ Vm[:, f:f + hd]
+                               for f in range(0, d, hd)])
+
     def layer(l, h):
         q, k, v = W["w_q", l] @ h, W["w_k", l] @ h, W["w_v", l] @ h
         K[l - 1].append(k)
         Vv[l - 1].append(v)
-        p = softmax(np.array(K[l - 1]) @ q * sc)
-        mid = h + W["w_o", l] @ (p @ np.array(Vv[l - 1]))
+        mid = h + W["w_o", l] @ attend(np.array(K[l - 1]), np.array(Vv[l - 1]), q)
         qc = W["w_qc", l] @ mid
         kc, vc = E @ W["w_kc", l].T, E @ W["w_vc", l].T
-        mid = mid + W["w_oc", l] @ (softmax(kc @ qc * sc) @ vc)
+        mid = mid + W["w_oc", l] @ attend(kc, vc, qc)
         return mid + W["w_down", l] @ np.maximum(W["w_up", l] @ mid, 0.0)
 
     for tok in prompt[:-1]:
@@ -82,3 +87,24 @@ def test_encoder_states_are_seeded_and_bf16(port):
     assert np.all(np.abs(e) <= 1.0 / np.sqrt(32))
     bits = e.astype(np.float32).view(np.uint32)
     assert np.all((bits & 0xFFFF) == 0)  # exactly representable in bf16
+
+
+def test_t5_multi_head_matches_numpy_restatement(port):
+    L, d, V, T = 3, 32, 48, 5
+    reqs = [(0.0, [1, 2, 3], 6), (0.0, [7, 5], 4)]
+    cfg = OB.engine_config(L, d, V, 11, "never", max_batch=2, pool_blocks=64, block_capacity=4, round_bf16=True)
+    toks = {}
+    for heads in (1, 4):
+        m = port.model(L, d, V, 11, True, encoder_len=T, n_heads=heads)
+        t = m.run(cfg, OB.Workload.from_requests(reqs))
+        got = {s["id"]: s["tokens"] for s in t.sequences}
+        for sid, (_, prompt, mx) in enumerate(reqs):
+            assert got[sid] == np_t5_decode(m, prompt, mx, sid, T, heads), (heads, sid)
+        toks[heads] = t["it_conf"]
+    assert not np.array_equal(toks[1], toks[4])  # the head split changes the model
+
+
+def test_multi_head_needs_a_divisor(port):
+    import pytest
+    with pytest.raises(ValueError):
+        port.model(2, 32, 48, 1, True, encoder_len=4, n_heads=5)
