@@ -945,6 +945,289 @@ __device__ __forceinline__ void attn_settle(const DevState& st, AttnSmem& a) {
     named_bar(1, kAttnWarps * 32);
 }
 
+// The consumer warps of an attention pass (see attn_body); MH: the multi-head variant (extension,
+// st.attn_heads > 1), a separate instantiation so the reference's single-head loop is unchanged.
+template <int NJ, bool MH>
+__device__ __forceinline__ void attn_consumer(const DevState& st, AttnSmem& a, uint8_t* stages, int seq0,
+                                              bool persistent, float* mbuf) {
+    const Dims& dm = st.dm;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int dp = dm.dp, nchunk = dp / 8;
+    const int S = st.attn_stages;
+    const uint32_t blk_bytes = (uint32_t)dm.bc * dp * 2;
+    const uint32_t stage_bytes = (uint32_t)attn_stage_bytes(dm);  // K | V | q (>= merge buffer)
+    // ---------------- consumer warps ----------------
+    float2 q[NJ][4], o[NJ][4];  // this lane's features 8j..8j+7, j = lane + 32t, as pairs
+#pragma unroll
+    for (int t = 0; t < NJ; ++t)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) q[t][i] = o[t][i] = make_float2(0.f, 0.f);
+    float m = -INFINITY, l = 0.f;
+    // multi-head (extension, MH): head of feature chunk j = j / cph, cph =
+    // head_dim / 8 lanes of one chunk group t; every lane keeps its head's (m, l) per t
+    const int heads = MH ? st.attn_heads : 1, cph = st.attn_hd >> 3;
+    float mh[NJ], lh[NJ];
+#pragma unroll
+    for (int t = 0; t < NJ; ++t) mh[t] = -INFINITY, lh[t] = 0.f;
+    int npend = 0;
+    const int r0 = warp, r1 = warp + kAttnWarps;
+    // Persistent kernel: the consumer path is cold in the instruction cache at
+    // the start of every pass (the other phases' code evicted it), so the
+    // first real block used to take ~4x a steady-state one.  Run the block
+    // math once on whatever the first stage holds while its data is still in
+    // flight (results are discarded: the first real descriptor of a pass is
+    // always a segment start, which resets q, o, m, l).
+    bool warm = persistent && !(EL_DBG(st) & (1 << 21));
+    for (int seq = seq0;; ++seq) {
+        const int s = seq % S;
+        AttnDesc d;
+        if (warm) {
+            d = AttnDesc{0, 0, dm.bc, 0, 0, 1, {0, 0}};
+        } else {
+            mbar_wait(&a.full[s], (seq / S) & 1);
+            d = a.desc[s];
+        }
+        if (d.b < 0) {  // terminal descriptor: release its slot too (the ring persists across passes)
+            if (tid == 0) a.seq_next = seq + 1;
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&a.empty[s]);
+        }
+        if ((EL_DBG(st) & 32) && tid == 0) {
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+            if (blockIdx.x < 4 && seq < 60) st.dbg_ts[8192 + blockIdx.x * 128 + seq] = t;
+            if (seq == 0) st.dbg_ts[24576 + 4 * blockIdx.x + 1] = t;
+            st.dbg_ts[24576 + 4 * blockIdx.x + 2] = t;
+        }
+        if (d.b < 0) {
+            if (tid == 0) EL_ATT_CLK(5);
+            break;
+        }
+        if (tid == 0 && seq == seq0 && !warm) EL_ATT_CLK(4);
+        uint8_t* sb = stages + (size_t)s * stage_bytes;
+        const uint4* sk = reinterpret_cast<const uint4*>(sb);
+        const uint4* sv = reinterpret_cast<const uint4*>(sb + blk_bytes);
+        if (d.first) {
+            const float2* qs = reinterpret_cast<const float2*>(sb + 2 * blk_bytes);
+#pragma unroll
+            for (int t = 0; t < NJ; ++t) {
+                const int j = lane + 32 * t;
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const float2 x = qs[min(j, nchunk - 1) * 4 + i];
+                    // features past dp (j >= nchunk) get q = 0: their (clamped) K loads add nothing
+                    q[t][i] = (j < nchunk) ? make_float2(x.x * st.attn_scale, x.y * st.attn_scale)
+                                           : make_float2(0.f, 0.f);
+                    o[t][i] = make_float2(0.f, 0.f);
+                }
+            }
+            m = -INFINITY;
+            l = 0.f;
+#pragma unroll
+            for (int t = 0; t < NJ; ++t) mh[t] = -INFINITY, lh[t] = 0.f;
+        }
+        // Branch-free block math: both rows' K and V are loaded up front (row indices
+        // clamped to valid rows, feature chunks clamped to the last one), an invalid
+        // second row gets score -inf (weight 0 times finite data).
+        const int nrows = (EL_DBG(st) & 1) ? 0 : d.rows;
+        for (int rb = 0; rb < nrows; rb += 2 * kAttnWarps) {
+            const int ra = rb + r0;
+            if (ra >= nrows) break;  // warp-uniform: no row of this warp left in the block
+            const bool vc = rb + r1 < nrows;
+            const int rc = vc ? rb + r1 : ra;
+            uint4 ka[NJ], kc[NJ], xa[NJ], xc[NJ];
+#pragma unroll
+            for (int t = 0; t < NJ; ++t) {
+                const int j = min(lane + 32 * t, nchunk - 1);
+                ka[t] = sk[ra * nchunk + j];
+                kc[t] = sk[rc * nchunk + j];
+            }
+#pragma unroll
+            for (int t = 0; t < NJ; ++t) {
+                const int j = min(lane + 32 * t, nchunk - 1);
+                xa[t] = sv[ra * nchunk + j];
+                xc[t] = sv[rc * nchunk + j];
+            }
+            if constexpr (MH) {  // per-head scores, softmax state and rescale
+                float sa[NJ], sc[NJ];
+#pragma unroll
+                for (int t = 0; t < NJ; ++t) {
+                    const float2 x = dot8p2(ka[t], q[t], make_float2(0.f, 0.f));
+                    const float2 y = dot8p2(kc[t], q[t], make_float2(0.f, 0.f));
+                    sa[t] = x.x + x.y;
+                    sc[t] = y.x + y.y;
+                }
+                for (int off = 1; off < cph; off <<= 1)
+#pragma unroll
+                    for (int t = 0; t < NJ; ++t) {
+                        sa[t] += __shfl_xor_sync(0xffffffffu, sa[t], off);
+                        sc[t] += __shfl_xor_sync(0xffffffffu, sc[t], off);
+                    }
+#pragma unroll
+                for (int t = 0; t < NJ; ++t) {
+                    if (!vc) sc[t] = -INFINITY;
+                    const float mn = fmaxf(mh[t], fmaxf(sa[t], sc[t]));
+                    const float pa = __expf(sa[t] - mn), pc = __expf(sc[t] - mn), alpha = __expf(mh[t] - mn);
+                    const float2 al = make_float2(alpha, alpha);
+                    lh[t] = lh[t] * alpha + (pa + pc);
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) o[t][i] = __fmul2_rn(o[t][i], al);
+                    axpy8p2(pa, xa[t], o[t]);
+                    axpy8p2(pc, xc[t], o[t]);
+                    mh[t] = mn;
+                }
+                continue;
+            }
+            float2 a2 = make_float2(0.f, 0.f), c2 = make_float2(0.f, 0.f);
+#pragma unroll
+            for (int t = 0; t < NJ; ++t) {
+                a2 = dot8p2(ka[t], q[t], a2);
+                c2 = dot8p2(kc[t], q[t], c2);
+            }
+            float sa = a2.x + a2.y, sc = c2.x + c2.y;
+#pragma unroll
+            for (int off = 16; off; off >>= 1) {
+                sa += __shfl_xor_sync(0xffffffffu, sa, off);
+                sc += __shfl_xor_sync(0xffffffffu, sc, off);
+            }
+            if (!vc) sc = -INFINITY;
+            const float m_new = fmaxf(m, fmaxf(sa, sc));
+            const float pa = __expf(sa - m_new), pc = __expf(sc - m_new);
+            if (m_new != m) {  // warp-uniform
+                const float alpha = __expf(m - m_new);
+                const float2 al = make_float2(alpha, alpha);
+                l *= alpha;
+#pragma unroll
+                for (int t = 0; t < NJ; ++t)
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) o[t][i] = __fmul2_rn(o[t][i], al);
+                m = m_new;
+            }
+            l += pa + pc;
+#pragma unroll
+            for (int t = 0; t < NJ; ++t) {
+                axpy8p2(pa, xa[t], o[t]);
+                axpy8p2(pc, xc[t], o[t]);
+            }
+        }
+        if ((EL_DBG(st) & 32) && tid == 0 && blockIdx.x < 4 && seq < 60) {  // block processed (before release)
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+            st.dbg_ts[8192 + 2048 + blockIdx.x * 128 + seq] = t;
+        }
+        if (warm) {  // dry run done: now the real first block of this stage
+            warm = false;
+            --seq;
+            continue;
+        }
+        if (!d.last || (EL_DBG(st) & 4)) {
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&a.empty[s]);
+            continue;
+        }
+
+        // ---- end of segment: merge the 8 warps in fixed order, publish the
+        //      segment's partial (o, m, l) and queue its completion count ----
+        float* merge = mbuf ? mbuf : reinterpret_cast<float*>(sb);  // [8][dp] fp32
+        if (mbuf) {  // the stage is free as soon as this warp is done with it
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&a.empty[s]);
+        }
+        named_bar(1, kAttnWarps * 32);  // (also: the previous merge's readers are done with mbuf / wm / wl)
+        if constexpr (MH) {
+#pragma unroll
+            for (int t = 0; t < NJ; ++t) {
+                const int j = lane + 32 * t;
+                if (j < nchunk && j % cph == 0) {
+                    a.wmh[warp][j / cph] = mh[t];
+                    a.wlh[warp][j / cph] = lh[t];
+                }
+            }
+        } else if (lane == 0) {
+            a.wm[warp] = m;
+            a.wl[warp] = l;
+        }
+#pragma unroll
+        for (int t = 0; t < NJ; ++t) {
+            const int j = lane + 32 * t;
+            if (j < nchunk) {
+                float4* dst = reinterpret_cast<float4*>(merge + (size_t)warp * dp + j * 8);
+                dst[0] = make_float4(o[t][0].x, o[t][0].y, o[t][1].x, o[t][1].y);
+                dst[1] = make_float4(o[t][2].x, o[t][2].y, o[t][3].x, o[t][3].y);
+            }
+        }
+        named_bar(1, kAttnWarps * 32);
+        if constexpr (MH) {  // per feature: its head's max / weights over the 8 warps (fixed order)
+            const size_t pidx = (size_t)d.b * st.attn_max_chunks + d.c;
+            const int hd = st.attn_hd;
+            for (int i = tid; i < dp; i += kAttnWarps * 32) {
+                const int h = i / hd;
+                float M = -INFINITY;
+#pragma unroll
+                for (int w = 0; w < kAttnWarps; ++w) M = fmaxf(M, a.wmh[w][h]);
+                float acc = 0.f, Lsum = 0.f;
+#pragma unroll
+                for (int w = 0; w < kAttnWarps; ++w) {
+                    const float sw = (a.wmh[w][h] == -INFINITY) ? 0.f : __expf(a.wmh[w][h] - M);
+                    acc += sw * merge[(size_t)w * dp + i];
+                    Lsum += sw * a.wlh[w][h];
+                }
+                st.attn_o[pidx * dp + i] = acc;
+                if (i % hd == 0) {
+                    st.attn_ml[(pidx * heads + h) * 2 + 0] = M;
+                    st.attn_ml[(pidx * heads + h) * 2 + 1] = Lsum;
+                }
+            }
+            if (tid == 0) {
+                a.pend_b[a.npend] = d.b;
+                a.pend_n[a.npend] = d.nseg;
+                ++a.npend;
+            }
+            if (!mbuf) {
+                named_bar(1, kAttnWarps * 32);
+                if (lane == 0) mbar_arrive(&a.empty[s]);
+            }
+            ++npend;
+            continue;
+        }
+        float M = -INFINITY;
+#pragma unroll
+        for (int w = 0; w < kAttnWarps; ++w) M = fmaxf(M, a.wm[w]);
+        float scw[kAttnWarps], Lsum = 0.f;
+#pragma unroll
+        for (int w = 0; w < kAttnWarps; ++w) {
+            scw[w] = (a.wm[w] == -INFINITY) ? 0.f : __expf(a.wm[w] - M);
+            Lsum += scw[w] * a.wl[w];
+        }
+        const size_t pidx = (size_t)d.b * st.attn_max_chunks + d.c;
+        for (int i = tid; i < dp; i += kAttnWarps * 32) {
+            float acc = 0.f;
+#pragma unroll
+            for (int w = 0; w < kAttnWarps; ++w) acc += scw[w] * merge[(size_t)w * dp + i];
+            st.attn_o[pidx * dp + i] = acc;
+        }
+        if (tid == 0) {
+            st.attn_ml[pidx * 2 + 0] = M;
+            st.attn_ml[pidx * 2 + 1] = Lsum;
+            a.pend_b[a.npend] = d.b;
+            a.pend_n[a.npend] = d.nseg;
+            ++a.npend;
+        }
+        if (!mbuf) {  // the merge lived in the stage: release it once every warp has read it
+            named_bar(1, kAttnWarps * 32);
+            if (lane == 0) mbar_arrive(&a.empty[s]);
+        }
+        if (EL_DEBUG && ((EL_DBG(st) & 8) || npend + 1 == kAttnPend)) {  // probe: settle every segment
+            attn_settle(st, a);
+            npend = 0;
+        }
+        ++npend;  // (<= rows <= kAttnPend: the list cannot overflow)
+    }
+    attn_settle(st, a);
+    if (tid == 0) EL_ATT_CLK(6);
+    pdl_trigger();
+}
+
 // persistent: called from the persistent kernel -- a.pref is already valid and
 // no programmatic-dependent-launch deferral is needed (every input is ready).
 template <int NJ>
@@ -1172,277 +1455,10 @@ __device__ __forceinline__ void attn_body(const DevState& st, AttnSmem& a, uint8
             mbar_arrive(&a.full[s]);
         }
         if (persistent && pre && layer < dm.L) gather(layer + 1);  // while the consumers finish
+    } else if (st.attn_heads > 1) {
+        attn_consumer<NJ, true>(st, a, stages, seq0, persistent, mbuf);
     } else {
-        // ---------------- consumer warps ----------------
-        float2 q[NJ][4], o[NJ][4];  // this lane's features 8j..8j+7, j = lane + 32t, as pairs
-#pragma unroll
-        for (int t = 0; t < NJ; ++t)
-#pragma unroll
-            for (int i = 0; i < 4; ++i) q[t][i] = o[t][i] = make_float2(0.f, 0.f);
-        float m = -INFINITY, l = 0.f;
-        // multi-head (T5 mode, st.attn_heads > 1): head of feature chunk j = j / cph, cph =
-        // head_dim / 8 lanes of one chunk group t; every lane keeps its head's (m, l) per t
-        const int heads = st.attn_heads, cph = st.attn_hd >> 3;
-        float mh[NJ], lh[NJ];
-#pragma unroll
-        for (int t = 0; t < NJ; ++t) mh[t] = -INFINITY, lh[t] = 0.f;
-        int npend = 0;
-        const int r0 = warp, r1 = warp + kAttnWarps;
-        // Persistent kernel: the consumer path is cold in the instruction cache at
-        // the start of every pass (the other phases' code evicted it), so the
-        // first real block used to take ~4x a steady-state one.  Run the block
-        // math once on whatever the first stage holds while its data is still in
-        // flight (results are discarded: the first real descriptor of a pass is
-        // always a segment start, which resets q, o, m, l).
-        bool warm = persistent && !(EL_DBG(st) & (1 << 21));
-        for (int seq = seq0;; ++seq) {
-            const int s = seq % S;
-            AttnDesc d;
-            if (warm) {
-                d = AttnDesc{0, 0, dm.bc, 0, 0, 1, {0, 0}};
-            } else {
-                mbar_wait(&a.full[s], (seq / S) & 1);
-                d = a.desc[s];
-            }
-            if (d.b < 0) {  // terminal descriptor: release its slot too (the ring persists across passes)
-                if (tid == 0) a.seq_next = seq + 1;
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&a.empty[s]);
-            }
-            if ((EL_DBG(st) & 32) && tid == 0) {
-                unsigned long long t;
-                asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-                if (blockIdx.x < 4 && seq < 60) st.dbg_ts[8192 + blockIdx.x * 128 + seq] = t;
-                if (seq == 0) st.dbg_ts[24576 + 4 * blockIdx.x + 1] = t;
-                st.dbg_ts[24576 + 4 * blockIdx.x + 2] = t;
-            }
-            if (d.b < 0) {
-                if (tid == 0) EL_ATT_CLK(5);
-                break;
-            }
-            if (tid == 0 && seq == seq0 && !warm) EL_ATT_CLK(4);
-            uint8_t* sb = stages + (size_t)s * stage_bytes;
-            const uint4* sk = reinterpret_cast<const uint4*>(sb);
-            const uint4* sv = reinterpret_cast<const uint4*>(sb + blk_bytes);
-            if (d.first) {
-                const float2* qs = reinterpret_cast<const float2*>(sb + 2 * blk_bytes);
-#pragma unroll
-                for (int t = 0; t < NJ; ++t) {
-                    const int j = lane + 32 * t;
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) {
-                        const float2 x = qs[min(j, nchunk - 1) * 4 + i];
-                        // features past dp (j >= nchunk) get q = 0: their (clamped) K loads add nothing
-                        q[t][i] = (j < nchunk) ? make_float2(x.x * st.attn_scale, x.y * st.attn_scale)
-                                               : make_float2(0.f, 0.f);
-                        o[t][i] = make_float2(0.f, 0.f);
-                    }
-                }
-                m = -INFINITY;
-                l = 0.f;
-#pragma unroll
-                for (int t = 0; t < NJ; ++t) mh[t] = -INFINITY, lh[t] = 0.f;
-            }
-            // Branch-free block math: both rows' K and V are loaded up front (row indices
-            // clamped to valid rows, feature chunks clamped to the last one), an invalid
-            // second row gets score -inf (weight 0 times finite data).
-            const int nrows = (EL_DBG(st) & 1) ? 0 : d.rows;
-            for (int rb = 0; rb < nrows; rb += 2 * kAttnWarps) {
-                const int ra = rb + r0;
-                if (ra >= nrows) break;  // warp-uniform: no row of this warp left in the block
-                const bool vc = rb + r1 < nrows;
-                const int rc = vc ? rb + r1 : ra;
-                uint4 ka[NJ], kc[NJ], xa[NJ], xc[NJ];
-#pragma unroll
-                for (int t = 0; t < NJ; ++t) {
-                    const int j = min(lane + 32 * t, nchunk - 1);
-                    ka[t] = sk[ra * nchunk + j];
-                    kc[t] = sk[rc * nchunk + j];
-                }
-#pragma unroll
-                for (int t = 0; t < NJ; ++t) {
-                    const int j = min(lane + 32 * t, nchunk - 1);
-                    xa[t] = sv[ra * nchunk + j];
-                    xc[t] = sv[rc * nchunk + j];
-                }
-                if (heads > 1) {  // (warp-uniform) per-head scores, softmax state and rescale
-                    float sa[NJ], sc[NJ];
-#pragma unroll
-                    for (int t = 0; t < NJ; ++t) {
-                        const float2 x = dot8p2(ka[t], q[t], make_float2(0.f, 0.f));
-                        const float2 y = dot8p2(kc[t], q[t], make_float2(0.f, 0.f));
-                        sa[t] = x.x + x.y;
-                        sc[t] = y.x + y.y;
-                    }
-                    for (int off = 1; off < cph; off <<= 1)
-#pragma unroll
-                        for (int t = 0; t < NJ; ++t) {
-                            sa[t] += __shfl_xor_sync(0xffffffffu, sa[t], off);
-                            sc[t] += __shfl_xor_sync(0xffffffffu, sc[t], off);
-                        }
-#pragma unroll
-                    for (int t = 0; t < NJ; ++t) {
-                        if (!vc) sc[t] = -INFINITY;
-                        const float mn = fmaxf(mh[t], fmaxf(sa[t], sc[t]));
-                        const float pa = __expf(sa[t] - mn), pc = __expf(sc[t] - mn), alpha = __expf(mh[t] - mn);
-                        const float2 al = make_float2(alpha, alpha);
-                        lh[t] = lh[t] * alpha + (pa + pc);
-#pragma unroll
-                        for (int i = 0; i < 4; ++i) o[t][i] = __fmul2_rn(o[t][i], al);
-                        axpy8p2(pa, xa[t], o[t]);
-                        axpy8p2(pc, xc[t], o[t]);
-                        mh[t] = mn;
-                    }
-                    continue;
-                }
-                float2 a2 = make_float2(0.f, 0.f), c2 = make_float2(0.f, 0.f);
-#pragma unroll
-                for (int t = 0; t < NJ; ++t) {
-                    a2 = dot8p2(ka[t], q[t], a2);
-                    c2 = dot8p2(kc[t], q[t], c2);
-                }
-                float sa = a2.x + a2.y, sc = c2.x + c2.y;
-#pragma unroll
-                for (int off = 16; off; off >>= 1) {
-                    sa += __shfl_xor_sync(0xffffffffu, sa, off);
-                    sc += __shfl_xor_sync(0xffffffffu, sc, off);
-                }
-                if (!vc) sc = -INFINITY;
-                const float m_new = fmaxf(m, fmaxf(sa, sc));
-                const float pa = __expf(sa - m_new), pc = __expf(sc - m_new);
-                if (m_new != m) {  // warp-uniform
-                    const float alpha = __expf(m - m_new);
-                    const float2 al = make_float2(alpha, alpha);
-                    l *= alpha;
-#pragma unroll
-                    for (int t = 0; t < NJ; ++t)
-#pragma unroll
-                        for (int i = 0; i < 4; ++i) o[t][i] = __fmul2_rn(o[t][i], al);
-                    m = m_new;
-                }
-                l += pa + pc;
-#pragma unroll
-                for (int t = 0; t < NJ; ++t) {
-                    axpy8p2(pa, xa[t], o[t]);
-                    axpy8p2(pc, xc[t], o[t]);
-                }
-            }
-            if ((EL_DBG(st) & 32) && tid == 0 && blockIdx.x < 4 && seq < 60) {  // block processed (before release)
-                unsigned long long t;
-                asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-                st.dbg_ts[8192 + 2048 + blockIdx.x * 128 + seq] = t;
-            }
-            if (warm) {  // dry run done: now the real first block of this stage
-                warm = false;
-                --seq;
-                continue;
-            }
-            if (!d.last || (EL_DBG(st) & 4)) {
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&a.empty[s]);
-                continue;
-            }
-
-            // ---- end of segment: merge the 8 warps in fixed order, publish the
-            //      segment's partial (o, m, l) and queue its completion count ----
-            float* merge = mbuf ? mbuf : reinterpret_cast<float*>(sb);  // [8][dp] fp32
-            if (mbuf) {  // the stage is free as soon as this warp is done with it
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&a.empty[s]);
-            }
-            named_bar(1, kAttnWarps * 32);  // (also: the previous merge's readers are done with mbuf / wm / wl)
-            if (heads > 1) {
-#pragma unroll
-                for (int t = 0; t < NJ; ++t) {
-                    const int j = lane + 32 * t;
-                    if (j < nchunk && j % cph == 0) {
-                        a.wmh[warp][j / cph] = mh[t];
-                        a.wlh[warp][j / cph] = lh[t];
-                    }
-                }
-            } else if (lane == 0) {
-                a.wm[warp] = m;
-                a.wl[warp] = l;
-            }
-#pragma unroll
-            for (int t = 0; t < NJ; ++t) {
-                const int j = lane + 32 * t;
-                if (j < nchunk) {
-                    float4* dst = reinterpret_cast<float4*>(merge + (size_t)warp * dp + j * 8);
-                    dst[0] = make_float4(o[t][0].x, o[t][0].y, o[t][1].x, o[t][1].y);
-                    dst[1] = make_float4(o[t][2].x, o[t][2].y, o[t][3].x, o[t][3].y);
-                }
-            }
-            named_bar(1, kAttnWarps * 32);
-            if (heads > 1) {  // per feature: its head's max / weights over the 8 warps (fixed order)
-                const size_t pidx = (size_t)d.b * st.attn_max_chunks + d.c;
-                const int hd = st.attn_hd;
-                for (int i = tid; i < dp; i += kAttnWarps * 32) {
-                    const int h = i / hd;
-                    float M = -INFINITY;
-#pragma unroll
-                    for (int w = 0; w < kAttnWarps; ++w) M = fmaxf(M, a.wmh[w][h]);
-                    float acc = 0.f, Lsum = 0.f;
-#pragma unroll
-                    for (int w = 0; w < kAttnWarps; ++w) {
-                        const float sw = (a.wmh[w][h] == -INFINITY) ? 0.f : __expf(a.wmh[w][h] - M);
-                        acc += sw * merge[(size_t)w * dp + i];
-                        Lsum += sw * a.wlh[w][h];
-                    }
-                    st.attn_o[pidx * dp + i] = acc;
-                    if (i % hd == 0) {
-                        st.attn_ml[(pidx * heads + h) * 2 + 0] = M;
-                        st.attn_ml[(pidx * heads + h) * 2 + 1] = Lsum;
-                    }
-                }
-                if (tid == 0) {
-                    a.pend_b[a.npend] = d.b;
-                    a.pend_n[a.npend] = d.nseg;
-                    ++a.npend;
-                }
-                if (!mbuf) {
-                    named_bar(1, kAttnWarps * 32);
-                    if (lane == 0) mbar_arrive(&a.empty[s]);
-                }
-                ++npend;
-                continue;
-            }
-            float M = -INFINITY;
-#pragma unroll
-            for (int w = 0; w < kAttnWarps; ++w) M = fmaxf(M, a.wm[w]);
-            float scw[kAttnWarps], Lsum = 0.f;
-#pragma unroll
-            for (int w = 0; w < kAttnWarps; ++w) {
-                scw[w] = (a.wm[w] == -INFINITY) ? 0.f : __expf(a.wm[w] - M);
-                Lsum += scw[w] * a.wl[w];
-            }
-            const size_t pidx = (size_t)d.b * st.attn_max_chunks + d.c;
-            for (int i = tid; i < dp; i += kAttnWarps * 32) {
-                float acc = 0.f;
-#pragma unroll
-                for (int w = 0; w < kAttnWarps; ++w) acc += scw[w] * merge[(size_t)w * dp + i];
-                st.attn_o[pidx * dp + i] = acc;
-            }
-            if (tid == 0) {
-                st.attn_ml[pidx * 2 + 0] = M;
-                st.attn_ml[pidx * 2 + 1] = Lsum;
-                a.pend_b[a.npend] = d.b;
-                a.pend_n[a.npend] = d.nseg;
-                ++a.npend;
-            }
-            if (!mbuf) {  // the merge lived in the stage: release it once every warp has read it
-                named_bar(1, kAttnWarps * 32);
-                if (lane == 0) mbar_arrive(&a.empty[s]);
-            }
-            if (EL_DEBUG && ((EL_DBG(st) & 8) || npend + 1 == kAttnPend)) {  // probe: settle every segment
-                attn_settle(st, a);
-                npend = 0;
-            }
-            ++npend;  // (<= rows <= kAttnPend: the list cannot overflow)
-        }
-        attn_settle(st, a);
-        if (tid == 0) EL_ATT_CLK(6);
-        pdl_trigger();
+        attn_consumer<NJ, false>(st, a, stages, seq0, persistent, mbuf);
     }
 }
 
