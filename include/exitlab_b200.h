@@ -75,6 +75,10 @@ typedef struct {
      * split into n_heads heads of d_model / n_heads features (own softmax, scale 1/sqrt(head_dim));
      * 0 or 1 = the reference's single head.  head_dim: 8, 16, 32, 64, 128 or 256; n_heads <= 32. */
     int n_heads;
+    /* T5 mode: > 0 runs a real encoder stack of this many bidirectional norm-free layers (own
+     * seeded weights) over seeded encoder input ids at admission, instead of seeded encoder
+     * states (extension; encoder_len <= 256). */
+    int encoder_layers;
 } el_engine_config;
 
 typedef struct el_engine el_engine;
@@ -126,6 +130,8 @@ int el_decode_records(el_engine* e, int first, int n, int32_t* tokens, int32_t* 
 int el_decode_iterations_done(el_engine* e);
 int el_set_fixed_confidences(el_engine* e, const float* conf /* [L][B] */);
 int el_session_kv(el_engine* e, int row, int layer, int pos, float* k, float* v);
+/* T5 mode: the static cross K/V of a session row at `layer` (encoder_len x d_model each) */
+int el_session_cross_kv(el_engine* e, int row, int layer, float* k, float* v);
 int el_session_hidden(el_engine* e, int parity, float* out /* [B][d] */);
 int el_session_block_table(el_engine* e, int row, int32_t* out /* [L][bpl] */, int bpl_cap);
 

@@ -231,7 +231,7 @@ class _Lib:
         return self.fn("last_error")().decode()
 
     # ---- model ----
-    def model(self, n_layers, d_model, vocab, seed, round_bf16=False, encoder_len=0, n_heads=1):
+    def model(self, n_layers, d_model, vocab, seed, round_bf16=False, encoder_len=0, n_heads=1, encoder_layers=0):
         """encoder_len > 0: the T5-mode extension (cross-attention over synthetic
         encoder states) -- the C restatement only; the compiled reference has no
         encoder, so parity of that mode is not pinned by it.  n_heads > 1 (extension, not in
@@ -249,6 +249,9 @@ class _Lib:
         m.encoder_len = encoder_len
         m.n_heads = n_heads
         if n_heads != 1 and self.fn("model_set_heads")(C.c_void_p(h), int(n_heads)):
+            raise ValueError(self.err())
+        m.encoder_layers = encoder_layers
+        if encoder_layers and self.fn("model_set_encoder_layers")(C.c_void_p(h), int(encoder_layers)):
             raise ValueError(self.err())
         return m
 
@@ -366,13 +369,21 @@ class Model:
         self.lib.fn("encoder_state")(self.h, seq_id, t, _p(out, C.c_double))
         return out
 
+    def encoder_token(self, seq_id, t):
+        """seeded encoder input id of (sequence, position) (T5 encoder stack)"""
+        f = self.lib.fn("encoder_token")
+        f.argtypes = [C.c_void_p, C.c_int, C.c_int]
+        return int(f(self.h, seq_id, t))
+
     def tensor(self, which, layer=0):
         names = {"embedding": 0, "lm_head": 1, "probe_w": 2, "probe_b": 3, "w_q": 4, "w_k": 5, "w_v": 6,
-                 "w_o": 7, "w_up": 8, "w_down": 9, "w_qc": 10, "w_kc": 11, "w_vc": 12, "w_oc": 13}
+                 "w_o": 7, "w_up": 8, "w_down": 9, "w_qc": 10, "w_kc": 11, "w_vc": 12, "w_oc": 13,
+                 "e_q": 20, "e_k": 21, "e_v": 22, "e_o": 23, "e_up": 24, "e_down": 25}
         w = names[which] if isinstance(which, str) else which
         d, V = self.d, self.V
         shape = {0: (V, d), 1: (V, d), 2: (d,), 3: (1,), 4: (d, d), 5: (d, d), 6: (d, d), 7: (d, d),
-                 8: (4 * d, d), 9: (d, 4 * d), 10: (d, d), 11: (d, d), 12: (d, d), 13: (d, d)}[w]
+                 8: (4 * d, d), 9: (d, 4 * d), 10: (d, d), 11: (d, d), 12: (d, d), 13: (d, d),
+                 20: (d, d), 21: (d, d), 22: (d, d), 23: (d, d), 24: (4 * d, d), 25: (d, 4 * d)}[w]
         out = np.zeros(int(np.prod(shape)))
         rc = self.lib.fn("model_tensor")(self.h, w, layer, _p(out, C.c_double), out.size)
         if rc:

@@ -89,6 +89,14 @@ struct eo_model {
        heads of d / n_heads features, each with its own softmax and scale 1 / sqrt(d / n_heads);
        1 = the reference's single head.  Sessions with heads use the layer_forward restatement. */
     int n_heads;
+    /* T5 encoder stack (extension): enc_layers > 0 replaces the seeded encoder states by the
+       output of enc_layers bidirectional norm-free blocks (the decoder block without the causal
+       mask) over the embeddings of seeded encoder input ids; outputs cached per sequence id */
+    int enc_layers;
+    double** we;   /* per encoder layer: q, k, v, o (d x d), up (4d x d), down (d x 4d) */
+    int n_enc_cache, cap_enc_cache;
+    int* enc_cache_id;
+    double** enc_cache;  /* [T][d] per cached sequence */
 };
 static const int kLayerTensors = 6;
 
@@ -116,9 +124,36 @@ int eo_model_set_heads(eo_model* m, int n_heads) {
     return EO_OK;
 }
 
+static const double* encoder_output(const eo_model* m, int seq_id);
 void eo_encoder_state(const eo_model* m, int seq_id, int t, double* out) {
+    if (m->enc_layers > 0) {
+        memcpy(out, encoder_output(m, seq_id) + (size_t)t * m->d, sizeof(double) * (size_t)m->d);
+        return;
+    }
     eo_seeded_vector(m->d, eo_splitmix64_at(m->enc_seed, ((uint64_t)seq_id << 20) | (uint64_t)t), out);
     if (m->round_bf16) round_all(out, (size_t)m->d);
+}
+/* encoder input id of (sequence, position): uniform over [1, V) like gen_workload's prompts */
+int eo_encoder_token(const eo_model* m, int seq_id, int t) {
+    return 1 + (int)(eo_splitmix64_at(m->enc_seed ^ 0x544F4Bu, ((uint64_t)seq_id << 20) | (uint64_t)t) %
+                     (uint64_t)(m->V - 1));
+}
+/* encoder weights: tags after the cross weights, 4 + 6L + 4L + 6i + k */
+int eo_model_set_encoder_layers(eo_model* m, int n) {
+    if (n < 0 || (n > 0 && m->enc_len == 0)) { set_err("ModelConfig: encoder_layers needs T5 mode"); return EO_INVALID_ARGUMENT; }
+    if (m->we) { set_err("encoder layers already set"); return EO_INVALID_ARGUMENT; }
+    const int d = m->d;
+    m->enc_layers = n;
+    m->we = (double**)calloc((size_t)(n > 0 ? n : 1) * 6, sizeof(double*));
+    for (int i = 0; i < n; ++i)
+        for (int k = 0; k < 6; ++k) {
+            const int r = k == 4 ? 4 * d : d, c = k == 5 ? 4 * d : d;
+            double* t = (double*)malloc(sizeof(double) * (size_t)r * c);
+            eo_seeded_matrix(r, c, eo_splitmix64_at(m->seed, 4 + (uint64_t)m->L * 10 + (uint64_t)i * 6 + k), t);
+            if (m->round_bf16) round_all(t, (size_t)r * c);
+            m->we[i * 6 + k] = t;
+        }
+    return EO_OK;
 }
 
 eo_model* eo_model_seeded_t5(int L, int d, int V, uint64_t seed, int round_bf16, int enc_len) {
@@ -171,6 +206,12 @@ eo_model* eo_model_seeded_t5(int L, int d, int V, uint64_t seed, int round_bf16,
 
 void eo_model_free(eo_model* m) {
     if (!m) return;
+    if (m->we) {
+        for (int i = 0; i < m->enc_layers * 6; ++i) free(m->we[i]);
+        free(m->we);
+    }
+    for (int i = 0; i < m->n_enc_cache; ++i) free(m->enc_cache[i]);
+    free(m->enc_cache); free(m->enc_cache_id);
     if (m->wc) {
         for (int i = 0; i < m->L * kCrossTensors; ++i) free(m->wc[i]);
         free(m->wc);
@@ -185,6 +226,11 @@ int eo_model_tensor(const eo_model* m, int which, int layer, double* out, int64_
     else if (which == 1) { src = m->lm; n = (int64_t)m->V * m->d; }
     else if (which == 2) { src = m->pw; n = m->d; }
     else if (which == 3) { src = &m->pb; n = 1; }
+    else if (which >= 20 && which < 26) {  /* T5 encoder stack: q, k, v, o, up, down */
+        if (!m->we || layer < 1 || layer > m->enc_layers) { set_err("bad tensor"); return EO_INVALID_ARGUMENT; }
+        src = m->we[(layer - 1) * 6 + (which - 20)];
+        n = (int64_t)m->d * m->d * ((which == 24 || which == 25) ? 4 : 1);
+    }
     else if (which >= 10 && which < 10 + kCrossTensors) {  /* T5 mode: q_c, k_c, v_c, o_c */
         if (!m->wc || layer < 1 || layer > m->L) { set_err("bad tensor"); return EO_INVALID_ARGUMENT; }
         src = m->wc[(layer - 1) * kCrossTensors + (which - 10)]; n = (int64_t)m->d * m->d;
@@ -456,6 +502,56 @@ static const double* mat_key_row(const void* c, int p) {
 static const double* mat_val_row(const void* c, int p) {
     const mat_ctx* x = ((const mat_ctx* const*)c)[1];
     return x->rows + (size_t)p * x->d;
+}
+
+/* The encoder stack over one sequence's T seeded input ids (fp64; bf16-rounded output when the
+   model is): X_0[t] = embedding(id_t); per layer X <- mid + W_down ReLU(W_up mid), mid = X + W_o a,
+   a_t = attention of q_t = W_q X_t over every position's (W_k X, W_v X) -- no causal mask. */
+static const double* encoder_output(const eo_model* m, int seq_id) {
+    eo_model* mm = (eo_model*)m;  /* the cache is logically const */
+    for (int i = 0; i < m->n_enc_cache; ++i)
+        if (m->enc_cache_id[i] == seq_id) return m->enc_cache[i];
+    const int d = m->d, T = m->enc_len;
+    double* X = (double*)malloc(sizeof(double) * (size_t)T * d);
+    double *Q = (double*)malloc(sizeof(double) * (size_t)T * d), *K = (double*)malloc(sizeof(double) * (size_t)T * d);
+    double *Vv = (double*)malloc(sizeof(double) * (size_t)T * d), *A = (double*)malloc(sizeof(double) * (size_t)d);
+    double *P = (double*)malloc(sizeof(double) * (size_t)d), *U = (double*)malloc(sizeof(double) * (size_t)4 * d);
+    double *sc = (double*)malloc(sizeof(double) * (size_t)T), *pr = (double*)malloc(sizeof(double) * (size_t)T);
+    double* mid = (double*)malloc(sizeof(double) * (size_t)T * d);
+    for (int t = 0; t < T; ++t)
+        memcpy(X + (size_t)t * d, m->emb + (size_t)eo_encoder_token(m, seq_id, t) * d, sizeof(double) * (size_t)d);
+    for (int l = 0; l < m->enc_layers; ++l) {
+        double* const* w = m->we + (size_t)l * 6;
+        for (int t = 0; t < T; ++t) {
+            matvec(w[0], d, d, X + (size_t)t * d, Q + (size_t)t * d);
+            matvec(w[1], d, d, X + (size_t)t * d, K + (size_t)t * d);
+            matvec(w[2], d, d, X + (size_t)t * d, Vv + (size_t)t * d);
+        }
+        const mat_ctx ck = {K, d}, cv = {Vv, d};
+        const mat_ctx* both[2] = {&ck, &cv};
+        for (int t = 0; t < T; ++t) {
+            attend_heads(d, m->n_heads, Q + (size_t)t * d, T, mat_key_row, mat_val_row, both, sc, pr, A);
+            matvec(w[3], d, d, A, P);
+            for (int i = 0; i < d; ++i) mid[(size_t)t * d + i] = X[(size_t)t * d + i] + P[i];
+        }
+        for (int t = 0; t < T; ++t) {
+            matvec(w[4], 4 * d, d, mid + (size_t)t * d, U);
+            for (int i = 0; i < 4 * d; ++i) U[i] = U[i] > 0.0 ? U[i] : 0.0;
+            matvec(w[5], d, 4 * d, U, P);
+            for (int i = 0; i < d; ++i) X[(size_t)t * d + i] = mid[(size_t)t * d + i] + P[i];
+        }
+    }
+    if (m->round_bf16) round_all(X, (size_t)T * d);
+    free(Q); free(K); free(Vv); free(A); free(P); free(U); free(sc); free(pr); free(mid);
+    if (mm->n_enc_cache == mm->cap_enc_cache) {
+        mm->cap_enc_cache = mm->cap_enc_cache ? 2 * mm->cap_enc_cache : 64;
+        mm->enc_cache_id = (int*)realloc(mm->enc_cache_id, sizeof(int) * (size_t)mm->cap_enc_cache);
+        mm->enc_cache = (double**)realloc(mm->enc_cache, sizeof(double*) * (size_t)mm->cap_enc_cache);
+    }
+    mm->enc_cache_id[mm->n_enc_cache] = seq_id;
+    mm->enc_cache[mm->n_enc_cache] = X;
+    ++mm->n_enc_cache;
+    return X;
 }
 
 /* h[B][d] in, out[B][d] out (out may not alias h). ids[B] are seq ids. */

@@ -68,6 +68,10 @@ void eo_encoder_state(const eo_model* m, int seq_id, int t, double* out);
 /* Extension: split self- (and in T5 mode cross-) attention into n_heads heads (d_model / n_heads
    features each, own softmax, scale 1 / sqrt(d_model / n_heads)); the reference has one head. */
 int eo_model_set_heads(eo_model* m, int n_heads);
+/* T5 mode: a real encoder stack of n bidirectional norm-free layers (own seeded weights, tags
+   4 + 10L + 6i + k) over seeded encoder input ids replaces the seeded encoder states. */
+int eo_model_set_encoder_layers(eo_model* m, int n);
+int eo_encoder_token(const eo_model* m, int seq_id, int t);
 void eo_model_free(eo_model* m);
 /* which: 0 embedding, 1 lm_head, 2 probe_w, 3 probe_b, 4+k: layer tensor k in
  * {q,k,v,o,up,down}; layer is 1-based (ignored for globals). Copies into out. */

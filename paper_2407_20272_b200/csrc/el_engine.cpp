@@ -195,6 +195,12 @@ struct el_engine {
     // T5 mode (encoder_len > 0): cross weights, static encoder K/V pool + tables, encoder-state staging
     DevBuf<uint16_t> wqc, wkvc, woc, ckpool, cvpool, enc_act;
     DevBuf<int> ctables, xslot, xid;
+    // T5 encoder stack (encoder_layers > 0): its weights, the scratch K/V of one launch's sequences
+    // (one block table per (local sequence, encoder layer)), the plan switch of mplan_for
+    DevBuf<uint16_t> e_wqkv, e_wo, e_wup, e_wdown, e_kpool, e_vpool;
+    DevBuf<int> e_tables;
+    int e_bpl = 0;
+    bool plan_encoder = false;
     int enc_blocks = 0;
     uint64_t enc_seed = 0;
     DevBuf<float> probe_w;
@@ -300,6 +306,9 @@ struct el_engine {
         if (c.d_model > 1024) fail(EL_INVALID_ARGUMENT, "d_model > 1024 unsupported on this engine");
         if (c.encoder_len < 0 || c.encoder_len > 2048)
             fail(EL_INVALID_ARGUMENT, "ModelConfig: encoder_len must be in [0, 2048]");
+        if (c.encoder_layers < 0 || c.encoder_layers > 64 || (c.encoder_layers > 0 && (c.encoder_len <= 0 || c.encoder_len > 256)))
+            fail(EL_INVALID_ARGUMENT, "ModelConfig: encoder_layers must be in [0, 64], > 0 only in T5 mode with "
+                                      "encoder_len <= 256");
         if (c.n_heads > 1) {  // extension: the reference has one head
             const int hd = c.d_model % c.n_heads ? 0 : c.d_model / c.n_heads;
             if (c.n_heads > 32 || !hd || hd < 8 || hd > 256 || (hd & (hd - 1)))
@@ -407,6 +416,34 @@ struct el_engine {
             xid.alloc((size_t)cfg.max_batch);
             enc_act.alloc((size_t)round_up(cfg.max_batch * T, 256) * dp, false);
             enc_seed = el::splitmix64_at(cfg.model_seed, 0x454E43u);  // oracle: eo_encoder_seed
+            if (cfg.encoder_layers > 0) {
+                // encoder stack weights: tags after the cross weights, 4 + 10L + 6i + k (oracle:
+                // eo_model_set_encoder_layers); scratch K/V for kPfRows / T sequences per launch
+                const int LE = cfg.encoder_layers;
+                e_wqkv.alloc((size_t)LE * 3 * dp * dp, false);
+                e_wo.alloc((size_t)LE * dp * dp, false);
+                e_wup.alloc((size_t)LE * fp * dp, false);
+                e_wdown.alloc((size_t)LE * dp * fp, false);
+                for (int i = 0; i < LE; ++i) {
+                    const uint64_t base = 4 + (uint64_t)L * 10 + (uint64_t)i * 6;
+                    uint16_t* q = e_wqkv.p + (size_t)i * 3 * dp * dp;
+                    el::launch_weightgen(q, d, d, dp, dp, tseed(base + 0), sd, 1, stream);
+                    el::launch_weightgen(q + (size_t)dp * dp, d, d, dp, dp, tseed(base + 1), sd, 1, stream);
+                    el::launch_weightgen(q + (size_t)2 * dp * dp, d, d, dp, dp, tseed(base + 2), sd, 1, stream);
+                    el::launch_weightgen(e_wo.p + (size_t)i * dp * dp, d, d, dp, dp, tseed(base + 3), sd, 1, stream);
+                    el::launch_weightgen(e_wup.p + (size_t)i * fp * dp, 4 * d, d, fp, dp, tseed(base + 4), sd, 1, stream);
+                    el::launch_weightgen(e_wdown.p + (size_t)i * dp * fp, d, 4 * d, dp, fp, tseed(base + 5), s4d, 1,
+                                         stream);
+                }
+                e_bpl = ceil_div(T, cfg.block_capacity);
+                const size_t eblk = (size_t)(kPfRows / T) * LE * e_bpl;
+                e_kpool.alloc(eblk * cfg.block_capacity * dp);
+                e_vpool.alloc(eblk * cfg.block_capacity * dp);
+                std::vector<int> et(eblk);
+                for (size_t i = 0; i < eblk; ++i) et[i] = (int)i;
+                e_tables.alloc(eblk);
+                CK(cudaMemcpy(e_tables.p, et.data(), sizeof(int) * eblk, cudaMemcpyHostToDevice));
+            }
         }
 
         // ---- KV pool + allocator ----
@@ -611,10 +648,15 @@ struct el_engine {
     el::IterPlan& mplan_for(int B, int nr_override = 0, int pipe_grid = 0) {
         const int n_pad = std::max(16, round_up(B, 16));
         const int NR = nr_override ? nr_override : this->NR;  // activation rows of the operand layout
-        const int key = n_pad + (nr_override ? 100000 : 0) + (pipe_grid ? 1000000 * pipe_grid : 0);
+        // plan_encoder: the plan of the T5 encoder stack (its own weights and layer count)
+        const bool encp = plan_encoder;
+        const int key = n_pad + (nr_override ? 100000 : 0) + (pipe_grid ? 1000000 * pipe_grid : 0) +
+                        (encp ? 400000000 : 0);
         auto it = mplans.find(key);
         if (it != mplans.end()) return it->second;
-        const int dp = dm.dp, fp = dm.fp, L = dm.L;
+        const int dp = dm.dp, fp = dm.fp, L = encp ? cfg.encoder_layers : dm.L;
+        const uint16_t *Wqkv = encp ? e_wqkv.p : wqkv.p, *Wo = encp ? e_wo.p : wo.p, *Wup = encp ? e_wup.p : wup.p,
+                       *Wdown = encp ? e_wdown.p : wdown.p;
         const int cap = 227 * 1024 - el::iter_smem_fixed();
         // attention ring of K|V|q stages (with the branch-free consumer a third stage pays at
         // d <= 768; at d = 1024 two leave room for the merge buffer and weight prefetch)
@@ -641,10 +683,10 @@ struct el_engine {
             x.nt = 0;
             return x;
         };
-        P.g[el::kIQkv] = g(wqkv.p, 3 * dp / 128, dp / 64, 3 * dp / 128, 0, mega_splits(3 * dp / 128, dp / 64, n_pad, ggrid));
-        P.g[el::kIWo] = g(wo.p, dp / 128, dp / 64, dp / 128, 0, mega_splits(dp / 128, dp / 64, n_pad, ggrid));
-        P.g[el::kIUp] = g(wup.p, fp / 128, dp / 64, fp / 128, 0, mega_splits(fp / 128, dp / 64, n_pad, ggrid));
-        P.g[el::kIDown] = g(wdown.p, dp / 128, fp / 64, dp / 128, 0,
+        P.g[el::kIQkv] = g(Wqkv, 3 * dp / 128, dp / 64, 3 * dp / 128, 0, mega_splits(3 * dp / 128, dp / 64, n_pad, ggrid));
+        P.g[el::kIWo] = g(Wo, dp / 128, dp / 64, dp / 128, 0, mega_splits(dp / 128, dp / 64, n_pad, ggrid));
+        P.g[el::kIUp] = g(Wup, fp / 128, dp / 64, fp / 128, 0, mega_splits(fp / 128, dp / 64, n_pad, ggrid));
+        P.g[el::kIDown] = g(Wdown, dp / 128, fp / 64, dp / 128, 0,
                             opt_mega_down_splits ? std::min(opt_mega_down_splits, fp / 64)
                                                  : mega_splits(dp / 128, fp / 64, n_pad, ggrid));
         // fill: full-K units (direct epilogue) at large N, where split-K partials would outweigh the weights
@@ -652,7 +694,7 @@ struct el_engine {
         P.g[el::kIWoc] = g(woc.p, dp / 128, dp / 64, dp / 128, 0, mega_splits(dp / 128, dp / 64, n_pad));
         int fs = opt_mega_fill_splits ? opt_mega_fill_splits : (n_pad >= 128 ? 1 : 2);  // (c2: 2 < 3 < 4 < 1)
         fs = std::min(fs, dp / 64);
-        P.g[el::kIFill] = g(wqkv.p, 2 * dp / 128, dp / 64, 3 * dp / 128, dp / 128, fs);
+        P.g[el::kIFill] = g(Wqkv, 2 * dp / 128, dp / 64, 3 * dp / 128, dp / 128, fs);
         P.n_pad = n_pad;
         // batch-M full-K GEMMs (no split-K reduce phase) for QKV / W_o / up at small batch
         int nt_max = 16, bm_w = 0;  // bm_w: the largest unit weight slab (nt rows x K)
@@ -1370,7 +1412,8 @@ struct el_engine {
         CK(cudaMemcpyAsync(xslot.p, slots.data(), sizeof(int) * n, cudaMemcpyHostToDevice, stream));
         CK(cudaMemcpyAsync(xid.p, ids.data(), sizeof(int) * n, cudaMemcpyHostToDevice, stream));
         const int N = n * T, NRe = round_up(N, 256);
-        el::launch_encoder_states(enc_act.p, NRe, xid.p, n, T, cfg.d_model, dp, enc_seed, stream);
+        if (cfg.encoder_layers > 0) encoder_run(ids, NRe);
+        else el::launch_encoder_states(enc_act.p, NRe, xid.p, n, T, cfg.d_model, dp, enc_seed, stream);
         el::GemmPlan P = make_plan(wkvc.p, enc_act.p, 0, 2 * dp / 128, dp, 256, false, 1);
         el::DevState s = state(true, N);
         s.rows.slot = xslot.p;
@@ -1381,6 +1424,54 @@ struct el_engine {
             el::launch_gemm(el::kGemmCross, P, s, stream, false);
         }
         CK(cudaStreamSynchronize(stream));  // l is a host stack variable
+    }
+
+    // T5 encoder stack over the seeded encoder ids of sequences `ids` -> enc_act rows [j T, (j+1) T)
+    // (bf16, act layout with NRe rows).  One persistent-kernel launch per kPfRows / T sequences:
+    // rows = (local sequence, position), each layer's K/V into the scratch pool, attention over all
+    // T positions of the row's sequence (enc_bidir), no exit / LM head / fill (prefill mode).
+    void encoder_run(const std::vector<int>& ids, int NRe) {
+        const int T = cfg.encoder_len, LE = cfg.encoder_layers, q = kPfRows / T, dp = dm.dp;
+        plan_encoder = true;
+        el::IterPlan& P = mplan_for(q * T, kPfRows);
+        plan_encoder = false;
+        for (size_t j0 = 0; j0 < ids.size(); j0 += (size_t)q) {
+            const int nq = (int)std::min<size_t>((size_t)q, ids.size() - j0), B = nq * T;
+            std::vector<int> hs((size_t)B), hp((size_t)B), ht((size_t)B);
+            for (int j = 0; j < nq; ++j)
+                for (int t = 0; t < T; ++t) {
+                    const size_t r = (size_t)j * T + t;
+                    hs[r] = j;
+                    hp[r] = t;
+                    ht[r] = encoder_token(ids[j0 + j], t);
+                }
+            CK(cudaMemcpyAsync(pf_slot.p, hs.data(), sizeof(int) * B, cudaMemcpyHostToDevice, stream));
+            CK(cudaMemcpyAsync(pf_pos.p, hp.data(), sizeof(int) * B, cudaMemcpyHostToDevice, stream));
+            CK(cudaMemcpyAsync(pf_tok.p, ht.data(), sizeof(int) * B, cudaMemcpyHostToDevice, stream));
+            el::DevState s = state(true, B);
+            s.cont_host = nullptr;
+            s.prefill = 1;
+            s.enc_bidir = T;
+            s.enc_len = 0;  // (no cross-attention inside the encoder)
+            s.dm.L = LE;
+            s.dm.bpl_max = e_bpl;
+            s.dm.slots = q;
+            s.wqkv = e_wqkv.p; s.wo = e_wo.p; s.wup = e_wup.p; s.wdown = e_wdown.p;
+            s.kpool = e_kpool.p; s.vpool = e_vpool.p; s.tables = e_tables.p;
+            s.NR = kPfRows;
+            s.h32 = pf_h32.p; s.hb = pf_hb.p; s.q32 = pf_q32.p; s.att_b = pf_att_b.p;
+            s.mid32 = pf_mid32.p; s.mid_b = pf_mid_b.p; s.up_b = pf_up_b.p;
+            s.attn_stages = mega_att_stages;
+            el::launch_iter(s, P, mmaps[P.map_key], mega_grid, stream);
+            // the last layer's bf16 output rows -> enc_act rows of these sequences
+            el::launch_act_rows_copy(enc_act.p, NRe, (int)j0 * T, pf_hb.p + (size_t)(LE & 1) * kPfRows * dp, kPfRows,
+                                     B, dp, stream);
+            CK(cudaStreamSynchronize(stream));  // host vectors are reused
+        }
+    }
+    int encoder_token(int seq_id, int t) const {  // oracle: eo_encoder_token
+        return 1 + (int)(el::splitmix64_at(enc_seed ^ 0x544F4Bu, ((uint64_t)seq_id << 20) | (uint64_t)t) %
+                         (uint64_t)(cfg.vocab_size - 1));
     }
 
     // seeded KV prefix for the sequences in `slots` (rows of the prefill row set)
@@ -2095,6 +2186,28 @@ int el_session_kv(el_engine* e, int row, int layer, int pos, float* k, float* v)
     const auto kk = e->read_kv(slot, layer, pos, 0), vv = e->read_kv(slot, layer, pos, 1);
     std::memcpy(k, kk.data(), sizeof(float) * kk.size());
     std::memcpy(v, vv.data(), sizeof(float) * vv.size());
+    API_END
+}
+
+int el_session_cross_kv(el_engine* e, int row, int layer, float* k, float* v) {
+    API_BEGIN
+    e->need_session();
+    if (e->cfg.encoder_len <= 0) fail(EL_INVALID_ARGUMENT, "cross K/V: not in T5 mode");
+    if (row < 0 || row >= e->sess_B || layer < 1 || layer > e->dm.L) fail(EL_INVALID_ARGUMENT, "bad row / layer");
+    CK(cudaStreamSynchronize(e->stream));
+    int slot = 0;
+    CK(cudaMemcpy(&slot, e->row_slot.p + row, sizeof(int), cudaMemcpyDeviceToHost));
+    const int T = e->cfg.encoder_len, d = e->dm.d, dp = e->dm.dp, bc = e->dm.bc;
+    const size_t blk0 = ((size_t)slot * e->dm.L + (layer - 1)) * e->enc_blocks;  // identity cross tables
+    std::vector<uint16_t> kb((size_t)T * dp), vb((size_t)T * dp);
+    CK(cudaMemcpy(kb.data(), e->ckpool.p + blk0 * bc * dp, sizeof(uint16_t) * kb.size(), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(vb.data(), e->cvpool.p + blk0 * bc * dp, sizeof(uint16_t) * vb.size(), cudaMemcpyDeviceToHost));
+    for (int t = 0; t < T; ++t)
+        for (int i = 0; i < d; ++i) {
+            uint32_t a = (uint32_t)kb[(size_t)t * dp + i] << 16, b = (uint32_t)vb[(size_t)t * dp + i] << 16;
+            std::memcpy(k + (size_t)t * d + i, &a, 4);
+            std::memcpy(v + (size_t)t * d + i, &b, 4);
+        }
     API_END
 }
 

@@ -1095,12 +1095,18 @@ __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(const __grid_cons
     }
 
     if (warp == kProducerWarp) {
-        attn_prefix_sum(st, sm.att);  // KV blocks per row: fixed for the iteration
+        if (st.enc_bidir > 0) {  // T5 encoder stack: every row streams all blocks of its sequence
+            const int nb = (st.enc_bidir + dm.bc - 1) / dm.bc;
+            for (int b = tid & 31; b <= B; b += 32) sm.att.pref[b] = b * nb;
+        } else {
+            attn_prefix_sum(st, sm.att);  // KV blocks per row: fixed for the iteration
+        }
         if (st.enc_len > 0)
             for (int b = tid & 31; b <= B; b += 32) sm.att.pref_c[b] = b * st.enc_blocks;
         __syncwarp();
     }
-    const AttnSrc self_src{st.tables, dm.bpl_max, st.kpool, st.vpool, 0, sm.att.pref, sm.pos, sm.slot, 0, nullptr, 0u};
+    const AttnSrc self_src{st.tables, dm.bpl_max, st.kpool, st.vpool, st.enc_bidir, sm.att.pref, sm.pos, sm.slot, 0,
+                           nullptr, 0u};
     const AttnSrc cross_src{st.ctables, st.enc_blocks, st.ckpool, st.cvpool, st.enc_len, sm.att.pref_c, sm.pos, sm.slot, 1, nullptr, 0u};
     // layers of this launch: 1..L (decode iteration / prefill), or the one layer of a turn
     const int lfirst = st.turn_layer > 0 ? st.turn_layer : 1, llast = st.turn_layer > 0 ? st.turn_layer : L;

@@ -1710,6 +1710,20 @@ __global__ void encoder_state_kernel(uint16_t* act, int NR, const int* ids, int 
     for (int i = threadIdx.x; i < dp; i += blockDim.x)
         act[act_offset(row, i, NR)] = (i < d) ? bf16_bits_rne(seeded_value(vs, (uint64_t)i, scale)) : (uint16_t)0;
 }
+// rows [0, n) of an act-layout buffer with NRs rows -> rows [row0, row0 + n) of one with NRd rows
+__global__ void act_rows_copy_kernel(uint16_t* dst, int NRd, int row0, const uint16_t* src, int NRs, int dp) {
+    const int b = blockIdx.x;
+    for (int i = threadIdx.x * 8; i < dp; i += blockDim.x * 8)
+        *reinterpret_cast<uint4*>(dst + act_offset(row0 + b, i, NRd)) =
+            *reinterpret_cast<const uint4*>(src + act_offset(b, i, NRs));
+}
+void launch_act_rows_copy(uint16_t* dst, int NRd, int row0, const uint16_t* src, int NRs, int n, int dp,
+                          cudaStream_t s) {
+    if (n <= 0) return;
+    act_rows_copy_kernel<<<n, 128, 0, s>>>(dst, NRd, row0, src, NRs, dp);
+    EL_CUDA_LAUNCH_CHECK();
+}
+
 void launch_encoder_states(uint16_t* act, int NR, const int* ids, int n, int T, int d, int dp, uint64_t enc_seed,
                            cudaStream_t s) {
     if (n * T <= 0) return;

@@ -83,6 +83,8 @@ struct DevState {
     float attn_scale; // 1/sqrt(d), or 1/sqrt(head_dim) with heads
     int attn_heads;   // attention heads (T5 mode; 1 = the reference's single head)
     int attn_hd;      // features per head (d when attn_heads == 1)
+    int enc_bidir;    // T5 encoder stack launch: > 0 = every row attends over this many positions of its
+                      // sequence's blocks (bidirectional self-attention), 0 = causal decode / prefill
     // split-K GEMM workspace
     // LM-head per-tile partials [Vp/128][Bmax] {max1, max2, sumexp(rel max1), argmax}
     float4* lm_part;
@@ -175,6 +177,8 @@ void launch_kv_prefix(const DevState& st, const int* row_seq_ids, int prefix_len
                       cudaStream_t s);
 void launch_embed(const DevState& st, cudaStream_t s);
 // T5 mode: seeded encoder states of n sequences (ids) as bf16 GEMM B operand rows j*T + t (act layout, NR rows)
+void launch_act_rows_copy(uint16_t* dst, int NRd, int row0, const uint16_t* src, int NRs, int n, int dp,
+                          cudaStream_t s);
 void launch_encoder_states(uint16_t* act, int NR, const int* ids, int n, int T, int d, int dp, uint64_t enc_seed,
                            cudaStream_t s);
 // one attention stage: K block | V block | q (fp32); also hosts the 8-warp merge

@@ -72,6 +72,7 @@ def lib():
         L.el_decode_iterations_done.argtypes = [C.c_void_p]
         L.el_set_fixed_confidences.argtypes = [C.c_void_p, C.c_void_p]
         L.el_session_kv.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p]
+        L.el_session_cross_kv.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_void_p]
         L.el_session_hidden.argtypes = [C.c_void_p, C.c_int, C.c_void_p]
         L.el_session_block_table.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_int]
         L.el_time_decode.argtypes = [C.c_void_p, C.c_int, C.POINTER(C.c_float)]
@@ -132,6 +133,7 @@ class ModelConfig:  # model.hpp:18-25
     seed: int = 0
     encoder_len: int = 0  # T5 mode (not in the reference): cross-attention over this many encoder states
     n_heads: int = 1  # extension: attention heads of d_model / n_heads features (the reference: 1)
+    encoder_layers: int = 0  # T5 mode: a real encoder stack of this many layers (0: seeded encoder states)
 
 
 @dataclass
@@ -223,7 +225,8 @@ class _CConfig(C.Structure):
                 ("c_check_classifier", C.c_double), ("c_check_state", C.c_double),
                 ("max_batch", C.c_int), ("pool_blocks", C.c_int), ("block_capacity", C.c_int),
                 ("eos_token", C.c_int), ("capture_kv", C.c_int), ("round_bf16", C.c_int),
-                ("synthetic_kv_seed", C.c_int64), ("encoder_len", C.c_int), ("n_heads", C.c_int)]
+                ("synthetic_kv_seed", C.c_int64), ("encoder_len", C.c_int), ("n_heads", C.c_int),
+                ("encoder_layers", C.c_int)]
 
 
 def to_c_config(cfg: EngineConfig) -> _CConfig:
@@ -243,6 +246,7 @@ def to_c_config(cfg: EngineConfig) -> _CConfig:
     c.synthetic_kv_seed = cfg.synthetic_kv_seed
     c.encoder_len = cfg.model.encoder_len
     c.n_heads = cfg.model.n_heads
+    c.encoder_layers = cfg.model.encoder_layers
     return c
 
 
@@ -708,6 +712,14 @@ class Engine:
         k = np.zeros(self.d, np.float32)
         v = np.zeros(self.d, np.float32)
         _check(lib().el_session_kv(self._h, row, layer, pos, _ptr(k), _ptr(v)))
+        return k, v
+
+    def cross_kv(self, row, layer):
+        """T5 mode: the row's static cross K/V at `layer` ([encoder_len][d] each)"""
+        T = self.config.model.encoder_len
+        k = np.zeros((T, self.d), np.float32)
+        v = np.zeros((T, self.d), np.float32)
+        _check(lib().el_session_cross_kv(self._h, row, layer, _ptr(k), _ptr(v)))
         return k, v
 
     def hidden(self, parity):

@@ -365,6 +365,37 @@ def test_multi_head_parity(port, L, d, heads, B, T):
     e.close()
 
 
+@pytest.mark.parametrize("L,d,heads,B,T,NE", [(3, 128, 1, 8, 24, 2), (2, 256, 4, 12, 64, 3), (2, 1024, 8, 3, 256, 2)])
+def test_t5_encoder_stack_parity(port, L, d, heads, B, T, NE):
+    """T5 mode with a real encoder stack (NE bidirectional layers over seeded encoder ids, run at
+    admission on the persistent kernel, 256 / T sequences per launch) feeding the cross K/V, vs the
+    oracle's encoder restatement (pinned to an independent numpy encoder, test_t5_oracle_cpu.py)."""
+    V = 512
+    g = X.EngineConfig(model=X.ModelConfig(L, d, V, 5, encoder_len=T, n_heads=heads, encoder_layers=NE),
+                       technique=X.ExitTechnique("state"), schedule=X.ThresholdSchedule(0.972, 0.998, 0.0),
+                       max_batch=B, pool_blocks=B * L * 8, eos_token=-1)
+    o = OB.engine_config(L, d, V, 5, "state", lambda0=0.972, gamma=0.998, max_batch=B, pool_blocks=B * L * 8,
+                         eos_token=-1, round_bf16=True)
+    e = X.Engine(g)
+    first = (np.arange(B) * 37 + 3) % V
+    e.session_begin(first, 30, 60, 1234)
+    m = port.model(L, d, V, 5, True, encoder_len=T, n_heads=heads, encoder_layers=NE)
+    s = m.session(o, first, 30, 60, 1234)
+    st = _teacher_forced(e, s, 3, m.tensor("lm_head"), V, d)
+    for x in st:
+        assert x["h"] <= HID_TOL, x["h"]
+        assert x["conf"] <= CONF_TOL, x["conf"]
+        assert np.all(x["agree"] | (x["gap"] < TIE_GAP)), x["gap"][~x["agree"]]
+    assert np.mean([x["agree"].mean() for x in st]) >= 0.9
+    # the cross K/V of layer 1 come from the encoder output: compare them with the oracle's
+    # W_kc / W_vc applied to its encoder states (bf16 storage)
+    wkc, wvc = m.tensor("w_kc", 1), m.tensor("w_vc", 1)
+    E = np.stack([m.encoder_state(1, t) for t in range(T)])
+    kc, vc = e.cross_kv(1, 1)
+    assert relerr(kc[:T], E @ wkc.T) <= 1e-2 and relerr(vc[:T], E @ wvc.T) <= 1e-2
+    e.close()
+
+
 def test_multi_head_config_checks():
     for heads, enc in ((3, 16), (64, 16), (32, 0)):  # no divisor; > 32 heads; head_dim 4 < 8
         with pytest.raises(ValueError):
@@ -372,16 +403,18 @@ def test_multi_head_config_checks():
                                     technique=X.ExitTechnique("never"), max_batch=2, pool_blocks=64))
 
 
-def test_t5_engine_run_matches_oracle(port):
-    """Engine::run in T5 mode (decoder prompt = start token, input in the encoder)."""
+@pytest.mark.parametrize("NE", [0, 2])
+def test_t5_engine_run_matches_oracle(port, NE):
+    """Engine::run in T5 mode (decoder prompt = start token, input in the encoder; NE > 0: the
+    encoder stack runs at each admission)."""
     L, d, V, T = 3, 64, 256, 16
-    g = X.EngineConfig(model=X.ModelConfig(L, d, V, 9, encoder_len=T), technique=X.ExitTechnique("never"),
-                       max_batch=4, pool_blocks=512, eos_token=-1)
+    g = X.EngineConfig(model=X.ModelConfig(L, d, V, 9, encoder_len=T, encoder_layers=NE),
+                       technique=X.ExitTechnique("never"), max_batch=4, pool_blocks=512, eos_token=-1)
     o = OB.engine_config(L, d, V, 9, "never", max_batch=4, pool_blocks=512, eos_token=-1, round_bf16=True)
     reqs = [(0.0, [1], 6), (0.0, [5], 4), (0.0, [9], 7), (0.01, [2], 3), (0.02, [7], 5)]
     e = X.Engine(g)
     t = e.run(X.Workload([X.Request(*r) for r in reqs]))
-    tp = port.model(L, d, V, 9, True, encoder_len=T).run(o, OB.Workload.from_requests(reqs))
+    tp = port.model(L, d, V, 9, True, encoder_len=T, encoder_layers=NE).run(o, OB.Workload.from_requests(reqs))
     for f in ["it_output_layer", "it_batch_off", "ps_seq", "sq_id"]:
         assert np.array_equal(t[f], tp[f]), f
     gt = {s["id"]: s["tokens"] for s in t.sequences}

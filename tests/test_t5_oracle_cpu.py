@@ -108,3 +108,46 @@ def test_multi_head_needs_a_divisor(port):
     import pytest
     with pytest.raises(ValueError):
         port.model(2, 32, 48, 1, True, encoder_len=4, n_heads=5)
+
+
+def np_encoder(m, seq_id, T, heads=1):
+    """independent numpy restatement of the T5 encoder stack: bidirectional norm-free blocks over
+    the embeddings of the seeded encoder ids, output bf16-rounded like the model"""
+    d = m.d
+    hd = d // heads
+    emb = m.tensor("embedding")
+    X = np.stack([emb[m.encoder_token(seq_id, t)] for t in range(T)])
+    for l in range(1, m.encoder_layers + 1):
+        W = {n: m.tensor(n, l) for n in ("e_q", "e_k", "e_v", "e_o", "e_up", "e_down")}
+        Q, K, Vv = X @ W["e_q"].T, X @ W["e_k"].T, X @ W["e_v"].T
+        A = np.zeros_like(X)
+        for f in range(0, d, hd):
+            S = Q[:, f:f + hd] @ K[:, f:f + hd].T / np.sqrt(hd)
+            P = np.exp(S - S.max(axis=1, keepdims=True))
+            A[:, f:f + hd] = (P / P.sum(axis=1, keepdims=True)) @ Vv[:, f:f + hd]
+        mid = X + A @ W["e_o"].T
+        X = mid + np.maximum(mid @ W["e_up"].T, 0.0) @ W["e_down"].T
+    b = np.ascontiguousarray(X, dtype=np.float64).view(np.uint64)  # RNE to 8 significant bits on fp64 bits
+    b = (b + np.uint64((1 << 44) - 1) + ((b >> np.uint64(45)) & np.uint64(1))) & ~np.uint64((1 << 45) - 1)
+    return b.view(np.float64)
+
+
+def test_t5_encoder_stack_matches_numpy(port):
+    L, d, V, T = 2, 32, 48, 6
+    for heads, nl in ((1, 2), (4, 3)):
+        m = port.model(L, d, V, 11, True, encoder_len=T, n_heads=heads, encoder_layers=nl)
+        for sid in (0, 3):
+            want = np_encoder(m, sid, T, heads)
+            got = np.stack([m.encoder_state(sid, t) for t in range(T)])
+            assert np.abs(got - want).max() <= 2 ** -8 * np.abs(want).max(), (heads, sid)  # one bf16 ulp
+        ids = [m.encoder_token(0, t) for t in range(T)]
+        assert all(1 <= i < V for i in ids) and len(set(ids)) > 1
+    # the stack changes the states, and the decode (vs seeded states)
+    m0 = port.model(L, d, V, 11, True, encoder_len=T)
+    m2 = port.model(L, d, V, 11, True, encoder_len=T, encoder_layers=2)
+    assert not np.allclose(m0.encoder_state(1, 2), m2.encoder_state(1, 2))
+    cfg = OB.engine_config(L, d, V, 11, "never", max_batch=2, pool_blocks=64, block_capacity=4, round_bf16=True)
+    reqs = [(0.0, [1], 6), (0.0, [7], 4)]
+    t2 = m2.run(cfg, OB.Workload.from_requests(reqs))
+    got = {s["id"]: s["tokens"] for s in t2.sequences}
+    assert got[0] == np_t5_decode(m2, [1], 6, 0, T) and got[1] == np_t5_decode(m2, [7], 4, 1, T)
