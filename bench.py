@@ -399,7 +399,10 @@ def run_ours(args, rank, world, local_rank, dist, stub=False):
               "ms_per_turn": round(ms_ll / timed_t, 4), "tokens": int(ntok),
               "mean_layers_per_token": round(float(new_exits.mean()), 3) if ntok else None,
               "mean_rows_per_turn": round(float(tr[warm_t:].mean()), 2),
-              "note": "one host round trip per turn (the next turn's rows depend on this turn's exits)"}
+              "token_turns": int((tl[warm_t:] == 0).sum()),
+              "note": "one host round trip per turn (the next turn's rows depend on this turn's exits); "
+                      "deferred tokens: exited sequences wait for a token turn (layer 0) that runs the LM "
+                      "head and the skipped-layer fill for all of them at once"}
 
     # 6. Engine::run (the reference's API, engine.cpp:110-330) end to end: this rank's requests with
     #    their real 512-token prompts (batched causal prefill on the device, no seeded KV), 128 new

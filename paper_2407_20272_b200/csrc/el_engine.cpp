@@ -863,6 +863,9 @@ struct el_engine {
         s.wqc = wqc.p; s.wkvc = wkvc.p; s.woc = woc.p;
         s.ckpool = ckpool.p; s.cvpool = cvpool.p; s.ctables = ctables.p;
         s.turn_layer = 0;
+        s.turn_defer = 0;
+        s.turn_token = 0;
+        s.row_exit = row_exit.p;
         s.hstore = hstore.p;
         s.row_seq = row_seq.p;
         s.run_active = run_ctl.p;
@@ -1741,12 +1744,14 @@ struct el_engine {
         bool on = false;
         int policy = 0;
         std::vector<double> M;  // [L][L] (linear policy)
-        std::vector<int> next, pos, tok;
+        bool defer = false;      // deferred tokens: next == 0 = the sequence waits for a token turn
+        std::vector<int> next, pos, tok, exit_at;
         std::vector<std::vector<int>> toks, exits;
-        std::vector<int> turn_layer, turn_n;
+        std::vector<int> turn_layer, turn_n;  // turn_layer 0 = a token turn
     } sch;
+    int opt_sched_defer = 1;
     DevBuf<float> hstore;
-    DevBuf<int> row_seq;
+    DevBuf<int> row_seq, row_exit;
     void sched_begin(int policy, const double* M) {
         need_session();
         if (cfg.encoder_len > 0) fail(EL_INVALID_ARGUMENT, "layer-level scheduling: T5 mode not supported");
@@ -1763,8 +1768,14 @@ struct el_engine {
         sch.tok = sess_first;
         sch.toks.assign((size_t)B, {});
         sch.exits.assign((size_t)B, {});
+        sch.exit_at.assign((size_t)B, 0);
+        // deferred tokens (default; not with softmax exit, whose check already holds the token's LM
+        // head): a sequence that exits waits at the token stage, and a token turn decodes the LM
+        // head and fills the skipped layers for every waiting sequence at once
+        sch.defer = opt_sched_defer && cfg.technique != EL_TECH_SOFTMAX;
         if (hstore.n < (size_t)dm.Bmax * dm.dp) hstore.alloc((size_t)dm.Bmax * dm.dp);
         if (row_seq.n < (size_t)dm.Bmax) row_seq.alloc((size_t)dm.Bmax);
+        if (row_exit.n < (size_t)dm.Bmax) row_exit.alloc((size_t)dm.Bmax);
     }
     int sched_pick(const std::vector<int>& v) const {
         const int L = dm.L;
@@ -1787,11 +1798,63 @@ struct el_engine {
         }
         return best;
     }
+    // token turn: the LM head + greedy token + skipped-layer fill of every waiting sequence
+    void sched_token_turn() {
+        const int B = sess_B, Bm = dm.Bmax;
+        std::vector<int> rs, rp, rt, rq, re;
+        int amin = dm.L;
+        for (int b = 0; b < B; ++b)
+            if (sch.next[(size_t)b] == 0) {
+                rs.push_back(sess_slots[(size_t)b]);
+                rp.push_back(sch.pos[(size_t)b]);
+                rt.push_back(sch.tok[(size_t)b]);
+                rq.push_back(b);
+                re.push_back(sch.exit_at[(size_t)b]);
+                amin = std::min(amin, sch.exit_at[(size_t)b]);
+            }
+        const int n = (int)rs.size();
+        CK(cudaMemcpyAsync(row_slot.p, rs.data(), sizeof(int) * n, cudaMemcpyHostToDevice, stream));
+        CK(cudaMemcpyAsync(row_pos.p, rp.data(), sizeof(int) * n, cudaMemcpyHostToDevice, stream));
+        CK(cudaMemcpyAsync(row_tok.p, rt.data(), sizeof(int) * n, cudaMemcpyHostToDevice, stream));
+        CK(cudaMemcpyAsync(row_seq.p, rq.data(), sizeof(int) * n, cudaMemcpyHostToDevice, stream));
+        CK(cudaMemcpyAsync(row_exit.p, re.data(), sizeof(int) * n, cudaMemcpyHostToDevice, stream));
+        el::IterPlan& P = mplan_for(n);
+        el::DevState s = state(false, n);
+        s.attn_stages = mega_att_stages;
+        s.turn_layer = amin;
+        s.turn_token = 1;
+        el::launch_iter(s, P, mmaps[P.map_key], mega_grid, stream);
+        const int cur = sess_iters % rec_cap;
+        CK(cudaMemcpyAsync(rec_host, rec.p + (size_t)cur * rec_stride, sizeof(int) * rec_stride, cudaMemcpyDeviceToHost,
+                           stream));
+        CK(cudaStreamSynchronize(stream));
+        ++sess_iters;
+        for (int r = 0; r < n; ++r) {
+            const int b = rq[(size_t)r];
+            sch.toks[(size_t)b].push_back(rec_host[r]);
+            sch.exits[(size_t)b].push_back(sch.exit_at[(size_t)b]);
+            sch.tok[(size_t)b] = rec_host[r];
+            ++sch.pos[(size_t)b];
+            sch.next[(size_t)b] = 1;
+        }
+        sch.turn_layer.push_back(0);
+        sch.turn_n.push_back(n);
+    }
     void sched_turn() {
         const int B = sess_B, L = dm.L, Bm = dm.Bmax;
         std::vector<int> v((size_t)L, 0);
-        for (int b = 0; b < B; ++b) ++v[(size_t)sch.next[(size_t)b] - 1];
+        int waiting = 0;
+        for (int b = 0; b < B; ++b) {
+            if (sch.next[(size_t)b] == 0) ++waiting;
+            else ++v[(size_t)sch.next[(size_t)b] - 1];
+        }
+        // the token stage competes like a layer: a token turn when the waiting sequences are at
+        // least as many as the policy's layer holds (or nothing else is runnable)
         const int a = sched_pick(v);
+        if (waiting > 0 && waiting >= v[(size_t)a - 1]) {
+            sched_token_turn();
+            return;
+        }
         std::vector<int> rs, rp, rt, rq;
         for (int b = 0; b < B; ++b)
             if (sch.next[(size_t)b] == a) {
@@ -1813,6 +1876,7 @@ struct el_engine {
         s.attn_stages = mega_att_stages;
         s.attn_seg_cost = opt_attn_seg_cost >= 0 ? opt_attn_seg_cost : (n <= 64 ? 2 : 0);
         s.turn_layer = a;
+        s.turn_defer = sch.defer ? 1 : 0;
         el::launch_iter(s, P, mmaps[P.map_key], mega_grid, stream);
         const int cur = sess_iters % rec_cap;
         CK(cudaMemcpyAsync(rec_host, rec.p + (size_t)cur * rec_stride, sizeof(int) * rec_stride, cudaMemcpyDeviceToHost,
@@ -1822,7 +1886,10 @@ struct el_engine {
         for (int r = 0; r < n; ++r) {
             const int b = rq[(size_t)r];
             const int ex = rec_host[Bm + r];
-            if (ex) {
+            if (ex && sch.defer) {  // waits for a token turn
+                sch.exit_at[(size_t)b] = ex;
+                sch.next[(size_t)b] = 0;
+            } else if (ex) {
                 sch.toks[(size_t)b].push_back(rec_host[r]);
                 sch.exits[(size_t)b].push_back(ex);
                 sch.tok[(size_t)b] = rec_host[r];
@@ -2010,6 +2077,8 @@ int el_engine_set_option(el_engine* e, const char* key, int64_t v) {
         if (v < 0 || v > 8) fail(EL_INVALID_ARGUMENT, "%s must be in [0 (auto), 8]", key);
         (key[5] == 'c' ? e->opt_attn_cb : e->opt_attn_stages) = (int)v;
         e->plan_attention();
+    } else if (!std::strcmp(key, "sched_defer")) {  // layer-level scheduling: deferred token turns (default 1)
+        e->opt_sched_defer = v != 0;
     } else if (!std::strcmp(key, "mega_bm_wstream")) {  // -1 auto (pipelined kernel), 0 off, 1 on
         if (v < -1 || v > 1) fail(EL_INVALID_ARGUMENT, "mega_bm_wstream must be -1, 0 or 1");
         e->opt_mega_bm_wstream = (int)v;

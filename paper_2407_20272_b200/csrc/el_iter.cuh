@@ -414,8 +414,9 @@ __device__ __forceinline__ void epi_fill_direct(const DevState& st, const IterSm
         float v[16];
         tmem_ld16(trow + (uint32_t)c0, v);
 #pragma unroll
-        for (int j = 0; j < 16; ++j)
-            if (c0 + j < nval) pool[kv_dst(st, sm, c0 + j, layer) + f] = f32_to_bf16(v[j]);
+        for (int j = 0; j < 16; ++j)  // (token turn: only layers past the row's own exit layer)
+            if (c0 + j < nval && !(st.turn_token && layer <= st.row_exit[c0 + j]))
+                pool[kv_dst(st, sm, c0 + j, layer) + f] = f32_to_bf16(v[j]);
     }
 }
 
@@ -505,6 +506,7 @@ __device__ __forceinline__ void reduce_range(const DevState& st, const IterSmem&
                 const int m2 = 2 * dp / kBM;
                 IterCtx y = x;
                 y.layer = x.layer + m / m2;  // x.layer = first skipped layer
+                if (st.turn_token && y.layer <= st.row_exit[c]) continue;  // (token turn: row's own range)
                 apply4<K>(st, sm, y, m % m2, c, r0, acc[j], &sd[j], dry);
             } else if constexpr (K == kIDown) {
                 const int R = m * kBM + r0;
@@ -1110,9 +1112,10 @@ __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(const __grid_cons
     const AttnSrc cross_src{st.ctables, st.enc_blocks, st.ckpool, st.cvpool, st.enc_len, sm.att.pref_c, sm.pos, sm.slot, 1, nullptr, 0u};
     // layers of this launch: 1..L (decode iteration / prefill), or the one layer of a turn
     const int lfirst = st.turn_layer > 0 ? st.turn_layer : 1, llast = st.turn_layer > 0 ? st.turn_layer : L;
-    if (st.turn_layer > 1) {
-        // layer-level turn past layer 1: each row's state entering this layer, kept per sequence
-        const int pin = (lfirst - 1) & 1;
+    if (st.turn_layer > 1 || st.turn_token) {
+        // layer-level turn past layer 1: each row's state entering this layer, kept per sequence;
+        // token turn: each row's exit state, into the parity of the smallest exit layer
+        const int pin = st.turn_token ? (lfirst & 1) : (lfirst - 1) & 1;
         for (int b = cta; b < B; b += G) {
             const float* src = st.hstore + (size_t)st.row_seq[b] * dp;
             float* h = st.h32 + ((size_t)pin * Bm + b) * dp;
@@ -1138,7 +1141,7 @@ __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(const __grid_cons
     grid_sync(p, st, nbar, g0);
 
     int e_out = llast;
-    for (int layer = lfirst; layer <= llast; ++layer) {
+    for (int layer = lfirst; layer <= llast && !st.turn_token; ++layer) {
         const IterCtx x{layer, (layer - 1) & 1, layer & 1};
         // q | k | v, K/V appended to the paged pool (model.cpp:218-226)
         if (p.g[kIQkv].mode) {
@@ -1271,6 +1274,35 @@ __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(const __grid_cons
         }
     }
 
+    if (st.turn_defer && !st.turn_token) {
+        // deferred layer turn: every row's state at this layer -> the per-sequence store (an
+        // exited row's is its exit state, for the token turn), exit flags -> the record
+        if (warp < 8) {
+            const int lane = tid & 31, cur = iter % st.rec_cap;
+            for (int b = cta + G * warp; b < B; b += G * 8) {
+                const float* src = st.h32 + ((size_t)(e_out & 1) * Bm + b) * dp;
+                float* dst = st.hstore + (size_t)st.row_seq[b] * dp;
+                for (int i = lane * 4; i < dp; i += 128)
+                    *reinterpret_cast<float4*>(dst + i) = __ldcg(reinterpret_cast<const float4*>(src + i));
+                if (lane == 0) {
+                    const bool ex = e_out == L || sm.status[b];
+                    rec_rec(st, cur)[b] = -1;
+                    rec_rec(st, cur)[Bm + b] = ex ? e_out : 0;
+                    rec_conf(st, cur)[(size_t)(e_out - 1) * Bm + b] = __ldcg(&st.conf[(size_t)(e_out - 1) * Bm + b]);
+                }
+            }
+        }
+        if (cta == 0 && tid == 0) {
+            *(volatile unsigned*)(p.bar + 2) = g0.y + (unsigned)G * (unsigned)nbar;  // next launch's count base
+            for (int i = 0; i < kINumGemm * 64; ++i) p.tcnt[i] = 0u;
+            *st.cur_iter = iter;
+            *st.iter_counter = iter + 1;
+        }
+        tc_fence_before();
+        __syncthreads();
+        if (warp == 0) tmem_dealloc(sm.tmem, 512);
+        return;
+    }
     if (st.prefill) {
         // batched causal prefill (engine.cpp:166-181): every layer's K/V of all rows is written;
         // no exit, no tokens, no records -- only the launch bookkeeping below
@@ -1289,7 +1321,7 @@ __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(const __grid_cons
     // a layer-level turn decodes a token only for rows that exit here (own accept, or the last
     // layer); every CTA holds the same decisions in sm.status, so this is grid-uniform
     bool any_exit = true;
-    if (st.turn_layer > 0 && e_out < L) {
+    if (st.turn_layer > 0 && e_out < L && !st.turn_token) {
         int a = 0;
         for (int b = tid; b < B; b += blockDim.x) a |= sm.status[b];
         any_exit = __syncthreads_or(a) != 0;
@@ -1332,6 +1364,14 @@ __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(const __grid_cons
         const int lane = tid & 31;
         const int cur = iter % st.rec_cap;
         for (int b = cta + G * warp; b < B; b += G * 8) {
+            if (st.turn_token) {  // token turn: every row's token; its exit layer back to the host
+                const LmPart r = lm_col_warp(st, b);
+                if (lane == 0) {
+                    rec_rec(st, cur)[b] = r.idx;
+                    rec_rec(st, cur)[Bm + b] = st.row_exit[b];
+                }
+                continue;
+            }
             if (st.turn_layer > 0) {
                 // turn record: the token of a row that exits at this layer, -1 for a row that
                 // continues (its state goes to the per-sequence store for the next layer)

@@ -120,6 +120,12 @@ struct DevState {
     int turn_layer;
     float* hstore;        // [Bmax][dp] fp32 state entering each sequence's next layer
     const int* row_seq;   // [Bmax] sequence index of each row of the turn
+    // deferred tokens (layer-level scheduling): turn_defer = 1: a layer turn stores every row's state
+    // (exited rows' too) and decodes no token; turn_token = 1: a token turn -- rows = sequences whose
+    // position exited at row_exit[b] (>= turn_layer = the smallest): LM head + greedy token + the
+    // skipped-layer fill of layers (row_exit[b], L] for every row at once, no layer computed
+    int turn_defer, turn_token;
+    const int* row_exit;
     // Engine::run between scheduling events: iterations queued back to back on the device skip
     // themselves once *run_active is 0 (set by run_step_kernel); nullptr = always run
     const int* run_active;

@@ -21,11 +21,12 @@ CONF_TOL = {"state": 1e-4, "classifier": 1e-4}
 TIE_GAP = 2e-2
 
 
-def _run(port, L, d, V, B, tech, lam, gamma, turns, policy="greedy", M=None, prefix=40):
+def _run(port, L, d, V, B, tech, lam, gamma, turns, policy="greedy", M=None, prefix=40, defer=1):
     cfg = X.EngineConfig(model=X.ModelConfig(L, d, V, 0), technique=X.ExitTechnique(tech),
                          schedule=X.ThresholdSchedule(lam, gamma, 0.0), max_batch=B, pool_blocks=B * L * 16,
                          eos_token=-1)
     e = X.Engine(cfg)
+    e.set_option("sched_defer", defer)  # deferred token turns (default) or a token per exiting row at once
     first = np.array([p[-1] % V for p in bench.workload(B)], np.int32)
     cap = prefix + 1 + 64
     e.session_begin(first, prefix, cap, 1, np.arange(B))
@@ -36,13 +37,15 @@ def _run(port, L, d, V, B, tech, lam, gamma, turns, policy="greedy", M=None, pre
     return e, first, got, layers, rows, cap
 
 
-@pytest.mark.parametrize("L,d,V,B,tech,lam,gamma", [(6, 256, 1024, 24, "state", 0.97, 0.998),
-                                                   (12, 768, 32128, 64, "state", 0.981, 0.997),
-                                                   (8, 512, 4096, 40, "classifier", 0.406, 0.999)])
-def test_layer_level_schedule_matches_single_sequence_decoding(port, L, d, V, B, tech, lam, gamma):
-    e, first, got, layers, rows, cap = _run(port, L, d, V, B, tech, lam, gamma, turns=8 * L)
-    # every turn engages exactly the sequences at its layer; the greedy layer is the most occupied
+@pytest.mark.parametrize("L,d,V,B,tech,lam,gamma,defer", [(6, 256, 1024, 24, "state", 0.97, 0.998, 1),
+                                                         (6, 256, 1024, 24, "state", 0.97, 0.998, 0),
+                                                         (12, 768, 32128, 64, "state", 0.981, 0.997, 1),
+                                                         (8, 512, 4096, 40, "classifier", 0.406, 0.999, 1)])
+def test_layer_level_schedule_matches_single_sequence_decoding(port, L, d, V, B, tech, lam, gamma, defer):
+    e, first, got, layers, rows, cap = _run(port, L, d, V, B, tech, lam, gamma, turns=8 * L, defer=defer)
+    # every turn engages exactly the sequences at its layer (layer 0: a token turn)
     assert len(layers) == 8 * L and rows.min() >= 1
+    assert (0 in set(layers.tolist())) == bool(defer)
     n_max = max(len(t) for t, _ in got)
     assert n_max >= 2 and sum(len(t) for t, _ in got) > B
     cfg = OB.engine_config(L, d, V, 0, tech, lambda0=lam, gamma=gamma, max_batch=B, pool_blocks=4096, eos_token=-1,
