@@ -23,7 +23,8 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 def flags() -> list[str]:
     return ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
             "-Xcompiler", "-fPIC", "-Xcompiler", "-O2", "--expt-relaxed-constexpr", "-cudart", "static",
-            f"-I{os.path.join(ROOT, 'include')}"] + (["-DEL_DEBUG=1"] if os.environ.get("EL_DEBUG") == "1" else [])
+            f"-I{os.path.join(ROOT, 'include')}"] + (["-DEL_DEBUG=1"] if os.environ.get("EL_DEBUG") == "1" else []) \
+        + os.environ.get("EL_EXTRA_FLAGS", "").split()  # (A/B variant builds, e.g. -DEL_LANE_ISSUE=0)
 
 
 def _stamp_text() -> str:

@@ -162,6 +162,13 @@ __device__ __forceinline__ void bulk_load_hint(uint32_t dst, const void* src, ui
         "l"(src), "r"(bytes), "r"(bar), "l"(policy)
         : "memory");
 }
+// Bulk copies of the producer rings: all from lane 0 (default), or from rotating lanes (1). One
+// thread's copies are processed one after another (scripts/ingest_probe*.cu), but in the kernels
+// the streams are bound by bytes in flight / latency and lane rotation measured -0.4 to -0.7 % at
+// c5 (same-box A/B, scripts/ab_early.sh), so it stays a build switch (EL_EXTRA_FLAGS).
+#ifndef EL_LANE_ISSUE
+#define EL_LANE_ISSUE 0
+#endif
 // request [src, src + bytes) into L2 (no completion tracking)
 __device__ __forceinline__ void l2_prefetch_bulk(const void* src, uint32_t bytes) {
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");

@@ -698,8 +698,9 @@ struct el_engine {
         P.n_pad = n_pad;
         // batch-M full-K GEMMs (no split-K reduce phase) for QKV / W_o / up at small batch
         int nt_max = 16, bm_w = 0;  // bm_w: the largest unit weight slab (nt rows x K)
-        // streamed batch-M weights (auto: the pipelined kernel)
-        const bool wstream = opt_mega_bm_wstream < 0 ? pipe_grid > 0 : opt_mega_bm_wstream != 0;
+        // streamed batch-M weights (auto: off -- -2.4 % full-depth iteration time in the pipelined
+        // kernel, but +1.5 % at the early-exit bench (c5, same-box A/B, scripts/ab_early.sh))
+        const bool wstream = opt_mega_bm_wstream > 0;
         // batch > 128: units cover 128-row groups of an activation layout with 128-row multiples
         const bool bm = n_pad <= opt_mega_bm_max && (n_pad <= 128 || NR % 128 == 0);
         if (bm) {

@@ -176,9 +176,9 @@ __device__ __forceinline__ void unit_mainloop(IterSmem& sm, uint8_t* ring, const
                 asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(fb), "r"(tx) : "memory");
             }
             __syncwarp();
-            const int il = 1 + 2 * (int)(s % 15u);
+            const int il = EL_LANE_ISSUE ? 1 + 2 * (int)(s % 15u) : 0;
             if (lane == il) bulk_load_hint(sb, ap, a_bytes, fb, a_policy);
-            else if (lane == il + 1) bulk_load_hint(sb + r.b_off, bp, b_bytes, fb, b_policy);
+            if (lane == (EL_LANE_ISSUE ? il + 1 : 0)) bulk_load_hint(sb + r.b_off, bp, b_bytes, fb, b_policy);
             ap += ast;
             bp += bst;
             if (++s == r.stages) {
@@ -802,17 +802,17 @@ __device__ __forceinline__ void unit_bm(IterSmem& sm, uint8_t* ring, const IterP
             __syncwarp();
             if (ws)
                 for (int j = 0; j < kc; ++j, ++issued)
-                    if (lane == 1 + issued % 31)
+                    if (lane == (EL_LANE_ISSUE ? 1 + issued % 31 : 0))
                         bulk_load_hint(ring0 + s * (uint32_t)p.bm_astage + wst + (uint32_t)j * wrow,
                                        wsrc + (size_t)(c * p.bm_kc + j) * (kBM * kBK), wrow, fb, kL2EvictFirst);
             if (!grouped) {
-                if (lane == 1 + issued % 31)
+                if (lane == (EL_LANE_ISSUE ? 1 + issued % 31 : 0))
                     bulk_load_hint(ring0 + s * (uint32_t)p.bm_astage, act + (size_t)c * p.bm_kc * p.bm_rows * kBK,
                                    bytes, fb, pol);
                 ++issued;
             } else {
                 for (int j = 0; j < kc; ++j, ++issued)
-                    if (lane == 1 + issued % 31)
+                    if (lane == (EL_LANE_ISSUE ? 1 + issued % 31 : 0))
                         bulk_load_hint(ring0 + s * (uint32_t)p.bm_astage + (uint32_t)j * NRb,
                                        act + (size_t)(c * p.bm_kc + j) * p.bm_rows * kBK, NRb, fb, pol);
             }

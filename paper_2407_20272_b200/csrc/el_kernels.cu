@@ -432,14 +432,14 @@ __global__ void __launch_bounds__(128, 1)
             for (int kb = 0; kb < pre; ++kb) mbar_arrive_expect_tx(&full[kb], kAStage + b_stage);
         __syncwarp();
         for (int kb = 0; kb < pre; ++kb)  // weights first: independent of the previous kernel
-            if (lane == 1 + 2 * (kb % 15))
+            if (lane == (EL_LANE_ISSUE ? 1 + 2 * (kb % 15) : 0))
                 bulk_load(sA + (size_t)kb * kAStage, a_tiles + (size_t)(kb0 + kb) * (kBM * kBK), kAStage, &full[kb]);
         // activations: the first n_pad rows of a k-block tile are contiguous
         const uint16_t* b_tiles = g.Bp + (size_t)b_row * g.b_par_stride;
         const size_t b_kstride = (size_t)g.NR * kBK;
         pdl_wait();  // no-op unless launched as a PDL secondary
         for (int kb = 0; kb < pre; ++kb)
-            if (lane == 2 + 2 * (kb % 15))
+            if (lane == (EL_LANE_ISSUE ? 2 + 2 * (kb % 15) : 0))
                 bulk_load(sB + (size_t)kb * b_stage, b_tiles + (size_t)(kb0 + kb) * b_kstride + (size_t)n0 * kBK,
                           b_stage, &full[kb]);
         for (int kb = pre; kb < nkb; ++kb) {
@@ -454,9 +454,9 @@ __global__ void __launch_bounds__(128, 1)
                 mbar_arrive_expect_tx(&full[s], kAStage + b_stage);
             }
             __syncwarp();
-            if (lane == 1 + 2 * (s % 15))
+            if (lane == (EL_LANE_ISSUE ? 1 + 2 * (s % 15) : 0))
                 bulk_load(sA + (size_t)s * kAStage, a_tiles + (size_t)(kb0 + kb) * (kBM * kBK), kAStage, &full[s]);
-            else if (lane == 2 + 2 * (s % 15))
+            if (lane == (EL_LANE_ISSUE ? 2 + 2 * (s % 15) : 0))
                 bulk_load(sB + (size_t)s * b_stage, b_tiles + (size_t)(kb0 + kb) * b_kstride + (size_t)n0 * kBK,
                           b_stage, &full[s]);
         }
@@ -1382,15 +1382,15 @@ __device__ __forceinline__ void attn_body(const DevState& st, AttnSmem& a, uint8
                     xgo = __shfl_sync(0xffffffffu, xgo, 0);
                     __syncwarp();  // (orders lane 0's empty-slot acquire before the other lanes' copies)
                     if (xgo) {
-                        const int il = 1 + 3 * (seq % 10);  // lanes 1..30
+                        const int il = EL_LANE_ISSUE ? 1 + 3 * (seq % 10) : 0;  // lanes 1..30
                         const int s = seq % S;
                         const uint32_t sb = smem_u32(stages + (size_t)s * stage_bytes), fb = smem_u32(&a.full[s]);
                         const uint32_t bytes = (uint32_t)min(dm.bc, ctx - blk * dm.bc) * dp * 2;
                         if (lane == il)
                             bulk_load_hint(sb, src.kpool + (size_t)id * dm.bc * dp, bytes, fb, kL2EvictFirst);
-                        else if (lane == il + 1)
+                        if (lane == (EL_LANE_ISSUE ? il + 1 : 0))
                             bulk_load_hint(sb + blk_bytes, src.vpool + (size_t)id * dm.bc * dp, bytes, fb, kL2EvictFirst);
-                        else if (lane == il + 2 && (xgo & 2))
+                        if (lane == (EL_LANE_ISSUE ? il + 2 : 0) && (xgo & 2))
                             bulk_load(stages + (size_t)s * stage_bytes + 2 * blk_bytes, st.q32 + (size_t)b * dp,
                                       (uint32_t)dp * 4, &a.full[s]);
                     }
