@@ -38,6 +38,7 @@ struct IterSmem {
     int pos[256], slot[256], status[256], first[256];
     int kvrow[256];  // per row: slot * L * bpl_max + pos / bc (block-table index at layer 1)
     int kvin[256];   // per row: (pos % bc) * dp (element offset of the position inside its block)
+    long long kvd[256];  // fill epilogue: per row, the K/V element offset of its position at the unit's layer
 };
 
 __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
@@ -302,6 +303,80 @@ __device__ void epi_lm(const DevState& st, const IterSmem& sm, float* tbuf, int 
     }
 }
 
+// Greedy-token LM-head tile epilogue (argmax only, lowest index on ties): per column the tile's
+// (max, argmax) -> lm_part[tile][col] as (max, -inf, 0, argmax).  Each warp reduces its 32 vocab
+// rows x 16 columns per TMEM load with a reduce-scatter butterfly (16 + 16 shuffles, after which
+// lanes 2k / 2k+1 hold column k), then one barrier and the 4 row groups in ascending order --
+// instead of epi_lm's shared-memory transpose and two barriers per 32 columns (8.5 -> ~3 us per
+// tile at c5, scripts/pipe_tail.py).
+__device__ __forceinline__ void lm_pick(float& v, int& i, float w, int k) {
+    if (w > v || (w == v && k < i)) {
+        v = w;
+        i = k;
+    }
+}
+__device__ void epi_lm_argmax(const DevState& st, const IterSmem& sm, float* tbuf, int tile, int nval) {
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int rg = warp & 3, row0 = tile * kBM;
+    const int my_row = row0 + 32 * rg + lane;
+    const bool valid = 32 * rg + lane < min(kBM, st.dm.V - row0);
+    const uint32_t trow = sm.tmem + ((uint32_t)(32 * rg) << 16);
+    float* bv = tbuf;                                  // [4][256] best value per row group and column
+    int* bi = reinterpret_cast<int*>(tbuf + 4 * 256);  // [4][256] its vocab index
+    for (int c0 = 16 * (warp >> 2); c0 < nval; c0 += 32) {
+        float v[16];
+        tmem_ld16(trow + (uint32_t)c0, v);
+        float w[8];
+        int k[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {  // xor 16: keep columns [0, 8) (lanes 0-15) or [8, 16)
+            const bool hi = lane & 16;
+            const float a = valid ? (hi ? v[j + 8] : v[j]) : -INFINITY;
+            const float send = valid ? (hi ? v[j] : v[j + 8]) : -INFINITY;
+            const float b = __shfl_xor_sync(0xffffffffu, send, 16);
+            const int kb = __shfl_xor_sync(0xffffffffu, my_row, 16);
+            w[j] = a;
+            k[j] = my_row;
+            lm_pick(w[j], k[j], b, kb);
+        }
+#pragma unroll
+        for (int o = 8, n = 4; o >= 2; o >>= 1, n >>= 1) {  // xor 8 / 4 / 2: halve the columns held
+            const bool hi = lane & o;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                if (j >= n) break;
+                const float send = hi ? w[j] : w[j + n];
+                const int sk = hi ? k[j] : k[j + n];
+                const float b = __shfl_xor_sync(0xffffffffu, send, o);
+                const int kb = __shfl_xor_sync(0xffffffffu, sk, o);
+                float a = hi ? w[j + n] : w[j];
+                int ka = hi ? k[j + n] : k[j];
+                lm_pick(a, ka, b, kb);
+                w[j] = a;
+                k[j] = ka;
+            }
+        }
+        {  // xor 1: the lane pair agrees on its column's best
+            const float b = __shfl_xor_sync(0xffffffffu, w[0], 1);
+            const int kb = __shfl_xor_sync(0xffffffffu, k[0], 1);
+            lm_pick(w[0], k[0], b, kb);
+        }
+        const int col = c0 + ((lane >> 1) & 15);
+        if (!(lane & 1) && col < nval) {
+            bv[rg * 256 + col] = w[0];
+            bi[rg * 256 + col] = k[0];
+        }
+    }
+    named_bar(2, 256);
+    for (int c = tid; c < nval; c += 256) {
+        float m = bv[c];
+        int i = bi[c];
+#pragma unroll
+        for (int g = 1; g < 4; ++g) lm_pick(m, i, bv[g * 256 + c], bi[g * 256 + c]);
+        st.lm_part[(size_t)tile * st.dm.Bmax + c] = make_float4(m, -INFINITY, 0.f, __int_as_float(i));
+    }
+}
+
 // one LM-head column reduced over all vocab tiles by one warp (fixed tree)
 __device__ __forceinline__ LmPart lm_col_warp(const DevState& st, int b) {
     const int lane = threadIdx.x & 31, tiles = st.dm.Vp / kBM;
@@ -401,9 +476,13 @@ __device__ __forceinline__ void apply4(const DevState& st, const IterSmem& sm, c
     }
 }
 
-// the fill epilogue for a full-K unit straight from TMEM (one row per thread)
-__device__ __forceinline__ void epi_fill_direct(const DevState& st, const IterSmem& sm, int layer, int m, int nval) {
+// the fill epilogue for a full-K unit straight from TMEM (one row per thread).  The rows' K/V
+// destinations at `layer` are looked up once per unit into shared memory (a dependent block-table
+// load per stored element made this epilogue ~7x slower: 28 us per unit at c5, scripts/pipe_tail.py)
+__device__ __forceinline__ void epi_fill_direct(const DevState& st, IterSmem& sm, int layer, int m, int nval) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, dp = st.dm.dp;
+    for (int c = threadIdx.x; c < nval; c += 256) sm.kvd[c] = kv_dst(st, sm, c, layer);
+    named_bar(2, 256);
     const int row = 32 * (warp & 3) + lane;
     const int R = m * kBM + row;
     const int kind = R / dp;  // 0 k, 1 v
@@ -416,7 +495,7 @@ __device__ __forceinline__ void epi_fill_direct(const DevState& st, const IterSm
 #pragma unroll
         for (int j = 0; j < 16; ++j)  // (token turn: only layers past the row's own exit layer)
             if (c0 + j < nval && !(st.turn_token && layer <= st.row_exit[c0 + j]))
-                pool[kv_dst(st, sm, c0 + j, layer) + f] = f32_to_bf16(v[j]);
+                pool[sm.kvd[c0 + j] + f] = f32_to_bf16(v[j]);
     }
 }
 
@@ -1335,7 +1414,7 @@ __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(const __grid_cons
             if (it < n_lm) {
                 unit_ws(sm, ring, p, kseq, st.lm + (size_t)it * (dp / kBK) * (kBM * kBK), bsrc, (size_t)NR * kBK, 0,
                         dp / kBK, useq);
-                if (warp < 8) epi_lm<false>(st, sm, tbuf, it, B);
+                if (warp < 8) epi_lm_argmax(st, sm, tbuf, it, B);
             } else {
                 const int u = it - n_lm;
                 const int mj = u / gf.splits, s = u % gf.splits;  // mj = (jj, m) flattened

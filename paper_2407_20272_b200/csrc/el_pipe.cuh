@@ -51,7 +51,7 @@ __device__ __forceinline__ void publish(unsigned* cnt) {
 // EL_DEBUG builds, dbg bit 128: %globaltimer stamps of (layer, half) events by attention CTA 0
 // (k = 0 wait done, 1 pass done) and GEMM CTA GA (k = 2 att ready, 3 W_o, 4 up, 5 down, 6 QKV(next))
 __device__ __forceinline__ void pipe_stamp(const DevState& st, int layer, int h, int k) {
-    if (EL_DEBUG && (EL_DBG(st) & 128) && threadIdx.x == 0 && layer <= 24) {
+    if (EL_DEBUG && (EL_DBG(st) & 128) && threadIdx.x == 0 && layer <= 25) {  // (layer 25: the tail)
         unsigned long long t;
         asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
         st.dbg_ts[200000 + ((layer - 1) * 2 + h) * 16 + k] = t;
@@ -245,6 +245,7 @@ __global__ void __launch_bounds__(kIterThreads, 1) pipe_kernel(const __grid_cons
     }
     // ---- everything of the layer loop is published: the stop layer is the output layer ----
     grid_sync(p, st, nbar, g0);
+    if (cta == 0) pipe_stamp(st, 25, 0, 0);
     const int e_out = (int)ld_acquire_u32(stop);
     if (cta == 0 && tid == 0) {  // nobody reads the hand-off words any more: zero them for the next launch
         for (int k = 0; k < 192; ++k) p.bar[kPipeGBar + k] = 0u;
@@ -258,11 +259,21 @@ __global__ void __launch_bounds__(kIterThreads, 1) pipe_kernel(const __grid_cons
     const int fill_units = (L - e_out) * m2 * gf.splits;
     {
         const uint16_t* bsrc = st.hb + (size_t)pe * NR * dp;
-        for (int it = cta; it < n_lm + fill_units; it += G) {
+        int un = 0;  // (dbg 128: per-unit stamps of CTAs 0 / 1 -- start, accumulator ready, epilogue done)
+        auto ustamp = [&](int k) {
+            if (EL_DEBUG && (EL_DBG(st) & 128) && cta < 2 && tid == 0 && un < 8) {
+                unsigned long long t;
+                asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+                st.dbg_ts[201000 + cta * 32 + un * 4 + k] = t;
+            }
+        };
+        for (int it = cta; it < n_lm + fill_units; it += G, ++un) {
+            ustamp(0);
             if (it < n_lm) {
                 unit_ws(sm, ring, p, kseq, st.lm + (size_t)it * (dp / kBK) * (kBM * kBK), bsrc, (size_t)NR * kBK, 0,
                         dp / kBK, useq);
-                if (warp < 8) epi_lm<false>(st, sm, tbuf, it, B);
+                ustamp(1);
+                if (warp < 8) epi_lm_argmax(st, sm, tbuf, it, B);
             } else {
                 const int u = it - n_lm;
                 const int mj = u / gf.splits, s = u % gf.splits;
@@ -271,6 +282,7 @@ __global__ void __launch_bounds__(kIterThreads, 1) pipe_kernel(const __grid_cons
                 const uint16_t* a =
                     gf.A + (size_t)((j - 1) * gf.layer_rows + gf.row_off + m) * gf.kb_total * (kBM * kBK);
                 unit_ws(sm, ring, p, kseq, a, bsrc, (size_t)NR * kBK, kb0, kb1 - kb0, useq);
+                ustamp(1);
                 if (warp < 8) {
                     if (gf.splits == 1) epi_fill_direct(st, sm, j, m, B);
                     else epi_partial(sm, p, u, B);
@@ -279,9 +291,12 @@ __global__ void __launch_bounds__(kIterThreads, 1) pipe_kernel(const __grid_cons
             ++useq;
             tc_fence_before();
             __syncthreads();
+            ustamp(2);
         }
     }
+    if (cta == 0) pipe_stamp(st, 25, 0, 1);
     grid_sync(p, st, nbar, g0);
+    if (cta == 0) pipe_stamp(st, 25, 0, 2);
     if (fill_units > 0 && gf.splits > 1) {
         const IterCtx x{e_out + 1, 0, 0};
         reduce_phase<kIFill>(st, sm, p, gf, x, B, 0, (L - e_out) * m2);
@@ -304,6 +319,7 @@ __global__ void __launch_bounds__(kIterThreads, 1) pipe_kernel(const __grid_cons
             }
         }
     }
+    if (cta == 0) pipe_stamp(st, 25, 0, 3);
     if (cta == 0 && tid == 0) {
         *(volatile unsigned*)(p.bar + 2) = g0.y + (unsigned)G * (unsigned)nbar;  // next launch's count base
         for (int i = 0; i < kINumGemm * 64; ++i) p.tcnt[i] = 0u;
