@@ -727,7 +727,7 @@ __device__ __forceinline__ void apply16_t(const DevState& st, const IterSmem& sm
 #pragma unroll
             for (int t = 0; t < 4; ++t) q[t] = make_float4(v[4 * t], v[4 * t + 1], v[4 * t + 2], v[4 * t + 3]);
         } else {
-            uint16_t* dst = (kind == 1 ? st.kpool : st.vpool) + kv_dst(st, sm, b, x.layer) + (f - kind * dp);
+            uint16_t* dst = (kind == 1 ? st.kpool : st.vpool) + sm.kvd[b] + (f - kind * dp);  // (gemm_phase_t)
             reinterpret_cast<uint4*>(dst)[0] = pack(v);
             reinterpret_cast<uint4*>(dst)[1] = pack(v + 8);
         }
@@ -1003,6 +1003,12 @@ __device__ __forceinline__ void gemm_phase_t(const DevState& st, IterSmem& sm, u
             st.dbg_ts[300000 + (size_t)blockIdx.x * 32 + K * 8 + k] = clock64();
     };
     stamp(0);
+    if constexpr (K == kIQkv) {  // the rows' K/V destinations at this layer, looked up once per phase
+        if (st.kpool) {
+            for (int b = threadIdx.x; b < B; b += blockDim.x) sm.kvd[b] = kv_dst(st, sm, b, x.layer);
+            __syncthreads();
+        }
+    }
     for (int u = CI; u < U; u += CN) {
         const int f0 = (u / R) * g.nt, rg = rg_only >= 0 ? rg_only : u % R;
         const int row_block = (x.layer - 1) * g.layer_rows + g.row_off + f0 / kBM;
