@@ -711,8 +711,10 @@ __device__ bool exit_decide(const DevState& st, IterSmem& sm, int layer, int B, 
 // per CTA (B x K bf16), cheap for B <= 128.
 // ---------------------------------------------------------------------------
 template <int K>
+// res (optional): the 16 residual inputs of this (row, features), loaded before the unit's
+// accumulator was ready (gemm_phase_t) so their L2 round trip overlaps the mainloop
 __device__ __forceinline__ void apply16_t(const DevState& st, const IterSmem& sm, const IterCtx& x, int b, int f,
-                                          const float* v) {
+                                          const float* v, const float4* res = nullptr) {
     const int dp = st.dm.dp, NR = st.NR, Bm = st.dm.Bmax;
     auto pack = [](const float* w) {
         return make_uint4((uint32_t)f32_to_bf16(w[0]) | ((uint32_t)f32_to_bf16(w[1]) << 16),
@@ -737,7 +739,7 @@ __device__ __forceinline__ void apply16_t(const DevState& st, const IterSmem& sm
         float o[16];
 #pragma unroll
         for (int t = 0; t < 4; ++t) {
-            const float4 hv = __ldcg(h + t);
+            const float4 hv = res ? res[t] : __ldcg(h + t);
             o[4 * t] = hv.x + v[4 * t];
             o[4 * t + 1] = hv.y + v[4 * t + 1];
             o[4 * t + 2] = hv.z + v[4 * t + 2];
@@ -754,7 +756,7 @@ __device__ __forceinline__ void apply16_t(const DevState& st, const IterSmem& sm
         float o[16];
 #pragma unroll
         for (int t = 0; t < 4; ++t) {
-            const float4 hv = __ldcg(m4 + t);
+            const float4 hv = res ? res[t] : __ldcg(m4 + t);
             o[4 * t] = hv.x + v[4 * t];
             o[4 * t + 1] = hv.y + v[4 * t + 1];
             o[4 * t + 2] = hv.z + v[4 * t + 2];
@@ -985,7 +987,7 @@ __device__ __forceinline__ bool bm_prefetch(IterSmem& sm, uint8_t* ring, const I
     return true;
 }
 
-template <int K>
+template <int K, bool kPre = false>  // kPre: residual prefetch (pipelined kernel: free registers)
 __device__ __forceinline__ void gemm_phase_t(const DevState& st, IterSmem& sm, uint8_t* ring, const IterPlan& p,
                                              const IterMaps& maps, int gid, const IterCtx& x, const uint16_t* act,
                                              uint32_t& cseq, uint32_t& wseq, uint32_t& useq, int B, bool& wpf,
@@ -1012,6 +1014,26 @@ __device__ __forceinline__ void gemm_phase_t(const DevState& st, IterSmem& sm, u
     for (int u = CI; u < U; u += CN) {
         const int f0 = (u / R) * g.nt, rg = rg_only >= 0 ? rg_only : u % R;
         const int row_block = (x.layer - 1) * g.layer_rows + g.row_off + f0 / kBM;
+        // residual-add epilogues: this thread's residual inputs (row b, its first two 16-feature
+        // chunks) are loaded now, their L2 latency hidden behind the mainloop
+        constexpr bool kRes = kPre && (K == kIWo || K == kIWoc);
+        float4 res[2][4];
+        const bool m64p = p.bm_m == 64;
+        const int bp = rg * p.bm_grp + (m64p ? 16 * (warp & 3) + lane : 32 * (warp & 3) + lane);
+        const bool vp = warp < 8 && bp < B && (!m64p || lane < 16);
+        if constexpr (kRes) {
+            if (vp) {
+                const float* base = (K == kIWo ? st.h32 + (size_t)x.pin * st.dm.Bmax * st.dm.dp : st.mid32) +
+                                    (size_t)bp * st.dm.dp + f0;
+#pragma unroll
+                for (int q = 0; q < 2; ++q) {
+                    const int c0 = 16 * (warp >> 2) + 32 * q;
+                    if (c0 < g.nt)
+#pragma unroll
+                        for (int t = 0; t < 4; ++t) res[q][t] = __ldcg(reinterpret_cast<const float4*>(base + c0) + t);
+                }
+            }
+        }
         unit_bm(sm, ring, p, cseq, wseq, &maps.w[gid], 0, f0 % kBM, row_block * g.kb_total,
                 act + (size_t)rg * p.bm_grp * kBK, g.kb_total, g.nt, useq, wpf,
                 g.A + (size_t)row_block * g.kb_total * (kBM * kBK) + (size_t)(f0 % kBM) * kBK);
@@ -1027,10 +1049,21 @@ __device__ __forceinline__ void gemm_phase_t(const DevState& st, IterSmem& sm, u
             const int b = rg * p.bm_grp + (m64 ? 16 * (warp & 3) + lane : 32 * (warp & 3) + lane);
             const bool valid = b < B && (!m64 || lane < 16);
             const uint32_t trow = sm.tmem + ((uint32_t)(32 * (warp & 3)) << 16);
-            for (int c0 = 16 * (warp >> 2); c0 < g.nt; c0 += 32) {
-                float v[16];
-                tmem_ld16(trow + (uint32_t)c0, v);
-                if (valid) apply16_t<K>(st, sm, x, b, f0 + c0, v);
+            if constexpr (kRes) {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {  // (nt <= 128: at most 4 chunks of 16 features per thread)
+                    const int c0 = 16 * (warp >> 2) + 32 * q;
+                    if (c0 >= g.nt) break;
+                    float v[16];
+                    tmem_ld16(trow + (uint32_t)c0, v);
+                    if (valid) apply16_t<K>(st, sm, x, b, f0 + c0, v, q < 2 ? res[q & 1] : nullptr);
+                }
+            } else {
+                for (int c0 = 16 * (warp >> 2); c0 < g.nt; c0 += 32) {
+                    float v[16];
+                    tmem_ld16(trow + (uint32_t)c0, v);
+                    if (valid) apply16_t<K>(st, sm, x, b, f0 + c0, v);
+                }
             }
         }
         stamp(3);

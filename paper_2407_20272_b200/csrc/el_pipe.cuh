@@ -200,7 +200,7 @@ __global__ void __launch_bounds__(kIterThreads, 1) pipe_kernel(const __grid_cons
                 fence_proxy_async_global();
                 if (gi == 0) pipe_stamp(st, layer, h, 2);
                 // W_o + residual (model.cpp:245-253), up + ReLU (255-260)
-                gemm_phase_t<kIWo>(st, sm, ring, p, maps, kIWo, x, st.att_b, kseq2, wseq, useq, B, wpf, kIUp, layer,
+                gemm_phase_t<kIWo, true>(st, sm, ring, p, maps, kIWo, x, st.att_b, kseq2, wseq, useq, B, wpf, kIUp, layer,
                                    gi, GG, h, h);
                 group_sync(gbar, (unsigned)GG, ++gk);
                 if (gi == 0) pipe_stamp(st, layer, h, 3);

@@ -1,0 +1,10 @@
+L=paper_2407_20272_b200/libexitlab_b200.so
+for rep in 1 2; do
+  for v in kvd res2; do
+    cp ab/lib_$v.so $L
+    for c in c5 c2; do
+    python bench.py --config $c --no-cpu-baseline --no-c4 --no-layer-level --no-engine-run 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$v $c', d['value'], d['ms_per_step'], d['full_layer']['value'])"
+    done
+  done
+done > gpurun_out/ab_res.txt 2>&1
+cp ab/lib_res2.so $L
