@@ -618,8 +618,10 @@ __device__ __forceinline__ void reduce_range(const DevState& st, const IterSmem&
                         for (int t = 0; t < 4; ++t) x0 += (double)wv[t] * (double)ov[t];
                     }
                     x0 = warp_sum_d(x0);
-                    x1 = warp_sum_d(x1);
-                    x2 = warp_sum_d(x2);
+                    if (st.technique == kState) {  // (classifier: one dot only)
+                        x1 = warp_sum_d(x1);
+                        x2 = warp_sum_d(x2);
+                    }
                     if (lane == 0 && !dry) {
                         double* q = st.exit_part + ((size_t)m * Bm + c) * 3;
                         q[0] = x0;

@@ -796,6 +796,9 @@ struct AttnSrc {
     // work range (the pipelined kernel runs attention for one half of the batch on a subset of
     // the CTAs): rows [r0, r1) (r1 < 0: all rows), CTA cta of ncta (< 0: blockIdx.x / gridDim.x)
     int r0 = 0, r1 = -1, cta = -1, ncta = -1;
+    // abort != nullptr: a speculative pass (the pipelined kernel's next-layer attention of the first
+    // half) stops issuing blocks once *abort turns non-zero (the batch exited; its results are unused)
+    const unsigned* abort = nullptr;
 };
 
 // attn_prefix_sum: the warp-parallel prefix sum of KV blocks per row into a.pref
@@ -1230,7 +1233,7 @@ __device__ __forceinline__ void attn_consumer(const DevState& st, AttnSmem& a, u
 
 // persistent: called from the persistent kernel -- a.pref is already valid and
 // no programmatic-dependent-launch deferral is needed (every input is ready).
-template <int NJ>
+template <int NJ, bool kAbort = false>  // kAbort: the pass may be stopped early (AttnSrc::abort)
 __device__ __forceinline__ void attn_body(const DevState& st, AttnSmem& a, uint8_t* stages, int layer, int seq0,
                           bool persistent, const AttnSrc& src, float* mbuf) {
     const Dims& dm = st.dm;
@@ -1324,6 +1327,7 @@ __device__ __forceinline__ void attn_body(const DevState& st, AttnSmem& a, uint8
             }
         };
         int seq = seq0;
+        bool aborted = false;
         // stream blocks [g, seg_end) (absolute flattened indices) of row b as one segment
         // (partial slot `slot` of `nseg`); pid: the block ids of [g, seg_end) already in shared
         // memory (a.ids), or nullptr
@@ -1339,15 +1343,21 @@ __device__ __forceinline__ void attn_body(const DevState& st, AttnSmem& a, uint8
                 for (int u = 0; u < nb; ++u, ++seq) {
                     const int id = __shfl_sync(0xffffffffu, my_id, u);
                     const int blk = blk_base + u;
-                    // 0: nothing for the issue lanes; bit 0: K|V of this block; bit 1: q too
+                    // 0: nothing for the issue lanes; bit 0: K|V of this block; bit 1: q too; -1: abort
                     int xgo = 0;
                     if (lane == 0) {
                         const int s = seq % S;
                         if (seq == seq0) EL_ATT_CLK(8);
+                        unsigned fl = 0;
                         if (seq >= S) {
+                            if constexpr (kAbort)
+                                if (src.abort) fl = *(volatile const unsigned*)src.abort;  // (latency under the wait)
                             if (!waited) flush();  // the ring is full: release the deferred stage first
                             mbar_wait(&a.empty[s], ((seq / S) - 1) & 1);
                         }
+                        if (kAbort && fl) {
+                            xgo = -1;
+                        } else {
                         if (seq == seq0) EL_ATT_CLK(9);
                         const int rows = min(dm.bc, ctx - blk * dm.bc);
                         const uint32_t bytes = (uint32_t)rows * dp * 2;
@@ -1374,6 +1384,7 @@ __device__ __forceinline__ void attn_body(const DevState& st, AttnSmem& a, uint8
                         } else {
                             xgo = first ? 3 : 1;
                         }
+                        }  // (not aborted)
                     }
                     // The block's copies are issued by lanes other than 0, a different lane triple per
                     // ring slot: one thread's bulk copies are processed one after another (~0.4 us each
@@ -1381,6 +1392,10 @@ __device__ __forceinline__ void attn_body(const DevState& st, AttnSmem& a, uint8
                     // lane caps a CTA at ~80 GB/s; copies of different lanes overlap.
                     xgo = __shfl_sync(0xffffffffu, xgo, 0);
                     __syncwarp();  // (orders lane 0's empty-slot acquire before the other lanes' copies)
+                    if (kAbort && xgo < 0) {  // aborted: this block is not issued (seq stays its slot)
+                        aborted = true;
+                        break;
+                    }
                     if (xgo) {
                         const int il = EL_LANE_ISSUE ? 1 + 3 * (seq % 10) : 0;  // lanes 1..30
                         const int s = seq % S;
@@ -1396,6 +1411,7 @@ __device__ __forceinline__ void attn_body(const DevState& st, AttnSmem& a, uint8
                     }
                 }
                 __syncwarp();
+                if (kAbort && aborted) break;
             }
         };
         // ---- this CTA's range ----
@@ -1443,6 +1459,7 @@ __device__ __forceinline__ void attn_body(const DevState& st, AttnSmem& a, uint8
                 int fc = 0;
                 const int nseg = row_static(b, fc);
                 emit(b, g, seg_end, CI - fc, nseg, pre ? a.ids[ib] + (g - g0) : nullptr);
+                if (kAbort && aborted) break;
                 g = seg_end;
                 ++b;
             }
@@ -1464,10 +1481,10 @@ __device__ __forceinline__ void attn_body(const DevState& st, AttnSmem& a, uint8
 
 // The persistent kernel's attention pass: one out-of-line copy for the self and the
 // cross pass (st points at the kernel's shared-memory copy of the parameters).
-template <int NJ>
+template <int NJ, bool kAbort = false>
 __device__ __forceinline__ void attn_pass(const DevState& st, AttnSmem& a, uint8_t* stages, int layer, int seq0,
                                        const AttnSrc src, float* mbuf) {
-    attn_body<NJ>(st, a, stages, layer, seq0, true, src, mbuf);
+    attn_body<NJ, kAbort>(st, a, stages, layer, seq0, true, src, mbuf);
 }
 
 template <int NJ>

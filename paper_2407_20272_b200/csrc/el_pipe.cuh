@@ -168,7 +168,10 @@ __global__ void __launch_bounds__(kIterThreads, 1) pipe_kernel(const __grid_cons
                 src.r1 = h ? B : H1;
                 src.cta = ai;
                 src.ncta = GA;
-                attn_pass<NJ>(st, sm.att, ring, layer, aseq, src, nullptr);
+                // the first half's pass of layer l >= 2 may be speculative (the exit decision of layer
+                // l - 1 comes from the GEMM CTAs during it): stop issuing once the batch has stopped
+                if (h == 0 && layer > 1) src.abort = stop;
+                attn_pass<NJ, true>(st, sm.att, ring, layer, aseq, src, nullptr);
                 publish(att_cnt + 32 * h);     // (its __syncthreads orders the consumers' seq_next write)
                 aseq = sm.att.seq_next;
                 if (ai == 0) pipe_stamp(st, layer, h, 1);
@@ -250,6 +253,10 @@ __global__ void __launch_bounds__(kIterThreads, 1) pipe_kernel(const __grid_cons
     if (cta == 0 && tid == 0) {  // nobody reads the hand-off words any more: zero them for the next launch
         for (int k = 0; k < 192; ++k) p.bar[kPipeGBar + k] = 0u;
     }
+    // an aborted speculative pass leaves its rows' segment counts partial: every attention pass is
+    // over, so clear them for the next launch (completed rows were cleared by their combine)
+    if (cta == 1 % G)
+        for (int b = tid; b < B; b += blockDim.x) st.attn_cnt[b] = 0;
 
     // ---- tail: greedy LM head over h_e and the skipped-layer fill (kv_cache.cpp:222-234), all CTAs ----
     const int pe = e_out & 1;
