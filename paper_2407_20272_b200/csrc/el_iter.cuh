@@ -504,7 +504,7 @@ __device__ __forceinline__ void epi_fill_direct(const DevState& st, IterSmem& sm
 // summed in split order (deterministic).  K == kIDown also produces the exit
 // check's per-tile partial dots (fp64, fixed shuffle tree).
 // pieces [P0, P) (piece = m * nval + c), this warp's first piece P0 + gw, stride GW
-template <int K>
+template <int K, int NP = 2>  // NP: pieces in flight per warp
 // dry: compute on whatever the partials hold and store nothing -- an instruction-cache
 // warm-up run of this exact code while the tile's other splits are still arriving
 // row0: batch row of column 0 (the pipelined kernel reduces one half of the batch at a time)
@@ -519,14 +519,15 @@ __device__ __forceinline__ void reduce_range(const DevState& st, const IterSmem&
     };
     rstamp(0);
     const int dp = st.dm.dp, Bm = st.dm.Bmax;
-    for (int p0 = P0 + gw; p0 < P; p0 += 2 * GW) {
-        int mm[2], cc[2];
-        bool ok[2];
-        float4 acc[2];
-        Side4 sd[2];
-        float4 dmid[2], dh[2], dw[2];  // down: mid row, previous h (state), probe weights (classifier)
+    constexpr int KC = NP == 2 ? 8 : 6;  // splits loaded per round (register budget: 168 at 288 threads)
+    for (int p0 = P0 + gw; p0 < P; p0 += NP * GW) {
+        int mm[NP], cc[NP];
+        bool ok[NP];
+        float4 acc[NP];
+        Side4 sd[NP];
+        float4 dmid[NP], dh[NP], dw[NP];  // down: mid row, previous h (state), probe weights (classifier)
 #pragma unroll
-        for (int j = 0; j < 2; ++j) {
+        for (int j = 0; j < NP; ++j) {
             const int pp = p0 + j * GW;
             ok[j] = pp < P;
             mm[j] = ok[j] ? pp / nval : 0;
@@ -552,12 +553,12 @@ __device__ __forceinline__ void reduce_range(const DevState& st, const IterSmem&
             }
         }
         rstamp(1);
-        for (int s0 = 0; s0 < S; s0 += 8) {
-            float4 v[2][8];
+        for (int s0 = 0; s0 < S; s0 += KC) {
+            float4 v[NP][KC];
 #pragma unroll
-            for (int j = 0; j < 2; ++j)
+            for (int j = 0; j < NP; ++j)
 #pragma unroll
-                for (int k = 0; k < 8; ++k) {
+                for (int k = 0; k < KC; ++k) {
                     v[j][k] = make_float4(0.f, 0.f, 0.f, 0.f);
                     if (ok[j] && s0 + k < S) {
                         // unit index of (tile m, split s): fill units are (jj, m2, s) with m = jj*m2 + m2 == tile index
@@ -566,9 +567,9 @@ __device__ __forceinline__ void reduce_range(const DevState& st, const IterSmem&
                     }
                 }
 #pragma unroll
-            for (int j = 0; j < 2; ++j)
+            for (int j = 0; j < NP; ++j)
 #pragma unroll
-                for (int k = 0; k < 8; ++k)
+                for (int k = 0; k < KC; ++k)
                     if (s0 + k < S) {
                         acc[j].x += v[j][k].x;
                         acc[j].y += v[j][k].y;
@@ -578,7 +579,7 @@ __device__ __forceinline__ void reduce_range(const DevState& st, const IterSmem&
         }
         rstamp(2);
 #pragma unroll
-        for (int j = 0; j < 2; ++j) {
+        for (int j = 0; j < NP; ++j) {
             if (!ok[j]) continue;  // warp-uniform
             const int m = mm[j], c = cc[j] + row0, r0 = 4 * lane;
             if constexpr (K == kIFill) {
@@ -1088,7 +1089,7 @@ __device__ __forceinline__ void gemm_phase_t(const DevState& st, IterSmem& sm, u
 // a launch and are zeroed at its end)
 // ci / cn: this CTA's index in the set of CTAs running the phase; row0 / n_rows: the batch rows
 // of the phase (bsrc must point at row row0 of the activation layout; n_rows 0 = n_pad)
-template <int K>
+template <int K, int NP = 2>
 __device__ void gemm_phase_fused(const DevState& st, IterSmem& sm, uint8_t* ring, const IterPlan& p, int gid,
                                  const IterCtx& x, const uint16_t* bsrc, uint32_t& kseq, uint32_t& useq, int nval,
                                  int use, int ci = -1, int cn = -1, int row0 = 0, int n_rows = 0) {
@@ -1145,7 +1146,7 @@ __device__ void gemm_phase_fused(const DevState& st, IterSmem& sm, uint8_t* ring
                 stamp(3);
             }
             if (warp < 8)
-                reduce_range<K>(st, sm, p, g, x, nval, 0, m * nval + c0, m * nval + c1, warp, 8, pass == 0, row0);
+                reduce_range<K, NP>(st, sm, p, g, x, nval, 0, m * nval + c0, m * nval + c1, warp, 8, pass == 0, row0);
         }
         __syncthreads();
         stamp(4);

@@ -214,6 +214,8 @@ __global__ void __launch_bounds__(kIterThreads, 1) pipe_kernel(const __grid_cons
                 // down + residual (261-270) + exit-check partial dots of these rows (split-K, fused reduce)
                 if (tid == kProducerWarp * 32 && layer < L)
                     wpf = bm_prefetch(sm, ring, p, maps, kIQkv, layer + 1, gi, h, GG);
+                // (3 pieces in flight per warp -- one round of loads for a tile's ~21 pieces instead of
+                //  two -- spills at the 168-register cap of 288 threads: -1 % at c5)
                 gemm_phase_fused<kIDown>(st, sm, ring, p, kIDown, x, st.up_b + (size_t)r0 * kBK, kseq, useq, hrows[h],
                                          ++down_uses, gi, GG, r0, H1);
                 group_sync(gbar, (unsigned)GG, ++gk);
