@@ -32,6 +32,7 @@
 #ifndef EXITLAB_B200_H
 #define EXITLAB_B200_H
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -91,6 +92,11 @@ int el_set_device(int device);
 int el_device_count(int* n);
 
 int el_engine_create(const el_engine_config* cfg, el_engine** out);
+/* The same, for callers compiled against another revision of this header: config_size =
+ * sizeof(el_engine_config) as the caller sees it; fields past it take their zero defaults (the
+ * reference's decoder-only, single-head model), fields the library does not know are rejected
+ * unless zero. */
+int el_engine_create_sized(const el_engine_config* cfg, size_t config_size, el_engine** out);
 int el_engine_destroy(el_engine* e);
 /* options: "graph" (1: CUDA graph with a device-side WHILE over layers, 0: eager),
  *          "rec_cap" (iterations kept in the device record ring) */

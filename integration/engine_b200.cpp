@@ -95,7 +95,7 @@ Transcript Engine::run(const Workload& workload) const {
         return out;
     }
     EngineHandle eh;
-    check(el_engine_create(&ec, &eh.e));
+    check(el_engine_create_sized(&ec, sizeof(ec), &eh.e));
     TranscriptHandle th;
     check(el_engine_run(eh.e, (int)arrival.size(), arrival.data(), off.data(), prompt.data(), max_new.data(), &th.t));
     const el_transcript* t = th.t;

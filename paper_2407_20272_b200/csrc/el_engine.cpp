@@ -1998,6 +1998,23 @@ int el_engine_create(const el_engine_config* cfg, el_engine** out) {
     API_END
 }
 
+int el_engine_create_sized(const el_engine_config* cfg, size_t config_size, el_engine** out) {
+    API_BEGIN
+    if (!cfg || !out) fail(EL_INVALID_ARGUMENT, "null argument");
+    *out = nullptr;
+    el_engine_config c{};
+    const size_t n = std::min(config_size, sizeof(el_engine_config));
+    std::memcpy(&c, cfg, n);
+    const unsigned char* extra = reinterpret_cast<const unsigned char*>(cfg) + n;
+    for (size_t i = n; i < config_size; ++i)
+        if (extra[i - n]) fail(EL_INVALID_ARGUMENT, "el_engine_config: unknown non-zero field at byte %zu", i);
+    auto e = std::make_unique<el_engine>();
+    e->cfg = c;
+    e->create();
+    *out = e.release();
+    API_END
+}
+
 int el_engine_destroy(el_engine* e) {
     API_BEGIN
     if (e) {

@@ -51,6 +51,7 @@ def lib():
         L = C.CDLL(LIB)
         L.el_last_error.restype = C.c_char_p
         L.el_engine_create.argtypes = [C.c_void_p, C.POINTER(C.c_void_p)]
+        L.el_engine_create_sized.argtypes = [C.c_void_p, C.c_size_t, C.POINTER(C.c_void_p)]
         L.el_engine_destroy.argtypes = [C.c_void_p]
         L.el_engine_set_option.argtypes = [C.c_void_p, C.c_char_p, C.c_int64]
         L.el_engine_run.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
@@ -641,7 +642,7 @@ class Engine:
         self.config = config
         self._c = to_c_config(config)
         h = C.c_void_p()
-        _check(lib().el_engine_create(C.byref(self._c), C.byref(h)))
+        _check(lib().el_engine_create_sized(C.byref(self._c), C.sizeof(self._c), C.byref(h)))
         self._h = h
         self.L, self.d, self.V = config.model.n_layers, config.model.d_model, config.model.vocab_size
         self.B = 0

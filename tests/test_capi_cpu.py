@@ -82,3 +82,18 @@ def test_workload_flat_round_trip():
     flat = w.flat()
     back = X.Workload.from_flat(*flat)
     assert back == w
+
+
+def test_create_sized_rejects_unknown_nonzero_fields():
+    """el_engine_create_sized: a caller's struct longer than the library's may only carry zeros
+    past it (checked before any device work, so this runs without a GPU)."""
+    import ctypes as C
+    from paper_2407_20272_b200 import exitlab as X
+    lib = X.lib()
+    n = C.sizeof(X._CConfig)
+    buf = (C.c_ubyte * (n + 8))()
+    buf[n + 3] = 1
+    h = C.c_void_p()
+    rc = lib.el_engine_create_sized(C.cast(buf, C.c_void_p), n + 8, C.byref(h))
+    assert rc == 1 and not h.value  # EL_INVALID_ARGUMENT
+    assert b"unknown non-zero field" in lib.el_last_error()
