@@ -759,10 +759,13 @@ struct el_engine {
         P.bm_stages = std::max(2, std::min(P.bm_wstream ? 6 : 4, (P.bm_woff - 16384) / P.bm_astage));
         if (bm && P.bm_stages * P.bm_astage > P.bm_woff)
             fail(EL_INVALID_ARGUMENT, "persistent kernel: batch-M ring does not fit");
-        P.bm_prefetch = (bm && !P.bm_wstream && opt_mega_bm_prefetch && ring_att <= P.bm_woff) ? 1 : 0;
+        // (the pipelined kernel's GEMM CTAs run no attention: their weight slab may overlap the
+        //  attention ring; its split-K / tail ring keeps the whole region, as no slab prefetch is
+        //  in flight while it runs -- the next layer's QKV weights are not prefetched there)
+        P.bm_prefetch = (bm && !P.bm_wstream && opt_mega_bm_prefetch && (pipe_grid || ring_att <= P.bm_woff)) ? 1 : 0;
         // weight-streaming ring + transpose buffer stay below the weight buffer when weights are
         // prefetched into it during other phases
-        const int ws_cap = (bm && P.bm_prefetch) ? P.bm_woff : cap;
+        const int ws_cap = (bm && P.bm_prefetch && !pipe_grid) ? P.bm_woff : cap;
         P.stages = std::min(8, (ws_cap - el::kIterTbufBytes) / stage);
         if (P.stages < 2) fail(EL_INVALID_ARGUMENT, "persistent kernel: GEMM ring does not fit");
         P.gemm_ring = P.stages * stage;

@@ -212,8 +212,10 @@ __global__ void __launch_bounds__(kIterThreads, 1) pipe_kernel(const __grid_cons
                 group_sync(gbar, (unsigned)GG, ++gk);
                 if (gi == 0) pipe_stamp(st, layer, h, 4);
                 // down + residual (261-270) + exit-check partial dots of these rows (split-K, fused reduce)
-                if (tid == kProducerWarp * 32 && layer < L)
-                    wpf = bm_prefetch(sm, ring, p, maps, kIQkv, layer + 1, gi, h, GG);
+                // next layer's QKV weights: L2 prefetch with streamed weights only (a slab prefetch
+                // would land in the region the down phase's split-K ring uses)
+                if (p.bm_wstream && tid == kProducerWarp * 32 && layer < L)
+                    bm_prefetch(sm, ring, p, maps, kIQkv, layer + 1, gi, h, GG);
                 // (3 pieces in flight per warp -- one round of loads for a tile's ~21 pieces instead of
                 //  two -- spills at the 168-register cap of 288 threads: -1 % at c5)
                 gemm_phase_fused<kIDown>(st, sm, ring, p, kIDown, x, st.up_b + (size_t)r0 * kBK, kseq, useq, hrows[h],
@@ -226,18 +228,6 @@ __global__ void __launch_bounds__(kIterThreads, 1) pipe_kernel(const __grid_cons
                         e_out = layer;
                         done = true;
                         if (tid == 0 && gi == 0) st_release_u32(stop, (unsigned)layer);
-                        // the prefetched QKV weights of the next layer: retire that load
-                        const IterGemm& gq = p.g[kIQkv];
-                        if (layer < L && p.bm_prefetch && gi < gq.m_tiles * kBM / gq.nt) {
-                            if (warp == 0) {
-                                mbar_wait(&sm.wfull, wseq & 1);
-                                ++wseq;
-                            }
-                            if (tid == kProducerWarp * 32) {
-                                ++wseq;
-                                wpf = false;
-                            }
-                        }
                         break;
                     }
                 }
