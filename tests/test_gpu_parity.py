@@ -455,6 +455,33 @@ def test_batched_prefill_kv_matches_oracle(port, mega):
     e.close()
 
 
+def test_batched_prefill_and_pipelined_decode_at_batch_144(port):
+    """f1 with more than 128 sequences (position-major prefill launches of up to 144 rows on the
+    persistent kernel -- the pipelined kernel measured slower for prefill, whose short early
+    contexts leave its attention CTAs idle) and the pipelined decode at batch 144, small dims.
+    K/V of every layer and the tokens vs the oracle's token-by-token fp64 prefill."""
+    L, d, V, B = 3, 128, 512, 144
+    g = X.EngineConfig(model=X.ModelConfig(L, d, V, 23), technique=X.ExitTechnique("never"), max_batch=B,
+                       pool_blocks=8192, eos_token=-1, capture_kv=True)
+    o = OB.engine_config(L, d, V, 23, "never", max_batch=B, pool_blocks=8192, eos_token=-1, capture_kv=True,
+                         round_bf16=True)
+    rng = np.random.default_rng(9)
+    reqs = [(0.0, [int(x) for x in rng.integers(1, V, 2 + (i * 7) % 9)], 2) for i in range(B)]
+    e = X.Engine(g, mega=True)
+    t = e.run(X.Workload([X.Request(*r) for r in reqs]))
+    tp = port.model(L, d, V, 23, True).run(o, OB.Workload.from_requests(reqs))
+    for sid in range(0, B, 7):
+        n = len(reqs[sid][1]) - 1
+        for layer in range(1, L + 1):
+            kg, vg = t.kv(sid, layer)
+            ko, vo = port.transcript_kv(tp, sid, layer, d)
+            assert relerr(kg[:n], ko[:n]) <= HID_TOL and relerr(vg[:n], vo[:n]) <= HID_TOL, (sid, layer)
+    gt = {s["id"]: s["tokens"] for s in t.sequences}
+    pt = {s["id"]: s["tokens"] for s in tp.sequences}
+    assert np.mean([a == b for k in pt for a, b in zip(gt[k], pt[k])]) >= 0.9
+    e.close()
+
+
 def test_transcript_jsonl_byte_identical_on_device(port, tmp_path):
     """f3: the B200 engine's transcript written in the reference's JSONL format is byte-identical
     to the oracle's (and so to the reference's writer, tests/test_transcript_jsonl_cpu.py) when
