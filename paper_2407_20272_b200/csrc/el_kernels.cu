@@ -690,26 +690,20 @@ void launch_gemm(GemmKind kind, const GemmPlan& p, const DevState& st, cudaStrea
 }
 
 // ===========================================================================
-// 2. Paged single-head decode attention over the block pool
-//    (model.cpp:223-243: scores = K q / sqrt(d), softmax, P V).
-//    grid (chunk, row): each CTA streams a chunk of `attn_cb` KV blocks of one
-//    sequence through a ring of shared-memory stages with 1-D TMA bulk copies
-//    (a block is bc x dp contiguous bf16 for K and for V), keeps an online
-//    softmax, and writes an unnormalised partial (o, m, l). The last CTA of a
-//    sequence combines the partials in chunk order (flash-decoding) and emits
-//    the bf16 attention output for the W_o GEMM.
+// 2. Paged decode attention over the block pool (model.cpp:223-243: scores = K q / sqrt(d),
+//    softmax, P V; the multi-head extension splits d into heads, each with its own softmax).
 // ===========================================================================
-// Work item = (sequence b, chunk c of attn_cb KV blocks).  The kernel is
-// persistent (one CTA per SM); a producer warp pulls items from an atomic
-// queue and streams their K/V blocks (plus the sequence's q on an item's first
-// block) through a ring of shared-memory stages with 1-D bulk TMA, running
-// ahead across item boundaries so HBM never idles.  Eight consumer warps own
-// two rows of every block each (processed together for ILP) and keep their
-// own online-softmax state (m, l, o); a stage is released by 8 warp arrivals
-// on its "empty" mbarrier, so the main loop has no CTA-wide barrier.  At the
-// end of an item the warps merge in fixed order inside the just-consumed
-// stage buffer; the last chunk of a sequence to finish combines the partials
-// in chunk order (flash-decoding) into the bf16 attention output.
+// The flattened (row, KV block) space of a pass is cut statically over the CTAs (cost-aware:
+// a row start costs attn_seg_cost extra blocks), one segment per (CTA, row).  A producer warp
+// streams the CTA's blocks (a block is bc x dp contiguous bf16 for K and for V, plus the row's
+// q on a segment's first block) through a ring of shared-memory stages with 1-D bulk copies,
+// running ahead across segment boundaries.  Eight consumer warps own two rows of every block
+// each (processed together for ILP) and keep their own online-softmax state (m, l, o); a stage
+// is released by 8 warp arrivals on its "empty" mbarrier, so the main loop has no CTA-wide
+// barrier.  At a segment's end the warps merge in fixed order and publish an unnormalised
+// partial (o, m, l); the last segment of a row to finish combines the partials in slot order
+// (flash-decoding) into the bf16 attention output for the W_o GEMM.  The standalone kernel
+// (attn_kernel) and the persistent / pipelined kernels' phases share this body.
 constexpr int kAttnWarps = 8;
 constexpr int kAttnThreads = (kAttnWarps + 1) * 32;
 

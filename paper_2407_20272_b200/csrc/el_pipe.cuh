@@ -120,6 +120,7 @@ __global__ void __launch_bounds__(kIterThreads, 1) pipe_kernel(const __grid_cons
         attn_prefix_sum(st, sm.att);  // KV blocks per row: fixed for the iteration
         __syncwarp();
     }
+    if (cta == 0) pipe_stamp(st, 25, 1, 0);  // (dbg 128: kernel start, embed done)
     // ---- embed (model.cpp:171-183), all CTAs ----
     for (int b = cta; b < B; b += G) {
         const uint16_t* e = st.emb + (size_t)st.rows.tok[b] * dp;
@@ -131,6 +132,7 @@ __global__ void __launch_bounds__(kIterThreads, 1) pipe_kernel(const __grid_cons
         }
     }
     grid_sync(p, st, nbar, g0);
+    if (cta == 0) pipe_stamp(st, 25, 1, 1);
 
     unsigned* gbar = p.bar + kPipeGBar;
     unsigned* qkv_cnt = p.bar + kPipeQkv;  // [h * 32]
@@ -319,7 +321,7 @@ __global__ void __launch_bounds__(kIterThreads, 1) pipe_kernel(const __grid_cons
         }
     }
     if (cta == 0) pipe_stamp(st, 25, 0, 3);
-    if (cta == 0 && tid == 0) {
+    if (cta == 0 && tid == 0) {  // (kernel end: the stamp after the records below)
         *(volatile unsigned*)(p.bar + 2) = g0.y + (unsigned)G * (unsigned)nbar;  // next launch's count base
         for (int i = 0; i < kINumGemm * 64; ++i) p.tcnt[i] = 0u;
         rec_rec(st, iter % st.rec_cap)[2 * Bm] = e_out;
