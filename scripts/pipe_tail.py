@@ -27,6 +27,11 @@ for it in range(3):
     lib.el_debug_timestamps(e._h, ts.ctypes.data_as(C.c_void_p), ts.size)
     t = ts[200000:200800].reshape(25, 2, 16).astype(np.float64)
     tail = t[24, 0, :4]
+    st0, emb = t[24, 1, 0], t[24, 1, 1]
+    l1 = t[0, 0, 0]  # attention CTA 0 starts layer 1 (QKV(H0, 1) published)
+    per_layer = [(t[l, 1, 6] - t[l - 1, 1, 6]) / 1e3 for l in range(1, 24) if t[l, 1, 6] and t[l - 1, 1, 6]]
+    print(f"  start -> embed done {(emb - st0) / 1e3:.1f} us -> first attention {(l1 - emb) / 1e3:.1f} us | layers "
+          f"{len(per_layer)} x {np.mean(per_layer) if per_layer else 0:.1f} us | total {(tail[3] - st0) / 1e3:.1f} us")
     ex = r["output_layer"]
     last = t[ex - 1, 1, 5] if t[ex - 1, 1, 5] else t[ex - 1, 1, :7].max()
     print(f"exit {ex}: loop end -> tail start {(tail[0] - last) / 1e3:.1f} us | LM + fill units {(tail[1] - tail[0]) / 1e3:.1f}"
