@@ -377,6 +377,61 @@ __device__ void epi_lm_argmax(const DevState& st, const IterSmem& sm, float* tbu
     }
 }
 
+// Softmax-check LM-head tile epilogue: per column the tile's (max1, max2, sum exp rel. max1,
+// argmax) -> lm_part[tile][col], by the same reduce-scatter butterfly as epi_lm_argmax with
+// lm_part_merge at every level (one exp per merge) and one barrier -- instead of epi_lm<true>'s
+// shared-memory transpose, sequential 16-row scans and two barriers per 32 columns.
+__device__ __forceinline__ LmPart lm_leaf(float v, int i) {
+    return LmPart{v, -INFINITY, v == -INFINITY ? 0.f : 1.f, i};
+}
+__device__ __forceinline__ LmPart lm_shfl(const LmPart& x, int o) {
+    return LmPart{__shfl_xor_sync(0xffffffffu, x.m1, o), __shfl_xor_sync(0xffffffffu, x.m2, o),
+                  __shfl_xor_sync(0xffffffffu, x.s, o), __shfl_xor_sync(0xffffffffu, x.idx, o)};
+}
+__device__ void epi_lm_full(const DevState& st, const IterSmem& sm, float* tbuf, int tile, int nval) {
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int rg = warp & 3, row0 = tile * kBM;
+    const int my_row = row0 + 32 * rg + lane;
+    const bool valid = 32 * rg + lane < min(kBM, st.dm.V - row0);
+    const uint32_t trow = sm.tmem + ((uint32_t)(32 * rg) << 16);
+    LmPart* gp = reinterpret_cast<LmPart*>(tbuf);  // [4][256] per row group and column (16 KB)
+    for (int c0 = 16 * (warp >> 2); c0 < nval; c0 += 32) {
+        float v[16];
+        tmem_ld16(trow + (uint32_t)c0, v);
+        LmPart w[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {  // xor 16: keep columns [0, 8) (lanes 0-15) or [8, 16)
+            const bool hi = lane & 16;
+            const float a = valid ? (hi ? v[j + 8] : v[j]) : -INFINITY;
+            const float send = valid ? (hi ? v[j] : v[j + 8]) : -INFINITY;
+            const float b = __shfl_xor_sync(0xffffffffu, send, 16);
+            const int kb = __shfl_xor_sync(0xffffffffu, my_row, 16);
+            w[j] = lm_part_merge(lm_leaf(a, my_row), lm_leaf(b, kb));
+        }
+#pragma unroll
+        for (int o = 8, n = 4; o >= 2; o >>= 1, n >>= 1) {  // xor 8 / 4 / 2: halve the columns held
+            const bool hi = lane & o;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                if (j >= n) break;
+                const LmPart send = hi ? w[j] : w[j + n];
+                const LmPart keep = hi ? w[j + n] : w[j];
+                w[j] = lm_part_merge(keep, lm_shfl(send, o));
+            }
+        }
+        w[0] = lm_part_merge(w[0], lm_shfl(w[0], 1));  // (the lane pair: same merge, same result)
+        const int col = c0 + ((lane >> 1) & 15);
+        if (!(lane & 1) && col < nval) gp[rg * 256 + col] = w[0];
+    }
+    named_bar(2, 256);
+    for (int c = tid; c < nval; c += 256) {
+        LmPart q = gp[c];
+#pragma unroll
+        for (int g = 1; g < 4; ++g) q = lm_part_merge(q, gp[g * 256 + c]);
+        st.lm_part[(size_t)tile * st.dm.Bmax + c] = make_float4(q.m1, q.m2, q.s, __int_as_float(q.idx));
+    }
+}
+
 // one LM-head column reduced over all vocab tiles by one warp (fixed tree)
 __device__ __forceinline__ LmPart lm_col_warp(const DevState& st, int b) {
     const int lane = threadIdx.x & 31, tiles = st.dm.Vp / kBM;
@@ -1358,7 +1413,7 @@ __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(const __grid_cons
             for (int t = cta; t < p.lm_tiles; t += G) {
                 unit_ws(sm, ring, p, kseq, st.lm + (size_t)t * (dp / kBK) * (kBM * kBK), bsrc, (size_t)NR * kBK, 0,
                         dp / kBK, useq);
-                if (warp < 8) epi_lm<true>(st, sm, tbuf, t, B);
+                if (warp < 8) epi_lm_full(st, sm, tbuf, t, B);
                 ++useq;
                 tc_fence_before();
                 __syncthreads();
