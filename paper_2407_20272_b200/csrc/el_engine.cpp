@@ -251,7 +251,7 @@ struct el_engine {
         opt_mega_bm_chunk_kb = 0, opt_mega_bm_nt_min = 16,
         opt_mega_bm_m128 = 0, opt_mega_bm_down = 0, opt_mega_down_splits = 0,
         opt_mega_splits_cap = 0, opt_att_mbuf = 1, opt_mega_att_early = 1, opt_attn_seg_cost = -1,
-        opt_attn_grid = 0, opt_mega_bm_wstream = -1;
+        opt_attn_grid = 0, opt_mega_bm_wstream = -1, opt_lm_keep = 1, opt_lm_pair = 2, opt_lm_tail = 0;
     int attn_cb = 1, attn_stages = 2, attn_max_chunks = 1, attn_grid = 148;
     int NR = 16;
 
@@ -751,6 +751,7 @@ struct el_engine {
                                                      (P.bm_grp * 128)));
         P.bm_m = (n_pad <= 64 && !opt_mega_bm_m128) ? 64 : 128;
         P.att_early = opt_mega_att_early;
+        P.lm_keep = opt_lm_keep;
         P.tcnt = mtcnt.p;
         P.bm_wstream = (bm && wstream) ? 1 : 0;
         // a stage: bm_kc activation k-blocks (+ with streamed weights bm_kc weight k-blocks of nt_max rows)
@@ -776,6 +777,14 @@ struct el_engine {
         P.ring_bytes = round_up(std::max({ring_att + (P.att_mbuf_off ? mbuf : 0), P.gemm_ring + el::kIterTbufBytes,
                                           P.bm_stages * P.bm_astage + 16384, bm ? P.bm_woff + bm_w : 0}), 1024);
         P.lm_tiles = dm.Vp / 128;
+        P.lm_pair = (opt_lm_pair && !pipe_grid && n_pad <= 256 &&
+                     P.stages * (2 * 16384 + n_pad * 128) + el::kIterTbufBytes <= P.ring_bytes)
+                        ? ((opt_lm_pair == 2 && n_pad != 128) ? 1 : opt_lm_pair) : 0;  // (2 needs M = 128 rows)
+        // transposed tail LM units: 48 KB stages (batch 256: the weight-streaming stage size; batch 128:
+        // the pair stage, which must fit next to the transpose buffer)
+        P.lm_tail_tr = opt_lm_tail && ((n_pad == 256 && NR % 128 == 0) ||
+                                       (n_pad == 128 && P.stages * (2 * 16384 + n_pad * 128) + el::kIterTbufBytes <=
+                                                            P.ring_bytes)) ? 1 : 0;
         if (el::iter_max_ctas_per_sm(dm, P.ring_bytes) < 1)
             fail(EL_CUDA_ERROR, "persistent kernel does not fit on an SM (%d bytes)", el::iter_smem_bytes(P.ring_bytes));
         size_t units = 0;
@@ -2049,6 +2058,20 @@ int el_engine_set_option(el_engine* e, const char* key, int64_t v) {
         if (v < 0 || v > 64) fail(EL_INVALID_ARGUMENT, "mega_bm_chunk_kb must be in [0 (auto), 64]");
         e->opt_mega_bm_chunk_kb = (int)v;
         e->mplans.clear();
+    } else if (!std::strcmp(key, "lm_pair")) {  // softmax checks on LM pair units (0 off, 1 on)
+        if (v < 0 || v > 2) fail(EL_INVALID_ARGUMENT, "lm_pair must be 0, 1 or 2 (transposed: batch rows on TMEM lanes)");
+        e->opt_lm_pair = (int)v;
+        e->mplans.clear();
+        e->invalidate_graphs();
+    } else if (!std::strcmp(key, "lm_tail")) {  // decode tail LM head on transposed units (0 off, 1 on)
+        e->opt_lm_tail = v != 0;
+        e->mplans.clear();
+        e->invalidate_graphs();
+    } else if (!std::strcmp(key, "lm_keep")) {  // LM-head tiles evict-last: 0 off, 1 softmax checks, 2 + final head
+        if (v < 0 || v > 2) fail(EL_INVALID_ARGUMENT, "lm_keep must be 0, 1 or 2");
+        e->opt_lm_keep = (int)v;
+        e->mplans.clear();
+        e->invalidate_graphs();
     } else if (!std::strcmp(key, "mega_att_early")) {
         e->opt_mega_att_early = v != 0;
         e->mplans.clear();
@@ -2447,7 +2470,8 @@ int el_plan_info(el_engine* e, int64_t* out, int cap) {
                          M.stages, M.bm_stages, e->mega_att_stages,
                          e->mega_for(e->in_session ? e->sess_B : e->dm.Bmax) ? 1 : 0,
                          (e->mega_for(e->in_session ? e->sess_B : e->dm.Bmax) &&
-                          e->pipe_for(e->in_session ? e->sess_B : e->dm.Bmax)) ? 1 : 0};
+                          e->pipe_for(e->in_session ? e->sess_B : e->dm.Bmax)) ? 1 : 0,
+                         M.lm_pair, M.lm_keep, M.lm_tail_tr};
     const int n = (int)(sizeof v / sizeof v[0]);
     for (int i = 0; i < std::min(n, cap); ++i) out[i] = v[i];
     return n;

@@ -225,11 +225,102 @@ __device__ __forceinline__ void unit_mainloop(IterSmem& sm, uint8_t* ring, const
 // rows, default n_pad; the ring stage always has room for n_pad)
 __device__ __forceinline__ void unit_ws(IterSmem& sm, uint8_t* ring, const IterPlan& p, uint32_t& kseq,
                                         const uint16_t* a_row, const uint16_t* b_src, size_t b_kstride, int kb0,
-                                        int nkb, uint32_t useq, int dbg = 0, int n_rows = 0) {
+                                        int nkb, uint32_t useq, int dbg = 0, int n_rows = 0,
+                                        uint64_t a_policy = kL2EvictFirst) {
     const RingDesc r{sm.full, sm.empty, (uint32_t)p.stages, (uint32_t)p.stage_bytes, (uint32_t)kAStage};
     const uint32_t n = (uint32_t)(n_rows > 0 ? n_rows : p.n_pad);
     unit_mainloop(sm, ring, r, kseq, a_row, kAStage, (size_t)(kBM * kBK), b_src, n * 128u, b_kstride,
-                  kb0, nkb, n, useq, kL2EvictFirst, kL2EvictLast, dbg);
+                  kb0, nkb, n, useq, a_policy, kL2EvictLast, dbg);
+    kseq += (uint32_t)nkb;
+}
+
+// LM-head pair unit (softmax checks): vocab tiles t0 and t0 + 1 (na = 2, or 1 for an odd last
+// tile) against one activation stream -- stage = A0 16 KB | A1 16 KB | B (n_pad rows), two MMAs
+// per k-step into TMEM columns [0, n) and [256, 256 + n).  One wave of (Vp / 128 + 1) / 2 units
+// instead of two of Vp / 128 single tiles, and each CTA reads the activations once per two
+// tiles.  Same barriers / stage count as the weight-streaming ring (stride 32 KB + n_pad * 128).
+__device__ __forceinline__ void unit_lm_pair(IterSmem& sm, uint8_t* ring, const IterPlan& p, uint32_t& kseq,
+                                             const uint16_t* a0, int na, const uint16_t* b_src, size_t b_kstride,
+                                             int nkb, uint32_t useq, uint64_t a_policy, bool tr = false,
+                                             int dbg = 0) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // tr at batch 256: one vocab tile (na = 1) against both 128-row groups (two M128 x N128 MMAs)
+    const bool two_rg = tr && p.n_pad == 256;
+    const uint32_t b_bytes = (uint32_t)p.n_pad * 128u, a_bytes = (uint32_t)kAStage;
+    const uint32_t boff = (two_rg ? 1u : 2u) * a_bytes;  // B region: after the weight tile(s)
+    const uint32_t stages = (uint32_t)p.stages, stride = boff + b_bytes;
+    const size_t tile_elems = (size_t)nkb * (kBM * kBK);
+    if (warp == kProducerWarp) {
+        uint32_t s = kseq % stages, ph = (kseq / stages) & 1;
+        bool wrapped = kseq >= stages;
+        const uint32_t ring0 = smem_u32(ring), full0 = smem_u32(sm.full), empty0 = smem_u32(sm.empty);
+        const uint32_t tx = (uint32_t)na * a_bytes + b_bytes;
+#pragma unroll 1
+        for (int i = 0; i < nkb; ++i) {
+            const uint32_t fb = full0 + 8 * s, sb = ring0 + s * stride;
+            if (lane == 0) {
+                if (wrapped) mbar_wait_addr(empty0 + 8 * s, ph ^ 1);
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(fb), "r"(tx) : "memory");
+            }
+            __syncwarp();
+            // three copies from three lanes (one thread's bulk copies are processed serially)
+            if (lane == 0) bulk_load_hint(sb, a0 + (size_t)i * (kBM * kBK), a_bytes, fb, a_policy);
+            if (lane == 1 && na > 1) bulk_load_hint(sb + a_bytes, a0 + tile_elems + (size_t)i * (kBM * kBK), a_bytes, fb, a_policy);
+            if (lane == 2) bulk_load_hint(sb + boff, b_src + (size_t)i * b_kstride, b_bytes, fb, kL2EvictLast);
+            if (++s == stages) {
+                s = 0;
+                ph ^= 1;
+                wrapped = true;
+            }
+        }
+        if (lane == 0 && (dbg & 64)) sm.tdbg[3] = clock64();
+    } else if (warp == 0) {
+        // tr: D^T = X . W^T -- M = the 128 batch rows (TMEM lanes), N = the 256 vocab rows of both
+        // tiles (their k-blocks are adjacent in the stage: one 256-row K-major operand)
+        const uint32_t idesc = two_rg ? idesc_bf16_m128(128u) : tr ? idesc_bf16_m128(256u) : idesc_bf16_m128((uint32_t)p.n_pad);
+        uint32_t s = kseq % stages, ph = (kseq / stages) & 1;
+        const uint32_t full0 = smem_u32(sm.full), ring0 = smem_u32(ring);
+#pragma unroll 1
+        for (int i = 0; i < nkb; ++i) {
+            mbar_wait_addr(full0 + 8 * s, ph);
+            if (lane == 0 && (dbg & 64) && (i == 0 || i == nkb - 1)) sm.tdbg[i == 0 ? 0 : 1] = clock64();
+            tc_fence_after();
+            const uint32_t sa = ring0 + s * stride;
+            const uint64_t ad0 = sdesc_k_sw128(sa), ad1 = sdesc_k_sw128(sa + a_bytes),
+                           bd = sdesc_k_sw128(sa + boff);
+            if (two_rg) {
+                const uint64_t bd1 = sdesc_k_sw128(sa + boff + 16384u);  // batch rows 128-255
+#pragma unroll
+                for (int k = 0; k < kBK / 16; ++k) {
+                    tc_mma_bf16_warp(sm.tmem, bd + (uint64_t)(2 * k), ad0 + (uint64_t)(2 * k), idesc, (i | k) != 0);
+                    tc_mma_bf16_warp(sm.tmem + 128u, bd1 + (uint64_t)(2 * k), ad0 + (uint64_t)(2 * k), idesc,
+                                     (i | k) != 0);
+                }
+            } else if (tr) {
+#pragma unroll
+                for (int k = 0; k < kBK / 16; ++k)
+                    tc_mma_bf16_warp(sm.tmem, bd + (uint64_t)(2 * k), ad0 + (uint64_t)(2 * k), idesc, (i | k) != 0);
+            } else
+#pragma unroll
+            for (int k = 0; k < kBK / 16; ++k) {
+                tc_mma_bf16_warp(sm.tmem, ad0 + (uint64_t)(2 * k), bd + (uint64_t)(2 * k), idesc, (i | k) != 0);
+                if (na > 1)
+                    tc_mma_bf16_warp(sm.tmem + 256u, ad1 + (uint64_t)(2 * k), bd + (uint64_t)(2 * k), idesc,
+                                     (i | k) != 0);
+            }
+            tc_commit_warp(&sm.empty[s]);
+            if (++s == stages) {
+                s = 0;
+                ph ^= 1;
+            }
+        }
+        tc_commit_warp(&sm.acc);
+    }
+    __syncwarp();
+    if (warp < 8) {
+        mbar_wait(&sm.acc, useq & 1);
+        tc_fence_after();
+    }
     kseq += (uint32_t)nkb;
 }
 
@@ -388,12 +479,13 @@ __device__ __forceinline__ LmPart lm_shfl(const LmPart& x, int o) {
     return LmPart{__shfl_xor_sync(0xffffffffu, x.m1, o), __shfl_xor_sync(0xffffffffu, x.m2, o),
                   __shfl_xor_sync(0xffffffffu, x.s, o), __shfl_xor_sync(0xffffffffu, x.idx, o)};
 }
-__device__ void epi_lm_full(const DevState& st, const IterSmem& sm, float* tbuf, int tile, int nval) {
+__device__ void epi_lm_full(const DevState& st, const IterSmem& sm, float* tbuf, int tile, int nval,
+                            uint32_t tcol = 0) {
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int rg = warp & 3, row0 = tile * kBM;
     const int my_row = row0 + 32 * rg + lane;
     const bool valid = 32 * rg + lane < min(kBM, st.dm.V - row0);
-    const uint32_t trow = sm.tmem + ((uint32_t)(32 * rg) << 16);
+    const uint32_t trow = sm.tmem + tcol + ((uint32_t)(32 * rg) << 16);
     LmPart* gp = reinterpret_cast<LmPart*>(tbuf);  // [4][256] per row group and column (16 KB)
     for (int c0 = 16 * (warp >> 2); c0 < nval; c0 += 32) {
         float v[16];
@@ -429,6 +521,79 @@ __device__ void epi_lm_full(const DevState& st, const IterSmem& sm, float* tbuf,
 #pragma unroll
         for (int g = 1; g < 4; ++g) q = lm_part_merge(q, gp[g * 256 + c]);
         st.lm_part[(size_t)tile * st.dm.Bmax + c] = make_float4(q.m1, q.m2, q.s, __int_as_float(q.idx));
+    }
+}
+
+// Transposed LM pair epilogue (unit_lm_pair with tr): TMEM lane = batch row, columns [128 h,
+// 128 h + 128) = vocab rows of tile t0 + h.  Warps 4h..4h+3 reduce tile t0 + h, each thread its
+// row's 128 logits in ascending vocab order (16 per TMEM load: chunk top-2 / argmax with strict >,
+// i.e. the lowest index on ties, then one rescale and 16 exps) -- no shuffles, no shared memory.
+// kFull false: greedy argmax only, (max, -inf, 0, argmax) as epi_lm_argmax.  two_rg (batch 256):
+// one tile, column half h = batch rows [128 h, 128 h + 128).
+template <bool kFull>
+__device__ void epi_lm_tr(const DevState& st, const IterSmem& sm, int t0, int na, int nval, bool two_rg = false) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int rg = warp & 3, h = warp >> 2;
+    if (!two_rg && h >= na) return;
+    const int row = (two_rg ? 128 * h : 0) + 32 * rg + lane, tile = two_rg ? t0 : t0 + h, v0 = tile * kBM;
+    const int nv = min(kBM, st.dm.V - v0);
+    const uint32_t taddr = sm.tmem + ((uint32_t)(32 * rg) << 16) + (uint32_t)(128 * h);
+    float m1 = -INFINITY, m2 = -INFINITY, sum = 0.f;
+    int idx = 0x7fffffff;
+#pragma unroll 1
+    for (int c0 = 0; c0 < kBM; c0 += 16) {
+        float v[16];
+        tmem_ld16(taddr + (uint32_t)c0, v);
+        float cm = m1, c2 = m2;
+        int ci = idx;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            if (c0 + j >= nv) v[j] = -INFINITY;
+            if (v[j] > cm) {
+                c2 = cm;
+                cm = v[j];
+                ci = v0 + c0 + j;
+            } else {
+                c2 = fmaxf(c2, v[j]);
+            }
+        }
+        if (cm == -INFINITY) continue;
+        if (kFull) {
+            float add = 0.f;
+#pragma unroll
+            for (int j = 0; j < 16; ++j) add += __expf(v[j] - cm);
+            sum = (m1 == -INFINITY ? 0.f : sum * __expf(m1 - cm)) + add;
+        }
+        m1 = cm;
+        m2 = c2;
+        idx = ci;
+    }
+    if (row < nval)
+        st.lm_part[(size_t)tile * st.dm.Bmax + row] =
+            kFull ? make_float4(m1, m2, sum, __int_as_float(idx)) : make_float4(m1, -INFINITY, 0.f, __int_as_float(idx));
+}
+
+// Greedy LM head of the decode tail, unit `it` of tail_lm_units(p): with p.lm_tail_tr a transposed
+// unit (batch 128: a vocab tile pair; batch 256: one tile, both row groups) and the per-thread
+// argmax epilogue, else one weight-streaming tile and the shuffle-butterfly argmax.
+__device__ __forceinline__ int tail_lm_units(const IterPlan& p) {
+    return (p.lm_tail_tr && p.n_pad == 128) ? (p.lm_tiles + 1) / 2 : p.lm_tiles;
+}
+__device__ void epi_lm_argmax(const DevState& st, const IterSmem& sm, float* tbuf, int tile, int nval);
+__device__ __forceinline__ void tail_lm_unit(const DevState& st, IterSmem& sm, uint8_t* ring, const IterPlan& p,
+                                             uint32_t& kseq, float* tbuf, const uint16_t* bsrc, int NR, int it,
+                                             int B, uint32_t useq) {
+    const int dp = st.dm.dp, warp = threadIdx.x >> 5;
+    const uint64_t pol = p.lm_keep == 2 ? kL2EvictLast : kL2EvictFirst;
+    if (p.lm_tail_tr) {
+        const int per = p.n_pad == 128 ? 2 : 1, t0 = it * per, na = min(per, p.lm_tiles - t0);
+        unit_lm_pair(sm, ring, p, kseq, st.lm + (size_t)t0 * (dp / kBK) * (kBM * kBK), na, bsrc, (size_t)NR * kBK,
+                     dp / kBK, useq, pol, true);
+        if (warp < 8) epi_lm_tr<false>(st, sm, t0, na, B, p.n_pad == 256);
+    } else {
+        unit_ws(sm, ring, p, kseq, st.lm + (size_t)it * (dp / kBK) * (kBM * kBK), bsrc, (size_t)NR * kBK, 0,
+                dp / kBK, useq, 0, 0, pol);
+        if (warp < 8) epi_lm_argmax(st, sm, tbuf, it, B);
     }
 }
 
@@ -1222,6 +1387,7 @@ __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(const __grid_cons
     const int G = (int)gridDim.x, cta = (int)blockIdx.x;
     const Dims& dm = st.dm;
     const int B = st.rows.B, L = dm.L, dp = dm.dp, Bm = dm.Bmax, NR = st.NR;
+    const bool lm_pair = st.technique == kSoftmax && p.lm_pair;  // softmax checks on LM pair units
 
     if (tid == 0) {
         for (int s = 0; s < 8; ++s) {
@@ -1401,22 +1567,57 @@ __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(const __grid_cons
         // down + residual (model.cpp:261-270) + exit-check partial dots
         if (p.g[kIDown].mode) {
             gemm_phase_t<kIDown>(st, sm, ring, p, maps, kIDown, x, st.up_b, kseq2, wseq, useq, B, wpf,
-                                 layer < llast ? (int)kIQkv : -1, layer + 1);
+                                 layer < llast && !lm_pair ? (int)kIQkv : -1, layer + 1);
         } else {
-            if (tid == kProducerWarp * 32 && layer < llast) wpf = bm_prefetch(sm, ring, p, maps, kIQkv, layer + 1);
+            // (softmax checks on LM pair units: the next QKV slab is prefetched after the LM head,
+            //  whose ring runs into the slab's region)
+            if (tid == kProducerWarp * 32 && layer < llast && !lm_pair)
+                wpf = bm_prefetch(sm, ring, p, maps, kIQkv, layer + 1);
             gemm_phase_fused<kIDown>(st, sm, ring, p, kIDown, x, st.up_b, kseq, useq, B, layer - lfirst + 1);
         }
         grid_sync(p, st, nbar, g0);
         if (st.technique == kSoftmax) {
             // LM head over h_l with the fused (max1, max2, sum exp) reduction
             const uint16_t* bsrc = st.hb + (size_t)x.pout * NR * dp;
-            for (int t = cta; t < p.lm_tiles; t += G) {
-                unit_ws(sm, ring, p, kseq, st.lm + (size_t)t * (dp / kBK) * (kBM * kBK), bsrc, (size_t)NR * kBK, 0,
-                        dp / kBK, useq);
-                if (warp < 8) epi_lm_full(st, sm, tbuf, t, B);
-                ++useq;
-                tc_fence_before();
-                __syncthreads();
+            const uint64_t lpol = p.lm_keep ? kL2EvictLast : kL2EvictFirst;
+            if (lm_pair) {
+                float* tb2 = reinterpret_cast<float*>(ring + p.stages * (2 * kAStage + p.n_pad * 128));
+                // (EL_DEBUG, dbg bit 64, layer 1: per-CTA clock64 stamps of the first unit at
+                //  dbg_ts[320000 + cta * 8]: start, first / last stage full, producer done, acc, epilogue)
+                const bool lstamp = (EL_DBG(st) & 64) && layer == 1 && cta < G;
+                if (lstamp && tid == 0) st.dbg_ts[320000 + (size_t)cta * 8] = clock64();
+                for (int u = cta; 2 * u < p.lm_tiles; u += G) {
+                    const int t0 = 2 * u, na = min(2, p.lm_tiles - t0);
+                    unit_lm_pair(sm, ring, p, kseq, st.lm + (size_t)t0 * (dp / kBK) * (kBM * kBK), na, bsrc,
+                                 (size_t)NR * kBK, dp / kBK, useq, lpol, p.lm_pair == 2, lstamp && u == cta ? 64 : 0);
+                    if (lstamp && u == cta && tid == 0) st.dbg_ts[320000 + (size_t)cta * 8 + 5] = clock64();
+                    if (p.lm_pair == 2) {
+                        if (warp < 8) epi_lm_tr<true>(st, sm, t0, na, B);
+                    } else if (warp < 8) {
+                        epi_lm_full(st, sm, tb2, t0, B);
+                        if (na > 1) {
+                            named_bar(2, 256);  // (the first tile's merge reads of tb2 are done)
+                            epi_lm_full(st, sm, tb2, t0 + 1, B, 256u);
+                        }
+                    }
+                    ++useq;
+                    tc_fence_before();
+                    __syncthreads();
+                    if (lstamp && u == cta && tid == 0) {
+                        st.dbg_ts[320000 + (size_t)cta * 8 + 6] = clock64();
+                        for (int k = 0; k < 4; ++k) if (k != 2) st.dbg_ts[320000 + (size_t)cta * 8 + 1 + k] = sm.tdbg[k];
+                    }
+                }
+                if (tid == kProducerWarp * 32 && layer < llast) wpf = bm_prefetch(sm, ring, p, maps, kIQkv, layer + 1);
+            } else {
+                for (int t = cta; t < p.lm_tiles; t += G) {
+                    unit_ws(sm, ring, p, kseq, st.lm + (size_t)t * (dp / kBK) * (kBM * kBK), bsrc, (size_t)NR * kBK,
+                            0, dp / kBK, useq, 0, 0, lpol);
+                    if (warp < 8) epi_lm_full(st, sm, tbuf, t, B);
+                    ++useq;
+                    tc_fence_before();
+                    __syncthreads();
+                }
             }
             grid_sync(p, st, nbar, g0);
             // softmax_response_confidence (exit_policy.cpp:57-72), rows spread over the grid
@@ -1502,16 +1703,14 @@ __global__ void __launch_bounds__(kIterThreads, 1) iter_kernel(const __grid_cons
         for (int b = tid; b < B; b += blockDim.x) a |= sm.status[b];
         any_exit = __syncthreads_or(a) != 0;
     }
-    const int n_lm = (st.technique == kSoftmax || !any_exit) ? 0 : p.lm_tiles;  // softmax: the last check's partials
+    const int n_lm = (st.technique == kSoftmax || !any_exit) ? 0 : tail_lm_units(p);  // softmax: the last check's partials
     const int m2 = 2 * dp / kBM;
     const int fill_units = any_exit ? (L - e_out) * m2 * gf.splits : 0;
     {
         const uint16_t* bsrc = st.hb + (size_t)pe * NR * dp;
         for (int it = cta; it < n_lm + fill_units; it += G) {
             if (it < n_lm) {
-                unit_ws(sm, ring, p, kseq, st.lm + (size_t)it * (dp / kBK) * (kBM * kBK), bsrc, (size_t)NR * kBK, 0,
-                        dp / kBK, useq);
-                if (warp < 8) epi_lm_argmax(st, sm, tbuf, it, B);
+                tail_lm_unit(st, sm, ring, p, kseq, tbuf, bsrc, NR, it, B, useq);
             } else {
                 const int u = it - n_lm;
                 const int mj = u / gf.splits, s = u % gf.splits;  // mj = (jj, m) flattened

@@ -256,6 +256,17 @@ struct IterPlan {
     float* part;     // split-K partials [unit][n_pad][128] fp32
     unsigned* bar;   // grid barrier: [0] arrivals, [32] generation
     int pipe_att_ctas;  // pipelined kernel (el_pipe.cuh): CTAs [0, pipe_att_ctas) run attention
+    // LM-head weight tiles loaded evict-last (1: the softmax checks, re-read every layer and
+    // small enough to stay in L2 under the evict-first K/V and layer-weight streams; 2: also the
+    // final LM head, kept across iterations); 0: evict-first like every other weight
+    int lm_keep;
+    // softmax checks on LM pair units (two vocab tiles per unit, one wave; the ring runs past the
+    // batch-M weight slab, so the next QKV slab is prefetched after the LM head): 1 vocab rows on
+    // TMEM lanes (shuffle-butterfly epilogue), 2 transposed -- batch rows on TMEM lanes, one
+    // M128 x N256 MMA per k-step, per-thread sequential reduction (batch of 128 rows only)
+    int lm_pair;
+    // decode tail's greedy LM head on transposed units (batch 128: tile pairs, 256: both row groups)
+    int lm_tail_tr;
 };
 
 // 3-D (64 x 128 rows x tiles, no swizzle: the tiles are pre-swizzled) tensor maps over the

@@ -255,7 +255,7 @@ __global__ void __launch_bounds__(kIterThreads, 1) pipe_kernel(const __grid_cons
     // ---- tail: greedy LM head over h_e and the skipped-layer fill (kv_cache.cpp:222-234), all CTAs ----
     const int pe = e_out & 1;
     const IterGemm& gf = p.g[kIFill];
-    const int n_lm = p.lm_tiles;
+    const int n_lm = tail_lm_units(p);
     const int m2 = 2 * dp / kBM;
     const int fill_units = (L - e_out) * m2 * gf.splits;
     {
@@ -271,10 +271,8 @@ __global__ void __launch_bounds__(kIterThreads, 1) pipe_kernel(const __grid_cons
         for (int it = cta; it < n_lm + fill_units; it += G, ++un) {
             ustamp(0);
             if (it < n_lm) {
-                unit_ws(sm, ring, p, kseq, st.lm + (size_t)it * (dp / kBK) * (kBM * kBK), bsrc, (size_t)NR * kBK, 0,
-                        dp / kBK, useq);
+                tail_lm_unit(st, sm, ring, p, kseq, tbuf, bsrc, NR, it, B, useq);
                 ustamp(1);
-                if (warp < 8) epi_lm_argmax(st, sm, tbuf, it, B);
             } else {
                 const int u = it - n_lm;
                 const int mj = u / gf.splits, s = u % gf.splits;

@@ -1,4 +1,7 @@
-"""Mean exit layer of the bench workload under a grid of threshold schedules."""
+"""Mean exit layer of the bench workload under a grid of threshold schedules (B200).
+
+    python scripts/calibrate.py L d B tech '[[lam, gamma], ...]' [iterations (16)]
+"""
 import json, sys
 import numpy as np
 sys.path.insert(0, "/root/repo")
@@ -6,6 +9,7 @@ from paper_2407_20272_b200 import exitlab as X
 from oracle import bindings as OB
 L, d, B, tech = int(sys.argv[1]), int(sys.argv[2]), int(sys.argv[3]), sys.argv[4]
 grid = json.loads(sys.argv[5])
+N = int(sys.argv[6]) if len(sys.argv) > 6 else 16
 V = 32128
 wl = OB.port().gen_workload(n_requests=B, prompt_len_min=512, prompt_len_max=512, output_len_min=128,
                             output_len_max=128, seed=1, vocab_size=V)
@@ -15,8 +19,8 @@ for lam, gam in grid:
                          schedule=X.ThresholdSchedule(lam, gam, 0.0), max_batch=B, pool_blocks=B * L * 40, eos_token=-1)
     e = X.Engine(cfg)
     e.session_begin(first, 511, 640, 1)
-    e.decode_run(16)
-    r = e.records(0, 16)
+    e.decode_run(N)
+    r = e.records(0, N)
     c = r["conf"]  # [it][L][B]
     print(json.dumps(dict(lam=lam, gamma=gam, mean_e=float(r["output_layer"].mean()), e=r["output_layer"].tolist(),
                           conf_p50_by_layer=[float(np.nanmedian(c[:, l, :])) for l in range(L)][:6],
