@@ -251,7 +251,7 @@ struct el_engine {
         opt_mega_bm_chunk_kb = 0, opt_mega_bm_nt_min = 16,
         opt_mega_bm_m128 = 0, opt_mega_bm_down = 0, opt_mega_down_splits = 0,
         opt_mega_splits_cap = 0, opt_att_mbuf = 1, opt_mega_att_early = 1, opt_attn_seg_cost = -1,
-        opt_attn_grid = 0, opt_mega_bm_wstream = -1, opt_lm_keep = 1, opt_lm_pair = 2, opt_lm_tail = 0;
+        opt_attn_grid = 0, opt_mega_bm_wstream = -1, opt_lm_keep = 1, opt_lm_pair = 2, opt_lm_tail = 1;
     int attn_cb = 1, attn_stages = 2, attn_max_chunks = 1, attn_grid = 148;
     int NR = 16;
 

@@ -601,9 +601,18 @@ __device__ __forceinline__ void tail_lm_unit(const DevState& st, IterSmem& sm, u
 __device__ __forceinline__ LmPart lm_col_warp(const DevState& st, int b) {
     const int lane = threadIdx.x & 31, tiles = st.dm.Vp / kBM;
     LmPart acc{-INFINITY, -INFINITY, 0.f, 0x7fffffff};
-    for (int t = lane; t < tiles; t += 32) {
-        const float4 q = __ldcg(&st.lm_part[(size_t)t * st.dm.Bmax + b]);
-        acc = lm_part_merge(acc, LmPart{q.x, q.y, q.z, __float_as_int(q.w)});
+    // the lane's partials loaded 8 at a time before merging them in the same order (8 dependent
+    // L2 round trips at V = 32128 were the critical path of the softmax confidence phase)
+    constexpr int kU = 8;
+    for (int t0 = lane; t0 < tiles; t0 += 32 * kU) {
+        float4 q[kU];
+#pragma unroll
+        for (int j = 0; j < kU; ++j)
+            q[j] = t0 + 32 * j < tiles ? __ldcg(&st.lm_part[(size_t)(t0 + 32 * j) * st.dm.Bmax + b])
+                                       : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int j = 0; j < kU; ++j)
+            if (t0 + 32 * j < tiles) acc = lm_part_merge(acc, LmPart{q[j].x, q[j].y, q[j].z, __float_as_int(q[j].w)});
     }
 #pragma unroll
     for (int off = 1; off < 32; off <<= 1) {
