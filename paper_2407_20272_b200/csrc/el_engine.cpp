@@ -185,8 +185,13 @@ struct el_engine {
     // pipelined iteration kernel (el_pipe.cuh) for batch 129..256: 0 off, 1 on, 2 auto (on outside
     // softmax exit / T5 mode); attention CTAs of its grid (the rest run the projection GEMMs)
     int use_pipe = 2, pipe_att = 100;  // attention CTAs of the pipelined kernel (the rest run GEMMs)
+    // batch 65..128 on the pipelined kernel with halves of 64 rows (64-row batch-M groups, UMMA
+    // M = 64; needs the 128-row activation layout)
+    int pipe128 = 1;
+    int pipe_att64 = 84;  // attention CTAs of the pipelined kernel at batch <= 128 (64-row halves)
     bool pipe_for(int B) const {
-        if (use_pipe == 0 || B <= 128 || B > 256 || cfg.encoder_len > 0 || cfg.technique == EL_TECH_SOFTMAX) return false;
+        if (use_pipe == 0 || B > 256 || cfg.encoder_len > 0 || cfg.technique == EL_TECH_SOFTMAX) return false;
+        if (B <= 128) return pipe128 && B > 64 && NR == 128;
         return true;
     }
 
@@ -746,10 +751,12 @@ struct el_engine {
         // so a prefetch into it never collides with the phase in flight.
         const int ring_att = mega_att_stages * att_stage;
         P.bm_rows = NR;
-        P.bm_grp = n_pad > 128 ? 128 : NR;  // batch > 128: units cover one 128-row group
+        // batch > 128: units cover one 128-row group; the pipelined kernel at batch <= 128: one 64-row half
+        const bool half64 = pipe_grid && n_pad <= 128;
+        P.bm_grp = n_pad > 128 ? 128 : half64 ? 64 : NR;
         P.bm_kc = std::max(1, std::min(dp / 64, (opt_mega_bm_chunk_kb ? opt_mega_bm_chunk_kb * 1024 : 32768) /
                                                      (P.bm_grp * 128)));
-        P.bm_m = (n_pad <= 64 && !opt_mega_bm_m128) ? 64 : 128;
+        P.bm_m = ((n_pad <= 64 || half64) && !opt_mega_bm_m128) ? 64 : 128;
         P.att_early = opt_mega_att_early;
         P.lm_keep = opt_lm_keep;
         P.tcnt = mtcnt.p;
@@ -809,7 +816,7 @@ struct el_engine {
         return mplans.emplace(key, P).first->second;
     }
     void launch_pipe(int B) {
-        const int ga = std::min(std::max(pipe_att, 16), sms - 16);
+        const int ga = std::min(std::max(B <= 128 ? pipe_att64 : pipe_att, 16), sms - 16);
         el::IterPlan& P = mplan_for(B, 0, sms - ga);
         if (!P.g[el::kIQkv].mode || !P.g[el::kIWo].mode || !P.g[el::kIUp].mode)
             fail(EL_RUNTIME_ERROR, "pipelined kernel: needs batch-M QKV / W_o / up phases");
@@ -2042,9 +2049,13 @@ int el_engine_set_option(el_engine* e, const char* key, int64_t v) {
     else if (!std::strcmp(key, "pipe")) {
         if (v < 0 || v > 2) fail(EL_INVALID_ARGUMENT, "pipe must be 0 (off), 1 (on) or 2 (auto)");
         e->use_pipe = (int)v;
-    } else if (!std::strcmp(key, "pipe_att_ctas")) {
-        if (v < 16 || v > 132) fail(EL_INVALID_ARGUMENT, "pipe_att_ctas must be in [16, 132]");
-        e->pipe_att = (int)v;
+    } else if (!std::strcmp(key, "pipe128")) {  // batch 65..128 on the pipelined kernel (halves of 64 rows)
+        e->pipe128 = v != 0;
+        e->mplans.clear();
+        e->invalidate_graphs();
+    } else if (!std::strcmp(key, "pipe_att_ctas") || !std::strcmp(key, "pipe_att_ctas64")) {
+        if (v < 16 || v > 132) fail(EL_INVALID_ARGUMENT, "%s must be in [16, 132]", key);
+        (key[13] == '6' ? e->pipe_att64 : e->pipe_att) = (int)v;
     }
     else if (!std::strcmp(key, "mega")) {
         if (v < 0 || v > 2) fail(EL_INVALID_ARGUMENT, "mega must be 0 (off), 1 (on) or 2 (auto)");
