@@ -189,10 +189,12 @@ struct el_engine {
     // M = 64; needs the 128-row activation layout)
     int pipe128 = 1;
     int pipe_att64 = 84;  // attention CTAs of the pipelined kernel at batch <= 128 (64-row halves)
+    int pipe_softmax = 1;  // softmax exit on the pipelined kernel (batch 65..128)
     bool pipe_for(int B) const {
-        if (use_pipe == 0 || B > 256 || cfg.encoder_len > 0 || cfg.technique == EL_TECH_SOFTMAX) return false;
-        if (B <= 128) return pipe128 && B > 64 && NR == 128;
-        return true;
+        if (use_pipe == 0 || B > 256 || cfg.encoder_len > 0) return false;
+        // (softmax: the LM-head check on the GEMM CTAs, pair units at batch <= 128 only)
+        if (B <= 128) return pipe128 && B > 64 && NR == 128 && (cfg.technique != EL_TECH_SOFTMAX || pipe_softmax);
+        return cfg.technique != EL_TECH_SOFTMAX;
     }
 
     // weights
@@ -787,6 +789,11 @@ struct el_engine {
         P.lm_pair = (opt_lm_pair && !pipe_grid && n_pad <= 256 &&
                      P.stages * (2 * 16384 + n_pad * 128) + el::kIterTbufBytes <= P.ring_bytes)
                         ? ((opt_lm_pair == 2 && n_pad != 128) ? 1 : opt_lm_pair) : 0;  // (2 needs M = 128 rows)
+        P.lm_stages = 0;
+        if (pipe_grid && n_pad <= 128) {  // pipelined kernel: the pair units' own ring (full3 / empty3)
+            P.lm_stages = std::min(4, (P.ring_bytes - el::kIterTbufBytes) / (2 * 16384 + n_pad * 128));
+            P.lm_pair = P.lm_stages >= 2 ? ((opt_lm_pair == 2 && n_pad == 128) ? 2 : 1) : 0;
+        }
         // transposed tail LM units: 48 KB stages (batch 256: the weight-streaming stage size; batch 128:
         // the pair stage, which must fit next to the transpose buffer)
         P.lm_tail_tr = opt_lm_tail && ((n_pad == 256 && NR % 128 == 0) ||
@@ -820,6 +827,8 @@ struct el_engine {
         el::IterPlan& P = mplan_for(B, 0, sms - ga);
         if (!P.g[el::kIQkv].mode || !P.g[el::kIWo].mode || !P.g[el::kIUp].mode)
             fail(EL_RUNTIME_ERROR, "pipelined kernel: needs batch-M QKV / W_o / up phases");
+        if (cfg.technique == EL_TECH_SOFTMAX && !P.lm_pair)
+            fail(EL_RUNTIME_ERROR, "pipelined kernel: the softmax check's LM pair ring does not fit");
         el::DevState s = state(false, B);
         // attention CTAs have the whole ring region to themselves: as many stages as fit
         s.attn_stages = std::min(8, P.ring_bytes / el::attn_stage_bytes(dm));
@@ -2049,6 +2058,10 @@ int el_engine_set_option(el_engine* e, const char* key, int64_t v) {
     else if (!std::strcmp(key, "pipe")) {
         if (v < 0 || v > 2) fail(EL_INVALID_ARGUMENT, "pipe must be 0 (off), 1 (on) or 2 (auto)");
         e->use_pipe = (int)v;
+    } else if (!std::strcmp(key, "pipe_softmax")) {  // softmax exit on the pipelined kernel (batch 65..128)
+        e->pipe_softmax = v != 0;
+        e->mplans.clear();
+        e->invalidate_graphs();
     } else if (!std::strcmp(key, "pipe128")) {  // batch 65..128 on the pipelined kernel (halves of 64 rows)
         e->pipe128 = v != 0;
         e->mplans.clear();
@@ -2482,7 +2495,7 @@ int el_plan_info(el_engine* e, int64_t* out, int cap) {
                          e->mega_for(e->in_session ? e->sess_B : e->dm.Bmax) ? 1 : 0,
                          (e->mega_for(e->in_session ? e->sess_B : e->dm.Bmax) &&
                           e->pipe_for(e->in_session ? e->sess_B : e->dm.Bmax)) ? 1 : 0,
-                         M.lm_pair, M.lm_keep, M.lm_tail_tr};
+                         M.lm_pair, M.lm_keep, M.lm_tail_tr, M.lm_stages};
     const int n = (int)(sizeof v / sizeof v[0]);
     for (int i = 0; i < std::min(n, cap); ++i) out[i] = v[i];
     return n;

@@ -31,6 +31,7 @@ struct IterSmem {
     AttnSmem att;  // attention ring barriers/descriptors (persist across layers)
     uint64_t full[8], empty[8], acc;
     uint64_t full2[16], empty2[16];  // batch-M GEMM activation ring
+    uint64_t full3[4], empty3[4];    // pipelined kernel: LM pair units of the softmax check (lm_stages)
     uint64_t wfull;                  // batch-M unit weights (one tensor copy per unit)
     unsigned long long tdbg[5];
     uint32_t tmem;
@@ -242,18 +243,22 @@ __device__ __forceinline__ void unit_ws(IterSmem& sm, uint8_t* ring, const IterP
 __device__ __forceinline__ void unit_lm_pair(IterSmem& sm, uint8_t* ring, const IterPlan& p, uint32_t& kseq,
                                              const uint16_t* a0, int na, const uint16_t* b_src, size_t b_kstride,
                                              int nkb, uint32_t useq, uint64_t a_policy, bool tr = false,
-                                             int dbg = 0) {
+                                             int dbg = 0, uint64_t* rfull = nullptr, uint64_t* rempty = nullptr,
+                                             int rstages = 0) {
+    // ring: the weight-streaming ring's barriers and depth, or (rfull) a separate set
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     // tr at batch 256: one vocab tile (na = 1) against both 128-row groups (two M128 x N128 MMAs)
     const bool two_rg = tr && p.n_pad == 256;
     const uint32_t b_bytes = (uint32_t)p.n_pad * 128u, a_bytes = (uint32_t)kAStage;
     const uint32_t boff = (two_rg ? 1u : 2u) * a_bytes;  // B region: after the weight tile(s)
-    const uint32_t stages = (uint32_t)p.stages, stride = boff + b_bytes;
+    const uint32_t stages = (uint32_t)(rfull ? rstages : p.stages), stride = boff + b_bytes;
+    uint64_t* const fullb = rfull ? rfull : sm.full;
+    uint64_t* const emptyb = rfull ? rempty : sm.empty;
     const size_t tile_elems = (size_t)nkb * (kBM * kBK);
     if (warp == kProducerWarp) {
         uint32_t s = kseq % stages, ph = (kseq / stages) & 1;
         bool wrapped = kseq >= stages;
-        const uint32_t ring0 = smem_u32(ring), full0 = smem_u32(sm.full), empty0 = smem_u32(sm.empty);
+        const uint32_t ring0 = smem_u32(ring), full0 = smem_u32(fullb), empty0 = smem_u32(emptyb);
         const uint32_t tx = (uint32_t)na * a_bytes + b_bytes;
 #pragma unroll 1
         for (int i = 0; i < nkb; ++i) {
@@ -279,7 +284,7 @@ __device__ __forceinline__ void unit_lm_pair(IterSmem& sm, uint8_t* ring, const 
         // tiles (their k-blocks are adjacent in the stage: one 256-row K-major operand)
         const uint32_t idesc = two_rg ? idesc_bf16_m128(128u) : tr ? idesc_bf16_m128(256u) : idesc_bf16_m128((uint32_t)p.n_pad);
         uint32_t s = kseq % stages, ph = (kseq / stages) & 1;
-        const uint32_t full0 = smem_u32(sm.full), ring0 = smem_u32(ring);
+        const uint32_t full0 = smem_u32(fullb), ring0 = smem_u32(ring);
 #pragma unroll 1
         for (int i = 0; i < nkb; ++i) {
             mbar_wait_addr(full0 + 8 * s, ph);
@@ -308,7 +313,7 @@ __device__ __forceinline__ void unit_lm_pair(IterSmem& sm, uint8_t* ring, const 
                     tc_mma_bf16_warp(sm.tmem + 256u, ad1 + (uint64_t)(2 * k), bd + (uint64_t)(2 * k), idesc,
                                      (i | k) != 0);
             }
-            tc_commit_warp(&sm.empty[s]);
+            tc_commit_warp(&emptyb[s]);
             if (++s == stages) {
                 s = 0;
                 ph ^= 1;

@@ -267,6 +267,7 @@ struct IterPlan {
     int lm_pair;
     // decode tail's greedy LM head on transposed units (batch 128: tile pairs, 256: both row groups)
     int lm_tail_tr;
+    int lm_stages;  // pipelined kernel: depth of the LM pair units' own ring (full3 / empty3)
 };
 
 // 3-D (64 x 128 rows x tiles, no swizzle: the tiles are pre-swizzled) tensor maps over the

@@ -16,8 +16,10 @@
 // skipped-layer fill then overwrites the K/V they wrote at layer l+1).  Results are those of
 // iter_kernel: the same phases, epilogues and reduction orders per row.
 //
-// Not in this kernel (iter_kernel serves them): softmax exit (its LM-head check needs every
-// CTA), T5 cross-attention, batched prefill, layer-level turns.
+// Softmax exit (batch <= 128): the LM-head check of layer l runs on the GEMM CTAs after down(H1, l)
+// (transposed pair units on their own ring, then the per-row merge), under attn(H0, l + 1).
+// Not in this kernel (iter_kernel serves them): softmax exit at batch > 128, T5 cross-attention,
+// batched prefill, layer-level turns.
 
 // control words (unsigned, 128-byte apart) past the grid barrier's: GEMM-group barrier, QKV
 // published per half, attention published per half, stop layer
@@ -92,6 +94,10 @@ __global__ void __launch_bounds__(kIterThreads, 1) pipe_kernel(const __grid_cons
             mbar_init(&sm.full2[s], 1);
             mbar_init(&sm.empty2[s], 1);
         }
+        for (int s = 0; s < 4; ++s) {
+            mbar_init(&sm.full3[s], 1);
+            mbar_init(&sm.empty3[s], 1);
+        }
         mbar_init(&sm.wfull, 1);
         sm.att.npend = 0;
         sm.att.ids_layer[0] = sm.att.ids_layer[1] = -1;
@@ -113,7 +119,7 @@ __global__ void __launch_bounds__(kIterThreads, 1) pipe_kernel(const __grid_cons
     __syncthreads();
     tc_fence_after();
 
-    uint32_t kseq = 0, kseq2 = 0, wseq = 0, useq = 0;
+    uint32_t kseq = 0, kseq2 = 0, kseq3 = 0, wseq = 0, useq = 0;
     bool wpf = false;
     int aseq = 0, nbar = 0;
     if (warp == kProducerWarp) {
@@ -225,6 +231,45 @@ __global__ void __launch_bounds__(kIterThreads, 1) pipe_kernel(const __grid_cons
                 group_sync(gbar, (unsigned)GG, ++gk);
                 if (gi == 0) pipe_stamp(st, layer, h, 5);
                 if (h == 1) {
+                    if (st.technique == kSoftmax) {
+                        // softmax check (exit_policy.cpp:57-72) on the GEMM CTAs while the attention
+                        // CTAs run the next layer's first half speculatively: the LM head over h_l of
+                        // both halves on pair units (their own ring), then each row's merge
+                        const uint16_t* bsrc = st.hb + (size_t)x.pout * NR * dp;
+                        const uint64_t lpol = p.lm_keep ? kL2EvictLast : kL2EvictFirst;
+                        const uint32_t pstride = 2u * kAStage + (uint32_t)p.n_pad * 128u;
+                        float* tb2 = reinterpret_cast<float*>(ring + (size_t)p.lm_stages * pstride);
+                        for (int u = gi; 2 * u < p.lm_tiles; u += GG) {
+                            const int t0 = 2 * u, na = min(2, p.lm_tiles - t0);
+                            unit_lm_pair(sm, ring, p, kseq3, st.lm + (size_t)t0 * (dp / kBK) * (kBM * kBK), na, bsrc,
+                                         (size_t)NR * kBK, dp / kBK, useq, lpol, p.lm_pair == 2, 0, sm.full3,
+                                         sm.empty3, p.lm_stages);
+                            if (p.lm_pair == 2) {
+                                if (warp < 8) epi_lm_tr<true>(st, sm, t0, na, B);
+                            } else if (warp < 8) {
+                                epi_lm_full(st, sm, tb2, t0, B);
+                                if (na > 1) {
+                                    named_bar(2, 256);
+                                    epi_lm_full(st, sm, tb2, t0 + 1, B, 256u);
+                                }
+                            }
+                            ++useq;
+                            tc_fence_before();
+                            __syncthreads();
+                        }
+                        group_sync(gbar, (unsigned)GG, ++gk);
+                        if (warp < 8)
+                            for (int b = gi + GG * warp; b < B; b += GG * 8) {
+                                const LmPart r = lm_col_warp(st, b);
+                                if ((tid & 31) == 0) {
+                                    const float gap = (r.m2 == -INFINITY) ? 1.f : -expm1f(r.m2 - r.m1);
+                                    const float conf = gap / r.s;
+                                    st.conf[(size_t)(layer - 1) * Bm + b] = conf;
+                                    st.accept[b] = (double)conf > st.lambdas[layer - 1];
+                                }
+                            }
+                        group_sync(gbar, (unsigned)GG, ++gk);
+                    }
                     // exit decision of this layer for the whole batch (engine.cpp:225-258)
                     if (exit_decide(st, sm, layer, B, dp / kBM, gemm0)) {
                         e_out = layer;
@@ -255,7 +300,7 @@ __global__ void __launch_bounds__(kIterThreads, 1) pipe_kernel(const __grid_cons
     // ---- tail: greedy LM head over h_e and the skipped-layer fill (kv_cache.cpp:222-234), all CTAs ----
     const int pe = e_out & 1;
     const IterGemm& gf = p.g[kIFill];
-    const int n_lm = tail_lm_units(p);
+    const int n_lm = st.technique == kSoftmax ? 0 : tail_lm_units(p);  // softmax: the last check's partials
     const int m2 = 2 * dp / kBM;
     const int fill_units = (L - e_out) * m2 * gf.splits;
     {

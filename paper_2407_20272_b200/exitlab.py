@@ -758,7 +758,7 @@ class Engine:
                  "down_splits", "fill_splits", "qkv_stages", "lm_tiles", "dp", "fp", "Vp", "bpl_max",
                  "mega_qkv_mode", "mega_wo_mode", "mega_up_mode", "mega_qkv_splits", "mega_wo_splits",
                  "mega_up_splits", "mega_down_splits", "mega_fill_splits", "mega_qkv_nt", "mega_wo_nt", "mega_up_nt",
-                 "mega_stages", "mega_stages2", "mega_att_stages", "mega", "pipe", "lm_pair", "lm_keep", "lm_tail_tr"]
+                 "mega_stages", "mega_stages2", "mega_att_stages", "mega", "pipe", "lm_pair", "lm_keep", "lm_tail_tr", "lm_stages"]
         return dict(zip(names, out[:n].tolist()))
 
     # ---- layer-level scheduling over the session's batch ----
