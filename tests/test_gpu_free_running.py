@@ -157,10 +157,12 @@ def test_free_running_parity(port, name, mega):
                 vp = orc["model"].tensor("w_v", layer) @ h_last[b]
                 fill_err = max(fill_err, float(np.abs(kg - kp).max() / np.abs(kp).max()),
                                float(np.abs(vg - vp).max() / np.abs(vp).max()))
+    # the single-launch strategy runs the pipelined kernel at batch 65-256 (el_pipe.cuh)
+    kernel = "per-phase" if not mega else ("pipelined" if e.plan_info().get("pipe") else "persistent")
     e.close()
     eo_all = np.array([x["e_oracle"] for x in rows])
     eg_all = np.array([x["e_b200"] for x in rows])
-    summary = dict(config=name, workload=c["name"], strategy="persistent" if mega else "per-phase", technique=tech,
+    summary = dict(config=name, workload=c["name"], strategy="persistent" if mega else "per-phase", kernel=kernel, technique=tech,
                    schedule=[c["lam"], c["gamma"]], batch=B, iterations=ITERS,
                    exit_layer_agreement=float(np.mean(eo_all == eg_all)),
                    accept_layer_agreement=float(np.mean([x["accept_agree"] for x in rows])),
