@@ -523,3 +523,31 @@ def test_pipelined_kernel_matches_persistent_kernel(B):
     assert [x["output_layer"] for x in ra] == [x["output_layer"] for x in rc]
     assert np.mean([np.mean(x["tokens"] == y["tokens"]) for x, y in zip(ra, rc)]) >= 0.97
     assert relerr(qa[0], qc[0]) <= 1e-2  # layer-1 K of the last position: same inputs, same GEMM
+
+
+@pytest.mark.parametrize("B,tech,lam", [(128, "classifier", 0.6), (100, "classifier", 0.6), (100, "softmax", 2.0),
+                                        (128, "softmax", 2.0)])
+def test_pipelined_kernel_64_row_halves_match_persistent_kernel(B, tech, lam):
+    """The pipelined kernel at batch 65-128 (halves of 64 rows, UMMA M = 64 batch-M groups; B = 100
+    has a ragged second half of 36 rows; softmax: the LM-head check on the GEMM CTAs, lam 2.0 keeps
+    every check to full depth) against the persistent kernel on the same session (max_batch 128):
+    same exit decisions, tokens up to summation order, run-to-run bitwise deterministic."""
+    L, d, V = 6, 1024, 2048
+    outs = []
+    for pipe in (1, 1, 0):
+        g, _ = cfg_pair(L, d, V, 8, tech, lam=lam, gamma=0.97, B=128)
+        e = X.Engine(g, mega=True)
+        e.set_option("pipe", pipe)
+        e.session_begin(np.arange(B) * 7 % V + 1, 60, 100, 5)
+        assert e.plan_info()["pipe"] == (1 if pipe else 0)
+        rs = [e.decode_iteration() for _ in range(4)]
+        outs.append((rs, e.hidden(rs[-1]["output_layer"] & 1), e.kv(B - 1, L, 63), e.kv(3, 1, 63)))
+        e.close()
+    (ra, ha, ka, qa), (rb, hb, kb, qb), (rc, hc, kc, qc) = outs
+    for x, y in zip(ra, rb):
+        assert x["output_layer"] == y["output_layer"] and np.array_equal(x["tokens"], y["tokens"])
+    assert np.array_equal(ha, hb) and np.array_equal(ka[0], kb[0]) and np.array_equal(qa[1], qb[1])
+    assert [x["output_layer"] for x in ra] == [x["output_layer"] for x in rc]
+    assert np.mean([np.mean(x["tokens"] == y["tokens"]) for x, y in zip(ra, rc)]) >= 0.97
+    assert relerr(ha[:B], hc[:B]) <= 1e-2
+    assert relerr(qa[0], qc[0]) <= 1e-2 and relerr(ka[0], kc[0]) <= 1e-2
