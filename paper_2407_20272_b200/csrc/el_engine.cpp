@@ -190,9 +190,13 @@ struct el_engine {
     int pipe128 = 1;
     int pipe_att64 = 84;  // attention CTAs of the pipelined kernel at batch <= 128 (64-row halves)
     int pipe_softmax = 1;  // softmax exit on the pipelined kernel (batch 65..128)
+    // batch 33..64 on the pipelined kernel with halves of 32 rows (UMMA M = 64 over a 32-row group:
+    // the upper 32 accumulator rows are discarded; needs the 64-row activation layout)
+    int pipe64 = 0, pipe_att32 = 84;
     bool pipe_for(int B) const {
         if (use_pipe == 0 || B > 256 || cfg.encoder_len > 0) return false;
         // (softmax: the LM-head check on the GEMM CTAs, pair units at batch <= 128 only)
+        if (B <= 64) return pipe64 && B > 32 && NR == 64 && cfg.technique != EL_TECH_SOFTMAX;
         if (B <= 128) return pipe128 && B > 64 && NR == 128 && (cfg.technique != EL_TECH_SOFTMAX || pipe_softmax);
         return cfg.technique != EL_TECH_SOFTMAX;
     }
@@ -755,7 +759,7 @@ struct el_engine {
         P.bm_rows = NR;
         // batch > 128: units cover one 128-row group; the pipelined kernel at batch <= 128: one 64-row half
         const bool half64 = pipe_grid && n_pad <= 128;
-        P.bm_grp = n_pad > 128 ? 128 : half64 ? 64 : NR;
+        P.bm_grp = n_pad > 128 ? 128 : half64 ? (n_pad > 64 ? 64 : 32) : NR;
         P.bm_kc = std::max(1, std::min(dp / 64, (opt_mega_bm_chunk_kb ? opt_mega_bm_chunk_kb * 1024 : 32768) /
                                                      (P.bm_grp * 128)));
         P.bm_m = ((n_pad <= 64 || half64) && !opt_mega_bm_m128) ? 64 : 128;
@@ -823,7 +827,7 @@ struct el_engine {
         return mplans.emplace(key, P).first->second;
     }
     void launch_pipe(int B) {
-        const int ga = std::min(std::max(B <= 128 ? pipe_att64 : pipe_att, 16), sms - 16);
+        const int ga = std::min(std::max(B <= 64 ? pipe_att32 : B <= 128 ? pipe_att64 : pipe_att, 16), sms - 16);
         el::IterPlan& P = mplan_for(B, 0, sms - ga);
         if (!P.g[el::kIQkv].mode || !P.g[el::kIWo].mode || !P.g[el::kIUp].mode)
             fail(EL_RUNTIME_ERROR, "pipelined kernel: needs batch-M QKV / W_o / up phases");
@@ -2062,6 +2066,13 @@ int el_engine_set_option(el_engine* e, const char* key, int64_t v) {
         e->pipe_softmax = v != 0;
         e->mplans.clear();
         e->invalidate_graphs();
+    } else if (!std::strcmp(key, "pipe64")) {  // batch 33..64 on the pipelined kernel (halves of 32 rows)
+        e->pipe64 = v != 0;
+        e->mplans.clear();
+        e->invalidate_graphs();
+    } else if (!std::strcmp(key, "pipe_att_ctas32")) {
+        if (v < 16 || v > 132) fail(EL_INVALID_ARGUMENT, "%s must be in [16, 132]", key);
+        e->pipe_att32 = (int)v;
     } else if (!std::strcmp(key, "pipe128")) {  // batch 65..128 on the pipelined kernel (halves of 64 rows)
         e->pipe128 = v != 0;
         e->mplans.clear();

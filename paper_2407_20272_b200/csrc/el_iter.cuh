@@ -1256,8 +1256,9 @@ __device__ __forceinline__ void gemm_phase_t(const DevState& st, IterSmem& sm, u
         constexpr bool kRes = kPre && (K == kIWo || K == kIWoc);
         float4 res[2][4];
         const bool m64p = p.bm_m == 64;
-        const int bp = rg * p.bm_grp + (m64p ? 16 * (warp & 3) + lane : 32 * (warp & 3) + lane);
-        const bool vp = warp < 8 && bp < B && (!m64p || lane < 16);
+        const int lp = m64p ? 16 * (warp & 3) + lane : 32 * (warp & 3) + lane;  // row inside the group
+        const int bp = rg * p.bm_grp + lp;
+        const bool vp = warp < 8 && bp < B && (!m64p || lane < 16) && lp < p.bm_grp;
         if constexpr (kRes) {
             if (vp) {
                 const float* base = (K == kIWo ? st.h32 + (size_t)x.pin * st.dm.Bmax * st.dm.dp : st.mid32) +
@@ -1283,8 +1284,10 @@ __device__ __forceinline__ void gemm_phase_t(const DevState& st, IterSmem& sm, u
         if (warp < 8) {
             // M = 128: batch row b in TMEM lane b.  M = 64: rows 16q..16q+15 in lanes 32q..32q+15.
             const bool m64 = p.bm_m == 64;
-            const int b = rg * p.bm_grp + (m64 ? 16 * (warp & 3) + lane : 32 * (warp & 3) + lane);
-            const bool valid = b < B && (!m64 || lane < 16);
+            const int lr = m64 ? 16 * (warp & 3) + lane : 32 * (warp & 3) + lane;  // row inside the group
+            const int b = rg * p.bm_grp + lr;
+            // (32-row groups of the pipelined kernel: UMMA M = 64, accumulator rows 32-63 discarded)
+            const bool valid = b < B && (!m64 || lane < 16) && lr < p.bm_grp;
             const uint32_t trow = sm.tmem + ((uint32_t)(32 * (warp & 3)) << 16);
             if constexpr (kRes) {
 #pragma unroll

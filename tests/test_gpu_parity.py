@@ -551,3 +551,30 @@ def test_pipelined_kernel_64_row_halves_match_persistent_kernel(B, tech, lam):
     assert np.mean([np.mean(x["tokens"] == y["tokens"]) for x, y in zip(ra, rc)]) >= 0.97
     assert relerr(ha[:B], hc[:B]) <= 1e-2
     assert relerr(qa[0], qc[0]) <= 1e-2 and relerr(ka[0], kc[0]) <= 1e-2
+
+
+@pytest.mark.parametrize("B,tech,lam", [(64, "state", 0.9), (48, "classifier", 0.6)])
+def test_pipelined_kernel_32_row_halves_match_persistent_kernel(B, tech, lam):
+    """The pipelined kernel at batch 33-64 (option pipe64: halves of 32 rows, UMMA M = 64 over a
+    32-row group with the upper accumulator rows discarded; B = 48 has a ragged second half)
+    against the persistent kernel on the same session (max_batch 64)."""
+    L, d, V = 6, 768, 2048
+    outs = []
+    for pipe in (1, 1, 0):
+        g, _ = cfg_pair(L, d, V, 8, tech, lam=lam, gamma=0.97, B=64)
+        e = X.Engine(g, mega=True)
+        e.set_option("pipe64", 1)
+        e.set_option("pipe", pipe)
+        e.session_begin(np.arange(B) * 7 % V + 1, 60, 100, 5)
+        assert e.plan_info()["pipe"] == (1 if pipe else 0)
+        rs = [e.decode_iteration() for _ in range(4)]
+        outs.append((rs, e.hidden(rs[-1]["output_layer"] & 1), e.kv(B - 1, L, 63), e.kv(3, 1, 63)))
+        e.close()
+    (ra, ha, ka, qa), (rb, hb, kb, qb), (rc, hc, kc, qc) = outs
+    for x, y in zip(ra, rb):
+        assert x["output_layer"] == y["output_layer"] and np.array_equal(x["tokens"], y["tokens"])
+    assert np.array_equal(ha, hb) and np.array_equal(ka[0], kb[0]) and np.array_equal(qa[1], qb[1])
+    assert [x["output_layer"] for x in ra] == [x["output_layer"] for x in rc]
+    assert np.mean([np.mean(x["tokens"] == y["tokens"]) for x, y in zip(ra, rc)]) >= 0.97
+    assert relerr(ha[:B], hc[:B]) <= 1e-2
+    assert relerr(qa[0], qc[0]) <= 1e-2 and relerr(ka[0], kc[0]) <= 1e-2
