@@ -189,6 +189,7 @@ struct el_engine {
     // M = 64; needs the 128-row activation layout)
     int pipe128 = 1;
     int pipe_att64 = 84;  // attention CTAs of the pipelined kernel at batch <= 128 (64-row halves)
+    int pipe_att64_sm = 80;  // the same with softmax exit (the LM-head check runs on the GEMM CTAs)
     int pipe_softmax = 1;  // softmax exit on the pipelined kernel (batch 65..128)
     // batch 33..64 on the pipelined kernel with halves of 32 rows (UMMA M = 64 over a 32-row group:
     // the upper 32 accumulator rows are discarded; needs the 64-row activation layout)
@@ -827,7 +828,8 @@ struct el_engine {
         return mplans.emplace(key, P).first->second;
     }
     void launch_pipe(int B) {
-        const int ga = std::min(std::max(B <= 64 ? pipe_att32 : B <= 128 ? pipe_att64 : pipe_att, 16), sms - 16);
+        const int ga64 = cfg.technique == EL_TECH_SOFTMAX ? pipe_att64_sm : pipe_att64;
+        const int ga = std::min(std::max(B <= 64 ? pipe_att32 : B <= 128 ? ga64 : pipe_att, 16), sms - 16);
         el::IterPlan& P = mplan_for(B, 0, sms - ga);
         if (!P.g[el::kIQkv].mode || !P.g[el::kIWo].mode || !P.g[el::kIUp].mode)
             fail(EL_RUNTIME_ERROR, "pipelined kernel: needs batch-M QKV / W_o / up phases");
@@ -2070,6 +2072,9 @@ int el_engine_set_option(el_engine* e, const char* key, int64_t v) {
         e->pipe64 = v != 0;
         e->mplans.clear();
         e->invalidate_graphs();
+    } else if (!std::strcmp(key, "pipe_att_ctas64_softmax")) {
+        if (v < 16 || v > 132) fail(EL_INVALID_ARGUMENT, "%s must be in [16, 132]", key);
+        e->pipe_att64_sm = (int)v;
     } else if (!std::strcmp(key, "pipe_att_ctas32")) {
         if (v < 16 || v > 132) fail(EL_INVALID_ARGUMENT, "%s must be in [16, 132]", key);
         e->pipe_att32 = (int)v;
