@@ -578,3 +578,39 @@ def test_pipelined_kernel_32_row_halves_match_persistent_kernel(B, tech, lam):
     assert np.mean([np.mean(x["tokens"] == y["tokens"]) for x, y in zip(ra, rc)]) >= 0.97
     assert relerr(ha[:B], hc[:B]) <= 1e-2
     assert relerr(qa[0], qc[0]) <= 1e-2 and relerr(ka[0], kc[0]) <= 1e-2
+
+
+@pytest.mark.parametrize("B", [128, 256])
+def test_lm_head_unit_variants_agree(B):
+    """The LM-head unit variants give the same decisions and tokens: the softmax check on single
+    tiles / pair units with the shuffle epilogue / transposed pair units (lm_pair 0 / 1 / 2, the
+    persistent kernel at full depth), and the decode tail's greedy head on single tiles or
+    transposed units (lm_tail 0 / 1, classifier exit: persistent at 128, pipelined at 256)."""
+    L, d, V = 4, 1024, 4096
+    first = np.arange(B) * 13 % V + 1
+    if B == 128:
+        runs = []
+        for k in (0, 1, 2):
+            g, _ = cfg_pair(L, d, V, 3, "softmax", lam=2.0, B=B)
+            e = X.Engine(g, mega=True)
+            e.set_option("pipe", 0)
+            e.set_option("lm_pair", k)
+            e.session_begin(first, 60, 100, 5)
+            e.decode_run(3)
+            runs.append(e.records(0, 3))
+            e.close()
+        for r in runs[1:]:
+            assert np.array_equal(r["output_layer"], runs[0]["output_layer"])
+            assert np.array_equal(r["tokens"], runs[0]["tokens"])
+            np.testing.assert_allclose(r["conf"], runs[0]["conf"], rtol=1e-4, atol=1e-12)
+    runs = []
+    for k in (0, 1):
+        g, _ = cfg_pair(L, d, V, 3, "classifier", lam=0.6, gamma=0.97, B=B)
+        e = X.Engine(g, mega=True)
+        e.set_option("lm_tail", k)
+        e.session_begin(first, 60, 100, 5)
+        e.decode_run(3)
+        runs.append(e.records(0, 3))
+        e.close()
+    assert np.array_equal(runs[0]["output_layer"], runs[1]["output_layer"])
+    assert np.array_equal(runs[0]["tokens"], runs[1]["tokens"])
