@@ -198,7 +198,9 @@ struct el_engine {
         if (use_pipe == 0 || B > 256 || cfg.encoder_len > 0) return false;
         // (softmax: the LM-head check on the GEMM CTAs, pair units at batch <= 128 only)
         if (B <= 64) return pipe64 && B > 32 && NR == 64 && cfg.technique != EL_TECH_SOFTMAX;
-        if (B <= 128) return pipe128 && B > 64 && NR == 128 && (cfg.technique != EL_TECH_SOFTMAX || pipe_softmax);
+        // (the pipelined kernel's softmax check has pair units only: lm_pair 0 keeps softmax on iter_kernel)
+        if (B <= 128)
+            return pipe128 && B > 64 && NR == 128 && (cfg.technique != EL_TECH_SOFTMAX || (pipe_softmax && opt_lm_pair));
         return cfg.technique != EL_TECH_SOFTMAX;
     }
 

@@ -614,3 +614,31 @@ def test_lm_head_unit_variants_agree(B):
         e.close()
     assert np.array_equal(runs[0]["output_layer"], runs[1]["output_layer"])
     assert np.array_equal(runs[0]["tokens"], runs[1]["tokens"])
+
+
+def test_engine_run_across_pipelined_and_persistent_batches(port):
+    """Engine::run at max_batch 128 with ragged output lengths: the decode batch shrinks from 128
+    through the pipelined kernel's 64-row-halves range (65-128) into the persistent kernel's
+    (<= 64) as sequences finish and are evicted. K/V of every layer (prompt and generated
+    positions) and the tokens vs the oracle's fp64 run on the same requests."""
+    L, d, V, B = 3, 256, 512, 128
+    g = X.EngineConfig(model=X.ModelConfig(L, d, V, 29), technique=X.ExitTechnique("never"), max_batch=B,
+                       pool_blocks=8192, eos_token=-1, capture_kv=True)
+    o = OB.engine_config(L, d, V, 29, "never", max_batch=B, pool_blocks=8192, eos_token=-1, capture_kv=True,
+                         round_bf16=True)
+    rng = np.random.default_rng(4)
+    reqs = [(0.0, [int(x) for x in rng.integers(1, V, 2 + i % 5)], 1 + (i * 5) % 9) for i in range(B)]
+    e = X.Engine(g, mega=True)
+    t = e.run(X.Workload([X.Request(*r) for r in reqs]))
+    tp = port.model(L, d, V, 29, True).run(o, OB.Workload.from_requests(reqs))
+    gt = {s["id"]: s["tokens"] for s in t.sequences}
+    pt = {s["id"]: s["tokens"] for s in tp.sequences}
+    assert all(len(gt[k]) == len(pt[k]) for k in pt)
+    assert np.mean([a == b for k in pt for a, b in zip(gt[k], pt[k])]) >= 0.9
+    for sid in range(0, B, 9):
+        n = len(reqs[sid][1]) - 1
+        for layer in range(1, L + 1):
+            kg, vg = t.kv(sid, layer)
+            ko, vo = port.transcript_kv(tp, sid, layer, d)
+            assert relerr(kg[:n], ko[:n]) <= HID_TOL and relerr(vg[:n], vo[:n]) <= HID_TOL, (sid, layer)
+    e.close()
